@@ -1,0 +1,194 @@
+/*
+ * hep.h — C ABI of the B200-native HarmonyEP token-scheduling MoE path.
+ *
+ * Plain C types only (pointers, sizes, int status codes); no torch types.
+ * Every pointer named d_* is a DEVICE pointer (cudaMalloc / torch CUDA
+ * tensor storage); every other pointer is host memory.  `stream` is a
+ * cudaStream_t passed as void*.  Nothing in this ABI allocates or
+ * synchronizes inside a hot call (hep_sched_solve, hep_moe_*): buffers are
+ * caller-owned, and the handle owns only its placement tables.
+ *
+ * Each entry point names the reference interface it replaces
+ * (paths relative to /root/reference/pkg/src/harmonyep/).
+ *
+ * Status codes mirror the reference error classes (core.py:36-84):
+ */
+#ifndef HEP_H_
+#define HEP_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HEP_OK 0
+#define HEP_E_DIMENSION 1  /* core.DimensionError  */
+#define HEP_E_PLACEMENT 2  /* core.PlacementError  */
+#define HEP_E_CONTRACT 3   /* core.ContractViolation */
+#define HEP_E_STALE 4      /* core.StaleStateError */
+#define HEP_E_CAPACITY 5   /* core.CapacityError   */
+#define HEP_E_INTERNAL 99
+#define HEP_E_CUDA 100     /* CUDA runtime / launch failure (message in hep_last_error) */
+
+/* Largest scheduling group the device solver handles (2^G subsets live in
+ * registers of one warp).  The reference's own tests use G <= 10. */
+#define HEP_MAX_GPUS 10
+
+/* Thread-local message for the last non-zero status returned on this thread. */
+const char *hep_last_error(void);
+int hep_abi_version(void);
+/* Number of SMs of the current device (grid sizing helper for callers). */
+int hep_device_sm_count(void);
+
+/* ======================================================================
+ * Scheduler: exact min-max replica loads + canonical lex-min plan,
+ * integerization, locality-first routing, transfer volumes.
+ * ====================================================================== */
+typedef struct hep_sched *hep_sched_t;
+
+/*
+ * Build the device placement tables (the `_BalanceNetwork` analogue,
+ * scheduler.py:181-207, built once per placement and owned by the handle —
+ * the SolverState of scheduler.py:151-170).
+ *   grp_off[E+1], grp_gpu[grp_off[E]] : EDP groups in LIST order (core.py:164-226)
+ *   slots[E]                           : local slot per expert (may be NULL)
+ *   gpus_per_node                      : 0 = single node (core.py:99)
+ * Replaces: SolverState(placement, options) / Placement validation (core.py:180-185).
+ */
+int hep_sched_create(int num_gpus, int num_experts, const int32_t *grp_off, const int32_t *grp_gpu,
+                     const int32_t *slots, int gpus_per_node, hep_sched_t *out);
+int hep_sched_destroy(hep_sched_t h);
+/* nnz = number of (expert, gpu) replicas; max_ranges = routing-table capacity;
+ * Q = lcm(1..G) (scheduler.py:184); transfer_len = G*G + 8*G + 2. */
+int hep_sched_sizes(hep_sched_t h, int64_t *nnz, int64_t *max_ranges, int64_t *Q, int64_t *transfer_len);
+
+/* Stage flags for hep_sched_solve */
+#define HEP_SCHED_SOLVE 1      /* m + lex-min plan      (scheduler.py:337-402)          */
+#define HEP_SCHED_INTEGERIZE 2 /* largest remainder     (scheduler.py:697-735)          */
+#define HEP_SCHED_ROUTE 4      /* Algorithm 1 ranges    (router.py:114-163)             */
+#define HEP_SCHED_TRANSFER 8   /* pair/send/recv/local  (router.py:178-226)             */
+#define HEP_SCHED_TOPO 16      /* route_topology_aware  (router.py:166-175) instead of route_tokens */
+#define HEP_SCHED_ALL 15
+
+/* Device output buffers, caller-allocated (sizes from hep_sched_sizes). */
+typedef struct {
+    int64_t *d_m;          /* [4]  m numerator, m denominator, Q, integerized objective */
+    int64_t *d_xq;         /* [nnz] replica loads x*Q, EDP-list order (ReplicaLoadPlan.entries) */
+    int64_t *d_xi;         /* [nnz] integerized replica loads */
+    int64_t *d_gpu_load;   /* [G]   integerized per-GPU load (ReplicaLoadPlan.gpu_loads) */
+    int64_t *d_ranges;     /* [max_ranges*4] (expert, src, dst, count) — RoutingTable.ranges */
+    int64_t *d_n_ranges;   /* [1] */
+    int64_t *d_transfer;   /* [G*G+8G+2] pair, send, recv, local, send_intra, recv_intra,
+                              send_inter, recv_inter, intra_volume, inter_volume (TransferPlan) */
+    int32_t *d_status;     /* [1] device-detected error (HEP_E_PLACEMENT, HEP_E_CAPACITY, ...) */
+} hep_sched_out;
+
+/*
+ * One micro-batch: loads -> m, plan, integerized plan, routing table, transfer plan,
+ * in ONE single-CTA kernel launch on `stream` (no host sync).
+ *   d_loads : int64 load matrix input_e^g, element (e,g) at d_loads[e*stride_e + g*stride_g]
+ *             ([E][G] expert-major: stride_e=G, stride_g=1; the all-gathered [G][E]
+ *             histogram: stride_e=1, stride_g=E)
+ *   d_base  : int64 [G] gpu_base (pipelined share, scheduler.py:405-433) or NULL
+ * Replaces: solve_replica_loads (scheduler.py:405-433), warm_solve (:436-461),
+ *           integerize_plan (:697-735), route_tokens (router.py:161-163),
+ *           route_topology_aware (:166-175), build_transfer_plan (:178-226).
+ * Canonical result: the unique lex-min optimal plan (scheduler.py:19-26), so the
+ * output is a pure function of (placement, loads): warm == cold, bit-identical
+ * on every rank.
+ */
+int hep_sched_solve(hep_sched_t h, const int64_t *d_loads, int64_t stride_e, int64_t stride_g,
+                    const int64_t *d_base, int flags, const hep_sched_out *out, void *stream);
+
+/*
+ * Integerize an arbitrary rational plan x = d_xnum / den (common denominator)
+ * on the device.  Replaces integerize_plan (scheduler.py:697-735) for plans not
+ * produced by hep_sched_solve.  Non-integer expert totals -> d_status = HEP_E_CONTRACT.
+ */
+int hep_sched_integerize(hep_sched_t h, const int64_t *d_xnum, int64_t den, const hep_sched_out *out,
+                         void *stream);
+/*
+ * Route a caller-provided integral plan d_xi (EDP-list order) against d_loads.
+ * Replaces route_tokens / route_topology_aware (router.py:114-175) incl. the
+ * _check_plan contract (router.py:97-111) -> d_status = HEP_E_CONTRACT.
+ */
+int hep_sched_route(hep_sched_t h, const int64_t *d_loads, int64_t stride_e, int64_t stride_g,
+                    const int64_t *d_xi, int flags, const hep_sched_out *out, void *stream);
+/* Aggregate an arbitrary routing table. Replaces build_transfer_plan (router.py:178-226). */
+int hep_transfer_plan(int num_gpus, int gpus_per_node, const int64_t *d_ranges, int64_t n_ranges,
+                      int64_t *d_transfer, int32_t *d_status, void *stream);
+
+/* ======================================================================
+ * MoE layer data path (builder-defined semantics; the reference models it only
+ * as a cost, simulator.py:439-476).  bf16 activations / weights, fp32 accumulate.
+ * ====================================================================== */
+
+/*
+ * K1 gate epilogue: top-K over fp32 router logits (+ optional per-expert
+ * selection bias), weights = softmax over the K selected logits, and the
+ * per-(source, expert) histogram (the load matrix column of source g,
+ * LoadMatrix core.py:229-268).  Tokens [t0, t0+tokens_per_src) belong to
+ * source (t / tokens_per_src).  Ties -> lower expert id.
+ *   d_logits [T][ld_logits] fp32 (first E columns used), d_bias [E] or NULL,
+ *   d_topk_idx [T][K] int32, d_topk_w [T][K] fp32, d_hist [n_src][E] int64 (zeroed here)
+ */
+int hep_gate_topk(const float *d_logits, int64_t ld_logits, const float *d_bias, int64_t T, int E, int K,
+                  int64_t tokens_per_src, int n_src, int32_t *d_topk_idx, float *d_topk_w, int64_t *d_hist,
+                  void *stream);
+
+/*
+ * Dense bf16 GEMM on tcgen05/TMEM/TMA (sm_100a): D[M][N] = A[M][K] . B[N][K]^T,
+ * fp32 accumulate, fp32 or bf16 output.  Used for the router logits (K1).
+ * Requires K % 64 == 0, N % 16 == 0, N <= 256 or N % 256 == 0.
+ */
+#define HEP_OUT_F32 0
+#define HEP_OUT_BF16 1
+int hep_gemm_bf16(const void *d_A, const void *d_B, void *d_D, int64_t M, int64_t N, int64_t K, int out_kind,
+                  void *stream);
+
+/*
+ * K4: per-assignment destination rows from the routing table (RoutingTable
+ * "ranges partition that source's tokens in sequence order", router.py:38-46).
+ * Receive layout ("rows"): [dst GPU][expert ascending][src GPU ascending][rank].
+ * Outputs:
+ *   d_tok_row [T][K] int32  row of assignment (t,k)
+ *   d_row_tok [R]    int32  token of each row (R = total assignments)
+ *   d_seg      [nnz][4] int32 grouped-GEMM segments (row_start, rows, expert, dst) in row order
+ *   d_dst_rows [G+1] int64  row offset of each destination GPU
+ * Needs the hep_sched_out of the same micro-batch (ranges + xi).
+ */
+int hep_moe_assign(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_topk_idx, int64_t T, int K,
+                   int64_t tokens_per_src, int32_t *d_tok_row, int32_t *d_row_tok, int32_t *d_seg,
+                   int64_t *d_dst_rows, void *workspace, size_t workspace_bytes, void *stream);
+size_t hep_moe_assign_workspace(hep_sched_t h, int64_t T, int K);
+
+/* K5 permute/dispatch: rows[tok_row[t][k]] = x[t]  (bf16, 128-bit vectorised scatter). */
+int hep_moe_permute(const void *d_x, const int32_t *d_tok_row, int64_t T, int K, int64_t d_model, void *d_rows,
+                    void *stream);
+
+/*
+ * K6 expert FFN as grouped GEMM (tcgen05/TMEM/TMA, SwiGLU fused in the first
+ * GEMM's epilogue):  per segment s with expert e:
+ *   H[r] = silu(X[r] W1_e^T) * (X[r] W3_e^T),  Y[r] = H[r] W2_e^T
+ *   d_w13 [E][2F][d]  rows interleaved in blocks of 128 (W1 block j, then W3 block j)
+ *   d_w2  [E][d][F]
+ *   d_h   [R][F] scratch, d_y [R][d] output (bf16)
+ * Segments/rows are read on the device (no host sync): d_seg as from hep_moe_assign
+ * (n_seg entries, R = capacity of d_rows / d_h / d_y in rows).
+ */
+int hep_moe_expert_ffn(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg,
+                       int n_seg, int64_t R, int64_t d_model, int64_t ffn, int n_experts, void *d_h, void *d_y,
+                       void *d_workspace, size_t workspace_bytes, int32_t *d_status, void *stream);
+/* workspace for hep_moe_expert_ffn's device-built m-tile list */
+size_t hep_moe_ffn_workspace(int n_seg, int64_t R, int n_experts);
+
+/* K7 combine/un-permute: out[t] = sum_k w[t][k] * y[tok_row[t][k]] (fp32 accumulate in k order). */
+int hep_moe_combine(const void *d_y, const int32_t *d_tok_row, const float *d_topk_w, int64_t T, int K,
+                    int64_t d_model, void *d_out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HEP_H_ */

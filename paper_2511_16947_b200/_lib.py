@@ -1,0 +1,116 @@
+"""ctypes binding of the in-tree C-ABI library ``libhep.so`` (include/hep.h).
+
+The library is the product: there is no Python or CPU fallback.  If it is
+missing, or no CUDA device is present, every compute entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .core import STATUS_ERRORS, HarmonyError
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libhep.so")
+
+c_i64p = ctypes.POINTER(ctypes.c_int64)
+c_i32p = ctypes.POINTER(ctypes.c_int32)
+vp = ctypes.c_void_p
+
+
+class HepSchedOut(ctypes.Structure):
+    """``hep_sched_out`` (include/hep.h): device output buffers of one solve."""
+
+    _fields_ = [
+        ("d_m", vp),
+        ("d_xq", vp),
+        ("d_xi", vp),
+        ("d_gpu_load", vp),
+        ("d_ranges", vp),
+        ("d_n_ranges", vp),
+        ("d_transfer", vp),
+        ("d_status", vp),
+    ]
+
+
+# (name, restype, argtypes) for every symbol declared in include/hep.h
+SIGNATURES = {
+    "hep_last_error": (ctypes.c_char_p, []),
+    "hep_abi_version": (ctypes.c_int, []),
+    "hep_device_sm_count": (ctypes.c_int, []),
+    "hep_sched_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, c_i32p, c_i32p, c_i32p, ctypes.c_int, ctypes.POINTER(vp)]),
+    "hep_sched_destroy": (ctypes.c_int, [vp]),
+    "hep_sched_sizes": (ctypes.c_int, [vp, c_i64p, c_i64p, c_i64p, c_i64p]),
+    "hep_sched_solve": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int64, vp, ctypes.c_int, ctypes.POINTER(HepSchedOut), vp]),
+    "hep_sched_integerize": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.POINTER(HepSchedOut), vp]),
+    "hep_sched_route": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int64, vp, ctypes.c_int, ctypes.POINTER(HepSchedOut), vp]),
+    "hep_transfer_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, vp, ctypes.c_int64, vp, vp, vp]),
+    "hep_gate_topk": (ctypes.c_int, [vp, ctypes.c_int64, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int, vp, vp, vp, vp]),
+    "hep_gemm_bf16": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp]),
+    "hep_moe_assign": (ctypes.c_int, [vp, ctypes.POINTER(HepSchedOut), vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]),
+    "hep_moe_assign_workspace": (ctypes.c_size_t, [vp, ctypes.c_int64, ctypes.c_int]),
+    "hep_moe_permute": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, vp, vp]),
+    "hep_moe_expert_ffn": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp, vp, vp, ctypes.c_size_t, vp, vp]),
+    "hep_moe_ffn_workspace": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_int64, ctypes.c_int]),
+    "hep_moe_combine": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, vp, vp]),
+}
+
+_LIB = None
+
+
+def lib():
+    """Load libhep.so once; raise if it was not built (no fallback)."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2511_16947_b200.build` "
+                "(the CUDA library is required; there is no CPU fallback)"
+            )
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = L
+    return _LIB
+
+
+def check(rc: int, where: str) -> None:
+    """Raise the reference exception class matching a C-ABI status code."""
+    if rc == 0:
+        return
+    msg = (lib().hep_last_error() or b"").decode(errors="replace")
+    cls = STATUS_ERRORS.get(rc)
+    if cls is None:
+        raise RuntimeError(f"{where}: status {rc}: {msg}")
+    raise cls(f"{where}: {msg}")
+
+
+def raise_status(code: int, where: str) -> None:
+    """Raise for a device-detected status word (``d_status``)."""
+    if code == 0:
+        return
+    cls = STATUS_ERRORS.get(int(code), HarmonyError)
+    raise cls(f"{where}: device reported status {code}")
+
+
+def require_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("a CUDA (sm_100a) device is required: this package has no CPU path")
+    lib()
+    return torch
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream

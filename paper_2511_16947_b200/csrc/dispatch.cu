@@ -1,0 +1,342 @@
+// dispatch.cu — K4 per-assignment slot assignment, K5 permute/dispatch and
+// K7 combine/un-permute.
+//
+// Receive layout ("rows"), identical on every rank: [dst GPU][expert
+// ascending][src GPU ascending][rank within (src, expert)].  The routing table
+// (reference RoutingTable, router.py:38-46) says, for every (expert, src), how
+// its tokens are split into consecutive ranges in sequence order; K4 turns
+// that into a row for every (token, k) assignment with a deterministic stable
+// counting pass (no atomics decide positions):
+//   plan_prep    one CTA: segment table, row bases, per-(expert, src) range lists
+//   chunk_count  per 64-token chunk: per-expert assignment counts
+//   chunk_scan   per (src, expert): exclusive prefix over chunks (sequence order)
+//   chunk_map    per chunk: walk tokens in order -> rank -> range -> row
+// K5/K7 are HBM-bound row copies with 128-bit vector loads/stores, one warp
+// per token (K5 reads each token once and writes its K rows; K7 reads K rows
+// and sums them in fixed k order with fp32 accumulation).
+#include "common.cuh"
+#include "sched_internal.cuh"
+
+namespace hep {
+
+constexpr int kChunk = 64;
+
+struct AssignWs {
+    int32_t *row_base;  // [nnz] first row of segment (dst, e) per nnz entry
+    int32_t *es_cnt;    // [E*G] number of ranges of (e, src)
+    int32_t *es_end;    // [E*G*G] rank end (exclusive) of each range, table order
+    int32_t *es_delta;  // [E*G*G] row - rank of each range
+    int32_t *first;     // [E+1] first range index of expert e (-1 = none)
+    int32_t *chunk_cnt; // [n_src * n_chunks * E]
+};
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+static size_t assign_ws_bytes(const hep_sched *h, int64_t T, int n_src, int64_t tps) {
+    const int64_t E = h->E, G = h->G;
+    const int64_t ncs = (tps + kChunk - 1) / kChunk;
+    size_t b = 0;
+    b += align256(4 * (size_t)h->nnz + 4);
+    b += align256(4 * (size_t)(E * G));
+    b += align256(4 * (size_t)(E * G * G));
+    b += align256(4 * (size_t)(E * G * G));
+    b += align256(4 * (size_t)(E + 1));
+    b += align256(4 * (size_t)(n_src * ncs * E));
+    return b;
+}
+
+static AssignWs carve_ws(const hep_sched *h, void *ws, int n_src, int64_t tps) {
+    const int64_t E = h->E, G = h->G;
+    const int64_t ncs = (tps + kChunk - 1) / kChunk;
+    char *p = (char *)ws;
+    AssignWs w;
+    w.row_base = (int32_t *)p; p += align256(4 * (size_t)h->nnz + 4);
+    w.es_cnt = (int32_t *)p; p += align256(4 * (size_t)(E * G));
+    w.es_end = (int32_t *)p; p += align256(4 * (size_t)(E * G * G));
+    w.es_delta = (int32_t *)p; p += align256(4 * (size_t)(E * G * G));
+    w.first = (int32_t *)p; p += align256(4 * (size_t)(E + 1));
+    w.chunk_cnt = (int32_t *)p;
+    (void)n_src;
+    return w;
+}
+
+// ---------------------------------------------------------------------------
+__global__ void plan_prep_kernel(int G, int E, int nnz, const int32_t *grp_off, const int32_t *grp_gpu,
+                                 const int32_t *hosted_off, const int32_t *seg_nnz, const int32_t *nnz_exp,
+                                 const int64_t *xi, const int64_t *ranges, const int64_t *n_ranges_p,
+                                 const int64_t *gpu_load, int64_t *dst_rows, int32_t *seg, AssignWs w,
+                                 int32_t *status) {
+    __shared__ int64_t s_dst[HEP_MAX_GPUS + 1];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int64_t n_ranges = *n_ranges_p;
+    if (tid == 0) {
+        int64_t acc = 0;
+        for (int g = 0; g < G; ++g) { s_dst[g] = acc; dst_rows[g] = acc; acc += gpu_load[g]; }
+        s_dst[G] = acc;
+        dst_rows[G] = acc;
+        if (acc >= (int64_t)1 << 31) atomicCAS(status, 0, HEP_E_CAPACITY);
+    }
+    for (int i = tid; i < E * G; i += nt) w.es_cnt[i] = 0;
+    for (int i = tid; i <= E; i += nt) w.first[i] = -1;
+    __syncthreads();
+    // segments [dst][expert asc]
+    if (tid < G) {
+        int64_t row = s_dst[tid];
+        for (int p = hosted_off[tid]; p < hosted_off[tid + 1]; ++p) {
+            const int i = seg_nnz[p];
+            seg[4 * p + 0] = (int32_t)row;
+            seg[4 * p + 1] = (int32_t)xi[i];
+            seg[4 * p + 2] = nnz_exp[i];
+            seg[4 * p + 3] = tid;
+            w.row_base[i] = (int32_t)row;
+            row += xi[i];
+        }
+    }
+    for (int64_t r = tid; r < n_ranges; r += nt) {
+        const int e = (int)ranges[4 * r];
+        if (r == 0 || ranges[4 * (r - 1)] != e) w.first[e] = (int)r;
+    }
+    __syncthreads();
+    for (int e = tid; e < E; e += nt) {
+        const int r0 = w.first[e];
+        if (r0 < 0) continue;
+        int r1 = r0;
+        while (r1 < n_ranges && ranges[4 * r1] == e) ++r1;
+        for (int j = r0; j < r1; ++j) {
+            const int src = (int)ranges[4 * j + 1], dst = (int)ranges[4 * j + 2];
+            const int64_t cnt = ranges[4 * j + 3];
+            int nz = -1;
+            for (int i = grp_off[e]; i < grp_off[e + 1]; ++i)
+                if (grp_gpu[i] == dst) nz = i;
+            if (nz < 0) { atomicCAS(status, 0, HEP_E_CONTRACT); continue; }
+            int64_t row = w.row_base[nz], rank = 0;
+            for (int k = r0; k < r1; ++k) {
+                const int ks = (int)ranges[4 * k + 1], kd = (int)ranges[4 * k + 2];
+                if (kd == dst && ks < src) row += ranges[4 * k + 3];
+                if (k < j && ks == src) rank += ranges[4 * k + 3];
+            }
+            const int es = e * G + src;
+            const int slot = w.es_cnt[es]++;
+            w.es_end[es * G + slot] = (int32_t)(rank + cnt);
+            w.es_delta[es * G + slot] = (int32_t)(row - rank);
+        }
+    }
+}
+
+__global__ void chunk_count_kernel(const int32_t *topk_idx, int K, int E, int64_t tps, int64_t T, int ncs,
+                                   int32_t *chunk_cnt) {
+    extern __shared__ int32_t cnt[];
+    const int src = blockIdx.x / ncs, c = blockIdx.x % ncs;
+    const int64_t t0 = (int64_t)src * tps + (int64_t)c * kChunk;
+    int64_t t1 = (int64_t)src * tps + tps;
+    if (t0 + kChunk < t1) t1 = t0 + kChunk;
+    if (T < t1) t1 = T;
+    for (int i = threadIdx.x; i < E; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    for (int64_t a = t0 * K + threadIdx.x; a < t1 * K; a += blockDim.x) atomicAdd(&cnt[topk_idx[a]], 1);
+    __syncthreads();
+    int32_t *out = chunk_cnt + (int64_t)blockIdx.x * E;
+    for (int i = threadIdx.x; i < E; i += blockDim.x) out[i] = cnt[i];
+}
+
+__global__ void chunk_scan_kernel(int n_src, int ncs, int E, int32_t *chunk_cnt) {
+    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    if (id >= n_src * E) return;
+    const int src = id / E, e = id % E;
+    int32_t run = 0;
+    for (int c = 0; c < ncs; ++c) {
+        int32_t *p = chunk_cnt + ((int64_t)src * ncs + c) * E + e;
+        const int32_t v = *p;
+        *p = run;
+        run += v;
+    }
+}
+
+// one warp per chunk; lanes k < K own pick k of each token (distinct experts)
+__global__ void chunk_map_kernel(const int32_t *topk_idx, int K, int E, int G, int64_t tps, int64_t T, int ncs,
+                                 const int32_t *chunk_cnt, AssignWs w, int32_t *tok_row, int32_t *row_tok) {
+    extern __shared__ int32_t sm[];
+    int32_t *ctr = sm;                // [E]
+    int32_t *l_cnt = ctr + E;         // [E]
+    int32_t *l_end = l_cnt + E;       // [E*G]
+    int32_t *l_delta = l_end + E * G; // [E*G]
+    const int src = blockIdx.x / ncs, c = blockIdx.x % ncs;
+    const int lane = threadIdx.x;
+    for (int e = lane; e < E; e += 32) {
+        ctr[e] = chunk_cnt[(int64_t)blockIdx.x * E + e];
+        const int es = e * G + src;
+        const int n = w.es_cnt[es];
+        l_cnt[e] = n;
+        for (int j = 0; j < n; ++j) {
+            l_end[e * G + j] = w.es_end[es * G + j];
+            l_delta[e * G + j] = w.es_delta[es * G + j];
+        }
+    }
+    __syncwarp();
+    const int64_t t0 = (int64_t)src * tps + (int64_t)c * kChunk;
+    int64_t t1 = (int64_t)src * tps + tps;
+    if (t0 + kChunk < t1) t1 = t0 + kChunk;
+    if (T < t1) t1 = T;
+    for (int64_t t = t0; t < t1; ++t) {
+        if (lane < K) {
+            const int e = topk_idx[t * K + lane];
+            const int q = ctr[e]++;
+            int j = 0;
+            const int n = l_cnt[e];
+            while (j + 1 < n && q >= l_end[e * G + j]) ++j;
+            const int row = q + l_delta[e * G + j];
+            tok_row[t * K + lane] = row;
+            row_tok[row] = (int32_t)t;
+        }
+        __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K5: rows[tok_row[t][k]] = x[t]
+__global__ void __launch_bounds__(256) permute_kernel(const int4 *__restrict__ x, const int32_t *__restrict__ tok_row,
+                                                      int64_t T, int K, int64_t nvec, int4 *__restrict__ rows) {
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = warp; t < T; t += nwarps) {
+        int32_t r[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (k < K) r[k] = tok_row[t * K + k];
+        const int4 *src = x + t * nvec;
+        for (int64_t v0 = lane; v0 < nvec; v0 += 32 * 4) {
+            int4 buf[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+                if (v0 + 32 * u < nvec) buf[u] = __ldg(src + v0 + 32 * u);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                if (k >= K) break;
+                int4 *dst = rows + (int64_t)r[k] * nvec;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (v0 + 32 * u < nvec) dst[v0 + 32 * u] = buf[u];
+            }
+        }
+    }
+}
+
+// K7: out[t] = sum_k w[t][k] * y[tok_row[t][k]]
+__global__ void __launch_bounds__(256) combine_kernel(const int4 *__restrict__ y, const int32_t *__restrict__ tok_row,
+                                                      const float *__restrict__ topk_w, int64_t T, int K,
+                                                      int64_t nvec, int4 *__restrict__ out) {
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = warp; t < T; t += nwarps) {
+        int32_t r[16];
+        float wk[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (k < K) { r[k] = tok_row[t * K + k]; wk[k] = topk_w[t * K + k]; }
+        for (int64_t v = lane; v < nvec; v += 32) {
+            float acc[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+            int4 in[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                if (k < K) in[k] = __ldg(y + (int64_t)r[k] * nvec + v);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                if (k >= K) break;
+                const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&in[k]);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float2 f = __bfloat1622float2(h[i]);
+                    acc[2 * i] = fmaf(wk[k], f.x, acc[2 * i]);
+                    acc[2 * i + 1] = fmaf(wk[k], f.y, acc[2 * i + 1]);
+                }
+            }
+            int4 o;
+            __nv_bfloat162 *oh = reinterpret_cast<__nv_bfloat162 *>(&o);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) oh[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+            out[t * nvec + v] = o;
+        }
+    }
+}
+
+static int grid_for_warps(int64_t T) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t want = (T + 7) / 8;  // 8 warps per block
+    const int64_t cap = (int64_t)sms * 8;
+    const int64_t g = want < cap ? want : cap;
+    return (int)(g > 1 ? g : 1);
+}
+
+}  // namespace hep
+
+using namespace hep;
+
+extern "C" size_t hep_moe_assign_workspace(hep_sched_t h, int64_t T, int K) {
+    (void)K;
+    if (!h) return 0;
+    const int n_src = h->G;
+    const int64_t tps = (T + n_src - 1) / n_src;
+    return assign_ws_bytes(h, T, n_src, tps > 0 ? tps : 1);
+}
+
+extern "C" int hep_moe_assign(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_topk_idx, int64_t T, int K,
+                              int64_t tokens_per_src, int32_t *d_tok_row, int32_t *d_row_tok, int32_t *d_seg,
+                              int64_t *d_dst_rows, void *workspace, size_t workspace_bytes, void *stream) {
+    HEP_REQUIRE(h && sched && d_topk_idx && d_tok_row && d_row_tok && d_seg && d_dst_rows && workspace,
+                HEP_E_CONTRACT, "hep_moe_assign: null argument");
+    HEP_REQUIRE(K >= 1 && K <= 16 && tokens_per_src >= 1, HEP_E_DIMENSION, "hep_moe_assign: K=%d", K);
+    const int n_src = h->G;
+    HEP_REQUIRE(tokens_per_src * n_src >= T, HEP_E_DIMENSION, "tokens_per_src * G < T");
+    HEP_REQUIRE(workspace_bytes >= assign_ws_bytes(h, T, n_src, tokens_per_src), HEP_E_CAPACITY,
+                "hep_moe_assign: workspace too small (%zu < %zu)", workspace_bytes,
+                assign_ws_bytes(h, T, n_src, tokens_per_src));
+    cudaStream_t s = (cudaStream_t)stream;
+    AssignWs w = carve_ws(h, workspace, n_src, tokens_per_src);
+    const int E = h->E, G = h->G;
+    plan_prep_kernel<<<1, 512, 0, s>>>(G, E, h->nnz, h->d_grp_off, h->d_grp_gpu, h->d_hosted_off, h->d_seg_nnz,
+                                       h->d_nnz_exp, sched->d_xi, sched->d_ranges, sched->d_n_ranges,
+                                       sched->d_gpu_load, d_dst_rows, d_seg, w, sched->d_status);
+    HEP_CHECK_LAUNCH();
+    if (T <= 0) return HEP_OK;
+    const int ncs = (int)((tokens_per_src + kChunk - 1) / kChunk);
+    const int nblk = n_src * ncs;
+    chunk_count_kernel<<<nblk, 128, E * sizeof(int32_t), s>>>(d_topk_idx, K, E, tokens_per_src, T, ncs, w.chunk_cnt);
+    HEP_CHECK_LAUNCH();
+    chunk_scan_kernel<<<(n_src * E + 255) / 256, 256, 0, s>>>(n_src, ncs, E, w.chunk_cnt);
+    HEP_CHECK_LAUNCH();
+    const size_t sm = sizeof(int32_t) * (2 * (size_t)E + 2 * (size_t)E * G);
+    HEP_REQUIRE(sm <= 200 * 1024, HEP_E_CAPACITY, "chunk_map smem %zu", sm);
+    if (sm > 48 * 1024) HEP_CHECK_CUDA(cudaFuncSetAttribute(chunk_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    chunk_map_kernel<<<nblk, 32, sm, s>>>(d_topk_idx, K, E, G, tokens_per_src, T, ncs, w.chunk_cnt, w, d_tok_row,
+                                          d_row_tok);
+    HEP_CHECK_LAUNCH();
+    return HEP_OK;
+}
+
+extern "C" int hep_moe_permute(const void *d_x, const int32_t *d_tok_row, int64_t T, int K, int64_t d_model,
+                               void *d_rows, void *stream) {
+    HEP_REQUIRE(d_x && d_tok_row && d_rows, HEP_E_CONTRACT, "hep_moe_permute: null pointer");
+    HEP_REQUIRE(d_model % 8 == 0 && K >= 1 && K <= 16, HEP_E_DIMENSION, "hep_moe_permute: d_model %% 8, K<=16");
+    if (T <= 0) return HEP_OK;
+    permute_kernel<<<grid_for_warps(T), 256, 0, (cudaStream_t)stream>>>(
+        (const int4 *)d_x, d_tok_row, T, K, d_model / 8, (int4 *)d_rows);
+    HEP_CHECK_LAUNCH();
+    return HEP_OK;
+}
+
+extern "C" int hep_moe_combine(const void *d_y, const int32_t *d_tok_row, const float *d_topk_w, int64_t T, int K,
+                               int64_t d_model, void *d_out, void *stream) {
+    HEP_REQUIRE(d_y && d_tok_row && d_topk_w && d_out, HEP_E_CONTRACT, "hep_moe_combine: null pointer");
+    HEP_REQUIRE(d_model % 8 == 0 && K >= 1 && K <= 16, HEP_E_DIMENSION, "hep_moe_combine: d_model %% 8, K<=16");
+    if (T <= 0) return HEP_OK;
+    combine_kernel<<<grid_for_warps(T), 256, 0, (cudaStream_t)stream>>>(
+        (const int4 *)d_y, d_tok_row, d_topk_w, T, K, d_model / 8, (int4 *)d_out);
+    HEP_CHECK_LAUNCH();
+    return HEP_OK;
+}

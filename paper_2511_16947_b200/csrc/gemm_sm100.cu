@@ -1,0 +1,464 @@
+// gemm_sm100.cu — K6 expert FFN (grouped GEMM) and the K1 router GEMM on
+// 5th-generation tensor cores.
+//
+// One persistent, warp-specialised kernel template (one CTA per SM):
+//   warp 0      TMA producer: A tile [128 x 64] + B tile [BN x 64] per stage,
+//               128-byte swizzle, STAGES-deep mbarrier ring
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//               (M=128, N=BN, K=16 per instruction, fp32 accumulator in TMEM,
+//               two accumulator buffers so the epilogue of tile i overlaps
+//               the MMAs of tile i+1)
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> fused op -> global
+//               (EPI_SWIGLU: silu(gate) * up -> bf16 H, the first expert GEMM;
+//                EPI_BF16: plain bf16 store, the down projection;
+//                EPI_F32: fp32 logits, the router GEMM)
+// Grouped mode walks a device-resident m-tile list built from the scheduler's
+// segments (no host sync): tiles are ordered expert-major, then N-block, then
+// M-tile, so one expert's weight block is streamed from HBM once per wave and
+// the expert's rows stay L2-resident across its N sweep.
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+#include "sm100.cuh"
+
+namespace hep {
+namespace gemm {
+
+using namespace sm100;
+
+constexpr int BM = 128;
+constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle atom row
+constexpr int kThreads = 192;
+
+enum Epi { EPI_SWIGLU = 0, EPI_BF16 = 1, EPI_F32 = 2 };
+
+struct Params {
+    int grouped;             // 0: dense M rows; 1: m-tile list
+    int64_t M;               // dense rows
+    int n_tiles;             // N / BN
+    int kblocks;             // K / 64
+    int64_t b_rows_per_exp;  // rows of B per expert (N_total)
+    const int32_t *mt_row0;  // [n_mtiles] first row of each m-tile
+    const int32_t *mt_rows;  // [n_mtiles] valid rows (<= 128)
+    const int32_t *exp_mt_off;  // [n_exp+1] m-tile offsets per expert
+    int n_exp;
+    void *out;
+    int64_t ld_out;          // elements per output row
+    int64_t out_cols;        // valid output columns (EPI_F32 masking)
+};
+
+template <int BN, int STAGES>
+struct Smem {
+    static constexpr int A_BYTES = BM * BK * 2;
+    static constexpr int B_BYTES = BN * BK * 2;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
+    static constexpr size_t BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + 8 * (2 * STAGES + 4) + 16;
+};
+
+struct Tile {
+    int expert, n_blk;
+    int32_t row0, rows;
+};
+
+__device__ __forceinline__ int64_t total_tiles(const Params &p) {
+    if (!p.grouped) return ((p.M + BM - 1) / BM) * p.n_tiles;
+    return (int64_t)p.exp_mt_off[p.n_exp] * p.n_tiles;
+}
+
+__device__ __forceinline__ Tile decode(const Params &p, int64_t t) {
+    Tile tl;
+    if (!p.grouped) {
+        const int64_t mt = (p.M + BM - 1) / BM;
+        tl.expert = 0;
+        tl.n_blk = (int)(t / mt);
+        const int64_t m = t % mt;
+        tl.row0 = (int32_t)(m * BM);
+        const int64_t left = p.M - m * BM;
+        tl.rows = (int32_t)(left < BM ? left : BM);
+        return tl;
+    }
+    // expert e owns tiles [off[e]*n_tiles, off[e+1]*n_tiles)
+    int lo = 0, hi = p.n_exp - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if ((int64_t)p.exp_mt_off[mid] * p.n_tiles <= t) lo = mid; else hi = mid - 1;
+    }
+    const int e = lo;
+    const int64_t base = (int64_t)p.exp_mt_off[e];
+    const int64_t mt_e = (int64_t)p.exp_mt_off[e + 1] - base;
+    const int64_t local = t - base * p.n_tiles;
+    tl.expert = e;
+    tl.n_blk = (int)(local / mt_e);
+    const int64_t m = base + local % mt_e;
+    tl.row0 = p.mt_row0[m];
+    tl.rows = p.mt_rows[m];
+    return tl;
+}
+
+__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+    __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t *>(&v);
+}
+
+template <int BN, int STAGES, int EPI>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params p) {
+    using S = Smem<BN, STAGES>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *sA = base;
+    uint8_t *sB = base + STAGES * S::A_BYTES;
+    uint64_t *full = reinterpret_cast<uint64_t *>(base + STAGES * S::STAGE_BYTES);
+    uint64_t *empty = full + STAGES;
+    uint64_t *tfull = empty + STAGES;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);
+        }
+        fence_barrier_init();
+        fence_proxy_async_smem();
+    }
+    if (warp == 1) tmem_alloc(tmem_slot, S::TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int64_t n_total = total_tiles(p);
+    const int kb = p.kblocks;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ===================== TMA producer =====================
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t t = blockIdx.x; t < n_total; t += gridDim.x) {
+                const Tile tl = decode(p, t);
+                const int32_t b_row = (int32_t)(tl.expert * p.b_rows_per_exp + (int64_t)tl.n_blk * BN);
+                for (int k = 0; k < kb; ++k) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
+                    tma_load_2d(sA + stage * S::A_BYTES, &tmA, &full[stage], k * BK, tl.row0);
+                    tma_load_2d(sB + stage * S::B_BYTES, &tmB, &full[stage], k * BK, b_row);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ===================== MMA issuer =====================
+            constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int64_t t = blockIdx.x; t < n_total; t += gridDim.x) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int k = 0; k < kb; ++k) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a_addr = smem_u32(sA + stage * S::A_BYTES);
+                    const uint32_t b_addr = smem_u32(sB + stage * S::B_BYTES);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk) {
+                        const uint64_t ad = desc_kmajor_sw128(a_addr + kk * 32);
+                        const uint64_t bd = desc_kmajor_sw128(b_addr + kk * 32);
+                        mma_bf16(d_tmem, ad, bd, idesc, (k | kk) ? 1u : 0u);
+                    }
+                    mma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else {
+        // ===================== epilogue (warps 2..5) =====================
+        const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32)
+        const int row_in_tile = quarter * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int64_t t = blockIdx.x; t < n_total; t += gridDim.x) {
+            const Tile tl = decode(p, t);
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+            const bool valid = row_in_tile < tl.rows;
+            const int64_t grow = (int64_t)tl.row0 + row_in_tile;
+            if constexpr (EPI == EPI_SWIGLU) {
+                // columns [0, BN/2) = gate (W1 block), [BN/2, BN) = up (W3 block)
+                __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(p.out) + grow * p.ld_out +
+                                     (int64_t)tl.n_blk * (BN / 2);
+#pragma unroll 1
+                for (int c = 0; c < BN / 2; c += 16) {
+                    uint32_t g[16], u[16];
+                    tmem_ld16(t_row + c, g);
+                    tmem_ld16(t_row + BN / 2 + c, u);
+                    tmem_ld_wait();
+                    uint32_t packed[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        float g0 = __uint_as_float(g[2 * i]), g1 = __uint_as_float(g[2 * i + 1]);
+                        float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
+                        packed[i] = pack_bf16(silu(g0) * u0, silu(g1) * u1);
+                    }
+                    if (valid) {
+                        uint4 *dst = reinterpret_cast<uint4 *>(out + c);
+                        dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+                        dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+                    }
+                }
+            } else if constexpr (EPI == EPI_BF16) {
+                __nv_bfloat16 *out =
+                    reinterpret_cast<__nv_bfloat16 *>(p.out) + grow * p.ld_out + (int64_t)tl.n_blk * BN;
+#pragma unroll 1
+                for (int c = 0; c < BN; c += 16) {
+                    uint32_t v[16];
+                    tmem_ld16(t_row + c, v);
+                    tmem_ld_wait();
+                    uint32_t packed[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        packed[i] = pack_bf16(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+                    if (valid) {
+                        uint4 *dst = reinterpret_cast<uint4 *>(out + c);
+                        dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+                        dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+                    }
+                }
+            } else {
+                float *out = reinterpret_cast<float *>(p.out) + grow * p.ld_out + (int64_t)tl.n_blk * BN;
+                const int64_t col0 = (int64_t)tl.n_blk * BN;
+#pragma unroll 1
+                for (int c = 0; c < BN; c += 16) {
+                    uint32_t v[16];
+                    tmem_ld16(t_row + c, v);
+                    tmem_ld_wait();
+                    if (valid) {
+                        if (col0 + c + 16 <= p.out_cols) {
+                            float4 *dst = reinterpret_cast<float4 *>(out + c);
+#pragma unroll
+                            for (int i = 0; i < 4; ++i)
+                                dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                                     __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (col0 + c + i < p.out_cols) out[c + i] = __uint_as_float(v[i]);
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem_base, S::TMEM_COLS);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// m-tile list from segments (row_start, rows, expert, dst): expert-major.
+// One CTA; one thread per expert, deterministic block scan.
+// ---------------------------------------------------------------------------
+__global__ void build_tiles_kernel(const int32_t *seg, int n_seg, int n_exp, int32_t *mt_row0, int32_t *mt_rows,
+                                   int32_t *exp_mt_off, int64_t cap, int32_t *status) {
+    __shared__ int64_t scan[64];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int chunk = (n_exp + nt - 1) / nt;
+    const int e0 = min(n_exp, tid * chunk), e1 = min(n_exp, e0 + chunk);
+    int64_t cnt = 0;
+    for (int e = e0; e < e1; ++e)
+        for (int s = 0; s < n_seg; ++s)
+            if (seg[4 * s + 2] == e) cnt += (seg[4 * s + 1] + BM - 1) / BM;
+    int64_t total;
+    int64_t pos = block_excl_scan_i64(cnt, scan, &total);
+    if (total > cap) {
+        if (tid == 0 && status) atomicCAS(status, 0, HEP_E_CAPACITY);
+        return;
+    }
+    for (int e = e0; e < e1; ++e) {
+        exp_mt_off[e] = (int32_t)pos;
+        for (int s = 0; s < n_seg; ++s) {
+            if (seg[4 * s + 2] != e) continue;
+            const int32_t r0 = seg[4 * s], n = seg[4 * s + 1];
+            for (int32_t m = 0; m < n; m += BM) {
+                mt_row0[pos] = r0 + m;
+                mt_rows[pos] = min(BM, n - m);
+                ++pos;
+            }
+        }
+    }
+    if (tid == nt - 1) exp_mt_off[n_exp] = (int32_t)total;
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    return fn;
+}
+
+// 2D bf16 row-major [rows][cols] tensor, box [box_rows][64], 128B swizzle
+static int make_tmap(CUtensorMap *m, const void *ptr, uint64_t rows, uint64_t cols, uint32_t box_rows) {
+    auto fn = encode_fn();
+    HEP_REQUIRE(fn, HEP_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    HEP_REQUIRE(((uintptr_t)ptr & 15) == 0 && (cols * 2) % 16 == 0, HEP_E_CONTRACT,
+                "TMA needs 16-byte aligned base and row pitch");
+    cuuint64_t dims[2] = {cols, rows};
+    cuuint64_t strides[1] = {cols * 2};
+    cuuint32_t box[2] = {(cuuint32_t)BK, box_rows};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    HEP_REQUIRE(r == CUDA_SUCCESS, HEP_E_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return HEP_OK;
+}
+
+static int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+template <int BN, int STAGES, int EPI>
+static int launch(const void *A, int64_t a_rows, int64_t K, const void *B, int64_t b_rows, const Params &p,
+                  int64_t max_tiles, cudaStream_t stream) {
+    using S = Smem<BN, STAGES>;
+    CUtensorMap ta, tb;
+    int rc = make_tmap(&ta, A, (uint64_t)a_rows, (uint64_t)K, BM);
+    if (rc) return rc;
+    rc = make_tmap(&tb, B, (uint64_t)b_rows, (uint64_t)K, BN);
+    if (rc) return rc;
+    auto kern = gemm_kernel<BN, STAGES, EPI>;
+    HEP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES));
+    int grid = sm_count();
+    if (max_tiles > 0 && max_tiles < grid) grid = (int)max_tiles;
+    if (grid < 1) grid = 1;
+    kern<<<grid, kThreads, S::BYTES, stream>>>(ta, tb, p);
+    HEP_CHECK_LAUNCH();
+    return HEP_OK;
+}
+
+}  // namespace gemm
+}  // namespace hep
+
+using namespace hep;
+using namespace hep::gemm;
+
+extern "C" int hep_gemm_bf16(const void *d_A, const void *d_B, void *d_D, int64_t M, int64_t N, int64_t K, int out_kind,
+                             void *stream) {
+    HEP_REQUIRE(d_A && d_B && d_D, HEP_E_CONTRACT, "hep_gemm_bf16: null pointer");
+    HEP_REQUIRE(M > 0 && N > 0 && K > 0 && K % BK == 0, HEP_E_DIMENSION, "hep_gemm_bf16: need K %% 64 == 0 (K=%lld)",
+                (long long)K);
+    Params p{};
+    p.grouped = 0;
+    p.M = M;
+    p.kblocks = (int)(K / BK);
+    p.b_rows_per_exp = 0;
+    p.out = d_D;
+    p.ld_out = N;
+    p.out_cols = N;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t mt = (M + BM - 1) / BM;
+    if (out_kind == HEP_OUT_F32) {
+        HEP_REQUIRE(N % 16 == 0, HEP_E_DIMENSION, "fp32 GEMM needs N %% 16 == 0");
+        int bn = N <= 16 ? 16 : N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+        p.n_tiles = (int)((N + bn - 1) / bn);
+        HEP_REQUIRE(N <= 256 || N % 256 == 0, HEP_E_DIMENSION, "fp32 GEMM: N=%lld", (long long)N);
+        switch (bn) {
+            case 16: return launch<16, 8, EPI_F32>(d_A, M, K, d_B, N, p, mt * p.n_tiles, s);
+            case 32: return launch<32, 8, EPI_F32>(d_A, M, K, d_B, N, p, mt * p.n_tiles, s);
+            case 64: return launch<64, 6, EPI_F32>(d_A, M, K, d_B, N, p, mt * p.n_tiles, s);
+            case 128: return launch<128, 5, EPI_F32>(d_A, M, K, d_B, N, p, mt * p.n_tiles, s);
+            default: return launch<256, 4, EPI_F32>(d_A, M, K, d_B, N, p, mt * p.n_tiles, s);
+        }
+    }
+    HEP_REQUIRE(N % 256 == 0, HEP_E_DIMENSION, "bf16 GEMM needs N %% 256 == 0");
+    p.n_tiles = (int)(N / 256);
+    return launch<256, 4, EPI_BF16>(d_A, M, K, d_B, N, p, mt * p.n_tiles, s);
+}
+
+extern "C" size_t hep_moe_ffn_workspace(int n_seg, int64_t R, int n_experts) {
+    const int64_t cap = R / BM + n_seg + 1;
+    return (size_t)(2 * cap + n_experts + 1 + 1) * sizeof(int32_t) + 64;
+}
+
+extern "C" int hep_moe_expert_ffn(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg,
+                                  int n_seg, int64_t R, int64_t d_model, int64_t ffn, int n_experts, void *d_h,
+                                  void *d_y, void *d_workspace, size_t workspace_bytes, int32_t *d_status,
+                                  void *stream) {
+    HEP_REQUIRE(d_rows && d_w13 && d_w2 && d_seg && d_h && d_y && d_workspace, HEP_E_CONTRACT,
+                "hep_moe_expert_ffn: null pointer");
+    HEP_REQUIRE(d_model % 256 == 0 && ffn % 128 == 0 && d_model % BK == 0, HEP_E_DIMENSION,
+                "expert FFN needs d_model %% 256 == 0 and ffn %% 128 == 0 (d=%lld F=%lld)", (long long)d_model,
+                (long long)ffn);
+    HEP_REQUIRE(workspace_bytes >= hep_moe_ffn_workspace(n_seg, R, n_experts), HEP_E_CAPACITY, "workspace too small");
+    if (R <= 0) return HEP_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t cap = R / BM + n_seg + 1;
+    int32_t *mt_row0 = reinterpret_cast<int32_t *>(d_workspace);
+    int32_t *mt_rows = mt_row0 + cap;
+    int32_t *exp_off = mt_rows + cap;
+    build_tiles_kernel<<<1, 1024, 0, s>>>(d_seg, n_seg, n_experts, mt_row0, mt_rows, exp_off, cap, d_status);
+    HEP_CHECK_LAUNCH();
+    Params p{};
+    p.grouped = 1;
+    p.mt_row0 = mt_row0;
+    p.mt_rows = mt_rows;
+    p.exp_mt_off = exp_off;
+    p.n_exp = n_experts;
+    // GEMM 1: H = silu(X W1^T) * (X W3^T), B = W13 [E][2F][d]
+    p.kblocks = (int)(d_model / BK);
+    p.n_tiles = (int)(2 * ffn / 256);
+    p.b_rows_per_exp = 2 * ffn;
+    p.out = d_h;
+    p.ld_out = ffn;
+    p.out_cols = ffn;
+    int rc = launch<256, 4, EPI_SWIGLU>(d_rows, R, d_model, d_w13, (int64_t)n_experts * 2 * ffn, p, 0, s);
+    if (rc) return rc;
+    // GEMM 2: Y = H W2^T, B = W2 [E][d][F]
+    p.kblocks = (int)(ffn / BK);
+    p.n_tiles = (int)(d_model / 256);
+    p.b_rows_per_exp = d_model;
+    p.out = d_y;
+    p.ld_out = d_model;
+    p.out_cols = d_model;
+    return launch<256, 4, EPI_BF16>(d_h, R, ffn, d_w2, (int64_t)n_experts * d_model, p, 0, s);
+}

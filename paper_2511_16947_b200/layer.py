@@ -1,0 +1,170 @@
+"""The token-scheduling MoE layer on one B200 (device-resident hot path).
+
+Per micro-batch, all on one CUDA stream, no host synchronisation:
+
+  K1  router GEMM   logits[T][E] = x . Wg^T            hep_gemm_bf16 (tcgen05, fp32 out)
+  K1  gate epilogue top-K + softmax(top-K) + hist[G][E] hep_gate_topk
+  K3  scheduler     m, lex-min plan, integerize, ranges hep_sched_solve (1 CTA)
+  K4  assignment    (token, k) -> receive row           hep_moe_assign
+  K5  permute       rows[row] = x[token]                hep_moe_permute
+  K6  expert FFN    SwiGLU grouped GEMM x2              hep_moe_expert_ffn (tcgen05)
+  K7  combine       out[t] = sum_k w * y[row]           hep_moe_combine
+
+``MoELayer`` with ``num_sources = G`` runs the paper's EP group of G GPUs
+*simulated on one device* (the reference's own "simulated EP" setting,
+BASELINE configs[0]): tokens [g*T/G, (g+1)*T/G) originate on virtual GPU g,
+the scheduler balances the G virtual GPUs exactly as on G real ones, the
+dispatch "all-to-all" is the K5 scatter into the [dst][expert][src] receive
+layout, and every virtual GPU's replicas run in one grouped GEMM (one
+physical weight copy per expert; replicas of an expert are identical by
+construction).  The schedule — routing decisions, per-GPU
+loads, token-to-GPU assignment — is the same bit-exact object the
+multi-GPU layer uses.
+
+Semantics owned by this builder (the reference never models the gate,
+SPEC.md:499): selection = top-K of (logit + bias_e) with ties to the lower
+expert id; weights = softmax over the K selected logits; expert =
+SwiGLU FFN  y = (silu(x W1^T) * (x W3^T)) W2^T  with a bf16 intermediate.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib
+from .core import Placement
+from .scheduler import HEP_SCHED_ALL, DeviceScheduler
+
+
+def interleave_w13(w1: torch.Tensor, w3: torch.Tensor) -> torch.Tensor:
+    """[E][F][d] x2 -> [E][2F][d] with 128-row blocks alternating W1, W3 (the
+    layout the fused SwiGLU epilogue expects, include/hep.h)."""
+    E, F, d = w1.shape
+    assert F % 128 == 0
+    a = w1.reshape(E, F // 128, 128, d)
+    b = w3.reshape(E, F // 128, 128, d)
+    return torch.stack((a, b), dim=2).reshape(E, 2 * F, d).contiguous()
+
+
+def init_expert_weights(num_experts: int, d_model: int, ffn: int, seed: int, device, dtype=torch.bfloat16):
+    """W1, W3 ~ N(0, 1/d), W2 ~ N(0, 1/F), seeded by expert id
+    so every replica of an expert is identical."""
+    w1 = torch.empty(num_experts, ffn, d_model, dtype=dtype, device=device)
+    w3 = torch.empty_like(w1)
+    w2 = torch.empty(num_experts, d_model, ffn, dtype=dtype, device=device)
+    for e in range(num_experts):
+        g = torch.Generator(device=device).manual_seed(seed * 100003 + e)
+        w1[e].copy_(torch.randn(ffn, d_model, generator=g, device=device) / d_model ** 0.5)
+        w3[e].copy_(torch.randn(ffn, d_model, generator=g, device=device) / d_model ** 0.5)
+        w2[e].copy_(torch.randn(d_model, ffn, generator=g, device=device) / ffn ** 0.5)
+    return w1, w2, w3
+
+
+class MoEBuffers:
+    """All device buffers of one micro-batch shape, allocated once (the hot
+    path allocates nothing; CUDA-graph capturable)."""
+
+    def __init__(self, sched: DeviceScheduler, T: int, K: int, E: int, e_pad: int, d_model: int, ffn: int, device):
+        L = _lib.lib()
+        G = sched.G
+        R = T * K
+        bf = dict(dtype=torch.bfloat16, device=device)
+        i32 = dict(dtype=torch.int32, device=device)
+        self.logits = torch.empty(T, e_pad, dtype=torch.float32, device=device)
+        self.topk_idx = torch.empty(T, K, **i32)
+        self.topk_w = torch.empty(T, K, dtype=torch.float32, device=device)
+        self.hist = torch.zeros(G, E, dtype=torch.int64, device=device)
+        self.tok_row = torch.empty(T, K, **i32)
+        self.row_tok = torch.empty(max(R, 1), **i32)
+        self.seg = torch.empty(max(sched.nnz, 1), 4, **i32)
+        self.dst_rows = torch.empty(G + 1, dtype=torch.int64, device=device)
+        ws = L.hep_moe_assign_workspace(sched.handle, T, K)
+        self.assign_ws = torch.empty(max(int(ws), 256), dtype=torch.uint8, device=device)
+        self.rows = torch.empty(max(R, 1), d_model, **bf)
+        self.h = torch.empty(max(R, 1), ffn, **bf)
+        self.y = torch.empty(max(R, 1), d_model, **bf)
+        fws = L.hep_moe_ffn_workspace(max(sched.nnz, 1), R, E)
+        self.ffn_ws = torch.empty(max(int(fws), 256), dtype=torch.uint8, device=device)
+        self.out = torch.empty(T, d_model, **bf)
+
+
+class MoELayer(torch.nn.Module):
+    """HarmonyEP MoE layer over a placement of ``placement.num_gpus`` (virtual)
+    GPUs, forward pass entirely in sm_100a kernels."""
+
+    def __init__(self, placement: Placement, d_model: int, ffn: int, top_k: int, *, seed: int = 0,
+                 gate_bias: torch.Tensor | None = None, device=None):
+        super().__init__()
+        torch_ = _lib.require_cuda()
+        self.device = torch_.device("cuda", torch_.cuda.current_device()) if device is None else torch_.device(device)
+        self.placement = placement
+        self.G = placement.num_gpus
+        self.E = placement.num_experts
+        self.K = top_k
+        self.d = d_model
+        self.F = ffn
+        if d_model % 256 or ffn % 128:
+            raise ValueError("d_model must be a multiple of 256 and ffn a multiple of 128")
+        self.e_pad = max(16, (self.E + 15) // 16 * 16)
+        self.sched = DeviceScheduler(placement, device=self.device)
+        g = torch.Generator(device=self.device).manual_seed(seed * 7919 + 17)
+        wg = torch.zeros(self.e_pad, d_model, dtype=torch.bfloat16, device=self.device)
+        wg[: self.E] = (torch.randn(self.E, d_model, generator=g, device=self.device) / d_model ** 0.5).to(torch.bfloat16)
+        self.wg = wg
+        w1, w2, w3 = init_expert_weights(self.E, d_model, ffn, seed, self.device)
+        self.w1, self.w3 = w1, w3
+        self.w13 = interleave_w13(w1, w3)
+        self.w2 = w2
+        self.gate_bias = None if gate_bias is None else gate_bias.to(self.device, torch.float32).contiguous()
+        self._bufs: dict[int, MoEBuffers] = {}
+
+    def buffers(self, T: int) -> MoEBuffers:
+        b = self._bufs.get(T)
+        if b is None:
+            b = MoEBuffers(self.sched, T, self.K, self.E, self.e_pad, self.d, self.F, self.device)
+            self._bufs[T] = b
+        return b
+
+    @torch.no_grad()
+    def forward(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+        """x [T][d] bf16 on the device, T divisible by G (tokens of virtual GPU g
+        are rows [g*T/G, (g+1)*T/G)).  Returns a view of the layer's output buffer."""
+        T = x.shape[0]
+        if x.dtype != torch.bfloat16 or x.shape[1] != self.d or not x.is_contiguous():
+            raise ValueError("x must be a contiguous [T, d_model] bf16 tensor")
+        if T % self.G:
+            raise ValueError(f"T={T} must be divisible by the {self.G} source GPUs")
+        b = self.buffers(T)
+        self.run(x, b, stream)
+        return b.out
+
+    def run(self, x: torch.Tensor, b: MoEBuffers, stream=None) -> None:
+        L = _lib.lib()
+        s = _lib.stream_handle(stream)
+        T, K, E, G = x.shape[0], self.K, self.E, self.G
+        tps = T // G
+        R = T * K
+        ck = _lib.check
+        ck(L.hep_gemm_bf16(x.data_ptr(), self.wg.data_ptr(), b.logits.data_ptr(), T, self.e_pad, self.d, 0, s),
+           "hep_gemm_bf16(router)")
+        ck(L.hep_gate_topk(b.logits.data_ptr(), self.e_pad, _lib.ptr(self.gate_bias), T, E, K, tps, G,
+                           b.topk_idx.data_ptr(), b.topk_w.data_ptr(), b.hist.data_ptr(), s), "hep_gate_topk")
+        # hist is [G][E] (source-major, the all-gather layout): stride_e = 1, stride_g = E
+        ck(L.hep_sched_solve(self.sched.handle, b.hist.data_ptr(), 1, E, None, HEP_SCHED_ALL,
+                             ctypes.byref(self.sched.out), s), "hep_sched_solve")
+        ck(L.hep_moe_assign(self.sched.handle, ctypes.byref(self.sched.out), b.topk_idx.data_ptr(), T, K, tps,
+                            b.tok_row.data_ptr(), b.row_tok.data_ptr(), b.seg.data_ptr(), b.dst_rows.data_ptr(),
+                            b.assign_ws.data_ptr(), b.assign_ws.numel(), s), "hep_moe_assign")
+        ck(L.hep_moe_permute(x.data_ptr(), b.tok_row.data_ptr(), T, K, self.d, b.rows.data_ptr(), s),
+           "hep_moe_permute")
+        ck(L.hep_moe_expert_ffn(b.rows.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(), b.seg.data_ptr(),
+                                self.sched.nnz, R, self.d, self.F, E, b.h.data_ptr(), b.y.data_ptr(),
+                                b.ffn_ws.data_ptr(), b.ffn_ws.numel(), self.sched.status.data_ptr(), s),
+           "hep_moe_expert_ffn")
+        ck(L.hep_moe_combine(b.y.data_ptr(), b.tok_row.data_ptr(), b.topk_w.data_ptr(), T, K, self.d,
+                             b.out.data_ptr(), s), "hep_moe_combine")
+
+    def check_status(self):
+        self.sched.check_status("MoELayer")

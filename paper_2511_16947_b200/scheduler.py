@@ -1,0 +1,325 @@
+"""Per-micro-batch replica-load scheduling on the GPU (drop-in API).
+
+Same public surface as the reference ``harmonyep.scheduler``
+(``/root/reference/pkg/src/harmonyep/scheduler.py``):
+
+  SolveOptions          :67-94    (balance mode; comm-aware modes are out of scope)
+  SolveStats            :138-148
+  SolverState           :151-170  (here: owns the device placement tables + output buffers)
+  solve_replica_loads   :405-433
+  warm_solve            :436-461
+  integerize_plan       :697-735
+
+Every solve is ONE launch of the single-CTA sm_100a scheduler kernel
+(``csrc/sched.cu``) through the C ABI ``hep_sched_solve`` (include/hep.h).
+The host only uploads the load matrix and, for this inspection API, reads the
+result back to build the reference's immutable plan objects; the MoE layer
+(``layer.py``) keeps everything on the device.
+
+The result is the unique lexicographically-minimal optimal plan, so it is a
+pure function of (placement, loads): warm and cold solves are bit-identical
+and independent replicas agree (scheduler.py:19-26).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from collections import OrderedDict
+from dataclasses import dataclass
+from fractions import Fraction
+
+import numpy as np
+
+from . import _lib
+from .core import (
+    CapacityError,
+    ContractViolation,
+    DimensionError,
+    LoadMatrix,
+    Placement,
+    ReplicaLoadPlan,
+    StaleStateError,
+    Topology,
+)
+
+BALANCE_ONLY = "balance_only"
+COMM_AWARE = "comm_aware"
+TOPOLOGY_AWARE = "topology_aware"
+_MODES = (BALANCE_ONLY, COMM_AWARE, TOPOLOGY_AWARE)
+
+HEP_SCHED_SOLVE = 1
+HEP_SCHED_INTEGERIZE = 2
+HEP_SCHED_ROUTE = 4
+HEP_SCHED_TRANSFER = 8
+HEP_SCHED_TOPO = 16
+HEP_SCHED_ALL = 15
+MAX_GPUS = 10  # HEP_MAX_GPUS
+
+
+@dataclass(frozen=True)
+class SolveOptions:
+    """Solver configuration (reference scheduler.py:67-94, same validation)."""
+
+    mode: str = BALANCE_ONLY
+    alpha: float = 1.0
+    alpha_intra: float = 0.1
+    alpha_inter: float = 1.0
+    tolerance: float = 1e-9
+    warm_state: "SolverState | None" = None
+
+    def __post_init__(self):
+        if self.mode not in _MODES:
+            raise ContractViolation(f"unknown mode {self.mode!r}; expected one of {_MODES}")
+        if min(self.alpha, self.alpha_intra, self.alpha_inter) < 0:
+            raise ContractViolation("communication weights must be >= 0")
+        if self.alpha_intra > self.alpha_inter:
+            raise ContractViolation("alpha_intra must not exceed alpha_inter (intra-node links are cheaper)")
+        if self.tolerance < 0:
+            raise ContractViolation("tolerance must be >= 0")
+
+
+@dataclass
+class SolveStats:
+    """Counters (reference :138-148).  The device solver has no probe loop:
+    one launch computes m and the plan, so ``probes`` counts solves and
+    ``iterations_last`` counts kernel launches of the last solve (1)."""
+
+    solves: int = 0
+    probes: int = 0
+    bfs_phases: int = 0
+    pivots: int = 0
+    iterations_last: int = 0
+
+    @property
+    def iterations_total(self) -> int:
+        return self.probes + self.bfs_phases + self.pivots
+
+
+class DeviceScheduler:
+    """Owns one ``hep_sched_t`` (device placement tables) plus the device output
+    buffers of one micro-batch (``hep_sched_out``)."""
+
+    def __init__(self, placement: Placement, gpus_per_node: int = 0, device=None):
+        torch = _lib.require_cuda()
+        self.placement = placement
+        self.G = placement.num_gpus
+        self.E = placement.num_experts
+        if self.G > MAX_GPUS:
+            raise CapacityError(f"device scheduler handles up to {MAX_GPUS} GPUs per scheduling group, got {self.G}")
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        off, gpu = placement.csr()
+        slots = np.asarray(placement.slots, dtype=np.int32)
+        h = ctypes.c_void_p()
+        L = _lib.lib()
+        _lib.check(
+            L.hep_sched_create(
+                self.G, self.E,
+                off.ctypes.data_as(_lib.c_i32p),
+                gpu.ctypes.data_as(_lib.c_i32p) if gpu.size else None,
+                slots.ctypes.data_as(_lib.c_i32p) if slots.size else None,
+                int(gpus_per_node),
+                ctypes.byref(h),
+            ),
+            "hep_sched_create",
+        )
+        self._h = h
+        self.off = off
+        nnz, max_ranges, Q, tlen = (ctypes.c_int64() for _ in range(4))
+        _lib.check(L.hep_sched_sizes(h, ctypes.byref(nnz), ctypes.byref(max_ranges), ctypes.byref(Q), ctypes.byref(tlen)),
+                   "hep_sched_sizes")
+        self.nnz, self.max_ranges, self.Q, self.tlen = nnz.value, max_ranges.value, Q.value, tlen.value
+        i64 = dict(dtype=torch.int64, device=self.device)
+        self.m = torch.zeros(4, **i64)
+        self.xq = torch.zeros(max(self.nnz, 1), **i64)
+        self.xi = torch.zeros(max(self.nnz, 1), **i64)
+        self.gpu_load = torch.zeros(self.G, **i64)
+        self.ranges = torch.zeros(4 * self.max_ranges, **i64)
+        self.n_ranges = torch.zeros(1, **i64)
+        self.transfer = torch.zeros(self.tlen, **i64)
+        self.status = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.out = _lib.HepSchedOut(
+            self.m.data_ptr(), self.xq.data_ptr(), self.xi.data_ptr(), self.gpu_load.data_ptr(),
+            self.ranges.data_ptr(), self.n_ranges.data_ptr(), self.transfer.data_ptr(), self.status.data_ptr(),
+        )
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _lib._LIB is not None:
+            _lib._LIB.hep_sched_destroy(h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    # -- launches (asynchronous on `stream`) ------------------------------
+    def launch_solve(self, d_loads, stride_e: int, stride_g: int, d_base=None, flags: int = HEP_SCHED_ALL, stream=None):
+        _lib.check(
+            _lib.lib().hep_sched_solve(
+                self._h, d_loads.data_ptr(), stride_e, stride_g, _lib.ptr(d_base), flags,
+                ctypes.byref(self.out), _lib.stream_handle(stream),
+            ),
+            "hep_sched_solve",
+        )
+
+    def launch_integerize(self, den: int, stream=None):
+        _lib.check(
+            _lib.lib().hep_sched_integerize(self._h, self.xq.data_ptr(), int(den), ctypes.byref(self.out),
+                                            _lib.stream_handle(stream)),
+            "hep_sched_integerize",
+        )
+
+    def launch_route(self, d_loads, stride_e, stride_g, d_xi, flags=0, stream=None):
+        _lib.check(
+            _lib.lib().hep_sched_route(self._h, d_loads.data_ptr(), stride_e, stride_g, d_xi.data_ptr(), flags,
+                                       ctypes.byref(self.out), _lib.stream_handle(stream)),
+            "hep_sched_route",
+        )
+
+    def check_status(self, where: str):
+        _lib.raise_status(int(self.status.item()), where)
+
+    # -- host views (synchronising; inspection / parity API only) ---------
+    def rows(self, t) -> list[list[int]]:
+        flat = t[: self.nnz].cpu().tolist() if self.nnz else []
+        return [flat[self.off[e]: self.off[e + 1]] for e in range(self.E)]
+
+    def host_ranges(self) -> tuple[tuple[int, int, int, int], ...]:
+        n = int(self.n_ranges.item())
+        if n == 0:
+            return ()
+        arr = self.ranges[: 4 * n].view(n, 4).cpu().tolist()
+        return tuple(tuple(r) for r in arr)
+
+
+_HANDLE_CACHE: "OrderedDict[tuple, DeviceScheduler]" = OrderedDict()
+
+
+def device_scheduler(placement: Placement, gpus_per_node: int = 0) -> DeviceScheduler:
+    """LRU cache of device schedulers keyed by placement (init-time objects)."""
+    torch = _lib.require_cuda()
+    key = (placement.num_gpus, placement.edp_groups, placement.slots, gpus_per_node, torch.cuda.current_device())
+    ds = _HANDLE_CACHE.get(key)
+    if ds is None:
+        ds = DeviceScheduler(placement, gpus_per_node)
+        _HANDLE_CACHE[key] = ds
+        while len(_HANDLE_CACHE) > 64:
+            _HANDLE_CACHE.popitem(last=False)
+    else:
+        _HANDLE_CACHE.move_to_end(key)
+    return ds
+
+
+class SolverState:
+    """Warm-start state (reference :151-170), reusable across micro-batches on
+    one placement.  Holds the device scheduler (placement tables already on
+    the GPU), so warm solves skip the placement upload."""
+
+    def __init__(self, placement: Placement, options: SolveOptions, topology: Topology | None = None):
+        self.placement = placement
+        self.options = options
+        self.topology = topology
+        self.stats = SolveStats()
+        self.last_objective = None
+        self._dev: DeviceScheduler | None = None
+
+    def _check_loads(self, loads: LoadMatrix) -> None:
+        if (loads.num_experts, loads.num_gpus) != (self.placement.num_experts, self.placement.num_gpus):
+            raise StaleStateError(
+                f"state placement is {self.placement.num_experts}x{self.placement.num_gpus}, "
+                f"loads are {loads.num_experts}x{loads.num_gpus}"
+            )
+
+
+def _check_dims(placement: Placement, loads: LoadMatrix) -> None:
+    if loads.num_experts != placement.num_experts:
+        raise DimensionError(f"loads cover {loads.num_experts} experts, placement {placement.num_experts}")
+    if loads.num_gpus != placement.num_gpus:
+        raise DimensionError(f"loads cover {loads.num_gpus} GPUs, placement {placement.num_gpus}")
+
+
+def _device_solve(state: SolverState, loads: LoadMatrix, gpu_base) -> ReplicaLoadPlan:
+    import torch
+
+    placement = state.placement
+    if state._dev is None:
+        state._dev = device_scheduler(placement)
+    dev = state._dev
+    G = placement.num_gpus
+    d_loads = torch.as_tensor(loads.as_array(), dtype=torch.int64).to(dev.device)
+    d_base = None
+    if gpu_base is not None:
+        if len(gpu_base) != G:
+            raise DimensionError(f"gpu_base has {len(gpu_base)} entries for {G} GPUs")
+        d_base = torch.as_tensor(np.asarray(gpu_base, dtype=np.int64)).to(dev.device)
+    dev.launch_solve(d_loads, G, 1, d_base, flags=HEP_SCHED_SOLVE)
+    dev.check_status("solve_replica_loads")
+    m_num, m_den, Q, _ = dev.m.cpu().tolist()
+    xq = dev.rows(dev.xq)
+    entries = tuple(tuple(Fraction(v, Q) for v in row) for row in xq)
+    objective = Fraction(m_num, m_den)
+    state.stats.solves += 1
+    state.stats.probes += 1
+    state.stats.iterations_last = 1
+    state.last_objective = objective
+    return ReplicaLoadPlan(num_gpus=G, groups=placement.edp_groups, entries=entries, objective=objective)
+
+
+def solve_replica_loads(placement: Placement, loads: LoadMatrix, options: SolveOptions | None = None, *,
+                        gpu_base: tuple[int, ...] | None = None) -> tuple[ReplicaLoadPlan, SolverState]:
+    """Exact min-max replica loads, canonical lex-min plan (reference :405-433)."""
+    options = options or SolveOptions()
+    if options.mode != BALANCE_ONLY:
+        raise ContractViolation(f"solve_replica_loads requires mode={BALANCE_ONLY!r}; use solve_comm_aware")
+    if options.warm_state is not None:
+        return warm_solve(options.warm_state, loads, gpu_base=gpu_base)
+    _check_dims(placement, loads)
+    state = SolverState(placement, options)
+    plan = _device_solve(state, loads, gpu_base)
+    return plan, state
+
+
+def warm_solve(prev_state: SolverState, new_loads: LoadMatrix, *,
+               gpu_base: tuple[int, ...] | None = None) -> tuple[ReplicaLoadPlan, SolverState]:
+    """Re-solve on the same placement (reference :436-461); identical to cold."""
+    if not isinstance(prev_state, SolverState):
+        raise StaleStateError("warm state is not a SolverState")
+    prev_state._check_loads(new_loads)
+    if prev_state.options.mode != BALANCE_ONLY:
+        raise ContractViolation("communication-aware warm solves are out of scope (DESIGN.md §scope)")
+    plan = _device_solve(prev_state, new_loads, gpu_base)
+    return plan, prev_state
+
+
+def integerize_plan(plan: ReplicaLoadPlan) -> ReplicaLoadPlan:
+    """Largest-remainder rounding on the device (reference :697-735): per
+    expert, +1 to the largest fractional parts, ties to the lowest GPU id."""
+    import torch
+
+    exact = [[Fraction(v) for v in row] for row in plan.entries]
+    den = 1
+    for row in exact:
+        for v in row:
+            den = math.lcm(den, v.denominator)
+    nums = [[int(v * den) for v in row] for row in exact]
+    biggest = max((abs(x) for row in nums for x in row), default=0)
+    if biggest * max(1, max((len(r) for r in nums), default=1)) >= (1 << 62):
+        raise CapacityError("plan entries too large for exact int64 integerization")
+    placement = Placement(plan.num_gpus, plan.groups, tuple(range(len(plan.groups))))
+    dev = device_scheduler(placement)
+    flat = [x for row in nums for x in row]
+    if flat:
+        dev.xq[: len(flat)].copy_(torch.tensor(flat, dtype=torch.int64))
+    dev.launch_integerize(den)
+    dev.check_status("integerize_plan")
+    xi = dev.rows(dev.xi)
+    objective = int(dev.m[3].item()) if plan.num_gpus else 0
+    return ReplicaLoadPlan(num_gpus=plan.num_gpus, groups=plan.groups, entries=tuple(tuple(r) for r in xi),
+                           objective=objective)
+
+
+def solve_comm_aware(*_args, **_kwargs):
+    """Communication-aware LP modes (reference scheduler.py:480-689) are outside
+    the scoped hot path; see DESIGN.md."""
+    raise NotImplementedError("comm-aware / topology-aware LP modes are not part of the B200 hot path")

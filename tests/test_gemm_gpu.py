@@ -1,0 +1,97 @@
+"""tcgen05/TMEM/TMA GEMMs (K1 router GEMM, K6 expert FFN) against a plain
+PyTorch fp32 reference of the same op.
+
+Tolerances: fp32 outputs of bf16 x bf16 products with fp32 accumulation —
+|err| <= 1e-3 * max|ref| + 1e-3; bf16 outputs — max|err| / max|ref| <= 1e-2
+(north-star bf16 tolerance)."""
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def L():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2511_16947_b200 import _lib
+
+    return _lib
+
+
+def _gemm(L, A, B, out_kind):
+    M, K = A.shape
+    N = B.shape[0]
+    D = torch.empty(M, N, dtype=torch.float32 if out_kind == 0 else torch.bfloat16, device="cuda")
+    L.check(L.lib().hep_gemm_bf16(A.data_ptr(), B.data_ptr(), D.data_ptr(), M, N, K, out_kind, L.stream_handle()), "gemm")
+    torch.cuda.synchronize()
+    return D
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 16, 64), (300, 16, 512), (1000, 32, 256), (257, 64, 128), (4096, 128, 2048),
+                                   (777, 256, 1024), (4096, 256, 7168), (130, 48, 64)])
+def test_dense_fp32_out(L, M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K)
+    A = torch.randn(M, K, generator=g, device="cuda").to(torch.bfloat16)
+    B = torch.randn(N, K, generator=g, device="cuda").to(torch.bfloat16)
+    D = _gemm(L, A, B, 0)
+    ref = A.float() @ B.float().T
+    err = (D - ref).abs().max().item()
+    assert err <= 1e-3 * ref.abs().max().item() + 1e-3, err
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (1000, 512, 512), (4096, 1024, 4096)])
+def test_dense_bf16_out(L, M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(11)
+    A = torch.randn(M, K, generator=g, device="cuda").to(torch.bfloat16)
+    B = torch.randn(N, K, generator=g, device="cuda").to(torch.bfloat16)
+    D = _gemm(L, A, B, 1).float()
+    ref = A.float() @ B.float().T
+    assert (D - ref).abs().max().item() / ref.abs().max().item() <= 1e-2
+
+
+def _ffn_ref(x, w1, w3, w2):
+    h = torch.nn.functional.silu(x @ w1.T) * (x @ w3.T)
+    return h.to(torch.bfloat16).float() @ w2.T
+
+
+@pytest.mark.parametrize("E,d,F,sizes", [
+    (4, 512, 1024, [300, 0, 129, 1000]),
+    (3, 256, 384, [1, 128, 255]),
+    (8, 1024, 768, [513, 64, 2000, 7, 0, 128, 300, 900]),
+])
+def test_grouped_expert_ffn(L, E, d, F, sizes):
+    from paper_2511_16947_b200.layer import init_expert_weights, interleave_w13
+
+    dev = "cuda"
+    w1, w2, w3 = init_expert_weights(E, d, F, seed=3, device=dev)
+    w13 = interleave_w13(w1, w3)
+    # segments in an arbitrary expert order (two segments per expert, like two dst GPUs)
+    segs, row = [], 0
+    for rep in range(2):
+        for e in reversed(range(E)):
+            n = sizes[e] if rep == 0 else sizes[e] // 3
+            segs.append((row, n, e, rep))
+            row += n
+    R = row
+    x = torch.randn(max(R, 1), d, device=dev).to(torch.bfloat16)
+    seg = torch.tensor(segs, dtype=torch.int32, device=dev)
+    h = torch.empty(max(R, 1), F, dtype=torch.bfloat16, device=dev)
+    y = torch.full((max(R, 1), d), float("nan"), dtype=torch.bfloat16, device=dev)
+    lib = L.lib()
+    ws = torch.empty(int(lib.hep_moe_ffn_workspace(len(segs), R, E)), dtype=torch.uint8, device=dev)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    L.check(lib.hep_moe_expert_ffn(x.data_ptr(), w13.data_ptr(), w2.data_ptr(), seg.data_ptr(), len(segs), R, d, F, E,
+                                   h.data_ptr(), y.data_ptr(), ws.data_ptr(), ws.numel(), st.data_ptr(),
+                                   L.stream_handle()), "ffn")
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    for (r0, n, e, _) in segs:
+        if n == 0:
+            continue
+        ref = _ffn_ref(x[r0:r0 + n].float(), w1[e].float(), w3[e].float(), w2[e].float())
+        got = y[r0:r0 + n].float()
+        assert torch.isfinite(got).all()
+        rel = (got - ref).abs().max().item() / max(ref.abs().max().item(), 1e-6)
+        assert rel <= 1e-2, (e, n, rel)

@@ -1,0 +1,104 @@
+"""End-to-end MoE layer parity on the B200 against the CPU oracle.
+
+Bit-exact: top-K routing decisions (on the device's own fp32 logits), the
+per-(source, expert) histogram = load matrix, the whole schedule (m, plan,
+integerized per-GPU loads, routing table) and the token -> receive-row
+assignment.  Tolerance: router logits |err| <= 1e-3·max|ref| (fp32 accumulate
+order), top-K weights 1e-5, layer output max|err|/max|ref| <= 1e-2 (bf16).
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2511_16947_b200 as P
+
+    return P
+
+
+def _run(P, G, E, K, d, F, T, s=1.0, seed=0, sample=None):
+    from oracle import layer_ref
+
+    shape = P.ClusterShape(G, E, 2)
+    pl = P.cayley_symmetric(shape) if E >= G else P.identical_placement(shape)
+    bias = torch.tensor(P.zipf_gate_bias(E, s, seed)) if s > 0 else None
+    layer = P.MoELayer(pl, d, F, K, seed=seed, gate_bias=bias)
+    g = torch.Generator(device="cuda").manual_seed(1000 + seed)
+    x = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
+    out = layer(x).clone()
+    torch.cuda.synchronize()
+    layer.check_status()
+    b = layer.buffers(T)
+    logits = b.logits[:, :E].cpu().numpy()
+    ref = layer_ref.layer_forward(
+        x.float().cpu().numpy(), logits, K, [tuple(gr) for gr in pl.edp_groups], G,
+        layer.w1.float().cpu().numpy(), layer.w2.float().cpu().numpy(), layer.w3.float().cpu().numpy(),
+        bias=None if bias is None else bias.numpy(), sample=sample,
+    )
+    return layer, x, out, b, ref, pl
+
+
+def test_tiny_config_bit_exact_schedule_and_output(P):
+    """BASELINE configs[0]: 8 experts top-2, d=512, ffn=1024, 4096 tokens,
+    simulated EP=4, Zipf-skewed routing."""
+    from oracle import layer_ref
+
+    layer, x, out, b, ref, pl = _run(P, G=4, E=8, K=2, d=512, F=1024, T=4096, s=1.0)
+    # router GEMM vs fp32
+    lref = x.float() @ layer.wg[: layer.E].float().T
+    lerr = (b.logits[:, : layer.E] - lref).abs().max().item()
+    assert lerr <= 1e-3 * lref.abs().max().item() + 1e-4
+    # routing decisions and loads: bit-exact
+    assert np.array_equal(b.topk_idx.cpu().numpy(), ref["topk_idx"])
+    assert np.allclose(b.topk_w.cpu().numpy(), ref["topk_w"], rtol=1e-5, atol=1e-6)
+    assert np.array_equal(b.hist.cpu().numpy(), ref["hist"])
+    sd = layer.sched
+    assert sd.m[:2].cpu().tolist() == list(ref["sched"]["m"])
+    assert sd.rows(sd.xi) == ref["sched"]["xi"]
+    assert [list(r) for r in sd.host_ranges()] == [list(r) for r in ref["sched"]["ranges"]]
+    assert sd.gpu_load.cpu().tolist() == ref["sched"]["gpu_load"]
+    # token -> row schedule: bit-exact
+    assert np.array_equal(b.tok_row.cpu().numpy(), ref["tok_row"])
+    assert b.dst_rows.cpu().tolist() == ref["dst_rows"].tolist()
+    # permuted rows are exact copies
+    R = x.shape[0] * layer.K
+    assert torch.equal(b.rows[:R], x[b.row_tok[:R].long()])
+    # layer output (bf16 tolerance)
+    got = out.float().cpu().numpy()
+    rel = np.abs(got - ref["out"]).max() / np.abs(ref["out"]).max()
+    assert rel <= 1e-2, rel
+
+
+@pytest.mark.parametrize("G,E,K,d,F,T,s", [
+    (8, 8, 2, 1024, 512, 8192, 1.5),     # Mixtral-like routing, small dims
+    (8, 128, 8, 512, 256, 8192, 1.0),    # Qwen3-like routing
+    (8, 256, 8, 512, 256, 4096, 1.5),    # DeepSeek-like routing
+    (2, 8, 2, 256, 128, 2048, 0.0),
+])
+def test_routing_shapes_sampled_output(P, G, E, K, d, F, T, s):
+    rng = np.random.default_rng(G * E + T)
+    sample = np.sort(rng.choice(T, size=96, replace=False))
+    layer, x, out, b, ref, pl = _run(P, G, E, K, d, F, T, s=s, seed=1, sample=sample)
+    assert np.array_equal(b.topk_idx.cpu().numpy(), ref["topk_idx"])
+    assert np.array_equal(b.hist.cpu().numpy(), ref["hist"])
+    assert layer.sched.rows(layer.sched.xi) == ref["sched"]["xi"]
+    assert np.array_equal(b.tok_row.cpu().numpy(), ref["tok_row"])
+    got = out.float().cpu().numpy()[sample]
+    rel = np.abs(got - ref["out"]).max() / np.abs(ref["out"]).max()
+    assert rel <= 1e-2, rel
+
+
+def test_repeatable_and_row_map_is_permutation(P):
+    layer, x, out, b, ref, pl = _run(P, G=8, E=16, K=2, d=256, F=256, T=4096, s=0.5, seed=2)
+    R = 4096 * 2
+    rows = b.tok_row.flatten().cpu().numpy()
+    assert np.array_equal(np.sort(rows), np.arange(R))
+    out2 = layer(x).clone()
+    assert torch.equal(out, out2)  # deterministic: no float atomics anywhere
