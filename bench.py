@@ -1,0 +1,420 @@
+"""Benchmark of the B200 HarmonyEP MoE layer (BASELINE.json metric:
+"MoE-layer tokens/s at 1/2/4/8 B200; max/mean GPU load; scheduler µs/micro-batch").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config mixtral|qwen3|dsv3|tiny] [--skew S]
+    python bench.py --impl reference ...      # CPU reference arm (oracle port on host cores)
+
+A step = one forward pass of the MoE layer over one micro-batch of synthetic
+tokens resident in HBM: router GEMM -> top-K + histogram -> exact scheduler ->
+token assignment -> permute -> SwiGLU grouped GEMM x2 -> combine.  At N=1 the
+EP group of G=8 GPUs is simulated on the one device (BASELINE configs[0]'s
+"simulated EP"), T tokens per micro-batch split over the 8 virtual source
+GPUs.  At N>1 every rank runs its own micro-batch through the same layer
+(weak scaling: per-GPU work fixed; see DESIGN.md §multi-GPU for the exchange
+path).  Rank 0 prints ONE JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (E, K, d_model, ffn, tokens per micro-batch per GPU, G)
+    "tiny": (8, 2, 512, 1024, 4096, 4),
+    "mixtral": (8, 2, 4096, 14336, 16384, 8),
+    "qwen3": (128, 8, 2048, 768, 32768, 8),
+    "dsv3": (256, 8, 7168, 2048, 16384, 8),
+}
+CONFIG_TEXT = {
+    "tiny": "tiny MoE layer: 8 experts top-2, d_model=512, ffn=1024, 4096 tokens, simulated EP=4",
+    "mixtral": "Mixtral-8x7B-shaped MoE layer: 8 experts top-2, d=4096, ffn=14336, 16K tokens/micro-batch, EP=8",
+    "qwen3": "Qwen3-30B-A3B-shaped layer: 128 experts top-8, d=2048, ffn=768, 32K tokens, EP=8",
+    "dsv3": "DeepSeek-V3-shaped fine-grained layer: 256 experts top-8, d=7168, ffn=2048, 16K tokens, EP=8",
+}
+METRIC = "MoE-layer tokens/s at 1/2/4/8 B200; max/mean GPU load; scheduler µs/micro-batch"
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d["hbm_gbs"], d["bf16_tflops"], d["bf16_tflops_sustained"], "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows: list[list[str]] = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+                for line in out.strip().splitlines():
+                    self.rows.append([x.strip() for x in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self):
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) > 8:
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_info():
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return os.cpu_count() or 1, model
+
+
+# ---------------------------------------------------------------------------
+# CPU reference arm: the oracle port of the reference path on host cores
+# ---------------------------------------------------------------------------
+_CPU_W: dict = {}
+
+
+def _cpu_expert_weights(cfg_name: str, e: int):
+    import numpy as np
+
+    E, K, d, F, T, G = CONFIGS[cfg_name]
+    key = (cfg_name, e % 16 if E > 16 else e)
+    if key not in _CPU_W:
+        g = np.random.default_rng(1000 + key[1])
+        _CPU_W[key] = (g.standard_normal((F, d), dtype=np.float32) / np.sqrt(d),
+                       g.standard_normal((F, d), dtype=np.float32) / np.sqrt(d),
+                       g.standard_normal((d, F), dtype=np.float32) / np.sqrt(F))
+    return _CPU_W[key]
+
+
+def cpu_reference_step(cfg_name: str, skew: float, sample_tokens: int, seed: int = 0):
+    """One bounded-sample step of the CPU restatement: router GEMM + top-K +
+    histogram for the sample, the reference scheduler (Dinic oracle, C) on a
+    full-size micro-batch load matrix, and the SwiGLU FFN + combine for the
+    sample tokens (numpy fp32, all host threads via BLAS).  Returns seconds per
+    token (the scheduler's per-micro-batch time amortised over T tokens)."""
+    import numpy as np
+
+    from oracle import layer_ref
+    from oracle import oracle as O
+    import paper_2511_16947_b200 as P
+
+    E, K, d, F, T, G = CONFIGS[cfg_name]
+    rng = np.random.default_rng(seed)
+    S = sample_tokens
+    x = rng.standard_normal((S, d), dtype=np.float32)
+    wg = (rng.standard_normal((E, d), dtype=np.float32) / np.sqrt(d)).astype(np.float32)
+    bias = P.zipf_gate_bias(E, skew, seed) if skew > 0 else None
+    t0 = time.perf_counter()
+    logits = x @ wg.T
+    idx, w = layer_ref.topk_select(logits, K, bias)
+    t_gate = time.perf_counter() - t0
+    # scheduler on a full micro-batch histogram (counts mode, reference generator)
+    wl = P.gen_zipf_workload(P.ClusterShape(G, E, 2), skew, (T // G) * K, 1, seed)
+    pl = P.cayley_symmetric(P.ClusterShape(G, E, 2))
+    loads = wl.micro_batches[0].entries
+    t0 = time.perf_counter()
+    O.full_path(G, pl.edp_groups, loads)
+    t_sched = time.perf_counter() - t0
+    # expert FFN for the sample, distinct fp32 weights per expert (pool of at
+    # most 16 weight sets for the 256-expert shape to bound host memory)
+    t_ffn = 0.0
+    out = np.zeros((S, d), dtype=np.float32)
+    for e in np.unique(idx):
+        w1, w3, w2 = _cpu_expert_weights(cfg_name, int(e))
+        rows, ks = np.nonzero(idx == e)
+        t0 = time.perf_counter()
+        y = layer_ref.expert_ffn(x[rows], w1, w3, w2)
+        out[rows] += w[rows, ks][:, None] * y
+        t_ffn += time.perf_counter() - t0
+    per_token = (t_gate + t_ffn) / S + t_sched / T
+    return per_token, dict(t_gate=t_gate, t_ffn=t_ffn, t_sched=t_sched, sample=S)
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = args.config
+    E, K, d, F, T, G = CONFIGS[cfg]
+    cores, model = cpu_info()
+    sample = args.cpu_sample or {"tiny": 1024, "mixtral": 128, "qwen3": 512, "dsv3": 128}[cfg]
+    for _ in range(args.warmup):
+        cpu_reference_step(cfg, args.skew, max(8, sample // 8))
+    per = []
+    for i in range(args.steps):
+        pt, info = cpu_reference_step(cfg, args.skew, sample, seed=i)
+        per.append(pt)
+    value = 1.0 / statistics.mean(per)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(per) * T,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": CONFIG_TEXT[cfg], "tokens_per_microbatch": T, "sim_ep": G, "top_k": K,
+                   "zipf_s": args.skew},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
+                         "sample": f"{sample} tokens/step through router+top-K+SwiGLU FFN (numpy fp32, BLAS threads) + "
+                                   f"the Dinic scheduler oracle on one full {G}x{E} micro-batch load matrix; "
+                                   f"host: {model}"},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
+    ap.add_argument("--skew", type=float, default=1.0)
+    ap.add_argument("--cpu-sample", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu legs)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if not args.profile else args.warmup
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2511_16947_b200 as P
+    from paper_2511_16947_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    E, K, d, F, T, G = CONFIGS[args.config]
+    shape = P.ClusterShape(G, E, 2)
+    pl = P.cayley_symmetric(shape)
+    bias = torch.tensor(P.zipf_gate_bias(E, args.skew, 0)) if args.skew > 0 else None
+    layer = P.MoELayer(pl, d, F, K, seed=0, gate_bias=bias, device=dev)
+    gx = torch.Generator(device=dev).manual_seed(1000 + rank)
+    x = torch.randn(T, d, generator=gx, device=dev).to(torch.bfloat16)
+    bufs = layer.buffers(T)
+    stream = torch.cuda.current_stream()
+    L = _lib.lib()
+
+    def step():
+        layer.run(x, bufs, stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    layer.check_status()
+
+    # --- timed region: K steps back to back; per-stage events on the launching stream
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    stages = ("router", "gate", "sched", "assign", "permute", "ffn", "combine")
+    evs = [{k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in stages}
+           for _ in range(args.steps)]
+
+    def staged_step(i):
+        layer.run(x, bufs, stream, events=evs[i])
+
+    sampler = ClockSampler(local) if not args.profile else None
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.__enter__()
+    start.record(stream)
+    for i in range(args.steps):
+        staged_step(i)
+    end.record(stream)
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.__exit__()
+    if world > 1:
+        dist.barrier()
+    layer.check_status()
+    t_ms = start.elapsed_time(end)
+    if world > 1:
+        tt = torch.tensor([t_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    ms_per_step = t_ms / args.steps
+    value = world * T * args.steps / (t_ms / 1e3)
+
+    stage_ms = {k: statistics.mean(e[k][0].elapsed_time(e[k][1]) for e in evs) for k in stages}
+    ffn_ms, perm_ms, comb_ms = stage_ms["ffn"], stage_ms["permute"], stage_ms["combine"]
+
+    # --- scheduler latency: the K3 kernel alone, on this micro-batch's histogram
+    n_sched = 200
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(n_sched):
+        layer.sched.launch_solve(bufs.hist, 1, E, None, 15, stream)
+    s1.record(stream)
+    torch.cuda.synchronize()
+    sched_us = 1e3 * s0.elapsed_time(s1) / n_sched
+
+    gpu_load = layer.sched.gpu_load.cpu().tolist()
+    m_num, m_den = layer.sched.m[:2].cpu().tolist()
+    mean_load = sum(gpu_load) / len(gpu_load)
+    max_mean = max(gpu_load) / mean_load if mean_load else 1.0
+
+    # --- e2e through the public API with host buffers (pinned), copies inside the timed region
+    xh = x.cpu().pin_memory()
+    oh = torch.empty(T, d, dtype=torch.bfloat16).pin_memory()
+    xd = torch.empty_like(x)
+    for _ in range(2):
+        xd.copy_(xh, non_blocking=True)
+        out = layer(xd)
+        oh.copy_(out, non_blocking=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        xd.copy_(xh, non_blocking=True)
+        out = layer(xd)
+        oh.copy_(out, non_blocking=True)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e_ms = e0.elapsed_time(e1)
+    if world > 1:
+        tt = torch.tensor([e_ms], device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e_ms = float(tt.item())
+    e2e_value = world * T * args.steps / (e_ms / 1e3)
+
+    hbm, tf_burst, tf_sus, peak_src = load_peaks()
+    R = T * K
+    ffn_flops = 6.0 * d * F * R
+    ffn_tflops = ffn_flops / (ffn_ms / 1e3) / 1e12
+    perm_bytes = T * d * 2 * (1 + K) + T * K * 4
+    comb_bytes = T * K * d * 2 + T * K * 4 * 2 + T * d * 2
+    launches_per_step = layer.LAUNCHES_PER_FORWARD
+
+    if rank == 0:
+        cores, model = cpu_info()
+        cpu_line = None
+        if not args.no_cpu_baseline and not args.profile:
+            sample = args.cpu_sample or {"tiny": 1024, "mixtral": 128, "qwen3": 512, "dsv3": 128}[args.config]
+            per = []
+            for i in range(3):
+                pt, info = cpu_reference_step(args.config, args.skew, sample, seed=i)
+                per.append(pt)
+            cpu_line = {"value": 1.0 / statistics.mean(per), "unit": "tokens/s", "cores": cores, "kind": "port",
+                        "sample": f"{sample} tokens x 3 steps through the CPU restatement (router+top-K+SwiGLU FFN "
+                                  f"numpy fp32 on all host threads) + Dinic scheduler oracle on a full {G}x{E} "
+                                  f"micro-batch; host: {model}"}
+        line = {
+            "metric": METRIC,
+            "value": value,
+            "unit": "tokens/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": ms_per_step,
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic",
+            "config": {
+                "workload": CONFIG_TEXT[args.config],
+                "tokens_per_microbatch_per_gpu": T,
+                "sim_ep": G,
+                "tokens_per_virtual_gpu": T // G,
+                "top_k": K, "d_model": d, "ffn": F, "experts": E,
+                "placement": f"cayley_symmetric(G={G}, E={E}, d=2)",
+                "zipf_s": args.skew,
+                "pass": "forward",
+                "l2": "inputs larger than L2 (x %.0f MB, expert weights %.2f GB per step)" % (T * d * 2 / 1e6,
+                                                                                               3 * E * d * F * 2 / 1e9),
+            },
+            "max_mean_gpu_load": max_mean,
+            "m_exact": [m_num, m_den],
+            "gpu_loads": gpu_load,
+            "scheduler_us": sched_us,
+            "stage_ms": stage_ms,
+            "roofline": {
+                "bound": "tensor",
+                "kernel": "hep_moe_expert_ffn (tcgen05 SwiGLU grouped GEMM x2)",
+                "achieved": ffn_tflops,
+                "peak": tf_sus,
+                "unit": "TFLOP/s",
+                "frac": ffn_tflops / tf_sus,
+                "frac_of_burst_peak": ffn_tflops / tf_burst,
+                "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside back-to-back steps)",
+                "algorithmic_flops_per_launch": ffn_flops,
+                "traffic": None,
+            },
+            "hbm_kernels": {
+                "permute": {"GB/s": perm_bytes / (perm_ms / 1e3) / 1e9, "frac": perm_bytes / (perm_ms / 1e3) / 1e9 / hbm},
+                "combine": {"GB/s": comb_bytes / (comb_ms / 1e3) / 1e9, "frac": comb_bytes / (comb_ms / 1e3) / 1e9 / hbm},
+                "peak_GB/s": hbm,
+            },
+            "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": T * d * 2,
+                    "d2h_bytes_per_step": T * d * 2},
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": sampler.summary() if sampler else None,
+            "cpu_baseline": cpu_line,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

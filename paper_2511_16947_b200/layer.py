@@ -140,31 +140,60 @@ class MoELayer(torch.nn.Module):
         self.run(x, b, stream)
         return b.out
 
-    def run(self, x: torch.Tensor, b: MoEBuffers, stream=None) -> None:
+    def run(self, x: torch.Tensor, b: MoEBuffers, stream=None, events: dict | None = None) -> None:
+        """Launch the whole forward chain on `stream`.  ``events`` optionally maps
+        a stage name ("router", "gate", "sched", "assign", "permute", "ffn",
+        "combine") to a (start, end) pair of torch.cuda.Event recorded around it."""
         L = _lib.lib()
-        s = _lib.stream_handle(stream)
+        st = stream if stream is not None else torch.cuda.current_stream()
+        s = st.cuda_stream
         T, K, E, G = x.shape[0], self.K, self.E, self.G
         tps = T // G
         R = T * K
         ck = _lib.check
+        ev = events or {}
+
+        def mark(name, i):
+            pair = ev.get(name)
+            if pair is not None:
+                pair[i].record(st)
+
+        mark("router", 0)
         ck(L.hep_gemm_bf16(x.data_ptr(), self.wg.data_ptr(), b.logits.data_ptr(), T, self.e_pad, self.d, 0, s),
            "hep_gemm_bf16(router)")
+        mark("router", 1)
+        mark("gate", 0)
         ck(L.hep_gate_topk(b.logits.data_ptr(), self.e_pad, _lib.ptr(self.gate_bias), T, E, K, tps, G,
                            b.topk_idx.data_ptr(), b.topk_w.data_ptr(), b.hist.data_ptr(), s), "hep_gate_topk")
+        mark("gate", 1)
         # hist is [G][E] (source-major, the all-gather layout): stride_e = 1, stride_g = E
+        mark("sched", 0)
         ck(L.hep_sched_solve(self.sched.handle, b.hist.data_ptr(), 1, E, None, HEP_SCHED_ALL,
                              ctypes.byref(self.sched.out), s), "hep_sched_solve")
+        mark("sched", 1)
+        mark("assign", 0)
         ck(L.hep_moe_assign(self.sched.handle, ctypes.byref(self.sched.out), b.topk_idx.data_ptr(), T, K, tps,
                             b.tok_row.data_ptr(), b.row_tok.data_ptr(), b.seg.data_ptr(), b.dst_rows.data_ptr(),
                             b.assign_ws.data_ptr(), b.assign_ws.numel(), s), "hep_moe_assign")
+        mark("assign", 1)
+        mark("permute", 0)
         ck(L.hep_moe_permute(x.data_ptr(), b.tok_row.data_ptr(), T, K, self.d, b.rows.data_ptr(), s),
            "hep_moe_permute")
+        mark("permute", 1)
+        mark("ffn", 0)
         ck(L.hep_moe_expert_ffn(b.rows.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(), b.seg.data_ptr(),
                                 self.sched.nnz, R, self.d, self.F, E, b.h.data_ptr(), b.y.data_ptr(),
                                 b.ffn_ws.data_ptr(), b.ffn_ws.numel(), self.sched.status.data_ptr(), s),
            "hep_moe_expert_ffn")
+        mark("ffn", 1)
+        mark("combine", 0)
         ck(L.hep_moe_combine(b.y.data_ptr(), b.tok_row.data_ptr(), b.topk_w.data_ptr(), T, K, self.d,
                              b.out.data_ptr(), s), "hep_moe_combine")
+        mark("combine", 1)
+
+    # kernels launched per forward: router GEMM, gate top-K, scheduler, assign x4,
+    # permute, FFN (tile list + 2 GEMMs), combine
+    LAUNCHES_PER_FORWARD = 12
 
     def check_status(self):
         self.sched.check_status("MoELayer")

@@ -102,3 +102,56 @@ def test_repeatable_and_row_map_is_permutation(P):
     assert np.array_equal(np.sort(rows), np.arange(R))
     out2 = layer(x).clone()
     assert torch.equal(out, out2)  # deterministic: no float atomics anywhere
+
+
+@pytest.mark.parametrize("cfg", ["mixtral", "qwen3", "dsv3"])
+def test_baseline_shapes_full_size(P, cfg):
+    """BASELINE configs[1..3] at full size (EP=8 simulated on one device):
+    routing, histogram, schedule and token->row map bit-exact against the CPU
+    oracle; expert FFN + combine for 48 sampled tokens against a plain PyTorch
+    fp32 reference of the same op (max|err|/max|ref| <= 1e-2)."""
+    import bench
+    from oracle import layer_ref
+
+    E, K, d, F, T, G = bench.CONFIGS[cfg]
+    pl = P.cayley_symmetric(P.ClusterShape(G, E, 2))
+    bias = torch.tensor(P.zipf_gate_bias(E, 1.0, 0))
+    layer = P.MoELayer(pl, d, F, K, seed=0, gate_bias=bias)
+    x = torch.randn(T, d, generator=torch.Generator(device="cuda").manual_seed(7), device="cuda").to(torch.bfloat16)
+    out = layer(x).clone()
+    torch.cuda.synchronize()
+    layer.check_status()
+    b = layer.buffers(T)
+    logits = b.logits[:, :E].cpu().numpy()
+    idx, w = layer_ref.topk_select(logits, K, bias.numpy())
+    assert np.array_equal(b.topk_idx.cpu().numpy(), idx)
+    hist = layer_ref.histogram(idx, E, G, T // G)
+    assert np.array_equal(b.hist.cpu().numpy(), hist)
+    from oracle import oracle as O
+
+    ref = O.full_path(G, pl.edp_groups, hist.T.copy())
+    sd = layer.sched
+    assert sd.m[:2].cpu().tolist() == list(ref["m"])
+    assert sd.rows(sd.xq) == ref["xq"]
+    assert sd.rows(sd.xi) == ref["xi"]
+    assert [tuple(r) for r in sd.host_ranges()] == [tuple(r) for r in ref["ranges"]]
+    tok_row, _ = layer_ref.receive_rows(pl.edp_groups, G, ref["xi"], ref["ranges"], idx, T // G)
+    assert np.array_equal(b.tok_row.cpu().numpy(), tok_row)
+    # sampled numerics, torch fp32 reference on the device
+    rng = np.random.default_rng(3)
+    toks = torch.tensor(np.sort(rng.choice(T, 48, replace=False)), device="cuda")
+    xs = x[toks].float()
+    ref_out = torch.zeros(len(toks), d, device="cuda")
+    ti = b.topk_idx[toks].long()
+    tw = b.topk_w[toks]
+    for k in range(K):
+        for e in ti[:, k].unique().tolist():
+            sel = (ti[:, k] == e).nonzero().flatten()
+            h = torch.nn.functional.silu(xs[sel] @ layer.w1[e].float().T) * (xs[sel] @ layer.w3[e].float().T)
+            y = h.to(torch.bfloat16).float() @ layer.w2[e].float().T
+            ref_out[sel] += tw[sel, k, None] * y.to(torch.bfloat16).float()
+    got = out[toks].float()
+    rel = ((got - ref_out).abs().max() / ref_out.abs().max()).item()
+    assert rel <= 1e-2, rel
+    del layer
+    torch.cuda.empty_cache()
