@@ -71,6 +71,7 @@ int hep_sched_sizes(hep_sched_t h, int64_t *nnz, int64_t *max_ranges, int64_t *Q
 #define HEP_SCHED_TRANSFER 8   /* pair/send/recv/local  (router.py:178-226)             */
 #define HEP_SCHED_TOPO 16      /* route_topology_aware  (router.py:166-175) instead of route_tokens */
 #define HEP_SCHED_ALL 15
+#define HEP_SCHED_PROFILE 32   /* diagnostics: record per-phase clock64 stamps (hep_sched_debug_timing) */
 
 /* Device output buffers, caller-allocated (sizes from hep_sched_sizes). */
 typedef struct {
@@ -116,6 +117,8 @@ int hep_sched_integerize(hep_sched_t h, const int64_t *d_xnum, int64_t den, cons
  */
 int hep_sched_route(hep_sched_t h, const int64_t *d_loads, int64_t stride_e, int64_t stride_g,
                     const int64_t *d_xi, int flags, const hep_sched_out *out, void *stream);
+/* Diagnostics: per-phase SM clock stamps of the last HEP_SCHED_PROFILE launch (n <= 16). */
+int hep_sched_debug_timing(int64_t *host_out, int n);
 /* Aggregate an arbitrary routing table. Replaces build_transfer_plan (router.py:178-226). */
 int hep_transfer_plan(int num_gpus, int gpus_per_node, const int64_t *d_ranges, int64_t n_ranges,
                       int64_t *d_transfer, int32_t *d_status, void *stream);
@@ -151,17 +154,18 @@ int hep_gemm_bf16(const void *d_A, const void *d_B, void *d_D, int64_t M, int64_
 /*
  * K4: per-assignment destination rows from the routing table (RoutingTable
  * "ranges partition that source's tokens in sequence order", router.py:38-46).
- * Receive layout ("rows"): [dst GPU][expert ascending][src GPU ascending][rank].
+ * Receive layout ("rows"): [expert ascending][dst GPU ascending][src GPU ascending][rank]
+ * (each expert's rows contiguous: one grouped-GEMM segment per expert).
  * Outputs:
  *   d_tok_row [T][K] int32  row of assignment (t,k)
  *   d_row_tok [R]    int32  token of each row (R = total assignments)
- *   d_seg      [nnz][4] int32 grouped-GEMM segments (row_start, rows, expert, dst) in row order
- *   d_dst_rows [G+1] int64  row offset of each destination GPU
+ *   d_seg      [nnz][4] int32 (row_start, rows, expert, dst) per replica, in row order
+ *   d_expert_rows [E+1] int64 first row of each expert's contiguous block
  * Needs the hep_sched_out of the same micro-batch (ranges + xi).
  */
 int hep_moe_assign(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_topk_idx, int64_t T, int K,
                    int64_t tokens_per_src, int32_t *d_tok_row, int32_t *d_row_tok, int32_t *d_seg,
-                   int64_t *d_dst_rows, void *workspace, size_t workspace_bytes, void *stream);
+                   int64_t *d_expert_rows, void *workspace, size_t workspace_bytes, void *stream);
 size_t hep_moe_assign_workspace(hep_sched_t h, int64_t T, int K);
 
 /* K5 permute/dispatch: rows[tok_row[t][k]] = x[t]  (bf16, 128-bit vectorised scatter). */

@@ -43,22 +43,19 @@ def histogram(topk_idx: np.ndarray, E: int, n_src: int, tps: int) -> np.ndarray:
 
 
 def receive_rows(groups, G: int, xi, ranges, topk_idx: np.ndarray, tps: int):
-    """Rows in the [dst][expert asc][src asc][rank] receive layout for every
-    (token, k); ranks within (src, expert) follow token order."""
+    """Rows in the [expert asc][dst asc][src asc][rank] receive layout for
+    every (token, k); ranks within (src, expert) follow token order."""
     T, K = topk_idx.shape
     E = len(groups)
-    gpu_load = np.zeros(G, dtype=np.int64)
-    for e, grp in enumerate(groups):
-        for g, v in zip(grp, xi[e]):
-            gpu_load[g] += v
-    dst_rows = np.concatenate([[0], np.cumsum(gpu_load)])
     base = {}
-    for dst in range(G):
-        row = dst_rows[dst]
-        for e in range(E):
-            if dst in groups[e]:
-                base[(e, dst)] = row
-                row += xi[e][list(groups[e]).index(dst)]
+    row = 0
+    expert_rows = np.zeros(E + 1, dtype=np.int64)
+    for e in range(E):
+        expert_rows[e] = row
+        for dst in sorted(groups[e]):
+            base[(e, dst)] = row
+            row += xi[e][list(groups[e]).index(dst)]
+    expert_rows[E] = row
     # per (e, src): list of (rank_end, row_minus_rank) in table order
     lists = {}
     by_e = {}
@@ -66,9 +63,9 @@ def receive_rows(groups, G: int, xi, ranges, topk_idx: np.ndarray, tps: int):
         by_e.setdefault(e, []).append((s, d, c))
     for e, rs in by_e.items():
         for j, (s, d, c) in enumerate(rs):
-            row = base[(e, d)] + sum(c2 for (s2, d2, c2) in rs if d2 == d and s2 < s)
+            r = base[(e, d)] + sum(c2 for (s2, d2, c2) in rs if d2 == d and s2 < s)
             rank = sum(c2 for (s2, d2, c2) in rs[:j] if s2 == s)
-            lists.setdefault((e, s), []).append((rank + c, row - rank))
+            lists.setdefault((e, s), []).append((rank + c, r - rank))
     tok_row = np.zeros((T, K), dtype=np.int64)
     ctr = {}
     for t in range(T):
@@ -82,7 +79,7 @@ def receive_rows(groups, G: int, xi, ranges, topk_idx: np.ndarray, tps: int):
             while j + 1 < len(lst) and q >= lst[j][0]:
                 j += 1
             tok_row[t, k] = q + lst[j][1]
-    return tok_row, dst_rows
+    return tok_row, expert_rows
 
 
 def bf16_round(a: np.ndarray) -> np.ndarray:
@@ -113,7 +110,7 @@ def layer_forward(x, logits, K, groups, G, w1, w2, w3, bias=None, sample=None):
     topk_idx, topk_w = topk_select(logits, K, bias)
     hist = histogram(topk_idx, E, G, tps)
     sched = O.full_path(G, groups, hist.T.copy())
-    tok_row, dst_rows = receive_rows(groups, G, sched["xi"], sched["ranges"], topk_idx, tps)
+    tok_row, expert_rows = receive_rows(groups, G, sched["xi"], sched["ranges"], topk_idx, tps)
     toks = np.arange(T) if sample is None else np.asarray(sample)
     out = np.zeros((len(toks), x.shape[1]), dtype=np.float32)
     for k in range(K):
@@ -122,5 +119,5 @@ def layer_forward(x, logits, K, groups, G, w1, w2, w3, bias=None, sample=None):
             sel = np.nonzero(e_of == e)[0]
             y = expert_ffn(x[toks[sel]], w1[e], w3[e], w2[e])
             out[sel] += topk_w[toks[sel], k][:, None] * bf16_round(y)
-    return dict(topk_idx=topk_idx, topk_w=topk_w, hist=hist, sched=sched, tok_row=tok_row, dst_rows=dst_rows,
+    return dict(topk_idx=topk_idx, topk_w=topk_w, hist=hist, sched=sched, tok_row=tok_row, expert_rows=expert_rows,
                 out=out, tokens=toks)

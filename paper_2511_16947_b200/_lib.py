@@ -45,6 +45,7 @@ SIGNATURES = {
     "hep_sched_solve": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int64, vp, ctypes.c_int, ctypes.POINTER(HepSchedOut), vp]),
     "hep_sched_integerize": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.POINTER(HepSchedOut), vp]),
     "hep_sched_route": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int64, vp, ctypes.c_int, ctypes.POINTER(HepSchedOut), vp]),
+    "hep_sched_debug_timing": (ctypes.c_int, [c_i64p, ctypes.c_int]),
     "hep_transfer_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, vp, ctypes.c_int64, vp, vp, vp]),
     "hep_gate_topk": (ctypes.c_int, [vp, ctypes.c_int64, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int, vp, vp, vp, vp]),
     "hep_gemm_bf16": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp]),

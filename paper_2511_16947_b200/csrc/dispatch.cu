@@ -1,8 +1,10 @@
 // dispatch.cu — K4 per-assignment slot assignment, K5 permute/dispatch and
 // K7 combine/un-permute.
 //
-// Receive layout ("rows"), identical on every rank: [dst GPU][expert
-// ascending][src GPU ascending][rank within (src, expert)].  The routing table
+// Receive layout ("rows"): [expert ascending][dst GPU ascending][src GPU
+// ascending][rank within (src, expert)] — every expert's rows are contiguous
+// (one grouped-GEMM segment per expert, whichever GPUs its replicas live on;
+// on a real rank the same rule restricted to dst = this rank).  The routing table
 // (reference RoutingTable, router.py:38-46) says, for every (expert, src), how
 // its tokens are split into consecutive ranges in sequence order; K4 turns
 // that into a row for every (token, k) assignment with a deterministic stable
@@ -62,36 +64,42 @@ static AssignWs carve_ws(const hep_sched *h, void *ws, int n_src, int64_t tps) {
 
 // ---------------------------------------------------------------------------
 __global__ void plan_prep_kernel(int G, int E, int nnz, const int32_t *grp_off, const int32_t *grp_gpu,
-                                 const int32_t *hosted_off, const int32_t *seg_nnz, const int32_t *nnz_exp,
-                                 const int64_t *xi, const int64_t *ranges, const int64_t *n_ranges_p,
-                                 const int64_t *gpu_load, int64_t *dst_rows, int32_t *seg, AssignWs w,
-                                 int32_t *status) {
-    __shared__ int64_t s_dst[HEP_MAX_GPUS + 1];
+                                 const int32_t *sorted, const int32_t *nnz_exp, const int64_t *xi,
+                                 const int64_t *ranges, const int64_t *n_ranges_p, int64_t *expert_rows,
+                                 int32_t *seg, AssignWs w, int32_t *status) {
+    __shared__ int64_t scan[64];
     const int tid = threadIdx.x, nt = blockDim.x;
     const int64_t n_ranges = *n_ranges_p;
-    if (tid == 0) {
-        int64_t acc = 0;
-        for (int g = 0; g < G; ++g) { s_dst[g] = acc; dst_rows[g] = acc; acc += gpu_load[g]; }
-        s_dst[G] = acc;
-        dst_rows[G] = acc;
-        if (acc >= (int64_t)1 << 31) atomicCAS(status, 0, HEP_E_CAPACITY);
-    }
     for (int i = tid; i < E * G; i += nt) w.es_cnt[i] = 0;
     for (int i = tid; i <= E; i += nt) w.first[i] = -1;
-    __syncthreads();
-    // segments [dst][expert asc]
-    if (tid < G) {
-        int64_t row = s_dst[tid];
-        for (int p = hosted_off[tid]; p < hosted_off[tid + 1]; ++p) {
-            const int i = seg_nnz[p];
-            seg[4 * p + 0] = (int32_t)row;
-            seg[4 * p + 1] = (int32_t)xi[i];
-            seg[4 * p + 2] = nnz_exp[i];
-            seg[4 * p + 3] = tid;
-            w.row_base[i] = (int32_t)row;
-            row += xi[i];
-        }
+    // segments in [expert][dst asc] order = the scheduler's sorted arc order
+    const int chunk = (nnz + nt - 1) / nt;
+    const int p0 = min(nnz, tid * chunk), p1 = min(nnz, p0 + chunk);
+    int64_t mine = 0;
+    for (int p = p0; p < p1; ++p) mine += xi[sorted[p]];
+    int64_t total;
+    int64_t row = block_excl_scan_i64(mine, scan, &total);
+    for (int p = p0; p < p1; ++p) {
+        const int i = sorted[p];
+        const int e = nnz_exp[i];
+        seg[4 * p + 0] = (int32_t)row;
+        seg[4 * p + 1] = (int32_t)xi[i];
+        seg[4 * p + 2] = e;
+        seg[4 * p + 3] = grp_gpu[i];
+        w.row_base[i] = (int32_t)row;
+        if (p == grp_off[e]) expert_rows[e] = row;
+        row += xi[i];
     }
+    for (int e = tid; e < E; e += nt)
+        if (grp_off[e] == grp_off[e + 1]) expert_rows[e] = -1;  // fixed below
+    if (tid == 0) {
+        expert_rows[E] = total;
+        if (total >= (int64_t)1 << 31) atomicCAS(status, 0, HEP_E_CAPACITY);
+    }
+    __syncthreads();
+    if (tid == 0)  // experts without replicas own an empty row range
+        for (int e = E - 1; e >= 0; --e)
+            if (expert_rows[e] < 0) expert_rows[e] = expert_rows[e + 1];
     for (int64_t r = tid; r < n_ranges; r += nt) {
         const int e = (int)ranges[4 * r];
         if (r == 0 || ranges[4 * (r - 1)] != e) w.first[e] = (int)r;
@@ -222,43 +230,52 @@ __global__ void __launch_bounds__(256) permute_kernel(const int4 *__restrict__ x
     }
 }
 
-// K7: out[t] = sum_k w[t][k] * y[tok_row[t][k]]
+// K7: out[t] = sum_k w[t][k] * y[tok_row[t][k]], fp32 accumulation in k order.
+// One warp per token; each lane keeps 2 x K 128-bit loads in flight.
+template <int K>
 __global__ void __launch_bounds__(256) combine_kernel(const int4 *__restrict__ y, const int32_t *__restrict__ tok_row,
-                                                      const float *__restrict__ topk_w, int64_t T, int K,
-                                                      int64_t nvec, int4 *__restrict__ out) {
+                                                      const float *__restrict__ topk_w, int64_t T, int64_t nvec,
+                                                      int4 *__restrict__ out) {
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t t = warp; t < T; t += nwarps) {
-        int32_t r[16];
-        float wk[16];
+        const int4 *src[K];
+        float wk[K];
 #pragma unroll
-        for (int k = 0; k < 16; ++k)
-            if (k < K) { r[k] = tok_row[t * K + k]; wk[k] = topk_w[t * K + k]; }
-        for (int64_t v = lane; v < nvec; v += 32) {
-            float acc[8];
+        for (int k = 0; k < K; ++k) {
+            src[k] = y + (int64_t)tok_row[t * K + k] * nvec;
+            wk[k] = topk_w[t * K + k];
+        }
+        for (int64_t v0 = lane; v0 < nvec; v0 += 64) {
+            int4 in[2][K];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) acc[i] = 0.f;
-            int4 in[16];
+            for (int u = 0; u < 2; ++u)
 #pragma unroll
-            for (int k = 0; k < 16; ++k)
-                if (k < K) in[k] = __ldg(y + (int64_t)r[k] * nvec + v);
+                for (int k = 0; k < K; ++k)
+                    if (v0 + 32 * u < nvec) in[u][k] = __ldg(src[k] + v0 + 32 * u);
 #pragma unroll
-            for (int k = 0; k < 16; ++k) {
-                if (k >= K) break;
-                const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&in[k]);
+            for (int u = 0; u < 2; ++u) {
+                if (v0 + 32 * u >= nvec) break;
+                float acc[8];
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const float2 f = __bfloat1622float2(h[i]);
-                    acc[2 * i] = fmaf(wk[k], f.x, acc[2 * i]);
-                    acc[2 * i + 1] = fmaf(wk[k], f.y, acc[2 * i + 1]);
+                for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&in[u][k]);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const float2 f = __bfloat1622float2(h[i]);
+                        acc[2 * i] = fmaf(wk[k], f.x, acc[2 * i]);
+                        acc[2 * i + 1] = fmaf(wk[k], f.y, acc[2 * i + 1]);
+                    }
                 }
-            }
-            int4 o;
-            __nv_bfloat162 *oh = reinterpret_cast<__nv_bfloat162 *>(&o);
+                int4 o;
+                __nv_bfloat162 *oh = reinterpret_cast<__nv_bfloat162 *>(&o);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) oh[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
-            out[t * nvec + v] = o;
+                for (int i = 0; i < 4; ++i) oh[i] = __floats2bfloat162_rn(acc[2 * i], acc[2 * i + 1]);
+                out[t * nvec + v0 + 32 * u] = o;
+            }
         }
     }
 }
@@ -287,8 +304,8 @@ extern "C" size_t hep_moe_assign_workspace(hep_sched_t h, int64_t T, int K) {
 
 extern "C" int hep_moe_assign(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_topk_idx, int64_t T, int K,
                               int64_t tokens_per_src, int32_t *d_tok_row, int32_t *d_row_tok, int32_t *d_seg,
-                              int64_t *d_dst_rows, void *workspace, size_t workspace_bytes, void *stream) {
-    HEP_REQUIRE(h && sched && d_topk_idx && d_tok_row && d_row_tok && d_seg && d_dst_rows && workspace,
+                              int64_t *d_expert_rows, void *workspace, size_t workspace_bytes, void *stream) {
+    HEP_REQUIRE(h && sched && d_topk_idx && d_tok_row && d_row_tok && d_seg && d_expert_rows && workspace,
                 HEP_E_CONTRACT, "hep_moe_assign: null argument");
     HEP_REQUIRE(K >= 1 && K <= 16 && tokens_per_src >= 1, HEP_E_DIMENSION, "hep_moe_assign: K=%d", K);
     const int n_src = h->G;
@@ -299,9 +316,9 @@ extern "C" int hep_moe_assign(hep_sched_t h, const hep_sched_out *sched, const i
     cudaStream_t s = (cudaStream_t)stream;
     AssignWs w = carve_ws(h, workspace, n_src, tokens_per_src);
     const int E = h->E, G = h->G;
-    plan_prep_kernel<<<1, 512, 0, s>>>(G, E, h->nnz, h->d_grp_off, h->d_grp_gpu, h->d_hosted_off, h->d_seg_nnz,
-                                       h->d_nnz_exp, sched->d_xi, sched->d_ranges, sched->d_n_ranges,
-                                       sched->d_gpu_load, d_dst_rows, d_seg, w, sched->d_status);
+    plan_prep_kernel<<<1, 512, 0, s>>>(G, E, h->nnz, h->d_grp_off, h->d_grp_gpu, h->d_sorted, h->d_nnz_exp,
+                                       sched->d_xi, sched->d_ranges, sched->d_n_ranges, d_expert_rows, d_seg, w,
+                                       sched->d_status);
     HEP_CHECK_LAUNCH();
     if (T <= 0) return HEP_OK;
     const int ncs = (int)((tokens_per_src + kChunk - 1) / kChunk);
@@ -335,8 +352,19 @@ extern "C" int hep_moe_combine(const void *d_y, const int32_t *d_tok_row, const 
     HEP_REQUIRE(d_y && d_tok_row && d_topk_w && d_out, HEP_E_CONTRACT, "hep_moe_combine: null pointer");
     HEP_REQUIRE(d_model % 8 == 0 && K >= 1 && K <= 16, HEP_E_DIMENSION, "hep_moe_combine: d_model %% 8, K<=16");
     if (T <= 0) return HEP_OK;
-    combine_kernel<<<grid_for_warps(T), 256, 0, (cudaStream_t)stream>>>(
-        (const int4 *)d_y, d_tok_row, d_topk_w, T, K, d_model / 8, (int4 *)d_out);
+    const int grid = grid_for_warps(T);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int4 *yv = (const int4 *)d_y;
+    int4 *ov = (int4 *)d_out;
+    const int64_t nv = d_model / 8;
+    switch (K) {
+#define HEP_COMBINE(KK) \
+        case KK: combine_kernel<KK><<<grid, 256, 0, st>>>(yv, d_tok_row, d_topk_w, T, nv, ov); break;
+        HEP_COMBINE(1) HEP_COMBINE(2) HEP_COMBINE(3) HEP_COMBINE(4) HEP_COMBINE(5) HEP_COMBINE(6) HEP_COMBINE(7)
+        HEP_COMBINE(8) HEP_COMBINE(9) HEP_COMBINE(10) HEP_COMBINE(11) HEP_COMBINE(12) HEP_COMBINE(13)
+        HEP_COMBINE(14) HEP_COMBINE(15) HEP_COMBINE(16)
+#undef HEP_COMBINE
+    }
     HEP_CHECK_LAUNCH();
     return HEP_OK;
 }

@@ -145,6 +145,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             // ===================== TMA producer =====================
             int stage = 0;
+            // grouped expert GEMMs reuse A (token rows) across N-blocks and stream B (weights);
+            // the router GEMM streams A (x) and reuses B (Wg)
+            const uint64_t pol_a = p.grouped ? policy_evict_last() : policy_evict_first();
+            const uint64_t pol_b = p.grouped ? policy_evict_first() : policy_evict_last();
             uint32_t phase = 0;
             for (int64_t t = blockIdx.x; t < n_total; t += gridDim.x) {
                 const Tile tl = decode(p, t);
@@ -152,8 +156,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int k = 0; k < kb; ++k) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
-                    tma_load_2d(sA + stage * S::A_BYTES, &tmA, &full[stage], k * BK, tl.row0);
-                    tma_load_2d(sB + stage * S::B_BYTES, &tmB, &full[stage], k * BK, b_row);
+                    tma_load_2d_hint(sA + stage * S::A_BYTES, &tmA, &full[stage], k * BK, tl.row0, pol_a);
+                    tma_load_2d_hint(sB + stage * S::B_BYTES, &tmB, &full[stage], k * BK, b_row, pol_b);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -281,8 +285,42 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ---------------------------------------------------------------------------
 // m-tile list from segments (row_start, rows, expert, dst): expert-major.
-// One CTA; one thread per expert, deterministic block scan.
+// Consecutive segments of one expert that are contiguous in rows are merged
+// (the receive layout keeps all replicas of an expert adjacent), so an m-tile
+// may span several destination GPUs' rows of the same expert.  One CTA; one
+// thread per expert chunk, deterministic block scan.
 // ---------------------------------------------------------------------------
+template <bool WRITE>
+__device__ int64_t expert_tiles(const int32_t *seg, int n_seg, int e, int32_t *mt_row0, int32_t *mt_rows,
+                                int64_t pos) {
+    int64_t cnt = 0;
+    int32_t r0 = 0, n = 0;
+    bool open = false;
+    auto flush = [&]() {
+        for (int32_t m = 0; m < n; m += BM) {
+            if (WRITE) {
+                mt_row0[pos + cnt] = r0 + m;
+                mt_rows[pos + cnt] = min(BM, n - m);
+            }
+            ++cnt;
+        }
+    };
+    for (int s = 0; s < n_seg; ++s) {
+        if (seg[4 * s + 2] != e || seg[4 * s + 1] == 0) continue;
+        const int32_t a = seg[4 * s], b = seg[4 * s + 1];
+        if (open && a == r0 + n) {
+            n += b;
+        } else {
+            if (open) flush();
+            r0 = a;
+            n = b;
+            open = true;
+        }
+    }
+    if (open) flush();
+    return cnt;
+}
+
 __global__ void build_tiles_kernel(const int32_t *seg, int n_seg, int n_exp, int32_t *mt_row0, int32_t *mt_rows,
                                    int32_t *exp_mt_off, int64_t cap, int32_t *status) {
     __shared__ int64_t scan[64];
@@ -290,26 +328,18 @@ __global__ void build_tiles_kernel(const int32_t *seg, int n_seg, int n_exp, int
     const int chunk = (n_exp + nt - 1) / nt;
     const int e0 = min(n_exp, tid * chunk), e1 = min(n_exp, e0 + chunk);
     int64_t cnt = 0;
-    for (int e = e0; e < e1; ++e)
-        for (int s = 0; s < n_seg; ++s)
-            if (seg[4 * s + 2] == e) cnt += (seg[4 * s + 1] + BM - 1) / BM;
+    for (int e = e0; e < e1; ++e) cnt += expert_tiles<false>(seg, n_seg, e, nullptr, nullptr, 0);
     int64_t total;
     int64_t pos = block_excl_scan_i64(cnt, scan, &total);
     if (total > cap) {
         if (tid == 0 && status) atomicCAS(status, 0, HEP_E_CAPACITY);
+        if (tid == 0) exp_mt_off[n_exp] = 0;
+        for (int e = e0; e < e1; ++e) exp_mt_off[e] = 0;
         return;
     }
     for (int e = e0; e < e1; ++e) {
         exp_mt_off[e] = (int32_t)pos;
-        for (int s = 0; s < n_seg; ++s) {
-            if (seg[4 * s + 2] != e) continue;
-            const int32_t r0 = seg[4 * s], n = seg[4 * s + 1];
-            for (int32_t m = 0; m < n; m += BM) {
-                mt_row0[pos] = r0 + m;
-                mt_rows[pos] = min(BM, n - m);
-                ++pos;
-            }
-        }
+        pos += expert_tiles<true>(seg, n_seg, e, mt_row0, mt_rows, pos);
     }
     if (tid == nt - 1) exp_mt_off[n_exp] = (int32_t)total;
 }

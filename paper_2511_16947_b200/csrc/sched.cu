@@ -2,107 +2,107 @@
 //
 // Replaces, bit-exactly, the reference chain (paths under
 // /root/reference/pkg/src/harmonyep/):
-//   solve_replica_loads / warm_solve   scheduler.py:337-461  (exact m + lex-min plan)
-//   integerize_plan                    scheduler.py:697-735
-//   route_tokens / route_topology_aware router.py:114-175    (Algorithm 1)
-//   build_transfer_plan                router.py:178-226
+//   solve_replica_loads / warm_solve    scheduler.py:337-461  (exact m + lex-min plan)
+//   integerize_plan                     scheduler.py:697-735
+//   route_tokens / route_topology_aware router.py:114-175     (Algorithm 1)
+//   build_transfer_plan                 router.py:178-226
 //
 // Device algorithm (not a port of the reference's Dinic max-flow): the
 // subset (Gale/Hall) formulation of SURVEY.md Appendix B.
-//   1. totals[e] = row sums of the load matrix                       (core.py:261)
-//   2. W[S] = sum of totals of experts whose EDP group ⊆ S: zeta transform
+//   1. stage the load matrix in shared memory; totals[e] = row sums   (core.py:261)
+//   2. W[S] = summed totals of experts whose EDP group ⊆ S: zeta transform
 //      over the 2^G GPU subsets (placement.py:131-143's transform)
-//   3. m = max_S (W[S] + base(S)) / |S| — the exact min-max GPU load
-//      (Eq. 3; equal to the reference's probe/min-cut fixpoint :354-371)
+//   3. m = max_S (W[S] + base(S)) / |S| — the exact min-max GPU load (Eq. 3;
+//      the fixpoint of the reference's probe / min-cut loop :354-371)
 //   4. lex-min canonical plan (scheduler.py:295-321): for arcs (e, g) in
 //      (expert, gpu) order the minimum feasible replica load is
 //        v = max(0, max_{S ⊇ need, g ∉ S} r + Wf[S] - C[S])
-//      with need = remaining group \ {g}, Wf = not-yet-processed load inside S,
-//      C = remaining capacity of S.  One warp holds all 2^G subsets in
-//      registers (SPL per lane) and reduces with shuffles — E·d sequential
-//      steps, no block barriers inside the loop.
-//   5-7. integerize / route / transfer: one thread per expert, deterministic
-//      block scans, integer shared-memory atomics (order-independent sums).
-// Everything is exact int64 in units of 1/Q, Q = lcm(1..G) (scheduler.py:184).
+//      with need = remaining group \ {g}, Wf = not-yet-processed load inside
+//      S, C = remaining capacity of S.  One warp holds all 2^G subsets in
+//      registers (SPL per lane); when every value fits 31 bits the per-arc
+//      reduction is a single redux.sync (int32 path), else int64 shuffles.
+//   5. integerize (largest remainder, ties -> lowest GPU id), one thread per
+//      expert, shared-memory plan
+//   6. Algorithm 1 routing, one thread per contiguous expert chunk, two passes
+//      (count, block scan, emit) so the table comes out in expert order; the
+//      pairwise transfer counts are accumulated with integer shared-memory
+//      atomics during emission (order-independent, deterministic)
+//   7. transfer plan vectors from the pair matrix
+// Everything is exact integer arithmetic in units of 1/Q, Q = lcm(1..G)
+// (scheduler.py:184).
 #include <stdlib.h>
 #include <string.h>
 
 #include <vector>
 
 #include "common.cuh"
-
 #include "sched_internal.cuh"
 
 namespace hep {
 
 constexpr int kSchedThreads = 256;
+constexpr int kProfSlots = 16;
+__device__ long long g_sched_prof[kProfSlots];
 
 struct SchedArgs {
     int G, E, nnz, gpn, flags;
-    int64_t Q, max_ranges, den;  // den: denominator of d_xq (Q when solved here)
+    int64_t Q, max_ranges, den;  // den: denominator of the input plan (Q when solved here)
     const int32_t *grp_off, *grp_gpu, *sorted;
     const uint32_t *mask;
     const int64_t *loads;
     int64_t se, sg;
     const int64_t *base;
-    const int64_t *xi_in;  // route-only: caller plan
+    const int64_t *xi_in;  // route-only: caller plan (global)
     hep_sched_out out;
 };
 
-// Shared memory carve-up (dynamic): see sched_smem_bytes()
 struct SchedSmem {
-    int64_t *totals;  // [E]
-    int64_t *W;       // [NS]
-    int32_t *grp_off; // [E+1]
-    uint32_t *mask;   // [E]
-    int32_t *arc_idx; // [nnz] sorted arcs: nnz index
-    int32_t *arc_gpu; // [nnz] sorted arcs: gpu
-    int64_t *gpu_load;// [G]
-    int64_t *pair;    // [G*G]
-    int64_t *scan;    // [kSchedThreads/32 + 2]
-    int64_t *misc;    // [8]
+    int64_t *totals;    // [E]
+    int64_t *W;         // [2^G]
+    int64_t *loads;     // [E*G]
+    int64_t *xq;        // [nnz]
+    int64_t *xi;        // [nnz]
+    int64_t *gpu_load;  // [G]
+    unsigned long long *pair;  // [G*G]
+    int64_t *scan;      // [kSchedThreads/32 + 2]
+    int64_t *misc;      // [8]
+    int32_t *grp_off;   // [E+1]
+    int32_t *grp_gpu;   // [nnz] list order
+    int32_t *arc_idx;   // [nnz] arcs in (e, gpu id) order: nnz index
+    int32_t *arc_gpu;   // [nnz] arcs in (e, gpu id) order: gpu
+    uint32_t *mask;     // [E]
 };
 
 __host__ __device__ inline size_t align8(size_t x) { return (x + 7) & ~size_t(7); }
 
 __host__ __device__ inline size_t sched_smem_bytes(int G, int E, int nnz) {
-    size_t ns = size_t(1) << G;
-    size_t b = 0;
-    b += align8(sizeof(int64_t) * E);
-    b += align8(sizeof(int64_t) * ns);
-    b += align8(sizeof(int32_t) * (E + 1));
-    b += align8(sizeof(uint32_t) * E);
-    b += align8(sizeof(int32_t) * nnz);
-    b += align8(sizeof(int32_t) * nnz);
-    b += align8(sizeof(int64_t) * G);
-    b += align8(sizeof(int64_t) * G * G);
-    b += align8(sizeof(int64_t) * (kSchedThreads / 32 + 2));
-    b += align8(sizeof(int64_t) * 8);
-    return b;
+    const size_t ns = size_t(1) << G;
+    return align8(8 * (size_t)E) + align8(8 * ns) + align8(8 * (size_t)E * G) + 2 * align8(8 * (size_t)nnz) +
+           align8(8 * (size_t)G) + align8(8 * (size_t)G * G) + align8(8 * (kSchedThreads / 32 + 2)) + 64 +
+           align8(4 * (size_t)(E + 1)) + 3 * align8(4 * (size_t)nnz) + align8(4 * (size_t)E);
 }
 
-__device__ inline SchedSmem carve(char *base, int G, int E, int nnz) {
+__device__ inline SchedSmem carve(char *p, int G, int E, int nnz) {
     SchedSmem s;
-    size_t ns = size_t(1) << G;
-    char *p = base;
-    s.totals = (int64_t *)p; p += align8(sizeof(int64_t) * E);
-    s.W = (int64_t *)p; p += align8(sizeof(int64_t) * ns);
-    s.grp_off = (int32_t *)p; p += align8(sizeof(int32_t) * (E + 1));
-    s.mask = (uint32_t *)p; p += align8(sizeof(uint32_t) * E);
-    s.arc_idx = (int32_t *)p; p += align8(sizeof(int32_t) * nnz);
-    s.arc_gpu = (int32_t *)p; p += align8(sizeof(int32_t) * nnz);
-    s.gpu_load = (int64_t *)p; p += align8(sizeof(int64_t) * G);
-    s.pair = (int64_t *)p; p += align8(sizeof(int64_t) * G * G);
-    s.scan = (int64_t *)p; p += align8(sizeof(int64_t) * (kSchedThreads / 32 + 2));
-    s.misc = (int64_t *)p;
+    const size_t ns = size_t(1) << G;
+    s.totals = (int64_t *)p; p += align8(8 * (size_t)E);
+    s.W = (int64_t *)p; p += align8(8 * ns);
+    s.loads = (int64_t *)p; p += align8(8 * (size_t)E * G);
+    s.xq = (int64_t *)p; p += align8(8 * (size_t)nnz);
+    s.xi = (int64_t *)p; p += align8(8 * (size_t)nnz);
+    s.gpu_load = (int64_t *)p; p += align8(8 * (size_t)G);
+    s.pair = (unsigned long long *)p; p += align8(8 * (size_t)G * G);
+    s.scan = (int64_t *)p; p += align8(8 * (kSchedThreads / 32 + 2));
+    s.misc = (int64_t *)p; p += 64;
+    s.grp_off = (int32_t *)p; p += align8(4 * (size_t)(E + 1));
+    s.grp_gpu = (int32_t *)p; p += align8(4 * (size_t)nnz);
+    s.arc_idx = (int32_t *)p; p += align8(4 * (size_t)nnz);
+    s.arc_gpu = (int32_t *)p; p += align8(4 * (size_t)nnz);
+    s.mask = (uint32_t *)p;
     return s;
 }
 
-__device__ __forceinline__ int64_t ld_load(const SchedArgs &a, int e, int g) {
-    return a.loads[(int64_t)e * a.se + (int64_t)g * a.sg];
-}
-
-// frac a/b > c/d with small positive denominators (<= 64) and |num| < 2^56
+// a/b > c/d, denominators <= 64, |numerators| < 2^56
 __device__ __forceinline__ bool frac_gt(int64_t a, int64_t b, int64_t c, int64_t d) {
     return (__int128)a * d > (__int128)c * b;
 }
@@ -110,44 +110,49 @@ __device__ __forceinline__ bool frac_gt(int64_t a, int64_t b, int64_t c, int64_t
 __device__ __forceinline__ int64_t gcd_i64(int64_t a, int64_t b) {
     if (a < 0) a = -a;
     while (b) {
-        int64_t t = a % b;
+        const int64_t t = a % b;
         a = b;
         b = t;
     }
     return a;
 }
 
+__device__ __forceinline__ void prof_mark(int flags, int slot) {
+    if ((flags & HEP_SCHED_PROFILE) && threadIdx.x == 0 && slot < kProfSlots) g_sched_prof[slot] = clock64();
+}
+
+// warp max of non-negative values
+__device__ __forceinline__ int64_t wmax(int64_t v) { return warp_max_i64(v); }
+__device__ __forceinline__ int32_t wmax(int32_t v) {
+    return (int32_t)__reduce_max_sync(0xffffffffu, (unsigned)v);
+}
+
 // ---------------------------------------------------------------------------
-// Step 4: lex-min canonical plan, warp 0 only.  SPL subsets per lane.
+// step 4: lex-min canonical plan, warp 0; V = int32_t when every quantity fits
 // ---------------------------------------------------------------------------
-template <int SPL>
+template <int SPL, typename V>
 __device__ void lexmin_warp(const SchedArgs &a, SchedSmem &s, int64_t mQ) {
     const int lane = threadIdx.x & 31;
     const int G = a.G, E = a.E;
-    const int NS = 1 << G;
+    const uint32_t NS = 1u << G;
     const int64_t Q = a.Q;
-    int64_t Wf[SPL], C[SPL];
-    int64_t cap[HEP_MAX_GPUS];
-#pragma unroll
-    for (int g = 0; g < HEP_MAX_GPUS; ++g) {
-        int64_t bq = (g < G && a.base) ? a.base[g] * Q : 0;
-        int64_t c = mQ - bq;
-        cap[g] = (g < G && c > 0) ? c : 0;
-    }
+    V Wf[SPL], C[SPL];
 #pragma unroll
     for (int j = 0; j < SPL; ++j) {
-        const int S = lane + 32 * j;
+        const uint32_t S = lane + 32 * j;
         int64_t c = 0;
-#pragma unroll
-        for (int g = 0; g < HEP_MAX_GPUS; ++g)
-            if ((S >> g) & 1) c += cap[g];
-        C[j] = c;
-        Wf[j] = S < NS ? s.W[S] * Q : 0;
+        for (int g = 0; g < G; ++g) {
+            if (!((S >> g) & 1)) continue;
+            const int64_t cg = mQ - (a.base ? a.base[g] * Q : 0);
+            c += cg > 0 ? cg : 0;
+        }
+        C[j] = (V)c;
+        Wf[j] = S < NS ? (V)(s.W[S] * Q) : (V)0;
     }
     for (int e = 0; e < E; ++e) {
         const int b = s.grp_off[e], n = s.grp_off[e + 1] - b;
         if (n == 0) continue;
-        int64_t r = s.totals[e] * Q;
+        V r = (V)(s.totals[e] * Q);
         uint32_t R = s.mask[e];
         if (r > 0) {
 #pragma unroll
@@ -160,23 +165,23 @@ __device__ void lexmin_warp(const SchedArgs &a, SchedSmem &s, int64_t mQ) {
             const int g = s.arc_gpu[b + k];
             const uint32_t gbit = 1u << g;
             const uint32_t need = R & ~gbit;
-            int64_t v;
+            V v;
             if (r == 0) {
-                v = 0;  // Wf <= C everywhere (feasible state) => bound <= 0
+                v = 0;  // Wf <= C on every subset (feasible state): the bound is <= 0
             } else if (need == 0) {
-                v = r;  // S = {} attains r; every other bound is <= r
+                v = r;  // S = {} attains r and every other bound is <= r
             } else {
-                int64_t best = 0;
+                V best = 0;
 #pragma unroll
                 for (int j = 0; j < SPL; ++j) {
                     const uint32_t S = lane + 32 * j;
-                    const bool ok = (S < (uint32_t)NS) && ((S & need) == need) && !(S & gbit);
-                    const int64_t cand = r + Wf[j] - C[j];
+                    const bool ok = (S < NS) && ((S & need) == need) && !(S & gbit);
+                    const V cand = r + Wf[j] - C[j];
                     if (ok && cand > best) best = cand;
                 }
-                v = __any_sync(0xffffffffu, best > 0) ? warp_max_i64(best) : 0;
+                v = wmax(best);
             }
-            if (lane == 0) a.out.d_xq[s.arc_idx[b + k]] = v;
+            if (lane == 0) s.xq[s.arc_idx[b + k]] = (int64_t)v;
             r -= v;
             R = need;
             if (v) {
@@ -195,49 +200,61 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
     extern __shared__ __align__(16) char smem_raw[];
     SchedSmem s = carve(smem_raw, a.G, a.E, a.nnz);
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int G = a.G, E = a.E, NS = 1 << G;
+    const int G = a.G, E = a.E, nnz = a.nnz;
+    const int NS = 1 << G;
     int32_t *status = a.out.d_status;
+    const bool solve = a.flags & HEP_SCHED_SOLVE;
+    const bool route = a.flags & HEP_SCHED_ROUTE;
+    prof_mark(a.flags, 0);
 
-    // placement tables -> smem (all stages read them in sequential loops)
+    // ---- step 1: stage placement + loads (+ caller plan) in shared memory -------
     for (int i = tid; i <= E; i += nt) s.grp_off[i] = a.grp_off[i];
     for (int i = tid; i < E; i += nt) s.mask[i] = a.mask[i];
-    for (int i = tid; i < a.nnz; i += nt) {
-        int idx = a.sorted[i];
+    for (int i = tid; i < nnz; i += nt) {
+        const int idx = a.sorted[i];
         s.arc_idx[i] = idx;
         s.arc_gpu[i] = a.grp_gpu[idx];
+        s.grp_gpu[i] = a.grp_gpu[i];
+        if (!solve) s.xq[i] = a.out.d_xq[i];
+        if (a.xi_in) s.xi[i] = a.xi_in[i];
     }
+    const bool need_loads = solve || route;
+    int bad = 0;
+    if (need_loads) {
+        for (int i = tid; i < E * G; i += nt) {
+            const int e = i / G, g = i - e * G;
+            const int64_t v = a.loads[(int64_t)e * a.se + (int64_t)g * a.sg];
+            bad |= v < 0;
+            s.loads[i] = v;
+        }
+    }
+    for (int i = tid; i < G * G; i += nt) s.pair[i] = 0;
+    for (int g = tid; g < G; g += nt) s.gpu_load[g] = 0;
     if (tid == 0) *status = 0;
     __syncthreads();
-
-    // ---------------- step 1: expert totals (LoadMatrix.expert_totals) -------------
-    const bool solve = a.flags & HEP_SCHED_SOLVE;
-    const bool need_loads = solve || (a.flags & HEP_SCHED_ROUTE);
-    int64_t my_total = 0, my_bad = 0;
+    if (bad) set_status(status, HEP_E_CONTRACT);
+    int64_t my_total = 0;
     if (need_loads) {
         for (int e = tid; e < E; e += nt) {
             int64_t t = 0;
-            for (int g = 0; g < G; ++g) {
-                int64_t v = ld_load(a, e, g);
-                if (v < 0) my_bad = 1;
-                t += v;
-            }
+            for (int g = 0; g < G; ++g) t += s.loads[e * G + g];
             s.totals[e] = t;
             my_total += t;
-            // scheduler.py:344-347 loaded expert with an empty EDP group
+            // scheduler.py:344-347: a loaded expert with an empty EDP group
             if (solve && t > 0 && s.grp_off[e + 1] == s.grp_off[e]) set_status(status, HEP_E_PLACEMENT);
         }
-        if (my_bad) set_status(status, HEP_E_CONTRACT);
     }
     int64_t base_sum = 0;
     if (tid == 0 && a.base)
         for (int g = 0; g < G; ++g) base_sum += a.base[g];
-    int64_t total_all = block_sum_i64(my_total + base_sum, s.scan);
+    const int64_t total_all = block_sum_i64(my_total + base_sum, s.scan);
     if (solve && (__int128)total_all * a.Q >= ((__int128)1 << 56)) set_status(status, HEP_E_CAPACITY);
     __syncthreads();
     if (*status) return;
+    prof_mark(a.flags, 1);
 
     if (solve) {
-        // ---------------- step 2: zeta transform over GPU subsets ----------------
+        // ---- step 2: zeta transform over GPU subsets --------------------------
         for (int S = tid; S < NS; S += nt) s.W[S] = 0;
         __syncthreads();
         for (int e = tid; e < E; e += nt)
@@ -249,23 +266,22 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
                 if ((S >> bit) & 1) s.W[S] += s.W[S ^ (1 << bit)];
             __syncthreads();
         }
-        // ---------------- step 3: m = max density (Eq. 3) ------------------------
+        // ---- step 3: m = max subset density (Eq. 3) ---------------------------
         int64_t bn = 0, bd = 1;
-        if (tid == 0 && a.base) {  // candidate max(base) (scheduler.py:357)
+        if (tid == 0 && a.base)  // candidate max(base) (scheduler.py:357)
             for (int g = 0; g < G; ++g)
                 if (a.base[g] > bn) bn = a.base[g];
-        }
         for (int S = tid + 1; S < NS; S += nt) {
             int64_t num = s.W[S];
             if (a.base)
                 for (int g = 0; g < G; ++g)
                     if ((S >> g) & 1) num += a.base[g];
-            int64_t den = __popc(S);
+            const int64_t den = __popc(S);
             if (frac_gt(num, den, bn, bd)) { bn = num; bd = den; }
         }
-        // block argmax over fractions
+#pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
-            int64_t on = __shfl_xor_sync(0xffffffffu, bn, o), od = __shfl_xor_sync(0xffffffffu, bd, o);
+            const int64_t on = __shfl_xor_sync(0xffffffffu, bn, o), od = __shfl_xor_sync(0xffffffffu, bd, o);
             if (frac_gt(on, od, bn, bd)) { bn = on; bd = od; }
         }
         __shared__ int64_t red_n[kSchedThreads / 32], red_d[kSchedThreads / 32];
@@ -276,64 +292,72 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
                 if (frac_gt(red_n[w], red_d[w], bn, bd)) { bn = red_n[w]; bd = red_d[w]; }
             int64_t g = gcd_i64(bn, bd);
             if (g == 0) g = 1;
-            bn /= g; bd /= g;
-            s.misc[0] = bn;
-            s.misc[1] = bd;
-            s.misc[2] = bn * (a.Q / bd);  // m scaled by Q (scheduler.py:267)
+            bn /= g;
+            bd /= g;
+            s.misc[0] = bn * (a.Q / bd);  // m scaled by Q (scheduler.py:267)
             a.out.d_m[0] = bn;
             a.out.d_m[1] = bd;
             a.out.d_m[2] = a.Q;
         }
         __syncthreads();
-        // ---------------- step 4: lex-min canonical plan -------------------------
-        if (tid < 32) lexmin_warp<SPL>(a, s, s.misc[2]);
+        prof_mark(a.flags, 2);
+        // ---- step 4: lex-min canonical plan ------------------------------------
+        if (tid < 32) {
+            const int64_t mQ = s.misc[0];
+            const bool fits32 = (__int128)G * (total_all + 1) * a.Q < ((__int128)1 << 31) &&
+                                (__int128)G * (mQ + 1) < ((__int128)1 << 31);
+            if (fits32) lexmin_warp<SPL, int32_t>(a, s, mQ);
+            else lexmin_warp<SPL, int64_t>(a, s, mQ);
+        }
         __syncthreads();
+        for (int i = tid; i < nnz; i += nt) a.out.d_xq[i] = s.xq[i];
+        prof_mark(a.flags, 3);
     }
 
-    const int64_t den = solve ? a.Q : a.den;
-    // ---------------- step 5: integerize (largest remainder) ----------------------
+    // ---- step 5: integerize (largest remainder, ties -> lowest GPU id) -----------
     if (a.flags & HEP_SCHED_INTEGERIZE) {
-        for (int g = tid; g < G; g += nt) s.gpu_load[g] = 0;
-        __syncthreads();
+        const int64_t den = solve ? a.Q : a.den;
         for (int e = tid; e < E; e += nt) {
             const int b = s.grp_off[e], n = s.grp_off[e + 1] - b;
-            __int128 total = 0;
-            int64_t sum_floor = 0;
+            int64_t total = 0, sum_floor = 0;
             for (int k = 0; k < n; ++k) {
-                int64_t v = a.out.d_xq[b + k];
-                int64_t fl = v >= 0 ? v / den : -((-v + den - 1) / den);
-                a.out.d_xi[b + k] = fl;
+                const int64_t v = s.xq[b + k];
+                const int64_t fl = v >= 0 ? v / den : -((-v + den - 1) / den);
+                s.xi[b + k] = fl;
                 sum_floor += fl;
                 total += v;
             }
-            // round(total) must be an integer within 1e-6 (scheduler.py:706-713)
-            int64_t t_fl = (int64_t)(total >= 0 ? total / den : -((-total + den - 1) / den));
-            int64_t t_rem = (int64_t)(total - (__int128)t_fl * den);
+            // round(total) must be an integer within 1e-6 (scheduler.py:706-713);
+            // Python rounds half to even
+            const int64_t t_fl = total >= 0 ? total / den : -((-total + den - 1) / den);
+            const int64_t t_rem = total - t_fl * den;
             int64_t rounded = t_fl;
-            if (2 * (__int128)t_rem > den || (2 * (__int128)t_rem == den && (t_fl & 1))) rounded = t_fl + 1;
-            __int128 diff = total - (__int128)rounded * den;
+            if (t_rem > den - t_rem || (t_rem == den - t_rem && (t_fl & 1))) rounded = t_fl + 1;
+            int64_t diff = total - rounded * den;
             if (diff < 0) diff = -diff;
-            if (diff * 1000000 > den) { set_status(status, HEP_E_CONTRACT); continue; }
-            int64_t units = rounded - sum_floor;
-            // remainder desc, ties -> lowest GPU id (key :718-721)
+            if ((__int128)diff * 1000000 > den) { set_status(status, HEP_E_CONTRACT); continue; }
+            const int64_t units = rounded - sum_floor;
             for (int u = 0; u < units && u < n; ++u) {
                 int best = -1, best_gpu = 0;
                 int64_t best_rem = -1;
                 for (int k = 0; k < n; ++k) {
-                    int64_t rem = a.out.d_xq[b + k] - a.out.d_xi[b + k] * den;
+                    const int64_t rem = s.xq[b + k] - s.xi[b + k] * den;
                     if (rem < 0) continue;  // already rounded up
-                    int gg = a.grp_gpu[b + k];
+                    const int gg = s.grp_gpu[b + k];
                     if (best < 0 || rem > best_rem || (rem == best_rem && gg < best_gpu)) {
-                        best = k; best_rem = rem; best_gpu = gg;
+                        best = k;
+                        best_rem = rem;
+                        best_gpu = gg;
                     }
                 }
                 if (best < 0) break;
-                a.out.d_xi[b + best] += 1;
+                s.xi[b + best] += 1;
             }
             for (int k = 0; k < n; ++k)
-                atomicAdd((unsigned long long *)&s.gpu_load[a.grp_gpu[b + k]], (unsigned long long)a.out.d_xi[b + k]);
+                atomicAdd((unsigned long long *)&s.gpu_load[s.grp_gpu[b + k]], (unsigned long long)s.xi[b + k]);
         }
         __syncthreads();
+        for (int i = tid; i < nnz; i += nt) a.out.d_xi[i] = s.xi[i];
         if (tid == 0) {
             int64_t mx = 0;
             for (int g = 0; g < G; ++g) {
@@ -343,15 +367,14 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
             a.out.d_m[3] = mx;
         }
         __syncthreads();
+        prof_mark(a.flags, 4);
     }
     if (*status) return;
 
-    // ---------------- step 6: Algorithm 1 routing (router.py:114-158) ------------------
-    if (a.flags & HEP_SCHED_ROUTE) {
-        const int64_t *xi = a.xi_in ? a.xi_in : a.out.d_xi;
+    // ---- step 6: Algorithm 1 routing (router.py:114-158) --------------------------
+    if (route) {
         const bool topo = (a.flags & HEP_SCHED_TOPO) && a.gpn > 0 && a.gpn < G;
-        // contiguous expert chunk per thread keeps ranges in expert order
-        const int chunk = (E + nt - 1) / nt;
+        const int chunk = (E + nt - 1) / nt;  // contiguous experts per thread: table in expert order
         const int e0 = min(E, tid * chunk), e1 = min(E, e0 + chunk);
         int64_t rin[HEP_MAX_GPUS], rx[HEP_MAX_GPUS];
         int64_t my_count = 0;
@@ -366,40 +389,48 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
             for (int e = e0; e < e1; ++e) {
                 const int b = s.grp_off[e], n = s.grp_off[e + 1] - b;
                 int64_t tot = 0, xs = 0;
-                for (int g = 0; g < G; ++g) { rin[g] = ld_load(a, e, g); rx[g] = 0; tot += rin[g]; }
-                if (n == 0 && tot == 0) continue;  // :125-126
-                bool bad = false;
-                for (int k = 0; k < n; ++k) {
-                    int64_t v = xi[b + k];
-                    if (v < 0) bad = true;
-                    xs += v;
-                    rx[a.grp_gpu[b + k]] = v;
+                for (int g = 0; g < G; ++g) {
+                    rin[g] = s.loads[e * G + g];
+                    rx[g] = 0;
+                    tot += rin[g];
                 }
-                if (bad || xs != tot) { set_status(status, HEP_E_CONTRACT); continue; }  // _check_plan :97-111
-#define HEP_EMIT(S_, D_, Y_)                                                   \
-    do {                                                                       \
-        if (pass == 0) {                                                       \
-            ++my_count;                                                        \
-        } else {                                                               \
-            int64_t *r_ = a.out.d_ranges + 4 * pos;                            \
-            r_[0] = e; r_[1] = (S_); r_[2] = (D_); r_[3] = (Y_);                \
-            ++pos;                                                             \
-        }                                                                      \
+                if (n == 0 && tot == 0) continue;  // :125-126
+                bool neg = false;
+                for (int k = 0; k < n; ++k) {
+                    const int64_t v = s.xi[b + k];
+                    neg |= v < 0;
+                    xs += v;
+                    rx[s.grp_gpu[b + k]] = v;
+                }
+                if (neg || xs != tot) { set_status(status, HEP_E_CONTRACT); continue; }  // _check_plan :97-111
+#define HEP_EMIT(S_, D_, Y_)                                                            \
+    do {                                                                                \
+        if (pass == 0) {                                                                \
+            ++my_count;                                                                 \
+        } else {                                                                        \
+            int64_t *r_ = a.out.d_ranges + 4 * pos;                                     \
+            r_[0] = e;                                                                  \
+            r_[1] = (S_);                                                               \
+            r_[2] = (D_);                                                               \
+            r_[3] = (Y_);                                                               \
+            atomicAdd(&s.pair[(S_) * G + (D_)], (unsigned long long)(Y_));              \
+            ++pos;                                                                      \
+        }                                                                               \
     } while (0)
-                // phase 1: same GPU, sorted(group)
+                // phase 1: keep tokens on their source GPU, g in sorted(group)
                 for (int k = 0; k < n; ++k) {
                     const int g = s.arc_gpu[b + k];
-                    int64_t y = rin[g] < rx[g] ? rin[g] : rx[g];
+                    const int64_t y = rin[g] < rx[g] ? rin[g] : rx[g];
                     if (y > 0) { HEP_EMIT(g, g, y); rin[g] -= y; rx[g] -= y; }
                 }
-                // phase 2 (topology-aware): same node
+                // phase 2 (topology-aware only): same node
                 if (topo) {
                     for (int src = 0; src < G; ++src) {
                         if (rin[src] == 0) continue;
                         for (int k = 0; k < n; ++k) {
-                            const int dst = a.grp_gpu[b + k];
+                            const int dst = s.grp_gpu[b + k];
                             if (dst == src || dst / a.gpn != src / a.gpn) continue;
-                            int64_t y = rin[src] < rx[dst] ? rin[src] : rx[dst];
+                            const int64_t y = rin[src] < rx[dst] ? rin[src] : rx[dst];
                             if (y > 0) { HEP_EMIT(src, dst, y); rin[src] -= y; rx[dst] -= y; }
                         }
                     }
@@ -408,8 +439,8 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
                 for (int src = 0; src < G; ++src) {
                     if (rin[src] == 0) continue;
                     for (int k = 0; k < n; ++k) {
-                        const int dst = a.grp_gpu[b + k];
-                        int64_t y = rin[src] < rx[dst] ? rin[src] : rx[dst];
+                        const int dst = s.grp_gpu[b + k];
+                        const int64_t y = rin[src] < rx[dst] ? rin[src] : rx[dst];
                         if (y > 0) { HEP_EMIT(src, dst, y); rin[src] -= y; rx[dst] -= y; }
                     }
                 }
@@ -419,37 +450,31 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
             if (*status) break;
         }
         __syncthreads();
+        prof_mark(a.flags, 5);
     }
     if (*status) return;
 
-    // ---------------- step 7: transfer plan (router.py:178-226) ------------------------
-    if (a.flags & HEP_SCHED_TRANSFER) {
-        for (int i = tid; i < G * G; i += nt) s.pair[i] = 0;
-        __syncthreads();
-        const int64_t n = *a.out.d_n_ranges;
-        for (int64_t i = tid; i < n; i += nt) {
-            const int64_t *r = a.out.d_ranges + 4 * i;
-            atomicAdd((unsigned long long *)&s.pair[r[1] * G + r[2]], (unsigned long long)r[3]);
-        }
-        __syncthreads();
+    // ---- step 7: transfer plan (router.py:178-226) from the pair matrix ----------
+    if (route && (a.flags & HEP_SCHED_TRANSFER)) {
         int64_t *T = a.out.d_transfer;
         const int gpn = a.gpn > 0 ? a.gpn : G;
-        for (int i = tid; i < G * G; i += nt) T[i] = s.pair[i];
+        for (int i = tid; i < G * G; i += nt) T[i] = (int64_t)s.pair[i];
         for (int g = tid; g < G; g += nt) {
-            int64_t send = 0, recv = 0, si = 0, ri = 0, sx = 0, rx = 0;
+            int64_t send = 0, recv = 0, si = 0, ri = 0, sx = 0, rxv = 0;
             for (int o = 0; o < G; ++o) {
                 if (o == g) continue;
-                int64_t out_c = s.pair[g * G + o], in_c = s.pair[o * G + g];
-                send += out_c; recv += in_c;
-                if (o / gpn == g / gpn) { si += out_c; ri += in_c; } else { sx += out_c; rx += in_c; }
+                const int64_t oc = s.pair[g * G + o], ic = s.pair[o * G + g];
+                send += oc;
+                recv += ic;
+                if (o / gpn == g / gpn) { si += oc; ri += ic; } else { sx += oc; rxv += ic; }
             }
             T[G * G + 0 * G + g] = send;
             T[G * G + 1 * G + g] = recv;
-            T[G * G + 2 * G + g] = s.pair[g * G + g];
+            T[G * G + 2 * G + g] = (int64_t)s.pair[g * G + g];
             T[G * G + 3 * G + g] = si;
             T[G * G + 4 * G + g] = ri;
             T[G * G + 5 * G + g] = sx;
-            T[G * G + 6 * G + g] = rx;
+            T[G * G + 6 * G + g] = rxv;
         }
         if (tid == 0) {
             int64_t intra = 0, inter = 0;
@@ -462,6 +487,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
             T[G * G + 7 * G + 1] = inter;
         }
     }
+    prof_mark(a.flags, 6);
 }
 
 // Standalone transfer plan over an arbitrary routing table (router.py:178-226)
@@ -484,12 +510,18 @@ __global__ void transfer_kernel(int G, int gpn, const int64_t *ranges, int64_t n
         int64_t send = 0, recv = 0, si = 0, ri = 0, sx = 0, rx = 0;
         for (int o = 0; o < G; ++o) {
             if (o == g) continue;
-            int64_t oc = pair[g * G + o], ic = pair[o * G + g];
-            send += oc; recv += ic;
+            const int64_t oc = pair[g * G + o], ic = pair[o * G + g];
+            send += oc;
+            recv += ic;
             if (o / gpn == g / gpn) { si += oc; ri += ic; } else { sx += oc; rx += ic; }
         }
-        T[G * G + g] = send; T[G * G + G + g] = recv; T[G * G + 2 * G + g] = pair[g * G + g];
-        T[G * G + 3 * G + g] = si; T[G * G + 4 * G + g] = ri; T[G * G + 5 * G + g] = sx; T[G * G + 6 * G + g] = rx;
+        T[G * G + g] = send;
+        T[G * G + G + g] = recv;
+        T[G * G + 2 * G + g] = pair[g * G + g];
+        T[G * G + 3 * G + g] = si;
+        T[G * G + 4 * G + g] = ri;
+        T[G * G + 5 * G + g] = sx;
+        T[G * G + 6 * G + g] = rx;
     }
     if (tid == 0) {
         int64_t intra = 0, inter = 0;
@@ -501,33 +533,41 @@ __global__ void transfer_kernel(int G, int gpn, const int64_t *ranges, int64_t n
     }
 }
 
-static int launch_sched(hep_sched *h, SchedArgs &a, cudaStream_t stream) {
-    a.G = h->G; a.E = h->E; a.nnz = h->nnz; a.gpn = h->gpn; a.Q = h->Q; a.max_ranges = h->max_ranges;
-    a.grp_off = h->d_grp_off; a.grp_gpu = h->d_grp_gpu; a.sorted = h->d_sorted; a.mask = h->d_mask;
-    size_t smem = sched_smem_bytes(h->G, h->E, h->nnz);
-    HEP_REQUIRE(smem <= 200 * 1024, HEP_E_CAPACITY, "scheduler shared memory %zu B exceeds 200 KB (E=%d G=%d)", smem,
-                h->E, h->G);
-    const int spl = h->G <= 5 ? 1 : (1 << (h->G - 5));
-#define HEP_LAUNCH_SPL(N)                                                                          \
-    case N: {                                                                                      \
-        HEP_CHECK_CUDA(cudaFuncSetAttribute(sched_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-        sched_kernel<N><<<1, kSchedThreads, smem, stream>>>(a);                                    \
-        break;                                                                                     \
+template <int SPL>
+static int launch_spl(hep_sched *h, const SchedArgs &a, size_t smem, cudaStream_t stream) {
+    if (h->smem_set < smem) {
+        HEP_CHECK_CUDA(cudaFuncSetAttribute(sched_kernel<SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        h->smem_set = smem;
     }
-    switch (spl) {
-        HEP_LAUNCH_SPL(1)
-        HEP_LAUNCH_SPL(2)
-        HEP_LAUNCH_SPL(4)
-        HEP_LAUNCH_SPL(8)
-        HEP_LAUNCH_SPL(16)
-        HEP_LAUNCH_SPL(32)
-        default:
-            set_error("unsupported G=%d", h->G);
-            return HEP_E_CAPACITY;
-    }
-#undef HEP_LAUNCH_SPL
+    sched_kernel<SPL><<<1, kSchedThreads, smem, stream>>>(a);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
+}
+
+static int launch_sched(hep_sched *h, SchedArgs &a, cudaStream_t stream) {
+    a.G = h->G;
+    a.E = h->E;
+    a.nnz = h->nnz;
+    a.gpn = h->gpn;
+    a.Q = h->Q;
+    a.max_ranges = h->max_ranges;
+    a.grp_off = h->d_grp_off;
+    a.grp_gpu = h->d_grp_gpu;
+    a.sorted = h->d_sorted;
+    a.mask = h->d_mask;
+    const size_t smem = sched_smem_bytes(h->G, h->E, h->nnz);
+    HEP_REQUIRE(smem <= 200 * 1024, HEP_E_CAPACITY, "scheduler shared memory %zu B exceeds 200 KB (E=%d G=%d)", smem,
+                h->E, h->G);
+    switch (h->G <= 5 ? 1 : (1 << (h->G - 5))) {
+        case 1: return launch_spl<1>(h, a, smem, stream);
+        case 2: return launch_spl<2>(h, a, smem, stream);
+        case 4: return launch_spl<4>(h, a, smem, stream);
+        case 8: return launch_spl<8>(h, a, smem, stream);
+        case 16: return launch_spl<16>(h, a, smem, stream);
+        case 32: return launch_spl<32>(h, a, smem, stream);
+    }
+    set_error("unsupported G=%d", h->G);
+    return HEP_E_CAPACITY;
 }
 
 }  // namespace hep
@@ -544,7 +584,7 @@ extern "C" int hep_sched_create(int num_gpus, int num_experts, const int32_t *gr
     HEP_REQUIRE(grp_off && grp_off[0] == 0, HEP_E_CONTRACT, "grp_off must start at 0");
     const int E = num_experts, G = num_gpus;
     const int nnz = grp_off[E];
-    std::vector<int32_t> off(grp_off, grp_off + E + 1), gpu(grp_gpu, grp_gpu + nnz), sorted(nnz);
+    std::vector<int32_t> off(grp_off, grp_off + E + 1), gpu(grp_gpu, grp_gpu + nnz), sorted(nnz), nnz_exp(nnz);
     std::vector<uint32_t> mask(E, 0);
     int64_t max_ranges = 0;
     for (int e = 0; e < E; ++e) {
@@ -554,27 +594,45 @@ extern "C" int hep_sched_create(int num_gpus, int num_experts, const int32_t *gr
             HEP_REQUIRE(!(mask[e] >> gpu[i] & 1u), HEP_E_PLACEMENT, "expert %d: duplicate GPU %d in EDP group", e,
                         gpu[i]);
             mask[e] |= 1u << gpu[i];
+            nnz_exp[i] = e;
         }
         // arcs of expert e in (e, gpu id) order (scheduler.py:303 sorted(arc_edges))
         int k = off[e];
         for (int g = 0; g < G; ++g)
             for (int i = off[e]; i < off[e + 1]; ++i)
                 if (gpu[i] == g) sorted[k++] = i;
-        const int n = off[e + 1] - off[e];
-        max_ranges += 3 * n + 2 * G;
+        max_ranges += 3 * (off[e + 1] - off[e]) + 2 * G;
     }
-    int gpn = gpus_per_node <= 0 ? G : gpus_per_node;
+    const int gpn = gpus_per_node <= 0 ? G : gpus_per_node;
     HEP_REQUIRE(G % gpn == 0, HEP_E_DIMENSION, "gpus_per_node=%d does not divide num_gpus=%d", gpn, G);
     int64_t Q = 1;
     for (int i = 2; i <= G; ++i) {
-        int64_t a = Q, b = i;
-        while (b) { int64_t t = a % b; a = b; b = t; }
-        Q = Q / a * i;
+        int64_t x = Q, y = i;
+        while (y) {
+            const int64_t t = x % y;
+            x = y;
+            y = t;
+        }
+        Q = Q / x * i;
     }
     hep_sched *h = new hep_sched();
-    h->G = G; h->E = E; h->nnz = nnz; h->gpn = gpn; h->Q = Q; h->max_ranges = max_ranges > 0 ? max_ranges : 1;
-    h->h_grp_off = off; h->h_grp_gpu = gpu;
+    h->G = G;
+    h->E = E;
+    h->nnz = nnz;
+    h->gpn = gpn;
+    h->Q = Q;
+    h->max_ranges = max_ranges > 0 ? max_ranges : 1;
+    h->h_grp_off = off;
+    h->h_grp_gpu = gpu;
     if (slots) h->h_slots.assign(slots, slots + E); else h->h_slots.assign(E, 0);
+    // per-destination hosted lists (expert ascending), for rank-local receive layouts
+    std::vector<int32_t> hosted_off(G + 1, 0), seg_nnz(nnz);
+    for (int i = 0; i < nnz; ++i) hosted_off[gpu[i] + 1]++;
+    for (int g = 0; g < G; ++g) hosted_off[g + 1] += hosted_off[g];
+    std::vector<int32_t> fill(G, 0);
+    for (int e = 0; e < E; ++e)
+        for (int i = off[e]; i < off[e + 1]; ++i) seg_nnz[hosted_off[gpu[i]] + fill[gpu[i]]++] = i;
+    h->h_hosted_off = hosted_off;
     auto up = [&](void **dst, const void *src, size_t bytes) -> cudaError_t {
         cudaError_t e = cudaMalloc(dst, bytes > 0 ? bytes : 4);
         if (e != cudaSuccess) return e;
@@ -587,20 +645,9 @@ extern "C" int hep_sched_create(int num_gpus, int num_experts, const int32_t *gr
     if (ce == cudaSuccess) ce = up((void **)&h->d_sorted, sorted.data(), sizeof(int32_t) * nnz);
     if (ce == cudaSuccess) ce = up((void **)&h->d_mask, mask.data(), sizeof(uint32_t) * E);
     if (ce == cudaSuccess) ce = up((void **)&h->d_slots, h->h_slots.data(), sizeof(int32_t) * E);
-    // receive-row layout tables: segments ordered [dst GPU][expert ascending]
-    {
-        std::vector<int32_t> hosted_off(G + 1, 0), seg_nnz(nnz), nnz_exp(nnz);
-        for (int e = 0; e < E; ++e)
-            for (int i = off[e]; i < off[e + 1]; ++i) { hosted_off[gpu[i] + 1]++; nnz_exp[i] = e; }
-        for (int g = 0; g < G; ++g) hosted_off[g + 1] += hosted_off[g];
-        std::vector<int32_t> fill(G, 0);
-        for (int e = 0; e < E; ++e)
-            for (int i = off[e]; i < off[e + 1]; ++i) seg_nnz[hosted_off[gpu[i]] + fill[gpu[i]]++] = i;
-        h->h_hosted_off = hosted_off;
-        if (ce == cudaSuccess) ce = up((void **)&h->d_hosted_off, hosted_off.data(), sizeof(int32_t) * (G + 1));
-        if (ce == cudaSuccess) ce = up((void **)&h->d_seg_nnz, seg_nnz.data(), sizeof(int32_t) * nnz);
-        if (ce == cudaSuccess) ce = up((void **)&h->d_nnz_exp, nnz_exp.data(), sizeof(int32_t) * nnz);
-    }
+    if (ce == cudaSuccess) ce = up((void **)&h->d_hosted_off, hosted_off.data(), sizeof(int32_t) * (G + 1));
+    if (ce == cudaSuccess) ce = up((void **)&h->d_seg_nnz, seg_nnz.data(), sizeof(int32_t) * nnz);
+    if (ce == cudaSuccess) ce = up((void **)&h->d_nnz_exp, nnz_exp.data(), sizeof(int32_t) * nnz);
     if (ce != cudaSuccess) {
         set_error("hep_sched_create: %s", cudaGetErrorString(ce));
         hep_sched_destroy(h);
@@ -639,8 +686,12 @@ extern "C" int hep_sched_solve(hep_sched_t h, const int64_t *d_loads, int64_t st
     HEP_REQUIRE(out->d_status, HEP_E_CONTRACT, "hep_sched_solve: d_status required");
     SchedArgs a{};
     a.flags = flags | HEP_SCHED_SOLVE;
-    a.loads = d_loads; a.se = stride_e; a.sg = stride_g; a.base = d_base;
-    a.xi_in = nullptr; a.den = h->Q;
+    a.loads = d_loads;
+    a.se = stride_e;
+    a.sg = stride_g;
+    a.base = d_base;
+    a.xi_in = nullptr;
+    a.den = h->Q;
     a.out = *out;
     return launch_sched(h, a, (cudaStream_t)stream);
 }
@@ -652,7 +703,9 @@ extern "C" int hep_sched_integerize(hep_sched_t h, const int64_t *d_xnum, int64_
     HEP_REQUIRE(den > 0, HEP_E_CONTRACT, "denominator must be positive");
     SchedArgs a{};
     a.flags = HEP_SCHED_INTEGERIZE;
-    a.den = den; a.loads = nullptr; a.out = *out;
+    a.den = den;
+    a.loads = nullptr;
+    a.out = *out;
     return launch_sched(h, a, (cudaStream_t)stream);
 }
 
@@ -660,8 +713,12 @@ extern "C" int hep_sched_route(hep_sched_t h, const int64_t *d_loads, int64_t st
                                const int64_t *d_xi, int flags, const hep_sched_out *out, void *stream) {
     HEP_REQUIRE(h && out && d_loads && d_xi, HEP_E_CONTRACT, "hep_sched_route: null argument");
     SchedArgs a{};
-    a.flags = HEP_SCHED_ROUTE | (flags & (HEP_SCHED_TRANSFER | HEP_SCHED_TOPO));
-    a.loads = d_loads; a.se = stride_e; a.sg = stride_g; a.xi_in = d_xi; a.den = 1;
+    a.flags = HEP_SCHED_ROUTE | (flags & (HEP_SCHED_TRANSFER | HEP_SCHED_TOPO | HEP_SCHED_PROFILE));
+    a.loads = d_loads;
+    a.se = stride_e;
+    a.sg = stride_g;
+    a.xi_in = d_xi;
+    a.den = 1;
     a.out = *out;
     return launch_sched(h, a, (cudaStream_t)stream);
 }
@@ -673,5 +730,13 @@ extern "C" int hep_transfer_plan(int num_gpus, int gpus_per_node, const int64_t 
     transfer_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(num_gpus, gpus_per_node, d_ranges, n_ranges, d_transfer,
                                                          d_status);
     HEP_CHECK_LAUNCH();
+    return HEP_OK;
+}
+
+extern "C" int hep_sched_debug_timing(int64_t *host_out, int n) {
+    HEP_REQUIRE(host_out && n > 0, HEP_E_CONTRACT, "null output");
+    long long tmp[kProfSlots];
+    HEP_CHECK_CUDA(cudaMemcpyFromSymbol(tmp, g_sched_prof, sizeof(tmp)));
+    for (int i = 0; i < n && i < kProfSlots; ++i) host_out[i] = tmp[i];
     return HEP_OK;
 }

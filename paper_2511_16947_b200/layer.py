@@ -14,7 +14,7 @@ Per micro-batch, all on one CUDA stream, no host synchronisation:
 *simulated on one device* (the reference's own "simulated EP" setting,
 BASELINE configs[0]): tokens [g*T/G, (g+1)*T/G) originate on virtual GPU g,
 the scheduler balances the G virtual GPUs exactly as on G real ones, the
-dispatch "all-to-all" is the K5 scatter into the [dst][expert][src] receive
+dispatch "all-to-all" is the K5 scatter into the [expert][dst][src] receive
 layout, and every virtual GPU's replicas run in one grouped GEMM (one
 physical weight copy per expert; replicas of an expert are identical by
 construction).  The schedule — routing decisions, per-GPU
@@ -79,7 +79,7 @@ class MoEBuffers:
         self.tok_row = torch.empty(T, K, **i32)
         self.row_tok = torch.empty(max(R, 1), **i32)
         self.seg = torch.empty(max(sched.nnz, 1), 4, **i32)
-        self.dst_rows = torch.empty(G + 1, dtype=torch.int64, device=device)
+        self.expert_rows = torch.empty(E + 1, dtype=torch.int64, device=device)
         ws = L.hep_moe_assign_workspace(sched.handle, T, K)
         self.assign_ws = torch.empty(max(int(ws), 256), dtype=torch.uint8, device=device)
         self.rows = torch.empty(max(R, 1), d_model, **bf)
@@ -173,7 +173,7 @@ class MoELayer(torch.nn.Module):
         mark("sched", 1)
         mark("assign", 0)
         ck(L.hep_moe_assign(self.sched.handle, ctypes.byref(self.sched.out), b.topk_idx.data_ptr(), T, K, tps,
-                            b.tok_row.data_ptr(), b.row_tok.data_ptr(), b.seg.data_ptr(), b.dst_rows.data_ptr(),
+                            b.tok_row.data_ptr(), b.row_tok.data_ptr(), b.seg.data_ptr(), b.expert_rows.data_ptr(),
                             b.assign_ws.data_ptr(), b.assign_ws.numel(), s), "hep_moe_assign")
         mark("assign", 1)
         mark("permute", 0)

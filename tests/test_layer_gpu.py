@@ -66,7 +66,7 @@ def test_tiny_config_bit_exact_schedule_and_output(P):
     assert sd.gpu_load.cpu().tolist() == ref["sched"]["gpu_load"]
     # token -> row schedule: bit-exact
     assert np.array_equal(b.tok_row.cpu().numpy(), ref["tok_row"])
-    assert b.dst_rows.cpu().tolist() == ref["dst_rows"].tolist()
+    assert b.expert_rows.cpu().tolist() == ref["expert_rows"].tolist()
     # permuted rows are exact copies
     R = x.shape[0] * layer.K
     assert torch.equal(b.rows[:R], x[b.row_tok[:R].long()])
