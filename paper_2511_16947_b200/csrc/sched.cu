@@ -59,6 +59,7 @@ struct SchedArgs {
 struct SchedSmem {
     int64_t *totals;    // [E]
     int64_t *W;         // [2^G]
+    int64_t *C;         // [2^G] capacity of each GPU subset at the optimum
     int64_t *loads;     // [E*G]
     int64_t *xq;        // [nnz]
     int64_t *xi;        // [nnz]
@@ -77,7 +78,7 @@ __host__ __device__ inline size_t align8(size_t x) { return (x + 7) & ~size_t(7)
 
 __host__ __device__ inline size_t sched_smem_bytes(int G, int E, int nnz) {
     const size_t ns = size_t(1) << G;
-    return align8(8 * (size_t)E) + align8(8 * ns) + align8(8 * (size_t)E * G) + 2 * align8(8 * (size_t)nnz) +
+    return align8(8 * (size_t)E) + 2 * align8(8 * ns) + align8(8 * (size_t)E * G) + 2 * align8(8 * (size_t)nnz) +
            align8(8 * (size_t)G) + align8(8 * (size_t)G * G) + align8(8 * (kSchedThreads / 32 + 2)) + 64 +
            align8(4 * (size_t)(E + 1)) + 3 * align8(4 * (size_t)nnz) + align8(4 * (size_t)E);
 }
@@ -87,6 +88,7 @@ __device__ inline SchedSmem carve(char *p, int G, int E, int nnz) {
     const size_t ns = size_t(1) << G;
     s.totals = (int64_t *)p; p += align8(8 * (size_t)E);
     s.W = (int64_t *)p; p += align8(8 * ns);
+    s.C = (int64_t *)p; p += align8(8 * ns);
     s.loads = (int64_t *)p; p += align8(8 * (size_t)E * G);
     s.xq = (int64_t *)p; p += align8(8 * (size_t)nnz);
     s.xi = (int64_t *)p; p += align8(8 * (size_t)nnz);
@@ -102,10 +104,9 @@ __device__ inline SchedSmem carve(char *p, int G, int E, int nnz) {
     return s;
 }
 
-// a/b > c/d, denominators <= 64, |numerators| < 2^56
-__device__ __forceinline__ bool frac_gt(int64_t a, int64_t b, int64_t c, int64_t d) {
-    return (__int128)a * d > (__int128)c * b;
-}
+// a/b > c/d with denominators |S| <= HEP_MAX_GPUS and numerators < 2^56
+// (capacity-checked), so the cross products fit int64
+__device__ __forceinline__ bool frac_gt(int64_t a, int64_t b, int64_t c, int64_t d) { return a * d > c * b; }
 
 __device__ __forceinline__ int64_t gcd_i64(int64_t a, int64_t b) {
     if (a < 0) a = -a;
@@ -121,65 +122,81 @@ __device__ __forceinline__ void prof_mark(int flags, int slot) {
     if ((flags & HEP_SCHED_PROFILE) && threadIdx.x == 0 && slot < kProfSlots) g_sched_prof[slot] = clock64();
 }
 
-// warp max of non-negative values
-__device__ __forceinline__ int64_t wmax(int64_t v) { return warp_max_i64(v); }
-__device__ __forceinline__ int32_t wmax(int32_t v) {
-    return (int32_t)__reduce_max_sync(0xffffffffu, (unsigned)v);
+// warp min of non-negative values
+__device__ __forceinline__ uint32_t wmin(uint32_t v) { return __reduce_min_sync(0xffffffffu, v); }
+__device__ __forceinline__ uint64_t wmin(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = w < v ? w : v;
+    }
+    return v;
+}
+
+// floor(v / d) for d > 0 without the 64-bit division routine: a double
+// estimate corrected to the exact quotient (|v| < 2^62 capacity-checked)
+__device__ __forceinline__ int64_t floordiv(int64_t v, int64_t d) {
+    int64_t q = (int64_t)floor((double)v / (double)d);
+    int64_t r = v - q * d;
+    while (r < 0) { --q; r += d; }
+    while (r >= d) { ++q; r -= d; }
+    return q;
 }
 
 // ---------------------------------------------------------------------------
-// step 4: lex-min canonical plan, warp 0; V = int32_t when every quantity fits
+// step 4: lex-min canonical plan, warp 0.  Each lane keeps the slack
+// C[S] - Wf[S] >= 0 of its SPL subsets; the minimum feasible load of arc
+// (e, g) is v = max(0, r - min{slack[S] : S ⊇ need, g ∉ S}).  U = uint32_t
+// when every slack and load fits 32 bits (one redux.sync per arc).
 // ---------------------------------------------------------------------------
-template <int SPL, typename V>
-__device__ void lexmin_warp(const SchedArgs &a, SchedSmem &s, int64_t mQ) {
+template <int SPL, typename U>
+__device__ void lexmin_warp(const SchedArgs &a, SchedSmem &s) {
     const int lane = threadIdx.x & 31;
-    const int G = a.G, E = a.E;
-    const uint32_t NS = 1u << G;
+    const int E = a.E;
+    const uint32_t NS = 1u << a.G;
     const int64_t Q = a.Q;
-    V Wf[SPL], C[SPL];
+    U sl[SPL];
+    uint32_t valid = 0;
 #pragma unroll
     for (int j = 0; j < SPL; ++j) {
         const uint32_t S = lane + 32 * j;
-        int64_t c = 0;
-        for (int g = 0; g < G; ++g) {
-            if (!((S >> g) & 1)) continue;
-            const int64_t cg = mQ - (a.base ? a.base[g] * Q : 0);
-            c += cg > 0 ? cg : 0;
-        }
-        C[j] = (V)c;
-        Wf[j] = S < NS ? (V)(s.W[S] * Q) : (V)0;
+        sl[j] = S < NS ? (U)(s.C[S] - s.W[S] * Q) : (U)0;
+        valid |= (S < NS) << j;
     }
+    int b_next = s.grp_off[0];
     for (int e = 0; e < E; ++e) {
-        const int b = s.grp_off[e], n = s.grp_off[e + 1] - b;
+        const int b = b_next;
+        b_next = s.grp_off[e + 1];
+        const int n = b_next - b;
         if (n == 0) continue;
-        V r = (V)(s.totals[e] * Q);
+        U r = (U)(s.totals[e] * Q);
         uint32_t R = s.mask[e];
-        if (r > 0) {
+        if (r) {
 #pragma unroll
             for (int j = 0; j < SPL; ++j) {
                 const uint32_t S = lane + 32 * j;
-                if ((S & R) == R) Wf[j] -= r;
+                if ((S & R) == R) sl[j] += r;  // expert e leaves the not-yet-processed set
             }
         }
         for (int k = 0; k < n; ++k) {
             const int g = s.arc_gpu[b + k];
             const uint32_t gbit = 1u << g;
             const uint32_t need = R & ~gbit;
-            V v;
+            U v;
             if (r == 0) {
-                v = 0;  // Wf <= C on every subset (feasible state): the bound is <= 0
+                v = 0;  // every bound r - slack is <= 0
             } else if (need == 0) {
-                v = r;  // S = {} attains r and every other bound is <= r
+                v = r;  // S = {} has slack 0; every other bound is <= r
             } else {
-                V best = 0;
+                U mn = ~(U)0;
 #pragma unroll
                 for (int j = 0; j < SPL; ++j) {
                     const uint32_t S = lane + 32 * j;
-                    const bool ok = (S < NS) && ((S & need) == need) && !(S & gbit);
-                    const V cand = r + Wf[j] - C[j];
-                    if (ok && cand > best) best = cand;
+                    const bool ok = ((valid >> j) & 1) && ((S & need) == need) && !(S & gbit);
+                    if (ok && sl[j] < mn) mn = sl[j];
                 }
-                v = wmax(best);
+                mn = wmin(mn);
+                v = r > mn ? r - mn : (U)0;
             }
             if (lane == 0) s.xq[s.arc_idx[b + k]] = (int64_t)v;
             r -= v;
@@ -188,11 +205,141 @@ __device__ void lexmin_warp(const SchedArgs &a, SchedSmem &s, int64_t mQ) {
 #pragma unroll
                 for (int j = 0; j < SPL; ++j) {
                     const uint32_t S = lane + 32 * j;
-                    if (S & gbit) C[j] -= v;
+                    if (S & gbit) sl[j] -= v;  // capacity of every subset holding g drops by v
                 }
             }
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// step 6: Algorithm 1 for one expert on one warp (lane = source GPU).
+// Phase 1 keeps min(input, quota) on every hosting GPU; the final sweep
+// ("src ascending x EDP list order", router.py:149-157) exhausts either the
+// current source or the current replica at every step, so it is exactly the
+// merge of the remaining source amounts (in src order) with the remaining
+// quotas (in list order): range (src, dst_k) carries the overlap of
+// [A_src, A_src + in_src) and [B_k, B_k + quota_k), A/B exclusive prefix sums.
+// EMIT=false counts, EMIT=true writes at `pos` and accumulates the pair matrix.
+// ---------------------------------------------------------------------------
+template <bool EMIT>
+__device__ int route_expert_warp(const SchedArgs &a, SchedSmem &s, int e, int64_t pos, int32_t *status) {
+    const int lane = threadIdx.x & 31;
+    const int G = a.G;
+    const int b = s.grp_off[e], n = s.grp_off[e + 1] - b;
+    const int64_t rin = lane < G ? s.loads[e * G + lane] : 0;
+    const int dst_k = lane < n ? s.grp_gpu[b + lane] : -1;
+    const int64_t x_k = lane < n ? s.xi[b + lane] : 0;
+    const int64_t tot = warp_sum_i64(rin);
+    if (n == 0 && tot == 0) return 0;  // router.py:125-126
+    const bool neg = __any_sync(0xffffffffu, x_k < 0);
+    if (neg || warp_sum_i64(x_k) != tot) {  // _check_plan (router.py:97-111)
+        if (lane == 0) set_status(status, HEP_E_CONTRACT);
+        return 0;
+    }
+    // quota of this lane's GPU (if it hosts a replica of e)
+    int64_t rxg = 0;
+    bool hosts = false;
+#pragma unroll 1
+    for (int k = 0; k < n; ++k) {
+        const int d = __shfl_sync(0xffffffffu, dst_k, k);
+        const int64_t xv = __shfl_sync(0xffffffffu, x_k, k);
+        if (d == lane) { rxg = xv; hosts = true; }
+    }
+    const int64_t y1 = hosts ? (rin < rxg ? rin : rxg) : 0;
+    const unsigned b1 = __ballot_sync(0xffffffffu, y1 > 0);
+    const int n1 = __popc(b1);
+    const int64_t in2 = rin - y1;
+    const int64_t rx2g = rxg - y1;
+    const int64_t q_k = __shfl_sync(0xffffffffu, rx2g, dst_k < 0 ? 0 : dst_k);
+    const int64_t qk = lane < n ? q_k : 0;
+    const int64_t B_k = warp_incl_scan_i64(qk) - qk;
+    const int64_t A = warp_incl_scan_i64(lane < G ? in2 : 0) - (lane < G ? in2 : 0);
+    int cnt2 = 0;
+#pragma unroll 1
+    for (int k = 0; k < n; ++k) {
+        const int64_t Bk = __shfl_sync(0xffffffffu, B_k, k);
+        const int64_t Lk = __shfl_sync(0xffffffffu, qk, k);
+        const int64_t lo = A > Bk ? A : Bk;
+        const int64_t hi = (A + in2) < (Bk + Lk) ? (A + in2) : (Bk + Lk);
+        cnt2 += (lane < G && hi > lo);
+    }
+    const int total = n1 + (int)warp_sum_i64(cnt2);
+    if (EMIT) {
+        if (y1 > 0) {
+            const int64_t p = pos + __popc(b1 & ((1u << lane) - 1));
+            int64_t *r_ = a.out.d_ranges + 4 * p;
+            r_[0] = e; r_[1] = lane; r_[2] = lane; r_[3] = y1;
+            atomicAdd(&s.pair[lane * G + lane], (unsigned long long)y1);
+        }
+        int64_t p = pos + n1 + (warp_incl_scan_i64(cnt2) - cnt2);
+    #pragma unroll 1
+    for (int k = 0; k < n; ++k) {
+            const int64_t Bk = __shfl_sync(0xffffffffu, B_k, k);
+            const int64_t Lk = __shfl_sync(0xffffffffu, qk, k);
+            const int d = __shfl_sync(0xffffffffu, dst_k, k);
+            const int64_t lo = A > Bk ? A : Bk;
+            const int64_t hi = (A + in2) < (Bk + Lk) ? (A + in2) : (Bk + Lk);
+            if (lane < G && hi > lo) {
+                int64_t *r_ = a.out.d_ranges + 4 * p;
+                r_[0] = e; r_[1] = lane; r_[2] = d; r_[3] = hi - lo;
+                atomicAdd(&s.pair[lane * G + d], (unsigned long long)(hi - lo));
+                ++p;
+            }
+        }
+    }
+    return total;
+}
+
+// Topology-aware variant (router.py:136-147): sequential per expert, one thread.
+template <bool EMIT>
+__device__ int route_expert_topo(const SchedArgs &a, SchedSmem &s, int e, int64_t pos, int32_t *status) {
+    const int G = a.G;
+    const int b = s.grp_off[e], n = s.grp_off[e + 1] - b;
+    int64_t rin[HEP_MAX_GPUS], rx[HEP_MAX_GPUS];
+    int64_t tot = 0, xs = 0;
+    for (int g = 0; g < G; ++g) { rin[g] = s.loads[e * G + g]; rx[g] = 0; tot += rin[g]; }
+    if (n == 0 && tot == 0) return 0;
+    bool neg = false;
+    for (int k = 0; k < n; ++k) {
+        const int64_t v = s.xi[b + k];
+        neg |= v < 0;
+        xs += v;
+        rx[s.grp_gpu[b + k]] = v;
+    }
+    if (neg || xs != tot) { set_status(status, HEP_E_CONTRACT); return 0; }
+    int cnt = 0;
+    auto emit = [&](int src, int dst, int64_t y) {
+        if (EMIT) {
+            int64_t *r_ = a.out.d_ranges + 4 * (pos + cnt);
+            r_[0] = e; r_[1] = src; r_[2] = dst; r_[3] = y;
+            atomicAdd(&s.pair[src * G + dst], (unsigned long long)y);
+        }
+        ++cnt;
+    };
+    for (int k = 0; k < n; ++k) {  // phase 1, sorted(group)
+        const int g = s.arc_gpu[b + k];
+        const int64_t y = rin[g] < rx[g] ? rin[g] : rx[g];
+        if (y > 0) { emit(g, g, y); rin[g] -= y; rx[g] -= y; }
+    }
+    for (int src = 0; src < G; ++src) {  // phase 2: same node
+        if (rin[src] == 0) continue;
+        for (int k = 0; k < n; ++k) {
+            const int dst = s.grp_gpu[b + k];
+            if (dst == src || dst / a.gpn != src / a.gpn) continue;
+            const int64_t y = rin[src] < rx[dst] ? rin[src] : rx[dst];
+            if (y > 0) { emit(src, dst, y); rin[src] -= y; rx[dst] -= y; }
+        }
+    }
+    for (int src = 0; src < G; ++src) {  // final phase
+        if (rin[src] == 0) continue;
+        for (int k = 0; k < n; ++k) {
+            const int dst = s.grp_gpu[b + k];
+            const int64_t y = rin[src] < rx[dst] ? rin[src] : rx[dst];
+            if (y > 0) { emit(src, dst, y); rin[src] -= y; rx[dst] -= y; }
+        }
+    }
+    return cnt;
 }
 
 template <int SPL>
@@ -300,14 +447,29 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
             a.out.d_m[2] = a.Q;
         }
         __syncthreads();
+        // capacity of every GPU subset: C[S] = sum_{g in S} max(mQ - base_g*Q, 0)
+        {
+            const int64_t mQ = s.misc[0];
+            for (int S = tid; S < NS; S += nt) {
+                int64_t c = 0;
+#pragma unroll 1
+                for (int g = 0; g < G; ++g) {
+                    if (!((S >> g) & 1)) continue;
+                    const int64_t cg = mQ - (a.base ? a.base[g] * a.Q : 0);
+                    c += cg > 0 ? cg : 0;
+                }
+                s.C[S] = c;
+            }
+        }
+        __syncthreads();
         prof_mark(a.flags, 2);
         // ---- step 4: lex-min canonical plan ------------------------------------
         if (tid < 32) {
             const int64_t mQ = s.misc[0];
             const bool fits32 = (__int128)G * (total_all + 1) * a.Q < ((__int128)1 << 31) &&
                                 (__int128)G * (mQ + 1) < ((__int128)1 << 31);
-            if (fits32) lexmin_warp<SPL, int32_t>(a, s, mQ);
-            else lexmin_warp<SPL, int64_t>(a, s, mQ);
+            if (fits32) lexmin_warp<SPL, uint32_t>(a, s);
+            else lexmin_warp<SPL, uint64_t>(a, s);
         }
         __syncthreads();
         for (int i = tid; i < nnz; i += nt) a.out.d_xq[i] = s.xq[i];
@@ -322,14 +484,14 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
             int64_t total = 0, sum_floor = 0;
             for (int k = 0; k < n; ++k) {
                 const int64_t v = s.xq[b + k];
-                const int64_t fl = v >= 0 ? v / den : -((-v + den - 1) / den);
+                const int64_t fl = floordiv(v, den);
                 s.xi[b + k] = fl;
                 sum_floor += fl;
                 total += v;
             }
             // round(total) must be an integer within 1e-6 (scheduler.py:706-713);
             // Python rounds half to even
-            const int64_t t_fl = total >= 0 ? total / den : -((-total + den - 1) / den);
+            const int64_t t_fl = floordiv(total, den);
             const int64_t t_rem = total - t_fl * den;
             int64_t rounded = t_fl;
             if (t_rem > den - t_rem || (t_rem == den - t_rem && (t_fl & 1))) rounded = t_fl + 1;
@@ -374,80 +536,39 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
     // ---- step 6: Algorithm 1 routing (router.py:114-158) --------------------------
     if (route) {
         const bool topo = (a.flags & HEP_SCHED_TOPO) && a.gpn > 0 && a.gpn < G;
-        const int chunk = (E + nt - 1) / nt;  // contiguous experts per thread: table in expert order
+        // pass 0: ranges per expert (warp per expert; one thread per expert for topology routing)
+        const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+        int64_t *ecount = s.totals;  // totals are no longer needed once the plan exists
+        if (!topo) {
+            for (int e = warp; e < E; e += nw) {
+                const int c = route_expert_warp<false>(a, s, e, 0, status);
+                if (lane == 0) ecount[e] = c;
+            }
+        } else {
+            for (int e = tid; e < E; e += nt) ecount[e] = route_expert_topo<false>(a, s, e, 0, status);
+        }
+        __syncthreads();
+        // exclusive scan over experts (contiguous chunk per thread) -> table positions
+        const int chunk = (E + nt - 1) / nt;
         const int e0 = min(E, tid * chunk), e1 = min(E, e0 + chunk);
-        int64_t rin[HEP_MAX_GPUS], rx[HEP_MAX_GPUS];
-        int64_t my_count = 0;
-        for (int pass = 0; pass < 2; ++pass) {
-            int64_t pos = 0;
-            if (pass == 1) {
-                int64_t tot;
-                pos = block_excl_scan_i64(my_count, s.scan, &tot);
-                if (tid == 0) *a.out.d_n_ranges = tot;
-                if (tot > a.max_ranges) { set_status(status, HEP_E_CAPACITY); break; }
+        int64_t mine = 0;
+        for (int e = e0; e < e1; ++e) mine += ecount[e];
+        int64_t total_ranges;
+        int64_t pos = block_excl_scan_i64(mine, s.scan, &total_ranges);
+        for (int e = e0; e < e1; ++e) {
+            const int64_t c = ecount[e];
+            ecount[e] = pos;
+            pos += c;
+        }
+        if (tid == 0) *a.out.d_n_ranges = total_ranges;
+        if (total_ranges > a.max_ranges) set_status(status, HEP_E_CAPACITY);
+        __syncthreads();
+        if (*status == 0) {
+            if (!topo) {
+                for (int e = warp; e < E; e += nw) route_expert_warp<true>(a, s, e, ecount[e], status);
+            } else {
+                for (int e = tid; e < E; e += nt) route_expert_topo<true>(a, s, e, ecount[e], status);
             }
-            for (int e = e0; e < e1; ++e) {
-                const int b = s.grp_off[e], n = s.grp_off[e + 1] - b;
-                int64_t tot = 0, xs = 0;
-                for (int g = 0; g < G; ++g) {
-                    rin[g] = s.loads[e * G + g];
-                    rx[g] = 0;
-                    tot += rin[g];
-                }
-                if (n == 0 && tot == 0) continue;  // :125-126
-                bool neg = false;
-                for (int k = 0; k < n; ++k) {
-                    const int64_t v = s.xi[b + k];
-                    neg |= v < 0;
-                    xs += v;
-                    rx[s.grp_gpu[b + k]] = v;
-                }
-                if (neg || xs != tot) { set_status(status, HEP_E_CONTRACT); continue; }  // _check_plan :97-111
-#define HEP_EMIT(S_, D_, Y_)                                                            \
-    do {                                                                                \
-        if (pass == 0) {                                                                \
-            ++my_count;                                                                 \
-        } else {                                                                        \
-            int64_t *r_ = a.out.d_ranges + 4 * pos;                                     \
-            r_[0] = e;                                                                  \
-            r_[1] = (S_);                                                               \
-            r_[2] = (D_);                                                               \
-            r_[3] = (Y_);                                                               \
-            atomicAdd(&s.pair[(S_) * G + (D_)], (unsigned long long)(Y_));              \
-            ++pos;                                                                      \
-        }                                                                               \
-    } while (0)
-                // phase 1: keep tokens on their source GPU, g in sorted(group)
-                for (int k = 0; k < n; ++k) {
-                    const int g = s.arc_gpu[b + k];
-                    const int64_t y = rin[g] < rx[g] ? rin[g] : rx[g];
-                    if (y > 0) { HEP_EMIT(g, g, y); rin[g] -= y; rx[g] -= y; }
-                }
-                // phase 2 (topology-aware only): same node
-                if (topo) {
-                    for (int src = 0; src < G; ++src) {
-                        if (rin[src] == 0) continue;
-                        for (int k = 0; k < n; ++k) {
-                            const int dst = s.grp_gpu[b + k];
-                            if (dst == src || dst / a.gpn != src / a.gpn) continue;
-                            const int64_t y = rin[src] < rx[dst] ? rin[src] : rx[dst];
-                            if (y > 0) { HEP_EMIT(src, dst, y); rin[src] -= y; rx[dst] -= y; }
-                        }
-                    }
-                }
-                // final phase: src ascending x EDP list order
-                for (int src = 0; src < G; ++src) {
-                    if (rin[src] == 0) continue;
-                    for (int k = 0; k < n; ++k) {
-                        const int dst = s.grp_gpu[b + k];
-                        const int64_t y = rin[src] < rx[dst] ? rin[src] : rx[dst];
-                        if (y > 0) { HEP_EMIT(src, dst, y); rin[src] -= y; rx[dst] -= y; }
-                    }
-                }
-#undef HEP_EMIT
-            }
-            __syncthreads();
-            if (*status) break;
         }
         __syncthreads();
         prof_mark(a.flags, 5);
@@ -459,32 +580,30 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
         int64_t *T = a.out.d_transfer;
         const int gpn = a.gpn > 0 ? a.gpn : G;
         for (int i = tid; i < G * G; i += nt) T[i] = (int64_t)s.pair[i];
-        for (int g = tid; g < G; g += nt) {
+        if (tid < 32) {
             int64_t send = 0, recv = 0, si = 0, ri = 0, sx = 0, rxv = 0;
-            for (int o = 0; o < G; ++o) {
-                if (o == g) continue;
-                const int64_t oc = s.pair[g * G + o], ic = s.pair[o * G + g];
-                send += oc;
-                recv += ic;
-                if (o / gpn == g / gpn) { si += oc; ri += ic; } else { sx += oc; rxv += ic; }
-            }
-            T[G * G + 0 * G + g] = send;
-            T[G * G + 1 * G + g] = recv;
-            T[G * G + 2 * G + g] = (int64_t)s.pair[g * G + g];
-            T[G * G + 3 * G + g] = si;
-            T[G * G + 4 * G + g] = ri;
-            T[G * G + 5 * G + g] = sx;
-            T[G * G + 6 * G + g] = rxv;
-        }
-        if (tid == 0) {
-            int64_t intra = 0, inter = 0;
-            for (int x = 0; x < G; ++x)
-                for (int y = 0; y < G; ++y) {
-                    if (x == y) continue;
-                    if (x / gpn == y / gpn) intra += s.pair[x * G + y]; else inter += s.pair[x * G + y];
+            const int g = tid;
+            if (g < G) {
+                for (int o = 0; o < G; ++o) {
+                    if (o == g) continue;
+                    const int64_t oc = s.pair[g * G + o], ic = s.pair[o * G + g];
+                    send += oc;
+                    recv += ic;
+                    if (o / gpn == g / gpn) { si += oc; ri += ic; } else { sx += oc; rxv += ic; }
                 }
-            T[G * G + 7 * G] = intra;
-            T[G * G + 7 * G + 1] = inter;
+                T[G * G + 0 * G + g] = send;
+                T[G * G + 1 * G + g] = recv;
+                T[G * G + 2 * G + g] = (int64_t)s.pair[g * G + g];
+                T[G * G + 3 * G + g] = si;
+                T[G * G + 4 * G + g] = ri;
+                T[G * G + 5 * G + g] = sx;
+                T[G * G + 6 * G + g] = rxv;
+            }
+            const int64_t intra = warp_sum_i64(si), inter = warp_sum_i64(sx);
+            if (tid == 0) {
+                T[G * G + 7 * G] = intra;
+                T[G * G + 7 * G + 1] = inter;
+            }
         }
     }
     prof_mark(a.flags, 6);
@@ -535,9 +654,12 @@ __global__ void transfer_kernel(int G, int gpn, const int64_t *ranges, int64_t n
 
 template <int SPL>
 static int launch_spl(hep_sched *h, const SchedArgs &a, size_t smem, cudaStream_t stream) {
-    if (h->smem_set < smem) {
+    // the opt-in is a property of the kernel (shared by every handle): only ever raise it
+    static size_t granted = 0;
+    (void)h;
+    if (granted < smem) {
         HEP_CHECK_CUDA(cudaFuncSetAttribute(sched_kernel<SPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        h->smem_set = smem;
+        granted = smem;
     }
     sched_kernel<SPL><<<1, kSchedThreads, smem, stream>>>(a);
     HEP_CHECK_LAUNCH();
