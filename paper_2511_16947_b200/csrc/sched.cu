@@ -49,6 +49,7 @@ struct SchedArgs {
     int64_t Q, max_ranges, den;  // den: denominator of the input plan (Q when solved here)
     const int32_t *grp_off, *grp_gpu, *sorted;
     const uint32_t *mask;
+    const int8_t *kidx;
     const int64_t *loads;
     int64_t se, sg;
     const int64_t *base;
@@ -72,6 +73,9 @@ struct SchedSmem {
     int32_t *arc_idx;   // [nnz] arcs in (e, gpu id) order: nnz index
     int32_t *arc_gpu;   // [nnz] arcs in (e, gpu id) order: gpu
     uint32_t *mask;     // [E]
+    int4 *emeta;        // [E] (arc base, #arcs, group mask, load*Q when it fits 32 bits)
+    int8_t *kidx;       // [E*G] list position of GPU g in expert e's group, -1 if absent
+    int32_t *rc;        // [2*E*G] per-(expert, source) range counts: phase 1, final merge
 };
 
 __host__ __device__ inline size_t align8(size_t x) { return (x + 7) & ~size_t(7); }
@@ -80,12 +84,14 @@ __host__ __device__ inline size_t sched_smem_bytes(int G, int E, int nnz) {
     const size_t ns = size_t(1) << G;
     return align8(8 * (size_t)E) + 2 * align8(8 * ns) + align8(8 * (size_t)E * G) + 2 * align8(8 * (size_t)nnz) +
            align8(8 * (size_t)G) + align8(8 * (size_t)G * G) + align8(8 * (kSchedThreads / 32 + 2)) + 64 +
-           align8(4 * (size_t)(E + 1)) + 3 * align8(4 * (size_t)nnz) + align8(4 * (size_t)E);
+           align8(4 * (size_t)(E + 1)) + 3 * align8(4 * (size_t)nnz) + align8(4 * (size_t)E) + 16 * (size_t)E +
+           align8((size_t)E * G) + 8 * (size_t)E * G;
 }
 
 __device__ inline SchedSmem carve(char *p, int G, int E, int nnz) {
     SchedSmem s;
     const size_t ns = size_t(1) << G;
+    s.emeta = (int4 *)p; p += 16 * (size_t)E;  // first: 16-byte aligned
     s.totals = (int64_t *)p; p += align8(8 * (size_t)E);
     s.W = (int64_t *)p; p += align8(8 * ns);
     s.C = (int64_t *)p; p += align8(8 * ns);
@@ -100,7 +106,9 @@ __device__ inline SchedSmem carve(char *p, int G, int E, int nnz) {
     s.grp_gpu = (int32_t *)p; p += align8(4 * (size_t)nnz);
     s.arc_idx = (int32_t *)p; p += align8(4 * (size_t)nnz);
     s.arc_gpu = (int32_t *)p; p += align8(4 * (size_t)nnz);
-    s.mask = (uint32_t *)p;
+    s.mask = (uint32_t *)p; p += align8(4 * (size_t)E);
+    s.kidx = (int8_t *)p; p += align8((size_t)E * G);
+    s.rc = (int32_t *)p;
     return s;
 }
 
@@ -146,11 +154,13 @@ __device__ __forceinline__ int64_t floordiv(int64_t v, int64_t d) {
 // ---------------------------------------------------------------------------
 // step 4: lex-min canonical plan, warp 0.  Each lane keeps the slack
 // C[S] - Wf[S] >= 0 of its SPL subsets; the minimum feasible load of arc
-// (e, g) is v = max(0, r - min{slack[S] : S ⊇ need, g ∉ S}).  U = uint32_t
-// when every slack and load fits 32 bits (one redux.sync per arc).
+// (e, g) is v = max(0, r - min{slack[S] : S ⊇ need, g ∉ S}).  The result of
+// arc p (p = position in (expert, gpu id) order) goes to vtmp[p].
+// U = uint32_t when every slack and load fits 32 bits: one redux.sync per
+// arc and the next expert's metadata prefetched (software pipelined).
 // ---------------------------------------------------------------------------
 template <int SPL, typename U>
-__device__ void lexmin_warp(const SchedArgs &a, SchedSmem &s) {
+__device__ void lexmin_warp(const SchedArgs &a, SchedSmem &s, int64_t *vtmp) {
     const int lane = threadIdx.x & 31;
     const int E = a.E;
     const uint32_t NS = 1u << a.G;
@@ -163,23 +173,67 @@ __device__ void lexmin_warp(const SchedArgs &a, SchedSmem &s) {
         sl[j] = S < NS ? (U)(s.C[S] - s.W[S] * Q) : (U)0;
         valid |= (S < NS) << j;
     }
-    int b_next = s.grp_off[0];
+    int4 nxt = s.emeta[0];
+    U r_nxt = sizeof(U) == 4 ? (U)(uint32_t)nxt.w : (U)(s.totals[0] * Q);
     for (int e = 0; e < E; ++e) {
-        const int b = b_next;
-        b_next = s.grp_off[e + 1];
-        const int n = b_next - b;
+        const int b = nxt.x, n = nxt.y;
+        uint32_t R = (uint32_t)nxt.z;
+        U r = r_nxt;
+        if (e + 1 < E) {  // prefetch the next expert while this one runs
+            nxt = s.emeta[e + 1];
+            r_nxt = sizeof(U) == 4 ? (U)(uint32_t)nxt.w : (U)(s.totals[e + 1] * Q);
+        }
         if (n == 0) continue;
-        U r = (U)(s.totals[e] * Q);
-        uint32_t R = s.mask[e];
+        if (n == 1) {  // single replica: v = r; +r on S ⊇ {g} and -r on S ∋ g cancel
+            if (lane == 0) vtmp[b] = (int64_t)r;
+            continue;
+        }
+        if (n == 2) {
+            // Two replicas a < c (the d=2 common case), folded into one reduction:
+            // arc a's family {S : c ∈ S, a ∉ S} never contains R, so it sees the slack
+            // before the "+r on S ⊇ R" step; the net update afterwards is -v_a on
+            // S ∋ a, S ∌ c and -v_c on S ∋ c, S ∌ a (S ⊇ R: +r - v_a - v_c = 0).
+            const int ga = s.arc_gpu[b], gc = s.arc_gpu[b + 1];
+            U v_a = 0;
+            if (r) {
+                U t[SPL];
+#pragma unroll
+                for (int j = 0; j < SPL; ++j) {
+                    const uint32_t S = lane + 32 * j;
+                    const bool ok = ((valid >> j) & 1) && ((S >> gc) & 1) && !((S >> ga) & 1);
+                    t[j] = ok ? sl[j] : ~(U)0;
+                }
+#pragma unroll
+                for (int w = 1; w < SPL; w <<= 1)  // pairwise tree (ILP), not a serial chain
+#pragma unroll
+                    for (int j = 0; j + w < SPL; j += 2 * w) t[j] = t[j + w] < t[j] ? t[j + w] : t[j];
+                const U mn = wmin(t[0]);
+                v_a = r > mn ? r - mn : (U)0;
+            }
+            const U v_c = r - v_a;
+            if (lane == 0) {
+                vtmp[b] = (int64_t)v_a;
+                vtmp[b + 1] = (int64_t)v_c;
+            }
+#pragma unroll
+            for (int j = 0; j < SPL; ++j) {
+                const uint32_t S = lane + 32 * j;
+                const uint32_t ha = (S >> ga) & 1, hc = (S >> gc) & 1;
+                sl[j] -= (ha & ~hc) ? v_a : ((hc & ~ha) ? v_c : (U)0);
+            }
+            continue;
+        }
         if (r) {
 #pragma unroll
             for (int j = 0; j < SPL; ++j) {
                 const uint32_t S = lane + 32 * j;
-                if ((S & R) == R) sl[j] += r;  // expert e leaves the not-yet-processed set
+                sl[j] += ((S & R) == R) ? r : (U)0;  // expert e leaves the not-yet-processed set
             }
         }
+        int g_nxt = s.arc_gpu[b];
         for (int k = 0; k < n; ++k) {
-            const int g = s.arc_gpu[b + k];
+            const int g = g_nxt;
+            if (k + 1 < n) g_nxt = s.arc_gpu[b + k + 1];
             const uint32_t gbit = 1u << g;
             const uint32_t need = R & ~gbit;
             U v;
@@ -193,102 +247,129 @@ __device__ void lexmin_warp(const SchedArgs &a, SchedSmem &s) {
                 for (int j = 0; j < SPL; ++j) {
                     const uint32_t S = lane + 32 * j;
                     const bool ok = ((valid >> j) & 1) && ((S & need) == need) && !(S & gbit);
-                    if (ok && sl[j] < mn) mn = sl[j];
+                    mn = (ok && sl[j] < mn) ? sl[j] : mn;
                 }
                 mn = wmin(mn);
                 v = r > mn ? r - mn : (U)0;
             }
-            if (lane == 0) s.xq[s.arc_idx[b + k]] = (int64_t)v;
+            if (lane == 0) vtmp[b + k] = (int64_t)v;
             r -= v;
             R = need;
             if (v) {
 #pragma unroll
                 for (int j = 0; j < SPL; ++j) {
                     const uint32_t S = lane + 32 * j;
-                    if (S & gbit) sl[j] -= v;  // capacity of every subset holding g drops by v
+                    sl[j] -= (S & gbit) ? v : (U)0;  // capacity of every subset holding g drops by v
                 }
             }
         }
     }
 }
 
-// ---------------------------------------------------------------------------
-// step 6: Algorithm 1 for one expert on one warp (lane = source GPU).
-// Phase 1 keeps min(input, quota) on every hosting GPU; the final sweep
-// ("src ascending x EDP list order", router.py:149-157) exhausts either the
-// current source or the current replica at every step, so it is exactly the
-// merge of the remaining source amounts (in src order) with the remaining
-// quotas (in list order): range (src, dst_k) carries the overlap of
-// [A_src, A_src + in_src) and [B_k, B_k + quota_k), A/B exclusive prefix sums.
-// EMIT=false counts, EMIT=true writes at `pos` and accumulates the pair matrix.
-// ---------------------------------------------------------------------------
+// Non-topology routing, one thread per (expert e, source src): the phase-1
+// range of src (if it hosts e) and src's ranges of the final merge, whose
+// offset A_src is the prefix of the remaining source amounts and whose
+// replica intervals start at the prefix B_k of the remaining quotas.  c1/c2
+// return the counts; EMIT writes them at pos1 / pos2.
 template <bool EMIT>
-__device__ int route_expert_warp(const SchedArgs &a, SchedSmem &s, int e, int64_t pos, int32_t *status) {
-    const int lane = threadIdx.x & 31;
+__device__ void route_pair(const SchedArgs &a, SchedSmem &s, int e, int src, int *c1, int *c2, int64_t pos1,
+                           int64_t pos2) {
     const int G = a.G;
     const int b = s.grp_off[e], n = s.grp_off[e + 1] - b;
-    const int64_t rin = lane < G ? s.loads[e * G + lane] : 0;
-    const int dst_k = lane < n ? s.grp_gpu[b + lane] : -1;
-    const int64_t x_k = lane < n ? s.xi[b + lane] : 0;
-    const int64_t tot = warp_sum_i64(rin);
-    if (n == 0 && tot == 0) return 0;  // router.py:125-126
-    const bool neg = __any_sync(0xffffffffu, x_k < 0);
-    if (neg || warp_sum_i64(x_k) != tot) {  // _check_plan (router.py:97-111)
-        if (lane == 0) set_status(status, HEP_E_CONTRACT);
-        return 0;
+    const int64_t *L = s.loads + (size_t)e * G;
+    const int8_t *kx = s.kidx + (size_t)e * G;
+    auto rem_of = [&](int g) -> int64_t {
+        const int kk = kx[g];
+        if (kk < 0) return L[g];
+        const int64_t d = L[g] - s.xi[b + kk];
+        return d > 0 ? d : 0;
+    };
+    const int kk = kx[src];
+    const int64_t in = L[src];
+    const int64_t y1 = kk >= 0 ? (in < s.xi[b + kk] ? in : s.xi[b + kk]) : 0;
+    *c1 = y1 > 0;
+    if (EMIT && y1 > 0) {
+        int64_t *r_ = a.out.d_ranges + 4 * pos1;
+        r_[0] = e; r_[1] = src; r_[2] = src; r_[3] = y1;
+        atomicAdd(&s.pair[src * G + src], (unsigned long long)y1);
     }
-    // quota of this lane's GPU (if it hosts a replica of e)
-    int64_t rxg = 0;
-    bool hosts = false;
-#pragma unroll 1
-    for (int k = 0; k < n; ++k) {
-        const int d = __shfl_sync(0xffffffffu, dst_k, k);
-        const int64_t xv = __shfl_sync(0xffffffffu, x_k, k);
-        if (d == lane) { rxg = xv; hosts = true; }
-    }
-    const int64_t y1 = hosts ? (rin < rxg ? rin : rxg) : 0;
-    const unsigned b1 = __ballot_sync(0xffffffffu, y1 > 0);
-    const int n1 = __popc(b1);
-    const int64_t in2 = rin - y1;
-    const int64_t rx2g = rxg - y1;
-    const int64_t q_k = __shfl_sync(0xffffffffu, rx2g, dst_k < 0 ? 0 : dst_k);
-    const int64_t qk = lane < n ? q_k : 0;
-    const int64_t B_k = warp_incl_scan_i64(qk) - qk;
-    const int64_t A = warp_incl_scan_i64(lane < G ? in2 : 0) - (lane < G ? in2 : 0);
-    int cnt2 = 0;
-#pragma unroll 1
-    for (int k = 0; k < n; ++k) {
-        const int64_t Bk = __shfl_sync(0xffffffffu, B_k, k);
-        const int64_t Lk = __shfl_sync(0xffffffffu, qk, k);
-        const int64_t lo = A > Bk ? A : Bk;
-        const int64_t hi = (A + in2) < (Bk + Lk) ? (A + in2) : (Bk + Lk);
-        cnt2 += (lane < G && hi > lo);
-    }
-    const int total = n1 + (int)warp_sum_i64(cnt2);
-    if (EMIT) {
-        if (y1 > 0) {
-            const int64_t p = pos + __popc(b1 & ((1u << lane) - 1));
-            int64_t *r_ = a.out.d_ranges + 4 * p;
-            r_[0] = e; r_[1] = lane; r_[2] = lane; r_[3] = y1;
-            atomicAdd(&s.pair[lane * G + lane], (unsigned long long)y1);
-        }
-        int64_t p = pos + n1 + (warp_incl_scan_i64(cnt2) - cnt2);
-    #pragma unroll 1
-    for (int k = 0; k < n; ++k) {
-            const int64_t Bk = __shfl_sync(0xffffffffu, B_k, k);
-            const int64_t Lk = __shfl_sync(0xffffffffu, qk, k);
-            const int d = __shfl_sync(0xffffffffu, dst_k, k);
-            const int64_t lo = A > Bk ? A : Bk;
-            const int64_t hi = (A + in2) < (Bk + Lk) ? (A + in2) : (Bk + Lk);
-            if (lane < G && hi > lo) {
-                int64_t *r_ = a.out.d_ranges + 4 * p;
-                r_[0] = e; r_[1] = lane; r_[2] = d; r_[3] = hi - lo;
-                atomicAdd(&s.pair[lane * G + d], (unsigned long long)(hi - lo));
-                ++p;
+    const int64_t rem = rem_of(src);
+    int cnt = 0;
+    if (rem > 0) {
+        int64_t A = 0;
+        for (int g = 0; g < src; ++g) A += rem_of(g);
+        int64_t B = 0;
+        for (int k = 0; k < n && B < A + rem; ++k) {
+            const int dst = s.grp_gpu[b + k];
+            const int64_t qd = s.xi[b + k] - L[dst];
+            const int64_t q = qd > 0 ? qd : 0;
+            const int64_t lo = A > B ? A : B, hi = (A + rem) < (B + q) ? (A + rem) : (B + q);
+            if (hi > lo) {
+                if (EMIT) {
+                    int64_t *r_ = a.out.d_ranges + 4 * (pos2 + cnt);
+                    r_[0] = e; r_[1] = src; r_[2] = dst; r_[3] = hi - lo;
+                    atomicAdd(&s.pair[src * G + dst], (unsigned long long)(hi - lo));
+                }
+                ++cnt;
             }
+            B += q;
         }
     }
-    return total;
+    *c2 = cnt;
+}
+
+// One thread per expert (used when E is large enough to fill the block):
+// phase 1 in sorted(group) order, then the final sweep as the two-pointer
+// merge of the remaining source amounts (src order) with the remaining
+// quotas (list order) — each emitting step of the reference sweep exhausts
+// either the current source or the current replica.
+template <bool EMIT>
+__device__ int route_expert_merge(const SchedArgs &a, SchedSmem &s, int e, int64_t pos) {
+    const int G = a.G;
+    const int b = s.grp_off[e], n = s.grp_off[e + 1] - b;
+    const int64_t *L = s.loads + (size_t)e * G;
+    const int8_t *kx = s.kidx + (size_t)e * G;
+    int cnt = 0;
+    auto emit = [&](int src, int dst, int64_t y) {
+        if (EMIT) {
+            int64_t *r_ = a.out.d_ranges + 4 * (pos + cnt);
+            r_[0] = e; r_[1] = src; r_[2] = dst; r_[3] = y;
+            atomicAdd(&s.pair[src * G + dst], (unsigned long long)y);
+        }
+        ++cnt;
+    };
+    for (int k = 0; k < n; ++k) {
+        const int g = s.arc_gpu[b + k];
+        const int64_t x = s.xi[s.arc_idx[b + k]];
+        const int64_t y = L[g] < x ? L[g] : x;
+        if (y > 0) emit(g, g, y);
+    }
+    auto rem_of = [&](int g) -> int64_t {
+        const int kk = kx[g];
+        if (kk < 0) return L[g];
+        const int64_t d = L[g] - s.xi[b + kk];
+        return d > 0 ? d : 0;
+    };
+    auto quota_of = [&](int kk) -> int64_t {
+        const int64_t d = s.xi[b + kk] - L[s.grp_gpu[b + kk]];
+        return d > 0 ? d : 0;
+    };
+    int src = 0, k = 0;
+    int64_t rem = rem_of(0), q = n > 0 ? quota_of(0) : 0;
+    while (true) {
+        while (rem == 0) {
+            if (++src >= G) return cnt;
+            rem = rem_of(src);
+        }
+        while (q == 0) {
+            if (++k >= n) return cnt;
+            q = quota_of(k);
+        }
+        const int64_t y = rem < q ? rem : q;
+        emit(src, s.grp_gpu[b + k], y);
+        rem -= y;
+        q -= y;
+    }
 }
 
 // Topology-aware variant (router.py:136-147): sequential per expert, one thread.
@@ -357,6 +438,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
     // ---- step 1: stage placement + loads (+ caller plan) in shared memory -------
     for (int i = tid; i <= E; i += nt) s.grp_off[i] = a.grp_off[i];
     for (int i = tid; i < E; i += nt) s.mask[i] = a.mask[i];
+    for (int i = tid; i < E * G; i += nt) s.kidx[i] = a.kidx[i];
     for (int i = tid; i < nnz; i += nt) {
         const int idx = a.sorted[i];
         s.arc_idx[i] = idx;
@@ -437,7 +519,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
         if (tid == 0) {
             for (int w = 1; w < nt / 32; ++w)
                 if (frac_gt(red_n[w], red_d[w], bn, bd)) { bn = red_n[w]; bd = red_d[w]; }
-            int64_t g = gcd_i64(bn, bd);
+            int64_t g = gcd_i64(bd, bn - floordiv(bn, bd) * bd);  // den <= G: one reduction step
             if (g == 0) g = 1;
             bn /= g;
             bd /= g;
@@ -461,6 +543,9 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
                 s.C[S] = c;
             }
         }
+        for (int e = tid; e < E; e += nt)
+            s.emeta[e] = make_int4(s.grp_off[e], s.grp_off[e + 1] - s.grp_off[e], (int)s.mask[e],
+                                   (int)(uint32_t)(s.totals[e] * a.Q));
         __syncthreads();
         prof_mark(a.flags, 2);
         // ---- step 4: lex-min canonical plan ------------------------------------
@@ -468,11 +553,16 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
             const int64_t mQ = s.misc[0];
             const bool fits32 = (__int128)G * (total_all + 1) * a.Q < ((__int128)1 << 31) &&
                                 (__int128)G * (mQ + 1) < ((__int128)1 << 31);
-            if (fits32) lexmin_warp<SPL, uint32_t>(a, s);
-            else lexmin_warp<SPL, uint64_t>(a, s);
+            if (fits32) lexmin_warp<SPL, uint32_t>(a, s, s.xi);
+            else lexmin_warp<SPL, uint64_t>(a, s, s.xi);
         }
         __syncthreads();
-        for (int i = tid; i < nnz; i += nt) a.out.d_xq[i] = s.xq[i];
+        for (int p = tid; p < nnz; p += nt) {  // (expert, gpu id) order -> EDP list order
+            const int64_t v = s.xi[p];
+            s.xq[s.arc_idx[p]] = v;
+            a.out.d_xq[s.arc_idx[p]] = v;
+        }
+        __syncthreads();
         prof_mark(a.flags, 3);
     }
 
@@ -536,13 +626,31 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
     // ---- step 6: Algorithm 1 routing (router.py:114-158) --------------------------
     if (route) {
         const bool topo = (a.flags & HEP_SCHED_TOPO) && a.gpn > 0 && a.gpn < G;
-        // pass 0: ranges per expert (warp per expert; one thread per expert for topology routing)
-        const int warp = tid >> 5, lane = tid & 31, nw = nt >> 5;
+        // pass 0: range counts (one thread per (expert, source); per expert for topology routing)
         int64_t *ecount = s.totals;  // totals are no longer needed once the plan exists
+        int32_t *rc1 = s.rc, *rc2 = s.rc + E * G;
+        const bool per_expert = !topo && E >= nt / 4;  // enough experts to fill the block
         if (!topo) {
-            for (int e = warp; e < E; e += nw) {
-                const int c = route_expert_warp<false>(a, s, e, 0, status);
-                if (lane == 0) ecount[e] = c;
+            if (per_expert) {
+                for (int e = tid; e < E; e += nt) rc1[e * G] = route_expert_merge<false>(a, s, e, 0);
+            } else {
+                for (int i = tid; i < E * G; i += nt) route_pair<false>(a, s, i / G, i % G, &rc1[i], &rc2[i], 0, 0);
+            }
+            for (int e = tid; e < E; e += nt) {  // _check_plan (router.py:97-111)
+                const int b = s.grp_off[e], n = s.grp_off[e + 1] - b;
+                int64_t tot = 0, xs = 0;
+                bool neg = false;
+                for (int g = 0; g < G; ++g) tot += s.loads[e * G + g];
+                for (int k = 0; k < n; ++k) { xs += s.xi[b + k]; neg |= s.xi[b + k] < 0; }
+                if (neg || xs != tot) set_status(status, HEP_E_CONTRACT);
+            }
+            __syncthreads();
+            for (int e = tid; e < E; e += nt) {
+                int64_t c = 0;
+                if (per_expert) c = rc1[e * G];
+                else
+                    for (int g = 0; g < G; ++g) c += rc1[e * G + g] + rc2[e * G + g];
+                ecount[e] = c;
             }
         } else {
             for (int e = tid; e < E; e += nt) ecount[e] = route_expert_topo<false>(a, s, e, 0, status);
@@ -564,8 +672,20 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
         if (total_ranges > a.max_ranges) set_status(status, HEP_E_CAPACITY);
         __syncthreads();
         if (*status == 0) {
-            if (!topo) {
-                for (int e = warp; e < E; e += nw) route_expert_warp<true>(a, s, e, ecount[e], status);
+            if (per_expert) {
+                for (int e = tid; e < E; e += nt) route_expert_merge<true>(a, s, e, ecount[e]);
+            } else if (!topo) {
+                for (int i = tid; i < E * G; i += nt) {
+                    const int e = i / G, src = i % G;
+                    int64_t p1 = ecount[e], n1 = 0, p2 = 0;
+                    for (int g = 0; g < G; ++g) {
+                        const int c = rc1[e * G + g];
+                        n1 += c;
+                        if (g < src) { p1 += c; p2 += rc2[e * G + g]; }
+                    }
+                    int d1, d2;
+                    route_pair<true>(a, s, e, src, &d1, &d2, p1, ecount[e] + n1 + p2);
+                }
             } else {
                 for (int e = tid; e < E; e += nt) route_expert_topo<true>(a, s, e, ecount[e], status);
             }
@@ -677,6 +797,7 @@ static int launch_sched(hep_sched *h, SchedArgs &a, cudaStream_t stream) {
     a.grp_gpu = h->d_grp_gpu;
     a.sorted = h->d_sorted;
     a.mask = h->d_mask;
+    a.kidx = h->d_kidx;
     const size_t smem = sched_smem_bytes(h->G, h->E, h->nnz);
     HEP_REQUIRE(smem <= 200 * 1024, HEP_E_CAPACITY, "scheduler shared memory %zu B exceeds 200 KB (E=%d G=%d)", smem,
                 h->E, h->G);
@@ -770,6 +891,10 @@ extern "C" int hep_sched_create(int num_gpus, int num_experts, const int32_t *gr
     if (ce == cudaSuccess) ce = up((void **)&h->d_hosted_off, hosted_off.data(), sizeof(int32_t) * (G + 1));
     if (ce == cudaSuccess) ce = up((void **)&h->d_seg_nnz, seg_nnz.data(), sizeof(int32_t) * nnz);
     if (ce == cudaSuccess) ce = up((void **)&h->d_nnz_exp, nnz_exp.data(), sizeof(int32_t) * nnz);
+    std::vector<int8_t> kidx((size_t)E * G, (int8_t)-1);
+    for (int e = 0; e < E; ++e)
+        for (int i = off[e]; i < off[e + 1]; ++i) kidx[(size_t)e * G + gpu[i]] = (int8_t)(i - off[e]);
+    if (ce == cudaSuccess) ce = up((void **)&h->d_kidx, kidx.data(), (size_t)E * G);
     if (ce != cudaSuccess) {
         set_error("hep_sched_create: %s", cudaGetErrorString(ce));
         hep_sched_destroy(h);
@@ -789,6 +914,7 @@ extern "C" int hep_sched_destroy(hep_sched_t h) {
     cudaFree(h->d_hosted_off);
     cudaFree(h->d_seg_nnz);
     cudaFree(h->d_nnz_exp);
+    cudaFree(h->d_kidx);
     delete h;
     return HEP_OK;
 }
