@@ -311,31 +311,38 @@ def main():
     mean_load = sum(gpu_load) / len(gpu_load)
     max_mean = max(gpu_load) / mean_load if mean_load else 1.0
 
-    # --- e2e through the public API with host buffers (pinned), copies inside the timed region
-    xh = x.cpu().pin_memory()
-    oh = torch.empty(T, d, dtype=torch.bfloat16).pin_memory()
-    xd = torch.empty_like(x)
-    for _ in range(2):
-        xd.copy_(xh, non_blocking=True)
-        out = layer(xd)
-        oh.copy_(out, non_blocking=True)
+    # --- e2e through the public API with host buffers (pinned): every step copies
+    # its input batch host->device and its output device->host inside the timed
+    # region (HostPipeline overlaps batch i+1's H2D and batch i-1's D2H with batch i)
+    from paper_2511_16947_b200.layer import HostPipeline
+
+    pipe = HostPipeline(layer, T)
+    xh = [x.cpu().pin_memory() for _ in range(2)]
+    for i in range(3):
+        pipe.submit(xh[i % 2])
+    pipe.drain()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
-    e0.record(stream)
-    for _ in range(args.steps):
-        xd.copy_(xh, non_blocking=True)
-        out = layer(xd)
-        oh.copy_(out, non_blocking=True)
-    e1.record(stream)
+    t0 = time.perf_counter()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e0.record(pipe.s_in)
+    last = None
+    for i in range(args.steps):
+        last = pipe.submit(xh[i % 2])
+    out_last = pipe.result(last)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e1.record(pipe.s_out)
     torch.cuda.synchronize()
     e_ms = e0.elapsed_time(e1)
+    e_wall = (time.perf_counter() - t0) * 1e3
+    e_ms = max(e_ms, e_wall)  # device span from first H2D to last D2H, never below the host clock
     if world > 1:
         tt = torch.tensor([e_ms], device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e_ms = float(tt.item())
     e2e_value = world * T * args.steps / (e_ms / 1e3)
+    assert torch.isfinite(out_last.float()).all()
 
     hbm, tf_burst, tf_sus, peak_src = load_peaks()
     R = T * K

@@ -197,3 +197,59 @@ class MoELayer(torch.nn.Module):
 
     def check_status(self):
         self.sched.check_status("MoELayer")
+
+
+class HostPipeline:
+    """Serving-style public entry point for host-resident micro-batches.
+
+    ``submit(x_host)`` copies a pinned host batch to the device on a copy
+    stream, runs the layer on the compute stream and copies the output back
+    into a pinned host buffer on a third stream; two device buffer sets are
+    rotated so the H2D copy of batch i+1 and the D2H copy of batch i-1
+    overlap the layer's kernels of batch i.  ``result(i)`` blocks until
+    batch i's output is in host memory.
+    """
+
+    def __init__(self, layer: MoELayer, T: int, depth: int = 2):
+        self.layer = layer
+        dev = layer.device
+        self.T = T
+        self.depth = depth
+        self.x_dev = [torch.empty(T, layer.d, dtype=torch.bfloat16, device=dev) for _ in range(depth)]
+        self.bufs = [MoEBuffers(layer.sched, T, layer.K, layer.E, layer.e_pad, layer.d, layer.F, dev)
+                     for _ in range(depth)]
+        self.out_host = [torch.empty(T, layer.d, dtype=torch.bfloat16).pin_memory() for _ in range(depth)]
+        self.s_in = torch.cuda.Stream(device=dev)
+        self.s_comp = torch.cuda.Stream(device=dev)
+        self.s_out = torch.cuda.Stream(device=dev)
+        self.ev_in = [torch.cuda.Event() for _ in range(depth)]
+        self.ev_comp = [torch.cuda.Event() for _ in range(depth)]
+        self.ev_out = [torch.cuda.Event() for _ in range(depth)]
+        self.n = 0
+
+    def submit(self, x_host: torch.Tensor) -> int:
+        i = self.n % self.depth
+        if self.n >= self.depth:  # slot reuse: the previous occupant must be fully drained
+            self.s_in.wait_event(self.ev_comp[i])
+            self.s_comp.wait_event(self.ev_out[i])
+        with torch.cuda.stream(self.s_in):
+            self.x_dev[i].copy_(x_host, non_blocking=True)
+            self.ev_in[i].record(self.s_in)
+        self.s_comp.wait_event(self.ev_in[i])
+        self.layer.run(self.x_dev[i], self.bufs[i], self.s_comp)
+        self.ev_comp[i].record(self.s_comp)
+        self.s_out.wait_event(self.ev_comp[i])
+        with torch.cuda.stream(self.s_out):
+            self.out_host[i].copy_(self.bufs[i].out, non_blocking=True)
+            self.ev_out[i].record(self.s_out)
+        self.n += 1
+        return self.n - 1
+
+    def result(self, ticket: int) -> torch.Tensor:
+        i = ticket % self.depth
+        self.ev_out[i].synchronize()
+        return self.out_host[i]
+
+    def drain(self):
+        for e in self.ev_out:
+            e.synchronize()
