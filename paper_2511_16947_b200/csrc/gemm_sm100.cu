@@ -17,6 +17,7 @@
 // M-tile, so one expert's weight block is streamed from HBM once per wave and
 // the expert's rows stay L2-resident across its N sweep.
 #include <cudaTypedefs.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -103,6 +104,76 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     return *reinterpret_cast<uint32_t *>(&v);
 }
 
+// Epilogue of one accumulator tile row (this thread's TMEM lane): TMEM ->
+// registers -> fused op -> global.  t_row = TMEM address of the row's first
+// column, grow = global output row.
+template <int BN, int EPI>
+__device__ __forceinline__ void store_tile(const Params &p, uint32_t t_row, int64_t grow, bool valid, int n_blk,
+                                           uint64_t pol_out) {
+    if constexpr (EPI == EPI_SWIGLU) {
+        // columns [0, BN/2) = gate (W1 block), [BN/2, BN) = up (W3 block)
+        __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(p.out) + grow * p.ld_out +
+                             (int64_t)n_blk * (BN / 2);
+#pragma unroll 1
+        for (int c = 0; c < BN / 2; c += 16) {
+            uint32_t g[16], u[16];
+            tmem_ld16(t_row + c, g);
+            tmem_ld16(t_row + BN / 2 + c, u);
+            tmem_ld_wait();
+            uint32_t packed[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                float g0 = __uint_as_float(g[2 * i]), g1 = __uint_as_float(g[2 * i + 1]);
+                float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
+                packed[i] = pack_bf16(silu(g0) * u0, silu(g1) * u1);
+            }
+            if (valid) {
+                st_global_v4_hint(out + c, make_uint4(packed[0], packed[1], packed[2], packed[3]), pol_out);
+                st_global_v4_hint(out + c + 8, make_uint4(packed[4], packed[5], packed[6], packed[7]), pol_out);
+            }
+        }
+    } else if constexpr (EPI == EPI_BF16) {
+        __nv_bfloat16 *out =
+            reinterpret_cast<__nv_bfloat16 *>(p.out) + grow * p.ld_out + (int64_t)n_blk * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 16) {
+            uint32_t v[16];
+            tmem_ld16(t_row + c, v);
+            tmem_ld_wait();
+            uint32_t packed[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                packed[i] = pack_bf16(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+            if (valid) {
+                st_global_v4_hint(out + c, make_uint4(packed[0], packed[1], packed[2], packed[3]), pol_out);
+                st_global_v4_hint(out + c + 8, make_uint4(packed[4], packed[5], packed[6], packed[7]), pol_out);
+            }
+        }
+    } else {
+        float *out = reinterpret_cast<float *>(p.out) + grow * p.ld_out + (int64_t)n_blk * BN;
+        const int64_t col0 = (int64_t)n_blk * BN;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 16) {
+            uint32_t v[16];
+            tmem_ld16(t_row + c, v);
+            tmem_ld_wait();
+            if (valid) {
+                if (col0 + c + 16 <= p.out_cols) {
+                    float4 *dst = reinterpret_cast<float4 *>(out + c);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                             __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+                } else {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        if (col0 + c + i < p.out_cols) out[c + i] = __uint_as_float(v[i]);
+                }
+            }
+        }
+    }
+}
+
 template <int BN, int STAGES, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params p) {
@@ -148,7 +219,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             // grouped expert GEMMs reuse A (token rows) across N-blocks and stream B (weights);
             // the router GEMM streams A (x) and reuses B (Wg)
             const uint64_t pol_a = p.grouped ? policy_evict_last() : policy_evict_first();
-            const uint64_t pol_b = p.grouped ? policy_evict_first() : policy_evict_last();
+            // weights are shared by the concurrently running m-tiles of one (expert, N-block): normal priority
+            const uint64_t pol_b = p.grouped ? policy_evict_normal() : policy_evict_last();
             uint32_t phase = 0;
             for (int64_t t = blockIdx.x; t < n_total; t += gridDim.x) {
                 const Tile tl = decode(p, t);
@@ -194,6 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else {
         // ===================== epilogue (warps 2..5) =====================
+        const uint64_t pol_out = policy_evict_first();  // outputs are not re-read from L2 soon
         const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32)
         const int row_in_tile = quarter * 32 + lane;
         int acc = 0;
@@ -205,70 +278,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
             const bool valid = row_in_tile < tl.rows;
             const int64_t grow = (int64_t)tl.row0 + row_in_tile;
-            if constexpr (EPI == EPI_SWIGLU) {
-                // columns [0, BN/2) = gate (W1 block), [BN/2, BN) = up (W3 block)
-                __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(p.out) + grow * p.ld_out +
-                                     (int64_t)tl.n_blk * (BN / 2);
-#pragma unroll 1
-                for (int c = 0; c < BN / 2; c += 16) {
-                    uint32_t g[16], u[16];
-                    tmem_ld16(t_row + c, g);
-                    tmem_ld16(t_row + BN / 2 + c, u);
-                    tmem_ld_wait();
-                    uint32_t packed[8];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) {
-                        float g0 = __uint_as_float(g[2 * i]), g1 = __uint_as_float(g[2 * i + 1]);
-                        float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
-                        packed[i] = pack_bf16(silu(g0) * u0, silu(g1) * u1);
-                    }
-                    if (valid) {
-                        uint4 *dst = reinterpret_cast<uint4 *>(out + c);
-                        dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-                        dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
-                    }
-                }
-            } else if constexpr (EPI == EPI_BF16) {
-                __nv_bfloat16 *out =
-                    reinterpret_cast<__nv_bfloat16 *>(p.out) + grow * p.ld_out + (int64_t)tl.n_blk * BN;
-#pragma unroll 1
-                for (int c = 0; c < BN; c += 16) {
-                    uint32_t v[16];
-                    tmem_ld16(t_row + c, v);
-                    tmem_ld_wait();
-                    uint32_t packed[8];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i)
-                        packed[i] = pack_bf16(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-                    if (valid) {
-                        uint4 *dst = reinterpret_cast<uint4 *>(out + c);
-                        dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-                        dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
-                    }
-                }
-            } else {
-                float *out = reinterpret_cast<float *>(p.out) + grow * p.ld_out + (int64_t)tl.n_blk * BN;
-                const int64_t col0 = (int64_t)tl.n_blk * BN;
-#pragma unroll 1
-                for (int c = 0; c < BN; c += 16) {
-                    uint32_t v[16];
-                    tmem_ld16(t_row + c, v);
-                    tmem_ld_wait();
-                    if (valid) {
-                        if (col0 + c + 16 <= p.out_cols) {
-                            float4 *dst = reinterpret_cast<float4 *>(out + c);
-#pragma unroll
-                            for (int i = 0; i < 4; ++i)
-                                dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
-                                                     __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
-                        } else {
-#pragma unroll
-                            for (int i = 0; i < 16; ++i)
-                                if (col0 + c + i < p.out_cols) out[c + i] = __uint_as_float(v[i]);
-                        }
-                    }
-                }
-            }
+            store_tile<BN, EPI>(p, t_row, grow, valid, tl.n_blk, pol_out);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -284,6 +294,149 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of two CTAs computes a 256 x 256
+// tile.  Each CTA TMA-loads its own 128 rows of A and its 128-row half of the
+// 256-wide weight tile into its own smem (the bytes complete on the leader's
+// barrier); the leader's single MMA thread issues
+// tcgen05.mma.cta_group::2 (M=256, N=256, K=16), whose operands come from both
+// CTAs' smem, and each CTA's TMEM receives its 128 accumulator rows.  Weights
+// cross L2->SM once per pair instead of once per CTA and the per-CTA stage is
+// 32 KB (6 stages).  Commits are multicast to both CTAs; the peer's epilogue
+// releases TMEM through a remote arrive on the leader's barrier.
+// ---------------------------------------------------------------------------
+constexpr int kPairRows = 256;
+
+template <int STAGES>
+struct Smem2 {
+    static constexpr int A_BYTES = 128 * BK * 2;
+    static constexpr int B_BYTES = 128 * BK * 2;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr size_t BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + 8 * (2 * STAGES + 4) + 16;
+};
+
+template <int STAGES, int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params p) {
+    constexpr int BN = 256;
+    constexpr uint32_t TMEM_COLS = 512;
+    using S = Smem2<STAGES>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *sA = base;
+    uint8_t *sB = base + STAGES * S::A_BYTES;
+    uint64_t *full = reinterpret_cast<uint64_t *>(base + STAGES * S::STAGE_BYTES);
+    uint64_t *empty = full + STAGES;
+    uint64_t *tfull = empty + STAGES;
+    uint64_t *tempty = tfull + 2;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
+        }
+        fence_barrier_init();
+        fence_proxy_async_smem();
+    }
+    if (warp == 1) tmem_alloc_2sm(tmem_slot, TMEM_COLS);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int64_t n_total = total_tiles(p);
+    const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const int kb = p.kblocks;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ===================== TMA producer (both CTAs) =====================
+            const uint64_t pol_a = policy_evict_last();
+            const uint64_t pol_b = policy_evict_normal();
+            const uint32_t full_l = mapa_shared(smem_u32(&full[0]), 0);  // leader's full[0]
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int64_t t = cid; t < n_total; t += ncl) {
+                const Tile tl = decode(p, t);
+                const int32_t a_row = tl.row0 + (int32_t)rank * 128;
+                const int32_t b_row = (int32_t)(tl.expert * p.b_rows_per_exp + (int64_t)tl.n_blk * BN) + (int32_t)rank * 128;
+                for (int k = 0; k < kb; ++k) {
+                    mbar_wait_cluster(&empty[stage], phase ^ 1);
+                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * S::STAGE_BYTES);
+                    tma_load_2d_2sm(sA + stage * S::A_BYTES, &tmA, full_l + 8 * stage, k * BK, a_row, pol_a);
+                    tma_load_2d_2sm(sB + stage * S::B_BYTES, &tmB, full_l + 8 * stage, k * BK, b_row, pol_b);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {
+            // ===================== MMA issuer (leader CTA) =====================
+            constexpr uint32_t idesc = idesc_bf16_f32(kPairRows, BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int64_t t = cid; t < n_total; t += ncl) {
+                mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int k = 0; k < kb; ++k) {
+                    mbar_wait_cluster(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a_addr = smem_u32(sA + stage * S::A_BYTES);
+                    const uint32_t b_addr = smem_u32(sB + stage * S::B_BYTES);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk)
+                        mma_bf16_2sm(d_tmem, desc_kmajor_sw128(a_addr + kk * 32), desc_kmajor_sw128(b_addr + kk * 32),
+                                     idesc, (k | kk) ? 1u : 0u);
+                    mma_commit_2sm_mc(&empty[stage], 0x3);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                mma_commit_2sm_mc(&tfull[acc], 0x3);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+    } else {
+        // ===================== epilogue (warps 2..5, both CTAs) =====================
+        const uint64_t pol_out = policy_evict_first();
+        const uint32_t tempty_l = mapa_shared(smem_u32(&tempty[0]), 0);
+        const int quarter = warp & 3;
+        const int row_in_cta = quarter * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int64_t t = cid; t < n_total; t += ncl) {
+            const Tile tl = decode(p, t);
+            mbar_wait_cluster(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+            const int local_row = (int)rank * 128 + row_in_cta;
+            store_tile<BN, EPI>(p, t_row, (int64_t)tl.row0 + local_row, local_row < tl.rows, tl.n_blk, pol_out);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty_l + 8 * acc);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_2sm(tmem_base, TMEM_COLS);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // m-tile list from segments (row_start, rows, expert, dst): expert-major.
 // Consecutive segments of one expert that are contiguous in rows are merged
 // (the receive layout keeps all replicas of an expert adjacent), so an m-tile
@@ -292,15 +445,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ---------------------------------------------------------------------------
 template <bool WRITE>
 __device__ int64_t expert_tiles(const int32_t *seg, int n_seg, int e, int32_t *mt_row0, int32_t *mt_rows,
-                                int64_t pos) {
+                                int64_t pos, int tile_rows) {
     int64_t cnt = 0;
     int32_t r0 = 0, n = 0;
     bool open = false;
     auto flush = [&]() {
-        for (int32_t m = 0; m < n; m += BM) {
+        for (int32_t m = 0; m < n; m += tile_rows) {
             if (WRITE) {
                 mt_row0[pos + cnt] = r0 + m;
-                mt_rows[pos + cnt] = min(BM, n - m);
+                mt_rows[pos + cnt] = min(tile_rows, n - m);
             }
             ++cnt;
         }
@@ -322,13 +475,13 @@ __device__ int64_t expert_tiles(const int32_t *seg, int n_seg, int e, int32_t *m
 }
 
 __global__ void build_tiles_kernel(const int32_t *seg, int n_seg, int n_exp, int32_t *mt_row0, int32_t *mt_rows,
-                                   int32_t *exp_mt_off, int64_t cap, int32_t *status) {
+                                   int32_t *exp_mt_off, int64_t cap, int32_t *status, int tile_rows) {
     __shared__ int64_t scan[64];
     const int tid = threadIdx.x, nt = blockDim.x;
     const int chunk = (n_exp + nt - 1) / nt;
     const int e0 = min(n_exp, tid * chunk), e1 = min(n_exp, e0 + chunk);
     int64_t cnt = 0;
-    for (int e = e0; e < e1; ++e) cnt += expert_tiles<false>(seg, n_seg, e, nullptr, nullptr, 0);
+    for (int e = e0; e < e1; ++e) cnt += expert_tiles<false>(seg, n_seg, e, nullptr, nullptr, 0, tile_rows);
     int64_t total;
     int64_t pos = block_excl_scan_i64(cnt, scan, &total);
     if (total > cap) {
@@ -339,7 +492,7 @@ __global__ void build_tiles_kernel(const int32_t *seg, int n_seg, int n_exp, int
     }
     for (int e = e0; e < e1; ++e) {
         exp_mt_off[e] = (int32_t)pos;
-        pos += expert_tiles<true>(seg, n_seg, e, mt_row0, mt_rows, pos);
+        pos += expert_tiles<true>(seg, n_seg, e, mt_row0, mt_rows, pos, tile_rows);
     }
     if (tid == nt - 1) exp_mt_off[n_exp] = (int32_t)total;
 }
@@ -406,6 +559,31 @@ static int launch(const void *A, int64_t a_rows, int64_t K, const void *B, int64
     return HEP_OK;
 }
 
+template <int STAGES, int EPI>
+static int launch2sm(const void *A, int64_t a_rows, int64_t K, const void *B, int64_t b_rows, const Params &p,
+                     cudaStream_t stream) {
+    using S = Smem2<STAGES>;
+    CUtensorMap ta, tb;
+    int rc = make_tmap(&ta, A, (uint64_t)a_rows, (uint64_t)K, 128);
+    if (rc) return rc;
+    rc = make_tmap(&tb, B, (uint64_t)b_rows, (uint64_t)K, 128);
+    if (rc) return rc;
+    auto kern = gemm2sm_kernel<STAGES, EPI>;
+    HEP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES));
+    const int grid = sm_count() & ~1;  // whole CTA pairs
+    kern<<<grid, kThreads, S::BYTES, stream>>>(ta, tb, p);
+    HEP_CHECK_LAUNCH();
+    return HEP_OK;
+}
+
+// CTA pairs when experts carry enough rows that 256-row tiles do not waste
+// more than the 128-row tiles they replace; HEP_FFN_PAIR=0/1 forces it.
+static bool use_pairs(int64_t R, int n_experts) {
+    const char *env = getenv("HEP_FFN_PAIR");
+    if (env && *env) return env[0] == '1';
+    return n_experts > 0 && R / n_experts >= 1024;
+}
+
 }  // namespace gemm
 }  // namespace hep
 
@@ -466,7 +644,9 @@ extern "C" int hep_moe_expert_ffn(const void *d_rows, const void *d_w13, const v
     int32_t *mt_row0 = reinterpret_cast<int32_t *>(d_workspace);
     int32_t *mt_rows = mt_row0 + cap;
     int32_t *exp_off = mt_rows + cap;
-    build_tiles_kernel<<<1, 1024, 0, s>>>(d_seg, n_seg, n_experts, mt_row0, mt_rows, exp_off, cap, d_status);
+    const bool pairs = use_pairs(R, n_experts);
+    build_tiles_kernel<<<1, 1024, 0, s>>>(d_seg, n_seg, n_experts, mt_row0, mt_rows, exp_off, cap, d_status,
+                                          pairs ? kPairRows : BM);
     HEP_CHECK_LAUNCH();
     Params p{};
     p.grouped = 1;
@@ -481,7 +661,8 @@ extern "C" int hep_moe_expert_ffn(const void *d_rows, const void *d_w13, const v
     p.out = d_h;
     p.ld_out = ffn;
     p.out_cols = ffn;
-    int rc = launch<256, 4, EPI_SWIGLU>(d_rows, R, d_model, d_w13, (int64_t)n_experts * 2 * ffn, p, 0, s);
+    int rc = pairs ? launch2sm<6, EPI_SWIGLU>(d_rows, R, d_model, d_w13, (int64_t)n_experts * 2 * ffn, p, s)
+                   : launch<256, 4, EPI_SWIGLU>(d_rows, R, d_model, d_w13, (int64_t)n_experts * 2 * ffn, p, 0, s);
     if (rc) return rc;
     // GEMM 2: Y = H W2^T, B = W2 [E][d][F]
     p.kblocks = (int)(ffn / BK);
@@ -490,5 +671,6 @@ extern "C" int hep_moe_expert_ffn(const void *d_rows, const void *d_w13, const v
     p.out = d_y;
     p.ld_out = d_model;
     p.out_cols = d_model;
-    return launch<256, 4, EPI_BF16>(d_h, R, ffn, d_w2, (int64_t)n_experts * d_model, p, 0, s);
+    return pairs ? launch2sm<6, EPI_BF16>(d_h, R, ffn, d_w2, (int64_t)n_experts * d_model, p, s)
+                 : launch<256, 4, EPI_BF16>(d_h, R, ffn, d_w2, (int64_t)n_experts * d_model, p, 0, s);
 }
