@@ -227,6 +227,29 @@ def fam_zipf(h):
     return out
 
 
+def fam_adaptive(h):
+    """evaluate_and_maybe_replace decisions (adaptive.py:119-166) on zipf histories."""
+    from fractions import Fraction
+
+    out = []
+    for G, E, s, seed in ((8, 8, 1.5, 0), (8, 32, 1.25, 1), (4, 16, 2.0, 2), (8, 32, 0.2, 3), (8, 128, 2.0, 4)):
+        shape = h.ClusterShape(G, E, 2)
+        cur = h.cayley_symmetric(shape)
+        wl = h.gen_zipf_workload(shape, s, 1024, 6, seed=seed)
+        hist = h.LoadHistory(4)
+        for mb in wl.micro_batches:
+            hist.push(h.aggregate_expert_loads(mb))
+        pol = h.ReplacementPolicy(mc_samples=25)
+        dec = h.evaluate_and_maybe_replace(cur, hist, pol, shape, seed)
+        out.append(dict(G=G, E=E, s=s, seed=seed, history=[list(r) for r in hist.entries],
+                        replaced=dec.replaced, groups=[list(g) for g in dec.placement.edp_groups],
+                        slots=list(dec.placement.slots), ratio=dec.predicted_ratio,
+                        old_m=[Fraction(dec.old_m).numerator, Fraction(dec.old_m).denominator],
+                        new_m=None if dec.new_m is None else [Fraction(dec.new_m).numerator, Fraction(dec.new_m).denominator],
+                        changed=dec.changed_slots, cost=dec.migration_cost_total))
+    return out
+
+
 def dump(name, obj):
     path = os.path.join(HERE, name)
     data = json.dumps(obj, separators=(",", ":")).encode()
@@ -249,6 +272,7 @@ def main():
     dump("sched_asym.json.gz", fam_asym(h))
     dump("placements.json", fam_placements(h))
     dump("zipf_counts.json.gz", fam_zipf(h))
+    dump("adaptive.json", fam_adaptive(h))
 
 
 if __name__ == "__main__":
