@@ -217,6 +217,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
     ap.add_argument("--skew", type=float, default=1.0)
+    ap.add_argument("--placement", default="adaptive", choices=["adaptive", "cayley"])
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu legs)")
@@ -252,12 +253,39 @@ def main():
     L = _lib.lib()
 
     def step():
-        layer.run(x, bufs, stream)
+        layer.run(x, layer.buffers(T), stream)
+
+    def gpu_balance():
+        gl = layer.sched.gpu_load.cpu().tolist()
+        mean = sum(gl) / len(gl)
+        return (max(gl) / mean if mean else 1.0), gl
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     layer.check_status()
+    static_max_mean, static_loads = gpu_balance()
+    placement_desc = f"cayley_symmetric(G={G}, E={E}, d=2)"
+    replacement = None
+    if args.placement == "adaptive":
+        # the paper's adaptive replacement (adaptive.py:119-166): score the static
+        # placement on the observed expert loads and adopt the greedy + Monte-Carlo
+        # candidate when it is better; a one-off, off the per-micro-batch path
+        from paper_2511_16947_b200.adaptive import LoadHistory, ReplacementPolicy, evaluate_and_maybe_replace
+
+        hist = LoadHistory(8)
+        hist.push(layer.expert_loads(T))
+        dec = evaluate_and_maybe_replace(pl, hist, ReplacementPolicy(threshold=1.0, mc_samples=200), shape, 0)
+        replacement = dec.to_event(args.warmup)
+        if dec.replaced:
+            layer.set_placement(dec.placement)
+            placement_desc = (f"adaptive: greedy replica counts {list(P.placement.greedy_replica_counts(hist.entries[0], E * 2, max_count=G))}"
+                              f" + Monte-Carlo layout (200 samples), from cayley_symmetric(G={G}, E={E}, d=2)")
+            for _ in range(args.warmup):
+                step()
+            torch.cuda.synchronize()
+            layer.check_status()
+    bufs = layer.buffers(T)
 
     # --- timed region: K steps back to back; per-stage events on the launching stream
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -384,13 +412,15 @@ def main():
                 "sim_ep": G,
                 "tokens_per_virtual_gpu": T // G,
                 "top_k": K, "d_model": d, "ffn": F, "experts": E,
-                "placement": f"cayley_symmetric(G={G}, E={E}, d=2)",
+                "placement": placement_desc,
                 "zipf_s": args.skew,
                 "pass": "forward",
                 "l2": "inputs larger than L2 (x %.0f MB, expert weights %.2f GB per step)" % (T * d * 2 / 1e6,
                                                                                                3 * E * d * F * 2 / 1e9),
             },
             "max_mean_gpu_load": max_mean,
+            "max_mean_gpu_load_static_cayley": static_max_mean,
+            "replacement": replacement,
             "m_exact": [m_num, m_den],
             "gpu_loads": gpu_load,
             "scheduler_us": sched_us,

@@ -120,6 +120,21 @@ class MoELayer(torch.nn.Module):
         self.gate_bias = None if gate_bias is None else gate_bias.to(self.device, torch.float32).contiguous()
         self._bufs: dict[int, MoEBuffers] = {}
 
+    def set_placement(self, placement: Placement) -> None:
+        """Adopt a new placement (adaptive replacement, ``adaptive.py``).  The
+        simulated EP group keeps one weight copy per expert, so only the
+        device scheduler tables change; buffers are re-sized lazily."""
+        if (placement.num_gpus, placement.num_experts) != (self.G, self.E):
+            raise ValueError("placement must keep the number of GPUs and experts")
+        self.placement = placement
+        self.sched = DeviceScheduler(placement, device=self.device)
+        self._bufs.clear()
+
+    def expert_loads(self, T: int) -> list[int]:
+        """Per-expert token counts of the last micro-batch (host copy of the
+        device histogram's column sums; for the adaptive policy)."""
+        return self.buffers(T).hist.sum(dim=0).cpu().tolist()
+
     def buffers(self, T: int) -> MoEBuffers:
         b = self._bufs.get(T)
         if b is None:
