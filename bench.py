@@ -207,6 +207,95 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
+# our arm, N > 1: real expert parallelism, one rank per GPU (ep.py)
+# ---------------------------------------------------------------------------
+def run_ep(args, world, rank, local, dev):
+    """Scheduling group = the N ranks; every rank owns T tokens per micro-batch
+    (weak scaling: per-GPU work fixed).  Histogram all-gather and the dispatch /
+    combine all-to-all-v run over NCCL; the placement is the Cayley layout of
+    the N GPUs, replaced by the adaptive one when it is better (decided from the
+    all-gathered loads, identically on every rank)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2511_16947_b200 as P
+    from paper_2511_16947_b200.adaptive import LoadHistory, ReplacementPolicy, evaluate_and_maybe_replace
+    from paper_2511_16947_b200.ep import DistComm, EPMoELayer
+
+    E, K, d, F, T, _ = CONFIGS[args.config]
+    G = world
+    shape = P.ClusterShape(G, E, 2)
+    pl = P.cayley_symmetric(shape) if (E & (E - 1)) == 0 and (G & (G - 1)) == 0 else P.placement.symmetric_placement(shape)
+    bias = torch.tensor(P.zipf_gate_bias(E, args.skew, 0)) if args.skew > 0 else None
+    comm = DistComm()
+    layer = EPMoELayer(pl, d, F, K, comm, [rank], seed=0, gate_bias=bias, device=dev)
+    x = torch.randn(T, d, generator=torch.Generator(device=dev).manual_seed(1000 + rank), device=dev).to(torch.bfloat16)
+    for _ in range(args.warmup):
+        layer.forward([x])
+    torch.cuda.synchronize()
+    gl = layer.ranks[0].sched.gpu_load.cpu().tolist()
+    static_mm = max(gl) * len(gl) / max(sum(gl), 1)
+    replacement = None
+    if args.placement == "adaptive":
+        hist = LoadHistory(8)
+        hist.push(layer.ranks[0].bufs[T]["hist_all"].sum(dim=0).cpu().tolist())
+        dec = evaluate_and_maybe_replace(pl, hist, ReplacementPolicy(threshold=1.0, mc_samples=200), shape, 0)
+        replacement = dec.to_event(args.warmup)
+        if dec.replaced:  # migration = re-materialising the replicas of the new layout
+            pl = dec.placement
+            layer = EPMoELayer(pl, d, F, K, comm, [rank], seed=0, gate_bias=bias, device=dev)
+            for _ in range(args.warmup):
+                layer.forward([x])
+            torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        layer.forward([x])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    t_ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    t_ms = float(t_ms.item())
+    gl = layer.ranks[0].sched.gpu_load.cpu().tolist()
+    mm = max(gl) * len(gl) / max(sum(gl), 1)
+    # e2e: host tokens in, host outputs back, every step
+    xh = x.cpu().pin_memory()
+    oh = torch.empty(T, d, dtype=torch.bfloat16).pin_memory()
+    xd = torch.empty_like(x)
+    dist.barrier()
+    torch.cuda.synchronize()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        xd.copy_(xh, non_blocking=True)
+        (out,) = layer.forward([xd])
+        oh.copy_(out, non_blocking=True)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    e_ms = torch.tensor([f0.elapsed_time(f1)], device=dev)
+    dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+    e_ms = float(e_ms.item())
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": world * T * args.steps / (t_ms / 1e3), "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": {"workload": CONFIG_TEXT[args.config], "tokens_per_microbatch_per_gpu": T, "ep": world,
+                       "top_k": K, "d_model": d, "ffn": F, "experts": E, "zipf_s": args.skew, "pass": "forward",
+                       "exchange": "NCCL all-gather (histograms) + all-to-all-v dispatch/combine"},
+            "max_mean_gpu_load": mm, "max_mean_gpu_load_static_cayley": static_mm, "replacement": replacement,
+            "e2e": {"value": world * T * args.steps / (e_ms / 1e3), "unit": "tokens/s",
+                    "h2d_bytes_per_step": T * d * 2, "d2h_bytes_per_step": T * d * 2},
+            "gpu_launches": args.steps * 13,
+        }))
+    dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
 def main():
@@ -242,6 +331,9 @@ def main():
     dev = torch.device("cuda", local)
 
     E, K, d, F, T, G = CONFIGS[args.config]
+    if world > 1:
+        run_ep(args, world, rank, local, dev)
+        return
     shape = P.ClusterShape(G, E, 2)
     pl = P.cayley_symmetric(shape)
     bias = torch.tensor(P.zipf_gate_bias(E, args.skew, 0)) if args.skew > 0 else None

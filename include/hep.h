@@ -168,6 +168,25 @@ int hep_moe_assign(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_t
                    int64_t *d_expert_rows, void *workspace, size_t workspace_bytes, void *stream);
 size_t hep_moe_assign_workspace(hep_sched_t h, int64_t T, int K);
 
+/*
+ * K4 for one rank of a real EP group (one process per GPU, rank r = source r
+ * of its own T tokens and destination r of its replicas).  Outputs:
+ *   d_tok_row [T][K] int32  position of assignment (t,k) in the send buffer
+ *                           [dst][expert asc][rank]; after the dispatch and the
+ *                           reverse (combine) all-to-all the expert outputs come
+ *                           back at the same positions
+ *   d_seg     [G*n_hosted][4] int32 receive-buffer segments ([src][hosted expert
+ *                           asc]): (row_start, rows, local weight slot, src)
+ *   d_counts  [2G] int64    rows sent to each dst, rows received from each src
+ *                           (the all-to-all-v split sizes)
+ */
+int hep_moe_assign_ep(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_topk_idx, int64_t T, int K, int rank,
+                      int32_t *d_tok_row, int32_t *d_seg, int64_t *d_counts, void *workspace, size_t workspace_bytes,
+                      void *stream);
+size_t hep_moe_assign_ep_workspace(hep_sched_t h, int64_t T, int K);
+/* experts hosted by `rank` and the number of local weight slots it needs */
+int hep_sched_hosted(hep_sched_t h, int rank, int *n_hosted, int *n_slots);
+
 /* K5 permute/dispatch: rows[tok_row[t][k]] = x[t]  (bf16, 128-bit vectorised scatter). */
 int hep_moe_permute(const void *d_x, const int32_t *d_tok_row, int64_t T, int K, int64_t d_model, void *d_rows,
                     void *stream);

@@ -30,6 +30,8 @@ struct AssignWs {
     int32_t *es_delta;  // [E*G*G] row - rank of each range
     int32_t *first;     // [E+1] first range index of expert e (-1 = none)
     int32_t *chunk_cnt; // [n_src * n_chunks * E]
+    int32_t *cnt3;      // [E*G*G] range count of (expert, src, dst)   (EP rank view)
+    int32_t *sbase;     // [E*G]   send-buffer base of (expert, dst)   (EP rank view)
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -44,6 +46,8 @@ static size_t assign_ws_bytes(const hep_sched *h, int64_t T, int n_src, int64_t 
     b += align256(4 * (size_t)(E * G * G));
     b += align256(4 * (size_t)(E + 1));
     b += align256(4 * (size_t)(n_src * ncs * E));
+    b += align256(4 * (size_t)(E * G * G));
+    b += align256(4 * (size_t)(E * G));
     return b;
 }
 
@@ -57,8 +61,9 @@ static AssignWs carve_ws(const hep_sched *h, void *ws, int n_src, int64_t tps) {
     w.es_end = (int32_t *)p; p += align256(4 * (size_t)(E * G * G));
     w.es_delta = (int32_t *)p; p += align256(4 * (size_t)(E * G * G));
     w.first = (int32_t *)p; p += align256(4 * (size_t)(E + 1));
-    w.chunk_cnt = (int32_t *)p;
-    (void)n_src;
+    w.chunk_cnt = (int32_t *)p; p += align256(4 * (size_t)(n_src * ((tps + kChunk - 1) / kChunk) * E));
+    w.cnt3 = (int32_t *)p; p += align256(4 * (size_t)(E * G * G));
+    w.sbase = (int32_t *)p;
     return w;
 }
 
@@ -162,7 +167,8 @@ __global__ void chunk_scan_kernel(int n_src, int ncs, int E, int32_t *chunk_cnt)
 
 // one warp per chunk; lanes k < K own pick k of each token (distinct experts)
 __global__ void chunk_map_kernel(const int32_t *topk_idx, int K, int E, int G, int64_t tps, int64_t T, int ncs,
-                                 const int32_t *chunk_cnt, AssignWs w, int32_t *tok_row, int32_t *row_tok) {
+                                 const int32_t *chunk_cnt, AssignWs w, int32_t *tok_row, int32_t *row_tok,
+                                 int src_base) {
     extern __shared__ int32_t sm[];
     int32_t *ctr = sm;                // [E]
     int32_t *l_cnt = ctr + E;         // [E]
@@ -172,7 +178,7 @@ __global__ void chunk_map_kernel(const int32_t *topk_idx, int K, int E, int G, i
     const int lane = threadIdx.x;
     for (int e = lane; e < E; e += 32) {
         ctr[e] = chunk_cnt[(int64_t)blockIdx.x * E + e];
-        const int es = e * G + src;
+        const int es = e * G + src_base + src;
         const int n = w.es_cnt[es];
         l_cnt[e] = n;
         for (int j = 0; j < n; ++j) {
@@ -194,9 +200,77 @@ __global__ void chunk_map_kernel(const int32_t *topk_idx, int K, int E, int G, i
             while (j + 1 < n && q >= l_end[e * G + j]) ++j;
             const int row = q + l_delta[e * G + j];
             tok_row[t * K + lane] = row;
-            row_tok[row] = (int32_t)t;
+            if (row_tok) row_tok[row] = (int32_t)t;
         }
         __syncwarp();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// EP rank view (one process per GPU).  Rank r is source r of its own T tokens
+// and destination r of its replicas.  Send buffer: [dst][expert asc][rank];
+// receive buffer (what NCCL all-to-all-v delivers): [src][expert asc][rank],
+// one grouped-GEMM segment per (src, hosted expert) carrying the expert's
+// local weight slot.  Every rank derives all offsets from the same routing
+// table, so both sides agree without exchanging anything but the rows.
+// ---------------------------------------------------------------------------
+__global__ void ep_prep_kernel(int G, int E, int rank, const int64_t *ranges, const int64_t *n_ranges_p,
+                               const int64_t *transfer, const int32_t *hosted, int n_hosted, const int32_t *nnz_exp,
+                               const int32_t *slots, int64_t *counts, int32_t *seg, AssignWs w, int32_t *status) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int64_t n_ranges = *n_ranges_p;
+    for (int i = tid; i < E * G * G; i += nt) w.cnt3[i] = 0;
+    for (int i = tid; i < E * G; i += nt) w.es_cnt[i] = 0;
+    for (int i = tid; i <= E; i += nt) w.first[i] = -1;
+    __syncthreads();
+    for (int64_t r = tid; r < n_ranges; r += nt) {
+        const int64_t *q = ranges + 4 * r;
+        const int e = (int)q[0];
+        w.cnt3[((int64_t)e * G + q[1]) * G + q[2]] = (int32_t)q[3];
+        if (r == 0 || ranges[4 * (r - 1)] != e) w.first[e] = (int)r;
+    }
+    __syncthreads();
+    if (tid < G) {
+        const int d = tid;
+        counts[d] = transfer[rank * G + d];      // rows this rank sends to d
+        counts[G + d] = transfer[d * G + rank];  // rows this rank receives from d
+        int64_t run = 0;
+        for (int dd = 0; dd < d; ++dd) run += transfer[rank * G + dd];
+        for (int e = 0; e < E; ++e) {
+            w.sbase[e * G + d] = (int32_t)run;
+            run += w.cnt3[((int64_t)e * G + rank) * G + d];
+        }
+        // receive segments of source d: [src][hosted expert asc]
+        int64_t row = 0;
+        for (int ss = 0; ss < d; ++ss) row += transfer[ss * G + rank];
+        for (int h = 0; h < n_hosted; ++h) {
+            const int e = nnz_exp[hosted[h]];
+            const int32_t c = w.cnt3[((int64_t)e * G + d) * G + rank];
+            int32_t *sg = seg + 4 * ((int64_t)d * n_hosted + h);
+            sg[0] = (int32_t)row;
+            sg[1] = c;
+            sg[2] = slots[e];
+            sg[3] = d;
+            row += c;
+        }
+        if (row >= ((int64_t)1 << 31)) atomicCAS(status, 0, HEP_E_CAPACITY);
+    }
+    __syncthreads();
+    // per (expert, this source): ranges in table order -> send positions
+    for (int e = tid; e < E; e += nt) {
+        const int r0 = w.first[e];
+        if (r0 < 0) continue;
+        int64_t rank_start = 0;
+        const int es = e * G + rank;
+        for (int64_t j = r0; j < n_ranges && ranges[4 * j] == e; ++j) {
+            if (ranges[4 * j + 1] != rank) continue;
+            const int dst = (int)ranges[4 * j + 2];
+            const int64_t c = ranges[4 * j + 3];
+            const int slot = w.es_cnt[es]++;
+            w.es_end[es * G + slot] = (int32_t)(rank_start + c);
+            w.es_delta[es * G + slot] = (int32_t)(w.sbase[e * G + dst] - rank_start);
+            rank_start += c;
+        }
     }
 }
 
@@ -331,7 +405,7 @@ extern "C" int hep_moe_assign(hep_sched_t h, const hep_sched_out *sched, const i
     HEP_REQUIRE(sm <= 200 * 1024, HEP_E_CAPACITY, "chunk_map smem %zu", sm);
     if (sm > 48 * 1024) HEP_CHECK_CUDA(cudaFuncSetAttribute(chunk_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     chunk_map_kernel<<<nblk, 32, sm, s>>>(d_topk_idx, K, E, G, tokens_per_src, T, ncs, w.chunk_cnt, w, d_tok_row,
-                                          d_row_tok);
+                                          d_row_tok, 0);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
 }
@@ -365,6 +439,57 @@ extern "C" int hep_moe_combine(const void *d_y, const int32_t *d_tok_row, const 
         HEP_COMBINE(14) HEP_COMBINE(15) HEP_COMBINE(16)
 #undef HEP_COMBINE
     }
+    HEP_CHECK_LAUNCH();
+    return HEP_OK;
+}
+
+extern "C" size_t hep_moe_assign_ep_workspace(hep_sched_t h, int64_t T, int K) {
+    (void)K;
+    if (!h) return 0;
+    return assign_ws_bytes(h, T, 1, T > 0 ? T : 1);
+}
+
+extern "C" int hep_sched_hosted(hep_sched_t h, int rank, int *n_hosted, int *n_slots) {
+    HEP_REQUIRE(h && rank >= 0 && rank < h->G, HEP_E_DIMENSION, "hep_sched_hosted: rank %d", rank);
+    const int b = h->h_hosted_off[rank], n = h->h_hosted_off[rank + 1] - b;
+    if (n_hosted) *n_hosted = n;
+    if (n_slots) {
+        int mx = 0;
+        for (int e = 0; e < h->E; ++e)
+            for (int i = h->h_grp_off[e]; i < h->h_grp_off[e + 1]; ++i)
+                if (h->h_grp_gpu[i] == rank && h->h_slots[e] + 1 > mx) mx = h->h_slots[e] + 1;
+        *n_slots = mx;
+    }
+    return HEP_OK;
+}
+
+extern "C" int hep_moe_assign_ep(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_topk_idx, int64_t T, int K,
+                                 int rank, int32_t *d_tok_row, int32_t *d_seg, int64_t *d_counts, void *workspace,
+                                 size_t workspace_bytes, void *stream) {
+    HEP_REQUIRE(h && sched && d_topk_idx && d_tok_row && d_seg && d_counts && workspace, HEP_E_CONTRACT,
+                "hep_moe_assign_ep: null argument");
+    HEP_REQUIRE(rank >= 0 && rank < h->G && K >= 1 && K <= 16, HEP_E_DIMENSION, "hep_moe_assign_ep: rank/K");
+    const int64_t tps = T > 0 ? T : 1;
+    HEP_REQUIRE(workspace_bytes >= assign_ws_bytes(h, T, 1, tps), HEP_E_CAPACITY, "hep_moe_assign_ep: workspace");
+    cudaStream_t s = (cudaStream_t)stream;
+    AssignWs w = carve_ws(h, workspace, 1, tps);
+    const int E = h->E, G = h->G;
+    const int n_hosted = h->h_hosted_off[rank + 1] - h->h_hosted_off[rank];
+    ep_prep_kernel<<<1, 512, 0, s>>>(G, E, rank, sched->d_ranges, sched->d_n_ranges, sched->d_transfer,
+                                     h->d_seg_nnz + h->h_hosted_off[rank], n_hosted, h->d_nnz_exp, h->d_slots,
+                                     d_counts, d_seg, w, sched->d_status);
+    HEP_CHECK_LAUNCH();
+    if (T <= 0) return HEP_OK;
+    const int ncs = (int)((tps + kChunk - 1) / kChunk);
+    chunk_count_kernel<<<ncs, 128, E * sizeof(int32_t), s>>>(d_topk_idx, K, E, tps, T, ncs, w.chunk_cnt);
+    HEP_CHECK_LAUNCH();
+    chunk_scan_kernel<<<(E + 255) / 256, 256, 0, s>>>(1, ncs, E, w.chunk_cnt);
+    HEP_CHECK_LAUNCH();
+    const size_t sm = sizeof(int32_t) * (2 * (size_t)E + 2 * (size_t)E * G);
+    HEP_REQUIRE(sm <= 200 * 1024, HEP_E_CAPACITY, "chunk_map smem %zu", sm);
+    if (sm > 48 * 1024)
+        HEP_CHECK_CUDA(cudaFuncSetAttribute(chunk_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+    chunk_map_kernel<<<ncs, 32, sm, s>>>(d_topk_idx, K, E, G, tps, T, ncs, w.chunk_cnt, w, d_tok_row, nullptr, rank);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
 }
