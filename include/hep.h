@@ -161,10 +161,12 @@ int hep_gemm_bf16(const void *d_A, const void *d_B, void *d_D, int64_t M, int64_
  *   d_row_tok [R]    int32  token of each row (R = total assignments)
  *   d_seg      [nnz][4] int32 (row_start, rows, expert, dst) per replica, in row order
  *   d_expert_rows [E+1] int64 first row of each expert's contiguous block
- * Needs the hep_sched_out of the same micro-batch (ranges + xi).
+ * Needs the hep_sched_out of the same micro-batch (ranges + xi).  row_align: every
+ * expert block starts on a multiple of row_align rows (1 = dense; 64 for training, so the
+ * weight-gradient GEMMs contract over whole 64-row blocks; padding rows are never written).
  */
 int hep_moe_assign(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_topk_idx, int64_t T, int K,
-                   int64_t tokens_per_src, int32_t *d_tok_row, int32_t *d_row_tok, int32_t *d_seg,
+                   int64_t tokens_per_src, int row_align, int32_t *d_tok_row, int32_t *d_row_tok, int32_t *d_seg,
                    int64_t *d_expert_rows, void *workspace, size_t workspace_bytes, void *stream);
 size_t hep_moe_assign_workspace(hep_sched_t h, int64_t T, int K);
 
@@ -210,6 +212,42 @@ size_t hep_moe_ffn_workspace(int n_seg, int64_t R, int n_experts);
 /* K7 combine/un-permute: out[t] = sum_k w[t][k] * y[tok_row[t][k]] (fp32 accumulate in k order). */
 int hep_moe_combine(const void *d_y, const int32_t *d_tok_row, const float *d_topk_w, int64_t T, int K,
                     int64_t d_model, void *d_out, void *stream);
+
+/* K7 with unit weights and an optional addend: out[t] = add[t] + sum_k w[t][k] y[row(t,k)]
+ * (d_topk_w may be NULL = all ones; d_add may be NULL).  The permute's transpose. */
+int hep_moe_gather_sum(const void *d_y, const int32_t *d_tok_row, const float *d_topk_w, const void *d_add, int64_t T,
+                       int K, int64_t d_model, void *d_out, void *stream);
+
+/* ======================================================================
+ * Backward (training).  Gradients of the layer above, all on the device.
+ * ====================================================================== */
+/* K7^T: dY[row(t,k)] = w[t][k] dout[t] (bf16), dw[t][k] = <dout[t], Y[row(t,k)]> (fp32) */
+int hep_moe_combine_bwd(const void *d_dout, const void *d_y, const int32_t *d_tok_row, const float *d_topk_w,
+                        int64_t T, int K, int64_t d_model, void *d_dy, float *d_dw, void *stream);
+/* zero the alignment padding rows of every expert block of a [rows][width] bf16 buffer */
+int hep_moe_zero_padding(const int64_t *d_expert_rows, const int32_t *d_seg, int n_seg, int E, void *d_buf,
+                         int64_t width, void *stream);
+/*
+ * K6^T: expert FFN backward.  Inputs: receive rows X, pre-activations A13 [R][2F]
+ * (stored by the forward when hep_moe_expert_ffn_train is used), H, dY (padding rows
+ * are zeroed here), weights.  Outputs: dA13 scratch, dX rows (bf16), dW13 / dW2 (fp32,
+ * [E][2F][d] W13 interleave, [E][d][F]).  Requires d % 256 == 0, F % 256 == 0.
+ */
+int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, const void *d_h, void *d_dy, const void *d_w13,
+                           const void *d_w2, const int32_t *d_seg, int n_seg, const int64_t *d_expert_rows,
+                           int64_t Rcap, int64_t d_model, int64_t ffn, int n_experts, void *d_da13, void *d_dx_rows,
+                           float *d_dw13, float *d_dw2, void *d_workspace, size_t workspace_bytes, int32_t *d_status,
+                           void *stream);
+/* forward FFN that also stores the pre-activations A13 for the backward */
+int hep_moe_expert_ffn_train(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg, int n_seg,
+                             int64_t R, int64_t d_model, int64_t ffn, int n_experts, void *d_h, void *d_y,
+                             void *d_pre, void *d_workspace, size_t workspace_bytes, int32_t *d_status, void *stream);
+/* router backward: dlogit = w (dw - sum w dw) on the selected experts, bf16 [T][ld] */
+int hep_gate_bwd(const int32_t *d_topk_idx, const float *d_topk_w, const float *d_dw, int64_t T, int K, int64_t ld,
+                 void *d_dlogits, void *stream);
+/* dWg = dlogits^T x (fp32 [E64][d]), dx_gate = dlogits Wg (bf16 [T][d]) */
+int hep_router_bwd(const void *d_x, const void *d_wg, const void *d_dlogits, int64_t T, int64_t d_model, int E64,
+                   float *d_dwg, void *d_dxg, void *stream);
 
 #ifdef __cplusplus
 }

@@ -49,7 +49,7 @@ SIGNATURES = {
     "hep_transfer_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, vp, ctypes.c_int64, vp, vp, vp]),
     "hep_gate_topk": (ctypes.c_int, [vp, ctypes.c_int64, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int, vp, vp, vp, vp]),
     "hep_gemm_bf16": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp]),
-    "hep_moe_assign": (ctypes.c_int, [vp, ctypes.POINTER(HepSchedOut), vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]),
+    "hep_moe_assign": (ctypes.c_int, [vp, ctypes.POINTER(HepSchedOut), vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, ctypes.c_int, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]),
     "hep_moe_assign_workspace": (ctypes.c_size_t, [vp, ctypes.c_int64, ctypes.c_int]),
     "hep_moe_assign_ep": (ctypes.c_int, [vp, ctypes.POINTER(HepSchedOut), vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, ctypes.c_size_t, vp]),
     "hep_moe_assign_ep_workspace": (ctypes.c_size_t, [vp, ctypes.c_int64, ctypes.c_int]),
@@ -58,6 +58,13 @@ SIGNATURES = {
     "hep_moe_expert_ffn": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp, vp, vp, ctypes.c_size_t, vp, vp]),
     "hep_moe_ffn_workspace": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_int64, ctypes.c_int]),
     "hep_moe_combine": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, vp, vp]),
+    "hep_moe_gather_sum": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, vp, vp]),
+    "hep_moe_combine_bwd": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, vp, vp, vp]),
+    "hep_moe_zero_padding": (ctypes.c_int, [vp, vp, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int64, vp]),
+    "hep_moe_expert_ffn_bwd": (ctypes.c_int, [vp, vp, vp, vp, vp, vp, vp, ctypes.c_int, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp, vp, vp, vp, vp, ctypes.c_size_t, vp, vp]),
+    "hep_moe_expert_ffn_train": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp, vp, vp, vp, ctypes.c_size_t, vp, vp]),
+    "hep_gate_bwd": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, vp, vp]),
+    "hep_router_bwd": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp, vp, vp]),
 }
 
 _LIB = None

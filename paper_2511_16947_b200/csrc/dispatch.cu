@@ -71,40 +71,43 @@ static AssignWs carve_ws(const hep_sched *h, void *ws, int n_src, int64_t tps) {
 __global__ void plan_prep_kernel(int G, int E, int nnz, const int32_t *grp_off, const int32_t *grp_gpu,
                                  const int32_t *sorted, const int32_t *nnz_exp, const int64_t *xi,
                                  const int64_t *ranges, const int64_t *n_ranges_p, int64_t *expert_rows,
-                                 int32_t *seg, AssignWs w, int32_t *status) {
+                                 int32_t *seg, AssignWs w, int32_t *status, int row_align) {
     __shared__ int64_t scan[64];
     const int tid = threadIdx.x, nt = blockDim.x;
     const int64_t n_ranges = *n_ranges_p;
     for (int i = tid; i < E * G; i += nt) w.es_cnt[i] = 0;
     for (int i = tid; i <= E; i += nt) w.first[i] = -1;
-    // segments in [expert][dst asc] order = the scheduler's sorted arc order
-    const int chunk = (nnz + nt - 1) / nt;
-    const int p0 = min(nnz, tid * chunk), p1 = min(nnz, p0 + chunk);
+    // expert blocks ([expert][dst asc][src][rank]), each starting on a row_align boundary
+    // (64 in training so weight-gradient GEMMs contract over whole 64-row blocks)
+    const int chunk = (E + nt - 1) / nt;
+    const int e0 = min(E, tid * chunk), e1 = min(E, e0 + chunk);
     int64_t mine = 0;
-    for (int p = p0; p < p1; ++p) mine += xi[sorted[p]];
+    for (int e = e0; e < e1; ++e) {
+        int64_t n = 0;
+        for (int p = grp_off[e]; p < grp_off[e + 1]; ++p) n += xi[sorted[p]];
+        mine += (n + row_align - 1) / row_align * row_align;
+    }
     int64_t total;
     int64_t row = block_excl_scan_i64(mine, scan, &total);
-    for (int p = p0; p < p1; ++p) {
-        const int i = sorted[p];
-        const int e = nnz_exp[i];
-        seg[4 * p + 0] = (int32_t)row;
-        seg[4 * p + 1] = (int32_t)xi[i];
-        seg[4 * p + 2] = e;
-        seg[4 * p + 3] = grp_gpu[i];
-        w.row_base[i] = (int32_t)row;
-        if (p == grp_off[e]) expert_rows[e] = row;
-        row += xi[i];
+    for (int e = e0; e < e1; ++e) {
+        expert_rows[e] = row;
+        int64_t r = row;
+        for (int p = grp_off[e]; p < grp_off[e + 1]; ++p) {  // segments in the scheduler's sorted arc order
+            const int i = sorted[p];
+            seg[4 * p + 0] = (int32_t)r;
+            seg[4 * p + 1] = (int32_t)xi[i];
+            seg[4 * p + 2] = e;
+            seg[4 * p + 3] = grp_gpu[i];
+            w.row_base[i] = (int32_t)r;
+            r += xi[i];
+        }
+        row += (r - row + row_align - 1) / row_align * row_align;
     }
-    for (int e = tid; e < E; e += nt)
-        if (grp_off[e] == grp_off[e + 1]) expert_rows[e] = -1;  // fixed below
     if (tid == 0) {
         expert_rows[E] = total;
         if (total >= (int64_t)1 << 31) atomicCAS(status, 0, HEP_E_CAPACITY);
     }
     __syncthreads();
-    if (tid == 0)  // experts without replicas own an empty row range
-        for (int e = E - 1; e >= 0; --e)
-            if (expert_rows[e] < 0) expert_rows[e] = expert_rows[e + 1];
     for (int64_t r = tid; r < n_ranges; r += nt) {
         const int e = (int)ranges[4 * r];
         if (r == 0 || ranges[4 * (r - 1)] != e) w.first[e] = (int)r;
@@ -309,7 +312,7 @@ __global__ void __launch_bounds__(256) permute_kernel(const int4 *__restrict__ x
 template <int K>
 __global__ void __launch_bounds__(256) combine_kernel(const int4 *__restrict__ y, const int32_t *__restrict__ tok_row,
                                                       const float *__restrict__ topk_w, int64_t T, int64_t nvec,
-                                                      int4 *__restrict__ out) {
+                                                      int4 *__restrict__ out, const int4 *__restrict__ add) {
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -319,7 +322,7 @@ __global__ void __launch_bounds__(256) combine_kernel(const int4 *__restrict__ y
 #pragma unroll
         for (int k = 0; k < K; ++k) {
             src[k] = y + (int64_t)tok_row[t * K + k] * nvec;
-            wk[k] = topk_w[t * K + k];
+            wk[k] = topk_w ? topk_w[t * K + k] : 1.0f;  // unit weights: the permute's transpose
         }
         for (int64_t v0 = lane; v0 < nvec; v0 += 64) {
             int4 in[2][K];
@@ -334,6 +337,16 @@ __global__ void __launch_bounds__(256) combine_kernel(const int4 *__restrict__ y
                 float acc[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+                if (add) {  // e.g. the router's contribution to dx
+                    const int4 av = add[t * nvec + v0 + 32 * u];
+                    const __nv_bfloat162 *ah = reinterpret_cast<const __nv_bfloat162 *>(&av);
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const float2 f = __bfloat1622float2(ah[i]);
+                        acc[2 * i] = f.x;
+                        acc[2 * i + 1] = f.y;
+                    }
+                }
 #pragma unroll
                 for (int k = 0; k < K; ++k) {
                     const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&in[u][k]);
@@ -377,8 +390,10 @@ extern "C" size_t hep_moe_assign_workspace(hep_sched_t h, int64_t T, int K) {
 }
 
 extern "C" int hep_moe_assign(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_topk_idx, int64_t T, int K,
-                              int64_t tokens_per_src, int32_t *d_tok_row, int32_t *d_row_tok, int32_t *d_seg,
-                              int64_t *d_expert_rows, void *workspace, size_t workspace_bytes, void *stream) {
+                              int64_t tokens_per_src, int row_align, int32_t *d_tok_row, int32_t *d_row_tok,
+                              int32_t *d_seg, int64_t *d_expert_rows, void *workspace, size_t workspace_bytes,
+                              void *stream) {
+    HEP_REQUIRE(row_align >= 1 && row_align <= 1024, HEP_E_DIMENSION, "row_align=%d", row_align);
     HEP_REQUIRE(h && sched && d_topk_idx && d_tok_row && d_row_tok && d_seg && d_expert_rows && workspace,
                 HEP_E_CONTRACT, "hep_moe_assign: null argument");
     HEP_REQUIRE(K >= 1 && K <= 16 && tokens_per_src >= 1, HEP_E_DIMENSION, "hep_moe_assign: K=%d", K);
@@ -392,7 +407,7 @@ extern "C" int hep_moe_assign(hep_sched_t h, const hep_sched_out *sched, const i
     const int E = h->E, G = h->G;
     plan_prep_kernel<<<1, 512, 0, s>>>(G, E, h->nnz, h->d_grp_off, h->d_grp_gpu, h->d_sorted, h->d_nnz_exp,
                                        sched->d_xi, sched->d_ranges, sched->d_n_ranges, d_expert_rows, d_seg, w,
-                                       sched->d_status);
+                                       sched->d_status, row_align);
     HEP_CHECK_LAUNCH();
     if (T <= 0) return HEP_OK;
     const int ncs = (int)((tokens_per_src + kChunk - 1) / kChunk);
@@ -423,17 +438,23 @@ extern "C" int hep_moe_permute(const void *d_x, const int32_t *d_tok_row, int64_
 
 extern "C" int hep_moe_combine(const void *d_y, const int32_t *d_tok_row, const float *d_topk_w, int64_t T, int K,
                                int64_t d_model, void *d_out, void *stream) {
-    HEP_REQUIRE(d_y && d_tok_row && d_topk_w && d_out, HEP_E_CONTRACT, "hep_moe_combine: null pointer");
+    return hep_moe_gather_sum(d_y, d_tok_row, d_topk_w, nullptr, T, K, d_model, d_out, stream);
+}
+
+extern "C" int hep_moe_gather_sum(const void *d_y, const int32_t *d_tok_row, const float *d_topk_w, const void *d_add,
+                                  int64_t T, int K, int64_t d_model, void *d_out, void *stream) {
+    HEP_REQUIRE(d_y && d_tok_row && d_out, HEP_E_CONTRACT, "hep_moe_gather_sum: null pointer");
     HEP_REQUIRE(d_model % 8 == 0 && K >= 1 && K <= 16, HEP_E_DIMENSION, "hep_moe_combine: d_model %% 8, K<=16");
     if (T <= 0) return HEP_OK;
     const int grid = grid_for_warps(T);
     cudaStream_t st = (cudaStream_t)stream;
     const int4 *yv = (const int4 *)d_y;
     int4 *ov = (int4 *)d_out;
+    const int4 *av = (const int4 *)d_add;
     const int64_t nv = d_model / 8;
     switch (K) {
 #define HEP_COMBINE(KK) \
-        case KK: combine_kernel<KK><<<grid, 256, 0, st>>>(yv, d_tok_row, d_topk_w, T, nv, ov); break;
+        case KK: combine_kernel<KK><<<grid, 256, 0, st>>>(yv, d_tok_row, d_topk_w, T, nv, ov, av); break;
         HEP_COMBINE(1) HEP_COMBINE(2) HEP_COMBINE(3) HEP_COMBINE(4) HEP_COMBINE(5) HEP_COMBINE(6) HEP_COMBINE(7)
         HEP_COMBINE(8) HEP_COMBINE(9) HEP_COMBINE(10) HEP_COMBINE(11) HEP_COMBINE(12) HEP_COMBINE(13)
         HEP_COMBINE(14) HEP_COMBINE(15) HEP_COMBINE(16)
@@ -490,6 +511,138 @@ extern "C" int hep_moe_assign_ep(hep_sched_t h, const hep_sched_out *sched, cons
     if (sm > 48 * 1024)
         HEP_CHECK_CUDA(cudaFuncSetAttribute(chunk_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     chunk_map_kernel<<<ncs, 32, sm, s>>>(d_topk_idx, K, E, G, tps, T, ncs, w.chunk_cnt, w, d_tok_row, nullptr, rank);
+    HEP_CHECK_LAUNCH();
+    return HEP_OK;
+}
+
+// ===========================================================================
+// Backward data-path kernels
+// ===========================================================================
+namespace hep {
+
+// K7^T: dY[row(t,k)] = w[t,k] * dout[t] (bf16 rows), dw[t,k] = <dout[t], Y[row(t,k)]> (fp32).
+// One warp per token; the dot products reduce with shuffles in a fixed order.
+template <int K>
+__global__ void __launch_bounds__(256) combine_bwd_kernel(const int4 *__restrict__ dout, const int4 *__restrict__ y,
+                                                          const int32_t *__restrict__ tok_row,
+                                                          const float *__restrict__ topk_w, int64_t T, int64_t nvec,
+                                                          int4 *__restrict__ dy, float *__restrict__ dw) {
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = warp; t < T; t += nwarps) {
+        int32_t r[K];
+        float wk[K], dot[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            r[k] = tok_row[t * K + k];
+            wk[k] = topk_w[t * K + k];
+            dot[k] = 0.f;
+        }
+        for (int64_t v = lane; v < nvec; v += 32) {
+            const int4 g = __ldg(dout + t * nvec + v);
+            const __nv_bfloat162 *gh = reinterpret_cast<const __nv_bfloat162 *>(&g);
+            float gf[8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const float2 f = __bfloat1622float2(gh[i]);
+                gf[2 * i] = f.x;
+                gf[2 * i + 1] = f.y;
+            }
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const int4 yv = __ldg(y + (int64_t)r[k] * nvec + v);
+                const __nv_bfloat162 *yh = reinterpret_cast<const __nv_bfloat162 *>(&yv);
+                int4 o;
+                __nv_bfloat162 *oh = reinterpret_cast<__nv_bfloat162 *>(&o);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float2 f = __bfloat1622float2(yh[i]);
+                    dot[k] = fmaf(gf[2 * i], f.x, dot[k]);
+                    dot[k] = fmaf(gf[2 * i + 1], f.y, dot[k]);
+                    oh[i] = __floats2bfloat162_rn(wk[k] * gf[2 * i], wk[k] * gf[2 * i + 1]);
+                }
+                dy[(int64_t)r[k] * nvec + v] = o;
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            float v = dot[k];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) dw[t * K + k] = v;
+        }
+    }
+}
+
+// zero the alignment padding rows of each expert block: [start + n_e, next start)
+__global__ void zero_pad_rows_kernel(const int64_t *expert_rows, const int32_t *seg, int n_seg, int E, int64_t nvec,
+                                     int4 *buf) {
+    const int e = blockIdx.x;
+    if (e >= E) return;
+    int64_t n = 0;
+    for (int s = 0; s < n_seg; ++s)
+        if (seg[4 * s + 2] == e) n += seg[4 * s + 1];
+    const int64_t r0 = expert_rows[e] + n, r1 = expert_rows[e + 1];
+    const int4 z = make_int4(0, 0, 0, 0);
+    for (int64_t i = (int64_t)threadIdx.x; i < (r1 - r0) * nvec; i += blockDim.x) buf[r0 * nvec + i] = z;
+}
+
+// router backward: weights w = softmax(selected logits), so
+// dlogit[t, idx_k] = w_k (dw_k - sum_j w_j dw_j); other columns 0.  bf16 [T][ld] out.
+__global__ void gate_bwd_kernel(const int32_t *topk_idx, const float *topk_w, const float *dw, int64_t T, int K,
+                                int64_t ld, __nv_bfloat16 *dlogits) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= T) return;
+    __nv_bfloat16 *row = dlogits + t * ld;
+    for (int64_t c = 0; c < ld; ++c) row[c] = __float2bfloat16(0.f);
+    float s = 0.f;
+    for (int k = 0; k < K; ++k) s += topk_w[t * K + k] * dw[t * K + k];
+    for (int k = 0; k < K; ++k) {
+        const float w = topk_w[t * K + k];
+        row[topk_idx[t * K + k]] = __float2bfloat16(w * (dw[t * K + k] - s));
+    }
+}
+
+}  // namespace hep
+
+extern "C" int hep_moe_combine_bwd(const void *d_dout, const void *d_y, const int32_t *d_tok_row, const float *d_topk_w,
+                                   int64_t T, int K, int64_t d_model, void *d_dy, float *d_dw, void *stream) {
+    HEP_REQUIRE(d_dout && d_y && d_tok_row && d_topk_w && d_dy && d_dw, HEP_E_CONTRACT, "hep_moe_combine_bwd: null");
+    HEP_REQUIRE(d_model % 8 == 0 && K >= 1 && K <= 16, HEP_E_DIMENSION, "hep_moe_combine_bwd: d_model %% 8, K<=16");
+    if (T <= 0) return HEP_OK;
+    const int grid = grid_for_warps(T);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t nv = d_model / 8;
+    switch (K) {
+#define HEP_CB(KK)                                                                                                 \
+        case KK:                                                                                                   \
+            combine_bwd_kernel<KK><<<grid, 256, 0, st>>>((const int4 *)d_dout, (const int4 *)d_y, d_tok_row,       \
+                                                         d_topk_w, T, nv, (int4 *)d_dy, d_dw);                     \
+            break;
+        HEP_CB(1) HEP_CB(2) HEP_CB(3) HEP_CB(4) HEP_CB(5) HEP_CB(6) HEP_CB(7) HEP_CB(8)
+        HEP_CB(9) HEP_CB(10) HEP_CB(11) HEP_CB(12) HEP_CB(13) HEP_CB(14) HEP_CB(15) HEP_CB(16)
+#undef HEP_CB
+    }
+    HEP_CHECK_LAUNCH();
+    return HEP_OK;
+}
+
+extern "C" int hep_moe_zero_padding(const int64_t *d_expert_rows, const int32_t *d_seg, int n_seg, int E, void *d_buf,
+                                    int64_t width, void *stream) {
+    HEP_REQUIRE(d_expert_rows && d_seg && d_buf && width % 8 == 0, HEP_E_CONTRACT, "hep_moe_zero_padding");
+    if (E <= 0) return HEP_OK;
+    zero_pad_rows_kernel<<<E, 256, 0, (cudaStream_t)stream>>>(d_expert_rows, d_seg, n_seg, E, width / 8, (int4 *)d_buf);
+    HEP_CHECK_LAUNCH();
+    return HEP_OK;
+}
+
+extern "C" int hep_gate_bwd(const int32_t *d_topk_idx, const float *d_topk_w, const float *d_dw, int64_t T, int K,
+                            int64_t ld, void *d_dlogits, void *stream) {
+    HEP_REQUIRE(d_topk_idx && d_topk_w && d_dw && d_dlogits && K >= 1 && K <= ld, HEP_E_CONTRACT, "hep_gate_bwd");
+    if (T <= 0) return HEP_OK;
+    gate_bwd_kernel<<<(unsigned)((T + 255) / 256), 256, 0, (cudaStream_t)stream>>>(d_topk_idx, d_topk_w, d_dw, T, K, ld,
+                                                                                   (__nv_bfloat16 *)d_dlogits);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
 }

@@ -31,10 +31,10 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle atom row
 constexpr int kThreads = 192;
 
-enum Epi { EPI_SWIGLU = 0, EPI_BF16 = 1, EPI_F32 = 2 };
+enum Epi { EPI_SWIGLU = 0, EPI_BF16 = 1, EPI_F32 = 2, EPI_SWIGLU_BWD = 3 };
 
 struct Params {
-    int grouped;             // 0: dense M rows; 1: m-tile list
+    int grouped;             // 0: dense M rows; 1: m-tile list; 2: per-expert K-ragged (weight gradients)
     int64_t M;               // dense rows
     int n_tiles;             // N / BN
     int kblocks;             // K / 64
@@ -46,6 +46,14 @@ struct Params {
     void *out;
     int64_t ld_out;          // elements per output row
     int64_t out_cols;        // valid output columns (EPI_F32 masking)
+    // mode 2 (weight gradients): expert e contracts over rows [exp_rows[e], exp_rows[e+1])
+    // (64-row padded blocks), output tile grid m_tiles x n_tiles per expert
+    const int64_t *exp_rows;
+    int m_tiles;
+    int64_t out_exp_stride;  // elements between consecutive experts' outputs
+    // EPI_SWIGLU: optional pre-activation store; EPI_SWIGLU_BWD: pre-activation input
+    void *aux;
+    int64_t ld_aux;
 };
 
 template <int BN, int STAGES>
@@ -60,16 +68,33 @@ struct Smem {
 struct Tile {
     int expert, n_blk;
     int32_t row0, rows;
+    int64_t k0;  // first contraction row (mode 2)
+    int kb;      // contraction blocks of 64
 };
 
 __device__ __forceinline__ int64_t total_tiles(const Params &p) {
-    if (!p.grouped) return ((p.M + BM - 1) / BM) * p.n_tiles;
+    if (p.grouped == 0) return ((p.M + BM - 1) / BM) * p.n_tiles;
+    if (p.grouped == 2) return (int64_t)p.n_exp * p.m_tiles * p.n_tiles;
     return (int64_t)p.exp_mt_off[p.n_exp] * p.n_tiles;
 }
 
 __device__ __forceinline__ Tile decode(const Params &p, int64_t t) {
     Tile tl;
-    if (!p.grouped) {
+    tl.k0 = 0;
+    tl.kb = p.kblocks;
+    if (p.grouped == 2) {
+        const int64_t per = (int64_t)p.m_tiles * p.n_tiles;
+        const int e = (int)(t / per);
+        const int64_t rem = t - (int64_t)e * per;
+        tl.expert = e;
+        tl.n_blk = (int)(rem / p.m_tiles);
+        tl.row0 = (int32_t)((rem % p.m_tiles) * BM);
+        tl.rows = (int32_t)(p.M - tl.row0 < BM ? p.M - tl.row0 : BM);
+        tl.k0 = p.exp_rows[e];
+        tl.kb = (int)((p.exp_rows[e + 1] - tl.k0) / BK);
+        return tl;
+    }
+    if (p.grouped == 0) {
         const int64_t mt = (p.M + BM - 1) / BM;
         tl.expert = 0;
         tl.n_blk = (int)(t / mt);
@@ -107,10 +132,51 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 // Epilogue of one accumulator tile row (this thread's TMEM lane): TMEM ->
 // registers -> fused op -> global.  t_row = TMEM address of the row's first
 // column, grow = global output row.
+__device__ __forceinline__ float sigmoid(float x) { return 1.0f / (1.0f + __expf(-x)); }
+
+__device__ __forceinline__ float bf16lo(uint32_t v) { return __uint_as_float(v << 16); }
+__device__ __forceinline__ float bf16hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
+
 template <int BN, int EPI>
 __device__ __forceinline__ void store_tile(const Params &p, uint32_t t_row, int64_t grow, bool valid, int n_blk,
-                                           uint64_t pol_out) {
-    if constexpr (EPI == EPI_SWIGLU) {
+                                           uint64_t pol_out, int expert = 0, bool zero = false) {
+    if constexpr (EPI == EPI_SWIGLU_BWD) {
+        // accumulator = dH for ffn columns [n_blk*BN, +BN); the pre-activations
+        // (gate a, up b) live in aux with the W13 interleave (128-blocks: gate j, up j).
+        // dA_gate = dH * b * silu'(a), dA_up = dH * silu(a); written in the same interleave.
+        const __nv_bfloat16 *pre = reinterpret_cast<const __nv_bfloat16 *>(p.aux) + grow * p.ld_aux;
+        __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(p.out) + grow * p.ld_out;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 16) {
+            uint32_t v[16];
+            tmem_ld16(t_row + c, v);
+            tmem_ld_wait();
+            if (!valid) continue;
+            const int64_t f = (int64_t)n_blk * BN + c;       // first ffn column of this chunk
+            const int64_t gcol = (f / 128) * 256 + (f % 128);  // gate column; up = gcol + 128
+            const uint4 *ga = reinterpret_cast<const uint4 *>(pre + gcol);
+            const uint4 *ua = reinterpret_cast<const uint4 *>(pre + gcol + 128);
+            uint32_t gw[8], uw[8];
+            *reinterpret_cast<uint4 *>(gw) = ga[0];
+            *reinterpret_cast<uint4 *>(gw + 4) = ga[1];
+            *reinterpret_cast<uint4 *>(uw) = ua[0];
+            *reinterpret_cast<uint4 *>(uw + 4) = ua[1];
+            uint32_t dg[8], du[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                float d0 = __uint_as_float(v[2 * i]), d1 = __uint_as_float(v[2 * i + 1]);
+                float a0 = bf16lo(gw[i]), a1 = bf16hi(gw[i]), b0 = bf16lo(uw[i]), b1 = bf16hi(uw[i]);
+                float s0 = sigmoid(a0), s1 = sigmoid(a1);
+                float ds0 = s0 * (1.0f + a0 * (1.0f - s0)), ds1 = s1 * (1.0f + a1 * (1.0f - s1));
+                dg[i] = pack_bf16(d0 * b0 * ds0, d1 * b1 * ds1);
+                du[i] = pack_bf16(d0 * a0 * s0, d1 * a1 * s1);
+            }
+            st_global_v4_hint(out + gcol, make_uint4(dg[0], dg[1], dg[2], dg[3]), pol_out);
+            st_global_v4_hint(out + gcol + 8, make_uint4(dg[4], dg[5], dg[6], dg[7]), pol_out);
+            st_global_v4_hint(out + gcol + 128, make_uint4(du[0], du[1], du[2], du[3]), pol_out);
+            st_global_v4_hint(out + gcol + 136, make_uint4(du[4], du[5], du[6], du[7]), pol_out);
+        }
+    } else if constexpr (EPI == EPI_SWIGLU) {
         // columns [0, BN/2) = gate (W1 block), [BN/2, BN) = up (W3 block)
         __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(p.out) + grow * p.ld_out +
                              (int64_t)n_blk * (BN / 2);
@@ -126,6 +192,19 @@ __device__ __forceinline__ void store_tile(const Params &p, uint32_t t_row, int6
                 float g0 = __uint_as_float(g[2 * i]), g1 = __uint_as_float(g[2 * i + 1]);
                 float u0 = __uint_as_float(u[2 * i]), u1 = __uint_as_float(u[2 * i + 1]);
                 packed[i] = pack_bf16(silu(g0) * u0, silu(g1) * u1);
+            }
+            if (valid && p.aux) {  // training: keep the pre-activations for the backward pass
+                __nv_bfloat16 *pre = reinterpret_cast<__nv_bfloat16 *>(p.aux) + grow * p.ld_aux + (int64_t)n_blk * BN + c;
+                uint32_t pg[8], pu[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    pg[i] = pack_bf16(__uint_as_float(g[2 * i]), __uint_as_float(g[2 * i + 1]));
+                    pu[i] = pack_bf16(__uint_as_float(u[2 * i]), __uint_as_float(u[2 * i + 1]));
+                }
+                st_global_v4_hint(pre, make_uint4(pg[0], pg[1], pg[2], pg[3]), pol_out);
+                st_global_v4_hint(pre + 8, make_uint4(pg[4], pg[5], pg[6], pg[7]), pol_out);
+                st_global_v4_hint(pre + BN / 2, make_uint4(pu[0], pu[1], pu[2], pu[3]), pol_out);
+                st_global_v4_hint(pre + BN / 2 + 8, make_uint4(pu[4], pu[5], pu[6], pu[7]), pol_out);
             }
             if (valid) {
                 st_global_v4_hint(out + c, make_uint4(packed[0], packed[1], packed[2], packed[3]), pol_out);
@@ -150,13 +229,17 @@ __device__ __forceinline__ void store_tile(const Params &p, uint32_t t_row, int6
             }
         }
     } else {
-        float *out = reinterpret_cast<float *>(p.out) + grow * p.ld_out + (int64_t)n_blk * BN;
+        float *out = reinterpret_cast<float *>(p.out) + (int64_t)expert * p.out_exp_stride + grow * p.ld_out +
+                     (int64_t)n_blk * BN;
         const int64_t col0 = (int64_t)n_blk * BN;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 16) {
             uint32_t v[16];
             tmem_ld16(t_row + c, v);
             tmem_ld_wait();
+            if (zero)  // empty contraction (expert without rows): the accumulator was never written
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] = 0u;
             if (valid) {
                 if (col0 + c + 16 <= p.out_cols) {
                     float4 *dst = reinterpret_cast<float4 *>(out + c);
@@ -174,7 +257,13 @@ __device__ __forceinline__ void store_tile(const Params &p, uint32_t t_row, int6
     }
 }
 
-template <int BN, int STAGES, int EPI>
+// A_MN / B_MN: operand stored MN-major in global memory (the contraction index
+// is the row index, e.g. activations [rows][d] contracted over rows for weight
+// gradients, or weights [K][N] used untransposed).  Such an operand is staged as
+// (extent/64) TMA boxes of 64(MN) x 64(K) — 128-byte rows along MN, k-groups of
+// 8 rows 1024 B apart (SBO), MN blocks 8 KB apart (LBO) — and each 16-deep MMA
+// step advances 2 KB.
+template <int BN, int STAGES, int EPI, bool A_MN = false, bool B_MN = false>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params p) {
     using S = Smem<BN, STAGES>;
@@ -225,11 +314,29 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int64_t t = blockIdx.x; t < n_total; t += gridDim.x) {
                 const Tile tl = decode(p, t);
                 const int32_t b_row = (int32_t)(tl.expert * p.b_rows_per_exp + (int64_t)tl.n_blk * BN);
-                for (int k = 0; k < kb; ++k) {
+                // contraction offsets: mode 2 contracts over the expert's rows; an MN-major
+                // weight (mode 1) is [K][N] per expert, stacked along K
+                const int32_t a_k0 = (int32_t)tl.k0;
+                const int32_t b_k0 = p.grouped == 2 ? (int32_t)tl.k0 : (B_MN ? b_row - tl.n_blk * BN : 0);
+                for (int k = 0; k < tl.kb; ++k) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
-                    tma_load_2d_hint(sA + stage * S::A_BYTES, &tmA, &full[stage], k * BK, tl.row0, pol_a);
-                    tma_load_2d_hint(sB + stage * S::B_BYTES, &tmB, &full[stage], k * BK, b_row, pol_b);
+                    if constexpr (A_MN) {
+#pragma unroll
+                        for (int i = 0; i < BM / 64; ++i)
+                            tma_load_2d_hint(sA + stage * S::A_BYTES + i * 8192, &tmA, &full[stage], tl.row0 + 64 * i,
+                                             a_k0 + k * BK, pol_a);
+                    } else {
+                        tma_load_2d_hint(sA + stage * S::A_BYTES, &tmA, &full[stage], a_k0 + k * BK, tl.row0, pol_a);
+                    }
+                    if constexpr (B_MN) {
+#pragma unroll
+                        for (int i = 0; i < BN / 64; ++i)
+                            tma_load_2d_hint(sB + stage * S::B_BYTES + i * 8192, &tmB, &full[stage],
+                                             tl.n_blk * BN + 64 * i, b_k0 + k * BK, pol_b);
+                    } else {
+                        tma_load_2d_hint(sB + stage * S::B_BYTES, &tmB, &full[stage], k * BK, b_row, pol_b);
+                    }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -237,24 +344,25 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         if (lane == 0) {
             // ===================== MMA issuer =====================
-            constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+            constexpr uint32_t idesc = idesc_bf16_f32(BM, BN) | (A_MN ? (1u << 15) : 0u) | (B_MN ? (1u << 16) : 0u);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int64_t t = blockIdx.x; t < n_total; t += gridDim.x) {
+                const int tkb = p.grouped == 2 ? decode(p, t).kb : kb;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
-                for (int k = 0; k < kb; ++k) {
+                for (int k = 0; k < tkb; ++k) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(sA + stage * S::A_BYTES);
                     const uint32_t b_addr = smem_u32(sB + stage * S::B_BYTES);
 #pragma unroll
                     for (int kk = 0; kk < BK / 16; ++kk) {
-                        const uint64_t ad = desc_kmajor_sw128(a_addr + kk * 32);
-                        const uint64_t bd = desc_kmajor_sw128(b_addr + kk * 32);
+                        const uint64_t ad = A_MN ? desc_mnmajor_sw128(a_addr + kk * 2048) : desc_kmajor_sw128(a_addr + kk * 32);
+                        const uint64_t bd = B_MN ? desc_mnmajor_sw128(b_addr + kk * 2048) : desc_kmajor_sw128(b_addr + kk * 32);
                         mma_bf16(d_tmem, ad, bd, idesc, (k | kk) ? 1u : 0u);
                     }
                     mma_commit(&empty[stage]);  // frees the smem slot when these MMAs finish
@@ -278,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
             const bool valid = row_in_tile < tl.rows;
             const int64_t grow = (int64_t)tl.row0 + row_in_tile;
-            store_tile<BN, EPI>(p, t_row, grow, valid, tl.n_blk, pol_out);
+            store_tile<BN, EPI>(p, t_row, grow, valid, tl.n_blk, pol_out, tl.expert, tl.kb == 0);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -540,6 +648,37 @@ static int sm_count() {
     return n;
 }
 
+// MN-major operand: global [k_rows][mn_cols] bf16 (mn contiguous), 64 x 64 boxes
+static int make_tmap_mn(CUtensorMap *m, const void *ptr, uint64_t k_rows, uint64_t mn_cols) {
+    auto fn = encode_fn();
+    HEP_REQUIRE(fn, HEP_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    HEP_REQUIRE(((uintptr_t)ptr & 15) == 0 && (mn_cols * 2) % 16 == 0, HEP_E_CONTRACT,
+                "TMA needs 16-byte aligned base and row pitch");
+    cuuint64_t dims[2] = {mn_cols, k_rows};
+    cuuint64_t strides[1] = {mn_cols * 2};
+    cuuint32_t box[2] = {64, 64};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(ptr), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    HEP_REQUIRE(r == CUDA_SUCCESS, HEP_E_CUDA, "cuTensorMapEncodeTiled (MN-major) failed (%d)", (int)r);
+    return HEP_OK;
+}
+
+template <int BN, int STAGES, int EPI, bool A_MN, bool B_MN>
+static int launch_maps(const CUtensorMap &ta, const CUtensorMap &tb, const Params &p, int64_t max_tiles,
+                       cudaStream_t stream) {
+    using S = Smem<BN, STAGES>;
+    auto kern = gemm_kernel<BN, STAGES, EPI, A_MN, B_MN>;
+    HEP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES));
+    int grid = sm_count();
+    if (max_tiles > 0 && max_tiles < grid) grid = (int)max_tiles;
+    if (grid < 1) grid = 1;
+    kern<<<grid, kThreads, S::BYTES, stream>>>(ta, tb, p);
+    HEP_CHECK_LAUNCH();
+    return HEP_OK;
+}
+
 template <int BN, int STAGES, int EPI>
 static int launch(const void *A, int64_t a_rows, int64_t K, const void *B, int64_t b_rows, const Params &p,
                   int64_t max_tiles, cudaStream_t stream) {
@@ -628,10 +767,30 @@ extern "C" size_t hep_moe_ffn_workspace(int n_seg, int64_t R, int n_experts) {
     return (size_t)(2 * cap + n_experts + 1 + 1) * sizeof(int32_t) + 64;
 }
 
+static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg, int n_seg,
+                          int64_t R, int64_t d_model, int64_t ffn, int n_experts, void *d_h, void *d_y, void *d_pre,
+                          void *d_workspace, size_t workspace_bytes, int32_t *d_status, void *stream);
+
 extern "C" int hep_moe_expert_ffn(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg,
                                   int n_seg, int64_t R, int64_t d_model, int64_t ffn, int n_experts, void *d_h,
                                   void *d_y, void *d_workspace, size_t workspace_bytes, int32_t *d_status,
                                   void *stream) {
+    return expert_ffn_fwd(d_rows, d_w13, d_w2, d_seg, n_seg, R, d_model, ffn, n_experts, d_h, d_y, nullptr,
+                          d_workspace, workspace_bytes, d_status, stream);
+}
+
+extern "C" int hep_moe_expert_ffn_train(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg,
+                                        int n_seg, int64_t R, int64_t d_model, int64_t ffn, int n_experts, void *d_h,
+                                        void *d_y, void *d_pre, void *d_workspace, size_t workspace_bytes,
+                                        int32_t *d_status, void *stream) {
+    HEP_REQUIRE(d_pre, HEP_E_CONTRACT, "hep_moe_expert_ffn_train: d_pre required");
+    return expert_ffn_fwd(d_rows, d_w13, d_w2, d_seg, n_seg, R, d_model, ffn, n_experts, d_h, d_y, d_pre, d_workspace,
+                          workspace_bytes, d_status, stream);
+}
+
+static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg, int n_seg,
+                          int64_t R, int64_t d_model, int64_t ffn, int n_experts, void *d_h, void *d_y, void *d_pre,
+                          void *d_workspace, size_t workspace_bytes, int32_t *d_status, void *stream) {
     HEP_REQUIRE(d_rows && d_w13 && d_w2 && d_seg && d_h && d_y && d_workspace, HEP_E_CONTRACT,
                 "hep_moe_expert_ffn: null pointer");
     HEP_REQUIRE(d_model % 256 == 0 && ffn % 128 == 0 && d_model % BK == 0, HEP_E_DIMENSION,
@@ -661,10 +820,13 @@ extern "C" int hep_moe_expert_ffn(const void *d_rows, const void *d_w13, const v
     p.out = d_h;
     p.ld_out = ffn;
     p.out_cols = ffn;
+    p.aux = d_pre;  // training: store the pre-activations A13 (W13 interleave)
+    p.ld_aux = 2 * ffn;
     int rc = pairs ? launch2sm<6, EPI_SWIGLU>(d_rows, R, d_model, d_w13, (int64_t)n_experts * 2 * ffn, p, s)
                    : launch<256, 4, EPI_SWIGLU>(d_rows, R, d_model, d_w13, (int64_t)n_experts * 2 * ffn, p, 0, s);
     if (rc) return rc;
     // GEMM 2: Y = H W2^T, B = W2 [E][d][F]
+    p.aux = nullptr;
     p.kblocks = (int)(ffn / BK);
     p.n_tiles = (int)(d_model / 256);
     p.b_rows_per_exp = d_model;
@@ -673,4 +835,128 @@ extern "C" int hep_moe_expert_ffn(const void *d_rows, const void *d_w13, const v
     p.out_cols = d_model;
     return pairs ? launch2sm<6, EPI_BF16>(d_h, R, ffn, d_w2, (int64_t)n_experts * d_model, p, s)
                  : launch<256, 4, EPI_BF16>(d_h, R, ffn, d_w2, (int64_t)n_experts * d_model, p, 0, s);
+}
+
+// ===========================================================================
+// Backward of the expert FFN (training).  Layout as in the forward; the receive
+// rows are in 64-row aligned expert blocks (hep_moe_assign row_align = 64) and
+// the forward kept the pre-activations A13 = [x W1^T | x W3^T] (W13 interleave).
+//   dA13    = swiglu'(A13) * (dY W2)      dgrad GEMM, W2 MN-major, fused epilogue
+//   dX_rows = dA13 W13                    dgrad GEMM, W13 MN-major
+//   dW2_e   = dY_e^T H_e                  wgrad GEMM, both operands MN-major, K = the
+//   dW13_e  = dA13_e^T X_e                expert's rows (K-ragged per expert)
+// ===========================================================================
+extern "C" int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, const void *d_h, void *d_dy,
+                                      const void *d_w13, const void *d_w2, const int32_t *d_seg, int n_seg,
+                                      const int64_t *d_expert_rows, int64_t Rcap, int64_t d_model, int64_t ffn,
+                                      int n_experts, void *d_da13, void *d_dx_rows, float *d_dw13, float *d_dw2,
+                                      void *d_workspace, size_t workspace_bytes, int32_t *d_status, void *stream) {
+    HEP_REQUIRE(d_rows && d_pre && d_h && d_dy && d_w13 && d_w2 && d_seg && d_expert_rows && d_da13 && d_dx_rows &&
+                    d_dw13 && d_dw2 && d_workspace,
+                HEP_E_CONTRACT, "hep_moe_expert_ffn_bwd: null pointer");
+    HEP_REQUIRE(d_model % 256 == 0 && ffn % 256 == 0, HEP_E_DIMENSION,
+                "FFN backward needs d_model %% 256 == 0 and ffn %% 256 == 0");
+    HEP_REQUIRE(workspace_bytes >= hep_moe_ffn_workspace(n_seg, Rcap, n_experts), HEP_E_CAPACITY, "workspace too small");
+    if (Rcap <= 0) return HEP_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    int rc = hep_moe_zero_padding(d_expert_rows, d_seg, n_seg, n_experts, d_dy, d_model, stream);
+    if (rc) return rc;
+    const int64_t cap = Rcap / BM + n_seg + 1;
+    int32_t *mt_row0 = reinterpret_cast<int32_t *>(d_workspace);
+    int32_t *mt_rows = mt_row0 + cap;
+    int32_t *exp_off = mt_rows + cap;
+    build_tiles_kernel<<<1, 1024, 0, s>>>(d_seg, n_seg, n_experts, mt_row0, mt_rows, exp_off, cap, d_status, BM);
+    HEP_CHECK_LAUNCH();
+    CUtensorMap ta, tb;
+    Params p{};
+    // --- dA13 = swiglu'(A13) * (dY W2)
+    p.grouped = 1;
+    p.mt_row0 = mt_row0;
+    p.mt_rows = mt_rows;
+    p.exp_mt_off = exp_off;
+    p.n_exp = n_experts;
+    p.kblocks = (int)(d_model / BK);
+    p.n_tiles = (int)(ffn / 256);
+    p.b_rows_per_exp = d_model;  // W2[e] is [d][F]: K rows per expert
+    p.out = d_da13;
+    p.ld_out = 2 * ffn;
+    p.out_cols = 2 * ffn;
+    p.aux = const_cast<void *>(d_pre);
+    p.ld_aux = 2 * ffn;
+    if ((rc = make_tmap(&ta, d_dy, (uint64_t)Rcap, (uint64_t)d_model, BM))) return rc;
+    if ((rc = make_tmap_mn(&tb, d_w2, (uint64_t)n_experts * d_model, (uint64_t)ffn))) return rc;
+    if ((rc = launch_maps<256, 4, EPI_SWIGLU_BWD, false, true>(ta, tb, p, 0, s))) return rc;
+    if ((rc = hep_moe_zero_padding(d_expert_rows, d_seg, n_seg, n_experts, d_da13, 2 * ffn, stream))) return rc;
+    // --- dX_rows = dA13 W13
+    p.kblocks = (int)(2 * ffn / BK);
+    p.n_tiles = (int)(d_model / 256);
+    p.b_rows_per_exp = 2 * ffn;  // W13[e] is [2F][d]
+    p.out = d_dx_rows;
+    p.ld_out = d_model;
+    p.out_cols = d_model;
+    p.aux = nullptr;
+    if ((rc = make_tmap(&ta, d_da13, (uint64_t)Rcap, (uint64_t)(2 * ffn), BM))) return rc;
+    if ((rc = make_tmap_mn(&tb, d_w13, (uint64_t)n_experts * 2 * ffn, (uint64_t)d_model))) return rc;
+    if ((rc = launch_maps<256, 4, EPI_BF16, false, true>(ta, tb, p, 0, s))) return rc;
+    // --- dW2_e = dY_e^T H_e   (fp32, [E][d][F])
+    Params q{};
+    q.grouped = 2;
+    q.exp_rows = d_expert_rows;
+    q.n_exp = n_experts;
+    q.M = d_model;
+    q.m_tiles = (int)(d_model / BM);
+    q.n_tiles = (int)(ffn / 256);
+    q.out = d_dw2;
+    q.ld_out = ffn;
+    q.out_cols = ffn;
+    q.out_exp_stride = d_model * ffn;
+    if ((rc = make_tmap_mn(&ta, d_dy, (uint64_t)Rcap, (uint64_t)d_model))) return rc;
+    if ((rc = make_tmap_mn(&tb, d_h, (uint64_t)Rcap, (uint64_t)ffn))) return rc;
+    if ((rc = launch_maps<256, 4, EPI_F32, true, true>(ta, tb, q, 0, s))) return rc;
+    // --- dW13_e = dA13_e^T X_e  (fp32, [E][2F][d], W13 interleave)
+    q.M = 2 * ffn;
+    q.m_tiles = (int)(2 * ffn / BM);
+    q.n_tiles = (int)(d_model / 256);
+    q.out = d_dw13;
+    q.ld_out = d_model;
+    q.out_cols = d_model;
+    q.out_exp_stride = 2 * ffn * d_model;
+    if ((rc = make_tmap_mn(&ta, d_da13, (uint64_t)Rcap, (uint64_t)(2 * ffn)))) return rc;
+    if ((rc = make_tmap_mn(&tb, d_rows, (uint64_t)Rcap, (uint64_t)d_model))) return rc;
+    return launch_maps<256, 4, EPI_F32, true, true>(ta, tb, q, 0, s);
+}
+
+// Router backward: dWg = dlogits^T x (fp32 [E64][d]) and dx_gate = dlogits Wg (bf16 [T][d]);
+// dlogits is bf16 [T][E64], Wg is [E64][d] (E64 = experts padded to 64), T % 64 == 0.
+extern "C" int hep_router_bwd(const void *d_x, const void *d_wg, const void *d_dlogits, int64_t T, int64_t d_model,
+                              int E64, float *d_dwg, void *d_dxg, void *stream) {
+    HEP_REQUIRE(d_x && d_wg && d_dlogits && d_dwg && d_dxg, HEP_E_CONTRACT, "hep_router_bwd: null pointer");
+    HEP_REQUIRE(T % 64 == 0 && E64 % 64 == 0 && d_model % 256 == 0, HEP_E_DIMENSION,
+                "hep_router_bwd: T %% 64, E64 %% 64, d %% 256");
+    if (T <= 0) return HEP_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    CUtensorMap ta, tb;
+    int rc;
+    Params p{};
+    p.grouped = 0;
+    p.M = E64;
+    p.kblocks = (int)(T / BK);
+    p.n_tiles = (int)(d_model / 256);
+    p.out = d_dwg;
+    p.ld_out = d_model;
+    p.out_cols = d_model;
+    if ((rc = make_tmap_mn(&ta, d_dlogits, (uint64_t)T, (uint64_t)E64))) return rc;
+    if ((rc = make_tmap_mn(&tb, d_x, (uint64_t)T, (uint64_t)d_model))) return rc;
+    if ((rc = launch_maps<256, 4, EPI_F32, true, true>(ta, tb, p, (E64 + BM - 1) / BM * p.n_tiles, s))) return rc;
+    Params q{};
+    q.grouped = 0;
+    q.M = T;
+    q.kblocks = E64 / BK;
+    q.n_tiles = (int)(d_model / 256);
+    q.out = d_dxg;
+    q.ld_out = d_model;
+    q.out_cols = d_model;
+    if ((rc = make_tmap(&ta, d_dlogits, (uint64_t)T, (uint64_t)E64, BM))) return rc;
+    if ((rc = make_tmap_mn(&tb, d_wg, (uint64_t)E64, (uint64_t)d_model))) return rc;
+    return launch_maps<256, 4, EPI_BF16, false, true>(ta, tb, q, (T + BM - 1) / BM * q.n_tiles, s);
 }

@@ -135,6 +135,17 @@ __device__ __forceinline__ uint64_t desc_kmajor_sw128(uint32_t smem_addr) {
     d |= (uint64_t)2 << 61;                        // SWIZZLE_128B
     return d;
 }
+// MN-major operand, 128-byte swizzle: 64-element (128 B) rows along MN, K-groups
+// of 8 rows 1024 B apart (SBO), 64-wide MN blocks 8 KB apart (LBO).
+__device__ __forceinline__ uint64_t desc_mnmajor_sw128(uint32_t smem_addr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);
+    d |= (uint64_t)(8192 >> 4) << 16;  // LBO: next 64-wide MN block
+    d |= (uint64_t)(1024 >> 4) << 32;  // SBO: next 8-row K group
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)2 << 61;
+    return d;
+}
 // Instruction descriptor: kind::f16, A=B=bf16, D=f32, both K-major, MxN.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
     return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);

@@ -66,10 +66,17 @@ class MoEBuffers:
     """All device buffers of one micro-batch shape, allocated once (the hot
     path allocates nothing; CUDA-graph capturable)."""
 
-    def __init__(self, sched: DeviceScheduler, T: int, K: int, E: int, e_pad: int, d_model: int, ffn: int, device):
+    def __init__(self, sched: DeviceScheduler, T: int, K: int, E: int, e_pad: int, d_model: int, ffn: int, device,
+                 train: bool = False):
         L = _lib.lib()
         G = sched.G
-        R = T * K
+        # training keeps every expert block 64-row aligned (weight-gradient GEMMs contract
+        # over whole 64-row blocks); padding rows are never written, so the row buffers
+        # start zeroed (a padding row only ever holds zeros or an older finite row)
+        self.row_align = 64 if train else 1
+        R = T * K + (E * 63 if train else 0)
+        self.R = R
+        alloc = torch.zeros if train else torch.empty
         bf = dict(dtype=torch.bfloat16, device=device)
         i32 = dict(dtype=torch.int32, device=device)
         self.logits = torch.empty(T, e_pad, dtype=torch.float32, device=device)
@@ -82,12 +89,13 @@ class MoEBuffers:
         self.expert_rows = torch.empty(E + 1, dtype=torch.int64, device=device)
         ws = L.hep_moe_assign_workspace(sched.handle, T, K)
         self.assign_ws = torch.empty(max(int(ws), 256), dtype=torch.uint8, device=device)
-        self.rows = torch.empty(max(R, 1), d_model, **bf)
-        self.h = torch.empty(max(R, 1), ffn, **bf)
-        self.y = torch.empty(max(R, 1), d_model, **bf)
+        self.rows = alloc(max(R, 1), d_model, **bf)
+        self.h = alloc(max(R, 1), ffn, **bf)
+        self.y = alloc(max(R, 1), d_model, **bf)
         fws = L.hep_moe_ffn_workspace(max(sched.nnz, 1), R, E)
         self.ffn_ws = torch.empty(max(int(fws), 256), dtype=torch.uint8, device=device)
         self.out = torch.empty(T, d_model, **bf)
+        self.pre = torch.zeros(max(R, 1), 2 * ffn, **bf) if train else None
 
 
 class MoELayer(torch.nn.Module):
@@ -95,8 +103,9 @@ class MoELayer(torch.nn.Module):
     GPUs, forward pass entirely in sm_100a kernels."""
 
     def __init__(self, placement: Placement, d_model: int, ffn: int, top_k: int, *, seed: int = 0,
-                 gate_bias: torch.Tensor | None = None, device=None):
+                 gate_bias: torch.Tensor | None = None, device=None, train: bool = False):
         super().__init__()
+        self.train_mode = train
         torch_ = _lib.require_cuda()
         self.device = torch_.device("cuda", torch_.cuda.current_device()) if device is None else torch_.device(device)
         self.placement = placement
@@ -110,7 +119,8 @@ class MoELayer(torch.nn.Module):
         self.e_pad = max(16, (self.E + 15) // 16 * 16)
         self.sched = DeviceScheduler(placement, device=self.device)
         g = torch.Generator(device=self.device).manual_seed(seed * 7919 + 17)
-        wg = torch.zeros(self.e_pad, d_model, dtype=torch.bfloat16, device=self.device)
+        self.e64 = (self.E + 63) // 64 * 64  # router rows padded to 64 for its backward GEMMs
+        wg = torch.zeros(self.e64, d_model, dtype=torch.bfloat16, device=self.device)
         wg[: self.E] = (torch.randn(self.E, d_model, generator=g, device=self.device) / d_model ** 0.5).to(torch.bfloat16)
         self.wg = wg
         w1, w2, w3 = init_expert_weights(self.E, d_model, ffn, seed, self.device)
@@ -138,7 +148,7 @@ class MoELayer(torch.nn.Module):
     def buffers(self, T: int) -> MoEBuffers:
         b = self._bufs.get(T)
         if b is None:
-            b = MoEBuffers(self.sched, T, self.K, self.E, self.e_pad, self.d, self.F, self.device)
+            b = MoEBuffers(self.sched, T, self.K, self.E, self.e_pad, self.d, self.F, self.device, self.train_mode)
             self._bufs[T] = b
         return b
 
@@ -164,7 +174,6 @@ class MoELayer(torch.nn.Module):
         s = st.cuda_stream
         T, K, E, G = x.shape[0], self.K, self.E, self.G
         tps = T // G
-        R = T * K
         ck = _lib.check
         ev = events or {}
 
@@ -188,7 +197,7 @@ class MoELayer(torch.nn.Module):
         mark("sched", 1)
         mark("assign", 0)
         ck(L.hep_moe_assign(self.sched.handle, ctypes.byref(self.sched.out), b.topk_idx.data_ptr(), T, K, tps,
-                            b.tok_row.data_ptr(), b.row_tok.data_ptr(), b.seg.data_ptr(), b.expert_rows.data_ptr(),
+                            b.row_align, b.tok_row.data_ptr(), b.row_tok.data_ptr(), b.seg.data_ptr(), b.expert_rows.data_ptr(),
                             b.assign_ws.data_ptr(), b.assign_ws.numel(), s), "hep_moe_assign")
         mark("assign", 1)
         mark("permute", 0)
@@ -196,10 +205,16 @@ class MoELayer(torch.nn.Module):
            "hep_moe_permute")
         mark("permute", 1)
         mark("ffn", 0)
-        ck(L.hep_moe_expert_ffn(b.rows.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(), b.seg.data_ptr(),
-                                self.sched.nnz, R, self.d, self.F, E, b.h.data_ptr(), b.y.data_ptr(),
-                                b.ffn_ws.data_ptr(), b.ffn_ws.numel(), self.sched.status.data_ptr(), s),
-           "hep_moe_expert_ffn")
+        if b.pre is None:
+            ck(L.hep_moe_expert_ffn(b.rows.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(), b.seg.data_ptr(),
+                                    self.sched.nnz, b.R, self.d, self.F, E, b.h.data_ptr(), b.y.data_ptr(),
+                                    b.ffn_ws.data_ptr(), b.ffn_ws.numel(), self.sched.status.data_ptr(), s),
+               "hep_moe_expert_ffn")
+        else:
+            ck(L.hep_moe_expert_ffn_train(b.rows.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(),
+                                          b.seg.data_ptr(), self.sched.nnz, b.R, self.d, self.F, E, b.h.data_ptr(),
+                                          b.y.data_ptr(), b.pre.data_ptr(), b.ffn_ws.data_ptr(), b.ffn_ws.numel(),
+                                          self.sched.status.data_ptr(), s), "hep_moe_expert_ffn_train")
         mark("ffn", 1)
         mark("combine", 0)
         ck(L.hep_moe_combine(b.y.data_ptr(), b.tok_row.data_ptr(), b.topk_w.data_ptr(), T, K, self.d,
@@ -212,6 +227,78 @@ class MoELayer(torch.nn.Module):
 
     def check_status(self):
         self.sched.check_status("MoELayer")
+
+    # ------------------------------------------------------------------ training
+    def backward_step(self, x: torch.Tensor, dout: torch.Tensor, stream=None):
+        """Gradients of the last forward on ``x`` (training mode), all on the device:
+        returns (dx bf16 [T][d], dWg fp32 [E][d], dW13 fp32 [E][2F][d] (W13
+        interleave), dW2 fp32 [E][d][F]).
+
+          K7^T  dY rows = w * dout, dw = <dout, Y>                hep_moe_combine_bwd
+          K6^T  dA13 = swiglu'(A13) * (dY W2), dX rows = dA13 W13,
+                dW2 = dY^T H, dW13 = dA13^T X  (per expert)       hep_moe_expert_ffn_bwd
+          K1^T  dlogits = w (dw - sum w dw) on the selected experts,
+                dWg = dlogits^T x, dx_gate = dlogits Wg           hep_gate_bwd, hep_router_bwd
+          K5^T  dx = dx_gate + sum_k dX[row(t,k)]                 hep_moe_gather_sum
+        """
+        if not self.train_mode:
+            raise RuntimeError("construct MoELayer(train=True) to run the backward pass")
+        L = _lib.lib()
+        st = stream if stream is not None else torch.cuda.current_stream()
+        s = st.cuda_stream
+        ck = _lib.check
+        T, K, E, d, F = x.shape[0], self.K, self.E, self.d, self.F
+        b = self.buffers(T)
+        dout = dout.contiguous()
+        dev = self.device
+        with torch.cuda.stream(st):
+            dy = torch.empty_like(b.y)
+            dw = torch.empty(T, K, dtype=torch.float32, device=dev)
+            da13 = torch.empty_like(b.pre)
+            dx_rows = torch.empty_like(b.rows)
+            dw13 = torch.empty(E, 2 * F, d, dtype=torch.float32, device=dev)
+            dw2 = torch.empty(E, d, F, dtype=torch.float32, device=dev)
+            dlogits = torch.empty(T, self.e64, dtype=torch.bfloat16, device=dev)
+            dwg = torch.empty(self.e64, d, dtype=torch.float32, device=dev)
+            dxg = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+            dx = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+        ck(L.hep_moe_combine_bwd(dout.data_ptr(), b.y.data_ptr(), b.tok_row.data_ptr(), b.topk_w.data_ptr(), T, K, d,
+                                 dy.data_ptr(), dw.data_ptr(), s), "hep_moe_combine_bwd")
+        ck(L.hep_moe_expert_ffn_bwd(b.rows.data_ptr(), b.pre.data_ptr(), b.h.data_ptr(), dy.data_ptr(),
+                                    self.w13.data_ptr(), self.w2.data_ptr(), b.seg.data_ptr(), self.sched.nnz,
+                                    b.expert_rows.data_ptr(), b.R, d, F, E, da13.data_ptr(), dx_rows.data_ptr(),
+                                    dw13.data_ptr(), dw2.data_ptr(), b.ffn_ws.data_ptr(), b.ffn_ws.numel(),
+                                    self.sched.status.data_ptr(), s), "hep_moe_expert_ffn_bwd")
+        ck(L.hep_gate_bwd(b.topk_idx.data_ptr(), b.topk_w.data_ptr(), dw.data_ptr(), T, K, self.e64,
+                          dlogits.data_ptr(), s), "hep_gate_bwd")
+        ck(L.hep_router_bwd(x.data_ptr(), self.wg.data_ptr(), dlogits.data_ptr(), T, d, self.e64, dwg.data_ptr(),
+                            dxg.data_ptr(), s), "hep_router_bwd")
+        ck(L.hep_moe_gather_sum(dx_rows.data_ptr(), b.tok_row.data_ptr(), None, dxg.data_ptr(), T, K, d,
+                                dx.data_ptr(), s), "hep_moe_gather_sum")
+        return dx, dwg[:E], dw13, dw2
+
+    LAUNCHES_PER_BACKWARD = 12  # combine_bwd, zero_pad x2, tiles, 4 GEMMs, gate_bwd, 2 router GEMMs, gather
+
+
+class MoEFunction(torch.autograd.Function):
+    """Autograd wrapper: forward and backward entirely in the layer's kernels.
+    Gradients flow to x and to the layer's parameters (wg, w13, w2)."""
+
+    @staticmethod
+    def forward(ctx, x, wg, w13, w2, layer):
+        out = layer(x).clone()
+        ctx.layer = layer
+        ctx.save_for_backward(x)
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        (x,) = ctx.saved_tensors
+        layer = ctx.layer
+        dx, dwg, dw13, dw2 = layer.backward_step(x, dout.to(torch.bfloat16))
+        gwg = torch.zeros_like(layer.wg)
+        gwg[: layer.E] = dwg.to(gwg.dtype)
+        return dx, gwg, dw13.to(layer.w13.dtype), dw2.to(layer.w2.dtype), None
 
 
 class HostPipeline:

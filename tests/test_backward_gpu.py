@@ -1,0 +1,95 @@
+"""Training path: gradients of the B200 layer against a plain PyTorch fp32
+autograd reference of the same op (same routing decisions: the discrete top-K
+is taken from the device; everything differentiable is recomputed in fp32).
+
+Tolerance (bf16 activations/weights, fp32 accumulation): max|err| / max|ref|
+<= 2e-2 for dx and every weight gradient."""
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+TOL = 2e-2
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    import paper_2511_16947_b200 as P
+
+    return P
+
+
+def _reference_grads(layer, x, dout, topk_idx):
+    E, K = layer.E, layer.K
+    xr = x.float().requires_grad_()
+    wg = layer.wg[:E].float().requires_grad_()
+    w1 = layer.w1.float().requires_grad_()
+    w3 = layer.w3.float().requires_grad_()
+    w2 = layer.w2.float().requires_grad_()
+    idx = topk_idx.long()
+    logits = xr @ wg.T
+    w = torch.softmax(logits.gather(1, idx), dim=1)
+    out = torch.zeros_like(xr)
+    for k in range(K):
+        yk = torch.zeros_like(xr)
+        for e in idx[:, k].unique().tolist():
+            sel = (idx[:, k] == e).nonzero().flatten()
+            xs = xr[sel]
+            h = torch.nn.functional.silu(xs @ w1[e].T) * (xs @ w3[e].T)
+            yk = yk.index_add(0, sel, h @ w2[e].T)
+        out = out + w[:, k:k + 1] * yk
+    (out * dout.float()).sum().backward()
+    return xr.grad, wg.grad, w1.grad, w3.grad, w2.grad
+
+
+def _rel(a, b):
+    return ((a.float() - b.float()).abs().max() / b.float().abs().max().clamp_min(1e-12)).item()
+
+
+@pytest.mark.parametrize("G,E,K,d,F,T,s", [
+    (4, 8, 2, 512, 1024, 2048, 1.0),
+    (8, 32, 4, 256, 256, 1024, 1.5),
+    (2, 8, 2, 256, 256, 512, 0.0),
+])
+def test_layer_gradients_match_fp32_reference(P, G, E, K, d, F, T, s):
+    from paper_2511_16947_b200.layer import interleave_w13
+
+    pl = P.cayley_symmetric(P.ClusterShape(G, E, 2))
+    bias = torch.tensor(P.zipf_gate_bias(E, s, 0)) if s > 0 else None
+    layer = P.MoELayer(pl, d, F, K, seed=2, gate_bias=bias, train=True)
+    g = torch.Generator(device="cuda").manual_seed(9)
+    x = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
+    dout = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
+    layer(x)
+    dx, dwg, dw13, dw2 = layer.backward_step(x, dout)
+    torch.cuda.synchronize()
+    layer.check_status()
+    b = layer.buffers(T)
+    rdx, rwg, rw1, rw3, rw2 = _reference_grads(layer, x, dout, b.topk_idx)
+    assert _rel(dx, rdx) <= TOL, _rel(dx, rdx)
+    assert _rel(dwg, rwg) <= TOL, _rel(dwg, rwg)
+    assert _rel(dw2, rw2) <= TOL, _rel(dw2, rw2)
+    assert _rel(dw13, interleave_w13(rw1, rw3)) <= TOL, _rel(dw13, interleave_w13(rw1, rw3))
+    # deterministic (no float atomics)
+    layer(x)
+    dx2, dwg2, dw132, dw22 = layer.backward_step(x, dout)
+    assert torch.equal(dx, dx2) and torch.equal(dw13, dw132) and torch.equal(dw2, dw22) and torch.equal(dwg, dwg2)
+
+
+def test_autograd_function(P):
+    from paper_2511_16947_b200.layer import MoEFunction
+
+    pl = P.cayley_symmetric(P.ClusterShape(4, 8, 2))
+    layer = P.MoELayer(pl, 256, 256, 2, seed=1, train=True)
+    wg = torch.nn.Parameter(layer.wg)
+    w13 = torch.nn.Parameter(layer.w13)
+    w2 = torch.nn.Parameter(layer.w2)
+    x = torch.randn(512, 256, device="cuda").to(torch.bfloat16).requires_grad_()
+    out = MoEFunction.apply(x, wg, w13, w2, layer)
+    out.float().square().mean().backward()
+    assert x.grad.shape == x.shape and torch.isfinite(x.grad.float()).all()
+    assert w13.grad.shape == w13.shape and w2.grad.shape == w2.shape and wg.grad.shape == wg.shape
+    assert w13.grad.float().abs().sum() > 0 and wg.grad[:8].float().abs().sum() > 0

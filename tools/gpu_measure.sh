@@ -1,6 +1,6 @@
 #!/bin/bash
 # One measurement round on the B200 box: tests, bench (3 configs), ncu launch
-# list and full captures of the top kernels.  Output under gpurun_out/.
+# lists and full captures of the top kernels.  Output under gpurun_out/.
 set -x
 R=${ROUND:-r01}
 timeout 900 python -m pytest tests -m gpu -q --timeout 600 > gpurun_out/t_all_$R.log 2>&1
@@ -12,13 +12,13 @@ done
 timeout 300 python bench.py --impl reference --config mixtral --steps 3 --warmup 1 > gpurun_out/bench_ref_mixtral_$R.json 2>&1
 for c in mixtral qwen3 dsv3; do
   timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -k regex:"gemm|sched|gate|chunk|plan|permute|combine|build_tiles" -c 12 --csv \
+    --kernel-name-base demangled -k regex:"hep::" -c 14 --csv \
     --log-file gpurun_out/launches_${c}_$R.csv python bench.py --config $c --profile --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
 done
-timeout 600 ncu --set full --clock-control none --import-source on \
-  -k regex:"gemm_kernel<256|sched_kernel|permute|combine|gate_topk|chunk_map" -c 7 \
+timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+  -k regex:"gemm2sm_kernel|gemm_kernel<.int.256|sched_kernel|permute|combine|gate_topk|chunk_map" -c 8 \
   -o gpurun_out/prof_mixtral_$R python bench.py --config mixtral --profile --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_mixtral_$R.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on \
-  -k regex:"gemm_kernel<256|sched_kernel|permute|combine" -c 5 \
+timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+  -k regex:"gemm_kernel<.int.256|sched_kernel|permute|combine" -c 5 \
   -o gpurun_out/prof_dsv3_$R python bench.py --config dsv3 --profile --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_dsv3_$R.log 2>&1
 echo done
