@@ -309,6 +309,7 @@ def main():
     ap.add_argument("--placement", default="adaptive", choices=["adaptive", "cayley"])
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-train", action="store_true", help="skip the forward+backward training-step measurement")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu legs)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if not args.profile else args.warmup
@@ -464,6 +465,44 @@ def main():
     e2e_value = world * T * args.steps / (e_ms / 1e3)
     assert torch.isfinite(out_last.float()).all()
 
+    # --- training step (forward + backward through the same kernels), reported beside
+    train_info = None
+    if not args.profile and not args.no_train:
+        del pipe
+        tl = P.MoELayer(layer.placement, d, F, K, seed=0, gate_bias=bias, device=dev, train=True)
+        dout = torch.randn(T, d, generator=torch.Generator(device=dev).manual_seed(77), device=dev).to(torch.bfloat16)
+        for _ in range(2):
+            tl(x)
+            tl.backward_step(x, dout)
+        torch.cuda.synchronize()
+        n_tr = max(3, args.steps // 5)
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_tr)]
+        fev = [{"ffn": (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))} for _ in range(n_tr)]
+        t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0e.record(stream)
+        for i in range(n_tr):
+            tl.run(x, tl.buffers(T), stream, events=fev[i])
+            ev[i][0].record(stream)
+            tl.backward_step(x, dout)
+            ev[i][1].record(stream)
+        t1e.record(stream)
+        torch.cuda.synchronize()
+        tl.check_status()
+        tr_ms = t0e.elapsed_time(t1e) / n_tr
+        bwd_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
+        ffn_f = statistics.mean(f["ffn"][0].elapsed_time(f["ffn"][1]) for f in fev)
+        train_info = {
+            "tokens_per_s": T / (tr_ms / 1e3),
+            "ms_per_step": tr_ms,
+            "backward_ms": bwd_ms,
+            "expert_ffn_fwd_ms": ffn_f,
+            "note": "forward + backward (dx, dWg, dW13, dW2) of the same layer, no optimizer; "
+                    "backward = combine^T, SwiGLU dgrad x2 + wgrad x2 (tcgen05), router^T, permute^T",
+            "steps": n_tr,
+        }
+        del tl
+        torch.cuda.empty_cache()
+
     hbm, tf_burst, tf_sus, peak_src = load_peaks()
     R = T * K
     ffn_flops = 6.0 * d * F * R
@@ -539,6 +578,7 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "clocks": sampler.summary() if sampler else None,
             "cpu_baseline": cpu_line,
+            "train_step": train_info,
         }
         print(json.dumps(line))
     if world > 1:
