@@ -54,7 +54,13 @@ struct Params {
     // EPI_SWIGLU: optional pre-activation store; EPI_SWIGLU_BWD: pre-activation input
     void *aux;
     int64_t ld_aux;
+    int raster_gm;  // grouped mode: m-tiles per raster band (0 = whole expert)
+    int pol_mode;  // 0: defaults; else (A policy | B policy << 2), 1 normal, 2 last, 3 first (tuning)
 };
+
+__device__ __forceinline__ uint64_t pick_policy(int k) {
+    return k == 2 ? sm100::policy_evict_last() : (k == 3 ? sm100::policy_evict_first() : sm100::policy_evict_normal());
+}
 
 template <int BN, int STAGES>
 struct Smem {
@@ -115,8 +121,19 @@ __device__ __forceinline__ Tile decode(const Params &p, int64_t t) {
     const int64_t mt_e = (int64_t)p.exp_mt_off[e + 1] - base;
     const int64_t local = t - base * p.n_tiles;
     tl.expert = e;
-    tl.n_blk = (int)(local / mt_e);
-    const int64_t m = base + local % mt_e;
+    int64_t m;
+    if (p.raster_gm > 0 && mt_e > p.raster_gm) {
+        // grouped raster: bands of raster_gm m-tiles, each swept across all N-blocks, so the
+        // operands live in L2 for one band instead of the whole expert
+        const int64_t band = local / ((int64_t)p.raster_gm * p.n_tiles);
+        const int64_t within = local - band * p.raster_gm * p.n_tiles;
+        const int64_t gm = (mt_e - band * p.raster_gm) < p.raster_gm ? (mt_e - band * p.raster_gm) : p.raster_gm;
+        tl.n_blk = (int)(within / gm);
+        m = base + band * p.raster_gm + within % gm;
+    } else {
+        tl.n_blk = (int)(local / mt_e);
+        m = base + local % mt_e;
+    }
     tl.row0 = p.mt_row0[m];
     tl.rows = p.mt_rows[m];
     return tl;
@@ -307,9 +324,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             // grouped expert GEMMs reuse A (token rows) across N-blocks and stream B (weights);
             // the router GEMM streams A (x) and reuses B (Wg)
-            const uint64_t pol_a = p.grouped ? policy_evict_last() : policy_evict_first();
+            const uint64_t pol_a = p.pol_mode ? pick_policy(p.pol_mode & 3) : (p.grouped ? policy_evict_last() : policy_evict_first());
             // weights are shared by the concurrently running m-tiles of one (expert, N-block): normal priority
-            const uint64_t pol_b = p.grouped ? policy_evict_normal() : policy_evict_last();
+            const uint64_t pol_b = p.pol_mode ? pick_policy((p.pol_mode >> 2) & 3) : (p.grouped ? policy_evict_normal() : policy_evict_last());
             uint32_t phase = 0;
             for (int64_t t = blockIdx.x; t < n_total; t += gridDim.x) {
                 const Tile tl = decode(p, t);
@@ -468,8 +485,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         if (lane == 0) {
             // ===================== TMA producer (both CTAs) =====================
-            const uint64_t pol_a = policy_evict_last();
-            const uint64_t pol_b = policy_evict_normal();
+            const uint64_t pol_a = p.pol_mode ? pick_policy(p.pol_mode & 3) : policy_evict_last();
+            const uint64_t pol_b = p.pol_mode ? pick_policy((p.pol_mode >> 2) & 3) : policy_evict_normal();
             const uint32_t full_l = mapa_shared(smem_u32(&full[0]), 0);  // leader's full[0]
             int stage = 0;
             uint32_t phase = 0;
@@ -804,11 +821,16 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
     int32_t *mt_rows = mt_row0 + cap;
     int32_t *exp_off = mt_rows + cap;
     const bool pairs = use_pairs(R, n_experts);
+    const char *pol_env = getenv("HEP_L2POL");
+    const int pol_mode = pol_env ? atoi(pol_env) : 0;
     build_tiles_kernel<<<1, 1024, 0, s>>>(d_seg, n_seg, n_experts, mt_row0, mt_rows, exp_off, cap, d_status,
                                           pairs ? kPairRows : BM);
     HEP_CHECK_LAUNCH();
     Params p{};
     p.grouped = 1;
+    p.pol_mode = pol_mode;
+    const char *gm_env = getenv("HEP_RASTER_GM");
+    p.raster_gm = gm_env ? atoi(gm_env) : 8;  // measured best (profiles/r01/raster.txt)
     p.mt_row0 = mt_row0;
     p.mt_rows = mt_rows;
     p.exp_mt_off = exp_off;
