@@ -152,40 +152,53 @@ __device__ __forceinline__ int64_t floordiv(int64_t v, int64_t d) {
 }
 
 // ---------------------------------------------------------------------------
-// step 4: lex-min canonical plan, warp 0.  Each lane keeps the slack
-// C[S] - Wf[S] >= 0 of its SPL subsets; the minimum feasible load of arc
-// (e, g) is v = max(0, r - min{slack[S] : S ⊇ need, g ∉ S}).  The result of
-// arc p (p = position in (expert, gpu id) order) goes to vtmp[p].
-// U = uint32_t when every slack and load fits 32 bits: one redux.sync per
-// arc and the next expert's metadata prefetched (software pipelined).
+// step 4: lex-min canonical plan, whole block.  Every thread keeps the slack
+// C[S] - Wf[S] >= 0 of its SPB subsets (S = tid + 256 j); the minimum feasible
+// load of arc (e, g) is v = max(0, r - min{slack[S] : S ⊇ need, g ∉ S}): a
+// warp redux.sync per warp, the 8 warp minima through shared memory (double
+// buffered by arc parity, one barrier per arc), then every thread applies the
+// same decision to its subsets.  Result of arc p (position in (expert, gpu id)
+// order) goes to vtmp[p].  U = uint32_t when every slack and load fits 32 bits.
 // ---------------------------------------------------------------------------
-template <int SPL, typename U>
-__device__ void lexmin_warp(const SchedArgs &a, SchedSmem &s, int64_t *vtmp) {
-    const int lane = threadIdx.x & 31;
+template <typename U>
+__device__ __forceinline__ U block_min(U v, U (*red)[kSchedThreads / 32], int &par) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    v = wmin(v);
+    if (lane == 0) red[par][w] = v;
+    __syncthreads();
+    U m = red[par][0];
+#pragma unroll
+    for (int i = 1; i < kSchedThreads / 32; ++i) m = red[par][i] < m ? red[par][i] : m;
+    par ^= 1;
+    return m;
+}
+
+template <int SPB, typename U>
+__device__ void lexmin_block(const SchedArgs &a, SchedSmem &s, int64_t *vtmp) {
+    __shared__ U red[2][kSchedThreads / 32];
+    const int tid = threadIdx.x;
     const int E = a.E;
     const uint32_t NS = 1u << a.G;
     const int64_t Q = a.Q;
-    U sl[SPL];
+    const U UMAX = ~(U)0;
+    U sl[SPB];
     uint32_t valid = 0;
 #pragma unroll
-    for (int j = 0; j < SPL; ++j) {
-        const uint32_t S = lane + 32 * j;
+    for (int j = 0; j < SPB; ++j) {
+        const uint32_t S = tid + kSchedThreads * j;
         sl[j] = S < NS ? (U)(s.C[S] - s.W[S] * Q) : (U)0;
         valid |= (S < NS) << j;
     }
+    int par = 0;
     int4 nxt = s.emeta[0];
-    U r_nxt = sizeof(U) == 4 ? (U)(uint32_t)nxt.w : (U)(s.totals[0] * Q);
     for (int e = 0; e < E; ++e) {
         const int b = nxt.x, n = nxt.y;
         uint32_t R = (uint32_t)nxt.z;
-        U r = r_nxt;
-        if (e + 1 < E) {  // prefetch the next expert while this one runs
-            nxt = s.emeta[e + 1];
-            r_nxt = sizeof(U) == 4 ? (U)(uint32_t)nxt.w : (U)(s.totals[e + 1] * Q);
-        }
+        U r = sizeof(U) == 4 ? (U)(uint32_t)nxt.w : (U)(s.totals[e] * Q);
+        if (e + 1 < E) nxt = s.emeta[e + 1];  // prefetch the next expert
         if (n == 0) continue;
         if (n == 1) {  // single replica: v = r; +r on S ⊇ {g} and -r on S ∋ g cancel
-            if (lane == 0) vtmp[b] = (int64_t)r;
+            if (tid == 0) vtmp[b] = (int64_t)r;
             continue;
         }
         if (n == 2) {
@@ -194,30 +207,23 @@ __device__ void lexmin_warp(const SchedArgs &a, SchedSmem &s, int64_t *vtmp) {
             // before the "+r on S ⊇ R" step; the net update afterwards is -v_a on
             // S ∋ a, S ∌ c and -v_c on S ∋ c, S ∌ a (S ⊇ R: +r - v_a - v_c = 0).
             const int ga = s.arc_gpu[b], gc = s.arc_gpu[b + 1];
-            U v_a = 0;
-            if (r) {
-                U t[SPL];
+            U mn = UMAX;
 #pragma unroll
-                for (int j = 0; j < SPL; ++j) {
-                    const uint32_t S = lane + 32 * j;
-                    const bool ok = ((valid >> j) & 1) && ((S >> gc) & 1) && !((S >> ga) & 1);
-                    t[j] = ok ? sl[j] : ~(U)0;
-                }
-#pragma unroll
-                for (int w = 1; w < SPL; w <<= 1)  // pairwise tree (ILP), not a serial chain
-#pragma unroll
-                    for (int j = 0; j + w < SPL; j += 2 * w) t[j] = t[j + w] < t[j] ? t[j + w] : t[j];
-                const U mn = wmin(t[0]);
-                v_a = r > mn ? r - mn : (U)0;
+            for (int j = 0; j < SPB; ++j) {
+                const uint32_t S = tid + kSchedThreads * j;
+                const bool ok = ((valid >> j) & 1) && ((S >> gc) & 1) && !((S >> ga) & 1);
+                mn = (ok && sl[j] < mn) ? sl[j] : mn;
             }
+            mn = block_min(mn, red, par);
+            const U v_a = r > mn ? r - mn : (U)0;
             const U v_c = r - v_a;
-            if (lane == 0) {
+            if (tid == 0) {
                 vtmp[b] = (int64_t)v_a;
                 vtmp[b + 1] = (int64_t)v_c;
             }
 #pragma unroll
-            for (int j = 0; j < SPL; ++j) {
-                const uint32_t S = lane + 32 * j;
+            for (int j = 0; j < SPB; ++j) {
+                const uint32_t S = tid + kSchedThreads * j;
                 const uint32_t ha = (S >> ga) & 1, hc = (S >> gc) & 1;
                 sl[j] -= (ha & ~hc) ? v_a : ((hc & ~ha) ? v_c : (U)0);
             }
@@ -225,15 +231,13 @@ __device__ void lexmin_warp(const SchedArgs &a, SchedSmem &s, int64_t *vtmp) {
         }
         if (r) {
 #pragma unroll
-            for (int j = 0; j < SPL; ++j) {
-                const uint32_t S = lane + 32 * j;
+            for (int j = 0; j < SPB; ++j) {
+                const uint32_t S = tid + kSchedThreads * j;
                 sl[j] += ((S & R) == R) ? r : (U)0;  // expert e leaves the not-yet-processed set
             }
         }
-        int g_nxt = s.arc_gpu[b];
         for (int k = 0; k < n; ++k) {
-            const int g = g_nxt;
-            if (k + 1 < n) g_nxt = s.arc_gpu[b + k + 1];
+            const int g = s.arc_gpu[b + k];
             const uint32_t gbit = 1u << g;
             const uint32_t need = R & ~gbit;
             U v;
@@ -242,23 +246,23 @@ __device__ void lexmin_warp(const SchedArgs &a, SchedSmem &s, int64_t *vtmp) {
             } else if (need == 0) {
                 v = r;  // S = {} has slack 0; every other bound is <= r
             } else {
-                U mn = ~(U)0;
+                U mn = UMAX;
 #pragma unroll
-                for (int j = 0; j < SPL; ++j) {
-                    const uint32_t S = lane + 32 * j;
+                for (int j = 0; j < SPB; ++j) {
+                    const uint32_t S = tid + kSchedThreads * j;
                     const bool ok = ((valid >> j) & 1) && ((S & need) == need) && !(S & gbit);
                     mn = (ok && sl[j] < mn) ? sl[j] : mn;
                 }
-                mn = wmin(mn);
+                mn = block_min(mn, red, par);
                 v = r > mn ? r - mn : (U)0;
             }
-            if (lane == 0) vtmp[b + k] = (int64_t)v;
+            if (tid == 0) vtmp[b + k] = (int64_t)v;
             r -= v;
             R = need;
             if (v) {
 #pragma unroll
-                for (int j = 0; j < SPL; ++j) {
-                    const uint32_t S = lane + 32 * j;
+                for (int j = 0; j < SPB; ++j) {
+                    const uint32_t S = tid + kSchedThreads * j;
                     sl[j] -= (S & gbit) ? v : (U)0;  // capacity of every subset holding g drops by v
                 }
             }
@@ -549,12 +553,13 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
         __syncthreads();
         prof_mark(a.flags, 2);
         // ---- step 4: lex-min canonical plan ------------------------------------
-        if (tid < 32) {
+        {
             const int64_t mQ = s.misc[0];
             const bool fits32 = (__int128)G * (total_all + 1) * a.Q < ((__int128)1 << 31) &&
                                 (__int128)G * (mQ + 1) < ((__int128)1 << 31);
-            if (fits32) lexmin_warp<SPL, uint32_t>(a, s, s.xi);
-            else lexmin_warp<SPL, uint64_t>(a, s, s.xi);
+            constexpr int SPB = SPL >= 8 ? SPL / 8 : 1;  // subsets per thread (2^G / 256)
+            if (fits32) lexmin_block<SPB, uint32_t>(a, s, s.xi);
+            else lexmin_block<SPB, uint64_t>(a, s, s.xi);
         }
         __syncthreads();
         for (int p = tid; p < nnz; p += nt) {  // (expert, gpu id) order -> EDP list order
