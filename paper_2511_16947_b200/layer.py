@@ -221,6 +221,22 @@ class MoELayer(torch.nn.Module):
                              b.out.data_ptr(), s), "hep_moe_combine")
         mark("combine", 1)
 
+    def capture(self, x: torch.Tensor) -> "torch.cuda.CUDAGraph":
+        """Record one forward on ``x`` (fixed buffers, no host sync anywhere in the
+        chain) as a CUDA graph; ``graph.replay()`` re-runs all 12 kernels with one
+        launch.  ``x`` must stay the input tensor (refill it in place)."""
+        b = self.buffers(x.shape[0])
+        side = torch.cuda.Stream(device=self.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # warm the launch paths (attributes, tensor maps) outside the capture
+            self.run(x, b, side)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize(self.device)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            self.run(x, b, side)
+        return g
+
     # kernels launched per forward: router GEMM, gate top-K, scheduler, assign x4,
     # permute, FFN (tile list + 2 GEMMs), combine
     LAUNCHES_PER_FORWARD = 12
