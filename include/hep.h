@@ -186,6 +186,17 @@ int hep_moe_assign_ep(hep_sched_t h, const hep_sched_out *sched, const int32_t *
                       int32_t *d_tok_row, int32_t *d_seg, int64_t *d_counts, void *workspace, size_t workspace_bytes,
                       void *stream);
 size_t hep_moe_assign_ep_workspace(hep_sched_t h, int64_t T, int K);
+/*
+ * EP training layout: map the receive buffer ([src][hosted expert], d_seg from
+ * hep_moe_assign_ep) onto a [local slot][src] layout where every slot's rows form one
+ * block starting on a multiple of row_align (the weight-gradient GEMMs contract over
+ * whole 64-row blocks).  Outputs: d_row_map [R_recv] aligned row of each received row,
+ * d_seg_out [n_slots][4] (row_start, rows, slot, 0) and d_slot_rows [n_slots+1] (block
+ * starts; the last entry = rows of the aligned buffer), the d_seg / d_expert_rows
+ * arguments of hep_moe_expert_ffn_train / hep_moe_expert_ffn_bwd with n_experts = n_slots.
+ */
+int hep_moe_ep_train_layout(const int32_t *d_seg, int n_hosted, int G, int n_slots, int row_align, int32_t *d_row_map,
+                            int32_t *d_seg_out, int64_t *d_slot_rows, void *stream);
 /* experts hosted by `rank` and the number of local weight slots it needs */
 int hep_sched_hosted(hep_sched_t h, int rank, int *n_hosted, int *n_slots);
 

@@ -628,6 +628,68 @@ extern "C" int hep_moe_combine_bwd(const void *d_dout, const void *d_y, const in
     return HEP_OK;
 }
 
+namespace hep {
+// EP training layout: the receive buffer is [src][hosted expert] (what the dispatch
+// all-to-all delivers); the weight-gradient GEMMs need every local slot's rows as one
+// block starting on a multiple of `align`.  Block b handles receive segment b = (src, h):
+// it recomputes the per-slot totals and their aligned prefix (n_slots <= 1024, G <= 10:
+// a few hundred adds) and writes row_map for the segment's rows; block 0 also writes
+// the per-slot segments and the slot row offsets.
+__global__ void __launch_bounds__(256) ep_layout_kernel(const int32_t *seg, int n_hosted, int G, int n_slots,
+                                                        int align, int32_t *row_map, int32_t *seg_out,
+                                                        int64_t *slot_rows) {
+    extern __shared__ int64_t sm_tot[];  // [n_slots] totals, then aligned starts
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int i = tid; i < n_slots; i += nt) sm_tot[i] = 0;
+    __syncthreads();
+    for (int h = tid; h < n_hosted; h += nt) {
+        int64_t n = 0;
+        for (int d = 0; d < G; ++d) n += seg[4 * (d * n_hosted + h) + 1];
+        sm_tot[seg[4 * h + 2]] = n;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int64_t run = 0;
+        for (int s = 0; s < n_slots; ++s) {
+            const int64_t n = sm_tot[s];
+            sm_tot[s] = run;
+            if (blockIdx.x == 0) {
+                slot_rows[s] = run;
+                seg_out[4 * s] = (int32_t)run;
+                seg_out[4 * s + 1] = (int32_t)n;
+                seg_out[4 * s + 2] = s;
+                seg_out[4 * s + 3] = 0;
+            }
+            run += (n + align - 1) / align * align;
+        }
+        if (blockIdx.x == 0) slot_rows[n_slots] = run;
+    }
+    __syncthreads();
+    if (n_hosted == 0) return;
+    const int b = blockIdx.x, src = b / n_hosted, h = b % n_hosted;
+    const int32_t *sg = seg + 4 * b;
+    int64_t dst = sm_tot[sg[2]];
+    for (int d = 0; d < src; ++d) dst += seg[4 * (d * n_hosted + h) + 1];
+    const int32_t r0 = sg[0], n = sg[1];
+    for (int i = tid; i < n; i += nt) row_map[r0 + i] = (int32_t)(dst + i);
+}
+}  // namespace hep
+
+extern "C" int hep_moe_ep_train_layout(const int32_t *d_seg, int n_hosted, int G, int n_slots, int row_align,
+                                       int32_t *d_row_map, int32_t *d_seg_out, int64_t *d_slot_rows, void *stream) {
+    HEP_REQUIRE(d_seg && d_row_map && d_seg_out && d_slot_rows, HEP_E_CONTRACT, "hep_moe_ep_train_layout: null");
+    HEP_REQUIRE(G >= 1 && G <= HEP_MAX_GPUS && n_hosted >= 0 && n_slots >= n_hosted && n_slots <= 1024 &&
+                    row_align >= 1,
+                HEP_E_DIMENSION, "hep_moe_ep_train_layout: G %d n_hosted %d n_slots %d align %d", G, n_hosted,
+                n_slots, row_align);
+    if (n_slots == 0) return HEP_OK;
+    const int blocks = n_hosted > 0 ? G * n_hosted : 1;
+    ep_layout_kernel<<<blocks, 256, sizeof(int64_t) * n_slots, (cudaStream_t)stream>>>(
+        d_seg, n_hosted, G, n_slots, row_align, d_row_map, d_seg_out, d_slot_rows);
+    HEP_CHECK_LAUNCH();
+    return HEP_OK;
+}
+
 extern "C" int hep_moe_zero_padding(const int64_t *d_expert_rows, const int32_t *d_seg, int n_seg, int E, void *d_buf,
                                     int64_t width, void *stream) {
     HEP_REQUIRE(d_expert_rows && d_seg && d_buf && width % 8 == 0, HEP_E_CONTRACT, "hep_moe_zero_padding");

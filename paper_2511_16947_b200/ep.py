@@ -12,6 +12,20 @@ Per micro-batch and rank r (all kernels are the sm_100a C-ABI ones):
   ---  combine all-to-all-v (transposed split sizes)         comm.all_to_all
   K7   weighted sum of the K returned rows per token        hep_moe_combine
 
+Training (``train=True``) re-lays the received rows out per local weight slot,
+64-row aligned (``hep_moe_ep_train_layout`` + ``hep_moe_permute``), stores the
+pre-activations, and ``backward`` runs the transposed chain with the same two
+exchanges reversed, then reduces each expert's weight gradients over its EDP
+group (the replicas of the expert) and the
+router gradient over all ranks:
+
+  K7^T combine backward (dY rows, dw)                       hep_moe_combine_bwd
+  ---  dY all-to-all-v (dispatch split sizes)                comm.all_to_all
+  K6^T SwiGLU dgrad + wgrad on the local slots               hep_moe_expert_ffn_bwd
+  ---  dX all-to-all-v (combine split sizes)                 comm.all_to_all
+  K1^T router backward, K5^T gather-sum into dx              hep_gate_bwd, hep_router_bwd, hep_moe_gather_sum
+  ---  expert-gradient exchange inside every EDP group, router all-reduce
+
 Two communicators implement the two exchanges: ``DistComm`` (one process per
 GPU over torch.distributed — NCCL on B200s, gloo for the CPU protocol tests)
 and ``LocalComm`` (all G ranks in one process on one device, exchanges as
@@ -51,6 +65,14 @@ class LocalComm:
         full = torch.cat(parts, dim=0)
         return [full for _ in parts]
 
+    def all_reduce(self, parts: list[torch.Tensor]) -> None:
+        """In-place sum over the ranks (rank order)."""
+        acc = parts[0].clone()
+        for p in parts[1:]:
+            acc += p
+        for p in parts:
+            p.copy_(acc)
+
     def all_to_all(self, sends: list[torch.Tensor], send_counts: list[list[int]],
                    recv_counts: list[list[int]]) -> list[torch.Tensor]:
         G = self.world
@@ -79,6 +101,10 @@ class DistComm:
         chunks = [torch.empty_like(p) for _ in range(self.world)]
         self.dist.all_gather(chunks, p.contiguous(), group=self.group)
         return [torch.cat(chunks, dim=0)]
+
+    def all_reduce(self, parts: list[torch.Tensor]) -> None:
+        (p,) = parts
+        self.dist.all_reduce(p, group=self.group)
 
     def all_to_all(self, sends: list[torch.Tensor], send_counts: list[list[int]],
                    recv_counts: list[list[int]]) -> list[torch.Tensor]:
@@ -145,16 +171,18 @@ class EPMoELayer:
     """
 
     def __init__(self, placement: Placement, d_model: int, ffn: int, top_k: int, comm, ranks, *, seed: int = 0,
-                 gate_bias: torch.Tensor | None = None, device=None):
+                 gate_bias: torch.Tensor | None = None, device=None, train: bool = False):
         _lib.require_cuda()
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.placement, self.comm = placement, comm
         self.G, self.E, self.K, self.d, self.F = placement.num_gpus, placement.num_experts, top_k, d_model, ffn
         if comm.world != self.G:
             raise ValueError(f"communicator has {comm.world} ranks, placement {self.G} GPUs")
+        self.train_mode = train
         self.e_pad = max(16, (self.E + 15) // 16 * 16)
+        self.e64 = (self.E + 63) // 64 * 64  # router rows padded to 64 for its backward GEMMs
         g = torch.Generator(device=self.device).manual_seed(seed * 7919 + 17)
-        wg = torch.zeros(self.e_pad, d_model, dtype=torch.bfloat16, device=self.device)
+        wg = torch.zeros(self.e64, d_model, dtype=torch.bfloat16, device=self.device)
         wg[: self.E] = (torch.randn(self.E, d_model, generator=g, device=self.device) / d_model ** 0.5).to(torch.bfloat16)
         self.wg = wg
         self.gate_bias = None if gate_bias is None else gate_bias.to(self.device, torch.float32).contiguous()
@@ -203,8 +231,29 @@ class EPMoELayer:
                                      recv_counts)
         ys = []
         for rk, b, recv in zip(self.ranks, bs, recvs):
-            R = recv.shape[0]
-            y = torch.empty(max(R, 1), d, dtype=torch.bfloat16, device=self.device)
+            ys.append(self._expert_ffn(rk, b, recv))
+        for i, b in enumerate(bs):
+            b["send_counts"], b["recv_counts"] = send_counts[i], recv_counts[i]
+        backs = self.comm.all_to_all(ys, recv_counts, send_counts)
+        outs = []
+        for x, b, back in zip(xs, bs, backs):
+            T = x.shape[0]
+            if self.train_mode:
+                b["x"], b["back"] = x, back
+            ck(L.hep_moe_combine(back.data_ptr(), b["tok_row"].data_ptr(), b["topk_w"].data_ptr(), T, K, d,
+                                 b["out"].data_ptr(), s), "hep_moe_combine")
+            outs.append(b["out"])
+        return outs
+
+    def _expert_ffn(self, rk: EPRank, b: dict, recv: torch.Tensor) -> torch.Tensor:
+        """K6 on the received rows of one rank; returns Y in receive order."""
+        L = _lib.lib()
+        ck = _lib.check
+        s = torch.cuda.current_stream().cuda_stream
+        G, d, F = self.G, self.d, self.F
+        R = recv.shape[0]
+        y = torch.empty(max(R, 1), d, dtype=torch.bfloat16, device=self.device)
+        if not self.train_mode:
             if R > 0:
                 h = torch.empty(R, F, dtype=torch.bfloat16, device=self.device)
                 n_seg = G * rk.n_hosted
@@ -213,12 +262,165 @@ class EPMoELayer:
                 ck(L.hep_moe_expert_ffn(recv.data_ptr(), rk.w13.data_ptr(), rk.w2.data_ptr(), b["seg"].data_ptr(),
                                         n_seg, R, d, F, rk.n_slots, h.data_ptr(), y.data_ptr(), ws.data_ptr(),
                                         ws.numel(), rk.sched.status.data_ptr(), s), "hep_moe_expert_ffn")
-            ys.append(y[:R])
-        backs = self.comm.all_to_all(ys, recv_counts, send_counts)
-        outs = []
-        for x, b, back in zip(xs, bs, backs):
+            return y[:R]
+        # training: per-slot 64-row aligned blocks (weight-gradient GEMMs), pre-activations kept
+        ns = rk.n_slots
+        i32 = dict(dtype=torch.int32, device=self.device)
+        row_map = torch.empty(max(R, 1), **i32)
+        seg_al = torch.empty(ns, 4, **i32)
+        slot_rows = torch.empty(ns + 1, dtype=torch.int64, device=self.device)
+        ck(L.hep_moe_ep_train_layout(b["seg"].data_ptr(), rk.n_hosted, G, ns, 64, row_map.data_ptr(),
+                                     seg_al.data_ptr(), slot_rows.data_ptr(), s), "hep_moe_ep_train_layout")
+        Ral = R + 63 * ns
+        bf = dict(dtype=torch.bfloat16, device=self.device)
+        rows_al = torch.empty(max(Ral, 1), d, **bf)
+        h_al = torch.empty(max(Ral, 1), F, **bf)
+        y_al = torch.empty(max(Ral, 1), d, **bf)
+        pre_al = torch.empty(max(Ral, 1), 2 * F, **bf)
+        ws = torch.empty(max(int(L.hep_moe_ffn_workspace(ns, Ral, ns)), 256), dtype=torch.uint8, device=self.device)
+        if R > 0:
+            ck(L.hep_moe_permute(recv.data_ptr(), row_map.data_ptr(), R, 1, d, rows_al.data_ptr(), s),
+               "hep_moe_permute(align)")
+        # padding rows are never written by the GEMMs; the weight-gradient GEMMs contract
+        # over them (dW13 += dA13^T X, dW2 += dY^T H), so X and H padding must be zero
+        ck(L.hep_moe_zero_padding(slot_rows.data_ptr(), seg_al.data_ptr(), ns, ns, rows_al.data_ptr(), d, s),
+           "hep_moe_zero_padding(rows)")
+        ck(L.hep_moe_zero_padding(slot_rows.data_ptr(), seg_al.data_ptr(), ns, ns, h_al.data_ptr(), F, s),
+           "hep_moe_zero_padding(h)")
+        ck(L.hep_moe_expert_ffn_train(rows_al.data_ptr(), rk.w13.data_ptr(), rk.w2.data_ptr(), seg_al.data_ptr(), ns,
+                                      Ral, d, F, ns, h_al.data_ptr(), y_al.data_ptr(), pre_al.data_ptr(),
+                                      ws.data_ptr(), ws.numel(), rk.sched.status.data_ptr(), s),
+           "hep_moe_expert_ffn_train")
+        if R > 0:
+            ck(L.hep_moe_gather_sum(y_al.data_ptr(), row_map.data_ptr(), None, None, R, 1, d, y.data_ptr(), s),
+               "hep_moe_gather_sum(unalign)")
+        b.update(row_map=row_map, seg_al=seg_al, slot_rows=slot_rows, Ral=Ral, rows_al=rows_al, h_al=h_al,
+                 pre_al=pre_al, ffn_ws=ws, R_recv=R)
+        return y[:R]
+
+    def backward(self, douts: list[torch.Tensor], stream=None):
+        """Gradients of the last training forward.  douts[i] = dL/dout of rank
+        self.ranks[i].  Returns, per driven rank, (dx bf16 [T][d], dWg fp32 [E][d]
+        summed over all ranks, dW13 fp32 [n_slots][2F][d], dW2 fp32 [n_slots][d][F])
+        where slot s of rank r holds the gradient of expert e (slots[e] = s) summed
+        over every replica of e in its EDP group — identical on all replicas."""
+        if not self.train_mode:
+            raise RuntimeError("construct EPMoELayer(train=True) to run the backward pass")
+        st = stream if stream is not None else torch.cuda.current_stream()
+        with torch.cuda.stream(st):
+            return self._backward(douts, st)
+
+    def _backward(self, douts, st):
+        L = _lib.lib()
+        s = st.cuda_stream
+        ck = _lib.check
+        K, E, G, d, F = self.K, self.E, self.G, self.d, self.F
+        dev = self.device
+        bs = [rk.buffers(self, b_x.shape[0]) for rk, b_x in zip(self.ranks, douts)]
+        dys, dws = [], []
+        for rk, b, dout in zip(self.ranks, bs, douts):
+            T = dout.shape[0]
+            dy = torch.empty(max(T * K, 1), d, dtype=torch.bfloat16, device=dev)
+            dw = torch.empty(T, K, dtype=torch.float32, device=dev)
+            ck(L.hep_moe_combine_bwd(dout.contiguous().data_ptr(), b["back"].data_ptr(), b["tok_row"].data_ptr(),
+                                     b["topk_w"].data_ptr(), T, K, d, dy.data_ptr(), dw.data_ptr(), s),
+               "hep_moe_combine_bwd")
+            dys.append(dy[: sum(b["send_counts"])])
+            dws.append(dw)
+        send_counts = [b["send_counts"] for b in bs]
+        recv_counts = [b["recv_counts"] for b in bs]
+        dy_recvs = self.comm.all_to_all(dys, send_counts, recv_counts)
+        dx_recvs, dw13s, dw2s = [], [], []
+        for rk, b, dyr in zip(self.ranks, bs, dy_recvs):
+            ns, R, Ral = rk.n_slots, b["R_recv"], b["Ral"]
+            bf = dict(dtype=torch.bfloat16, device=dev)
+            dy_al = torch.empty(max(Ral, 1), d, **bf)
+            if R > 0:
+                ck(L.hep_moe_permute(dyr.data_ptr(), b["row_map"].data_ptr(), R, 1, d, dy_al.data_ptr(), s),
+                   "hep_moe_permute(align)")
+            da13 = torch.empty(max(Ral, 1), 2 * F, **bf)
+            dx_al = torch.empty(max(Ral, 1), d, **bf)
+            dw13 = torch.empty(ns, 2 * F, d, dtype=torch.float32, device=dev)
+            dw2 = torch.empty(ns, d, F, dtype=torch.float32, device=dev)
+            ck(L.hep_moe_expert_ffn_bwd(b["rows_al"].data_ptr(), b["pre_al"].data_ptr(), b["h_al"].data_ptr(),
+                                        dy_al.data_ptr(), rk.w13.data_ptr(), rk.w2.data_ptr(), b["seg_al"].data_ptr(),
+                                        ns, b["slot_rows"].data_ptr(), Ral, d, F, ns, da13.data_ptr(),
+                                        dx_al.data_ptr(), dw13.data_ptr(), dw2.data_ptr(), b["ffn_ws"].data_ptr(),
+                                        b["ffn_ws"].numel(), rk.sched.status.data_ptr(), s),
+               "hep_moe_expert_ffn_bwd")
+            dxr = torch.empty(max(R, 1), d, **bf)
+            if R > 0:
+                ck(L.hep_moe_gather_sum(dx_al.data_ptr(), b["row_map"].data_ptr(), None, None, R, 1, d,
+                                        dxr.data_ptr(), s), "hep_moe_gather_sum(unalign)")
+            dx_recvs.append(dxr[:R])
+            dw13s.append(dw13)
+            dw2s.append(dw2)
+        dx_sends = self.comm.all_to_all(dx_recvs, recv_counts, send_counts)
+        dxs, dwgs = [], []
+        for b, dxs_rows, dw in zip(bs, dx_sends, dws):
+            x = b["x"]
             T = x.shape[0]
-            ck(L.hep_moe_combine(back.data_ptr(), b["tok_row"].data_ptr(), b["topk_w"].data_ptr(), T, K, d,
-                                 b["out"].data_ptr(), s), "hep_moe_combine")
-            outs.append(b["out"])
-        return outs
+            dlogits = torch.empty(T, self.e64, dtype=torch.bfloat16, device=dev)
+            dwg = torch.empty(self.e64, d, dtype=torch.float32, device=dev)
+            dxg = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+            dx = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+            ck(L.hep_gate_bwd(b["topk_idx"].data_ptr(), b["topk_w"].data_ptr(), dw.data_ptr(), T, K, self.e64,
+                              dlogits.data_ptr(), s), "hep_gate_bwd")
+            ck(L.hep_router_bwd(x.data_ptr(), self.wg.data_ptr(), dlogits.data_ptr(), T, d, self.e64,
+                                dwg.data_ptr(), dxg.data_ptr(), s), "hep_router_bwd")
+            ck(L.hep_moe_gather_sum(dxs_rows.data_ptr(), b["tok_row"].data_ptr(), None, dxg.data_ptr(), T, K, d,
+                                    dx.data_ptr(), s), "hep_moe_gather_sum")
+            dxs.append(dx)
+            dwgs.append(dwg)
+        self.comm.all_reduce(dwgs)
+        edp_reduce(self.placement, self.comm, [rk.rank for rk in self.ranks], dw13s, dw2s)
+        return [(dx, dwg[:E], dw13, dw2) for dx, dwg, dw13, dw2 in zip(dxs, dwgs, dw13s, dw2s)]
+
+
+def edp_reduce(placement: Placement, comm, ranks: list[int], dw13s: list[torch.Tensor],
+               dw2s: list[torch.Tensor]) -> None:
+    """Sum every expert's weight gradient over its EDP group (the GPUs holding a
+    replica of it), in place, so every replica applies the same update
+    (SURVEY.md §8e).  dw13s[i] / dw2s[i] are rank ranks[i]'s
+    per-slot gradients [n_slots][2F][d] / [n_slots][d][F] (slot = placement.slots[e]).
+
+    One all-to-all-v carries, from rank r to rank q, the gradients of the experts
+    both host (ascending expert id) — no per-group communicators; each replica
+    then adds its group's contributions in ascending rank order, so all replicas
+    end bit-identical."""
+    pl, G = placement, placement.num_gpus
+    hosted = [set(h) for h in pl.hosted]
+    shp13, shp2 = tuple(dw13s[0].shape[1:]), tuple(dw2s[0].shape[1:])
+    n13, n2 = dw13s[0][0].numel(), dw2s[0][0].numel()
+    per = n13 + n2
+    shared = [[sorted(hosted[r] & hosted[q]) if q != r else [] for q in range(G)] for r in range(G)]
+    sends, send_counts, recv_counts = [], [], []
+    for r, dw13, dw2 in zip(ranks, dw13s, dw2s):
+        parts = []
+        for q in range(G):
+            for e in shared[r][q]:
+                sl = pl.slots[e]
+                parts += [dw13[sl].reshape(-1), dw2[sl].reshape(-1)]
+        sends.append(torch.cat(parts) if parts else dw13.new_empty(0))
+        send_counts.append([len(shared[r][q]) * per for q in range(G)])
+        recv_counts.append([len(shared[q][r]) * per for q in range(G)])
+    recvs = comm.all_to_all(sends, send_counts, recv_counts)
+    for r, dw13, dw2, recv, rc in zip(ranks, dw13s, dw2s, recvs, recv_counts):
+        off = _offsets(rc)
+        for e in sorted(hosted[r]):
+            members = sorted(set(pl.edp_groups[e]))
+            if len(members) < 2:
+                continue
+            sl = pl.slots[e]
+            t13 = t2 = None
+            for q in members:
+                if q == r:
+                    g13, g2 = dw13[sl], dw2[sl]
+                else:
+                    base = off[q] + shared[q][r].index(e) * per
+                    g13 = recv[base: base + n13].view(shp13)
+                    g2 = recv[base + n13: base + per].view(shp2)
+                t13 = g13.clone() if t13 is None else t13.add_(g13)
+                t2 = g2.clone() if t2 is None else t2.add_(g2)
+            dw13[sl].copy_(t13)
+            dw2[sl].copy_(t2)

@@ -59,3 +59,60 @@ def test_dist_comm_matches_local_comm(world):
     for p in procs:
         p.join(timeout=60)
     assert all(res.values()), res
+
+
+def _grads(world, E, seed):
+    from paper_2511_16947_b200.core import ClusterShape
+    from paper_2511_16947_b200.placement import greedy_replica_counts, monte_carlo_placement
+
+    shape = ClusterShape(world, E, 2)
+    loads = [(e * 37) % 11 + 1 for e in range(E)]
+    pl = monte_carlo_placement(loads, greedy_replica_counts(loads, 2 * E, max_count=world), shape, 8, seed)
+    n_slots = max(max(pl.slots[e] for e in h) + 1 if h else 1 for h in pl.hosted)
+    g = torch.Generator().manual_seed(seed)
+    dw13 = [torch.randn(n_slots, 4, 3, generator=g) for _ in range(world)]
+    dw2 = [torch.randn(n_slots, 3, 2, generator=g) for _ in range(world)]
+    return pl, dw13, dw2
+
+
+def _edp_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2511_16947_b200.ep import DistComm, LocalComm, edp_reduce
+
+        pl, dw13, dw2 = _grads(world, 6, 3)
+        # expected: sum over the replicas of each expert, identical on every replica
+        exp13 = {e: sum(dw13[r][pl.slots[e]] for r in sorted(set(pl.edp_groups[e]))) for e in range(pl.num_experts)}
+        exp2 = {e: sum(dw2[r][pl.slots[e]] for r in sorted(set(pl.edp_groups[e]))) for e in range(pl.num_experts)}
+        loc13, loc2 = [t.clone() for t in dw13], [t.clone() for t in dw2]
+        edp_reduce(pl, LocalComm(world), list(range(world)), loc13, loc2)
+        mine13, mine2 = dw13[rank].clone(), dw2[rank].clone()
+        edp_reduce(pl, DistComm(), [rank], [mine13], [mine2])
+        ok = torch.equal(mine13, loc13[rank]) and torch.equal(mine2, loc2[rank])
+        for e in pl.hosted[rank]:
+            sl = pl.slots[e]
+            ok = ok and torch.allclose(mine13[sl], exp13[e]) and torch.allclose(mine2[sl], exp2[e])
+        red = torch.full((3,), float(rank + 1))
+        DistComm().all_reduce([red])
+        ok = ok and torch.equal(red, torch.full((3,), float(world * (world + 1) // 2)))
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_edp_gradient_reduction_over_gloo(world):
+    """The expert-gradient reduction inside each EDP group (one all-to-all-v of the
+    shared experts' gradients) gives, on every replica, the sum over the replicas
+    — the same bits as the single-process LocalComm run."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_edp_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res.values()), res
