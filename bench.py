@@ -310,6 +310,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-train", action="store_true", help="skip the forward+backward training-step measurement")
+    ap.add_argument("--pipeline-ratio", type=float, default=None,
+                    help="harmony_pipelined: share of tokens through the exact scheduler (rest split statically)")
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of a CUDA-graph replay")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu legs)")
     args = ap.parse_args()
@@ -339,7 +341,7 @@ def main():
     shape = P.ClusterShape(G, E, 2)
     pl = P.cayley_symmetric(shape)
     bias = torch.tensor(P.zipf_gate_bias(E, args.skew, 0)) if args.skew > 0 else None
-    layer = P.MoELayer(pl, d, F, K, seed=0, gate_bias=bias, device=dev)
+    layer = P.MoELayer(pl, d, F, K, seed=0, gate_bias=bias, device=dev, pipeline_ratio=args.pipeline_ratio)
     gx = torch.Generator(device=dev).manual_seed(1000 + rank)
     x = torch.randn(T, d, generator=gx, device=dev).to(torch.bfloat16)
     bufs = layer.buffers(T)
@@ -564,6 +566,8 @@ def main():
                 "tokens_per_virtual_gpu": T // G,
                 "top_k": K, "d_model": d, "ffn": F, "experts": E,
                 "placement": placement_desc,
+                "schedule": ("harmony" if args.pipeline_ratio is None
+                             else f"harmony_pipelined (pipeline_ratio={args.pipeline_ratio})"),
                 "zipf_s": args.skew,
                 "pass": "forward",
                 "launch": "cuda-graph replay" if graph is not None else "eager",

@@ -117,6 +117,22 @@ int hep_sched_integerize(hep_sched_t h, const int64_t *d_xnum, int64_t den, cons
  */
 int hep_sched_route(hep_sched_t h, const int64_t *d_loads, int64_t stride_e, int64_t stride_g,
                     const int64_t *d_xi, int flags, const hep_sched_out *out, void *stream);
+/*
+ * Pipelined split (the reference's harmony_pipelined strategy, simulator.py:420-435):
+ *   former = floor(loads * share_num / share_den), latter = loads - former   (_split_loads :291-298)
+ *   static phase:    even split of each expert's former total over its replicas
+ *                    (_even_split_plan :301-322), integerized, routed, transfer plan -> *former
+ *   scheduled phase: exact solve of latter with gpu_base = the static phase's integerized
+ *                    GPU loads, integerize, route, transfer                          -> *latter
+ * share = 1 - pipeline_ratio (:375).  d_split: caller buffer int64 [2][E][G] (former,
+ * latter; expert-major) that the route stages read.  The static phase's outputs are
+ * final before the scheduled phase's solve starts (same stream), so its dispatch can be
+ * issued on another stream right after the first two launches.  The phases need
+ * distinct d_status words.  flags: TRANSFER / TOPO as for hep_sched_solve.
+ */
+int hep_sched_pipelined(hep_sched_t h, const int64_t *d_loads, int64_t stride_e, int64_t stride_g, int64_t share_num,
+                        int64_t share_den, int flags, int64_t *d_split, const hep_sched_out *former,
+                        const hep_sched_out *latter, void *stream);
 /* Diagnostics: per-phase SM clock stamps of the last HEP_SCHED_PROFILE launch (n <= 16). */
 int hep_sched_debug_timing(int64_t *host_out, int n);
 /* Aggregate an arbitrary routing table. Replaces build_transfer_plan (router.py:178-226). */
@@ -169,6 +185,20 @@ int hep_moe_assign(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_t
                    int64_t tokens_per_src, int row_align, int32_t *d_tok_row, int32_t *d_row_tok, int32_t *d_seg,
                    int64_t *d_expert_rows, void *workspace, size_t workspace_bytes, void *stream);
 size_t hep_moe_assign_workspace(hep_sched_t h, int64_t T, int K);
+/*
+ * K4 for one phase of the pipelined split (hep_sched_pipelined): the assignments of
+ * (expert e, source src) whose rank q (sequence order) lies in this phase's window
+ * [rank_base[e][src], rank_base[e][src] + this phase's count) get rows; the others are
+ * left untouched.  Static phase: d_rank_base = d_row_base = NULL (window starts at 0);
+ * scheduled phase: d_rank_base = the static share [E][G] (d_split), d_row_base = the
+ * static phase's d_expert_rows + E (its row count), so the receive buffer is
+ * [phase][expert][dst][src][rank] and the static phase's rows are final before the
+ * scheduled phase is solved.  Same workspace as hep_moe_assign; row_align = 1.
+ */
+int hep_moe_assign_phase(hep_sched_t h, const hep_sched_out *sched, const int64_t *d_rank_base,
+                         const int64_t *d_row_base, const int32_t *d_topk_idx, int64_t T, int K, int64_t tokens_per_src,
+                         int32_t *d_tok_row, int32_t *d_row_tok, int32_t *d_seg, int64_t *d_expert_rows,
+                         void *workspace, size_t workspace_bytes, void *stream);
 
 /*
  * K4 for one rank of a real EP group (one process per GPU, rank r = source r

@@ -82,6 +82,44 @@ def receive_rows(groups, G: int, xi, ranges, topk_idx: np.ndarray, tps: int):
     return tok_row, expert_rows
 
 
+def receive_rows_pipelined(groups, G: int, former, latter, former_loads, topk_idx: np.ndarray, tps: int):
+    """Pipelined split (simulator.py:420-435) receive layout [phase][expert][dst][src][rank]:
+    within (expert, src) the first former_loads[e][src] assignments in token order
+    belong to the static phase (its ranges), the rest to the scheduled phase (its
+    ranges, ranks continuing).  ``former`` / ``latter`` = dict(xi=..., ranges=...)."""
+    T, K = topk_idx.shape
+    E = len(groups)
+    lists = {}
+    row0 = 0
+    for ph, plan in enumerate((former, latter)):
+        base = {}
+        row = row0
+        for e in range(E):
+            for dst in sorted(groups[e]):
+                base[(e, dst)] = row
+                row += plan["xi"][e][list(groups[e]).index(dst)]
+        by_e = {}
+        for (e, s, d, c) in plan["ranges"]:
+            by_e.setdefault(e, []).append((s, d, c))
+        for e, rs in by_e.items():
+            for j, (s, d, c) in enumerate(rs):
+                r = base[(e, d)] + sum(c2 for (s2, d2, c2) in rs if d2 == d and s2 < s)
+                rank = (former_loads[e][s] if ph else 0) + sum(c2 for (s2, d2, c2) in rs[:j] if s2 == s)
+                lists.setdefault((e, s), []).append((rank, rank + c, r - rank))
+        row0 = row
+    tok_row = np.zeros((T, K), dtype=np.int64)
+    ctr = {}
+    for t in range(T):
+        s = min(t // tps, G - 1)
+        for k in range(K):
+            e = int(topk_idx[t, k])
+            q = ctr.get((e, s), 0)
+            ctr[(e, s)] = q + 1
+            (hit,) = [lst for lst in lists[(e, s)] if lst[0] <= q < lst[1]]
+            tok_row[t, k] = q + hit[2]
+    return tok_row, row0
+
+
 def bf16_round(a: np.ndarray) -> np.ndarray:
     """Round fp32 -> bf16 (round to nearest even) -> fp32."""
     a = np.ascontiguousarray(a, dtype=np.float32)

@@ -32,6 +32,7 @@ struct AssignWs {
     int32_t *chunk_cnt; // [n_src * n_chunks * E]
     int32_t *cnt3;      // [E*G*G] range count of (expert, src, dst)   (EP rank view)
     int32_t *sbase;     // [E*G]   send-buffer base of (expert, dst)   (EP rank view)
+    int32_t *es_lo;     // [E*G]   first rank of (e, src) in this phase (pipelined split)
 };
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -48,6 +49,7 @@ static size_t assign_ws_bytes(const hep_sched *h, int64_t T, int n_src, int64_t 
     b += align256(4 * (size_t)(n_src * ncs * E));
     b += align256(4 * (size_t)(E * G * G));
     b += align256(4 * (size_t)(E * G));
+    b += align256(4 * (size_t)(E * G));
     return b;
 }
 
@@ -63,7 +65,8 @@ static AssignWs carve_ws(const hep_sched *h, void *ws, int n_src, int64_t tps) {
     w.first = (int32_t *)p; p += align256(4 * (size_t)(E + 1));
     w.chunk_cnt = (int32_t *)p; p += align256(4 * (size_t)(n_src * ((tps + kChunk - 1) / kChunk) * E));
     w.cnt3 = (int32_t *)p; p += align256(4 * (size_t)(E * G * G));
-    w.sbase = (int32_t *)p;
+    w.sbase = (int32_t *)p; p += align256(4 * (size_t)(E * G));
+    w.es_lo = (int32_t *)p;
     return w;
 }
 
@@ -71,11 +74,16 @@ static AssignWs carve_ws(const hep_sched *h, void *ws, int n_src, int64_t tps) {
 __global__ void plan_prep_kernel(int G, int E, int nnz, const int32_t *grp_off, const int32_t *grp_gpu,
                                  const int32_t *sorted, const int32_t *nnz_exp, const int64_t *xi,
                                  const int64_t *ranges, const int64_t *n_ranges_p, int64_t *expert_rows,
-                                 int32_t *seg, AssignWs w, int32_t *status, int row_align) {
+                                 int32_t *seg, AssignWs w, int32_t *status, int row_align,
+                                 const int64_t *rank_base, const int64_t *row_base_p) {
     __shared__ int64_t scan[64];
     const int tid = threadIdx.x, nt = blockDim.x;
     const int64_t n_ranges = *n_ranges_p;
-    for (int i = tid; i < E * G; i += nt) w.es_cnt[i] = 0;
+    const int64_t row_off = row_base_p ? *row_base_p : 0;  // phase block start (pipelined split)
+    for (int i = tid; i < E * G; i += nt) {
+        w.es_cnt[i] = 0;
+        w.es_lo[i] = rank_base ? (int32_t)rank_base[i] : 0;
+    }
     for (int i = tid; i <= E; i += nt) w.first[i] = -1;
     // expert blocks ([expert][dst asc][src][rank]), each starting on a row_align boundary
     // (64 in training so weight-gradient GEMMs contract over whole 64-row blocks)
@@ -88,7 +96,8 @@ __global__ void plan_prep_kernel(int G, int E, int nnz, const int32_t *grp_off, 
         mine += (n + row_align - 1) / row_align * row_align;
     }
     int64_t total;
-    int64_t row = block_excl_scan_i64(mine, scan, &total);
+    int64_t row = block_excl_scan_i64(mine, scan, &total) + row_off;
+    total += row_off;
     for (int e = e0; e < e1; ++e) {
         expert_rows[e] = row;
         int64_t r = row;
@@ -125,7 +134,7 @@ __global__ void plan_prep_kernel(int G, int E, int nnz, const int32_t *grp_off, 
             for (int i = grp_off[e]; i < grp_off[e + 1]; ++i)
                 if (grp_gpu[i] == dst) nz = i;
             if (nz < 0) { atomicCAS(status, 0, HEP_E_CONTRACT); continue; }
-            int64_t row = w.row_base[nz], rank = 0;
+            int64_t row = w.row_base[nz], rank = w.es_lo[e * G + src];
             for (int k = r0; k < r1; ++k) {
                 const int ks = (int)ranges[4 * k + 1], kd = (int)ranges[4 * k + 2];
                 if (kd == dst && ks < src) row += ranges[4 * k + 3];
@@ -171,12 +180,13 @@ __global__ void chunk_scan_kernel(int n_src, int ncs, int E, int32_t *chunk_cnt)
 // one warp per chunk; lanes k < K own pick k of each token (distinct experts)
 __global__ void chunk_map_kernel(const int32_t *topk_idx, int K, int E, int G, int64_t tps, int64_t T, int ncs,
                                  const int32_t *chunk_cnt, AssignWs w, int32_t *tok_row, int32_t *row_tok,
-                                 int src_base) {
+                                 int src_base, bool windowed) {
     extern __shared__ int32_t sm[];
     int32_t *ctr = sm;                // [E]
     int32_t *l_cnt = ctr + E;         // [E]
     int32_t *l_end = l_cnt + E;       // [E*G]
     int32_t *l_delta = l_end + E * G; // [E*G]
+    int32_t *l_lo = l_delta + E * G;  // [E] (windowed: first rank of this phase)
     const int src = blockIdx.x / ncs, c = blockIdx.x % ncs;
     const int lane = threadIdx.x;
     for (int e = lane; e < E; e += 32) {
@@ -184,6 +194,7 @@ __global__ void chunk_map_kernel(const int32_t *topk_idx, int K, int E, int G, i
         const int es = e * G + src_base + src;
         const int n = w.es_cnt[es];
         l_cnt[e] = n;
+        if (windowed) l_lo[e] = w.es_lo[es];
         for (int j = 0; j < n; ++j) {
             l_end[e * G + j] = w.es_end[es * G + j];
             l_delta[e * G + j] = w.es_delta[es * G + j];
@@ -200,10 +211,14 @@ __global__ void chunk_map_kernel(const int32_t *topk_idx, int K, int E, int G, i
             const int q = ctr[e]++;
             int j = 0;
             const int n = l_cnt[e];
-            while (j + 1 < n && q >= l_end[e * G + j]) ++j;
-            const int row = q + l_delta[e * G + j];
-            tok_row[t * K + lane] = row;
-            if (row_tok) row_tok[row] = (int32_t)t;
+            // pipelined split: this phase owns ranks [lo, end of its last range) of (e, src)
+            const bool mine = !windowed || (n > 0 && q >= l_lo[e] && q < l_end[e * G + n - 1]);
+            if (mine) {
+                while (j + 1 < n && q >= l_end[e * G + j]) ++j;
+                const int row = q + l_delta[e * G + j];
+                tok_row[t * K + lane] = row;
+                if (row_tok) row_tok[row] = (int32_t)t;
+            }
         }
         __syncwarp();
     }
@@ -389,10 +404,10 @@ extern "C" size_t hep_moe_assign_workspace(hep_sched_t h, int64_t T, int K) {
     return assign_ws_bytes(h, T, n_src, tps > 0 ? tps : 1);
 }
 
-extern "C" int hep_moe_assign(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_topk_idx, int64_t T, int K,
-                              int64_t tokens_per_src, int row_align, int32_t *d_tok_row, int32_t *d_row_tok,
-                              int32_t *d_seg, int64_t *d_expert_rows, void *workspace, size_t workspace_bytes,
-                              void *stream) {
+static int assign_impl(hep_sched_t h, const hep_sched_out *sched, bool windowed, const int64_t *d_rank_base,
+                       const int64_t *d_row_base, const int32_t *d_topk_idx, int64_t T, int K, int64_t tokens_per_src,
+                       int row_align, int32_t *d_tok_row, int32_t *d_row_tok, int32_t *d_seg, int64_t *d_expert_rows,
+                       void *workspace, size_t workspace_bytes, void *stream) {
     HEP_REQUIRE(row_align >= 1 && row_align <= 1024, HEP_E_DIMENSION, "row_align=%d", row_align);
     HEP_REQUIRE(h && sched && d_topk_idx && d_tok_row && d_row_tok && d_seg && d_expert_rows && workspace,
                 HEP_E_CONTRACT, "hep_moe_assign: null argument");
@@ -407,7 +422,7 @@ extern "C" int hep_moe_assign(hep_sched_t h, const hep_sched_out *sched, const i
     const int E = h->E, G = h->G;
     plan_prep_kernel<<<1, 512, 0, s>>>(G, E, h->nnz, h->d_grp_off, h->d_grp_gpu, h->d_sorted, h->d_nnz_exp,
                                        sched->d_xi, sched->d_ranges, sched->d_n_ranges, d_expert_rows, d_seg, w,
-                                       sched->d_status, row_align);
+                                       sched->d_status, row_align, d_rank_base, d_row_base);
     HEP_CHECK_LAUNCH();
     if (T <= 0) return HEP_OK;
     const int ncs = (int)((tokens_per_src + kChunk - 1) / kChunk);
@@ -416,13 +431,29 @@ extern "C" int hep_moe_assign(hep_sched_t h, const hep_sched_out *sched, const i
     HEP_CHECK_LAUNCH();
     chunk_scan_kernel<<<(n_src * E + 255) / 256, 256, 0, s>>>(n_src, ncs, E, w.chunk_cnt);
     HEP_CHECK_LAUNCH();
-    const size_t sm = sizeof(int32_t) * (2 * (size_t)E + 2 * (size_t)E * G);
+    const size_t sm = sizeof(int32_t) * (3 * (size_t)E + 2 * (size_t)E * G);
     HEP_REQUIRE(sm <= 200 * 1024, HEP_E_CAPACITY, "chunk_map smem %zu", sm);
     if (sm > 48 * 1024) HEP_CHECK_CUDA(cudaFuncSetAttribute(chunk_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     chunk_map_kernel<<<nblk, 32, sm, s>>>(d_topk_idx, K, E, G, tokens_per_src, T, ncs, w.chunk_cnt, w, d_tok_row,
-                                          d_row_tok, 0);
+                                          d_row_tok, 0, windowed);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
+}
+
+extern "C" int hep_moe_assign(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_topk_idx, int64_t T, int K,
+                              int64_t tokens_per_src, int row_align, int32_t *d_tok_row, int32_t *d_row_tok,
+                              int32_t *d_seg, int64_t *d_expert_rows, void *workspace, size_t workspace_bytes,
+                              void *stream) {
+    return assign_impl(h, sched, false, nullptr, nullptr, d_topk_idx, T, K, tokens_per_src, row_align, d_tok_row, d_row_tok,
+                       d_seg, d_expert_rows, workspace, workspace_bytes, stream);
+}
+
+extern "C" int hep_moe_assign_phase(hep_sched_t h, const hep_sched_out *sched, const int64_t *d_rank_base,
+                                    const int64_t *d_row_base, const int32_t *d_topk_idx, int64_t T, int K,
+                                    int64_t tokens_per_src, int32_t *d_tok_row, int32_t *d_row_tok, int32_t *d_seg,
+                                    int64_t *d_expert_rows, void *workspace, size_t workspace_bytes, void *stream) {
+    return assign_impl(h, sched, true, d_rank_base, d_row_base, d_topk_idx, T, K, tokens_per_src, 1, d_tok_row, d_row_tok,
+                       d_seg, d_expert_rows, workspace, workspace_bytes, stream);
 }
 
 extern "C" int hep_moe_permute(const void *d_x, const int32_t *d_tok_row, int64_t T, int K, int64_t d_model,
@@ -510,7 +541,7 @@ extern "C" int hep_moe_assign_ep(hep_sched_t h, const hep_sched_out *sched, cons
     HEP_REQUIRE(sm <= 200 * 1024, HEP_E_CAPACITY, "chunk_map smem %zu", sm);
     if (sm > 48 * 1024)
         HEP_CHECK_CUDA(cudaFuncSetAttribute(chunk_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    chunk_map_kernel<<<ncs, 32, sm, s>>>(d_topk_idx, K, E, G, tps, T, ncs, w.chunk_cnt, w, d_tok_row, nullptr, rank);
+    chunk_map_kernel<<<ncs, 32, sm, s>>>(d_topk_idx, K, E, G, tps, T, ncs, w.chunk_cnt, w, d_tok_row, nullptr, rank, false);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
 }

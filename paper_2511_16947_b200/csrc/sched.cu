@@ -54,6 +54,7 @@ struct SchedArgs {
     int64_t se, sg;
     const int64_t *base;
     const int64_t *xi_in;  // route-only: caller plan (global)
+    int status_in;         // keep an error already in out.d_status (set by a preceding kernel)
     hep_sched_out out;
 };
 
@@ -463,7 +464,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
     }
     for (int i = tid; i < G * G; i += nt) s.pair[i] = 0;
     for (int g = tid; g < G; g += nt) s.gpu_load[g] = 0;
-    if (tid == 0) *status = 0;
+    if (tid == 0 && !a.status_in) *status = 0;
     __syncthreads();
     if (bad) set_status(status, HEP_E_CONTRACT);
     int64_t my_total = 0;
@@ -974,6 +975,75 @@ extern "C" int hep_sched_route(hep_sched_t h, const int64_t *d_loads, int64_t st
     a.den = 1;
     a.out = *out;
     return launch_sched(h, a, (cudaStream_t)stream);
+}
+
+namespace hep {
+// Pipelined split (simulator.py:291-322): former = floor(v * num / den), latter = v - former
+// ([E][G] each, expert-major), and the static phase's even plan over each expert's replicas
+// as numerators over Q (Q/n is integral: n <= G).  One thread per expert.
+__global__ void split_kernel(const int64_t *loads, int64_t se, int64_t sg, int E, int G, int64_t num, int64_t den,
+                             const int32_t *grp_off, int64_t Q, int64_t *former, int64_t *latter, int64_t *xq_former,
+                             int32_t *status) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    int64_t tot = 0;
+    for (int g = 0; g < G; ++g) {
+        const int64_t v = loads[(int64_t)e * se + (int64_t)g * sg];
+        if (v < 0) { atomicCAS(status, 0, HEP_E_CONTRACT); return; }
+        const int64_t f = (int64_t)(((__int128)v * num) / den);
+        former[(int64_t)e * G + g] = f;
+        latter[(int64_t)e * G + g] = v - f;
+        tot += f;
+    }
+    const int b = grp_off[e], n = grp_off[e + 1] - b;
+    if (n == 0) {
+        if (tot) atomicCAS(status, 0, HEP_E_CONTRACT);  // "expert has load but no replicas" (:312-314)
+        return;
+    }
+    const int64_t x = tot * (Q / n);
+    for (int k = 0; k < n; ++k) xq_former[b + k] = x;
+}
+}  // namespace hep
+
+extern "C" int hep_sched_pipelined(hep_sched_t h, const int64_t *d_loads, int64_t stride_e, int64_t stride_g,
+                                   int64_t share_num, int64_t share_den, int flags, int64_t *d_split,
+                                   const hep_sched_out *former, const hep_sched_out *latter, void *stream) {
+    HEP_REQUIRE(h && d_loads && d_split && former && latter, HEP_E_CONTRACT, "hep_sched_pipelined: null argument");
+    HEP_REQUIRE(former->d_status && latter->d_status && former->d_status != latter->d_status, HEP_E_CONTRACT,
+                "hep_sched_pipelined: the two phases need distinct d_status words");
+    HEP_REQUIRE(share_den > 0 && share_num >= 0 && share_num <= share_den, HEP_E_CONTRACT,
+                "static share %lld/%lld outside [0, 1]", (long long)share_num, (long long)share_den);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int E = h->E, G = h->G;
+    int64_t *f_loads = d_split, *l_loads = d_split + (int64_t)E * G;
+    HEP_CHECK_CUDA(cudaMemsetAsync(former->d_status, 0, sizeof(int32_t), s));
+    if (E > 0) {
+        split_kernel<<<(E + 127) / 128, 128, 0, s>>>(d_loads, stride_e, stride_g, E, G, share_num, share_den,
+                                                     h->d_grp_off, h->Q, f_loads, l_loads, former->d_xq,
+                                                     former->d_status);
+        HEP_CHECK_LAUNCH();
+    }
+    // static phase: integerize the even plan, route, transfer (no solve)
+    SchedArgs a{};
+    a.flags = HEP_SCHED_INTEGERIZE | HEP_SCHED_ROUTE | (flags & (HEP_SCHED_TRANSFER | HEP_SCHED_TOPO));
+    a.loads = f_loads;
+    a.se = G;
+    a.sg = 1;
+    a.den = h->Q;
+    a.status_in = 1;
+    a.out = *former;
+    int rc = launch_sched(h, a, s);
+    if (rc) return rc;
+    // scheduled phase: exact solve with the static phase's GPU loads as gpu_base
+    SchedArgs b{};
+    b.flags = (flags & HEP_SCHED_ALL) | HEP_SCHED_SOLVE;
+    b.loads = l_loads;
+    b.se = G;
+    b.sg = 1;
+    b.base = former->d_gpu_load;
+    b.den = h->Q;
+    b.out = *latter;
+    return launch_sched(h, b, s);
 }
 
 extern "C" int hep_transfer_plan(int num_gpus, int gpus_per_node, const int64_t *d_ranges, int64_t n_ranges,

@@ -30,6 +30,7 @@ SwiGLU FFN  y = (silu(x W1^T) * (x W3^T)) W2^T  with a bf16 intermediate.
 from __future__ import annotations
 
 import ctypes
+from fractions import Fraction
 
 import torch
 
@@ -67,7 +68,7 @@ class MoEBuffers:
     path allocates nothing; CUDA-graph capturable)."""
 
     def __init__(self, sched: DeviceScheduler, T: int, K: int, E: int, e_pad: int, d_model: int, ffn: int, device,
-                 train: bool = False):
+                 train: bool = False, pipelined: bool = False):
         L = _lib.lib()
         G = sched.G
         # training keeps every expert block 64-row aligned (weight-gradient GEMMs contract
@@ -85,14 +86,17 @@ class MoEBuffers:
         self.hist = torch.zeros(G, E, dtype=torch.int64, device=device)
         self.tok_row = torch.empty(T, K, **i32)
         self.row_tok = torch.empty(max(R, 1), **i32)
-        self.seg = torch.empty(max(sched.nnz, 1), 4, **i32)
+        # pipelined split: [phase][expert][dst][src][rank], one segment list per phase
+        self.n_seg = sched.nnz * (2 if pipelined else 1)
+        self.seg = torch.empty(max(self.n_seg, 1), 4, **i32)
         self.expert_rows = torch.empty(E + 1, dtype=torch.int64, device=device)
+        self.expert_rows2 = torch.empty(E + 1, dtype=torch.int64, device=device) if pipelined else None
         ws = L.hep_moe_assign_workspace(sched.handle, T, K)
         self.assign_ws = torch.empty(max(int(ws), 256), dtype=torch.uint8, device=device)
         self.rows = alloc(max(R, 1), d_model, **bf)
         self.h = alloc(max(R, 1), ffn, **bf)
         self.y = alloc(max(R, 1), d_model, **bf)
-        fws = L.hep_moe_ffn_workspace(max(sched.nnz, 1), R, E)
+        fws = L.hep_moe_ffn_workspace(max(self.n_seg, 1), R, E)
         self.ffn_ws = torch.empty(max(int(fws), 256), dtype=torch.uint8, device=device)
         self.out = torch.empty(T, d_model, **bf)
         self.pre = torch.zeros(max(R, 1), 2 * ffn, **bf) if train else None
@@ -103,9 +107,21 @@ class MoELayer(torch.nn.Module):
     GPUs, forward pass entirely in sm_100a kernels."""
 
     def __init__(self, placement: Placement, d_model: int, ffn: int, top_k: int, *, seed: int = 0,
-                 gate_bias: torch.Tensor | None = None, device=None, train: bool = False):
+                 gate_bias: torch.Tensor | None = None, device=None, train: bool = False,
+                 pipeline_ratio: float | Fraction | None = None):
         super().__init__()
         self.train_mode = train
+        # harmony_pipelined (simulator.py:17-20, :375, :420-435): a 1 - pipeline_ratio
+        # static share is split evenly over each expert's replicas and assigned before
+        # the scheduled share is solved (gpu_base = the static share's GPU loads)
+        self.static_share = None
+        if pipeline_ratio is not None:
+            if not (0.0 < float(pipeline_ratio) <= 1.0):
+                raise ValueError("pipeline_ratio must be in (0, 1]")  # SimulationConfig (simulator.py:117-118)
+            if train:
+                raise ValueError("the pipelined split is a forward (serving) schedule; train with pipeline_ratio=None")
+            self.static_share = Fraction(1) - Fraction(pipeline_ratio)
+        self.LAUNCHES_PER_FORWARD = 12 if self.static_share is None else 18
         torch_ = _lib.require_cuda()
         self.device = torch_.device("cuda", torch_.cuda.current_device()) if device is None else torch_.device(device)
         self.placement = placement
@@ -148,7 +164,8 @@ class MoELayer(torch.nn.Module):
     def buffers(self, T: int) -> MoEBuffers:
         b = self._bufs.get(T)
         if b is None:
-            b = MoEBuffers(self.sched, T, self.K, self.E, self.e_pad, self.d, self.F, self.device, self.train_mode)
+            b = MoEBuffers(self.sched, T, self.K, self.E, self.e_pad, self.d, self.F, self.device, self.train_mode,
+                           self.static_share is not None)
             self._bufs[T] = b
         return b
 
@@ -192,13 +209,29 @@ class MoELayer(torch.nn.Module):
         mark("gate", 1)
         # hist is [G][E] (source-major, the all-gather layout): stride_e = 1, stride_g = E
         mark("sched", 0)
-        ck(L.hep_sched_solve(self.sched.handle, b.hist.data_ptr(), 1, E, None, HEP_SCHED_ALL,
-                             ctypes.byref(self.sched.out), s), "hep_sched_solve")
+        if self.static_share is None:
+            ck(L.hep_sched_solve(self.sched.handle, b.hist.data_ptr(), 1, E, None, HEP_SCHED_ALL,
+                                 ctypes.byref(self.sched.out), s), "hep_sched_solve")
+        else:
+            self.sched.launch_pipelined(b.hist, 1, E, self.static_share, HEP_SCHED_ALL, st)
         mark("sched", 1)
         mark("assign", 0)
-        ck(L.hep_moe_assign(self.sched.handle, ctypes.byref(self.sched.out), b.topk_idx.data_ptr(), T, K, tps,
-                            b.row_align, b.tok_row.data_ptr(), b.row_tok.data_ptr(), b.seg.data_ptr(), b.expert_rows.data_ptr(),
-                            b.assign_ws.data_ptr(), b.assign_ws.numel(), s), "hep_moe_assign")
+        if self.static_share is None:
+            ck(L.hep_moe_assign(self.sched.handle, ctypes.byref(self.sched.out), b.topk_idx.data_ptr(), T, K, tps,
+                                b.row_align, b.tok_row.data_ptr(), b.row_tok.data_ptr(), b.seg.data_ptr(),
+                                b.expert_rows.data_ptr(), b.assign_ws.data_ptr(), b.assign_ws.numel(), s),
+               "hep_moe_assign")
+        else:
+            nnz = self.sched.nnz
+            ck(L.hep_moe_assign_phase(self.sched.handle, ctypes.byref(self.sched.former.out), None, None,
+                                      b.topk_idx.data_ptr(), T, K, tps, b.tok_row.data_ptr(), b.row_tok.data_ptr(),
+                                      b.seg.data_ptr(), b.expert_rows.data_ptr(), b.assign_ws.data_ptr(),
+                                      b.assign_ws.numel(), s), "hep_moe_assign_phase(static)")
+            ck(L.hep_moe_assign_phase(self.sched.handle, ctypes.byref(self.sched.out), self.sched.split.data_ptr(),
+                                      b.expert_rows.data_ptr() + 8 * E, b.topk_idx.data_ptr(), T, K, tps,
+                                      b.tok_row.data_ptr(), b.row_tok.data_ptr(), b.seg.data_ptr() + 16 * nnz,
+                                      b.expert_rows2.data_ptr(), b.assign_ws.data_ptr(), b.assign_ws.numel(), s),
+               "hep_moe_assign_phase(scheduled)")
         mark("assign", 1)
         mark("permute", 0)
         ck(L.hep_moe_permute(x.data_ptr(), b.tok_row.data_ptr(), T, K, self.d, b.rows.data_ptr(), s),
@@ -207,7 +240,7 @@ class MoELayer(torch.nn.Module):
         mark("ffn", 0)
         if b.pre is None:
             ck(L.hep_moe_expert_ffn(b.rows.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(), b.seg.data_ptr(),
-                                    self.sched.nnz, b.R, self.d, self.F, E, b.h.data_ptr(), b.y.data_ptr(),
+                                    b.n_seg, b.R, self.d, self.F, E, b.h.data_ptr(), b.y.data_ptr(),
                                     b.ffn_ws.data_ptr(), b.ffn_ws.numel(), self.sched.status.data_ptr(), s),
                "hep_moe_expert_ffn")
         else:
@@ -238,7 +271,8 @@ class MoELayer(torch.nn.Module):
         return g
 
     # kernels launched per forward: router GEMM, gate top-K, scheduler, assign x4,
-    # permute, FFN (tile list + 2 GEMMs), combine
+    # permute, FFN (tile list + 2 GEMMs), combine (pipelined split: + split kernel,
+    # second scheduler launch, second assignment x4)
     LAUNCHES_PER_FORWARD = 12
 
     def check_status(self):
@@ -334,8 +368,8 @@ class HostPipeline:
         self.T = T
         self.depth = depth
         self.x_dev = [torch.empty(T, layer.d, dtype=torch.bfloat16, device=dev) for _ in range(depth)]
-        self.bufs = [MoEBuffers(layer.sched, T, layer.K, layer.E, layer.e_pad, layer.d, layer.F, dev)
-                     for _ in range(depth)]
+        self.bufs = [MoEBuffers(layer.sched, T, layer.K, layer.E, layer.e_pad, layer.d, layer.F, dev,
+                                pipelined=layer.static_share is not None) for _ in range(depth)]
         self.out_host = [torch.empty(T, layer.d, dtype=torch.bfloat16).pin_memory() for _ in range(depth)]
         self.s_in = torch.cuda.Stream(device=dev)
         self.s_comp = torch.cuda.Stream(device=dev)

@@ -142,6 +142,7 @@ class DeviceScheduler:
             self.m.data_ptr(), self.xq.data_ptr(), self.xi.data_ptr(), self.gpu_load.data_ptr(),
             self.ranges.data_ptr(), self.n_ranges.data_ptr(), self.transfer.data_ptr(), self.status.data_ptr(),
         )
+        self.former: SchedBuffers | None = None  # static phase of the pipelined split
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -177,8 +178,28 @@ class DeviceScheduler:
             "hep_sched_route",
         )
 
+    def launch_pipelined(self, d_loads, stride_e: int, stride_g: int, share, flags: int = HEP_SCHED_ALL, stream=None):
+        """Pipelined split (``simulator.py:420-435``): the static share's phase goes to
+        ``self.former`` (a ``SchedBuffers``), the scheduled share's to this object.
+        ``share`` = static share as a Fraction (1 - pipeline_ratio)."""
+        share = Fraction(share)
+        if self.former is None:
+            self.former = SchedBuffers(self)
+            self.split = _lib.require_cuda().zeros(2 * max(self.E * self.G, 1), dtype=_lib.require_cuda().int64,
+                                                   device=self.device)
+        _lib.check(
+            _lib.lib().hep_sched_pipelined(
+                self._h, d_loads.data_ptr(), stride_e, stride_g, share.numerator, share.denominator, flags,
+                self.split.data_ptr(), ctypes.byref(self.former.out), ctypes.byref(self.out),
+                _lib.stream_handle(stream),
+            ),
+            "hep_sched_pipelined",
+        )
+
     def check_status(self, where: str):
         _lib.raise_status(int(self.status.item()), where)
+        if self.former is not None:
+            _lib.raise_status(int(self.former.status.item()), where + " (static phase)")
 
     # -- host views (synchronising; inspection / parity API only) ---------
     def rows(self, t) -> list[list[int]]:
@@ -191,6 +212,32 @@ class DeviceScheduler:
             return ()
         arr = self.ranges[: 4 * n].view(n, 4).cpu().tolist()
         return tuple(tuple(r) for r in arr)
+
+
+class SchedBuffers:
+    """A second set of ``hep_sched_out`` buffers on the same placement (the
+    static phase of the pipelined split); same field names and host views as
+    ``DeviceScheduler``."""
+
+    def __init__(self, ds: DeviceScheduler):
+        torch = _lib.require_cuda()
+        self.E, self.G, self.nnz, self.off = ds.E, ds.G, ds.nnz, ds.off
+        i64 = dict(dtype=torch.int64, device=ds.device)
+        self.m = torch.zeros(4, **i64)
+        self.xq = torch.zeros(max(ds.nnz, 1), **i64)
+        self.xi = torch.zeros(max(ds.nnz, 1), **i64)
+        self.gpu_load = torch.zeros(ds.G, **i64)
+        self.ranges = torch.zeros(4 * ds.max_ranges, **i64)
+        self.n_ranges = torch.zeros(1, **i64)
+        self.transfer = torch.zeros(ds.tlen, **i64)
+        self.status = torch.zeros(1, dtype=torch.int32, device=ds.device)
+        self.out = _lib.HepSchedOut(
+            self.m.data_ptr(), self.xq.data_ptr(), self.xi.data_ptr(), self.gpu_load.data_ptr(),
+            self.ranges.data_ptr(), self.n_ranges.data_ptr(), self.transfer.data_ptr(), self.status.data_ptr(),
+        )
+
+    rows = DeviceScheduler.rows
+    host_ranges = DeviceScheduler.host_ranges
 
 
 _HANDLE_CACHE: "OrderedDict[tuple, DeviceScheduler]" = OrderedDict()

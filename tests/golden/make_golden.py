@@ -23,6 +23,7 @@ Instance families:
   warm100    100 micro-batches on one placement (``test_scheduler.py:188-201``)
   base       pipelined solves with ``gpu_base`` (``simulator.py:420-435``)
   asym       adaptive asymmetric placements (greedy counts + Monte-Carlo, ``placement.py:377-450``)
+  pipelined  both phases of the pipelined split (static even share + gpu_base solve)
 """
 
 from __future__ import annotations
@@ -187,6 +188,48 @@ def fam_base(h):
     return out
 
 
+def fam_pipelined(h):
+    """Both phases of ``harmony_pipelined`` (``simulator.py:420-435``): split by the
+    static share (``_split_loads`` :291-298, share = 1 - pipeline_ratio :375), the
+    static share's even plan (``_even_split_plan`` :301-322) integerized and routed,
+    then the scheduled share solved with the static phase's GPU loads as gpu_base."""
+    from harmonyep.simulator import _even_split_plan, _split_loads
+
+    out = []
+    rng = np.random.default_rng(2025)
+    cases = [(4, 8, "cayley"), (8, 8, "cayley"), (8, 32, "cayley"), (8, 128, "cayley"), (8, 16, "asym"), (6, 12, "random")]
+    ratios = [0.5, 0.3, 0.75, 1.0, 0.1]
+    for ci, (G, E, kind) in enumerate(cases):
+        shape = h.ClusterShape(G, E, 2)
+        s = float(rng.choice([0.5, 1.0, 1.5, 2.0]))
+        wl = h.gen_zipf_workload(shape, s, 1024 if E <= 32 else 8192, 2, seed=int(rng.integers(0, 1000)))
+        if kind == "cayley":
+            placement = h.cayley_symmetric(shape)
+        elif kind == "asym":
+            totals = wl.micro_batches[0].expert_totals()
+            placement = h.monte_carlo_placement(totals, h.greedy_replica_counts(totals, 2 * E, max_count=G), shape, 10, ci)
+        else:
+            placement = h.random_placement(shape, ci)
+        for mi, loads in enumerate(wl.micro_batches):
+            ratio = ratios[(ci + mi) % len(ratios)]
+            share = Fraction(1) - Fraction(ratio)
+            former, latter = _split_loads(loads, share)
+            fplan = h.integerize_plan(_even_split_plan(placement, former))
+            ftab = h.route_tokens(placement, former, fplan)
+            ftp = h.build_transfer_plan(ftab, h.Topology(G, G))
+            base = tuple(int(v) for v in fplan.gpu_loads())
+            lat = record(h, placement, latter, base=base)
+            out.append(dict(
+                G=G, E=E, groups=[list(g) for g in placement.edp_groups], slots=list(placement.slots),
+                loads=[list(r) for r in loads.entries], ratio=ratio, share=[share.numerator, share.denominator],
+                former=dict(loads=[list(r) for r in former.entries], xi=[[int(v) for v in r] for r in fplan.entries],
+                            gpu_load=list(base), ranges=[list(r) for r in ftab.ranges],
+                            pair=[list(r) for r in ftp.pair_counts], send=list(ftp.send), recv=list(ftp.recv),
+                            local=list(ftp.local)),
+                latter=lat))
+    return out
+
+
 def fam_asym(h):
     """Asymmetric placements as the adaptive replacement would build them."""
     out = []
@@ -270,6 +313,7 @@ def main():
     dump("sched_warm100.json.gz", fam_warm100(h))
     dump("sched_base.json.gz", fam_base(h))
     dump("sched_asym.json.gz", fam_asym(h))
+    dump("sched_pipelined.json.gz", fam_pipelined(h))
     dump("placements.json", fam_placements(h))
     dump("zipf_counts.json.gz", fam_zipf(h))
     dump("adaptive.json", fam_adaptive(h))

@@ -174,3 +174,43 @@ def test_baseline_shapes_full_size(P, cfg):
     assert rel <= 1e-2, rel
     del layer
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("ratio,kind", [(0.5, "cayley"), (0.3, "cayley"), (0.8, "identical"), (1.0, "cayley")])
+def test_pipelined_split_layer(P, ratio, kind):
+    """harmony_pipelined on the device: static share split evenly over replicas and
+    assigned first, scheduled share solved with gpu_base.  Both phases' schedules
+    and the [phase][expert][dst][src][rank] token->row map bit-exact against the
+    oracle; the layer output bit-identical to the single-phase layer (rows are
+    independent in the GEMMs, combine sums k in a fixed order)."""
+    from fractions import Fraction
+
+    from oracle import layer_ref
+    from oracle import oracle as O
+
+    G, E, K, d, F, T = 8, 16, 2, 256, 256, 4096
+    shape = P.ClusterShape(G, E, 2)
+    pl = P.cayley_symmetric(shape) if kind == "cayley" else P.identical_placement(shape)
+    bias = torch.tensor(P.zipf_gate_bias(E, 1.2, 1))
+    x = torch.randn(T, d, generator=torch.Generator(device="cuda").manual_seed(8), device="cuda").to(torch.bfloat16)
+    plain = P.MoELayer(pl, d, F, K, seed=5, gate_bias=bias)
+    ref_out = plain(x).clone()
+    pip = P.MoELayer(pl, d, F, K, seed=5, gate_bias=bias, pipeline_ratio=ratio)
+    out = pip(x).clone()
+    torch.cuda.synchronize()
+    pip.check_status()
+    assert torch.equal(out, ref_out)
+    b = pip.buffers(T)
+    share = Fraction(1) - Fraction(ratio)
+    loads = b.hist.cpu().numpy().T.tolist()
+    f, lat = O.pipelined_path(G, [tuple(g) for g in pl.edp_groups], loads, share.numerator, share.denominator)
+    ds = pip.sched
+    assert ds.former.rows(ds.former.xi) == f["xi"]
+    assert [tuple(r) for r in ds.former.host_ranges()] == [tuple(r) for r in f["ranges"]]
+    assert ds.m[:2].cpu().tolist() == list(lat["m"])
+    assert ds.rows(ds.xi) == lat["xi"]
+    assert [tuple(r) for r in ds.host_ranges()] == [tuple(r) for r in lat["ranges"]]
+    tok_row, n_rows = layer_ref.receive_rows_pipelined(pl.edp_groups, G, f, lat, f["loads"],
+                                                       b.topk_idx.cpu().numpy(), T // G)
+    assert n_rows == T * K
+    assert np.array_equal(b.tok_row.cpu().numpy(), tok_row)

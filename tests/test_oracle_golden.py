@@ -35,6 +35,26 @@ def test_oracle_matches_reference_fixtures(oracle_lib, family):
         assert out["iters"] == rec["iters"], "Dinic traversal order diverged from the reference"
 
 
+def test_oracle_pipelined_matches_reference(oracle_lib):
+    """harmony_pipelined (simulator.py:420-435): the static phase's split loads,
+    even-split integerized plan, GPU loads, routing and transfer, and the
+    scheduled phase's gpu_base solve — all bit-exact."""
+    recs = load_golden("sched_pipelined.json.gz")
+    assert len(recs) >= 10
+    for rec in recs:
+        num, den = rec["share"]
+        f, lat = oracle_lib.pipelined_path(rec["G"], rec["groups"], rec["loads"], num, den)
+        ref_f = rec["former"]
+        assert f["loads"] == ref_f["loads"]
+        assert lat["loads"] == rec["latter"]["loads"]
+        assert f["xi"] == ref_f["xi"] and f["gpu_load"] == ref_f["gpu_load"]
+        assert [list(r) for r in f["ranges"]] == ref_f["ranges"]
+        for k in ("pair", "send", "recv", "local"):
+            assert f[k] == ref_f[k], k
+        _compare(lat, rec["latter"])
+        assert lat["iters"] == rec["latter"]["iters"]
+
+
 def test_known_answers(oracle_lib):
     """Hand-derived answers of the reference tests (test_scheduler.py:33-69,
     test_router.py:32-151)."""
