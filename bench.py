@@ -209,6 +209,16 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # our arm, N > 1: real expert parallelism, one rank per GPU (ep.py)
 # ---------------------------------------------------------------------------
+def _max_over_ranks(v: float, dev) -> float:
+    """Max of a host float over all ranks (device tensor under NCCL, host under gloo)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device=dev if dist.get_backend() == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ep(args, world, rank, local, dev):
     """Scheduling group = the N ranks; every rank owns T tokens per micro-batch
     (weak scaling: per-GPU work fixed).  Histogram all-gather and the dispatch /
@@ -241,25 +251,47 @@ def run_ep(args, world, rank, local, dev):
         hist.push(layer.ranks[0].bufs[T]["hist_all"].sum(dim=0).cpu().tolist())
         dec = evaluate_and_maybe_replace(pl, hist, ReplacementPolicy(threshold=1.0, mc_samples=200), shape, 0)
         replacement = dec.to_event(args.warmup)
-        if dec.replaced:  # migration = re-materialising the replicas of the new layout
+        if dec.replaced:  # migration: the new replicas' weights move over NCCL from an old holder
             pl = dec.placement
-            layer = EPMoELayer(pl, d, F, K, comm, [rank], seed=0, gate_bias=bias, device=dev)
+            dist.barrier()
+            m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            m0.record()
+            mig = layer.migrate(pl)
+            m1.record()
+            torch.cuda.synchronize()
+            mt = _max_over_ranks(m0.elapsed_time(m1), dev)
+            replacement = dict(replacement or {}, migration_ms=mt, moved_replicas=mig["moved_replicas"],
+                               bytes_per_replica=mig["bytes_per_replica"])
             for _ in range(args.warmup):
                 layer.forward([x])
             torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
     dist.barrier()
     torch.cuda.synchronize()
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.__enter__()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
         layer.forward([x])
     e1.record(stream)
     torch.cuda.synchronize()
+    if sampler:
+        sampler.__exit__()
     dist.barrier()
-    t_ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
-    dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
-    t_ms = float(t_ms.item())
+    # FFN share (roofline): a few extra steps with events around the expert GEMMs
+    n_f = min(args.steps, 10)
+    fev = [{"ffn": (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))} for _ in range(n_f)]
+    for i in range(n_f):
+        layer.forward([x], events=fev[i])
+    torch.cuda.synchronize()
+    ffn_ms = statistics.mean(f["ffn"][0].elapsed_time(f["ffn"][1]) for f in fev)
+    R = layer.ranks[0].bufs[T]["R_recv"]
+    ffn_tf = 6.0 * d * F * R / (ffn_ms / 1e3) / 1e12
+    min_tf = -_max_over_ranks(-ffn_tf, dev)
+    hbm, tf_burst, tf_sus, peak_src = load_peaks()
+    t_ms = _max_over_ranks(e0.elapsed_time(e1), dev)
     gl = layer.ranks[0].sched.gpu_load.cpu().tolist()
     mm = max(gl) * len(gl) / max(sum(gl), 1)
     # e2e: host tokens in, host outputs back, every step
@@ -276,9 +308,7 @@ def run_ep(args, world, rank, local, dev):
         oh.copy_(out, non_blocking=True)
     f1.record(stream)
     torch.cuda.synchronize()
-    e_ms = torch.tensor([f0.elapsed_time(f1)], device=dev)
-    dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-    e_ms = float(e_ms.item())
+    e_ms = _max_over_ranks(f0.elapsed_time(f1), dev)
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": world * T * args.steps / (t_ms / 1e3), "unit": "tokens/s", "n_gpus": world,
@@ -286,11 +316,17 @@ def run_ep(args, world, rank, local, dev):
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": CONFIG_TEXT[args.config], "tokens_per_microbatch_per_gpu": T, "ep": world,
                        "top_k": K, "d_model": d, "ffn": F, "experts": E, "zipf_s": args.skew, "pass": "forward",
-                       "exchange": "NCCL all-gather (histograms) + all-to-all-v dispatch/combine"},
+                       "exchange": ("NCCL" if args.dist_backend == "nccl" else "gloo, host-staged (protocol check)")
+                                   + " all-gather (histograms) + all-to-all-v dispatch/combine"},
             "max_mean_gpu_load": mm, "max_mean_gpu_load_static_cayley": static_mm, "replacement": replacement,
             "e2e": {"value": world * T * args.steps / (e_ms / 1e3), "unit": "tokens/s",
                     "h2d_bytes_per_step": T * d * 2, "d2h_bytes_per_step": T * d * 2},
             "gpu_launches": args.steps * 13,
+            "roofline": {"bound": "tensor", "kernel": "hep_moe_expert_ffn on the received rows (rank 0)",
+                         "achieved": ffn_tf, "peak": tf_sus, "unit": "TFLOP/s", "frac": ffn_tf / tf_sus,
+                         "min_over_ranks": min_tf, "rows_rank0": R,
+                         "peak_source": f"{peak_src} bf16_tflops_sustained", "traffic": None},
+            "clocks": sampler.summary() if sampler else None,
         }))
     dist.destroy_process_group()
 
@@ -312,6 +348,8 @@ def main():
     ap.add_argument("--no-train", action="store_true", help="skip the forward+backward training-step measurement")
     ap.add_argument("--pipeline-ratio", type=float, default=None,
                     help="harmony_pipelined: share of tokens through the exact scheduler (rest split statically)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: run the N>1 EP protocol with every rank on GPU 0 (host-staged collectives; a check, not a bench)")
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of a CUDA-graph replay")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu legs)")
     args = ap.parse_args()
@@ -329,9 +367,14 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and args.dist_backend == "gloo":  # protocol check, all ranks may share one GPU
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "gloo":  # collectives staged through the host
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
     E, K, d, F, T, G = CONFIGS[args.config]

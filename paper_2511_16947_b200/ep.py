@@ -42,7 +42,7 @@ import ctypes
 import torch
 
 from . import _lib
-from .core import Placement
+from .core import Placement, PlacementError
 from .layer import init_expert_weights, interleave_w13
 from .scheduler import HEP_SCHED_ALL, DeviceScheduler
 
@@ -95,46 +95,56 @@ class DistComm:
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        # gloo (CPU protocol tests, or all ranks sharing one GPU): device tensors go through the host
+        self.host_staged = dist.get_backend(group) == "gloo"
+
+    def _h(self, t):
+        return t.cpu() if self.host_staged and t.is_cuda else t
 
     def all_gather(self, parts: list[torch.Tensor]) -> list[torch.Tensor]:
         (p,) = parts
-        chunks = [torch.empty_like(p) for _ in range(self.world)]
-        self.dist.all_gather(chunks, p.contiguous(), group=self.group)
-        return [torch.cat(chunks, dim=0)]
+        q = self._h(p.contiguous())
+        chunks = [torch.empty_like(q) for _ in range(self.world)]
+        self.dist.all_gather(chunks, q, group=self.group)
+        return [torch.cat(chunks, dim=0).to(p.device)]
 
     def all_reduce(self, parts: list[torch.Tensor]) -> None:
         (p,) = parts
-        self.dist.all_reduce(p, group=self.group)
+        q = self._h(p)
+        self.dist.all_reduce(q, group=self.group)
+        if q is not p:
+            p.copy_(q)
 
     def all_to_all(self, sends: list[torch.Tensor], send_counts: list[list[int]],
                    recv_counts: list[list[int]]) -> list[torch.Tensor]:
         (s,) = sends
-        recv = torch.empty((sum(recv_counts[0]),) + tuple(s.shape[1:]), dtype=s.dtype, device=s.device)
-        self.dist.all_to_all_single(recv, s, output_split_sizes=list(recv_counts[0]),
+        q = self._h(s.contiguous())
+        recv = torch.empty((sum(recv_counts[0]),) + tuple(s.shape[1:]), dtype=s.dtype, device=q.device)
+        self.dist.all_to_all_single(recv, q, output_split_sizes=list(recv_counts[0]),
                                     input_split_sizes=list(send_counts[0]), group=self.group)
-        return [recv]
+        return [recv.to(s.device)]
 
 
 class EPRank:
     """Per-rank state: local expert weights (by slot) and per-micro-batch buffers."""
 
-    def __init__(self, layer: "EPMoELayer", rank: int, w1, w2, w3):
+    def __init__(self, layer: "EPMoELayer", rank: int, w1=None, w2=None, w3=None, placement: Placement | None = None):
         self.rank = rank
         L = _lib.lib()
         dev = layer.device
-        self.sched = DeviceScheduler(layer.placement, device=dev)
+        pl = layer.placement if placement is None else placement
+        self.sched = DeviceScheduler(pl, device=dev)
         nh, ns = ctypes.c_int(), ctypes.c_int()
         _lib.check(L.hep_sched_hosted(self.sched.handle, rank, ctypes.byref(nh), ctypes.byref(ns)), "hep_sched_hosted")
         self.n_hosted, self.n_slots = nh.value, max(ns.value, 1)
         F, d = layer.F, layer.d
-        w13 = torch.zeros(self.n_slots, 2 * F, d, dtype=torch.bfloat16, device=dev)
-        w2l = torch.zeros(self.n_slots, d, F, dtype=torch.bfloat16, device=dev)
-        pl = layer.placement
-        for e in pl.hosted[rank]:
-            s = pl.slots[e]
-            w13[s] = interleave_w13(w1[e:e + 1], w3[e:e + 1])[0]
-            w2l[s] = w2[e]
-        self.w13, self.w2 = w13, w2l
+        self.w13 = torch.zeros(self.n_slots, 2 * F, d, dtype=torch.bfloat16, device=dev)
+        self.w2 = torch.zeros(self.n_slots, d, F, dtype=torch.bfloat16, device=dev)
+        if w1 is not None:
+            for e in pl.hosted[rank]:
+                s = pl.slots[e]
+                self.w13[s] = interleave_w13(w1[e:e + 1], w3[e:e + 1])[0]
+                self.w2[s] = w2[e]
         self.bufs: dict[int, dict] = {}
 
     def buffers(self, layer: "EPMoELayer", T: int) -> dict:
@@ -191,13 +201,33 @@ class EPMoELayer:
         del w1, w2, w3
 
     @torch.no_grad()
-    def forward(self, xs: list[torch.Tensor], stream=None) -> list[torch.Tensor]:
-        """xs[i] = [T][d] bf16 tokens of rank self.ranks[i]; returns their outputs."""
+    def migrate(self, placement: Placement) -> dict:
+        """Adopt a new placement (adaptive replacement, ``adaptive.py:119-166``) by moving
+        expert weights between GPUs: every replica the new placement adds on a GPU is
+        fetched from the lowest-id GPU that held the expert before (one all-to-all-v of
+        weight panels), replicas that stay on a GPU are copied between local slots.
+        Returns the moved-replica count (= the reference's ``changed_slots``, the
+        (expert, GPU) pairs new to the placement) and this process's bytes sent."""
+        if (placement.num_gpus, placement.num_experts) != (self.G, self.E):
+            raise ValueError("placement must keep the number of GPUs and experts")
+        new_ranks = [EPRank(self, rk.rank, placement=placement) for rk in self.ranks]
+        stats = migrate_weights(self.placement, placement, self.comm, [rk.rank for rk in self.ranks],
+                                [rk.w13 for rk in self.ranks], [rk.w2 for rk in self.ranks],
+                                [nr.w13 for nr in new_ranks], [nr.w2 for nr in new_ranks])
+        self.placement = placement
+        self.ranks = new_ranks
+        return stats
+
+    @torch.no_grad()
+    def forward(self, xs: list[torch.Tensor], stream=None, events: dict | None = None) -> list[torch.Tensor]:
+        """xs[i] = [T][d] bf16 tokens of rank self.ranks[i]; returns their outputs.
+        ``events`` optionally maps "ffn" to a (start, end) torch.cuda.Event pair
+        recorded around the expert FFN launches."""
         st = stream if stream is not None else torch.cuda.current_stream()
         with torch.cuda.stream(st):
-            return self._forward(xs, st)
+            return self._forward(xs, st, events or {})
 
-    def _forward(self, xs, st):
+    def _forward(self, xs, st, ev):
         L = _lib.lib()
         s = st.cuda_stream
         ck = _lib.check
@@ -230,8 +260,13 @@ class EPMoELayer:
         recvs = self.comm.all_to_all([b["send"][: sum(sc)] for b, sc in zip(bs, send_counts)], send_counts,
                                      recv_counts)
         ys = []
+        if "ffn" in ev:
+            ev["ffn"][0].record(st)
         for rk, b, recv in zip(self.ranks, bs, recvs):
+            b["R_recv"] = recv.shape[0]
             ys.append(self._expert_ffn(rk, b, recv))
+        if "ffn" in ev:
+            ev["ffn"][1].record(st)
         for i, b in enumerate(bs):
             b["send_counts"], b["recv_counts"] = send_counts[i], recv_counts[i]
         backs = self.comm.all_to_all(ys, recv_counts, send_counts)
@@ -424,3 +459,55 @@ def edp_reduce(placement: Placement, comm, ranks: list[int], dw13s: list[torch.T
                 t2 = g2.clone() if t2 is None else t2.add_(g2)
             dw13[sl].copy_(t13)
             dw2[sl].copy_(t2)
+
+
+def migrate_weights(old: Placement, new: Placement, comm, ranks: list[int], old_w13s, old_w2s, new_w13s,
+                    new_w2s) -> dict:
+    """Move expert weight slots from ``old`` to ``new`` placement.  ``old_*[i]`` /
+    ``new_*[i]`` are rank ``ranks[i]``'s slot tensors ([n_slots][...], slot =
+    placement.slots[e]).  A replica (e, g) new to the placement is sent by
+    src(e) = the lowest GPU in e's old EDP group; all ranks derive the same plan
+    from the two placements, so only weights travel (one all-to-all-v)."""
+    G = old.num_gpus
+    old_sets = [set(g) for g in old.edp_groups]
+    src = {}
+    moves = [[[] for _ in range(G)] for _ in range(G)]  # moves[q][r]: experts q sends to r (ascending)
+    for e, grp in enumerate(new.edp_groups):
+        for r in sorted(set(grp)):
+            if r in old_sets[e]:
+                continue
+            if not old_sets[e]:
+                raise PlacementError(f"expert {e} has no replica in the old placement to copy from")
+            src[e] = min(old_sets[e])
+            moves[src[e]][r].append(e)
+    for q in range(G):
+        for r in range(G):
+            moves[q][r].sort()
+    sh13, sh2 = tuple(old_w13s[0].shape[1:]), tuple(old_w2s[0].shape[1:])
+    n13, n2 = old_w13s[0][0].numel(), old_w2s[0][0].numel()
+    per = n13 + n2
+    sends, send_counts, recv_counts = [], [], []
+    for r, w13, w2, nw13, nw2 in zip(ranks, old_w13s, old_w2s, new_w13s, new_w2s):
+        for e in new.hosted[r]:  # replicas staying on this GPU: local slot copy
+            if r in old_sets[e]:
+                nw13[new.slots[e]].copy_(w13[old.slots[e]])
+                nw2[new.slots[e]].copy_(w2[old.slots[e]])
+        parts = []
+        for q in range(G):
+            for e in moves[r][q]:
+                parts += [w13[old.slots[e]].reshape(-1), w2[old.slots[e]].reshape(-1)]
+        sends.append(torch.cat(parts) if parts else w13.new_empty(0))
+        send_counts.append([len(moves[r][q]) * per for q in range(G)])
+        recv_counts.append([len(moves[q][r]) * per for q in range(G)])
+    recvs = comm.all_to_all(sends, send_counts, recv_counts)
+    for r, nw13, nw2, recv, rc in zip(ranks, new_w13s, new_w2s, recvs, recv_counts):
+        off = _offsets(rc)
+        for q in range(G):
+            for j, e in enumerate(moves[q][r]):
+                base = off[q] + j * per
+                nw13[new.slots[e]].copy_(recv[base: base + n13].view(sh13))
+                nw2[new.slots[e]].copy_(recv[base + n13: base + per].view(sh2))
+    moved = sum(len(moves[q][r]) for q in range(G) for r in range(G))
+    elem = old_w13s[0].element_size()
+    return {"moved_replicas": moved, "bytes_sent": sum(sum(c) for c in send_counts) * elem,
+            "bytes_per_replica": per * elem}

@@ -116,3 +116,59 @@ def test_edp_gradient_reduction_over_gloo(world):
     for p in procs:
         p.join(timeout=60)
     assert all(res.values()), res
+
+
+def _mig_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2511_16947_b200.core import ClusterShape
+        from paper_2511_16947_b200.ep import DistComm, migrate_weights
+        from paper_2511_16947_b200.placement import greedy_replica_counts, monte_carlo_placement, random_placement
+
+        E = 6
+        shape = ClusterShape(world, E, 2)
+        old = random_placement(shape, 1)
+        loads = [40, 1, 1, 9, 3, 2]
+        new = monte_carlo_placement(loads, greedy_replica_counts(loads, 2 * E, max_count=world), shape, 8, 2)
+
+        def nslots(pl, r):
+            return max([pl.slots[e] + 1 for e in pl.hosted[r]] + [1])
+
+        def expert_w(e):  # every replica of expert e holds the same weights
+            g = torch.Generator().manual_seed(100 + e)
+            return torch.randn(4, 3, generator=g), torch.randn(3, 2, generator=g)
+
+        w13 = torch.zeros(nslots(old, rank), 4, 3)
+        w2 = torch.zeros(nslots(old, rank), 3, 2)
+        for e in old.hosted[rank]:
+            w13[old.slots[e]], w2[old.slots[e]] = expert_w(e)
+        n13 = torch.full((nslots(new, rank), 4, 3), float("nan"))
+        n2 = torch.full((nslots(new, rank), 3, 2), float("nan"))
+        st = migrate_weights(old, new, DistComm(), [rank], [w13], [w2], [n13], [n2])
+        ok = True
+        for e in new.hosted[rank]:
+            a, b = expert_w(e)
+            ok = ok and torch.equal(n13[new.slots[e]], a) and torch.equal(n2[new.slots[e]], b)
+        pairs = lambda pl: {(e, g) for e, grp in enumerate(pl.edp_groups) for g in grp}  # noqa: E731
+        ok = ok and st["moved_replicas"] == len(pairs(new) - pairs(old))
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_weight_migration_over_gloo(world):
+    """Adaptive replacement on real ranks: after migrate_weights every GPU holds
+    exactly the experts of the new placement in the new slots, and the number of
+    replicas moved equals the reference's changed_slots (adaptive.py:157)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_mig_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert all(res.values()), res

@@ -110,3 +110,28 @@ def test_local_ep_backward_matches_simulated_layer(P, G, E, K, d, F, T, kind, s)
             assert _rel(grads[q][3][sl], rdw2[e]) <= 1e-3, (e, q)
             assert torch.equal(grads[q][2][sl], grads[members[0]][2][sl])
             assert torch.equal(grads[q][3][sl], grads[members[0]][3][sl])
+
+
+def test_local_ep_weight_migration(P):
+    """Cayley -> adaptive placement by moving weights between the ranks' slots:
+    the migrated layer's outputs are bit-identical to a layer built directly on
+    the new placement, and the moved replicas equal the reference's changed_slots."""
+    from paper_2511_16947_b200.ep import EPMoELayer, LocalComm
+
+    G, E, K, d, F, T = 8, 16, 2, 256, 256, 4096
+    old = _placement(P, G, E, "cayley", 1.5)
+    new = _placement(P, G, E, "asym", 1.5, seed=1)
+    bias = torch.tensor(P.zipf_gate_bias(E, 1.5, 0))
+    ep = EPMoELayer(old, d, F, K, LocalComm(G), range(G), seed=2, gate_bias=bias)
+    st = ep.migrate(new)
+    fresh = EPMoELayer(new, d, F, K, LocalComm(G), range(G), seed=2, gate_bias=bias)
+    x = torch.randn(T, d, generator=torch.Generator(device="cuda").manual_seed(4), device="cuda").to(torch.bfloat16)
+    xs = [x[r * (T // G):(r + 1) * (T // G)].contiguous() for r in range(G)]
+    got = torch.cat([o.clone() for o in ep.forward(xs)])
+    ref = torch.cat([o.clone() for o in fresh.forward(xs)])
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
+    for a, b in zip(ep.ranks, fresh.ranks):
+        assert torch.equal(a.w13, b.w13) and torch.equal(a.w2, b.w2)
+    pairs = lambda pl: {(e, g) for e, grp in enumerate(pl.edp_groups) for g in grp}  # noqa: E731
+    assert st["moved_replicas"] == len(pairs(new) - pairs(old)) > 0
