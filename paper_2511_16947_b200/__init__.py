@@ -28,7 +28,25 @@ from .core import (
     balance_ratio,
     gpu_load_balance_ratio,
 )
-from .placement import cayley_symmetric, identical_placement, validate_placement
+from .placement import (
+    DensityReport,
+    PlacementGraph,
+    cayley_symmetric,
+    density_oracle,
+    greedy_replica_counts,
+    identical_placement,
+    monte_carlo_placement,
+    random_placement,
+    symmetric_placement,
+    validate_placement,
+)
+from .adaptive import (
+    LoadHistory,
+    ReplacementDecision,
+    ReplacementPolicy,
+    evaluate_and_maybe_replace,
+    predict_loads,
+)
 from .router import (
     RoutingTable,
     TransferPlan,
@@ -44,10 +62,12 @@ from .scheduler import (
     SolverState,
     SolveStats,
     integerize_plan,
+    solve_comm_aware,
     solve_replica_loads,
     warm_solve,
 )
-from .workload import Workload, gen_zipf_workload, zipf_gate_bias
+from .workload import Workload, gen_zipf_workload, load_trace, save_trace, zipf_gate_bias
+from .sweep import STRATEGIES, CostModel, MicrobatchMetrics, RunResult, SweepResult, run_skew_sweep, run_strategy
 from .layer import MoELayer
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -230,6 +230,30 @@ def fam_pipelined(h):
     return out
 
 
+def fam_sweep(h):
+    """``run_skew_sweep`` metrics.csv / summary.json / replacement events
+    (simulator.py:566-640) for the device-scheduled strategies."""
+    from harmonyep.simulator import CostModel, run_skew_sweep
+
+    out = []
+    cases = [
+        (4, 8, 2, ("vanilla_ep", "merged_ep", "harmony", "harmony_pipelined"), 0.5, None),
+        (8, 32, 8, ("harmony", "harmony_pipelined", "merged_ep"), 0.7, dict(check_interval=4, mc_samples=10)),
+        (8, 16, 4, ("harmony", "vanilla_ep"), 1.0, dict(check_interval=3, mc_samples=8, threshold=1.05)),
+    ]
+    for G, E, gpn, strategies, ratio, pol in cases:
+        shape = h.ClusterShape(G, E, 2, gpus_per_node=gpn)
+        placement = h.cayley_symmetric(shape)
+        cost = CostModel(pipeline_ratio=ratio)
+        policy = h.ReplacementPolicy(**pol) if pol else None
+        res = run_skew_sweep(shape, (0.5, 1.5), strategies, (0, 1), placement=placement, tokens_per_gpu=512,
+                             n_microbatches=10, cost=cost, policy=policy, workers=1)
+        out.append(dict(G=G, E=E, gpn=gpn, strategies=list(strategies), ratio=ratio, policy=pol,
+                        groups=[list(g) for g in placement.edp_groups], slots=list(placement.slots),
+                        csv=res.to_csv(), summary=res.summary(), events=res.events, lp_solves=res.lp_solves))
+    return out
+
+
 def fam_asym(h):
     """Asymmetric placements as the adaptive replacement would build them."""
     out = []
@@ -314,6 +338,7 @@ def main():
     dump("sched_base.json.gz", fam_base(h))
     dump("sched_asym.json.gz", fam_asym(h))
     dump("sched_pipelined.json.gz", fam_pipelined(h))
+    dump("sweep_metrics.json.gz", fam_sweep(h))
     dump("placements.json", fam_placements(h))
     dump("zipf_counts.json.gz", fam_zipf(h))
     dump("adaptive.json", fam_adaptive(h))

@@ -150,3 +150,47 @@ def test_package_never_imports_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 for bad in ("import oracle", "from oracle", "hep_oracle", "libhep_oracle"):
                     assert bad not in src, (f, bad)
+
+
+REFERENCE_NAMES = (  # harmonyep/__init__.py:11-82 minus the comm-aware LP statistics type
+    "CapacityError ClusterShape ConfigError ConstructionError ContractViolation DimensionError HarmonyError "
+    "LoadMatrix Placement PlacementError ReplicaLoadPlan StaleStateError Topology TraceParseError "
+    "UndefinedMetricError aggregate_expert_loads balance_ratio BALANCE_ONLY COMM_AWARE TOPOLOGY_AWARE SolveOptions "
+    "SolverState integerize_plan solve_comm_aware solve_replica_loads warm_solve RoutingTable TransferPlan "
+    "build_transfer_plan route_tokens route_topology_aware DensityReport PlacementGraph cayley_symmetric "
+    "density_oracle greedy_replica_counts identical_placement monte_carlo_placement random_placement "
+    "symmetric_placement validate_placement LoadHistory ReplacementDecision ReplacementPolicy "
+    "evaluate_and_maybe_replace predict_loads STRATEGIES CostModel MicrobatchMetrics RunResult SweepResult Workload "
+    "gen_zipf_workload load_trace run_skew_sweep run_strategy save_trace"
+).split()
+
+
+def test_reference_api_surface_is_exported():
+    import paper_2511_16947_b200 as P
+
+    missing = [n for n in REFERENCE_NAMES if not hasattr(P, n)]
+    assert not missing, missing
+
+
+def test_trace_roundtrip_and_errors(tmp_path):
+    import paper_2511_16947_b200 as P
+
+    shape = P.ClusterShape(4, 8, 2)
+    wl = P.gen_zipf_workload(shape, 1.2, 300, 4, 5)
+    path = tmp_path / "t.csv"
+    P.save_trace(wl, str(path))
+    back = P.load_trace(str(path), shape)
+    assert back.micro_batches == wl.micro_batches
+    bad = tmp_path / "bad.csv"
+    bad.write_text("microbatch,expert,gpu,tokens\n0,1,2,3\n0,9,0,1\n")
+    with pytest.raises(P.TraceParseError) as ei:
+        P.load_trace(str(bad), shape)
+    assert ei.value.line_no == 3 and "expert 9 out of range 0..7" in str(ei.value)
+    bad.write_text("mb,expert,gpu,tokens\n")
+    with pytest.raises(P.TraceParseError):
+        P.load_trace(str(bad), shape)
+    # repeated rows add up; gaps are empty micro-batches
+    ok = tmp_path / "ok.csv"
+    ok.write_text("microbatch,expert,gpu,tokens\n2,0,0,5\n2,0,0,6\n")
+    w = P.load_trace(str(ok), shape)
+    assert len(w.micro_batches) == 3 and w.micro_batches[2].entries[0][0] == 11 and w.micro_batches[0].total() == 0
