@@ -209,6 +209,16 @@ def run_reference(args):
 # ---------------------------------------------------------------------------
 # our arm, N > 1: real expert parallelism, one rank per GPU (ep.py)
 # ---------------------------------------------------------------------------
+def load_traffic(config: str) -> dict:
+    """Per-launch DRAM bytes of the hot kernels from the committed ncu launch
+    list (profiles/traffic.json, written by tools/traffic.py); {} if absent."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return {}
+    with open(p) as f:
+        return json.load(f).get(config, {})
+
+
 def _max_over_ranks(v: float, dev) -> float:
     """Max of a host float over all ranks (device tensor under NCCL, host under gloo)."""
     import torch
@@ -569,6 +579,7 @@ def main():
         torch.cuda.empty_cache()
 
     hbm, tf_burst, tf_sus, peak_src = load_peaks()
+    traffic = load_traffic(args.config)
     R = T * K
     ffn_flops = 6.0 * d * F * R
     ffn_tflops = ffn_flops / (ffn_ms / 1e3) / 1e12
@@ -634,11 +645,16 @@ def main():
                 "frac_of_burst_peak": ffn_tflops / tf_burst,
                 "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside back-to-back steps)",
                 "algorithmic_flops_per_launch": ffn_flops,
-                "traffic": None,
+                # minimal DRAM bytes of one launch: every weight once, X read, H written + read, Y written
+                "algorithmic_bytes_per_launch": E * 3 * d * F * 2 + R * d * 2 * 2 + R * F * 2 * 2,
+                "traffic": traffic.get("ffn", {}).get("bytes"),
+                "traffic_source": traffic.get("source"),
             },
             "hbm_kernels": {
-                "permute": {"GB/s": perm_bytes / (perm_ms / 1e3) / 1e9, "frac": perm_bytes / (perm_ms / 1e3) / 1e9 / hbm},
-                "combine": {"GB/s": comb_bytes / (comb_ms / 1e3) / 1e9, "frac": comb_bytes / (comb_ms / 1e3) / 1e9 / hbm},
+                "permute": {"GB/s": perm_bytes / (perm_ms / 1e3) / 1e9, "frac": perm_bytes / (perm_ms / 1e3) / 1e9 / hbm,
+                            "algorithmic_bytes": perm_bytes, "traffic": traffic.get("permute", {}).get("bytes")},
+                "combine": {"GB/s": comb_bytes / (comb_ms / 1e3) / 1e9, "frac": comb_bytes / (comb_ms / 1e3) / 1e9 / hbm,
+                            "algorithmic_bytes": comb_bytes, "traffic": traffic.get("combine", {}).get("bytes")},
                 "peak_GB/s": hbm,
             },
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": T * d * 2,

@@ -1,20 +1,24 @@
 #!/bin/bash
-# One measurement round on the B200 box: tests, bench (3 configs), ncu launch
-# lists and full captures of the top kernels.  Output under gpurun_out/.
+# One measurement round on the B200 box: tests, ncu launch lists (-> per-launch DRAM
+# traffic), bench (3 configs + pipelined variant + reference arm), full ncu captures
+# of the top kernels.  Output under gpurun_out/ (copy what is judged to profiles/).
 set -x
 R=${ROUND:-r01}
-timeout 900 python -m pytest tests -m gpu -q --timeout 600 > gpurun_out/t_all_$R.log 2>&1
+timeout 1200 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/t_all_$R.log 2>&1
 tail -2 gpurun_out/t_all_$R.log
 timeout 120 python tools/sched_timing.py > gpurun_out/sched_timing_$R.json 2>&1
 for c in mixtral qwen3 dsv3; do
-  timeout 900 python bench.py --config $c > gpurun_out/bench_${c}_$R.json 2> gpurun_out/bench_${c}_$R.err
-done
-timeout 300 python bench.py --impl reference --config mixtral --steps 3 --warmup 1 > gpurun_out/bench_ref_mixtral_$R.json 2>&1
-for c in mixtral qwen3 dsv3; do
   timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    --kernel-name-base demangled -k regex:"hep::" -c 14 --csv \
+    --kernel-name-base demangled -k regex:"hep::|gemm::|sched_kernel|permute|combine|chunk|plan_prep|gate_topk" -c 12 --csv \
     --log-file gpurun_out/launches_${c}_$R.csv python bench.py --config $c --profile --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
 done
+python tools/traffic.py gpurun_out/launches_mixtral_$R.csv gpurun_out/launches_qwen3_$R.csv gpurun_out/launches_dsv3_$R.csv > gpurun_out/traffic_$R.json
+cp gpurun_out/traffic_$R.json profiles/traffic.json
+for c in mixtral qwen3 dsv3; do
+  timeout 900 python bench.py --config $c > gpurun_out/bench_${c}_$R.json 2> gpurun_out/bench_${c}_$R.err
+done
+timeout 600 python bench.py --config mixtral --pipeline-ratio 0.5 --no-cpu-baseline --no-train > gpurun_out/bench_mixtral_pipelined_$R.json 2>&1
+timeout 300 python bench.py --impl reference --config mixtral --steps 3 --warmup 1 > gpurun_out/bench_ref_mixtral_$R.json 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
   -k regex:"gemm2sm_kernel|gemm_kernel<.int.256|sched_kernel|permute|combine|gate_topk|chunk_map" -c 8 \
   -o gpurun_out/prof_mixtral_$R python bench.py --config mixtral --profile --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_mixtral_$R.log 2>&1
