@@ -248,7 +248,7 @@ def run_ep(args, world, rank, local, dev):
     pl = P.cayley_symmetric(shape) if (E & (E - 1)) == 0 and (G & (G - 1)) == 0 else P.placement.symmetric_placement(shape)
     bias = torch.tensor(P.zipf_gate_bias(E, args.skew, 0)) if args.skew > 0 else None
     comm = DistComm()
-    layer = EPMoELayer(pl, d, F, K, comm, [rank], seed=0, gate_bias=bias, device=dev)
+    layer = EPMoELayer(pl, d, F, K, comm, [rank], seed=0, gate_bias=bias, device=dev, exchange=args.exchange)
     x = torch.randn(T, d, generator=torch.Generator(device=dev).manual_seed(1000 + rank), device=dev).to(torch.bfloat16)
     for _ in range(args.warmup):
         layer.forward([x])
@@ -297,7 +297,7 @@ def run_ep(args, world, rank, local, dev):
         layer.forward([x], events=fev[i])
     torch.cuda.synchronize()
     ffn_ms = statistics.mean(f["ffn"][0].elapsed_time(f["ffn"][1]) for f in fev)
-    R = layer.ranks[0].bufs[T]["R_recv"]
+    R = int(layer.ranks[0].bufs[T]["counts"][G:].sum().item())  # rows this rank received (outside the timing)
     ffn_tf = 6.0 * d * F * R / (ffn_ms / 1e3) / 1e12
     min_tf = -_max_over_ranks(-ffn_tf, dev)
     hbm, tf_burst, tf_sus, peak_src = load_peaks()
@@ -326,12 +326,15 @@ def run_ep(args, world, rank, local, dev):
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": CONFIG_TEXT[args.config], "tokens_per_microbatch_per_gpu": T, "ep": world,
                        "top_k": K, "d_model": d, "ffn": F, "experts": E, "zipf_s": args.skew, "pass": "forward",
-                       "exchange": ("NCCL" if args.dist_backend == "nccl" else "gloo, host-staged (protocol check)")
-                                   + " all-gather (histograms) + all-to-all-v dispatch/combine"},
+                       "exchange": (("NVLink peer stores: dispatch kernel -> peers' receive buffers, down-projection "
+                                     "epilogue -> sources' return buffers (CUDA IPC); histogram all-gather + 2 barriers")
+                                    if args.exchange == "p2p" else
+                                    ("NCCL" if args.dist_backend == "nccl" else "gloo, host-staged (protocol check)")
+                                    + " all-gather (histograms) + all-to-all-v dispatch/combine")},
             "max_mean_gpu_load": mm, "max_mean_gpu_load_static_cayley": static_mm, "replacement": replacement,
             "e2e": {"value": world * T * args.steps / (e_ms / 1e3), "unit": "tokens/s",
                     "h2d_bytes_per_step": T * d * 2, "d2h_bytes_per_step": T * d * 2},
-            "gpu_launches": args.steps * 13,
+            "gpu_launches": args.steps * (13 if args.exchange == "p2p" else 12),
             "roofline": {"bound": "tensor", "kernel": "hep_moe_expert_ffn on the received rows (rank 0)",
                          "achieved": ffn_tf, "peak": tf_sus, "unit": "TFLOP/s", "frac": ffn_tf / tf_sus,
                          "min_over_ranks": min_tf, "rows_rank0": R,
@@ -360,6 +363,8 @@ def main():
                     help="harmony_pipelined: share of tokens through the exact scheduler (rest split statically)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: run the N>1 EP protocol with every rank on GPU 0 (host-staged collectives; a check, not a bench)")
+    ap.add_argument("--exchange", default="p2p", choices=["p2p", "nccl"],
+                    help="N>1 token exchange: NVLink peer stores fused into the dispatch / GEMM kernels, or NCCL all-to-all-v")
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of a CUDA-graph replay")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu legs)")
     args = ap.parse_args()

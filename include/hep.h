@@ -230,6 +230,39 @@ int hep_moe_ep_train_layout(const int32_t *d_seg, int n_hosted, int G, int n_slo
 /* experts hosted by `rank` and the number of local weight slots it needs */
 int hep_sched_hosted(hep_sched_t h, int rank, int *n_hosted, int *n_slots);
 
+/*
+ * EP exchange over NVLink peer memory (one kernel per direction, no NCCL on the data
+ * path; every rank derives all offsets from the identical transfer plan):
+ *   d_pair         = hep_sched_out.d_transfer (pair[s][d] first, G*G int64)
+ *   d_peer_recv[d] = address of rank d's receive buffer ([src][hosted expert] rows)
+ *   d_peer_back[s] = address of rank s's return buffer ([dst][expert][rank] = send layout)
+ * hep_moe_dispatch_p2p: K5 fused with the dispatch all-to-all — x[t] of every
+ *   assignment (send position tok_row[t][k] from hep_moe_assign_ep) is stored straight
+ *   into its destination rank's receive buffer.
+ * hep_moe_return_addr: per received row, the address of its slot in the source rank's
+ *   return buffer (capacity rows at most); hep_moe_expert_ffn_p2p stores the
+ *   down-projection output rows there from the GEMM epilogue (combine all-to-all fused
+ *   into the GEMM), after which hep_moe_combine runs on the source as usual.  R = capacity
+ *   of the receive buffer (rows actually present come from d_seg on the device);
+ *   rows_hint = expected rows (picks the 1-CTA / CTA-pair tile shape like R does for
+ *   hep_moe_expert_ffn).
+ * The caller orders the exchanges across ranks (stream sync + a barrier): a rank's
+ * receive buffer is complete once every source's dispatch kernel has finished.
+ */
+int hep_moe_dispatch_p2p(const void *d_x, const int32_t *d_tok_row, int64_t T, int K, int64_t d_model, int rank,
+                         int num_gpus, const int64_t *d_pair, const uint64_t *d_peer_recv, void *stream);
+int hep_moe_return_addr(const int64_t *d_pair, int rank, int num_gpus, const uint64_t *d_peer_back, int64_t row_bytes,
+                        int64_t capacity, uint64_t *d_addr, void *stream);
+int hep_moe_expert_ffn_p2p(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg, int n_seg,
+                           int64_t R, int64_t rows_hint, int64_t d_model, int64_t ffn, int n_experts, void *d_h,
+                           const uint64_t *d_y_addr, void *d_workspace, size_t workspace_bytes, int32_t *d_status,
+                           void *stream);
+/* CUDA IPC plumbing for the peer buffers: 64-byte handle of the allocation holding d_ptr
+ * plus d_ptr's byte offset in it (exchanged by the host); open maps the allocation base. */
+int hep_ipc_handle(const void *d_ptr, void *handle_out, int64_t *offset_out);
+int hep_ipc_open(const void *handle, void **d_ptr);
+int hep_ipc_close(void *d_ptr);
+
 /* K5 permute/dispatch: rows[tok_row[t][k]] = x[t]  (bf16, 128-bit vectorised scatter). */
 int hep_moe_permute(const void *d_x, const int32_t *d_tok_row, int64_t T, int K, int64_t d_model, void *d_rows,
                     void *stream);

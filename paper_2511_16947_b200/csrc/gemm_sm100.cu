@@ -56,6 +56,10 @@ struct Params {
     int64_t ld_aux;
     int raster_gm;  // grouped mode: m-tiles per raster band (0 = whole expert)
     int pol_mode;  // 0: defaults; else (A policy | B policy << 2), 1 normal, 2 last, 3 first (tuning)
+    // EPI_BF16: optional per-row destination addresses (row r -> row_addr[r]); the fused
+    // combine all-to-all stores each expert output row straight into its source GPU's
+    // buffer over NVLink (peer pointers), instead of into `out`
+    const uint64_t *row_addr;
 };
 
 __device__ __forceinline__ uint64_t pick_policy(int k) {
@@ -229,8 +233,11 @@ __device__ __forceinline__ void store_tile(const Params &p, uint32_t t_row, int6
             }
         }
     } else if constexpr (EPI == EPI_BF16) {
+        const bool remote = p.row_addr != nullptr;
         __nv_bfloat16 *out =
-            reinterpret_cast<__nv_bfloat16 *>(p.out) + grow * p.ld_out + (int64_t)n_blk * BN;
+            (remote ? (valid ? reinterpret_cast<__nv_bfloat16 *>(p.row_addr[grow]) : nullptr)
+                    : reinterpret_cast<__nv_bfloat16 *>(p.out) + grow * p.ld_out) +
+            (int64_t)n_blk * BN;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 16) {
             uint32_t v[16];
@@ -241,8 +248,14 @@ __device__ __forceinline__ void store_tile(const Params &p, uint32_t t_row, int6
             for (int i = 0; i < 8; ++i)
                 packed[i] = pack_bf16(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
             if (valid) {
-                st_global_v4_hint(out + c, make_uint4(packed[0], packed[1], packed[2], packed[3]), pol_out);
-                st_global_v4_hint(out + c + 8, make_uint4(packed[4], packed[5], packed[6], packed[7]), pol_out);
+                if (remote) {  // peer (NVLink) or local destination row: plain 16-byte stores
+                    uint4 *o = reinterpret_cast<uint4 *>(out + c);
+                    o[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+                    o[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+                } else {
+                    st_global_v4_hint(out + c, make_uint4(packed[0], packed[1], packed[2], packed[3]), pol_out);
+                    st_global_v4_hint(out + c + 8, make_uint4(packed[4], packed[5], packed[6], packed[7]), pol_out);
+                }
             }
         }
     } else {
@@ -786,7 +799,17 @@ extern "C" size_t hep_moe_ffn_workspace(int n_seg, int64_t R, int n_experts) {
 
 static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg, int n_seg,
                           int64_t R, int64_t d_model, int64_t ffn, int n_experts, void *d_h, void *d_y, void *d_pre,
-                          void *d_workspace, size_t workspace_bytes, int32_t *d_status, void *stream);
+                          void *d_workspace, size_t workspace_bytes, int32_t *d_status, void *stream,
+                          const uint64_t *d_y_addr = nullptr, int64_t rows_hint = -1);
+
+extern "C" int hep_moe_expert_ffn_p2p(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg,
+                                      int n_seg, int64_t R, int64_t rows_hint, int64_t d_model, int64_t ffn,
+                                      int n_experts, void *d_h, const uint64_t *d_y_addr, void *d_workspace,
+                                      size_t workspace_bytes, int32_t *d_status, void *stream) {
+    HEP_REQUIRE(d_y_addr, HEP_E_CONTRACT, "hep_moe_expert_ffn_p2p: d_y_addr required");
+    return expert_ffn_fwd(d_rows, d_w13, d_w2, d_seg, n_seg, R, d_model, ffn, n_experts, d_h, (void *)d_y_addr,
+                          nullptr, d_workspace, workspace_bytes, d_status, stream, d_y_addr, rows_hint);
+}
 
 extern "C" int hep_moe_expert_ffn(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg,
                                   int n_seg, int64_t R, int64_t d_model, int64_t ffn, int n_experts, void *d_h,
@@ -807,7 +830,8 @@ extern "C" int hep_moe_expert_ffn_train(const void *d_rows, const void *d_w13, c
 
 static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg, int n_seg,
                           int64_t R, int64_t d_model, int64_t ffn, int n_experts, void *d_h, void *d_y, void *d_pre,
-                          void *d_workspace, size_t workspace_bytes, int32_t *d_status, void *stream) {
+                          void *d_workspace, size_t workspace_bytes, int32_t *d_status, void *stream,
+                          const uint64_t *d_y_addr, int64_t rows_hint) {
     HEP_REQUIRE(d_rows && d_w13 && d_w2 && d_seg && d_h && d_y && d_workspace, HEP_E_CONTRACT,
                 "hep_moe_expert_ffn: null pointer");
     HEP_REQUIRE(d_model % 256 == 0 && ffn % 128 == 0 && d_model % BK == 0, HEP_E_DIMENSION,
@@ -820,7 +844,7 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
     int32_t *mt_row0 = reinterpret_cast<int32_t *>(d_workspace);
     int32_t *mt_rows = mt_row0 + cap;
     int32_t *exp_off = mt_rows + cap;
-    const bool pairs = use_pairs(R, n_experts);
+    const bool pairs = use_pairs(rows_hint >= 0 ? rows_hint : R, n_experts);
     const char *pol_env = getenv("HEP_L2POL");
     const int pol_mode = pol_env ? atoi(pol_env) : 0;
     build_tiles_kernel<<<1, 1024, 0, s>>>(d_seg, n_seg, n_experts, mt_row0, mt_rows, exp_off, cap, d_status,
@@ -830,7 +854,10 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
     p.grouped = 1;
     p.pol_mode = pol_mode;
     const char *gm_env = getenv("HEP_RASTER_GM");
-    p.raster_gm = gm_env ? atoi(gm_env) : 8;  // measured best (profiles/r01/raster.txt)
+    const int gm_default = gm_env ? atoi(gm_env) : 8;  // measured best (profiles/r01/raster.txt)
+    const char *gm1_env = getenv("HEP_RASTER_GM1");
+    const char *gm2_env = getenv("HEP_RASTER_GM2");
+    p.raster_gm = gm1_env ? atoi(gm1_env) : gm_default;
     p.mt_row0 = mt_row0;
     p.mt_rows = mt_rows;
     p.exp_mt_off = exp_off;
@@ -849,6 +876,8 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
     if (rc) return rc;
     // GEMM 2: Y = H W2^T, B = W2 [E][d][F]
     p.aux = nullptr;
+    p.row_addr = d_y_addr;
+    p.raster_gm = gm2_env ? atoi(gm2_env) : gm_default;
     p.kblocks = (int)(ffn / BK);
     p.n_tiles = (int)(d_model / 256);
     p.b_rows_per_exp = d_model;

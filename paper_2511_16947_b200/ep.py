@@ -65,6 +65,13 @@ class LocalComm:
         full = torch.cat(parts, dim=0)
         return [full for _ in parts]
 
+    def exchange_ptrs(self, ptrs: list[int]) -> list[list[int]]:
+        """Every rank's device address of a buffer, for every driven rank."""
+        return [list(ptrs) for _ in ptrs]
+
+    def barrier(self) -> None:
+        """All ranks share one stream here: launch order already orders them."""
+
     def all_reduce(self, parts: list[torch.Tensor]) -> None:
         """In-place sum over the ranks (rank order)."""
         acc = parts[0].clone()
@@ -97,6 +104,7 @@ class DistComm:
         self.rank = dist.get_rank(group)
         # gloo (CPU protocol tests, or all ranks sharing one GPU): device tensors go through the host
         self.host_staged = dist.get_backend(group) == "gloo"
+        self._opened: list[int] = []  # IPC mappings of peer buffers
 
     def _h(self, t):
         return t.cpu() if self.host_staged and t.is_cuda else t
@@ -107,6 +115,32 @@ class DistComm:
         chunks = [torch.empty_like(q) for _ in range(self.world)]
         self.dist.all_gather(chunks, q, group=self.group)
         return [torch.cat(chunks, dim=0).to(p.device)]
+
+    def exchange_ptrs(self, ptrs: list[int]) -> list[list[int]]:
+        """CUDA IPC: all-gather (handle, offset) of this rank's buffer, map the peers'."""
+        (ptr,) = ptrs
+        L = _lib.lib()
+        h = ctypes.create_string_buffer(64)
+        off = ctypes.c_int64()
+        _lib.check(L.hep_ipc_handle(ptr, h, ctypes.byref(off)), "hep_ipc_handle")
+        allh = [None] * self.world
+        self.dist.all_gather_object(allh, (bytes(h.raw), off.value), group=self.group)
+        out = []
+        for r, (hb, o) in enumerate(allh):
+            if r == self.rank:
+                out.append(ptr)
+                continue
+            base = ctypes.c_void_p()
+            _lib.check(L.hep_ipc_open(ctypes.create_string_buffer(hb, 64), ctypes.byref(base)), "hep_ipc_open")
+            self._opened.append(base.value)
+            out.append(base.value + o)
+        return [out]
+
+    def barrier(self) -> None:
+        """Peer writes of this rank's kernels are complete and visible once its stream
+        has drained; the barrier makes every rank wait for all of them."""
+        torch.cuda.current_stream().synchronize()
+        self.dist.barrier(group=self.group)
 
     def all_reduce(self, parts: list[torch.Tensor]) -> None:
         (p,) = parts
@@ -147,6 +181,25 @@ class EPRank:
                 self.w2[s] = w2[e]
         self.bufs: dict[int, dict] = {}
 
+    def p2p_buffers(self, layer: "EPMoELayer", T: int) -> dict:
+        """Exchange buffers of the NVLink path, fixed addresses (peers write into them):
+        recv [G*T*K][d] (worst case: every assignment of every source lands here),
+        back [T*K][d] (send layout; peers' FFN epilogues return rows into it)."""
+        b = self.buffers(layer, T)
+        if "recv" not in b:
+            dev, K, G, d = layer.device, layer.K, layer.G, layer.d
+            cap = max(G * T * K, 1)
+            b["cap"] = cap
+            b["recv"] = torch.empty(cap, d, dtype=torch.bfloat16, device=dev)
+            b["back"] = torch.empty(max(T * K, 1), d, dtype=torch.bfloat16, device=dev)
+            b["h"] = torch.empty(cap, layer.F, dtype=torch.bfloat16, device=dev)
+            b["y_addr"] = torch.empty(cap, dtype=torch.int64, device=dev)
+            L = _lib.lib()
+            n_seg = max(G * self.n_hosted, 1)
+            b["ffn_ws"] = torch.empty(max(int(L.hep_moe_ffn_workspace(n_seg, cap, self.n_slots)), 256),
+                                      dtype=torch.uint8, device=dev)
+        return b
+
     def buffers(self, layer: "EPMoELayer", T: int) -> dict:
         b = self.bufs.get(T)
         if b is None:
@@ -181,8 +234,14 @@ class EPMoELayer:
     """
 
     def __init__(self, placement: Placement, d_model: int, ffn: int, top_k: int, comm, ranks, *, seed: int = 0,
-                 gate_bias: torch.Tensor | None = None, device=None, train: bool = False):
+                 gate_bias: torch.Tensor | None = None, device=None, train: bool = False, exchange: str = "nccl"):
         _lib.require_cuda()
+        if exchange not in ("nccl", "p2p"):
+            raise ValueError("exchange must be 'nccl' (all-to-all-v collectives) or 'p2p' (NVLink peer stores)")
+        if exchange == "p2p" and train:
+            raise ValueError("the peer-memory exchange is built for the forward pass; train with exchange='nccl'")
+        self.exchange = exchange
+        self._peer_tables: dict[int, list] = {}
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.placement, self.comm = placement, comm
         self.G, self.E, self.K, self.d, self.F = placement.num_gpus, placement.num_experts, top_k, d_model, ffn
@@ -216,6 +275,7 @@ class EPMoELayer:
                                 [nr.w13 for nr in new_ranks], [nr.w2 for nr in new_ranks])
         self.placement = placement
         self.ranks = new_ranks
+        self._peer_tables.clear()  # new exchange buffers: peers re-map them on the next forward
         return stats
 
     @torch.no_grad()
@@ -225,7 +285,79 @@ class EPMoELayer:
         recorded around the expert FFN launches."""
         st = stream if stream is not None else torch.cuda.current_stream()
         with torch.cuda.stream(st):
+            if self.exchange == "p2p":
+                return self._forward_p2p(xs, st, events or {})
             return self._forward(xs, st, events or {})
+
+    def _peer_table(self, T: int) -> list:
+        """Per driven rank: device tables of every rank's receive / return buffer address."""
+        tab = self._peer_tables.get(T)
+        if tab is None:
+            bs = [rk.p2p_buffers(self, T) for rk in self.ranks]
+            recv = self.comm.exchange_ptrs([b["recv"].data_ptr() for b in bs])
+            back = self.comm.exchange_ptrs([b["back"].data_ptr() for b in bs])
+            tab = [(torch.tensor(rv, dtype=torch.int64, device=self.device),
+                    torch.tensor(bk, dtype=torch.int64, device=self.device)) for rv, bk in zip(recv, back)]
+            self._peer_tables[T] = tab
+        return tab
+
+    def _forward_p2p(self, xs, st, ev):
+        """Forward with both exchanges as NVLink peer stores: the dispatch kernel writes
+        rows into the destination ranks' receive buffers, the down-projection GEMM's
+        epilogue writes expert outputs into the source ranks' return buffers.  The only
+        collectives are the histogram all-gather and two barriers (no host reads of the
+        schedule, no NCCL on the data path)."""
+        L = _lib.lib()
+        s = st.cuda_stream
+        ck = _lib.check
+        K, E, G, d, F = self.K, self.E, self.G, self.d, self.F
+        T0 = xs[0].shape[0]
+        tabs = self._peer_table(T0)
+        bs = []
+        for rk, x in zip(self.ranks, xs):
+            T = x.shape[0]
+            b = rk.p2p_buffers(self, T)
+            bs.append(b)
+            ck(L.hep_gemm_bf16(x.data_ptr(), self.wg.data_ptr(), b["logits"].data_ptr(), T, self.e_pad, d, 0, s),
+               "hep_gemm_bf16(router)")
+            ck(L.hep_gate_topk(b["logits"].data_ptr(), self.e_pad, _lib.ptr(self.gate_bias), T, E, K, T, 1,
+                               b["topk_idx"].data_ptr(), b["topk_w"].data_ptr(), b["hist"].data_ptr(), s),
+               "hep_gate_topk")
+        hists = self.comm.all_gather([b["hist"] for b in bs])
+        for rk, x, b, h, (p_recv, p_back) in zip(self.ranks, xs, bs, hists, tabs):
+            T = x.shape[0]
+            b["hist_all"] = h
+            ck(L.hep_sched_solve(rk.sched.handle, h.data_ptr(), 1, E, None, HEP_SCHED_ALL,
+                                 ctypes.byref(rk.sched.out), s), "hep_sched_solve")
+            ck(L.hep_moe_assign_ep(rk.sched.handle, ctypes.byref(rk.sched.out), b["topk_idx"].data_ptr(), T, K,
+                                   rk.rank, b["tok_row"].data_ptr(), b["seg"].data_ptr(), b["counts"].data_ptr(),
+                                   b["assign_ws"].data_ptr(), b["assign_ws"].numel(), s), "hep_moe_assign_ep")
+            ck(L.hep_moe_dispatch_p2p(x.data_ptr(), b["tok_row"].data_ptr(), T, K, d, rk.rank, G,
+                                      rk.sched.transfer.data_ptr(), p_recv.data_ptr(), s), "hep_moe_dispatch_p2p")
+            ck(L.hep_moe_return_addr(rk.sched.transfer.data_ptr(), rk.rank, G, p_back.data_ptr(), d * 2, b["cap"],
+                                     b["y_addr"].data_ptr(), s), "hep_moe_return_addr")
+        self.comm.barrier()  # every receive buffer complete
+        if "ffn" in ev:
+            ev["ffn"][0].record(st)
+        for rk, b, x in zip(self.ranks, bs, xs):
+            n_seg = G * rk.n_hosted
+            x_rows = x.shape[0]  # balanced schedule: about T*K rows land on every rank
+            if n_seg:
+                ck(L.hep_moe_expert_ffn_p2p(b["recv"].data_ptr(), rk.w13.data_ptr(), rk.w2.data_ptr(),
+                                            b["seg"].data_ptr(), n_seg, b["cap"], x_rows * K, d, F, rk.n_slots,
+                                            b["h"].data_ptr(),
+                                            b["y_addr"].data_ptr(), b["ffn_ws"].data_ptr(), b["ffn_ws"].numel(),
+                                            rk.sched.status.data_ptr(), s), "hep_moe_expert_ffn_p2p")
+        if "ffn" in ev:
+            ev["ffn"][1].record(st)
+        self.comm.barrier()  # every expert output back at its source
+        outs = []
+        for x, b in zip(xs, bs):
+            T = x.shape[0]
+            ck(L.hep_moe_combine(b["back"].data_ptr(), b["tok_row"].data_ptr(), b["topk_w"].data_ptr(), T, K, d,
+                                 b["out"].data_ptr(), s), "hep_moe_combine")
+            outs.append(b["out"])
+        return outs
 
     def _forward(self, xs, st, ev):
         L = _lib.lib()

@@ -135,3 +135,95 @@ def test_local_ep_weight_migration(P):
         assert torch.equal(a.w13, b.w13) and torch.equal(a.w2, b.w2)
     pairs = lambda pl: {(e, g) for e, grp in enumerate(pl.edp_groups) for g in grp}  # noqa: E731
     assert st["moved_replicas"] == len(pairs(new) - pairs(old)) > 0
+
+
+@pytest.mark.parametrize("G,E,K,d,F,T,kind,s", [
+    (4, 8, 2, 512, 512, 4096, "cayley", 1.0),
+    (8, 32, 4, 256, 256, 4096, "asym", 1.5),
+    (8, 128, 8, 256, 256, 8192, "cayley", 1.0),
+])
+def test_local_ep_p2p_exchange_matches_collectives(P, G, E, K, d, F, T, kind, s):
+    """Both exchanges as peer-memory stores (dispatch kernel into the destination's
+    receive buffer, down-projection epilogue into the source's return buffer) give
+    the same bits as the all-to-all-v collectives and as the single-device layer."""
+    from paper_2511_16947_b200.ep import EPMoELayer, LocalComm
+
+    pl = _placement(P, G, E, kind, s)
+    bias = torch.tensor(P.zipf_gate_bias(E, s, 0))
+    x = torch.randn(T, d, generator=torch.Generator(device="cuda").manual_seed(11), device="cuda").to(torch.bfloat16)
+    xs = [x[r * (T // G):(r + 1) * (T // G)].contiguous() for r in range(G)]
+    a = EPMoELayer(pl, d, F, K, LocalComm(G), range(G), seed=6, gate_bias=bias)
+    b = EPMoELayer(pl, d, F, K, LocalComm(G), range(G), seed=6, gate_bias=bias, exchange="p2p")
+    ref = torch.cat([o.clone() for o in a.forward(xs)])
+    got = torch.cat([o.clone() for o in b.forward(xs)])
+    got2 = torch.cat([o.clone() for o in b.forward(xs)])  # buffers reused across micro-batches
+    torch.cuda.synchronize()
+    for rk in b.ranks:
+        rk.sched.check_status("p2p")
+    assert torch.equal(got, ref)
+    assert torch.equal(got2, ref)
+    sim = P.MoELayer(pl, d, F, K, seed=6, gate_bias=bias)
+    assert torch.equal(sim(x), ref)
+
+
+def _p2p_worker(rank, world, port, q):
+    import os
+
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2511_16947_b200 as P
+        from paper_2511_16947_b200.ep import DistComm, EPMoELayer
+
+        G, E, K, d, F, T = world, 8, 2, 256, 256, 2048
+        pl = P.cayley_symmetric(P.ClusterShape(G, E, 2))
+        bias = torch.tensor(P.zipf_gate_bias(E, 1.0, 0))
+        x = torch.randn(G * T, d, generator=torch.Generator(device="cuda").manual_seed(12), device="cuda")
+        x = x.to(torch.bfloat16)[rank * T:(rank + 1) * T].contiguous()
+        layer = EPMoELayer(pl, d, F, K, DistComm(), [rank], seed=7, gate_bias=bias, exchange="p2p")
+        outs = [layer.forward([x])[0].clone() for _ in range(2)]
+        torch.cuda.synchronize()
+        q.put((rank, outs[0].float().cpu().numpy(), outs[1].float().cpu().numpy()))  # pickled by value
+    except Exception as exc:  # report instead of hanging the parent
+        q.put((rank, repr(exc), None))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ep_p2p_over_cuda_ipc_two_processes(P):
+    """One process per rank (both on this GPU), peer buffers mapped with CUDA IPC:
+    the NVLink-path forward equals the in-process reference bit for bit."""
+    import socket
+
+    import torch.multiprocessing as mp
+    from paper_2511_16947_b200.ep import EPMoELayer, LocalComm
+
+    world = 2
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, o1, o2 = q.get(timeout=300)
+        res[r] = (o1, o2)
+    for p in procs:
+        p.join(timeout=60)
+    G, E, K, d, F, T = world, 8, 2, 256, 256, 2048
+    pl = P.cayley_symmetric(P.ClusterShape(G, E, 2))
+    bias = torch.tensor(P.zipf_gate_bias(E, 1.0, 0))
+    x = torch.randn(G * T, d, generator=torch.Generator(device="cuda").manual_seed(12), device="cuda").to(torch.bfloat16)
+    ref = EPMoELayer(pl, d, F, K, LocalComm(G), range(G), seed=7, gate_bias=bias).forward(
+        [x[r * T:(r + 1) * T].contiguous() for r in range(G)])
+    for r in range(world):
+        o1, o2 = res[r]
+        assert not isinstance(o1, str), o1
+        want = ref[r].float().cpu().numpy()
+        assert np.array_equal(o1, want) and np.array_equal(o2, want), r
