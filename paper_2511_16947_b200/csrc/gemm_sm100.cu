@@ -581,58 +581,120 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 // may span several destination GPUs' rows of the same expert.  One CTA; one
 // thread per expert chunk, deterministic block scan.
 // ---------------------------------------------------------------------------
+// Tiles of expert e: its segments in list order, contiguous ones (next row_start = end
+// of the previous) merged into runs, each run cut into tile_rows-row m-tiles.  One warp
+// per expert: lanes test 32 segments at a time, matches are merged in list order from
+// a ballot (all lanes keep the same run state), tile rows are written lane-parallel.
 template <bool WRITE>
-__device__ int64_t expert_tiles(const int32_t *seg, int n_seg, int e, int32_t *mt_row0, int32_t *mt_rows,
-                                int64_t pos, int tile_rows) {
+__device__ int64_t expert_tiles_warp(const int32_t *seg, int n_seg, int e, int32_t *mt_row0, int32_t *mt_rows,
+                                     int64_t pos, int tile_rows, int lane) {
     int64_t cnt = 0;
     int32_t r0 = 0, n = 0;
     bool open = false;
     auto flush = [&]() {
-        for (int32_t m = 0; m < n; m += tile_rows) {
-            if (WRITE) {
-                mt_row0[pos + cnt] = r0 + m;
-                mt_rows[pos + cnt] = min(tile_rows, n - m);
+        const int32_t nt = (n + tile_rows - 1) / tile_rows;
+        if (WRITE)
+            for (int32_t j = lane; j < nt; j += 32) {
+                mt_row0[pos + cnt + j] = r0 + j * tile_rows;
+                mt_rows[pos + cnt + j] = min(tile_rows, n - j * tile_rows);
             }
-            ++cnt;
-        }
+        cnt += nt;
     };
-    for (int s = 0; s < n_seg; ++s) {
-        if (seg[4 * s + 2] != e || seg[4 * s + 1] == 0) continue;
-        const int32_t a = seg[4 * s], b = seg[4 * s + 1];
-        if (open && a == r0 + n) {
-            n += b;
-        } else {
-            if (open) flush();
-            r0 = a;
-            n = b;
-            open = true;
+    for (int base = 0; base < n_seg; base += 32) {
+        const int s = base + lane;
+        int32_t a = 0, b = 0;
+        bool m = false;
+        if (s < n_seg) {
+            a = seg[4 * s];
+            b = seg[4 * s + 1];
+            m = seg[4 * s + 2] == e && b != 0;
+        }
+        uint32_t mask = __ballot_sync(0xffffffffu, m);
+        while (mask) {
+            const int l = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const int32_t sa = __shfl_sync(0xffffffffu, a, l), sb = __shfl_sync(0xffffffffu, b, l);
+            if (open && sa == r0 + n) {
+                n += sb;
+            } else {
+                if (open) flush();
+                r0 = sa;
+                n = sb;
+                open = true;
+            }
         }
     }
     if (open) flush();
     return cnt;
 }
 
-__global__ void build_tiles_kernel(const int32_t *seg, int n_seg, int n_exp, int32_t *mt_row0, int32_t *mt_rows,
-                                   int32_t *exp_mt_off, int64_t cap, int32_t *status, int tile_rows) {
+constexpr int kTileSegSmem = 2048;  // segments staged in shared memory (16 B each)
+constexpr int kTileWarps = 8;       // experts per block (one warp each)
+
+__device__ __forceinline__ const int32_t *stage_segments(const int32_t *seg_g, int n_seg, int4 *st) {
+    if (n_seg > kTileSegSmem) return seg_g;
+    for (int i = threadIdx.x; i < n_seg; i += blockDim.x) st[i] = reinterpret_cast<const int4 *>(seg_g)[i];
+    __syncthreads();
+    return reinterpret_cast<const int32_t *>(st);
+}
+
+// pass 1: m-tiles per expert (one warp per expert, experts spread over blocks/SMs)
+__global__ void __launch_bounds__(32 * kTileWarps) tile_count_kernel(const int32_t *seg_g, int n_seg, int n_exp,
+                                                                     int32_t *exp_cnt, int tile_rows) {
+    extern __shared__ int4 st[];
+    const int32_t *seg = stage_segments(seg_g, n_seg, st);
+    const int lane = threadIdx.x & 31, e = blockIdx.x * kTileWarps + (threadIdx.x >> 5);
+    if (e >= n_exp) return;
+    const int64_t c = expert_tiles_warp<false>(seg, n_seg, e, nullptr, nullptr, 0, tile_rows, lane);
+    if (lane == 0) exp_cnt[e] = (int32_t)c;
+}
+
+// pass 2: every block scans the per-expert counts (n_exp <= 1024) and writes its experts'
+// m-tiles at their offsets; block 0 publishes the offsets.
+__global__ void __launch_bounds__(32 * kTileWarps) tile_write_kernel(const int32_t *seg_g, int n_seg, int n_exp,
+                                                                     const int32_t *exp_cnt, int32_t *mt_row0,
+                                                                     int32_t *mt_rows, int32_t *exp_mt_off,
+                                                                     int64_t cap, int32_t *status, int tile_rows) {
+    extern __shared__ int4 st[];
     __shared__ int64_t scan[64];
-    const int tid = threadIdx.x, nt = blockDim.x;
+    __shared__ int64_t off_sm[kTileWarps];
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5;
+    const int e_first = blockIdx.x * kTileWarps;
     const int chunk = (n_exp + nt - 1) / nt;
     const int e0 = min(n_exp, tid * chunk), e1 = min(n_exp, e0 + chunk);
-    int64_t cnt = 0;
-    for (int e = e0; e < e1; ++e) cnt += expert_tiles<false>(seg, n_seg, e, nullptr, nullptr, 0, tile_rows);
+    int64_t mine = 0;
+    for (int e = e0; e < e1; ++e) mine += exp_cnt[e];
     int64_t total;
-    int64_t pos = block_excl_scan_i64(cnt, scan, &total);
+    int64_t pos = block_excl_scan_i64(mine, scan, &total);
+    for (int e = e0; e < e1; ++e) {
+        if (e >= e_first && e < e_first + kTileWarps) off_sm[e - e_first] = pos;
+        if (blockIdx.x == 0 && total <= cap) exp_mt_off[e] = (int32_t)pos;
+        pos += exp_cnt[e];
+    }
     if (total > cap) {
-        if (tid == 0 && status) atomicCAS(status, 0, HEP_E_CAPACITY);
-        if (tid == 0) exp_mt_off[n_exp] = 0;
-        for (int e = e0; e < e1; ++e) exp_mt_off[e] = 0;
+        if (blockIdx.x == 0 && tid == 0 && status) atomicCAS(status, 0, HEP_E_CAPACITY);
+        if (blockIdx.x == 0)
+            for (int e = tid; e <= n_exp; e += nt) exp_mt_off[e] = 0;
         return;
     }
-    for (int e = e0; e < e1; ++e) {
-        exp_mt_off[e] = (int32_t)pos;
-        pos += expert_tiles<true>(seg, n_seg, e, mt_row0, mt_rows, pos, tile_rows);
-    }
-    if (tid == nt - 1) exp_mt_off[n_exp] = (int32_t)total;
+    if (blockIdx.x == 0 && tid == 0) exp_mt_off[n_exp] = (int32_t)total;
+    const int32_t *seg = stage_segments(seg_g, n_seg, st);  // includes the barrier for off_sm
+    const int e = e_first + w;
+    if (e < n_exp) expert_tiles_warp<true>(seg, n_seg, e, mt_row0, mt_rows, off_sm[w], tile_rows, lane);
+}
+
+// build the device m-tile list of a grouped GEMM from its segments (2 launches)
+static int build_tiles(const int32_t *d_seg, int n_seg, int n_exp, int32_t *mt_row0, int32_t *mt_rows,
+                       int32_t *exp_off, int32_t *exp_cnt, int64_t cap, int32_t *d_status, int tile_rows,
+                       cudaStream_t s) {
+    const size_t sm = n_seg <= kTileSegSmem ? 16 * (size_t)n_seg : 0;
+    const int blocks = n_exp > 0 ? (n_exp + kTileWarps - 1) / kTileWarps : 1;
+    tile_count_kernel<<<blocks, 32 * kTileWarps, sm, s>>>(d_seg, n_seg, n_exp, exp_cnt, tile_rows);
+    HEP_CHECK_LAUNCH();
+    tile_write_kernel<<<blocks, 32 * kTileWarps, sm, s>>>(d_seg, n_seg, n_exp, exp_cnt, mt_row0, mt_rows, exp_off, cap,
+                                                          d_status, tile_rows);
+    HEP_CHECK_LAUNCH();
+    return HEP_OK;
 }
 
 // ---------------------------------------------------------------------------
@@ -794,7 +856,8 @@ extern "C" int hep_gemm_bf16(const void *d_A, const void *d_B, void *d_D, int64_
 
 extern "C" size_t hep_moe_ffn_workspace(int n_seg, int64_t R, int n_experts) {
     const int64_t cap = R / BM + n_seg + 1;
-    return (size_t)(2 * cap + n_experts + 1 + 1) * sizeof(int32_t) + 64;
+    // m-tile rows / sizes [cap] x2, expert tile offsets [E+1], per-expert tile counts [E]
+    return (size_t)(2 * cap + 2 * (int64_t)n_experts + 2) * sizeof(int32_t) + 64;
 }
 
 static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg, int n_seg,
@@ -847,17 +910,19 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
     const bool pairs = use_pairs(rows_hint >= 0 ? rows_hint : R, n_experts);
     const char *pol_env = getenv("HEP_L2POL");
     const int pol_mode = pol_env ? atoi(pol_env) : 0;
-    build_tiles_kernel<<<1, 1024, 0, s>>>(d_seg, n_seg, n_experts, mt_row0, mt_rows, exp_off, cap, d_status,
-                                          pairs ? kPairRows : BM);
-    HEP_CHECK_LAUNCH();
+    int rc0 = build_tiles(d_seg, n_seg, n_experts, mt_row0, mt_rows, exp_off, exp_off + n_experts + 1, cap, d_status,
+                          pairs ? kPairRows : BM, s);
+    if (rc0) return rc0;
     Params p{};
     p.grouped = 1;
     p.pol_mode = pol_mode;
+    // raster bands (m-tiles swept across all N-blocks before the next band): 16 for the
+    // SwiGLU GEMM, 8 for the down projection (profiles/r01/raster*.txt)
     const char *gm_env = getenv("HEP_RASTER_GM");
-    const int gm_default = gm_env ? atoi(gm_env) : 8;  // measured best (profiles/r01/raster.txt)
     const char *gm1_env = getenv("HEP_RASTER_GM1");
     const char *gm2_env = getenv("HEP_RASTER_GM2");
-    p.raster_gm = gm1_env ? atoi(gm1_env) : gm_default;
+    const int gm_default = gm_env ? atoi(gm_env) : -1;
+    p.raster_gm = gm1_env ? atoi(gm1_env) : (gm_default >= 0 ? gm_default : 16);
     p.mt_row0 = mt_row0;
     p.mt_rows = mt_rows;
     p.exp_mt_off = exp_off;
@@ -877,7 +942,7 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
     // GEMM 2: Y = H W2^T, B = W2 [E][d][F]
     p.aux = nullptr;
     p.row_addr = d_y_addr;
-    p.raster_gm = gm2_env ? atoi(gm2_env) : gm_default;
+    p.raster_gm = gm2_env ? atoi(gm2_env) : (gm_default >= 0 ? gm_default : 8);
     p.kblocks = (int)(ffn / BK);
     p.n_tiles = (int)(d_model / 256);
     p.b_rows_per_exp = d_model;
@@ -916,8 +981,9 @@ extern "C" int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, con
     int32_t *mt_row0 = reinterpret_cast<int32_t *>(d_workspace);
     int32_t *mt_rows = mt_row0 + cap;
     int32_t *exp_off = mt_rows + cap;
-    build_tiles_kernel<<<1, 1024, 0, s>>>(d_seg, n_seg, n_experts, mt_row0, mt_rows, exp_off, cap, d_status, BM);
-    HEP_CHECK_LAUNCH();
+    if ((rc = build_tiles(d_seg, n_seg, n_experts, mt_row0, mt_rows, exp_off, exp_off + n_experts + 1, cap, d_status,
+                          BM, s)))
+        return rc;
     CUtensorMap ta, tb;
     Params p{};
     // --- dA13 = swiglu'(A13) * (dY W2)

@@ -121,7 +121,7 @@ class MoELayer(torch.nn.Module):
             if train:
                 raise ValueError("the pipelined split is a forward (serving) schedule; train with pipeline_ratio=None")
             self.static_share = Fraction(1) - Fraction(pipeline_ratio)
-        self.LAUNCHES_PER_FORWARD = 12 if self.static_share is None else 18
+        self.LAUNCHES_PER_FORWARD = 13 if self.static_share is None else 19
         torch_ = _lib.require_cuda()
         self.device = torch_.device("cuda", torch_.cuda.current_device()) if device is None else torch_.device(device)
         self.placement = placement
@@ -256,7 +256,7 @@ class MoELayer(torch.nn.Module):
 
     def capture(self, x: torch.Tensor) -> "torch.cuda.CUDAGraph":
         """Record one forward on ``x`` (fixed buffers, no host sync anywhere in the
-        chain) as a CUDA graph; ``graph.replay()`` re-runs all 12 kernels with one
+        chain) as a CUDA graph; ``graph.replay()`` re-runs all 13 kernels with one
         launch.  ``x`` must stay the input tensor (refill it in place)."""
         b = self.buffers(x.shape[0])
         side = torch.cuda.Stream(device=self.device)
@@ -271,9 +271,9 @@ class MoELayer(torch.nn.Module):
         return g
 
     # kernels launched per forward: router GEMM, gate top-K, scheduler, assign x4,
-    # permute, FFN (tile list + 2 GEMMs), combine (pipelined split: + split kernel,
-    # second scheduler launch, second assignment x4)
-    LAUNCHES_PER_FORWARD = 12
+    # permute, FFN (tile count + tile list + 2 GEMMs), combine (pipelined split: + split
+    # kernel, second scheduler launch, second assignment x4)
+    LAUNCHES_PER_FORWARD = 13
 
     def check_status(self):
         self.sched.check_status("MoELayer")
@@ -327,7 +327,7 @@ class MoELayer(torch.nn.Module):
                                 dx.data_ptr(), s), "hep_moe_gather_sum")
         return dx, dwg[:E], dw13, dw2
 
-    LAUNCHES_PER_BACKWARD = 12  # combine_bwd, zero_pad x2, tiles, 4 GEMMs, gate_bwd, 2 router GEMMs, gather
+    LAUNCHES_PER_BACKWARD = 13  # combine_bwd, zero_pad x2, tiles x2, 4 GEMMs, gate_bwd, 2 router GEMMs, gather
 
 
 class MoEFunction(torch.autograd.Function):

@@ -4,8 +4,8 @@
 
 Each CSV is one `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,
 dram__bytes_write.sum --csv` run of `bench.py --config <cfg> --profile`.  The
-expert FFN (`hep_moe_expert_ffn` = tile-list kernel + two grouped GEMMs) is
-summed over its three launches; permute and combine are single launches.
+expert FFN (`hep_moe_expert_ffn` = two tile-list kernels + two grouped GEMMs) is
+summed over its four launches; permute and combine are single launches.
 bench.py reads the resulting JSON to fill `roofline.traffic`."""
 import csv
 import json
@@ -28,8 +28,8 @@ def summarise(path):
     ks = launches(path)
     out = {"source": os.path.relpath(path)}
     for i, k in enumerate(ks):
-        if "build_tiles_kernel" in k["name"] and i + 2 < len(ks):
-            trio = ks[i:i + 3]
+        if "tile_count_kernel" in k["name"] and i + 3 < len(ks):
+            trio = ks[i:i + 4]  # tile count, tile list, SwiGLU GEMM, down-projection GEMM
             out["ffn"] = {
                 "bytes": sum(x.get("dram__bytes_read.sum", 0) + x.get("dram__bytes_write.sum", 0) for x in trio),
                 "read": sum(x.get("dram__bytes_read.sum", 0) for x in trio),
