@@ -29,7 +29,8 @@ using namespace sm100;
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle atom row
-constexpr int kThreads = 192;
+constexpr int kEpiWarps = 8;  // two epilogue warps per TMEM lane quarter, each half the columns
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 
 enum Epi { EPI_SWIGLU = 0, EPI_BF16 = 1, EPI_F32 = 2, EPI_SWIGLU_BWD = 3 };
 
@@ -160,7 +161,14 @@ __device__ __forceinline__ float bf16hi(uint32_t v) { return __uint_as_float(v &
 
 template <int BN, int EPI>
 __device__ __forceinline__ void store_tile(const Params &p, uint32_t t_row, int64_t grow, bool valid, int n_blk,
-                                           uint64_t pol_out, int expert = 0, bool zero = false) {
+                                           uint64_t pol_out, int expert, bool zero, int half) {
+    // this warp's share of the tile's columns: half 0 / 1 of the accumulator
+    // (spans under 32 columns are not split: the second warp of the quarter idles)
+    constexpr int SPAN = EPI == EPI_SWIGLU ? BN / 2 : BN;
+    constexpr bool SPLIT = SPAN >= 32;
+    static_assert(EPI != EPI_BF16 || SPAN % 64 == 0, "bf16 epilogue stores 32 columns per step");
+    const int c_begin = SPLIT ? half * (SPAN / 2) : 0;
+    const int c_end = SPLIT ? c_begin + SPAN / 2 : (half == 0 ? SPAN : 0);
     if constexpr (EPI == EPI_SWIGLU_BWD) {
         // accumulator = dH for ffn columns [n_blk*BN, +BN); the pre-activations
         // (gate a, up b) live in aux with the W13 interleave (128-blocks: gate j, up j).
@@ -168,7 +176,7 @@ __device__ __forceinline__ void store_tile(const Params &p, uint32_t t_row, int6
         const __nv_bfloat16 *pre = reinterpret_cast<const __nv_bfloat16 *>(p.aux) + grow * p.ld_aux;
         __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(p.out) + grow * p.ld_out;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 16) {
+        for (int c = c_begin; c < c_end; c += 16) {
             uint32_t v[16];
             tmem_ld16(t_row + c, v);
             tmem_ld_wait();
@@ -202,7 +210,7 @@ __device__ __forceinline__ void store_tile(const Params &p, uint32_t t_row, int6
         __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(p.out) + grow * p.ld_out +
                              (int64_t)n_blk * (BN / 2);
 #pragma unroll 1
-        for (int c = 0; c < BN / 2; c += 16) {
+        for (int c = c_begin; c < c_end; c += 16) {
             uint32_t g[16], u[16];
             tmem_ld16(t_row + c, g);
             tmem_ld16(t_row + BN / 2 + c, u);
@@ -239,22 +247,25 @@ __device__ __forceinline__ void store_tile(const Params &p, uint32_t t_row, int6
                     : reinterpret_cast<__nv_bfloat16 *>(p.out) + grow * p.ld_out) +
             (int64_t)n_blk * BN;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 16) {
-            uint32_t v[16];
+        for (int c = c_begin; c < c_end; c += 32) {  // two TMEM loads in flight per wait
+            uint32_t v[16], w[16];
             tmem_ld16(t_row + c, v);
+            tmem_ld16(t_row + c + 16, w);
             tmem_ld_wait();
-            uint32_t packed[8];
+            uint32_t packed[16];
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < 8; ++i) {
                 packed[i] = pack_bf16(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+                packed[8 + i] = pack_bf16(__uint_as_float(w[2 * i]), __uint_as_float(w[2 * i + 1]));
+            }
             if (valid) {
-                if (remote) {  // peer (NVLink) or local destination row: plain 16-byte stores
-                    uint4 *o = reinterpret_cast<uint4 *>(out + c);
-                    o[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-                    o[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
-                } else {
-                    st_global_v4_hint(out + c, make_uint4(packed[0], packed[1], packed[2], packed[3]), pol_out);
-                    st_global_v4_hint(out + c + 8, make_uint4(packed[4], packed[5], packed[6], packed[7]), pol_out);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint4 val = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
+                    if (remote)  // peer (NVLink) or local destination row: plain 16-byte stores
+                        reinterpret_cast<uint4 *>(out + c)[q] = val;
+                    else
+                        st_global_v4_hint(out + c + 8 * q, val, pol_out);
                 }
             }
         }
@@ -263,7 +274,7 @@ __device__ __forceinline__ void store_tile(const Params &p, uint32_t t_row, int6
                      (int64_t)n_blk * BN;
         const int64_t col0 = (int64_t)n_blk * BN;
 #pragma unroll 1
-        for (int c = 0; c < BN; c += 16) {
+        for (int c = c_begin; c < c_end; c += 16) {
             uint32_t v[16];
             tmem_ld16(t_row + c, v);
             tmem_ld_wait();
@@ -317,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);
+            mbar_init(&tempty[a], kEpiWarps);
         }
         fence_barrier_init();
         fence_proxy_async_smem();
@@ -403,9 +414,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else {
-        // ===================== epilogue (warps 2..5) =====================
+        // ===================== epilogue (warps 2..9) =====================
         const uint64_t pol_out = policy_evict_first();  // outputs are not re-read from L2 soon
         const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32)
+        const int half = (warp - 2) >> 2;  // which half of the columns
         const int row_in_tile = quarter * 32 + lane;
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -416,7 +428,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
             const bool valid = row_in_tile < tl.rows;
             const int64_t grow = (int64_t)tl.row0 + row_in_tile;
-            store_tile<BN, EPI>(p, t_row, grow, valid, tl.n_blk, pol_out, tl.expert, tl.kb == 0);
+            store_tile<BN, EPI>(p, t_row, grow, valid, tl.n_blk, pol_out, tl.expert, tl.kb == 0, half);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -480,7 +492,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 8);  // 4 epilogue warps x 2 CTAs
+            mbar_init(&tempty[a], 2 * kEpiWarps);  // epilogue warps of both CTAs
         }
         fence_barrier_init();
         fence_proxy_async_smem();
@@ -545,10 +557,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             }
         }
     } else {
-        // ===================== epilogue (warps 2..5, both CTAs) =====================
+        // ===================== epilogue (warps 2..9, both CTAs) =====================
         const uint64_t pol_out = policy_evict_first();
         const uint32_t tempty_l = mapa_shared(smem_u32(&tempty[0]), 0);
         const int quarter = warp & 3;
+        const int half = (warp - 2) >> 2;
         const int row_in_cta = quarter * 32 + lane;
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -558,7 +571,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
             const int local_row = (int)rank * 128 + row_in_cta;
-            store_tile<BN, EPI>(p, t_row, (int64_t)tl.row0 + local_row, local_row < tl.rows, tl.n_blk, pol_out);
+            store_tile<BN, EPI>(p, t_row, (int64_t)tl.row0 + local_row, local_row < tl.rows, tl.n_blk, pol_out, 0, false,
+                                half);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(tempty_l + 8 * acc);
