@@ -28,7 +28,7 @@ NVCC_FLAGS = [
     "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
     "--expt-relaxed-constexpr",
     "-Xptxas", "-v",
-]
+] + os.environ.get("HEP_NVCC_DEFS", "").split()  # tuning builds, e.g. -DHEP_EPI_SPLIT=4
 
 
 def _stale(target: str, deps: list[str]) -> bool:

@@ -29,7 +29,11 @@ using namespace sm100;
 
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B = one swizzle atom row
-constexpr int kEpiWarps = 8;  // two epilogue warps per TMEM lane quarter, each half the columns
+#ifndef HEP_EPI_SPLIT
+#define HEP_EPI_SPLIT 2
+#endif
+constexpr int kEpiSplit = HEP_EPI_SPLIT;  // epilogue warps per TMEM lane quarter (column slices)
+constexpr int kEpiWarps = 4 * kEpiSplit;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 
 enum Epi { EPI_SWIGLU = 0, EPI_BF16 = 1, EPI_F32 = 2, EPI_SWIGLU_BWD = 3 };
@@ -67,13 +71,18 @@ __device__ __forceinline__ uint64_t pick_policy(int k) {
     return k == 2 ? sm100::policy_evict_last() : (k == 3 ? sm100::policy_evict_first() : sm100::policy_evict_normal());
 }
 
+// grouped mode: p.exp_mt_off staged in shared memory (the per-tile binary search over
+// experts would otherwise be a chain of dependent global loads in every warp role)
+constexpr int kMaxExpSmem = 1024;
+constexpr int kOffBytes = 4 * (kMaxExpSmem + 4);
+
 template <int BN, int STAGES>
 struct Smem {
     static constexpr int A_BYTES = BM * BK * 2;
     static constexpr int B_BYTES = BN * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128 : (2 * BN <= 256) ? 256 : 512;
-    static constexpr size_t BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + 8 * (2 * STAGES + 4) + 16;
+    static constexpr size_t BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + 8 * (2 * STAGES + 4) + 16 + kOffBytes;
 };
 
 struct Tile {
@@ -89,7 +98,7 @@ __device__ __forceinline__ int64_t total_tiles(const Params &p) {
     return (int64_t)p.exp_mt_off[p.n_exp] * p.n_tiles;
 }
 
-__device__ __forceinline__ Tile decode(const Params &p, int64_t t) {
+__device__ __forceinline__ Tile decode(const Params &p, int64_t t, const int32_t *off) {
     Tile tl;
     tl.k0 = 0;
     tl.kb = p.kblocks;
@@ -119,11 +128,11 @@ __device__ __forceinline__ Tile decode(const Params &p, int64_t t) {
     int lo = 0, hi = p.n_exp - 1;
     while (lo < hi) {
         int mid = (lo + hi + 1) >> 1;
-        if ((int64_t)p.exp_mt_off[mid] * p.n_tiles <= t) lo = mid; else hi = mid - 1;
+        if ((int64_t)off[mid] * p.n_tiles <= t) lo = mid; else hi = mid - 1;
     }
     const int e = lo;
-    const int64_t base = (int64_t)p.exp_mt_off[e];
-    const int64_t mt_e = (int64_t)p.exp_mt_off[e + 1] - base;
+    const int64_t base = (int64_t)off[e];
+    const int64_t mt_e = (int64_t)off[e + 1] - base;
     const int64_t local = t - base * p.n_tiles;
     tl.expert = e;
     int64_t m;
@@ -163,12 +172,12 @@ template <int BN, int EPI>
 __device__ __forceinline__ void store_tile(const Params &p, uint32_t t_row, int64_t grow, bool valid, int n_blk,
                                            uint64_t pol_out, int expert, bool zero, int half) {
     // this warp's share of the tile's columns: half 0 / 1 of the accumulator
-    // (spans under 32 columns are not split: the second warp of the quarter idles)
+    // (spans under 16 columns per slice are not split: slice 0 takes them all)
     constexpr int SPAN = EPI == EPI_SWIGLU ? BN / 2 : BN;
-    constexpr bool SPLIT = SPAN >= 32;
-    static_assert(EPI != EPI_BF16 || SPAN % 64 == 0, "bf16 epilogue stores 32 columns per step");
-    const int c_begin = SPLIT ? half * (SPAN / 2) : 0;
-    const int c_end = SPLIT ? c_begin + SPAN / 2 : (half == 0 ? SPAN : 0);
+    constexpr bool SPLIT = SPAN / kEpiSplit >= 16;
+    static_assert(EPI != EPI_BF16 || (SPAN / kEpiSplit) % 32 == 0, "bf16 epilogue stores 32 columns per step");
+    const int c_begin = SPLIT ? half * (SPAN / kEpiSplit) : 0;
+    const int c_end = SPLIT ? c_begin + SPAN / kEpiSplit : (half == 0 ? SPAN : 0);
     if constexpr (EPI == EPI_SWIGLU_BWD) {
         // accumulator = dH for ffn columns [n_blk*BN, +BN); the pre-activations
         // (gate a, up b) live in aux with the W13 interleave (128-blocks: gate j, up j).
@@ -317,6 +326,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *tfull = empty + STAGES;
     uint64_t *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    int32_t *s_off = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(tmem_slot) + 16);
+    if (p.grouped == 1)
+        for (int i = threadIdx.x; i <= p.n_exp; i += blockDim.x) s_off[i] = p.exp_mt_off[i];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == 0 && lane == 0) {
@@ -353,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t pol_b = p.pol_mode ? pick_policy((p.pol_mode >> 2) & 3) : (p.grouped ? policy_evict_normal() : policy_evict_last());
             uint32_t phase = 0;
             for (int64_t t = blockIdx.x; t < n_total; t += gridDim.x) {
-                const Tile tl = decode(p, t);
+                const Tile tl = decode(p, t, s_off);
                 const int32_t b_row = (int32_t)(tl.expert * p.b_rows_per_exp + (int64_t)tl.n_blk * BN);
                 // contraction offsets: mode 2 contracts over the expert's rows; an MN-major
                 // weight (mode 1) is [K][N] per expert, stacked along K
@@ -391,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int64_t t = blockIdx.x; t < n_total; t += gridDim.x) {
-                const int tkb = p.grouped == 2 ? decode(p, t).kb : kb;
+                const int tkb = p.grouped == 2 ? decode(p, t, s_off).kb : kb;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
@@ -417,12 +429,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ===================== epilogue (warps 2..9) =====================
         const uint64_t pol_out = policy_evict_first();  // outputs are not re-read from L2 soon
         const int quarter = warp & 3;  // TMEM lanes [32*quarter, 32*quarter+32)
-        const int half = (warp - 2) >> 2;  // which half of the columns
+        const int half = (warp - 2) >> 2;  // which column slice
         const int row_in_tile = quarter * 32 + lane;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int64_t t = blockIdx.x; t < n_total; t += gridDim.x) {
-            const Tile tl = decode(p, t);
+            const Tile tl = decode(p, t, s_off);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
@@ -431,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             store_tile<BN, EPI>(p, t_row, grow, valid, tl.n_blk, pol_out, tl.expert, tl.kb == 0, half);
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) mbar_arrive_relaxed(&tempty[acc]);
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
     }
@@ -461,7 +473,7 @@ struct Smem2 {
     static constexpr int A_BYTES = 128 * BK * 2;
     static constexpr int B_BYTES = 128 * BK * 2;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr size_t BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + 8 * (2 * STAGES + 4) + 16;
+    static constexpr size_t BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + 8 * (2 * STAGES + 4) + 16 + kOffBytes;
 };
 
 template <int STAGES, int EPI>
@@ -479,6 +491,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint64_t *tfull = empty + STAGES;
     uint64_t *tempty = tfull + 2;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    int32_t *s_off = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(tmem_slot) + 16);
+    if (p.grouped == 1)
+        for (int i = threadIdx.x; i <= p.n_exp; i += blockDim.x) s_off[i] = p.exp_mt_off[i];
 
     const uint32_t rank = cluster_ctarank();
     const bool leader = rank == 0;
@@ -516,7 +531,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int64_t t = cid; t < n_total; t += ncl) {
-                const Tile tl = decode(p, t);
+                const Tile tl = decode(p, t, s_off);
                 const int32_t a_row = tl.row0 + (int32_t)rank * 128;
                 const int32_t b_row = (int32_t)(tl.expert * p.b_rows_per_exp + (int64_t)tl.n_blk * BN) + (int32_t)rank * 128;
                 for (int k = 0; k < kb; ++k) {
@@ -566,7 +581,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int64_t t = cid; t < n_total; t += ncl) {
-            const Tile tl = decode(p, t);
+            const Tile tl = decode(p, t, s_off);
             mbar_wait_cluster(&tfull[acc], acc_phase);
             tc_fence_after();
             const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
@@ -575,7 +590,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                                 half);
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(tempty_l + 8 * acc);
+            if (lane == 0) mbar_arrive_cluster_relaxed(tempty_l + 8 * acc);
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
     }
@@ -915,6 +930,7 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
                 "expert FFN needs d_model %% 256 == 0 and ffn %% 128 == 0 (d=%lld F=%lld)", (long long)d_model,
                 (long long)ffn);
     HEP_REQUIRE(workspace_bytes >= hep_moe_ffn_workspace(n_seg, R, n_experts), HEP_E_CAPACITY, "workspace too small");
+    HEP_REQUIRE(n_experts <= kMaxExpSmem, HEP_E_CAPACITY, "expert FFN: at most %d experts (slots)", kMaxExpSmem);
     if (R <= 0) return HEP_OK;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t cap = R / BM + n_seg + 1;
@@ -987,6 +1003,7 @@ extern "C" int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, con
     HEP_REQUIRE(d_model % 256 == 0 && ffn % 256 == 0, HEP_E_DIMENSION,
                 "FFN backward needs d_model %% 256 == 0 and ffn %% 256 == 0");
     HEP_REQUIRE(workspace_bytes >= hep_moe_ffn_workspace(n_seg, Rcap, n_experts), HEP_E_CAPACITY, "workspace too small");
+    HEP_REQUIRE(n_experts <= kMaxExpSmem, HEP_E_CAPACITY, "expert FFN backward: at most %d experts", kMaxExpSmem);
     if (Rcap <= 0) return HEP_OK;
     cudaStream_t s = (cudaStream_t)stream;
     int rc = hep_moe_zero_padding(d_expert_rows, d_seg, n_seg, n_experts, d_dy, d_model, stream);
