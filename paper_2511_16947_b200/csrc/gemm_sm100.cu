@@ -707,7 +707,8 @@ __global__ void __launch_bounds__(32 * kTileWarps) tile_write_kernel(const int32
         return;
     }
     if (blockIdx.x == 0 && tid == 0) exp_mt_off[n_exp] = (int32_t)total;
-    const int32_t *seg = stage_segments(seg_g, n_seg, st);  // includes the barrier for off_sm
+    __syncthreads();  // off_sm (stage_segments only synchronises when it stages)
+    const int32_t *seg = stage_segments(seg_g, n_seg, st);
     const int e = e_first + w;
     if (e < n_exp) expert_tiles_warp<true>(seg, n_seg, e, mt_row0, mt_rows, off_sm[w], tile_rows, lane);
 }
@@ -836,12 +837,14 @@ static int launch2sm(const void *A, int64_t a_rows, int64_t K, const void *B, in
     return HEP_OK;
 }
 
-// CTA pairs when experts carry enough rows that 256-row tiles do not waste
-// more than the 128-row tiles they replace; HEP_FFN_PAIR=0/1 forces it.
+// CTA pairs unless experts carry so few rows that 256-row tiles waste more than
+// the pair's halved operand traffic saves: measured in-process (tools/ffn_ab.py,
+// profiles/r01/ffn_ab_r01d.txt) the pair wins at 512 rows per expert (DeepSeek-V3
+// shape) and above.  HEP_FFN_PAIR=0/1 forces it.
 static bool use_pairs(int64_t R, int n_experts) {
     const char *env = getenv("HEP_FFN_PAIR");
     if (env && *env) return env[0] == '1';
-    return n_experts > 0 && R / n_experts >= 1024;
+    return n_experts > 0 && R / n_experts >= 512;
 }
 
 }  // namespace gemm

@@ -95,3 +95,57 @@ def test_grouped_expert_ffn(L, E, d, F, sizes):
         assert torch.isfinite(got).all()
         rel = (got - ref).abs().max().item() / max(ref.abs().max().item(), 1e-6)
         assert rel <= 1e-2, (e, n, rel)
+
+
+def _run_ffn(L, x, w13, w2, segs, R, d, F, E):
+    dev = x.device
+    seg = torch.tensor(segs, dtype=torch.int32, device=dev)
+    h = torch.empty(max(R, 1), F, dtype=torch.bfloat16, device=dev)
+    y = torch.full((max(R, 1), d), float("nan"), dtype=torch.bfloat16, device=dev)
+    lib = L.lib()
+    ws = torch.empty(int(lib.hep_moe_ffn_workspace(len(segs), R, E)), dtype=torch.uint8, device=dev)
+    st = torch.zeros(1, dtype=torch.int32, device=dev)
+    L.check(lib.hep_moe_expert_ffn(x.data_ptr(), w13.data_ptr(), w2.data_ptr(), seg.data_ptr(), len(segs), R, d, F, E,
+                                   h.data_ptr(), y.data_ptr(), ws.data_ptr(), ws.numel(), st.data_ptr(),
+                                   L.stream_handle()), "ffn")
+    torch.cuda.synchronize()
+    assert int(st.item()) == 0
+    return h, y
+
+
+@pytest.mark.parametrize("E,d,F", [(24, 512, 768), (40, 256, 256), (12, 512, 1024)])
+def test_grouped_ffn_skewed_sizes_pair_and_single(L, E, d, F, monkeypatch):
+    """Skewed expert sizes as a Zipf gate produces them: most experts carry a handful
+    of rows (one partial m-tile), a few carry many tiles with a partial tail.  Both the
+    1-CTA kernel (128-row tiles) and the CTA-pair kernel (256-row tiles) are checked
+    against fp32 torch, and must agree bit for bit (each output element is the same
+    K-ordered dot product whatever tile it lands in)."""
+    from paper_2511_16947_b200.layer import init_expert_weights, interleave_w13
+
+    dev = "cuda"
+    w1, w2, w3 = init_expert_weights(E, d, F, seed=5, device=dev)
+    w13 = interleave_w13(w1, w3)
+    base = [0, 1, 2, 15, 16, 17, 31, 33, 64, 65, 100, 111, 112, 113, 127, 128, 129, 255, 257, 320, 700, 1500]
+    sizes = [base[(7 * e) % len(base)] for e in range(E)]
+    segs, row = [], 0
+    for e in reversed(range(E)):  # one contiguous segment per expert, arbitrary expert order
+        segs.append((row, sizes[e], e, 0))
+        row += sizes[e]
+    R = row
+    x = torch.randn(R, d, device=dev).to(torch.bfloat16)
+    outs = {}
+    for pair in ("0", "1"):
+        monkeypatch.setenv("HEP_FFN_PAIR", pair)
+        outs[pair] = _run_ffn(L, x, w13, w2, segs, R, d, F, E)
+    for pair in ("0", "1"):
+        h, y = outs[pair]
+        for (r0, n, e, _) in segs:
+            if n == 0:
+                continue
+            ref = _ffn_ref(x[r0:r0 + n].float(), w1[e].float(), w3[e].float(), w2[e].float())
+            got = y[r0:r0 + n].float()
+            assert torch.isfinite(got).all()
+            rel = (got - ref).abs().max().item() / max(ref.abs().max().item(), 1e-6)
+            assert rel <= 1e-2, (pair, e, n, rel)
+    assert torch.equal(outs["0"][0], outs["1"][0])
+    assert torch.equal(outs["0"][1], outs["1"][1])
