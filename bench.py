@@ -334,7 +334,7 @@ def run_ep(args, world, rank, local, dev):
             "max_mean_gpu_load": mm, "max_mean_gpu_load_static_cayley": static_mm, "replacement": replacement,
             "e2e": {"value": world * T * args.steps / (e_ms / 1e3), "unit": "tokens/s",
                     "h2d_bytes_per_step": T * d * 2, "d2h_bytes_per_step": T * d * 2},
-            "gpu_launches": args.steps * (14 if args.exchange == "p2p" else 13),
+            "gpu_launches": args.steps * (13 if args.exchange == "p2p" else 12),
             "roofline": {"bound": "tensor", "kernel": "hep_moe_expert_ffn on the received rows (rank 0)",
                          "achieved": ffn_tf, "peak": tf_sus, "unit": "TFLOP/s", "frac": ffn_tf / tf_sus,
                          "min_over_ranks": min_tf, "rows_rank0": R,
@@ -451,7 +451,7 @@ def main():
     def staged_step(i):
         layer.run(x, bufs, stream, events=evs[i])
 
-    # the timed step is one CUDA-graph replay of the whole forward (13 kernels, no host
+    # the timed step is one CUDA-graph replay of the whole forward (11 kernels, no host
     # sync); per-stage times come from an eager pass with events around each stage
     graph = None
     if not args.profile and not args.eager:

@@ -158,6 +158,26 @@ int hep_gate_topk(const float *d_logits, int64_t ld_logits, const float *d_bias,
                   void *stream);
 
 /*
+ * K1 fused: router GEMM logits = x . Wg^T (tcgen05, fp32 accumulators in TMEM) with the
+ * gate in its epilogue — one TMEM lane holds one token's whole logit row, so top-K,
+ * the top-K softmax and the histogram (exactly hep_gate_topk's semantics, bit for bit)
+ * are computed without the logits leaving the SM.
+ *   d_x [T][d_model] bf16, d_wg [e_pad][d_model] bf16 (rows >= E zero), e_pad % 16 == 0
+ *   d_logits [T][e_pad] fp32 or NULL (written when given; required when e_pad > 256 or
+ *   K not in {1,2,4,6,8}, which take the unfused hep_gemm_bf16 + hep_gate_topk path)
+ *   d_chunk_cnt: NULL, or the per-64-token-chunk expert counts hep_moe_assign_precounted
+ *   consumes ([n_src][ceil(tps/64)][E] int32 at hep_moe_assign_chunk_offset of its
+ *   workspace); fused into the epilogue when tokens_per_src % 64 == 0
+ * Replaces: the LoadMatrix producer (core.py:229-268; the reference never models the gate).
+ */
+int hep_router_topk(const void *d_x, const void *d_wg, int64_t T, int64_t d_model, int E, int e_pad,
+                    const float *d_bias, int K, int64_t tokens_per_src, int n_src, float *d_logits,
+                    int32_t *d_topk_idx, float *d_topk_w, int64_t *d_hist, int32_t *d_chunk_cnt, void *stream);
+/* Per-64-token-chunk expert counts of a top-K assignment (the unfused producer of d_chunk_cnt). */
+int hep_gate_chunk_counts(const int32_t *d_topk_idx, int64_t T, int K, int E, int64_t tokens_per_src, int n_src,
+                          int32_t *d_chunk_cnt, void *stream);
+
+/*
  * Dense bf16 GEMM on tcgen05/TMEM/TMA (sm_100a): D[M][N] = A[M][K] . B[N][K]^T,
  * fp32 accumulate, fp32 or bf16 output.  Used for the router logits (K1).
  * Requires K % 64 == 0, N % 16 == 0, N <= 256 or N % 256 == 0.
@@ -185,6 +205,13 @@ int hep_moe_assign(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_t
                    int64_t tokens_per_src, int row_align, int32_t *d_tok_row, int32_t *d_row_tok, int32_t *d_seg,
                    int64_t *d_expert_rows, void *workspace, size_t workspace_bytes, void *stream);
 size_t hep_moe_assign_workspace(hep_sched_t h, int64_t T, int K);
+/* hep_moe_assign with the chunk counts already in the workspace (written by
+ * hep_router_topk's epilogue at byte offset hep_moe_assign_chunk_offset). */
+int hep_moe_assign_precounted(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_topk_idx, int64_t T, int K,
+                              int64_t tokens_per_src, int row_align, int32_t *d_tok_row, int32_t *d_row_tok,
+                              int32_t *d_seg, int64_t *d_expert_rows, void *workspace, size_t workspace_bytes,
+                              void *stream);
+size_t hep_moe_assign_chunk_offset(hep_sched_t h, int64_t T, int K);
 /*
  * K4 for one phase of the pipelined split (hep_sched_pipelined): the assignments of
  * (expert e, source src) whose rank q (sequence order) lies in this phase's window

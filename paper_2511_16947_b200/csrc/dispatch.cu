@@ -164,16 +164,26 @@ __global__ void chunk_count_kernel(const int32_t *topk_idx, int K, int E, int64_
     for (int i = threadIdx.x; i < E; i += blockDim.x) out[i] = cnt[i];
 }
 
+// exclusive prefix over a source's chunks, one warp per (src, expert): 32 chunks per
+// step, all loads of a step in flight together (the serial walk was a chain of
+// dependent L2 round trips)
 __global__ void chunk_scan_kernel(int n_src, int ncs, int E, int32_t *chunk_cnt) {
-    const int id = blockIdx.x * blockDim.x + threadIdx.x;
+    const int id = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
     if (id >= n_src * E) return;
     const int src = id / E, e = id % E;
     int32_t run = 0;
-    for (int c = 0; c < ncs; ++c) {
+    for (int c0 = 0; c0 < ncs; c0 += 32) {
+        const int c = c0 + lane;
         int32_t *p = chunk_cnt + ((int64_t)src * ncs + c) * E + e;
-        const int32_t v = *p;
-        *p = run;
-        run += v;
+        const int32_t v = c < ncs ? *p : 0;
+        int32_t inc = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (c < ncs) *p = run + inc - v;
+        run += __shfl_sync(0xffffffffu, inc, 31);
     }
 }
 
@@ -189,18 +199,22 @@ __global__ void chunk_map_kernel(const int32_t *topk_idx, int K, int E, int G, i
     int32_t *l_lo = l_delta + E * G;  // [E] (windowed: first rank of this phase)
     const int src = blockIdx.x / ncs, c = blockIdx.x % ncs;
     const int lane = threadIdx.x;
-    for (int e = lane; e < E; e += 32) {
+    // stage this source's range lists with the whole block, independent loads (all G
+    // slots of every expert; slots past es_cnt are never read)
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
         ctr[e] = chunk_cnt[(int64_t)blockIdx.x * E + e];
         const int es = e * G + src_base + src;
-        const int n = w.es_cnt[es];
-        l_cnt[e] = n;
+        l_cnt[e] = w.es_cnt[es];
         if (windowed) l_lo[e] = w.es_lo[es];
-        for (int j = 0; j < n; ++j) {
-            l_end[e * G + j] = w.es_end[es * G + j];
-            l_delta[e * G + j] = w.es_delta[es * G + j];
-        }
     }
-    __syncwarp();
+    for (int i = threadIdx.x; i < E * G; i += blockDim.x) {
+        const int e = i / G, j = i - e * G;
+        const int64_t es = (int64_t)e * G + src_base + src;
+        l_end[i] = w.es_end[es * G + j];
+        l_delta[i] = w.es_delta[es * G + j];
+    }
+    __syncthreads();
+    if (threadIdx.x >= 32) return;
     const int64_t t0 = (int64_t)src * tps + (int64_t)c * kChunk;
     int64_t t1 = (int64_t)src * tps + tps;
     if (t0 + kChunk < t1) t1 = t0 + kChunk;
@@ -404,7 +418,8 @@ extern "C" size_t hep_moe_assign_workspace(hep_sched_t h, int64_t T, int K) {
     return assign_ws_bytes(h, T, n_src, tps > 0 ? tps : 1);
 }
 
-static int assign_impl(hep_sched_t h, const hep_sched_out *sched, bool windowed, const int64_t *d_rank_base,
+static int assign_impl(hep_sched_t h, const hep_sched_out *sched, bool windowed, bool precounted,
+                       const int64_t *d_rank_base,
                        const int64_t *d_row_base, const int32_t *d_topk_idx, int64_t T, int K, int64_t tokens_per_src,
                        int row_align, int32_t *d_tok_row, int32_t *d_row_tok, int32_t *d_seg, int64_t *d_expert_rows,
                        void *workspace, size_t workspace_bytes, void *stream) {
@@ -427,15 +442,18 @@ static int assign_impl(hep_sched_t h, const hep_sched_out *sched, bool windowed,
     if (T <= 0) return HEP_OK;
     const int ncs = (int)((tokens_per_src + kChunk - 1) / kChunk);
     const int nblk = n_src * ncs;
-    chunk_count_kernel<<<nblk, 128, E * sizeof(int32_t), s>>>(d_topk_idx, K, E, tokens_per_src, T, ncs, w.chunk_cnt);
-    HEP_CHECK_LAUNCH();
-    chunk_scan_kernel<<<(n_src * E + 255) / 256, 256, 0, s>>>(n_src, ncs, E, w.chunk_cnt);
+    if (!precounted) {
+        chunk_count_kernel<<<nblk, 128, E * sizeof(int32_t), s>>>(d_topk_idx, K, E, tokens_per_src, T, ncs,
+                                                                  w.chunk_cnt);
+        HEP_CHECK_LAUNCH();
+    }
+    chunk_scan_kernel<<<(n_src * E + 7) / 8, 256, 0, s>>>(n_src, ncs, E, w.chunk_cnt);
     HEP_CHECK_LAUNCH();
     const size_t sm = sizeof(int32_t) * (3 * (size_t)E + 2 * (size_t)E * G);
     HEP_REQUIRE(sm <= 200 * 1024, HEP_E_CAPACITY, "chunk_map smem %zu", sm);
     if (sm > 48 * 1024) HEP_CHECK_CUDA(cudaFuncSetAttribute(chunk_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    chunk_map_kernel<<<nblk, 32, sm, s>>>(d_topk_idx, K, E, G, tokens_per_src, T, ncs, w.chunk_cnt, w, d_tok_row,
-                                          d_row_tok, 0, windowed);
+    chunk_map_kernel<<<nblk, 128, sm, s>>>(d_topk_idx, K, E, G, tokens_per_src, T, ncs, w.chunk_cnt, w, d_tok_row,
+                                           d_row_tok, 0, windowed);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
 }
@@ -444,16 +462,46 @@ extern "C" int hep_moe_assign(hep_sched_t h, const hep_sched_out *sched, const i
                               int64_t tokens_per_src, int row_align, int32_t *d_tok_row, int32_t *d_row_tok,
                               int32_t *d_seg, int64_t *d_expert_rows, void *workspace, size_t workspace_bytes,
                               void *stream) {
-    return assign_impl(h, sched, false, nullptr, nullptr, d_topk_idx, T, K, tokens_per_src, row_align, d_tok_row, d_row_tok,
-                       d_seg, d_expert_rows, workspace, workspace_bytes, stream);
+    return assign_impl(h, sched, false, false, nullptr, nullptr, d_topk_idx, T, K, tokens_per_src, row_align, d_tok_row,
+                       d_row_tok, d_seg, d_expert_rows, workspace, workspace_bytes, stream);
+}
+
+extern "C" size_t hep_moe_assign_chunk_offset(hep_sched_t h, int64_t T, int K) {
+    (void)T;
+    (void)K;
+    if (!h) return 0;
+    const int64_t E = h->E, G = h->G;
+    return align256(4 * (size_t)h->nnz + 4) + align256(4 * (size_t)(E * G)) + 2 * align256(4 * (size_t)(E * G * G)) +
+           align256(4 * (size_t)(E + 1));
+}
+
+extern "C" int hep_moe_assign_precounted(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_topk_idx,
+                                         int64_t T, int K, int64_t tokens_per_src, int row_align, int32_t *d_tok_row,
+                                         int32_t *d_row_tok, int32_t *d_seg, int64_t *d_expert_rows, void *workspace,
+                                         size_t workspace_bytes, void *stream) {
+    return assign_impl(h, sched, false, true, nullptr, nullptr, d_topk_idx, T, K, tokens_per_src, row_align, d_tok_row,
+                       d_row_tok, d_seg, d_expert_rows, workspace, workspace_bytes, stream);
+}
+
+extern "C" int hep_gate_chunk_counts(const int32_t *d_topk_idx, int64_t T, int K, int E, int64_t tokens_per_src,
+                                     int n_src, int32_t *d_chunk_cnt, void *stream) {
+    HEP_REQUIRE(d_topk_idx && d_chunk_cnt, HEP_E_CONTRACT, "hep_gate_chunk_counts: null pointer");
+    HEP_REQUIRE(E >= 1 && K >= 1 && tokens_per_src >= 1 && n_src >= 1, HEP_E_DIMENSION, "hep_gate_chunk_counts");
+    if (T <= 0) return HEP_OK;
+    const int ncs = (int)((tokens_per_src + kChunk - 1) / kChunk);
+    chunk_count_kernel<<<n_src * ncs, 128, E * sizeof(int32_t), (cudaStream_t)stream>>>(d_topk_idx, K, E,
+                                                                                       tokens_per_src, T, ncs,
+                                                                                       d_chunk_cnt);
+    HEP_CHECK_LAUNCH();
+    return HEP_OK;
 }
 
 extern "C" int hep_moe_assign_phase(hep_sched_t h, const hep_sched_out *sched, const int64_t *d_rank_base,
                                     const int64_t *d_row_base, const int32_t *d_topk_idx, int64_t T, int K,
                                     int64_t tokens_per_src, int32_t *d_tok_row, int32_t *d_row_tok, int32_t *d_seg,
                                     int64_t *d_expert_rows, void *workspace, size_t workspace_bytes, void *stream) {
-    return assign_impl(h, sched, true, d_rank_base, d_row_base, d_topk_idx, T, K, tokens_per_src, 1, d_tok_row, d_row_tok,
-                       d_seg, d_expert_rows, workspace, workspace_bytes, stream);
+    return assign_impl(h, sched, true, false, d_rank_base, d_row_base, d_topk_idx, T, K, tokens_per_src, 1, d_tok_row,
+                       d_row_tok, d_seg, d_expert_rows, workspace, workspace_bytes, stream);
 }
 
 extern "C" int hep_moe_permute(const void *d_x, const int32_t *d_tok_row, int64_t T, int K, int64_t d_model,
@@ -535,13 +583,14 @@ extern "C" int hep_moe_assign_ep(hep_sched_t h, const hep_sched_out *sched, cons
     const int ncs = (int)((tps + kChunk - 1) / kChunk);
     chunk_count_kernel<<<ncs, 128, E * sizeof(int32_t), s>>>(d_topk_idx, K, E, tps, T, ncs, w.chunk_cnt);
     HEP_CHECK_LAUNCH();
-    chunk_scan_kernel<<<(E + 255) / 256, 256, 0, s>>>(1, ncs, E, w.chunk_cnt);
+    chunk_scan_kernel<<<(E + 7) / 8, 256, 0, s>>>(1, ncs, E, w.chunk_cnt);
     HEP_CHECK_LAUNCH();
     const size_t sm = sizeof(int32_t) * (2 * (size_t)E + 2 * (size_t)E * G);
     HEP_REQUIRE(sm <= 200 * 1024, HEP_E_CAPACITY, "chunk_map smem %zu", sm);
     if (sm > 48 * 1024)
         HEP_CHECK_CUDA(cudaFuncSetAttribute(chunk_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    chunk_map_kernel<<<ncs, 32, sm, s>>>(d_topk_idx, K, E, G, tps, T, ncs, w.chunk_cnt, w, d_tok_row, nullptr, rank, false);
+    chunk_map_kernel<<<ncs, 128, sm, s>>>(d_topk_idx, K, E, G, tps, T, ncs, w.chunk_cnt, w, d_tok_row, nullptr, rank,
+                                          false);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
 }

@@ -36,7 +36,27 @@ constexpr int kEpiSplit = HEP_EPI_SPLIT;  // epilogue warps per TMEM lane quarte
 constexpr int kEpiWarps = 4 * kEpiSplit;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 
-enum Epi { EPI_SWIGLU = 0, EPI_BF16 = 1, EPI_F32 = 2, EPI_SWIGLU_BWD = 3 };
+enum Epi { EPI_SWIGLU = 0, EPI_BF16 = 1, EPI_F32 = 2, EPI_SWIGLU_BWD = 3, EPI_GATE = 4 };
+
+// EPI_GATE (router GEMM with the gate fused into its epilogue): the accumulator tile
+// holds 128 tokens x all E_pad <= 256 logits, so one TMEM lane = one token's whole
+// logit row and the epilogue thread selects its top-K, the softmax weights and
+// counts the load-matrix histogram without the logits ever leaving the SM.
+constexpr int kGateMaxK = 8;
+constexpr int kGateMaxSrc = 16;
+constexpr int kGateMaxE = 256;
+constexpr int kGateSmemBytes = 4 * (kGateMaxSrc * kGateMaxE + 3 * kGateMaxE);
+struct GateParams {
+    const float *bias;   // [E] selection bias or null
+    int K, E;            // top-K, experts (columns >= E are padding)
+    int64_t tps;         // tokens per source GPU (token t belongs to source t / tps)
+    int n_src;
+    int ncs;             // 64-token chunks per source (chunk counts; 0 = none)
+    int32_t *topk_idx;   // [T][K]
+    float *topk_w;       // [T][K]
+    int64_t *hist;       // [n_src][E], zeroed by the caller's launch sequence
+    int32_t *chunk_cnt;  // [n_src][ncs][E] or null
+};
 
 struct Params {
     int grouped;             // 0: dense M rows; 1: m-tile list; 2: per-expert K-ragged (weight gradients)
@@ -65,6 +85,7 @@ struct Params {
     // combine all-to-all stores each expert output row straight into its source GPU's
     // buffer over NVLink (peer pointers), instead of into `out`
     const uint64_t *row_addr;
+    GateParams gate;  // EPI_GATE only
 };
 
 __device__ __forceinline__ uint64_t pick_policy(int k) {
@@ -307,6 +328,106 @@ __device__ __forceinline__ void store_tile(const Params &p, uint32_t t_row, int6
     }
 }
 
+__device__ __forceinline__ uint32_t order_key(float f) {
+    const uint32_t u = __float_as_uint(f + 0.0f);  // -0 -> +0: equal scores must tie
+    return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+
+// EPI_GATE epilogue of one 128-token tile, run by the 4 warps of column slice 0
+// (one TMEM lane quarter each; named barrier 1 is shared by those 128 threads).
+// Selection and weights are exactly hep_gate_topk's (gate.cu): top-K of the order key
+// of (logit + bias) with ties to the lower expert id (strict '>' while scanning experts
+// in ascending order keeps the earlier one), softmax over the K selected logits in pick
+// order.  The running top-KG list is a branch-free insertion network: every slot's new
+// value depends only on the previous column's list, so the KG compare/selects of one
+// column issue back to back.  Histogram counts go to shared memory (flushed once per
+// CTA); the per-64-token chunk counts of the tile's two chunks are written directly.
+template <int KG>
+__device__ __forceinline__ void gate_tile(const Params &p, uint32_t t_row, int64_t row0, int rows, int row_in_tile,
+                                          int32_t *s_hist, int32_t *s_chunk, const float *s_bias, int E_pad) {
+    const GateParams &g = p.gate;
+    const int E = g.E;
+    const int tid = row_in_tile;  // 0..127 over the 4 participating warps
+    if (g.chunk_cnt) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's chunk counts are out
+        for (int i = tid; i < 2 * E; i += 128) s_chunk[i] = 0;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
+    const bool valid = row_in_tile < rows;
+    const int64_t t = row0 + row_in_tile;
+    uint32_t tk[KG];
+    int te[KG];
+    float tv[KG];
+#pragma unroll
+    for (int i = 0; i < KG; ++i) {
+        tk[i] = 0u;
+        te[i] = 0;
+        tv[i] = 0.f;
+    }
+    float *lrow = (valid && p.out) ? reinterpret_cast<float *>(p.out) + t * p.ld_out : nullptr;
+#pragma unroll 1
+    for (int c = 0; c < E_pad; c += 16) {
+        uint32_t v[16];
+        tmem_ld16(t_row + c, v);
+        tmem_ld_wait();
+        if (lrow && c < p.out_cols) {  // logits buffer is [T][e_pad]; BN may be wider
+            float4 *dst = reinterpret_cast<float4 *>(lrow + c);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+                dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
+                                     __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const int e = c + i;
+            const float l = __uint_as_float(v[i]);
+            // padding columns get key 0, which never enters (strict '>' against >= 0)
+            const uint32_t key = e < E ? order_key(l + s_bias[e]) : 0u;
+#pragma unroll
+            for (int j = KG - 1; j >= 0; --j) {
+                const bool up = j > 0 && key > tk[j > 0 ? j - 1 : 0];  // slot j takes slot j-1's entry
+                const bool here = key > tk[j];                          // ... or the new one
+                tk[j] = up ? tk[j > 0 ? j - 1 : 0] : (here ? key : tk[j]);
+                te[j] = up ? te[j > 0 ? j - 1 : 0] : (here ? e : te[j]);
+                tv[j] = up ? tv[j > 0 ? j - 1 : 0] : (here ? l : tv[j]);
+            }
+        }
+    }
+    if (valid) {
+        float mx = tv[0];
+#pragma unroll
+        for (int k = 1; k < KG; ++k) mx = fmaxf(mx, tv[k]);
+        float ex[KG], den = 0.f;
+#pragma unroll
+        for (int k = 0; k < KG; ++k) {
+            ex[k] = expf(tv[k] - mx);
+            den += ex[k];
+        }
+        const int64_t s64 = t / g.tps;
+        const int src = (int)(s64 < g.n_src - 1 ? s64 : g.n_src - 1);
+#pragma unroll
+        for (int k = 0; k < KG; ++k) {
+            g.topk_idx[t * KG + k] = te[k];
+            g.topk_w[t * KG + k] = ex[k] / den;
+            atomicAdd(&s_hist[src * E + te[k]], 1);
+            if (g.chunk_cnt) atomicAdd(&s_chunk[(row_in_tile >> 6) * E + te[k]], 1);
+        }
+    }
+    if (g.chunk_cnt) {
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        // tile = chunks of 64 tokens (the launch guarantees tps % 64 == 0 and 128-row tiles)
+        for (int i = tid; i < 2 * E; i += 128) {
+            const int half = i / E, e = i - half * E;
+            const int64_t t0 = row0 + 64 * half;
+            if (64 * half < rows) {
+                const int64_t src = t0 / g.tps;
+                const int64_t c = (t0 - src * g.tps) >> 6;
+                g.chunk_cnt[((int64_t)src * g.ncs + c) * E + e] = s_chunk[i];
+            }
+        }
+    }
+}
+
 // A_MN / B_MN: operand stored MN-major in global memory (the contraction index
 // is the row index, e.g. activations [rows][d] contracted over rows for weight
 // gradients, or weights [K][N] used untransposed).  Such an operand is staged as
@@ -329,6 +450,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     int32_t *s_off = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(tmem_slot) + 16);
     if (p.grouped == 1)
         for (int i = threadIdx.x; i <= p.n_exp; i += blockDim.x) s_off[i] = p.exp_mt_off[i];
+    int32_t *s_hist = s_off + kMaxExpSmem + 4;             // EPI_GATE: [n_src][E] counts
+    int32_t *s_chunk = s_hist + kGateMaxSrc * kGateMaxE;  // EPI_GATE: [2][E] tile chunk counts
+    float *s_bias = reinterpret_cast<float *>(s_chunk + 2 * kGateMaxE);  // EPI_GATE: [E_pad] bias
+    if constexpr (EPI == EPI_GATE) {
+        for (int i = threadIdx.x; i < p.gate.n_src * p.gate.E; i += blockDim.x) s_hist[i] = 0;
+        for (int i = threadIdx.x; i < BN; i += blockDim.x)
+            s_bias[i] = (p.gate.bias && i < p.gate.E) ? p.gate.bias[i] : 0.f;
+    }
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp == 0 && lane == 0) {
@@ -438,9 +567,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-            const bool valid = row_in_tile < tl.rows;
-            const int64_t grow = (int64_t)tl.row0 + row_in_tile;
-            store_tile<BN, EPI>(p, t_row, grow, valid, tl.n_blk, pol_out, tl.expert, tl.kb == 0, half);
+            if constexpr (EPI == EPI_GATE) {
+                if (half == 0) {
+                    switch (p.gate.K) {  // the insertion network is unrolled per K
+                        case 1: gate_tile<1>(p, t_row, tl.row0, tl.rows, row_in_tile, s_hist, s_chunk, s_bias, BN); break;
+                        case 2: gate_tile<2>(p, t_row, tl.row0, tl.rows, row_in_tile, s_hist, s_chunk, s_bias, BN); break;
+                        case 4: gate_tile<4>(p, t_row, tl.row0, tl.rows, row_in_tile, s_hist, s_chunk, s_bias, BN); break;
+                        case 6: gate_tile<6>(p, t_row, tl.row0, tl.rows, row_in_tile, s_hist, s_chunk, s_bias, BN); break;
+                        default: gate_tile<8>(p, t_row, tl.row0, tl.rows, row_in_tile, s_hist, s_chunk, s_bias, BN); break;
+                    }
+                }
+            } else {
+                const bool valid = row_in_tile < tl.rows;
+                const int64_t grow = (int64_t)tl.row0 + row_in_tile;
+                store_tile<BN, EPI>(p, t_row, grow, valid, tl.n_blk, pol_out, tl.expert, tl.kb == 0, half);
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_relaxed(&tempty[acc]);
@@ -452,6 +593,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem_base, S::TMEM_COLS);
+    }
+    if constexpr (EPI == EPI_GATE) {  // integer sums: order-free, deterministic
+        for (int i = threadIdx.x; i < p.gate.n_src * p.gate.E; i += blockDim.x)
+            if (s_hist[i]) atomicAdd(reinterpret_cast<unsigned long long *>(p.gate.hist) + i, (unsigned long long)s_hist[i]);
     }
 }
 
@@ -884,6 +1029,79 @@ extern "C" int hep_gemm_bf16(const void *d_A, const void *d_B, void *d_D, int64_
     HEP_REQUIRE(N % 256 == 0, HEP_E_DIMENSION, "bf16 GEMM needs N %% 256 == 0");
     p.n_tiles = (int)(N / 256);
     return launch<256, 4, EPI_BF16>(d_A, M, K, d_B, N, p, mt * p.n_tiles, s);
+}
+
+template <int BN, int STAGES>
+static int launch_gate(const void *x, const void *wg, int64_t T, int64_t d_model, int e_pad, const Params &p,
+                       cudaStream_t s) {
+    using S = Smem<BN, STAGES>;
+    CUtensorMap ta, tb;
+    int rc = make_tmap(&ta, x, (uint64_t)T, (uint64_t)d_model, BM);
+    if (rc) return rc;
+    rc = make_tmap(&tb, wg, (uint64_t)e_pad, (uint64_t)d_model, BN);  // rows past e_pad: TMA zero fill
+    if (rc) return rc;
+    auto kern = gemm_kernel<BN, STAGES, EPI_GATE>;
+    const int bytes = (int)S::BYTES + kGateSmemBytes;
+    HEP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    const int64_t tiles = (T + BM - 1) / BM;
+    const int grid = (int)(tiles < sm_count() ? tiles : sm_count());
+    kern<<<grid, kThreads, bytes, s>>>(ta, tb, p);
+    HEP_CHECK_LAUNCH();
+    return HEP_OK;
+}
+
+extern "C" int hep_gate_chunk_counts(const int32_t *d_topk_idx, int64_t T, int K, int E, int64_t tokens_per_src,
+                                     int n_src, int32_t *d_chunk_cnt, void *stream);
+
+extern "C" int hep_router_topk(const void *d_x, const void *d_wg, int64_t T, int64_t d_model, int E, int e_pad,
+                               const float *d_bias, int K, int64_t tokens_per_src, int n_src, float *d_logits,
+                               int32_t *d_topk_idx, float *d_topk_w, int64_t *d_hist, int32_t *d_chunk_cnt,
+                               void *stream) {
+    HEP_REQUIRE(d_x && d_wg && d_topk_idx && d_topk_w && d_hist, HEP_E_CONTRACT, "hep_router_topk: null pointer");
+    HEP_REQUIRE(E >= 1 && K >= 1 && K <= E && e_pad >= E && e_pad % 16 == 0 && d_model % BK == 0, HEP_E_DIMENSION,
+                "hep_router_topk: E=%d e_pad=%d K=%d d=%lld", E, e_pad, K, (long long)d_model);
+    HEP_REQUIRE(tokens_per_src >= 1 && n_src >= 1 && tokens_per_src * n_src >= T, HEP_E_DIMENSION,
+                "hep_router_topk: tokens_per_src * n_src < T");
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool fused = e_pad <= kGateMaxE && (K == 1 || K == 2 || K == 4 || K == 6 || K == 8) && n_src <= kGateMaxSrc;
+    if (!fused) {  // unfused: logits through HBM, then the gate kernel (both still on the device)
+        HEP_REQUIRE(d_logits, HEP_E_CONTRACT, "hep_router_topk: E_pad > 256 / K not in {1,2,4,6,8} needs d_logits");
+        int rc = hep_gemm_bf16(d_x, d_wg, d_logits, T, e_pad, d_model, HEP_OUT_F32, stream);
+        if (rc) return rc;
+        rc = hep_gate_topk(d_logits, e_pad, d_bias, T, E, K, tokens_per_src, n_src, d_topk_idx, d_topk_w, d_hist, stream);
+        if (rc || !d_chunk_cnt) return rc;
+        return hep_gate_chunk_counts(d_topk_idx, T, K, E, tokens_per_src, n_src, d_chunk_cnt, stream);
+    }
+    HEP_CHECK_CUDA(cudaMemsetAsync(d_hist, 0, sizeof(int64_t) * (size_t)n_src * E, s));
+    if (T <= 0) return HEP_OK;
+    // chunk counts come out of the epilogue when every 64-token chunk lies inside one tile
+    const bool chunks_fused = d_chunk_cnt && tokens_per_src % 64 == 0 && tokens_per_src * n_src == T;
+    Params p{};
+    p.grouped = 0;
+    p.M = T;
+    p.kblocks = (int)(d_model / BK);
+    p.n_tiles = 1;
+    p.out = d_logits;
+    p.ld_out = e_pad;
+    p.out_cols = e_pad;
+    p.gate.bias = d_bias;
+    p.gate.K = K;
+    p.gate.E = E;
+    p.gate.tps = tokens_per_src;
+    p.gate.n_src = n_src;
+    p.gate.ncs = (int)((tokens_per_src + 63) / 64);
+    p.gate.topk_idx = d_topk_idx;
+    p.gate.topk_w = d_topk_w;
+    p.gate.hist = d_hist;
+    p.gate.chunk_cnt = chunks_fused ? d_chunk_cnt : nullptr;
+    int rc;
+    if (e_pad <= 16) rc = launch_gate<16, 8>(d_x, d_wg, T, d_model, e_pad, p, s);
+    else if (e_pad <= 32) rc = launch_gate<32, 8>(d_x, d_wg, T, d_model, e_pad, p, s);
+    else if (e_pad <= 64) rc = launch_gate<64, 6>(d_x, d_wg, T, d_model, e_pad, p, s);
+    else if (e_pad <= 128) rc = launch_gate<128, 5>(d_x, d_wg, T, d_model, e_pad, p, s);
+    else rc = launch_gate<256, 4>(d_x, d_wg, T, d_model, e_pad, p, s);
+    if (rc || !d_chunk_cnt || chunks_fused) return rc;
+    return hep_gate_chunk_counts(d_topk_idx, T, K, E, tokens_per_src, n_src, d_chunk_cnt, stream);
 }
 
 extern "C" size_t hep_moe_ffn_workspace(int n_seg, int64_t R, int n_experts) {

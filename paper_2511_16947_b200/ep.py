@@ -318,11 +318,9 @@ class EPMoELayer:
             T = x.shape[0]
             b = rk.p2p_buffers(self, T)
             bs.append(b)
-            ck(L.hep_gemm_bf16(x.data_ptr(), self.wg.data_ptr(), b["logits"].data_ptr(), T, self.e_pad, d, 0, s),
-               "hep_gemm_bf16(router)")
-            ck(L.hep_gate_topk(b["logits"].data_ptr(), self.e_pad, _lib.ptr(self.gate_bias), T, E, K, T, 1,
-                               b["topk_idx"].data_ptr(), b["topk_w"].data_ptr(), b["hist"].data_ptr(), s),
-               "hep_gate_topk")
+            ck(L.hep_router_topk(x.data_ptr(), self.wg.data_ptr(), T, d, E, self.e_pad, _lib.ptr(self.gate_bias), K,
+                                 T, 1, b["logits"].data_ptr(), b["topk_idx"].data_ptr(), b["topk_w"].data_ptr(),
+                                 b["hist"].data_ptr(), None, s), "hep_router_topk")
         hists = self.comm.all_gather([b["hist"] for b in bs])
         for rk, x, b, h, (p_recv, p_back) in zip(self.ranks, xs, bs, hists, tabs):
             T = x.shape[0]
@@ -369,11 +367,9 @@ class EPMoELayer:
             T = x.shape[0]
             b = rk.buffers(self, T)
             bs.append(b)
-            ck(L.hep_gemm_bf16(x.data_ptr(), self.wg.data_ptr(), b["logits"].data_ptr(), T, self.e_pad, d, 0, s),
-               "hep_gemm_bf16(router)")
-            ck(L.hep_gate_topk(b["logits"].data_ptr(), self.e_pad, _lib.ptr(self.gate_bias), T, E, K, T, 1,
-                               b["topk_idx"].data_ptr(), b["topk_w"].data_ptr(), b["hist"].data_ptr(), s),
-               "hep_gate_topk")
+            ck(L.hep_router_topk(x.data_ptr(), self.wg.data_ptr(), T, d, E, self.e_pad, _lib.ptr(self.gate_bias), K,
+                                 T, 1, b["logits"].data_ptr(), b["topk_idx"].data_ptr(), b["topk_w"].data_ptr(),
+                                 b["hist"].data_ptr(), None, s), "hep_router_topk")
         hists = self.comm.all_gather([b["hist"] for b in bs])  # [G][E] on every rank
         for rk, x, b, h in zip(self.ranks, xs, bs, hists):
             T = x.shape[0]

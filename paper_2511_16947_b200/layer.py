@@ -2,10 +2,10 @@
 
 Per micro-batch, all on one CUDA stream, no host synchronisation:
 
-  K1  router GEMM   logits[T][E] = x . Wg^T            hep_gemm_bf16 (tcgen05, fp32 out)
-  K1  gate epilogue top-K + softmax(top-K) + hist[G][E] hep_gate_topk
+  K1  router GEMM   logits[T][E] = x . Wg^T, with the    hep_router_topk (tcgen05; gate in the
+      + gate        top-K + softmax(top-K) + hist[G][E]  epilogue, one TMEM lane per token)
   K3  scheduler     m, lex-min plan, integerize, ranges hep_sched_solve (1 CTA)
-  K4  assignment    (token, k) -> receive row           hep_moe_assign
+  K4  assignment    (token, k) -> receive row           hep_moe_assign_precounted
   K5  permute       rows[row] = x[token]                hep_moe_permute
   K6  expert FFN    SwiGLU grouped GEMM x2              hep_moe_expert_ffn (tcgen05)
   K7  combine       out[t] = sum_k w * y[row]           hep_moe_combine
@@ -93,6 +93,7 @@ class MoEBuffers:
         self.expert_rows2 = torch.empty(E + 1, dtype=torch.int64, device=device) if pipelined else None
         ws = L.hep_moe_assign_workspace(sched.handle, T, K)
         self.assign_ws = torch.empty(max(int(ws), 256), dtype=torch.uint8, device=device)
+        self.chunk_off = int(L.hep_moe_assign_chunk_offset(sched.handle, T, K))  # router-written chunk counts
         self.rows = alloc(max(R, 1), d_model, **bf)
         self.h = alloc(max(R, 1), ffn, **bf)
         self.y = alloc(max(R, 1), d_model, **bf)
@@ -121,7 +122,7 @@ class MoELayer(torch.nn.Module):
             if train:
                 raise ValueError("the pipelined split is a forward (serving) schedule; train with pipeline_ratio=None")
             self.static_share = Fraction(1) - Fraction(pipeline_ratio)
-        self.LAUNCHES_PER_FORWARD = 13 if self.static_share is None else 19
+        self.LAUNCHES_PER_FORWARD = 11 if self.static_share is None else 18
         torch_ = _lib.require_cuda()
         self.device = torch_.device("cuda", torch_.cuda.current_device()) if device is None else torch_.device(device)
         self.placement = placement
@@ -199,13 +200,15 @@ class MoELayer(torch.nn.Module):
             if pair is not None:
                 pair[i].record(st)
 
+        # K1: router GEMM with the gate (top-K, weights, histogram, per-chunk counts) fused
+        # into its epilogue; the logits are also written (parity tests, inspection)
         mark("router", 0)
-        ck(L.hep_gemm_bf16(x.data_ptr(), self.wg.data_ptr(), b.logits.data_ptr(), T, self.e_pad, self.d, 0, s),
-           "hep_gemm_bf16(router)")
+        chunk = None if self.static_share is not None else b.assign_ws.data_ptr() + b.chunk_off
+        ck(L.hep_router_topk(x.data_ptr(), self.wg.data_ptr(), T, self.d, E, self.e_pad, _lib.ptr(self.gate_bias), K,
+                             tps, G, b.logits.data_ptr(), b.topk_idx.data_ptr(), b.topk_w.data_ptr(),
+                             b.hist.data_ptr(), chunk, s), "hep_router_topk")
         mark("router", 1)
-        mark("gate", 0)
-        ck(L.hep_gate_topk(b.logits.data_ptr(), self.e_pad, _lib.ptr(self.gate_bias), T, E, K, tps, G,
-                           b.topk_idx.data_ptr(), b.topk_w.data_ptr(), b.hist.data_ptr(), s), "hep_gate_topk")
+        mark("gate", 0)  # fused into the router kernel
         mark("gate", 1)
         # hist is [G][E] (source-major, the all-gather layout): stride_e = 1, stride_g = E
         mark("sched", 0)
@@ -217,10 +220,10 @@ class MoELayer(torch.nn.Module):
         mark("sched", 1)
         mark("assign", 0)
         if self.static_share is None:
-            ck(L.hep_moe_assign(self.sched.handle, ctypes.byref(self.sched.out), b.topk_idx.data_ptr(), T, K, tps,
-                                b.row_align, b.tok_row.data_ptr(), b.row_tok.data_ptr(), b.seg.data_ptr(),
-                                b.expert_rows.data_ptr(), b.assign_ws.data_ptr(), b.assign_ws.numel(), s),
-               "hep_moe_assign")
+            ck(L.hep_moe_assign_precounted(self.sched.handle, ctypes.byref(self.sched.out), b.topk_idx.data_ptr(), T,
+                                           K, tps, b.row_align, b.tok_row.data_ptr(), b.row_tok.data_ptr(),
+                                           b.seg.data_ptr(), b.expert_rows.data_ptr(), b.assign_ws.data_ptr(),
+                                           b.assign_ws.numel(), s), "hep_moe_assign_precounted")
         else:
             nnz = self.sched.nnz
             ck(L.hep_moe_assign_phase(self.sched.handle, ctypes.byref(self.sched.former.out), None, None,
@@ -256,7 +259,7 @@ class MoELayer(torch.nn.Module):
 
     def capture(self, x: torch.Tensor) -> "torch.cuda.CUDAGraph":
         """Record one forward on ``x`` (fixed buffers, no host sync anywhere in the
-        chain) as a CUDA graph; ``graph.replay()`` re-runs all 13 kernels with one
+        chain) as a CUDA graph; ``graph.replay()`` re-runs all 11 kernels with one
         launch.  ``x`` must stay the input tensor (refill it in place)."""
         b = self.buffers(x.shape[0])
         side = torch.cuda.Stream(device=self.device)
@@ -270,10 +273,11 @@ class MoELayer(torch.nn.Module):
             self.run(x, b, side)
         return g
 
-    # kernels launched per forward: router GEMM, gate top-K, scheduler, assign x4,
+    # kernels launched per forward: router GEMM + gate epilogue, scheduler, assign x3
+    # (plan prep, chunk scan, chunk map; the chunk counts come from the router epilogue),
     # permute, FFN (tile count + tile list + 2 GEMMs), combine (pipelined split: + split
-    # kernel, second scheduler launch, second assignment x4)
-    LAUNCHES_PER_FORWARD = 13
+    # kernel, second scheduler launch, per-phase assignment x4 each)
+    LAUNCHES_PER_FORWARD = 11
 
     def check_status(self):
         self.sched.check_status("MoELayer")

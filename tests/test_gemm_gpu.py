@@ -149,3 +149,59 @@ def test_grouped_ffn_skewed_sizes_pair_and_single(L, E, d, F, monkeypatch):
             assert rel <= 1e-2, (pair, e, n, rel)
     assert torch.equal(outs["0"][0], outs["1"][0])
     assert torch.equal(outs["0"][1], outs["1"][1])
+
+
+@pytest.mark.parametrize("T,d,E,K,G,bias", [
+    (4096, 512, 8, 2, 4, True), (2000, 256, 8, 1, 2, False), (4096, 1024, 40, 6, 8, True),
+    (8192, 512, 128, 8, 8, True), (3000, 512, 128, 8, 3, False), (4096, 768, 200, 8, 8, True),
+    (2048, 512, 256, 8, 8, True), (1024, 256, 512, 8, 4, True), (1024, 256, 64, 10, 4, True),
+])
+def test_router_topk_fused_equals_unfused(L, T, d, E, K, G, bias):
+    """hep_router_topk (gate in the router GEMM's epilogue) against the unfused chain
+    hep_gemm_bf16 -> hep_gate_topk -> hep_gate_chunk_counts: logits, top-K indices,
+    weights, histogram and per-64-token chunk counts bit for bit (E > 256 and K not in
+    {1, 2, 4, 6, 8} take the unfused path inside the same entry point)."""
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(T + E + K)
+    e_pad = max(16, (E + 15) // 16 * 16)
+    e64 = (E + 63) // 64 * 64
+    x = torch.randn(T, d, generator=g, device=dev).to(torch.bfloat16)
+    wg = torch.zeros(max(e64, e_pad), d, dtype=torch.bfloat16, device=dev)
+    wg[:E] = (torch.randn(E, d, generator=g, device=dev) / d ** 0.5).to(torch.bfloat16)
+    # duplicate two experts' rows so exact ties occur (ties -> lower expert id)
+    wg[E - 1] = wg[0]
+    b = (torch.randn(E, generator=g, device=dev) * 0.5).float() if bias else None
+    if b is not None:
+        b[E - 1] = b[0]
+    tps = (T + G - 1) // G
+    ncs = (tps + 63) // 64
+    lib = L.lib()
+    s = L.stream_handle()
+
+    def bufs():
+        return (torch.full((T, e_pad), float("nan"), device=dev), torch.full((T, K), -1, dtype=torch.int32, device=dev),
+                torch.full((T, K), float("nan"), device=dev), torch.zeros(G, E, dtype=torch.int64, device=dev),
+                torch.full((G * ncs * E,), -7, dtype=torch.int32, device=dev))
+
+    lg0, i0, w0, h0, c0 = bufs()
+    L.check(lib.hep_gemm_bf16(x.data_ptr(), wg.data_ptr(), lg0.data_ptr(), T, e_pad, d, 0, s), "gemm")
+    L.check(lib.hep_gate_topk(lg0.data_ptr(), e_pad, L.ptr(b), T, E, K, tps, G, i0.data_ptr(), w0.data_ptr(),
+                              h0.data_ptr(), s), "gate")
+    L.check(lib.hep_gate_chunk_counts(i0.data_ptr(), T, K, E, tps, G, c0.data_ptr(), s), "chunks")
+    lg1, i1, w1, h1, c1 = bufs()
+    L.check(lib.hep_router_topk(x.data_ptr(), wg.data_ptr(), T, d, E, e_pad, L.ptr(b), K, tps, G, lg1.data_ptr(),
+                                i1.data_ptr(), w1.data_ptr(), h1.data_ptr(), c1.data_ptr(), s), "router_topk")
+    torch.cuda.synchronize()
+    assert torch.equal(lg0, lg1)
+    assert torch.equal(i0, i1)
+    assert torch.equal(w0, w1)
+    assert torch.equal(h0, h1)
+    assert int(h1.sum()) == T * K
+    assert torch.equal(c0, c1)
+    # and without the logits buffer (fused path only)
+    if E <= 256 and K in (1, 2, 4, 6, 8):
+        _, i2, w2, h2, c2 = bufs()
+        L.check(lib.hep_router_topk(x.data_ptr(), wg.data_ptr(), T, d, E, e_pad, L.ptr(b), K, tps, G, None,
+                                    i2.data_ptr(), w2.data_ptr(), h2.data_ptr(), c2.data_ptr(), s), "router_topk")
+        torch.cuda.synchronize()
+        assert torch.equal(i0, i2) and torch.equal(w0, w2) and torch.equal(h0, h2) and torch.equal(c0, c2)
