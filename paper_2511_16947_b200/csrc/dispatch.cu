@@ -22,6 +22,7 @@
 namespace hep {
 
 constexpr int kChunk = 64;
+constexpr int kPrepSmemMax = 160 * 1024;  // plan_prep: routing table staged in shared memory up to this size
 
 struct AssignWs {
     int32_t *row_base;  // [nnz] first row of segment (dst, e) per nnz entry
@@ -75,13 +76,17 @@ __global__ void plan_prep_kernel(int G, int E, int nnz, const int32_t *grp_off, 
                                  const int32_t *sorted, const int32_t *nnz_exp, const int64_t *xi,
                                  const int64_t *ranges, const int64_t *n_ranges_p, int64_t *expert_rows,
                                  int32_t *seg, AssignWs w, int32_t *status, int row_align,
-                                 const int64_t *rank_base, const int64_t *row_base_p) {
+                                 const int64_t *rank_base, const int64_t *row_base_p, int64_t stage_cap) {
     __shared__ int64_t scan[64];
     const int tid = threadIdx.x, nt = blockDim.x;
     const int64_t n_ranges = *n_ranges_p;
     const int64_t row_off = row_base_p ? *row_base_p : 0;  // phase block start (pipelined split)
+    // dynamic smem: [E*G] per-(expert, src) range counters, then the staged routing table
+    extern __shared__ int4 s_dyn[];
+    int32_t *s_cnt = reinterpret_cast<int32_t *>(s_dyn);
+    int4 *s_rng = s_dyn + (E * G + 3) / 4;
     for (int i = tid; i < E * G; i += nt) {
-        w.es_cnt[i] = 0;
+        s_cnt[i] = 0;
         w.es_lo[i] = rank_base ? (int32_t)rank_base[i] : 0;
     }
     for (int i = tid; i <= E; i += nt) w.first[i] = -1;
@@ -116,36 +121,52 @@ __global__ void plan_prep_kernel(int G, int E, int nnz, const int32_t *grp_off, 
         expert_rows[E] = total;
         if (total >= (int64_t)1 << 31) atomicCAS(status, 0, HEP_E_CAPACITY);
     }
+    // the routing table as int4 (expert, src, dst, count) in shared memory when it fits
+    // (the per-expert passes below re-read each expert's ranges O(ranges^2) times)
+    const bool staged = n_ranges <= stage_cap;
+    if (staged)
+        for (int64_t r = tid; r < n_ranges; r += nt)
+            s_rng[r] = make_int4((int)ranges[4 * r], (int)ranges[4 * r + 1], (int)ranges[4 * r + 2],
+                                 (int)ranges[4 * r + 3]);
     __syncthreads();
+    auto rng = [&](int64_t j) -> int4 {
+        return staged ? s_rng[j]
+                      : make_int4((int)ranges[4 * j], (int)ranges[4 * j + 1], (int)ranges[4 * j + 2],
+                                  (int)ranges[4 * j + 3]);
+    };
     for (int64_t r = tid; r < n_ranges; r += nt) {
-        const int e = (int)ranges[4 * r];
-        if (r == 0 || ranges[4 * (r - 1)] != e) w.first[e] = (int)r;
+        const int e = rng(r).x;
+        if (r == 0 || rng(r - 1).x != e) w.first[e] = (int)r;
     }
     __syncthreads();
     for (int e = tid; e < E; e += nt) {
         const int r0 = w.first[e];
         if (r0 < 0) continue;
         int r1 = r0;
-        while (r1 < n_ranges && ranges[4 * r1] == e) ++r1;
+        while (r1 < n_ranges && rng(r1).x == e) ++r1;
         for (int j = r0; j < r1; ++j) {
-            const int src = (int)ranges[4 * j + 1], dst = (int)ranges[4 * j + 2];
-            const int64_t cnt = ranges[4 * j + 3];
+            const int4 rj = rng(j);
+            const int src = rj.y, dst = rj.z;
+            const int64_t cnt = rj.w;
             int nz = -1;
             for (int i = grp_off[e]; i < grp_off[e + 1]; ++i)
                 if (grp_gpu[i] == dst) nz = i;
             if (nz < 0) { atomicCAS(status, 0, HEP_E_CONTRACT); continue; }
-            int64_t row = w.row_base[nz], rank = w.es_lo[e * G + src];
+            int64_t row = w.row_base[nz], rank = rank_base ? rank_base[e * G + src] : 0;
             for (int k = r0; k < r1; ++k) {
-                const int ks = (int)ranges[4 * k + 1], kd = (int)ranges[4 * k + 2];
-                if (kd == dst && ks < src) row += ranges[4 * k + 3];
-                if (k < j && ks == src) rank += ranges[4 * k + 3];
+                const int4 rk = rng(k);
+                const int ks = rk.y, kd = rk.z;
+                if (kd == dst && ks < src) row += rk.w;
+                if (k < j && ks == src) rank += rk.w;
             }
             const int es = e * G + src;
-            const int slot = w.es_cnt[es]++;
+            const int slot = s_cnt[es]++;  // (e, *) belongs to this thread alone
             w.es_end[es * G + slot] = (int32_t)(rank + cnt);
             w.es_delta[es * G + slot] = (int32_t)(row - rank);
         }
     }
+    __syncthreads();
+    for (int i = tid; i < E * G; i += nt) w.es_cnt[i] = s_cnt[i];
 }
 
 __global__ void chunk_count_kernel(const int32_t *topk_idx, int K, int E, int64_t tps, int64_t T, int ncs,
@@ -197,6 +218,7 @@ __global__ void chunk_map_kernel(const int32_t *topk_idx, int K, int E, int G, i
     int32_t *l_end = l_cnt + E;       // [E*G]
     int32_t *l_delta = l_end + E * G; // [E*G]
     int32_t *l_lo = l_delta + E * G;  // [E] (windowed: first rank of this phase)
+    int32_t *l_idx = l_lo + E;        // [kChunk * K] this chunk's top-K picks
     const int src = blockIdx.x / ncs, c = blockIdx.x % ncs;
     const int lane = threadIdx.x;
     // stage this source's range lists with the whole block, independent loads (all G
@@ -213,16 +235,25 @@ __global__ void chunk_map_kernel(const int32_t *topk_idx, int K, int E, int G, i
         l_end[i] = w.es_end[es * G + j];
         l_delta[i] = w.es_delta[es * G + j];
     }
-    __syncthreads();
-    if (threadIdx.x >= 32) return;
     const int64_t t0 = (int64_t)src * tps + (int64_t)c * kChunk;
     int64_t t1 = (int64_t)src * tps + tps;
     if (t0 + kChunk < t1) t1 = t0 + kChunk;
     if (T < t1) t1 = T;
-    for (int64_t t = t0; t < t1; ++t) {
-        if (lane < K) {
-            const int e = topk_idx[t * K + lane];
-            const int q = ctr[e]++;
+    // the chunk's picks, so the sequential walk below reads shared memory only
+    for (int64_t i = threadIdx.x; i < (t1 - t0) * K; i += blockDim.x) l_idx[i] = topk_idx[t0 * K + i];
+    __syncthreads();
+    if (threadIdx.x >= 32) return;
+    // 32 assignments (token-major, k minor = sequence order: a token's picks are distinct
+    // experts) per step: lanes with the same expert find each other with match.any, their
+    // ranks are the running counter plus the number of earlier peers; the lowest peer
+    // advances the counter
+    const int n_asg = (int)(t1 - t0) * K;
+    for (int a0 = 0; a0 < n_asg; a0 += 32) {
+        const int a = a0 + lane;
+        const int e = a < n_asg ? l_idx[a] : -1 - lane;
+        const uint32_t peers = __match_any_sync(0xffffffffu, e);
+        if (e >= 0) {
+            const int q = ctr[e] + __popc(peers & ((1u << lane) - 1u));
             int j = 0;
             const int n = l_cnt[e];
             // pipelined split: this phase owns ranks [lo, end of its last range) of (e, src)
@@ -230,10 +261,13 @@ __global__ void chunk_map_kernel(const int32_t *topk_idx, int K, int E, int G, i
             if (mine) {
                 while (j + 1 < n && q >= l_end[e * G + j]) ++j;
                 const int row = q + l_delta[e * G + j];
-                tok_row[t * K + lane] = row;
+                const int64_t t = t0 + a / K;
+                tok_row[t * K + (a - (a / K) * K)] = row;
                 if (row_tok) row_tok[row] = (int32_t)t;
             }
         }
+        __syncwarp();
+        if (e >= 0 && (__ffs(peers) - 1) == lane) ctr[e] += __popc(peers);
         __syncwarp();
     }
 }
@@ -435,9 +469,16 @@ static int assign_impl(hep_sched_t h, const hep_sched_out *sched, bool windowed,
     cudaStream_t s = (cudaStream_t)stream;
     AssignWs w = carve_ws(h, workspace, n_src, tokens_per_src);
     const int E = h->E, G = h->G;
-    plan_prep_kernel<<<1, 512, 0, s>>>(G, E, h->nnz, h->d_grp_off, h->d_grp_gpu, h->d_sorted, h->d_nnz_exp,
-                                       sched->d_xi, sched->d_ranges, sched->d_n_ranges, d_expert_rows, d_seg, w,
-                                       sched->d_status, row_align, d_rank_base, d_row_base);
+    const size_t cnt_sm = 16 * (size_t)((E * G + 3) / 4);
+    HEP_REQUIRE(cnt_sm <= kPrepSmemMax, HEP_E_CAPACITY, "plan_prep: E*G too large");
+    int64_t stage_cap = h->max_ranges;
+    if (cnt_sm + 16 * stage_cap > kPrepSmemMax) stage_cap = 0;  // too large to stage: read the table from global
+    const size_t prep_sm = cnt_sm + 16 * (size_t)stage_cap;
+    if (prep_sm + 512 > 48 * 1024)  // + the kernel's static scan buffer
+        HEP_CHECK_CUDA(cudaFuncSetAttribute(plan_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPrepSmemMax));
+    plan_prep_kernel<<<1, 512, prep_sm, s>>>(G, E, h->nnz, h->d_grp_off, h->d_grp_gpu, h->d_sorted, h->d_nnz_exp,
+                                             sched->d_xi, sched->d_ranges, sched->d_n_ranges, d_expert_rows, d_seg, w,
+                                             sched->d_status, row_align, d_rank_base, d_row_base, stage_cap);
     HEP_CHECK_LAUNCH();
     if (T <= 0) return HEP_OK;
     const int ncs = (int)((tokens_per_src + kChunk - 1) / kChunk);
@@ -449,10 +490,10 @@ static int assign_impl(hep_sched_t h, const hep_sched_out *sched, bool windowed,
     }
     chunk_scan_kernel<<<(n_src * E + 7) / 8, 256, 0, s>>>(n_src, ncs, E, w.chunk_cnt);
     HEP_CHECK_LAUNCH();
-    const size_t sm = sizeof(int32_t) * (3 * (size_t)E + 2 * (size_t)E * G);
+    const size_t sm = sizeof(int32_t) * (3 * (size_t)E + 2 * (size_t)E * G + (size_t)kChunk * K);
     HEP_REQUIRE(sm <= 200 * 1024, HEP_E_CAPACITY, "chunk_map smem %zu", sm);
     if (sm > 48 * 1024) HEP_CHECK_CUDA(cudaFuncSetAttribute(chunk_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    chunk_map_kernel<<<nblk, 128, sm, s>>>(d_topk_idx, K, E, G, tokens_per_src, T, ncs, w.chunk_cnt, w, d_tok_row,
+    chunk_map_kernel<<<nblk, 256, sm, s>>>(d_topk_idx, K, E, G, tokens_per_src, T, ncs, w.chunk_cnt, w, d_tok_row,
                                            d_row_tok, 0, windowed);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
@@ -585,11 +626,11 @@ extern "C" int hep_moe_assign_ep(hep_sched_t h, const hep_sched_out *sched, cons
     HEP_CHECK_LAUNCH();
     chunk_scan_kernel<<<(E + 7) / 8, 256, 0, s>>>(1, ncs, E, w.chunk_cnt);
     HEP_CHECK_LAUNCH();
-    const size_t sm = sizeof(int32_t) * (2 * (size_t)E + 2 * (size_t)E * G);
+    const size_t sm = sizeof(int32_t) * (3 * (size_t)E + 2 * (size_t)E * G + (size_t)kChunk * K);
     HEP_REQUIRE(sm <= 200 * 1024, HEP_E_CAPACITY, "chunk_map smem %zu", sm);
     if (sm > 48 * 1024)
         HEP_CHECK_CUDA(cudaFuncSetAttribute(chunk_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    chunk_map_kernel<<<ncs, 128, sm, s>>>(d_topk_idx, K, E, G, tps, T, ncs, w.chunk_cnt, w, d_tok_row, nullptr, rank,
+    chunk_map_kernel<<<ncs, 256, sm, s>>>(d_topk_idx, K, E, G, tps, T, ncs, w.chunk_cnt, w, d_tok_row, nullptr, rank,
                                           false);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
