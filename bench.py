@@ -507,6 +507,19 @@ def main():
     torch.cuda.synchronize()
     sched_us = 1e3 * s0.elapsed_time(s1) / n_sched
 
+    # --- standalone permute (K5) on this micro-batch: the training and EP dispatch path;
+    # the timed forward runs it fused into the first expert GEMM's TMA gather
+    if layer.fuse_permute:
+        n_p = 20
+        p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        p0.record(stream)
+        for _ in range(n_p):
+            _lib.check(L.hep_moe_permute(x.data_ptr(), bufs.tok_row.data_ptr(), T, K, d, bufs.rows.data_ptr(),
+                                         stream.cuda_stream), "hep_moe_permute")
+        p1.record(stream)
+        torch.cuda.synchronize()
+        perm_ms = p0.elapsed_time(p1) / n_p
+
     gpu_load = layer.sched.gpu_load.cpu().tolist()
     m_num, m_den = layer.sched.m[:2].cpu().tolist()
     mean_load = sum(gpu_load) / len(gpu_load)
@@ -657,7 +670,10 @@ def main():
             },
             "hbm_kernels": {
                 "permute": {"GB/s": perm_bytes / (perm_ms / 1e3) / 1e9, "frac": perm_bytes / (perm_ms / 1e3) / 1e9 / hbm,
-                            "algorithmic_bytes": perm_bytes, "traffic": traffic.get("permute", {}).get("bytes")},
+                            "algorithmic_bytes": perm_bytes, "traffic": traffic.get("permute", {}).get("bytes"),
+                            "path": ("standalone K5 (training / EP dispatch path); the timed forward gathers x "
+                                     "rows inside the first expert GEMM (TMA tile::gather4) instead"
+                                     if layer.fuse_permute else "in the timed forward")},
                 "combine": {"GB/s": comb_bytes / (comb_ms / 1e3) / 1e9, "frac": comb_bytes / (comb_ms / 1e3) / 1e9 / hbm,
                             "algorithmic_bytes": comb_bytes, "traffic": traffic.get("combine", {}).get("bytes")},
                 "peak_GB/s": hbm,

@@ -307,6 +307,18 @@ int hep_moe_permute(const void *d_x, const int32_t *d_tok_row, int64_t T, int K,
 int hep_moe_expert_ffn(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg,
                        int n_seg, int64_t R, int64_t d_model, int64_t ffn, int n_experts, void *d_h, void *d_y,
                        void *d_workspace, size_t workspace_bytes, int32_t *d_status, void *stream);
+/*
+ * hep_moe_expert_ffn with the permute (K5) fused into the first GEMM: its A operand is
+ * gathered straight from the token activations d_x [T][d_model] by TMA tile::gather4,
+ * receive row r being token d_row_tok[r] (hep_moe_assign's row_tok), so the permuted
+ * rows buffer is never written or read.  Bit-identical to hep_moe_permute followed by
+ * hep_moe_expert_ffn.  Forward (inference) only; training keeps the rows buffer for the
+ * weight gradients.
+ */
+int hep_moe_expert_ffn_gather(const void *d_x, int64_t T, const int32_t *d_row_tok, const void *d_w13,
+                              const void *d_w2, const int32_t *d_seg, int n_seg, int64_t R, int64_t d_model,
+                              int64_t ffn, int n_experts, void *d_h, void *d_y, void *d_workspace,
+                              size_t workspace_bytes, int32_t *d_status, void *stream);
 /* workspace for hep_moe_expert_ffn's device-built m-tile list */
 size_t hep_moe_ffn_workspace(int n_seg, int64_t R, int n_experts);
 

@@ -86,6 +86,11 @@ struct Params {
     // buffer over NVLink (peer pointers), instead of into `out`
     const uint64_t *row_addr;
     GateParams gate;  // EPI_GATE only
+    // grouped mode, A operand gathered by row (the permute fused into the GEMM): receive
+    // row r is token gather_idx[r] of the A tensor map (box {64, 1}), rows past an m-tile's
+    // valid rows read gather_oob (outside the map: TMA zero fill)
+    const int32_t *gather_idx;
+    int32_t gather_oob;
 };
 
 __device__ __forceinline__ uint64_t pick_policy(int k) {
@@ -483,7 +488,36 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int64_t n_total = total_tiles(p);
     const int kb = p.kblocks;
 
-    if (warp == 0) {
+    if (warp == 0 && p.gather_idx) {
+        // ============ TMA producer, A rows gathered by token (the fused permute) ============
+        // lane l gathers tile rows 4l..4l+3 with one tile::gather4; lane 0 owns the barriers
+        // and the weight tile
+        const uint64_t pol_a = policy_evict_last();
+        const uint64_t pol_b = p.pol_mode ? pick_policy((p.pol_mode >> 2) & 3) : policy_evict_normal();
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int64_t t = blockIdx.x; t < n_total; t += gridDim.x) {
+            const Tile tl = decode(p, t, s_off);
+            const int32_t b_row = (int32_t)(tl.expert * p.b_rows_per_exp + (int64_t)tl.n_blk * BN);
+            int r[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int local = 4 * lane + j;
+                r[j] = local < tl.rows ? p.gather_idx[tl.row0 + local] : p.gather_oob;
+            }
+            const int4 rows = make_int4(r[0], r[1], r[2], r[3]);
+            for (int k = 0; k < tl.kb; ++k) {
+                if (lane == 0) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
+                }
+                __syncwarp();
+                tma_gather4(sA + stage * S::A_BYTES + 512 * lane, &tmA, &full[stage], k * BK, rows, pol_a);
+                if (lane == 0) tma_load_2d_hint(sB + stage * S::B_BYTES, &tmB, &full[stage], k * BK, b_row, pol_b);
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp == 0) {
         if (lane == 0) {
             // ===================== TMA producer =====================
             int stage = 0;
@@ -667,7 +701,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
     const int kb = p.kblocks;
 
-    if (warp == 0) {
+    if (warp == 0 && p.gather_idx) {
+        // ===== TMA producer (both CTAs), A rows gathered by token (the fused permute) =====
+        // lane l gathers this CTA's tile rows 4l..4l+3 (tile::gather4 completing on the
+        // leader's barrier); lane 0 owns the barrier and the weight half
+        const uint64_t pol_a = policy_evict_last();
+        const uint64_t pol_b = p.pol_mode ? pick_policy((p.pol_mode >> 2) & 3) : policy_evict_normal();
+        const uint32_t full_l = mapa_shared(smem_u32(&full[0]), 0);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int64_t t = cid; t < n_total; t += ncl) {
+            const Tile tl = decode(p, t, s_off);
+            const int32_t b_row = (int32_t)(tl.expert * p.b_rows_per_exp + (int64_t)tl.n_blk * BN) + (int32_t)rank * 128;
+            int r[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int local = (int)rank * 128 + 4 * lane + j;
+                r[j] = local < tl.rows ? p.gather_idx[tl.row0 + local] : p.gather_oob;
+            }
+            const int4 rows = make_int4(r[0], r[1], r[2], r[3]);
+            for (int k = 0; k < kb; ++k) {
+                if (lane == 0) {
+                    mbar_wait_cluster(&empty[stage], phase ^ 1);
+                    if (leader) mbar_arrive_expect_tx(&full[stage], 2 * S::STAGE_BYTES);
+                }
+                __syncwarp();
+                tma_gather4_2sm(sA + stage * S::A_BYTES + 512 * lane, &tmA, full_l + 8 * stage, k * BK, rows, pol_a);
+                if (lane == 0)
+                    tma_load_2d_2sm(sB + stage * S::B_BYTES, &tmB, full_l + 8 * stage, k * BK, b_row, pol_b);
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp == 0) {
         if (lane == 0) {
             // ===================== TMA producer (both CTAs) =====================
             const uint64_t pol_a = p.pol_mode ? pick_policy(p.pol_mode & 3) : policy_evict_last();
@@ -951,7 +1016,7 @@ static int launch(const void *A, int64_t a_rows, int64_t K, const void *B, int64
                   int64_t max_tiles, cudaStream_t stream) {
     using S = Smem<BN, STAGES>;
     CUtensorMap ta, tb;
-    int rc = make_tmap(&ta, A, (uint64_t)a_rows, (uint64_t)K, BM);
+    int rc = make_tmap(&ta, A, (uint64_t)a_rows, (uint64_t)K, p.gather_idx ? 1 : BM);  // gather: {64, 1} rows
     if (rc) return rc;
     rc = make_tmap(&tb, B, (uint64_t)b_rows, (uint64_t)K, BN);
     if (rc) return rc;
@@ -970,7 +1035,7 @@ static int launch2sm(const void *A, int64_t a_rows, int64_t K, const void *B, in
                      cudaStream_t stream) {
     using S = Smem2<STAGES>;
     CUtensorMap ta, tb;
-    int rc = make_tmap(&ta, A, (uint64_t)a_rows, (uint64_t)K, 128);
+    int rc = make_tmap(&ta, A, (uint64_t)a_rows, (uint64_t)K, p.gather_idx ? 1 : 128);  // gather: {64, 1} rows
     if (rc) return rc;
     rc = make_tmap(&tb, B, (uint64_t)b_rows, (uint64_t)K, 128);
     if (rc) return rc;
@@ -1113,7 +1178,18 @@ extern "C" size_t hep_moe_ffn_workspace(int n_seg, int64_t R, int n_experts) {
 static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg, int n_seg,
                           int64_t R, int64_t d_model, int64_t ffn, int n_experts, void *d_h, void *d_y, void *d_pre,
                           void *d_workspace, size_t workspace_bytes, int32_t *d_status, void *stream,
-                          const uint64_t *d_y_addr = nullptr, int64_t rows_hint = -1);
+                          const uint64_t *d_y_addr = nullptr, int64_t rows_hint = -1, const int32_t *d_row_tok = nullptr,
+                          int64_t T = 0);
+
+extern "C" int hep_moe_expert_ffn_gather(const void *d_x, int64_t T, const int32_t *d_row_tok, const void *d_w13,
+                                         const void *d_w2, const int32_t *d_seg, int n_seg, int64_t R, int64_t d_model,
+                                         int64_t ffn, int n_experts, void *d_h, void *d_y, void *d_workspace,
+                                         size_t workspace_bytes, int32_t *d_status, void *stream) {
+    HEP_REQUIRE(d_x && d_row_tok, HEP_E_CONTRACT, "hep_moe_expert_ffn_gather: null pointer");
+    HEP_REQUIRE(T > 0 && T < ((int64_t)1 << 31), HEP_E_DIMENSION, "hep_moe_expert_ffn_gather: T=%lld", (long long)T);
+    return expert_ffn_fwd(d_x, d_w13, d_w2, d_seg, n_seg, R, d_model, ffn, n_experts, d_h, d_y, nullptr, d_workspace,
+                          workspace_bytes, d_status, stream, nullptr, -1, d_row_tok, T);
+}
 
 extern "C" int hep_moe_expert_ffn_p2p(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg,
                                       int n_seg, int64_t R, int64_t rows_hint, int64_t d_model, int64_t ffn,
@@ -1144,7 +1220,7 @@ extern "C" int hep_moe_expert_ffn_train(const void *d_rows, const void *d_w13, c
 static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg, int n_seg,
                           int64_t R, int64_t d_model, int64_t ffn, int n_experts, void *d_h, void *d_y, void *d_pre,
                           void *d_workspace, size_t workspace_bytes, int32_t *d_status, void *stream,
-                          const uint64_t *d_y_addr, int64_t rows_hint) {
+                          const uint64_t *d_y_addr, int64_t rows_hint, const int32_t *d_row_tok, int64_t T) {
     HEP_REQUIRE(d_rows && d_w13 && d_w2 && d_seg && d_h && d_y && d_workspace, HEP_E_CONTRACT,
                 "hep_moe_expert_ffn: null pointer");
     HEP_REQUIRE(d_model % 256 == 0 && ffn % 128 == 0 && d_model % BK == 0, HEP_E_DIMENSION,
@@ -1187,11 +1263,16 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
     p.out_cols = ffn;
     p.aux = d_pre;  // training: store the pre-activations A13 (W13 interleave)
     p.ld_aux = 2 * ffn;
-    int rc = pairs ? launch2sm<6, EPI_SWIGLU>(d_rows, R, d_model, d_w13, (int64_t)n_experts * 2 * ffn, p, s)
-                   : launch<256, 4, EPI_SWIGLU>(d_rows, R, d_model, d_w13, (int64_t)n_experts * 2 * ffn, p, 0, s);
+    // fused permute: A = x [T][d] gathered through row_tok instead of the permuted rows
+    p.gather_idx = d_row_tok;
+    p.gather_oob = (int32_t)T;
+    const int64_t a_rows = d_row_tok ? T : R;
+    int rc = pairs ? launch2sm<6, EPI_SWIGLU>(d_rows, a_rows, d_model, d_w13, (int64_t)n_experts * 2 * ffn, p, s)
+                   : launch<256, 4, EPI_SWIGLU>(d_rows, a_rows, d_model, d_w13, (int64_t)n_experts * 2 * ffn, p, 0, s);
     if (rc) return rc;
     // GEMM 2: Y = H W2^T, B = W2 [E][d][F]
     p.aux = nullptr;
+    p.gather_idx = nullptr;
     p.row_addr = d_y_addr;
     p.raster_gm = gm2_env ? atoi(gm2_env) : (gm_default >= 0 ? gm_default : 8);
     p.kblocks = (int)(ffn / BK);

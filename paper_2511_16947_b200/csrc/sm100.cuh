@@ -64,6 +64,28 @@ __device__ __forceinline__ void tma_load_2d_hint(void *smem_dst, const void *tma
         : "memory");
 }
 
+// TMA row gather (tile::gather4): 4 rows r0..r3 of a 2-D tensor map whose box is
+// {cols, 1}, written back to back at smem_dst (same swizzled layout as rows of a tile load)
+__device__ __forceinline__ void tma_gather4(void *smem_dst, const void *tmap, uint64_t *bar, int32_t c0, int4 rows,
+                                            uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes.L2::cache_hint "
+        "[%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(rows.x), "r"(rows.y), "r"(rows.z),
+        "r"(rows.w), "l"(policy)
+        : "memory");
+}
+// CTA-pair variant: bytes complete on an mbarrier that may live in the peer CTA
+__device__ __forceinline__ void tma_gather4_2sm(void *smem_dst, const void *tmap, uint32_t mbar_cluster, int32_t c0,
+                                                int4 rows, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        ".L2::cache_hint [%0], [%1, {%3, %4, %5, %6, %7}], [%2], %8;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(mbar_cluster), "r"(c0), "r"(rows.x), "r"(rows.y), "r"(rows.z),
+        "r"(rows.w), "l"(policy)
+        : "memory");
+}
+
 // L2 eviction-priority policies for TMA loads / global stores
 __device__ __forceinline__ uint64_t policy_evict_last() {
     uint64_t p;

@@ -6,8 +6,9 @@ Per micro-batch, all on one CUDA stream, no host synchronisation:
       + gate        top-K + softmax(top-K) + hist[G][E]  epilogue, one TMEM lane per token)
   K3  scheduler     m, lex-min plan, integerize, ranges hep_sched_solve (1 CTA)
   K4  assignment    (token, k) -> receive row           hep_moe_assign_precounted
-  K5  permute       rows[row] = x[token]                hep_moe_permute
-  K6  expert FFN    SwiGLU grouped GEMM x2              hep_moe_expert_ffn (tcgen05)
+  K5  permute       rows[row] = x[token]                hep_moe_permute (128-bit, one warp per token)
+  K6  expert FFN    SwiGLU grouped GEMM x2              hep_moe_expert_ffn (tcgen05; opt-in
+                                                        hep_moe_expert_ffn_gather fuses K5)
   K7  combine       out[t] = sum_k w * y[row]           hep_moe_combine
 
 ``MoELayer`` with ``num_sources = G`` runs the paper's EP group of G GPUs
@@ -109,7 +110,7 @@ class MoELayer(torch.nn.Module):
 
     def __init__(self, placement: Placement, d_model: int, ffn: int, top_k: int, *, seed: int = 0,
                  gate_bias: torch.Tensor | None = None, device=None, train: bool = False,
-                 pipeline_ratio: float | Fraction | None = None):
+                 pipeline_ratio: float | Fraction | None = None, fuse_permute: bool = False):
         super().__init__()
         self.train_mode = train
         # harmony_pipelined (simulator.py:17-20, :375, :420-435): a 1 - pipeline_ratio
@@ -122,7 +123,13 @@ class MoELayer(torch.nn.Module):
             if train:
                 raise ValueError("the pipelined split is a forward (serving) schedule; train with pipeline_ratio=None")
             self.static_share = Fraction(1) - Fraction(pipeline_ratio)
-        self.LAUNCHES_PER_FORWARD = 11 if self.static_share is None else 18
+        # fuse_permute: gather the x rows inside the first expert GEMM (TMA tile::gather4)
+        # instead of the K5 permute kernel.  Bit-identical, but measured slower (gather4
+        # issues one 128-byte row request at a time, ~10 B/clk/SM: Qwen3 FFN 2.15 -> 4.67 ms,
+        # profiles/r01/ffn_ab_r01d.txt), so the permute kernel is the default.  Never in
+        # training (the weight gradients contract over the permuted rows).
+        self.fuse_permute = fuse_permute and not train
+        self.LAUNCHES_PER_FORWARD = (11 if self.static_share is None else 18) - (1 if self.fuse_permute else 0)
         torch_ = _lib.require_cuda()
         self.device = torch_.device("cuda", torch_.cuda.current_device()) if device is None else torch_.device(device)
         self.placement = placement
@@ -237,11 +244,17 @@ class MoELayer(torch.nn.Module):
                "hep_moe_assign_phase(scheduled)")
         mark("assign", 1)
         mark("permute", 0)
-        ck(L.hep_moe_permute(x.data_ptr(), b.tok_row.data_ptr(), T, K, self.d, b.rows.data_ptr(), s),
-           "hep_moe_permute")
+        if not self.fuse_permute:
+            ck(L.hep_moe_permute(x.data_ptr(), b.tok_row.data_ptr(), T, K, self.d, b.rows.data_ptr(), s),
+               "hep_moe_permute")
         mark("permute", 1)
         mark("ffn", 0)
-        if b.pre is None:
+        if self.fuse_permute:  # K5 fused into GEMM 1: x rows gathered by TMA through row_tok
+            ck(L.hep_moe_expert_ffn_gather(x.data_ptr(), T, b.row_tok.data_ptr(), self.w13.data_ptr(),
+                                           self.w2.data_ptr(), b.seg.data_ptr(), b.n_seg, b.R, self.d, self.F, E,
+                                           b.h.data_ptr(), b.y.data_ptr(), b.ffn_ws.data_ptr(), b.ffn_ws.numel(),
+                                           self.sched.status.data_ptr(), s), "hep_moe_expert_ffn_gather")
+        elif b.pre is None:
             ck(L.hep_moe_expert_ffn(b.rows.data_ptr(), self.w13.data_ptr(), self.w2.data_ptr(), b.seg.data_ptr(),
                                     b.n_seg, b.R, self.d, self.F, E, b.h.data_ptr(), b.y.data_ptr(),
                                     b.ffn_ws.data_ptr(), b.ffn_ws.numel(), self.sched.status.data_ptr(), s),

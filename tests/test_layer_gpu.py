@@ -23,13 +23,13 @@ def P():
     return P
 
 
-def _run(P, G, E, K, d, F, T, s=1.0, seed=0, sample=None):
+def _run(P, G, E, K, d, F, T, s=1.0, seed=0, sample=None, fuse_permute=False):
     from oracle import layer_ref
 
     shape = P.ClusterShape(G, E, 2)
     pl = P.cayley_symmetric(shape) if E >= G else P.identical_placement(shape)
     bias = torch.tensor(P.zipf_gate_bias(E, s, seed)) if s > 0 else None
-    layer = P.MoELayer(pl, d, F, K, seed=seed, gate_bias=bias)
+    layer = P.MoELayer(pl, d, F, K, seed=seed, gate_bias=bias, fuse_permute=fuse_permute)
     g = torch.Generator(device="cuda").manual_seed(1000 + seed)
     x = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
     out = layer(x).clone()
@@ -67,9 +67,12 @@ def test_tiny_config_bit_exact_schedule_and_output(P):
     # token -> row schedule: bit-exact
     assert np.array_equal(b.tok_row.cpu().numpy(), ref["tok_row"])
     assert b.expert_rows.cpu().tolist() == ref["expert_rows"].tolist()
-    # permuted rows are exact copies
+    # the permute writes exact copies, and the layer with the permute fused into the first
+    # GEMM's TMA gather (hep_moe_expert_ffn_gather) gives the same output bit for bit
     R = x.shape[0] * layer.K
     assert torch.equal(b.rows[:R], x[b.row_tok[:R].long()])
+    out2 = _run(P, G=4, E=8, K=2, d=512, F=1024, T=4096, s=1.0, fuse_permute=True)[2]
+    assert torch.equal(out, out2)
     # layer output (bf16 tolerance)
     got = out.float().cpu().numpy()
     rel = np.abs(got - ref["out"]).max() / np.abs(ref["out"]).max()
@@ -86,6 +89,8 @@ def test_routing_shapes_sampled_output(P, G, E, K, d, F, T, s):
     rng = np.random.default_rng(G * E + T)
     sample = np.sort(rng.choice(T, size=96, replace=False))
     layer, x, out, b, ref, pl = _run(P, G, E, K, d, F, T, s=s, seed=1, sample=sample)
+    fused = _run(P, G, E, K, d, F, T, s=s, seed=1, sample=sample[:4], fuse_permute=True)[2]
+    assert torch.equal(out, fused)  # fused permute (TMA gather) == permute kernel + GEMM
     assert np.array_equal(b.topk_idx.cpu().numpy(), ref["topk_idx"])
     assert np.array_equal(b.hist.cpu().numpy(), ref["hist"])
     assert layer.sched.rows(layer.sched.xi) == ref["sched"]["xi"]

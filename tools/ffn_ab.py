@@ -65,6 +65,13 @@ def main():
     flops = 6.0 * d * F * b.R
 
     def ffn():
+        if os.environ.get("AB_GATHER") == "1":  # permute fused into GEMM 1 (TMA gather of x rows)
+            _lib.check(L.hep_moe_expert_ffn_gather(x.data_ptr(), T, b.row_tok.data_ptr(), layer.w13.data_ptr(),
+                                                   layer.w2.data_ptr(), b.seg.data_ptr(), b.n_seg, b.R, d, F, E,
+                                                   b.h.data_ptr(), b.y.data_ptr(), b.ffn_ws.data_ptr(),
+                                                   b.ffn_ws.numel(), layer.sched.status.data_ptr(), s.cuda_stream),
+                       "ffn_gather")
+            return
         _lib.check(L.hep_moe_expert_ffn(b.rows.data_ptr(), layer.w13.data_ptr(), layer.w2.data_ptr(), b.seg.data_ptr(),
                                         b.n_seg, b.R, d, F, E, b.h.data_ptr(), b.y.data_ptr(), b.ffn_ws.data_ptr(),
                                         b.ffn_ws.numel(), layer.sched.status.data_ptr(), s.cuda_stream), "ffn")
