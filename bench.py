@@ -497,6 +497,27 @@ def main():
     stage_ms = {k: statistics.mean(e[k][0].elapsed_time(e[k][1]) for e in evs) for k in stages}
     ffn_ms, perm_ms, comb_ms = stage_ms["ffn"], stage_ms["permute"], stage_ms["combine"]
 
+    # --- the SM clock the expert GEMMs actually ran at: CTA 0 stamps clock64 and the
+    # global timer at entry/exit of each GEMM (HEP_FFN_CLOCK=1), eager steps back to back
+    ffn_clock = None
+    if not args.profile:
+        import ctypes as _ct
+
+        os.environ["HEP_FFN_CLOCK"] = "1"
+        try:
+            for i in range(min(args.steps, 10)):
+                staged_step(i)
+            torch.cuda.synchronize()
+            st = (_ct.c_int64 * 8)()
+            _lib.check(L.hep_ffn_debug_clock(st), "hep_ffn_debug_clock")
+            mhz = [1e3 * (st[4 * g + 2] - st[4 * g]) / max(1, st[4 * g + 3] - st[4 * g + 1]) for g in range(2)]
+            ns = [st[4 * g + 3] - st[4 * g + 1] for g in range(2)]
+            ffn_clock = {"gemm1_mhz": round(mhz[0], 1), "gemm2_mhz": round(mhz[1], 1),
+                         "mhz": round((mhz[0] * ns[0] + mhz[1] * ns[1]) / max(1, ns[0] + ns[1]), 1),
+                         "source": "clock64 / globaltimer of CTA 0 across each expert GEMM (eager steps)"}
+        finally:
+            del os.environ["HEP_FFN_CLOCK"]
+
     # --- scheduler latency: the K3 kernel alone, on this micro-batch's histogram
     n_sched = 200
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -661,6 +682,10 @@ def main():
                 "unit": "TFLOP/s",
                 "frac": ffn_tflops / tf_sus,
                 "frac_of_burst_peak": ffn_tflops / tf_burst,
+                # dense bf16 tcgen05 rate at the clock the GEMMs ran at: 8192 flop/clk/SM x 148 SMs
+                "ffn_sm_clock": ffn_clock,
+                "frac_of_peak_at_ffn_clock": (ffn_tflops / (8192 * L.hep_device_sm_count() * ffn_clock["mhz"] * 1e6 / 1e12)
+                                              if ffn_clock else None),
                 "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside back-to-back steps)",
                 "algorithmic_flops_per_launch": ffn_flops,
                 # minimal DRAM bytes of one launch: every weight once, X read, H written + read, Y written

@@ -315,6 +315,10 @@ int hep_moe_expert_ffn(const void *d_rows, const void *d_w13, const void *d_w2, 
  * hep_moe_expert_ffn.  Forward (inference) only; training keeps the rows buffer for the
  * weight gradients.
  */
+/* Diagnostics: with HEP_FFN_CLOCK=1 in the environment, CTA 0 of each expert GEMM records
+ * (clock64, globaltimer ns) at entry and exit; out[8] = GEMM1 {c0, t0, c1, t1}, GEMM2 {...}
+ * of the last such launch, i.e. the SM clock the tensor cores ran at. */
+int hep_ffn_debug_clock(int64_t *host_out8);
 int hep_moe_expert_ffn_gather(const void *d_x, int64_t T, const int32_t *d_row_tok, const void *d_w13,
                               const void *d_w2, const int32_t *d_seg, int n_seg, int64_t R, int64_t d_model,
                               int64_t ffn, int n_experts, void *d_h, void *d_y, void *d_workspace,

@@ -91,7 +91,21 @@ struct Params {
     // valid rows read gather_oob (outside the map: TMA zero fill)
     const int32_t *gather_idx;
     int32_t gather_oob;
+    int clk_slot;  // > 0: CTA 0 stamps (clock64, globaltimer) at entry and exit into g_gemm_clk[clk_slot - 1]
 };
+
+// Diagnostics (HEP_FFN_CLOCK=1): SM clock cycles and wall nanoseconds of CTA 0 across
+// the two expert GEMMs, i.e. the SM clock the tensor cores actually ran at (the
+// power-capped clock of a long GEMM is not what nvidia-smi samples between kernels).
+__device__ long long g_gemm_clk[2][4];
+__device__ __forceinline__ void clk_stamp(const Params &p, int at) {
+    if (p.clk_slot > 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+        long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        g_gemm_clk[p.clk_slot - 1][2 * at] = clock64();
+        g_gemm_clk[p.clk_slot - 1][2 * at + 1] = ns;
+    }
+}
 
 __device__ __forceinline__ uint64_t pick_policy(int k) {
     return k == 2 ? sm100::policy_evict_last() : (k == 3 ? sm100::policy_evict_first() : sm100::policy_evict_normal());
@@ -484,6 +498,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    clk_stamp(p, 0);
 
     const int64_t n_total = total_tiles(p);
     const int kb = p.kblocks;
@@ -624,6 +639,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
+    clk_stamp(p, 1);
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem_base, S::TMEM_COLS);
@@ -696,6 +712,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    clk_stamp(p, 0);
 
     const int64_t n_total = total_tiles(p);
     const int64_t cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
@@ -807,6 +824,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     tc_fence_before();
     __syncthreads();
     cluster_sync();
+    clk_stamp(p, 1);
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc_2sm(tmem_base, TMEM_COLS);
@@ -1243,6 +1261,9 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
     Params p{};
     p.grouped = 1;
     p.pol_mode = pol_mode;
+    const char *clk_env = getenv("HEP_FFN_CLOCK");
+    const bool clk = clk_env && clk_env[0] == '1';
+    p.clk_slot = clk ? 1 : 0;
     // raster bands (m-tiles swept across all N-blocks before the next band): 16 for the
     // SwiGLU GEMM, 8 for the down projection (profiles/r01/raster*.txt)
     const char *gm_env = getenv("HEP_RASTER_GM");
@@ -1273,6 +1294,7 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
     // GEMM 2: Y = H W2^T, B = W2 [E][d][F]
     p.aux = nullptr;
     p.gather_idx = nullptr;
+    p.clk_slot = clk ? 2 : 0;
     p.row_addr = d_y_addr;
     p.raster_gm = gm2_env ? atoi(gm2_env) : (gm_default >= 0 ? gm_default : 8);
     p.kblocks = (int)(ffn / BK);
@@ -1409,4 +1431,14 @@ extern "C" int hep_router_bwd(const void *d_x, const void *d_wg, const void *d_d
     if ((rc = make_tmap(&ta, d_dlogits, (uint64_t)T, (uint64_t)E64, BM))) return rc;
     if ((rc = make_tmap_mn(&tb, d_wg, (uint64_t)E64, (uint64_t)d_model))) return rc;
     return launch_maps<256, 4, EPI_BF16, false, true>(ta, tb, q, (T + BM - 1) / BM * q.n_tiles, s);
+}
+
+// [gemm][start cycles, start ns, end cycles, end ns] of CTA 0 in the last FFN launched
+// with HEP_FFN_CLOCK=1 (diagnostic: the effective SM clock of the expert GEMMs)
+extern "C" int hep_ffn_debug_clock(int64_t *host_out8) {
+    HEP_REQUIRE(host_out8, HEP_E_CONTRACT, "null output");
+    long long tmp[8];
+    HEP_CHECK_CUDA(cudaMemcpyFromSymbol(tmp, hep::gemm::g_gemm_clk, sizeof(tmp)));
+    for (int i = 0; i < 8; ++i) host_out8[i] = tmp[i];
+    return HEP_OK;
 }
