@@ -624,6 +624,7 @@ def main():
     ffn_tflops = ffn_flops / (ffn_ms / 1e3) / 1e12
     perm_bytes = T * d * 2 * (1 + K) + T * K * 4
     comb_bytes = T * K * d * 2 + T * K * 4 * 2 + T * d * 2
+    rg_bytes = T * d * 2 + layer.e_pad * d * 2 + T * layer.e_pad * 4 + T * K * 8  # x, Wg, logits, top-K
     launches_per_step = layer.LAUNCHES_PER_FORWARD
 
     if rank == 0:
@@ -701,6 +702,11 @@ def main():
                                      if layer.fuse_permute else "in the timed forward")},
                 "combine": {"GB/s": comb_bytes / (comb_ms / 1e3) / 1e9, "frac": comb_bytes / (comb_ms / 1e3) / 1e9 / hbm,
                             "algorithmic_bytes": comb_bytes, "traffic": traffic.get("combine", {}).get("bytes")},
+                # K1 fused router GEMM + gate: reads x and Wg, writes logits, top-K, weights
+                "router_gate": {"GB/s": rg_bytes / (stage_ms["router"] / 1e3) / 1e9,
+                                "frac": rg_bytes / (stage_ms["router"] / 1e3) / 1e9 / hbm,
+                                "algorithmic_bytes": rg_bytes, "traffic": traffic.get("router_gate", {}).get("bytes"),
+                                "note": "eager stage time (includes the histogram memset and launch gap)"},
                 "peak_GB/s": hbm,
             },
             "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": T * d * 2,

@@ -20,7 +20,7 @@ done
 timeout 600 python bench.py --config mixtral --pipeline-ratio 0.5 --no-cpu-baseline --no-train > gpurun_out/bench_mixtral_pipelined_$R.json 2>&1
 timeout 300 python bench.py --impl reference --config mixtral --steps 3 --warmup 1 > gpurun_out/bench_ref_mixtral_$R.json 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k regex:"gemm2sm_kernel|gemm_kernel<.int.256|sched_kernel|permute|combine|gate_topk|chunk_map" -c 8 \
+  -k regex:"gemm2sm_kernel|gemm_kernel|sched_kernel|permute|combine|chunk_map|plan_prep" -c 9 \
   -o gpurun_out/prof_mixtral_$R python bench.py --config mixtral --profile --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_mixtral_$R.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
   -k regex:"gemm_kernel<.int.256|sched_kernel|permute|combine" -c 5 \

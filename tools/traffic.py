@@ -38,9 +38,10 @@ def summarise(path):
                 "kernels": [re.sub(r"\(.*", "", x["name"]) for x in trio],
             }
             break
-    for key, pat in (("permute", "permute_kernel"), ("combine", "combine_kernel"), ("sched", "sched_kernel")):
+    for key, pat in (("permute", "permute_kernel"), ("combine", "combine_kernel"), ("sched", "sched_kernel"),
+                     ("router_gate", r"gemm_kernel<\d+, \d+, 4,")):
         for k in ks:
-            if pat in k["name"]:
+            if re.search(pat, k["name"]):
                 out[key] = {"bytes": k.get("dram__bytes_read.sum", 0) + k.get("dram__bytes_write.sum", 0),
                             "ns": k.get("gpu__time_duration.sum", 0)}
                 break
