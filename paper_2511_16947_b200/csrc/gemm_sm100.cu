@@ -91,6 +91,7 @@ struct Params {
     // valid rows read gather_oob (outside the map: TMA zero fill)
     const int32_t *gather_idx;
     int32_t gather_oob;
+    int tile_m;    // modes 0 / 2: rows per m-tile (0 = BM; 256 on the CTA pair)
     int clk_slot;  // > 0: CTA 0 stamps (clock64, globaltimer) at entry and exit into g_gemm_clk[clk_slot - 1]
 };
 
@@ -133,7 +134,8 @@ struct Tile {
 };
 
 __device__ __forceinline__ int64_t total_tiles(const Params &p) {
-    if (p.grouped == 0) return ((p.M + BM - 1) / BM) * p.n_tiles;
+    const int tm = p.tile_m ? p.tile_m : BM;
+    if (p.grouped == 0) return ((p.M + tm - 1) / tm) * p.n_tiles;
     if (p.grouped == 2) return (int64_t)p.n_exp * p.m_tiles * p.n_tiles;
     return (int64_t)p.exp_mt_off[p.n_exp] * p.n_tiles;
 }
@@ -142,26 +144,27 @@ __device__ __forceinline__ Tile decode(const Params &p, int64_t t, const int32_t
     Tile tl;
     tl.k0 = 0;
     tl.kb = p.kblocks;
+    const int tm = p.tile_m ? p.tile_m : BM;
     if (p.grouped == 2) {
         const int64_t per = (int64_t)p.m_tiles * p.n_tiles;
         const int e = (int)(t / per);
         const int64_t rem = t - (int64_t)e * per;
         tl.expert = e;
         tl.n_blk = (int)(rem / p.m_tiles);
-        tl.row0 = (int32_t)((rem % p.m_tiles) * BM);
-        tl.rows = (int32_t)(p.M - tl.row0 < BM ? p.M - tl.row0 : BM);
+        tl.row0 = (int32_t)((rem % p.m_tiles) * tm);
+        tl.rows = (int32_t)(p.M - tl.row0 < tm ? p.M - tl.row0 : tm);
         tl.k0 = p.exp_rows[e];
         tl.kb = (int)((p.exp_rows[e + 1] - tl.k0) / BK);
         return tl;
     }
     if (p.grouped == 0) {
-        const int64_t mt = (p.M + BM - 1) / BM;
+        const int64_t mt = (p.M + tm - 1) / tm;
         tl.expert = 0;
         tl.n_blk = (int)(t / mt);
         const int64_t m = t % mt;
-        tl.row0 = (int32_t)(m * BM);
-        const int64_t left = p.M - m * BM;
-        tl.rows = (int32_t)(left < BM ? left : BM);
+        tl.row0 = (int32_t)(m * tm);
+        const int64_t left = p.M - m * tm;
+        tl.rows = (int32_t)(left < tm ? left : tm);
         return tl;
     }
     // expert e owns tiles [off[e]*n_tiles, off[e+1]*n_tiles)
@@ -671,7 +674,9 @@ struct Smem2 {
     static constexpr size_t BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + 8 * (2 * STAGES + 4) + 16 + kOffBytes;
 };
 
-template <int STAGES, int EPI>
+// A_MN / B_MN as in gemm_kernel (the backward GEMMs): an MN-major operand half of 128
+// rows is two 64 x 64 boxes per stage, 8 KB apart (the descriptor's LBO).
+template <int STAGES, int EPI, bool A_MN = false, bool B_MN = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params p) {
     constexpr int BN = 256;
@@ -761,11 +766,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const Tile tl = decode(p, t, s_off);
                 const int32_t a_row = tl.row0 + (int32_t)rank * 128;
                 const int32_t b_row = (int32_t)(tl.expert * p.b_rows_per_exp + (int64_t)tl.n_blk * BN) + (int32_t)rank * 128;
-                for (int k = 0; k < kb; ++k) {
+                // contraction offsets (gemm_kernel's): mode 2 contracts over the expert's rows;
+                // an MN-major weight is [K][N] per expert, stacked along K
+                const int32_t a_k0 = (int32_t)tl.k0;
+                const int32_t b_k0 = p.grouped == 2 ? (int32_t)tl.k0 : (int32_t)(tl.expert * p.b_rows_per_exp);
+                const int32_t b_mn = tl.n_blk * BN + (int32_t)rank * 128;
+                for (int k = 0; k < tl.kb; ++k) {
                     mbar_wait_cluster(&empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * S::STAGE_BYTES);
-                    tma_load_2d_2sm(sA + stage * S::A_BYTES, &tmA, full_l + 8 * stage, k * BK, a_row, pol_a);
-                    tma_load_2d_2sm(sB + stage * S::B_BYTES, &tmB, full_l + 8 * stage, k * BK, b_row, pol_b);
+                    if constexpr (A_MN) {
+#pragma unroll
+                        for (int i = 0; i < 2; ++i)
+                            tma_load_2d_2sm(sA + stage * S::A_BYTES + i * 8192, &tmA, full_l + 8 * stage, a_row + 64 * i,
+                                            a_k0 + k * BK, pol_a);
+                    } else {
+                        tma_load_2d_2sm(sA + stage * S::A_BYTES, &tmA, full_l + 8 * stage, a_k0 + k * BK, a_row, pol_a);
+                    }
+                    if constexpr (B_MN) {
+#pragma unroll
+                        for (int i = 0; i < 2; ++i)
+                            tma_load_2d_2sm(sB + stage * S::B_BYTES + i * 8192, &tmB, full_l + 8 * stage, b_mn + 64 * i,
+                                            b_k0 + k * BK, pol_b);
+                    } else {
+                        tma_load_2d_2sm(sB + stage * S::B_BYTES, &tmB, full_l + 8 * stage, k * BK, b_row, pol_b);
+                    }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -773,24 +797,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         if (leader && lane == 0) {
             // ===================== MMA issuer (leader CTA) =====================
-            constexpr uint32_t idesc = idesc_bf16_f32(kPairRows, BN);
+            constexpr uint32_t idesc =
+                idesc_bf16_f32(kPairRows, BN) | (A_MN ? (1u << 15) : 0u) | (B_MN ? (1u << 16) : 0u);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int64_t t = cid; t < n_total; t += ncl) {
+                const int tkb = p.grouped == 2 ? decode(p, t, s_off).kb : kb;
                 mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
-                for (int k = 0; k < kb; ++k) {
+                for (int k = 0; k < tkb; ++k) {
                     mbar_wait_cluster(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(sA + stage * S::A_BYTES);
                     const uint32_t b_addr = smem_u32(sB + stage * S::B_BYTES);
 #pragma unroll
-                    for (int kk = 0; kk < BK / 16; ++kk)
-                        mma_bf16_2sm(d_tmem, desc_kmajor_sw128(a_addr + kk * 32), desc_kmajor_sw128(b_addr + kk * 32),
-                                     idesc, (k | kk) ? 1u : 0u);
+                    for (int kk = 0; kk < BK / 16; ++kk) {
+                        const uint64_t ad = A_MN ? desc_mnmajor_sw128(a_addr + kk * 2048) : desc_kmajor_sw128(a_addr + kk * 32);
+                        const uint64_t bd = B_MN ? desc_mnmajor_sw128(b_addr + kk * 2048) : desc_kmajor_sw128(b_addr + kk * 32);
+                        mma_bf16_2sm(d_tmem, ad, bd, idesc, (k | kk) ? 1u : 0u);
+                    }
                     mma_commit_2sm_mc(&empty[stage], 0x3);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -813,8 +841,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
             const int local_row = (int)rank * 128 + row_in_cta;
-            store_tile<BN, EPI>(p, t_row, (int64_t)tl.row0 + local_row, local_row < tl.rows, tl.n_blk, pol_out, 0, false,
-                                half);
+            store_tile<BN, EPI>(p, t_row, (int64_t)tl.row0 + local_row, local_row < tl.rows, tl.n_blk, pol_out, tl.expert,
+                                tl.kb == 0, half);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster_relaxed(tempty_l + 8 * acc);
@@ -1060,6 +1088,17 @@ static int launch2sm(const void *A, int64_t a_rows, int64_t K, const void *B, in
     auto kern = gemm2sm_kernel<STAGES, EPI>;
     HEP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES));
     const int grid = sm_count() & ~1;  // whole CTA pairs
+    kern<<<grid, kThreads, S::BYTES, stream>>>(ta, tb, p);
+    HEP_CHECK_LAUNCH();
+    return HEP_OK;
+}
+
+template <int STAGES, int EPI, bool A_MN, bool B_MN>
+static int launch2sm_maps(const CUtensorMap &ta, const CUtensorMap &tb, const Params &p, cudaStream_t stream) {
+    using S = Smem2<STAGES>;
+    auto kern = gemm2sm_kernel<STAGES, EPI, A_MN, B_MN>;
+    HEP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES));
+    const int grid = sm_count() & ~1;
     kern<<<grid, kThreads, S::BYTES, stream>>>(ta, tb, p);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
@@ -1336,8 +1375,11 @@ extern "C" int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, con
     int32_t *mt_row0 = reinterpret_cast<int32_t *>(d_workspace);
     int32_t *mt_rows = mt_row0 + cap;
     int32_t *exp_off = mt_rows + cap;
+    // CTA pairs (256-row tiles, half the operand traffic per SM) on the same rule as the
+    // forward; MN-major operands are two 64-wide boxes per CTA half
+    const bool pairs = use_pairs(Rcap, n_experts) && d_model % 256 == 0 && (2 * ffn) % 256 == 0;
     if ((rc = build_tiles(d_seg, n_seg, n_experts, mt_row0, mt_rows, exp_off, exp_off + n_experts + 1, cap, d_status,
-                          BM, s)))
+                          pairs ? kPairRows : BM, s)))
         return rc;
     CUtensorMap ta, tb;
     Params p{};
@@ -1355,9 +1397,11 @@ extern "C" int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, con
     p.out_cols = 2 * ffn;
     p.aux = const_cast<void *>(d_pre);
     p.ld_aux = 2 * ffn;
-    if ((rc = make_tmap(&ta, d_dy, (uint64_t)Rcap, (uint64_t)d_model, BM))) return rc;
+    if ((rc = make_tmap(&ta, d_dy, (uint64_t)Rcap, (uint64_t)d_model, pairs ? 128 : BM))) return rc;
     if ((rc = make_tmap_mn(&tb, d_w2, (uint64_t)n_experts * d_model, (uint64_t)ffn))) return rc;
-    if ((rc = launch_maps<256, 4, EPI_SWIGLU_BWD, false, true>(ta, tb, p, 0, s))) return rc;
+    if ((rc = pairs ? launch2sm_maps<6, EPI_SWIGLU_BWD, false, true>(ta, tb, p, s)
+                    : launch_maps<256, 4, EPI_SWIGLU_BWD, false, true>(ta, tb, p, 0, s)))
+        return rc;
     if ((rc = hep_moe_zero_padding(d_expert_rows, d_seg, n_seg, n_experts, d_da13, 2 * ffn, stream))) return rc;
     // --- dX_rows = dA13 W13
     p.kblocks = (int)(2 * ffn / BK);
@@ -1367,16 +1411,20 @@ extern "C" int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, con
     p.ld_out = d_model;
     p.out_cols = d_model;
     p.aux = nullptr;
-    if ((rc = make_tmap(&ta, d_da13, (uint64_t)Rcap, (uint64_t)(2 * ffn), BM))) return rc;
+    if ((rc = make_tmap(&ta, d_da13, (uint64_t)Rcap, (uint64_t)(2 * ffn), pairs ? 128 : BM))) return rc;
     if ((rc = make_tmap_mn(&tb, d_w13, (uint64_t)n_experts * 2 * ffn, (uint64_t)d_model))) return rc;
-    if ((rc = launch_maps<256, 4, EPI_BF16, false, true>(ta, tb, p, 0, s))) return rc;
+    if ((rc = pairs ? launch2sm_maps<6, EPI_BF16, false, true>(ta, tb, p, s)
+                    : launch_maps<256, 4, EPI_BF16, false, true>(ta, tb, p, 0, s)))
+        return rc;
     // --- dW2_e = dY_e^T H_e   (fp32, [E][d][F])
     Params q{};
     q.grouped = 2;
     q.exp_rows = d_expert_rows;
     q.n_exp = n_experts;
+    const int tm = pairs ? kPairRows : BM;
+    q.tile_m = pairs ? kPairRows : 0;
     q.M = d_model;
-    q.m_tiles = (int)(d_model / BM);
+    q.m_tiles = (int)(d_model / tm);
     q.n_tiles = (int)(ffn / 256);
     q.out = d_dw2;
     q.ld_out = ffn;
@@ -1384,10 +1432,12 @@ extern "C" int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, con
     q.out_exp_stride = d_model * ffn;
     if ((rc = make_tmap_mn(&ta, d_dy, (uint64_t)Rcap, (uint64_t)d_model))) return rc;
     if ((rc = make_tmap_mn(&tb, d_h, (uint64_t)Rcap, (uint64_t)ffn))) return rc;
-    if ((rc = launch_maps<256, 4, EPI_F32, true, true>(ta, tb, q, 0, s))) return rc;
+    if ((rc = pairs ? launch2sm_maps<6, EPI_F32, true, true>(ta, tb, q, s)
+                    : launch_maps<256, 4, EPI_F32, true, true>(ta, tb, q, 0, s)))
+        return rc;
     // --- dW13_e = dA13_e^T X_e  (fp32, [E][2F][d], W13 interleave)
     q.M = 2 * ffn;
-    q.m_tiles = (int)(2 * ffn / BM);
+    q.m_tiles = (int)(2 * ffn / tm);
     q.n_tiles = (int)(d_model / 256);
     q.out = d_dw13;
     q.ld_out = d_model;
@@ -1395,7 +1445,8 @@ extern "C" int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, con
     q.out_exp_stride = 2 * ffn * d_model;
     if ((rc = make_tmap_mn(&ta, d_da13, (uint64_t)Rcap, (uint64_t)(2 * ffn)))) return rc;
     if ((rc = make_tmap_mn(&tb, d_rows, (uint64_t)Rcap, (uint64_t)d_model))) return rc;
-    return launch_maps<256, 4, EPI_F32, true, true>(ta, tb, q, 0, s);
+    return pairs ? launch2sm_maps<6, EPI_F32, true, true>(ta, tb, q, s)
+                 : launch_maps<256, 4, EPI_F32, true, true>(ta, tb, q, 0, s);
 }
 
 // Router backward: dWg = dlogits^T x (fp32 [E64][d]) and dx_gate = dlogits Wg (bf16 [T][d]);

@@ -93,3 +93,31 @@ def test_autograd_function(P):
     assert x.grad.shape == x.shape and torch.isfinite(x.grad.float()).all()
     assert w13.grad.shape == w13.shape and w2.grad.shape == w2.shape and wg.grad.shape == wg.shape
     assert w13.grad.float().abs().sum() > 0 and wg.grad[:8].float().abs().sum() > 0
+
+
+def test_backward_pair_and_single_cta_agree(P, monkeypatch):
+    """The backward GEMMs (SwiGLU dgrad, dX dgrad, K-ragged weight gradients) on the
+    CTA-pair kernel (256-row tiles, MN-major operand halves) and on the 1-CTA kernel:
+    both within tolerance of fp32 autograd and identical bit for bit (same K order)."""
+    from paper_2511_16947_b200.layer import interleave_w13
+
+    G, E, K, d, F, T, s = 4, 8, 2, 512, 1024, 4096, 1.0
+    pl = P.cayley_symmetric(P.ClusterShape(G, E, 2))
+    bias = torch.tensor(P.zipf_gate_bias(E, s, 0))
+    g = torch.Generator(device="cuda").manual_seed(19)
+    x = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
+    dout = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
+    res = {}
+    for pair in ("0", "1"):
+        monkeypatch.setenv("HEP_FFN_PAIR", pair)
+        layer = P.MoELayer(pl, d, F, K, seed=2, gate_bias=bias, train=True)
+        layer(x)
+        res[pair] = [t.clone() for t in layer.backward_step(x, dout)]
+        torch.cuda.synchronize()
+        layer.check_status()
+    rdx, rwg, rw1, rw3, rw2 = _reference_grads(layer, x, dout, layer.buffers(T).topk_idx)
+    for pair in ("0", "1"):
+        dx, dwg, dw13, dw2 = res[pair]
+        assert _rel(dx, rdx) <= TOL and _rel(dw2, rw2) <= TOL and _rel(dw13, interleave_w13(rw1, rw3)) <= TOL
+    for a, b in zip(res["0"], res["1"]):
+        assert torch.equal(a, b)
