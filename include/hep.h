@@ -284,6 +284,18 @@ int hep_moe_expert_ffn_p2p(const void *d_rows, const void *d_w13, const void *d_
                            int64_t R, int64_t rows_hint, int64_t d_model, int64_t ffn, int n_experts, void *d_h,
                            const uint64_t *d_y_addr, void *d_workspace, size_t workspace_bytes, int32_t *d_status,
                            void *stream);
+/*
+ * Device-side group barrier over peer memory (no host synchronisation; graph-capturable).
+ * d_my_flags: this rank's uint32 [world + 1], zero-initialised, mapped by every peer;
+ * d_peer_flags[i] = rank i's flags array.  Each call arrives (release, system scope) in
+ * slot `rank` of every peer and waits (acquire) until every peer arrived with the same
+ * epoch.  hep_p2p_allgather first stores this rank's `bytes` (multiple of 16) of d_src
+ * at d_peer_dst[i] + rank * bytes of every rank i, then runs the barrier.
+ * Replaces: the dist.barrier / all_gather of the modelled all-to-all (simulator.py:457-463).
+ */
+int hep_p2p_barrier(const uint64_t *d_peer_flags, uint32_t *d_my_flags, int rank, int world, void *stream);
+int hep_p2p_allgather(const void *d_src, int64_t bytes, const uint64_t *d_peer_dst, const uint64_t *d_peer_flags,
+                      uint32_t *d_my_flags, int rank, int world, void *stream);
 /* CUDA IPC plumbing for the peer buffers: 64-byte handle of the allocation holding d_ptr
  * plus d_ptr's byte offset in it (exchanged by the host); open maps the allocation base. */
 int hep_ipc_handle(const void *d_ptr, void *handle_out, int64_t *offset_out);

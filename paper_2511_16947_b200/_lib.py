@@ -72,6 +72,8 @@ SIGNATURES = {
     "hep_moe_dispatch_p2p": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_int, vp, vp, vp]),
     "hep_moe_return_addr": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int64, ctypes.c_int64, vp, vp]),
     "hep_moe_expert_ffn_p2p": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp, vp, vp, ctypes.c_size_t, vp, vp]),
+    "hep_p2p_barrier": (ctypes.c_int, [vp, vp, ctypes.c_int, ctypes.c_int, vp]),
+    "hep_p2p_allgather": (ctypes.c_int, [vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int, ctypes.c_int, vp]),
     "hep_ipc_handle": (ctypes.c_int, [vp, vp, ctypes.POINTER(ctypes.c_int64)]),
     "hep_ipc_open": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_void_p)]),
     "hep_ipc_close": (ctypes.c_int, [vp]),

@@ -96,9 +96,72 @@ __global__ void return_addr_kernel(const int64_t *__restrict__ pair, int me, int
     }
 }
 
+// ---------------------------------------------------------------------------
+// Device-side group barrier (and all-gather) through peer memory, so an EP forward
+// needs no host synchronisation: every rank owns flags[world + 1] (uint32) mapped by
+// every peer; slot r holds the last epoch rank r arrived with, slot `world` this rank's
+// own epoch counter (advanced by the kernel itself, so the launch is graph-capturable).
+// Arrival is a release store at system scope into every peer's slot `rank`, made after
+// the optional payload stores; waiting is an acquire load per peer slot.  Stream order
+// puts the peer stores of earlier kernels (dispatch, the GEMM epilogue) before the
+// release (cumulativity), and every later kernel after the acquire.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void st_release_sys(uint32_t *p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(256) p2p_barrier_kernel(const uint64_t *__restrict__ peer_flags, uint32_t *my_flags,
+                                                          int rank, int world, const int4 *__restrict__ src,
+                                                          int64_t nvec, const uint64_t *__restrict__ peer_dst) {
+    __shared__ uint32_t epoch;
+    if (src)  // all-gather payload: this rank's block into slot `rank` of every peer's buffer
+        for (int i = 0; i < world; ++i) {
+            int4 *dst = reinterpret_cast<int4 *>(peer_dst[i]) + (int64_t)rank * nvec;
+            for (int64_t v = threadIdx.x; v < nvec; v += blockDim.x) dst[v] = src[v];
+        }
+    if (threadIdx.x == 0) {
+        epoch = my_flags[world] + 1;
+        my_flags[world] = epoch;
+    }
+    __syncthreads();  // payload stores of every thread precede thread i's release below
+    __threadfence_system();
+    if (threadIdx.x < world)
+        st_release_sys(reinterpret_cast<uint32_t *>(peer_flags[threadIdx.x]) + rank, epoch);
+    if (threadIdx.x < world)
+        while ((int32_t)(ld_acquire_sys(my_flags + threadIdx.x) - epoch) < 0) __nanosleep(64);
+    __syncthreads();
+}
+
 }  // namespace hep
 
 using namespace hep;
+
+extern "C" int hep_p2p_barrier(const uint64_t *d_peer_flags, uint32_t *d_my_flags, int rank, int world, void *stream) {
+    HEP_REQUIRE(d_peer_flags && d_my_flags, HEP_E_CONTRACT, "hep_p2p_barrier: null pointer");
+    HEP_REQUIRE(world >= 1 && world <= HEP_MAX_GPUS && rank >= 0 && rank < world, HEP_E_DIMENSION,
+                "hep_p2p_barrier: rank %d of %d", rank, world);
+    p2p_barrier_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(d_peer_flags, d_my_flags, rank, world, nullptr, 0, nullptr);
+    HEP_CHECK_LAUNCH();
+    return HEP_OK;
+}
+
+extern "C" int hep_p2p_allgather(const void *d_src, int64_t bytes, const uint64_t *d_peer_dst,
+                                 const uint64_t *d_peer_flags, uint32_t *d_my_flags, int rank, int world,
+                                 void *stream) {
+    HEP_REQUIRE(d_src && d_peer_dst && d_peer_flags && d_my_flags, HEP_E_CONTRACT, "hep_p2p_allgather: null pointer");
+    HEP_REQUIRE(world >= 1 && world <= HEP_MAX_GPUS && rank >= 0 && rank < world && bytes >= 0 && bytes % 16 == 0,
+                HEP_E_DIMENSION, "hep_p2p_allgather: rank %d of %d, %lld bytes (multiple of 16)", rank, world,
+                (long long)bytes);
+    p2p_barrier_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(d_peer_flags, d_my_flags, rank, world,
+                                                            (const int4 *)d_src, bytes / 16, d_peer_dst);
+    HEP_CHECK_LAUNCH();
+    return HEP_OK;
+}
 
 extern "C" int hep_moe_dispatch_p2p(const void *d_x, const int32_t *d_tok_row, int64_t T, int K, int64_t d_model,
                                     int rank, int num_gpus, const int64_t *d_pair, const uint64_t *d_peer_recv,

@@ -58,6 +58,10 @@ def _offsets(counts):
 class LocalComm:
     """The G ranks of the group live in this process (lists indexed by rank)."""
 
+    # every driven rank's kernels run in launch order on one stream: a device-side
+    # barrier between them would wait for a rank whose kernels are queued behind it
+    device_sync = False
+
     def __init__(self, world: int):
         self.world = world
 
@@ -95,9 +99,13 @@ class LocalComm:
 class DistComm:
     """This process is one rank; collectives through torch.distributed."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, device_sync: bool = True):
+        """device_sync: the NVLink exchange synchronises the ranks with device-side
+        barriers / all-gathers through peer memory (hep_p2p_barrier / hep_p2p_allgather,
+        no host involvement) instead of a stream drain + dist.barrier."""
         import torch.distributed as dist
 
+        self.device_sync = device_sync
         self.dist = dist
         self.group = group
         self.world = dist.get_world_size(group)
@@ -212,7 +220,7 @@ class EPRank:
                 logits=torch.empty(T, layer.e_pad, dtype=torch.float32, device=dev),
                 topk_idx=torch.empty(T, K, **i32),
                 topk_w=torch.empty(T, K, dtype=torch.float32, device=dev),
-                hist=torch.zeros(1, E, dtype=torch.int64, device=dev),
+                hist_buf=torch.zeros(E + (E & 1), dtype=torch.int64, device=dev),  # 16-byte rows
                 tok_row=torch.empty(T, K, **i32),
                 seg=torch.empty(n_seg, 4, **i32),
                 counts=torch.empty(2 * G, dtype=torch.int64, device=dev),
@@ -220,6 +228,7 @@ class EPRank:
                 send=torch.empty(max(T * K, 1), layer.d, dtype=torch.bfloat16, device=dev),
                 out=torch.empty(T, layer.d, dtype=torch.bfloat16, device=dev),
             )
+            b["hist"] = b["hist_buf"][:E].view(1, E)
             self.bufs[T] = b
         return b
 
@@ -301,6 +310,26 @@ class EPMoELayer:
             self._peer_tables[T] = tab
         return tab
 
+    def _sync_table(self) -> list:
+        """Device-side synchronisation state per driven rank (built once): flags [G + 1]
+        uint32 and the gathered histogram hist_all [G][E2] int64, both mapped by every
+        peer, with device tables of the peers' addresses."""
+        if getattr(self, "_sync", None) is None:
+            G, E2 = self.G, self.E + (self.E & 1)
+            flags = [torch.zeros(G + 1, dtype=torch.int32, device=self.device) for _ in self.ranks]
+            hall = [torch.zeros(G, E2, dtype=torch.int64, device=self.device) for _ in self.ranks]
+            pf = self.comm.exchange_ptrs([f.data_ptr() for f in flags])
+            ph = self.comm.exchange_ptrs([h.data_ptr() for h in hall])
+            self._sync = [(f, h, torch.tensor(a, dtype=torch.int64, device=self.device),
+                           torch.tensor(b, dtype=torch.int64, device=self.device))
+                          for f, h, a, b in zip(flags, hall, pf, ph)]
+        return self._sync
+
+    def _device_barrier(self, s) -> None:
+        L = _lib.lib()
+        for rk, (flags, _, pflags, _) in zip(self.ranks, self._sync_table()):
+            _lib.check(L.hep_p2p_barrier(pflags.data_ptr(), flags.data_ptr(), rk.rank, self.G, s), "hep_p2p_barrier")
+
     def _forward_p2p(self, xs, st, ev):
         """Forward with both exchanges as NVLink peer stores: the dispatch kernel writes
         rows into the destination ranks' receive buffers, the down-projection GEMM's
@@ -321,11 +350,22 @@ class EPMoELayer:
             ck(L.hep_router_topk(x.data_ptr(), self.wg.data_ptr(), T, d, E, self.e_pad, _lib.ptr(self.gate_bias), K,
                                  T, 1, b["logits"].data_ptr(), b["topk_idx"].data_ptr(), b["topk_w"].data_ptr(),
                                  b["hist"].data_ptr(), None, s), "hep_router_topk")
-        hists = self.comm.all_gather([b["hist"] for b in bs])
+        sync = getattr(self.comm, "device_sync", False)
+        if sync:  # histogram rows straight into every peer's hist_all, then a device barrier
+            E2 = E + (E & 1)
+            hists = []
+            for rk, b, (flags, hall, pflags, phall) in zip(self.ranks, bs, self._sync_table()):
+                ck(L.hep_p2p_allgather(b["hist_buf"].data_ptr(), 8 * E2, phall.data_ptr(), pflags.data_ptr(),
+                                       flags.data_ptr(), rk.rank, G, s), "hep_p2p_allgather")
+                hists.append(hall)
+            hist_stride = E2
+        else:
+            hists = self.comm.all_gather([b["hist"] for b in bs])
+            hist_stride = E
         for rk, x, b, h, (p_recv, p_back) in zip(self.ranks, xs, bs, hists, tabs):
             T = x.shape[0]
-            b["hist_all"] = h
-            ck(L.hep_sched_solve(rk.sched.handle, h.data_ptr(), 1, E, None, HEP_SCHED_ALL,
+            b["hist_all"] = h[:, :E]  # [G][E] view (device-gathered rows are padded to even E)
+            ck(L.hep_sched_solve(rk.sched.handle, h.data_ptr(), 1, hist_stride, None, HEP_SCHED_ALL,
                                  ctypes.byref(rk.sched.out), s), "hep_sched_solve")
             ck(L.hep_moe_assign_ep(rk.sched.handle, ctypes.byref(rk.sched.out), b["topk_idx"].data_ptr(), T, K,
                                    rk.rank, b["tok_row"].data_ptr(), b["seg"].data_ptr(), b["counts"].data_ptr(),
@@ -334,7 +374,10 @@ class EPMoELayer:
                                       rk.sched.transfer.data_ptr(), p_recv.data_ptr(), s), "hep_moe_dispatch_p2p")
             ck(L.hep_moe_return_addr(rk.sched.transfer.data_ptr(), rk.rank, G, p_back.data_ptr(), d * 2, b["cap"],
                                      b["y_addr"].data_ptr(), s), "hep_moe_return_addr")
-        self.comm.barrier()  # every receive buffer complete
+        if sync:
+            self._device_barrier(s)  # every receive buffer complete
+        else:
+            self.comm.barrier()
         if "ffn" in ev:
             ev["ffn"][0].record(st)
         for rk, b, x in zip(self.ranks, bs, xs):
@@ -348,7 +391,10 @@ class EPMoELayer:
                                             rk.sched.status.data_ptr(), s), "hep_moe_expert_ffn_p2p")
         if "ffn" in ev:
             ev["ffn"][1].record(st)
-        self.comm.barrier()  # every expert output back at its source
+        if sync:
+            self._device_barrier(s)  # every expert output back at its source
+        else:
+            self.comm.barrier()
         outs = []
         for x, b in zip(xs, bs):
             T = x.shape[0]
