@@ -276,6 +276,26 @@ def run_ep(args, world, rank, local, dev):
                 layer.forward([x])
             torch.cuda.synchronize()
     stream = torch.cuda.current_stream()
+    # the NVLink exchange with device-side barriers has no host synchronisation in the
+    # step: capture it as one CUDA graph per rank (the barrier epochs advance on the device)
+    graph = None
+    if args.exchange == "p2p" and comm.device_sync and not args.eager:
+        try:
+            side = torch.cuda.Stream(device=dev)
+            side.wait_stream(stream)
+            torch.cuda.synchronize()
+            dist.barrier()
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=side):
+                layer.forward([x], stream=side)
+            torch.cuda.synchronize()
+            dist.barrier()
+            for _ in range(2):
+                graph.replay()
+            torch.cuda.synchronize()
+        except Exception as exc:  # eager launches are the same kernels
+            print(f"[bench] rank {rank}: CUDA graph capture failed ({exc}); timing eager launches", file=sys.stderr)
+            graph = None
     dist.barrier()
     torch.cuda.synchronize()
     sampler = ClockSampler(local) if rank == 0 else None
@@ -284,7 +304,10 @@ def run_ep(args, world, rank, local, dev):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for _ in range(args.steps):
-        layer.forward([x])
+        if graph is not None:
+            graph.replay()
+        else:
+            layer.forward([x])
     e1.record(stream)
     torch.cuda.synchronize()
     if sampler:
@@ -326,6 +349,8 @@ def run_ep(args, world, rank, local, dev):
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": CONFIG_TEXT[args.config], "tokens_per_microbatch_per_gpu": T, "ep": world,
                        "top_k": K, "d_model": d, "ffn": F, "experts": E, "zipf_s": args.skew, "pass": "forward",
+                       "launch": ("cuda-graph replay (device-side barriers, no host sync)" if graph is not None
+                                  else "eager"),
                        "exchange": (("NVLink peer stores: dispatch kernel -> peers' receive buffers, down-projection "
                                      "epilogue -> sources' return buffers (CUDA IPC); histogram all-gather + 2 barriers")
                                     if args.exchange == "p2p" else

@@ -186,7 +186,18 @@ def _p2p_worker(rank, world, port, q):
         layer = EPMoELayer(pl, d, F, K, DistComm(), [rank], seed=7, gate_bias=bias, exchange="p2p")
         outs = [layer.forward([x])[0].clone() for _ in range(2)]
         torch.cuda.synchronize()
-        q.put((rank, outs[0].float().cpu().numpy(), outs[1].float().cpu().numpy()))  # pickled by value
+        # the device-synchronised step has no host sync: capture it as a CUDA graph and replay
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        dist.barrier()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            out_g = layer.forward([x], stream=side)[0]
+        torch.cuda.synchronize()
+        dist.barrier()
+        g.replay()
+        torch.cuda.synchronize()
+        q.put((rank, outs[0].float().cpu().numpy(), out_g.float().cpu().numpy()))  # pickled by value
     except Exception as exc:  # report instead of hanging the parent
         q.put((rank, repr(exc), None))
     finally:
@@ -194,8 +205,9 @@ def _p2p_worker(rank, world, port, q):
 
 
 def test_ep_p2p_over_cuda_ipc_two_processes(P):
-    """One process per rank (both on this GPU), peer buffers mapped with CUDA IPC:
-    the NVLink-path forward equals the in-process reference bit for bit."""
+    """One process per rank (both on this GPU), peer buffers mapped with CUDA IPC and the
+    ranks synchronised by device-side barriers: the NVLink-path forward — eager, and
+    replayed from a CUDA graph — equals the in-process reference bit for bit."""
     import socket
 
     import torch.multiprocessing as mp
