@@ -315,11 +315,18 @@ def run_ep(args, world, rank, local, dev):
     dist.barrier()
     # FFN share (roofline): a few extra steps with events around the expert GEMMs
     n_f = min(args.steps, 10)
-    fev = [{"ffn": (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))} for _ in range(n_f)]
+    fev = [{k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in ("ffn", "a2a")}
+           for _ in range(n_f)]
     for i in range(n_f):
         layer.forward([x], events=fev[i])
     torch.cuda.synchronize()
     ffn_ms = statistics.mean(f["ffn"][0].elapsed_time(f["ffn"][1]) for f in fev)
+    a2a_ms = _max_over_ranks(statistics.mean(f["a2a"][0].elapsed_time(f["a2a"][1]) for f in fev), dev)
+    # bytes this rank sends to other ranks per step (its transfer-plan row minus the local part)
+    pair = layer.ranks[0].sched.transfer[: G * G].view(G, G).cpu()
+    sent_rows = int(pair[rank].sum().item() - pair[rank, rank].item())
+    a2a_bytes = sent_rows * d * 2
+    a2a_gbs = -_max_over_ranks(-(a2a_bytes / (a2a_ms / 1e3) / 1e9), dev)  # slowest rank
     R = int(layer.ranks[0].bufs[T]["counts"][G:].sum().item())  # rows this rank received (outside the timing)
     ffn_tf = 6.0 * d * F * R / (ffn_ms / 1e3) / 1e12
     min_tf = -_max_over_ranks(-ffn_tf, dev)
@@ -365,6 +372,14 @@ def run_ep(args, world, rank, local, dev):
                          "min_over_ranks": min_tf, "rows_rank0": R,
                          "peak_source": f"{peak_src} bf16_tflops_sustained", "traffic": None},
             "clocks": sampler.summary() if sampler else None,
+            # dispatch exchange: bytes each rank sends to other ranks / the exchange's event time
+            # (p2p: the dispatch kernel storing into the peers' receive buffers, permute included;
+            # NCCL: the all-to-all-v), against NVLink 5's 900 GB/s per direction per GPU
+            "a2a": {"kind": "dispatch (" + ("NVLink peer stores" if args.exchange == "p2p" else "NCCL all-to-all-v") + ")",
+                    "GB/s": a2a_gbs, "bytes_per_step_rank0": a2a_bytes, "ms": a2a_ms,
+                    "frac_of_nvlink": a2a_gbs / 900.0, "nvlink_GB/s": 900.0,
+                    "note": ("all ranks share one GPU (protocol check): not an NVLink figure"
+                             if args.dist_backend == "gloo" else "max over ranks of the exchange time")},
         }))
     dist.destroy_process_group()
 

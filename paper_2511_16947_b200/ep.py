@@ -290,8 +290,9 @@ class EPMoELayer:
     @torch.no_grad()
     def forward(self, xs: list[torch.Tensor], stream=None, events: dict | None = None) -> list[torch.Tensor]:
         """xs[i] = [T][d] bf16 tokens of rank self.ranks[i]; returns their outputs.
-        ``events`` optionally maps "ffn" to a (start, end) torch.cuda.Event pair
-        recorded around the expert FFN launches."""
+        ``events`` optionally maps "ffn" (the expert FFN launches) and "a2a" (the dispatch
+        exchange: the peer-store dispatch kernel, or the NCCL all-to-all-v) to a
+        (start, end) torch.cuda.Event pair."""
         st = stream if stream is not None else torch.cuda.current_stream()
         with torch.cuda.stream(st):
             if self.exchange == "p2p":
@@ -370,8 +371,12 @@ class EPMoELayer:
             ck(L.hep_moe_assign_ep(rk.sched.handle, ctypes.byref(rk.sched.out), b["topk_idx"].data_ptr(), T, K,
                                    rk.rank, b["tok_row"].data_ptr(), b["seg"].data_ptr(), b["counts"].data_ptr(),
                                    b["assign_ws"].data_ptr(), b["assign_ws"].numel(), s), "hep_moe_assign_ep")
+            if "a2a" in ev:
+                ev["a2a"][0].record(st)
             ck(L.hep_moe_dispatch_p2p(x.data_ptr(), b["tok_row"].data_ptr(), T, K, d, rk.rank, G,
                                       rk.sched.transfer.data_ptr(), p_recv.data_ptr(), s), "hep_moe_dispatch_p2p")
+            if "a2a" in ev:
+                ev["a2a"][1].record(st)
             ck(L.hep_moe_return_addr(rk.sched.transfer.data_ptr(), rk.rank, G, p_back.data_ptr(), d * 2, b["cap"],
                                      b["y_addr"].data_ptr(), s), "hep_moe_return_addr")
         if sync:
@@ -431,8 +436,12 @@ class EPMoELayer:
         counts = [b["counts"].cpu().tolist() for b in bs]
         send_counts = [c[:G] for c in counts]
         recv_counts = [c[G:] for c in counts]
+        if "a2a" in ev:
+            ev["a2a"][0].record(st)
         recvs = self.comm.all_to_all([b["send"][: sum(sc)] for b, sc in zip(bs, send_counts)], send_counts,
                                      recv_counts)
+        if "a2a" in ev:
+            ev["a2a"][1].record(st)
         ys = []
         if "ffn" in ev:
             ev["ffn"][0].record(st)
