@@ -41,6 +41,7 @@
 namespace hep {
 
 constexpr int kSchedThreads = 256;
+constexpr int kSchedSmemMax = 227 * 1024 - 1024;  // opt-in dynamic shared memory per block, minus the static arrays
 constexpr int kProfSlots = 16;
 __device__ long long g_sched_prof[kProfSlots];
 
@@ -76,7 +77,7 @@ struct SchedSmem {
     uint32_t *mask;     // [E]
     int4 *emeta;        // [E] (arc base, #arcs, group mask, load*Q when it fits 32 bits)
     int8_t *kidx;       // [E*G] list position of GPU g in expert e's group, -1 if absent
-    int32_t *rc;        // [2*E*G] per-(expert, source) range counts: phase 1, final merge
+    int16_t *rc;        // [2*E*G] per-(expert, source) range counts: phase 1, final merge (<= 3d + 2G)
 };
 
 __host__ __device__ inline size_t align8(size_t x) { return (x + 7) & ~size_t(7); }
@@ -86,7 +87,7 @@ __host__ __device__ inline size_t sched_smem_bytes(int G, int E, int nnz) {
     return align8(8 * (size_t)E) + 2 * align8(8 * ns) + align8(8 * (size_t)E * G) + 2 * align8(8 * (size_t)nnz) +
            align8(8 * (size_t)G) + align8(8 * (size_t)G * G) + align8(8 * (kSchedThreads / 32 + 2)) + 64 +
            align8(4 * (size_t)(E + 1)) + 3 * align8(4 * (size_t)nnz) + align8(4 * (size_t)E) + 16 * (size_t)E +
-           align8((size_t)E * G) + 8 * (size_t)E * G;
+           align8((size_t)E * G) + 4 * (size_t)E * G;
 }
 
 __device__ inline SchedSmem carve(char *p, int G, int E, int nnz) {
@@ -109,7 +110,7 @@ __device__ inline SchedSmem carve(char *p, int G, int E, int nnz) {
     s.arc_gpu = (int32_t *)p; p += align8(4 * (size_t)nnz);
     s.mask = (uint32_t *)p; p += align8(4 * (size_t)E);
     s.kidx = (int8_t *)p; p += align8((size_t)E * G);
-    s.rc = (int32_t *)p;
+    s.rc = (int16_t *)p;
     return s;
 }
 
@@ -634,13 +635,18 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
         const bool topo = (a.flags & HEP_SCHED_TOPO) && a.gpn > 0 && a.gpn < G;
         // pass 0: range counts (one thread per (expert, source); per expert for topology routing)
         int64_t *ecount = s.totals;  // totals are no longer needed once the plan exists
-        int32_t *rc1 = s.rc, *rc2 = s.rc + E * G;
+        int16_t *rc1 = s.rc, *rc2 = s.rc + E * G;
         const bool per_expert = !topo && E >= nt / 4;  // enough experts to fill the block
         if (!topo) {
             if (per_expert) {
-                for (int e = tid; e < E; e += nt) rc1[e * G] = route_expert_merge<false>(a, s, e, 0);
+                for (int e = tid; e < E; e += nt) rc1[e * G] = (int16_t)route_expert_merge<false>(a, s, e, 0);
             } else {
-                for (int i = tid; i < E * G; i += nt) route_pair<false>(a, s, i / G, i % G, &rc1[i], &rc2[i], 0, 0);
+                for (int i = tid; i < E * G; i += nt) {
+                    int c1, c2;
+                    route_pair<false>(a, s, i / G, i % G, &c1, &c2, 0, 0);
+                    rc1[i] = (int16_t)c1;
+                    rc2[i] = (int16_t)c2;
+                }
             }
             for (int e = tid; e < E; e += nt) {  // _check_plan (router.py:97-111)
                 const int b = s.grp_off[e], n = s.grp_off[e + 1] - b;
@@ -805,8 +811,8 @@ static int launch_sched(hep_sched *h, SchedArgs &a, cudaStream_t stream) {
     a.mask = h->d_mask;
     a.kidx = h->d_kidx;
     const size_t smem = sched_smem_bytes(h->G, h->E, h->nnz);
-    HEP_REQUIRE(smem <= 200 * 1024, HEP_E_CAPACITY, "scheduler shared memory %zu B exceeds 200 KB (E=%d G=%d)", smem,
-                h->E, h->G);
+    HEP_REQUIRE(smem <= kSchedSmemMax, HEP_E_CAPACITY, "scheduler shared memory %zu B exceeds %d B (E=%d G=%d)", smem,
+                kSchedSmemMax, h->E, h->G);
     switch (h->G <= 5 ? 1 : (1 << (h->G - 5))) {
         case 1: return launch_spl<1>(h, a, smem, stream);
         case 2: return launch_spl<2>(h, a, smem, stream);

@@ -219,3 +219,42 @@ def test_pipelined_split_layer(P, ratio, kind):
                                                        b.topk_idx.cpu().numpy(), T // G)
     assert n_rows == T * K
     assert np.array_equal(b.tok_row.cpu().numpy(), tok_row)
+
+
+@pytest.mark.parametrize("G,E,K,d,F,T,case", [
+    (8, 1024, 16, 256, 128, 2048, "max_experts_topk"),  # E and K at the ABI limits (unfused gate path)
+    (10, 20, 3, 256, 128, 1000, "max_gpus_ragged"),     # G = HEP_MAX_GPUS, T not a multiple of 64/128
+    (4, 8, 2, 256, 128, 4, "one_token_per_source"),
+    (8, 64, 4, 256, 128, 2048, "all_tokens_to_k_experts"),  # every other expert empty
+])
+def test_edge_cases_against_oracle(P, G, E, K, d, F, T, case):
+    """Edge cases of the path, whole layer against the oracle: routing, histogram,
+    schedule and token->row map bit-exact, outputs within the bf16 tolerance."""
+    from oracle import layer_ref
+
+    shape = P.ClusterShape(G, E, 2)
+    pl = (P.cayley_symmetric(shape) if (E & (E - 1)) == 0 and (G & (G - 1)) == 0
+          else P.placement.symmetric_placement(shape))
+    if case == "all_tokens_to_k_experts":
+        bias = torch.full((E,), -30.0)
+        bias[3:3 + K] = 30.0
+    else:
+        bias = torch.tensor(P.zipf_gate_bias(E, 1.0, 0))
+    layer = P.MoELayer(pl, d, F, K, seed=4, gate_bias=bias)
+    x = torch.randn(T, d, generator=torch.Generator(device="cuda").manual_seed(21), device="cuda").to(torch.bfloat16)
+    out = layer(x).float().cpu().numpy()
+    torch.cuda.synchronize()
+    layer.check_status()
+    b = layer.buffers(T)
+    ref = layer_ref.layer_forward(
+        x.float().cpu().numpy(), b.logits[:, :E].cpu().numpy(), K, [tuple(g) for g in pl.edp_groups], G,
+        layer.w1.float().cpu().numpy(), layer.w2.float().cpu().numpy(), layer.w3.float().cpu().numpy(),
+        bias=bias.numpy())
+    assert np.array_equal(b.topk_idx.cpu().numpy(), ref["topk_idx"])
+    assert np.array_equal(b.hist.cpu().numpy(), ref["hist"])
+    assert layer.sched.rows(layer.sched.xi) == ref["sched"]["xi"]
+    assert np.array_equal(b.tok_row.cpu().numpy(), ref["tok_row"])
+    if case == "all_tokens_to_k_experts":
+        assert int((b.hist.sum(dim=0) > 0).sum()) == K
+    rel = np.abs(out - ref["out"]).max() / np.abs(ref["out"]).max()
+    assert rel <= 1e-2, rel
