@@ -206,7 +206,8 @@ int hep_moe_assign(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_t
                    int64_t *d_expert_rows, void *workspace, size_t workspace_bytes, void *stream);
 size_t hep_moe_assign_workspace(hep_sched_t h, int64_t T, int K);
 /* hep_moe_assign with the chunk counts already in the workspace (written by
- * hep_router_topk's epilogue at byte offset hep_moe_assign_chunk_offset). */
+ * hep_router_topk's epilogue at byte offset hep_moe_assign_chunk_offset); the counts
+ * are left intact, so the call is repeatable on the same micro-batch. */
 int hep_moe_assign_precounted(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_topk_idx, int64_t T, int K,
                               int64_t tokens_per_src, int row_align, int32_t *d_tok_row, int32_t *d_row_tok,
                               int32_t *d_seg, int64_t *d_expert_rows, void *workspace, size_t workspace_bytes,

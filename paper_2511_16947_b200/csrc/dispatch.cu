@@ -30,7 +30,8 @@ struct AssignWs {
     int32_t *es_end;    // [E*G*G] rank end (exclusive) of each range, table order
     int32_t *es_delta;  // [E*G*G] row - rank of each range
     int32_t *first;     // [E+1] first range index of expert e (-1 = none)
-    int32_t *chunk_cnt; // [n_src * n_chunks * E]
+    int32_t *chunk_cnt; // [n_src * n_chunks * E] per-chunk expert counts (router-written when precounted)
+    int32_t *chunk_pre; // [n_src * n_chunks * E] their exclusive prefix over chunks (the counts stay intact)
     int32_t *cnt3;      // [E*G*G] range count of (expert, src, dst)   (EP rank view)
     int32_t *sbase;     // [E*G]   send-buffer base of (expert, dst)   (EP rank view)
     int32_t *es_lo;     // [E*G]   first rank of (e, src) in this phase (pipelined split)
@@ -47,7 +48,7 @@ static size_t assign_ws_bytes(const hep_sched *h, int64_t T, int n_src, int64_t 
     b += align256(4 * (size_t)(E * G * G));
     b += align256(4 * (size_t)(E * G * G));
     b += align256(4 * (size_t)(E + 1));
-    b += align256(4 * (size_t)(n_src * ncs * E));
+    b += 2 * align256(4 * (size_t)(n_src * ncs * E));
     b += align256(4 * (size_t)(E * G * G));
     b += align256(4 * (size_t)(E * G));
     b += align256(4 * (size_t)(E * G));
@@ -65,6 +66,7 @@ static AssignWs carve_ws(const hep_sched *h, void *ws, int n_src, int64_t tps) {
     w.es_delta = (int32_t *)p; p += align256(4 * (size_t)(E * G * G));
     w.first = (int32_t *)p; p += align256(4 * (size_t)(E + 1));
     w.chunk_cnt = (int32_t *)p; p += align256(4 * (size_t)(n_src * ((tps + kChunk - 1) / kChunk) * E));
+    w.chunk_pre = (int32_t *)p; p += align256(4 * (size_t)(n_src * ((tps + kChunk - 1) / kChunk) * E));
     w.cnt3 = (int32_t *)p; p += align256(4 * (size_t)(E * G * G));
     w.sbase = (int32_t *)p; p += align256(4 * (size_t)(E * G));
     w.es_lo = (int32_t *)p;
@@ -188,29 +190,29 @@ __global__ void chunk_count_kernel(const int32_t *topk_idx, int K, int E, int64_
 // exclusive prefix over a source's chunks, one warp per (src, expert): 32 chunks per
 // step, all loads of a step in flight together (the serial walk was a chain of
 // dependent L2 round trips)
-__global__ void chunk_scan_kernel(int n_src, int ncs, int E, int32_t *chunk_cnt) {
+__global__ void chunk_scan_kernel(int n_src, int ncs, int E, const int32_t *chunk_cnt, int32_t *chunk_pre) {
     const int id = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
     if (id >= n_src * E) return;
     const int src = id / E, e = id % E;
     int32_t run = 0;
     for (int c0 = 0; c0 < ncs; c0 += 32) {
         const int c = c0 + lane;
-        int32_t *p = chunk_cnt + ((int64_t)src * ncs + c) * E + e;
-        const int32_t v = c < ncs ? *p : 0;
+        const int64_t at = ((int64_t)src * ncs + c) * E + e;
+        const int32_t v = c < ncs ? chunk_cnt[at] : 0;
         int32_t inc = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const int32_t y = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= o) inc += y;
         }
-        if (c < ncs) *p = run + inc - v;
+        if (c < ncs) chunk_pre[at] = run + inc - v;
         run += __shfl_sync(0xffffffffu, inc, 31);
     }
 }
 
 // one warp per chunk; lanes k < K own pick k of each token (distinct experts)
 __global__ void chunk_map_kernel(const int32_t *topk_idx, int K, int E, int G, int64_t tps, int64_t T, int ncs,
-                                 const int32_t *chunk_cnt, AssignWs w, int32_t *tok_row, int32_t *row_tok,
+                                 const int32_t *chunk_pre, AssignWs w, int32_t *tok_row, int32_t *row_tok,
                                  int src_base, bool windowed) {
     extern __shared__ int32_t sm[];
     int32_t *ctr = sm;                // [E]
@@ -224,7 +226,7 @@ __global__ void chunk_map_kernel(const int32_t *topk_idx, int K, int E, int G, i
     // stage this source's range lists with the whole block, independent loads (all G
     // slots of every expert; slots past es_cnt are never read)
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
-        ctr[e] = chunk_cnt[(int64_t)blockIdx.x * E + e];
+        ctr[e] = chunk_pre[(int64_t)blockIdx.x * E + e];
         const int es = e * G + src_base + src;
         l_cnt[e] = w.es_cnt[es];
         if (windowed) l_lo[e] = w.es_lo[es];
@@ -488,12 +490,12 @@ static int assign_impl(hep_sched_t h, const hep_sched_out *sched, bool windowed,
                                                                   w.chunk_cnt);
         HEP_CHECK_LAUNCH();
     }
-    chunk_scan_kernel<<<(n_src * E + 7) / 8, 256, 0, s>>>(n_src, ncs, E, w.chunk_cnt);
+    chunk_scan_kernel<<<(n_src * E + 7) / 8, 256, 0, s>>>(n_src, ncs, E, w.chunk_cnt, w.chunk_pre);
     HEP_CHECK_LAUNCH();
     const size_t sm = sizeof(int32_t) * (3 * (size_t)E + 2 * (size_t)E * G + (size_t)kChunk * K);
     HEP_REQUIRE(sm <= 200 * 1024, HEP_E_CAPACITY, "chunk_map smem %zu", sm);
     if (sm > 48 * 1024) HEP_CHECK_CUDA(cudaFuncSetAttribute(chunk_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    chunk_map_kernel<<<nblk, 256, sm, s>>>(d_topk_idx, K, E, G, tokens_per_src, T, ncs, w.chunk_cnt, w, d_tok_row,
+    chunk_map_kernel<<<nblk, 256, sm, s>>>(d_topk_idx, K, E, G, tokens_per_src, T, ncs, w.chunk_pre, w, d_tok_row,
                                            d_row_tok, 0, windowed);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
@@ -624,13 +626,13 @@ extern "C" int hep_moe_assign_ep(hep_sched_t h, const hep_sched_out *sched, cons
     const int ncs = (int)((tps + kChunk - 1) / kChunk);
     chunk_count_kernel<<<ncs, 128, E * sizeof(int32_t), s>>>(d_topk_idx, K, E, tps, T, ncs, w.chunk_cnt);
     HEP_CHECK_LAUNCH();
-    chunk_scan_kernel<<<(E + 7) / 8, 256, 0, s>>>(1, ncs, E, w.chunk_cnt);
+    chunk_scan_kernel<<<(E + 7) / 8, 256, 0, s>>>(1, ncs, E, w.chunk_cnt, w.chunk_pre);
     HEP_CHECK_LAUNCH();
     const size_t sm = sizeof(int32_t) * (3 * (size_t)E + 2 * (size_t)E * G + (size_t)kChunk * K);
     HEP_REQUIRE(sm <= 200 * 1024, HEP_E_CAPACITY, "chunk_map smem %zu", sm);
     if (sm > 48 * 1024)
         HEP_CHECK_CUDA(cudaFuncSetAttribute(chunk_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    chunk_map_kernel<<<ncs, 256, sm, s>>>(d_topk_idx, K, E, G, tps, T, ncs, w.chunk_cnt, w, d_tok_row, nullptr, rank,
+    chunk_map_kernel<<<ncs, 256, sm, s>>>(d_topk_idx, K, E, G, tps, T, ncs, w.chunk_pre, w, d_tok_row, nullptr, rank,
                                           false);
     HEP_CHECK_LAUNCH();
     return HEP_OK;

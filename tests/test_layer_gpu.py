@@ -258,3 +258,24 @@ def test_edge_cases_against_oracle(P, G, E, K, d, F, T, case):
         assert int((b.hist.sum(dim=0) > 0).sum()) == K
     rel = np.abs(out - ref["out"]).max() / np.abs(ref["out"]).max()
     assert rel <= 1e-2, rel
+
+
+def test_assignment_is_repeatable(P):
+    """hep_moe_assign_precounted leaves the router's chunk counts intact: re-running the
+    assignment on the same micro-batch reproduces the token->row map (regression: the
+    chunk scan used to overwrite the counts in place)."""
+    import ctypes
+
+    from paper_2511_16947_b200 import _lib
+
+    layer, x, out, b, ref, pl = _run(P, G=8, E=16, K=2, d=256, F=256, T=4096, s=0.5, seed=4)
+    first = b.tok_row.clone()
+    L = _lib.lib()
+    for _ in range(3):
+        _lib.check(L.hep_moe_assign_precounted(layer.sched.handle, ctypes.byref(layer.sched.out),
+                                               b.topk_idx.data_ptr(), 4096, 2, 4096 // 8, b.row_align,
+                                               b.tok_row.data_ptr(), b.row_tok.data_ptr(), b.seg.data_ptr(),
+                                               b.expert_rows.data_ptr(), b.assign_ws.data_ptr(), b.assign_ws.numel(),
+                                               _lib.stream_handle()), "assign")
+    torch.cuda.synchronize()
+    assert torch.equal(b.tok_row, first)
