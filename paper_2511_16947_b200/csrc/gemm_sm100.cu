@@ -92,6 +92,7 @@ struct Params {
     const int32_t *gather_idx;
     int32_t gather_oob;
     int tile_m;    // modes 0 / 2: rows per m-tile (0 = BM; 256 on the CTA pair)
+    int light_first;  // grouped: weights of single-m-tile experts loaded evict-first
     int clk_slot;  // > 0: CTA 0 stamps (clock64, globaltimer) at entry and exit into g_gemm_clk[clk_slot - 1]
 };
 
@@ -544,6 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t pol_a = p.pol_mode ? pick_policy(p.pol_mode & 3) : (p.grouped ? policy_evict_last() : policy_evict_first());
             // weights are shared by the concurrently running m-tiles of one (expert, N-block): normal priority
             const uint64_t pol_b = p.pol_mode ? pick_policy((p.pol_mode >> 2) & 3) : (p.grouped ? policy_evict_normal() : policy_evict_last());
+            const uint64_t pol_first = policy_evict_first();
             uint32_t phase = 0;
             for (int64_t t = blockIdx.x; t < n_total; t += gridDim.x) {
                 const Tile tl = decode(p, t, s_off);
@@ -552,6 +554,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // weight (mode 1) is [K][N] per expert, stacked along K
                 const int32_t a_k0 = (int32_t)tl.k0;
                 const int32_t b_k0 = p.grouped == 2 ? (int32_t)tl.k0 : (B_MN ? b_row - tl.n_blk * BN : 0);
+                // an expert with a single m-tile streams its weights once: keep them out of L2's way
+                const bool light = p.light_first && p.grouped == 1 && s_off[tl.expert + 1] - s_off[tl.expert] == 1;
                 for (int k = 0; k < tl.kb; ++k) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
@@ -569,7 +573,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                             tma_load_2d_hint(sB + stage * S::B_BYTES + i * 8192, &tmB, &full[stage],
                                              tl.n_blk * BN + 64 * i, b_k0 + k * BK, pol_b);
                     } else {
-                        tma_load_2d_hint(sB + stage * S::B_BYTES, &tmB, &full[stage], k * BK, b_row, pol_b);
+                        tma_load_2d_hint(sB + stage * S::B_BYTES, &tmB, &full[stage], k * BK, b_row,
+                                         light ? pol_first : pol_b);
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -759,6 +764,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             // ===================== TMA producer (both CTAs) =====================
             const uint64_t pol_a = p.pol_mode ? pick_policy(p.pol_mode & 3) : policy_evict_last();
             const uint64_t pol_b = p.pol_mode ? pick_policy((p.pol_mode >> 2) & 3) : policy_evict_normal();
+            const uint64_t pol_first = policy_evict_first();
             const uint32_t full_l = mapa_shared(smem_u32(&full[0]), 0);  // leader's full[0]
             int stage = 0;
             uint32_t phase = 0;
@@ -771,6 +777,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 const int32_t a_k0 = (int32_t)tl.k0;
                 const int32_t b_k0 = p.grouped == 2 ? (int32_t)tl.k0 : (int32_t)(tl.expert * p.b_rows_per_exp);
                 const int32_t b_mn = tl.n_blk * BN + (int32_t)rank * 128;
+                // an expert with a single m-tile streams its weights once: keep them out of L2's way
+                const bool light = p.light_first && p.grouped == 1 && s_off[tl.expert + 1] - s_off[tl.expert] == 1;
                 for (int k = 0; k < tl.kb; ++k) {
                     mbar_wait_cluster(&empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * S::STAGE_BYTES);
@@ -788,7 +796,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                             tma_load_2d_2sm(sB + stage * S::B_BYTES + i * 8192, &tmB, full_l + 8 * stage, b_mn + 64 * i,
                                             b_k0 + k * BK, pol_b);
                     } else {
-                        tma_load_2d_2sm(sB + stage * S::B_BYTES, &tmB, full_l + 8 * stage, k * BK, b_row, pol_b);
+                        tma_load_2d_2sm(sB + stage * S::B_BYTES, &tmB, full_l + 8 * stage, k * BK, b_row,
+                                        light ? pol_first : pol_b);
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -1300,6 +1309,11 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
     Params p{};
     p.grouped = 1;
     p.pol_mode = pol_mode;
+    // experts whose rows fit one m-tile stream their weights exactly once: load them
+    // evict-first so they do not push the reused panels of the other experts out of L2
+    // (DeepSeek-V3 shape 13.36 -> 12.87 ms, Qwen3 2.06 -> 2.00 ms; HEP_LIGHT_FIRST=0 disables)
+    const char *lf_env = getenv("HEP_LIGHT_FIRST");
+    p.light_first = lf_env ? atoi(lf_env) : 1;
     const char *clk_env = getenv("HEP_FFN_CLOCK");
     const bool clk = clk_env && clk_env[0] == '1';
     p.clk_slot = clk ? 1 : 0;
