@@ -164,7 +164,7 @@ int hep_gate_topk(const float *d_logits, int64_t ld_logits, const float *d_bias,
  * are computed without the logits leaving the SM.
  *   d_x [T][d_model] bf16, d_wg [e_pad][d_model] bf16 (rows >= E zero), e_pad % 16 == 0
  *   d_logits [T][e_pad] fp32 or NULL (written when given; required when e_pad > 256 or
- *   K not in {1,2,4,6,8}, which take the unfused hep_gemm_bf16 + hep_gate_topk path)
+ *   K > 8, which take the unfused hep_gemm_bf16 + hep_gate_topk path)
  *   d_chunk_cnt: NULL, or the per-64-token-chunk expert counts hep_moe_assign_precounted
  *   consumes ([n_src][ceil(tps/64)][E] int32 at hep_moe_assign_chunk_offset of its
  *   workspace); fused into the epilogue when tokens_per_src % 64 == 0

@@ -627,13 +627,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
             if constexpr (EPI == EPI_GATE) {
                 if (half == 0) {
+#define HEP_GATE_K(KK) \
+    case KK: gate_tile<KK>(p, t_row, tl.row0, tl.rows, row_in_tile, s_hist, s_chunk, s_bias, BN); break;
                     switch (p.gate.K) {  // the insertion network is unrolled per K
-                        case 1: gate_tile<1>(p, t_row, tl.row0, tl.rows, row_in_tile, s_hist, s_chunk, s_bias, BN); break;
-                        case 2: gate_tile<2>(p, t_row, tl.row0, tl.rows, row_in_tile, s_hist, s_chunk, s_bias, BN); break;
-                        case 4: gate_tile<4>(p, t_row, tl.row0, tl.rows, row_in_tile, s_hist, s_chunk, s_bias, BN); break;
-                        case 6: gate_tile<6>(p, t_row, tl.row0, tl.rows, row_in_tile, s_hist, s_chunk, s_bias, BN); break;
-                        default: gate_tile<8>(p, t_row, tl.row0, tl.rows, row_in_tile, s_hist, s_chunk, s_bias, BN); break;
+                        HEP_GATE_K(1) HEP_GATE_K(2) HEP_GATE_K(3) HEP_GATE_K(4)
+                        HEP_GATE_K(5) HEP_GATE_K(6) HEP_GATE_K(7) default: gate_tile<8>(p, t_row, tl.row0, tl.rows, row_in_tile, s_hist, s_chunk, s_bias, BN); break;
                     }
+#undef HEP_GATE_K
                 }
             } else {
                 const bool valid = row_in_tile < tl.rows;
@@ -1195,9 +1195,9 @@ extern "C" int hep_router_topk(const void *d_x, const void *d_wg, int64_t T, int
     HEP_REQUIRE(tokens_per_src >= 1 && n_src >= 1 && tokens_per_src * n_src >= T, HEP_E_DIMENSION,
                 "hep_router_topk: tokens_per_src * n_src < T");
     cudaStream_t s = (cudaStream_t)stream;
-    const bool fused = e_pad <= kGateMaxE && (K == 1 || K == 2 || K == 4 || K == 6 || K == 8) && n_src <= kGateMaxSrc;
+    const bool fused = e_pad <= kGateMaxE && K <= kGateMaxK && n_src <= kGateMaxSrc;
     if (!fused) {  // unfused: logits through HBM, then the gate kernel (both still on the device)
-        HEP_REQUIRE(d_logits, HEP_E_CONTRACT, "hep_router_topk: E_pad > 256 / K not in {1,2,4,6,8} needs d_logits");
+        HEP_REQUIRE(d_logits, HEP_E_CONTRACT, "hep_router_topk: E_pad > 256 / K > 8 needs d_logits");
         int rc = hep_gemm_bf16(d_x, d_wg, d_logits, T, e_pad, d_model, HEP_OUT_F32, stream);
         if (rc) return rc;
         rc = hep_gate_topk(d_logits, e_pad, d_bias, T, E, K, tokens_per_src, n_src, d_topk_idx, d_topk_w, d_hist, stream);
