@@ -93,6 +93,7 @@ struct Params {
     int32_t gather_oob;
     int tile_m;    // modes 0 / 2: rows per m-tile (0 = BM; 256 on the CTA pair)
     int light_first;  // grouped: weights of single-m-tile experts loaded evict-first
+    int k_split;      // mode 0: contraction split into k_split ranges, partial s -> out + s*out_exp_stride
     int clk_slot;  // > 0: CTA 0 stamps (clock64, globaltimer) at entry and exit into g_gemm_clk[clk_slot - 1]
 };
 
@@ -136,7 +137,7 @@ struct Tile {
 
 __device__ __forceinline__ int64_t total_tiles(const Params &p) {
     const int tm = p.tile_m ? p.tile_m : BM;
-    if (p.grouped == 0) return ((p.M + tm - 1) / tm) * p.n_tiles;
+    if (p.grouped == 0) return ((p.M + tm - 1) / tm) * p.n_tiles * (p.k_split > 1 ? p.k_split : 1);
     if (p.grouped == 2) return (int64_t)p.n_exp * p.m_tiles * p.n_tiles;
     return (int64_t)p.exp_mt_off[p.n_exp] * p.n_tiles;
 }
@@ -161,6 +162,16 @@ __device__ __forceinline__ Tile decode(const Params &p, int64_t t, const int32_t
     if (p.grouped == 0) {
         const int64_t mt = (p.M + tm - 1) / tm;
         tl.expert = 0;
+        if (p.k_split > 1) {  // split-K: partial s of every output tile, over k-blocks [s*kps, ...)
+            const int64_t per = mt * p.n_tiles;
+            const int sp = (int)(t / per);
+            t -= (int64_t)sp * per;
+            const int kps = (p.kblocks + p.k_split - 1) / p.k_split;
+            tl.expert = sp;
+            tl.k0 = (int64_t)sp * kps * BK;
+            tl.kb = min(kps, p.kblocks - sp * kps);
+            if (tl.kb < 0) tl.kb = 0;
+        }
         tl.n_blk = (int)(t / mt);
         const int64_t m = t % mt;
         tl.row0 = (int32_t)(m * tm);
@@ -554,7 +565,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // contraction offsets: mode 2 contracts over the expert's rows; an MN-major
                 // weight (mode 1) is [K][N] per expert, stacked along K
                 const int32_t a_k0 = (int32_t)tl.k0;
-                const int32_t b_k0 = p.grouped == 2 ? (int32_t)tl.k0 : (B_MN ? b_row - tl.n_blk * BN : 0);
+                const int32_t b_k0 = (p.grouped == 2 || p.k_split > 1) ? (int32_t)tl.k0
+                                                                       : (B_MN ? b_row - tl.n_blk * BN : 0);
                 // an expert with a single m-tile streams its weights once: keep them out of L2's way
                 const bool light = p.light_first && p.grouped == 1 && s_off[tl.expert + 1] - s_off[tl.expert] == 1;
                 for (int k = 0; k < tl.kb; ++k) {
@@ -590,7 +602,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int64_t t = blockIdx.x; t < n_total; t += gridDim.x) {
-                const int tkb = p.grouped == 2 ? decode(p, t, s_off).kb : kb;
+                const int tkb = (p.grouped == 2 || p.k_split > 1) ? decode(p, t, s_off).kb : kb;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
@@ -814,7 +826,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int64_t t = cid; t < n_total; t += ncl) {
-                const int tkb = p.grouped == 2 ? decode(p, t, s_off).kb : kb;
+                const int tkb = (p.grouped == 2 || p.k_split > 1) ? decode(p, t, s_off).kb : kb;
                 mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
@@ -1464,6 +1476,21 @@ extern "C" int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, con
                  : launch_maps<256, 4, EPI_F32, true, true>(ta, tb, q, 0, s);
 }
 
+// split-K reduction: out[i] = sum_s part[s][i], s ascending (deterministic)
+__global__ void splitk_reduce_kernel(const float4 *__restrict__ part, int S, int64_t n4, float4 *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+        float4 a = part[i];
+        for (int sp = 1; sp < S; ++sp) {
+            const float4 b = part[(int64_t)sp * n4 + i];
+            a.x += b.x;
+            a.y += b.y;
+            a.z += b.z;
+            a.w += b.w;
+        }
+        out[i] = a;
+    }
+}
+
 // Router backward: dWg = dlogits^T x (fp32 [E64][d]) and dx_gate = dlogits Wg (bf16 [T][d]);
 // dlogits is bf16 [T][E64], Wg is [E64][d] (E64 = experts padded to 64), T % 64 == 0.
 extern "C" int hep_router_bwd(const void *d_x, const void *d_wg, const void *d_dlogits, int64_t T, int64_t d_model,
@@ -1483,9 +1510,28 @@ extern "C" int hep_router_bwd(const void *d_x, const void *d_wg, const void *d_d
     p.out = d_dwg;
     p.ld_out = d_model;
     p.out_cols = d_model;
+    // dWg has only ceil(E64/128) x d/256 output tiles but a T-long contraction: split the
+    // contraction so every SM works (fp32 partials staged in the dx_gate buffer, which the
+    // second GEMM overwrites afterwards, then summed in split order — deterministic)
+    const int64_t tiles = (E64 + BM - 1) / BM * p.n_tiles;
+    int S = (int)(sm_count() / (tiles > 0 ? tiles : 1));
+    const int64_t cap_split = T / (2 * (int64_t)E64);  // S x E64 x d fp32 must fit in T x d bf16
+    if (S > cap_split) S = (int)cap_split;
+    if (S > p.kblocks) S = p.kblocks;
+    if (S > 1) {
+        p.k_split = S;
+        p.out = d_dxg;
+        p.out_exp_stride = (int64_t)E64 * d_model;
+    }
     if ((rc = make_tmap_mn(&ta, d_dlogits, (uint64_t)T, (uint64_t)E64))) return rc;
     if ((rc = make_tmap_mn(&tb, d_x, (uint64_t)T, (uint64_t)d_model))) return rc;
-    if ((rc = launch_maps<256, 4, EPI_F32, true, true>(ta, tb, p, (E64 + BM - 1) / BM * p.n_tiles, s))) return rc;
+    if ((rc = launch_maps<256, 4, EPI_F32, true, true>(ta, tb, p, tiles * (S > 1 ? S : 1), s))) return rc;
+    if (S > 1) {
+        const int64_t n4 = (int64_t)E64 * d_model / 4;
+        splitk_reduce_kernel<<<(unsigned)((n4 + 255) / 256 < 4 * 148 ? (n4 + 255) / 256 : 4 * 148), 256, 0, s>>>(
+            reinterpret_cast<const float4 *>(d_dxg), S, n4, reinterpret_cast<float4 *>(d_dwg));
+        HEP_CHECK_LAUNCH();
+    }
     Params q{};
     q.grouped = 0;
     q.M = T;

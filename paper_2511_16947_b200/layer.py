@@ -344,7 +344,7 @@ class MoELayer(torch.nn.Module):
                                 dx.data_ptr(), s), "hep_moe_gather_sum")
         return dx, dwg[:E], dw13, dw2
 
-    LAUNCHES_PER_BACKWARD = 13  # combine_bwd, zero_pad x2, tiles x2, 4 GEMMs, gate_bwd, 2 router GEMMs, gather
+    LAUNCHES_PER_BACKWARD = 14  # combine_bwd, zero_pad x2, tiles x2, 4 GEMMs, gate_bwd, 2 router GEMMs (+ split-K sum), gather
 
 
 class MoEFunction(torch.autograd.Function):
