@@ -56,6 +56,7 @@ struct SchedArgs {
     const int64_t *base;
     const int64_t *xi_in;  // route-only: caller plan (global)
     int status_in;         // keep an error already in out.d_status (set by a preceding kernel)
+    int lexmin_warps;      // warps on the lex-min arc chain (8 = whole block, 4)
     hep_sched_out out;
 };
 
@@ -162,20 +163,21 @@ __device__ __forceinline__ int64_t floordiv(int64_t v, int64_t d) {
 // same decision to its subsets.  Result of arc p (position in (expert, gpu id)
 // order) goes to vtmp[p].  U = uint32_t when every slack and load fits 32 bits.
 // ---------------------------------------------------------------------------
-template <typename U>
+template <typename U, int NW = kSchedThreads / 32>
 __device__ __forceinline__ U block_min(U v, U (*red)[kSchedThreads / 32], int &par) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     v = wmin(v);
     if (lane == 0) red[par][w] = v;
-    __syncthreads();
+    if constexpr (NW == kSchedThreads / 32) __syncthreads();
+    else asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
     U m = red[par][0];
 #pragma unroll
-    for (int i = 1; i < kSchedThreads / 32; ++i) m = red[par][i] < m ? red[par][i] : m;
+    for (int i = 1; i < NW; ++i) m = red[par][i] < m ? red[par][i] : m;
     par ^= 1;
     return m;
 }
 
-template <int SPB, typename U>
+template <int SPB, typename U, int NT = kSchedThreads>
 __device__ void lexmin_block(const SchedArgs &a, SchedSmem &s, int64_t *vtmp) {
     __shared__ U red[2][kSchedThreads / 32];
     const int tid = threadIdx.x;
@@ -187,7 +189,7 @@ __device__ void lexmin_block(const SchedArgs &a, SchedSmem &s, int64_t *vtmp) {
     uint32_t valid = 0;
 #pragma unroll
     for (int j = 0; j < SPB; ++j) {
-        const uint32_t S = tid + kSchedThreads * j;
+        const uint32_t S = tid + NT * j;
         sl[j] = S < NS ? (U)(s.C[S] - s.W[S] * Q) : (U)0;
         valid |= (S < NS) << j;
     }
@@ -212,11 +214,11 @@ __device__ void lexmin_block(const SchedArgs &a, SchedSmem &s, int64_t *vtmp) {
             U mn = UMAX;
 #pragma unroll
             for (int j = 0; j < SPB; ++j) {
-                const uint32_t S = tid + kSchedThreads * j;
+                const uint32_t S = tid + NT * j;
                 const bool ok = ((valid >> j) & 1) && ((S >> gc) & 1) && !((S >> ga) & 1);
                 mn = (ok && sl[j] < mn) ? sl[j] : mn;
             }
-            mn = block_min(mn, red, par);
+            mn = block_min<U, NT / 32>(mn, red, par);
             const U v_a = r > mn ? r - mn : (U)0;
             const U v_c = r - v_a;
             if (tid == 0) {
@@ -225,7 +227,7 @@ __device__ void lexmin_block(const SchedArgs &a, SchedSmem &s, int64_t *vtmp) {
             }
 #pragma unroll
             for (int j = 0; j < SPB; ++j) {
-                const uint32_t S = tid + kSchedThreads * j;
+                const uint32_t S = tid + NT * j;
                 const uint32_t ha = (S >> ga) & 1, hc = (S >> gc) & 1;
                 sl[j] -= (ha & ~hc) ? v_a : ((hc & ~ha) ? v_c : (U)0);
             }
@@ -234,7 +236,7 @@ __device__ void lexmin_block(const SchedArgs &a, SchedSmem &s, int64_t *vtmp) {
         if (r) {
 #pragma unroll
             for (int j = 0; j < SPB; ++j) {
-                const uint32_t S = tid + kSchedThreads * j;
+                const uint32_t S = tid + NT * j;
                 sl[j] += ((S & R) == R) ? r : (U)0;  // expert e leaves the not-yet-processed set
             }
         }
@@ -251,11 +253,11 @@ __device__ void lexmin_block(const SchedArgs &a, SchedSmem &s, int64_t *vtmp) {
                 U mn = UMAX;
 #pragma unroll
                 for (int j = 0; j < SPB; ++j) {
-                    const uint32_t S = tid + kSchedThreads * j;
+                    const uint32_t S = tid + NT * j;
                     const bool ok = ((valid >> j) & 1) && ((S & need) == need) && !(S & gbit);
                     mn = (ok && sl[j] < mn) ? sl[j] : mn;
                 }
-                mn = block_min(mn, red, par);
+                mn = block_min<U, NT / 32>(mn, red, par);
                 v = r > mn ? r - mn : (U)0;
             }
             if (tid == 0) vtmp[b + k] = (int64_t)v;
@@ -264,7 +266,7 @@ __device__ void lexmin_block(const SchedArgs &a, SchedSmem &s, int64_t *vtmp) {
             if (v) {
 #pragma unroll
                 for (int j = 0; j < SPB; ++j) {
-                    const uint32_t S = tid + kSchedThreads * j;
+                    const uint32_t S = tid + NT * j;
                     sl[j] -= (S & gbit) ? v : (U)0;  // capacity of every subset holding g drops by v
                 }
             }
@@ -560,8 +562,17 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
             const bool fits32 = (__int128)G * (total_all + 1) * a.Q < ((__int128)1 << 31) &&
                                 (__int128)G * (mQ + 1) < ((__int128)1 << 31);
             constexpr int SPB = SPL >= 8 ? SPL / 8 : 1;  // subsets per thread (2^G / 256)
-            if (fits32) lexmin_block<SPB, uint32_t>(a, s, s.xi);
-            else lexmin_block<SPB, uint64_t>(a, s, s.xi);
+            constexpr int SPB4 = SPL >= 4 ? SPL / 4 : 1;  // ... with 4 warps (2^G / 128)
+            if (a.lexmin_warps == 4) {  // half the block: fewer warps meet at each arc's barrier
+                if (threadIdx.x < 128) {
+                    if (fits32) lexmin_block<SPB4, uint32_t, 128>(a, s, s.xi);
+                    else lexmin_block<SPB4, uint64_t, 128>(a, s, s.xi);
+                }
+            } else if (fits32) {
+                lexmin_block<SPB, uint32_t>(a, s, s.xi);
+            } else {
+                lexmin_block<SPB, uint64_t>(a, s, s.xi);
+            }
         }
         __syncthreads();
         for (int p = tid; p < nnz; p += nt) {  // (expert, gpu id) order -> EDP list order
@@ -799,6 +810,10 @@ static int launch_spl(hep_sched *h, const SchedArgs &a, size_t smem, cudaStream_
 }
 
 static int launch_sched(hep_sched *h, SchedArgs &a, cudaStream_t stream) {
+    // lex-min arc chain on 4 warps (2 subsets per thread, named barrier): 93.4K vs 97.6K
+    // cycles at E=256 (8 warps), 97.7K on 2 warps; HEP_SCHED_LEXMIN_WARPS=8 for the whole block
+    const char *lw = getenv("HEP_SCHED_LEXMIN_WARPS");
+    a.lexmin_warps = lw ? atoi(lw) : 4;
     a.G = h->G;
     a.E = h->E;
     a.nnz = h->nnz;
