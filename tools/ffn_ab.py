@@ -2,7 +2,7 @@
 energy per launch (the FFN-heavy configs run power-capped, so joules per step
 decide the achieved clock).
 
-    python tools/ffn_ab.py --config dsv3 --variants "HEP_FFN_LIGHT=0;HEP_FFN_LIGHT=1" [--iters 30 --rounds 4]
+    python tools/ffn_ab.py --config dsv3 --variants "HEP_FFN_PAIR=0;HEP_FFN_PAIR=1" [--iters 30 --rounds 4]
 
 The layer is built and placed as in bench.py (Zipf s=1 gate bias; adaptive
 replacement when it beats Cayley), one forward fills the receive rows, then
@@ -26,7 +26,7 @@ sys.path.insert(0, ROOT)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="dsv3")
-    ap.add_argument("--variants", default="HEP_FFN_LIGHT=1")
+    ap.add_argument("--variants", default="HEP_FFN_PAIR=1")
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--rounds", type=int, default=4)
     ap.add_argument("--skew", type=float, default=1.0)
