@@ -19,7 +19,6 @@ device.
 
 from __future__ import annotations
 
-import ctypes
 import io
 from dataclasses import dataclass
 
@@ -27,7 +26,7 @@ import numpy as np
 
 from . import _lib
 from .core import ContractViolation, DimensionError, LoadMatrix, Placement, ReplicaLoadPlan, Topology
-from .scheduler import HEP_SCHED_TOPO, HEP_SCHED_TRANSFER, MAX_GPUS, CapacityError, device_scheduler
+from .scheduler import HEP_SCHED_TOPO, MAX_GPUS, CapacityError, device_scheduler
 
 
 @dataclass(frozen=True)

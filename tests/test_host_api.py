@@ -7,7 +7,6 @@ import os
 import re
 from fractions import Fraction
 
-import numpy as np
 import pytest
 
 from conftest import ROOT, load_golden

@@ -17,7 +17,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import statistics
 import sys
 import time
 
@@ -33,7 +32,6 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     args = ap.parse_args()
 
-    import numpy as np
     import torch
 
     import ctypes
