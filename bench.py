@@ -312,6 +312,7 @@ def run_ep(args, world, rank, local, dev):
     torch.cuda.synchronize()
     if sampler:
         sampler.__exit__()
+    layer.check_sync()
     dist.barrier()
     # FFN share (roofline): a few extra steps with events around the expert GEMMs
     n_f = min(args.steps, 10)

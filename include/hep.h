@@ -287,7 +287,8 @@ int hep_moe_expert_ffn_p2p(const void *d_rows, const void *d_w13, const void *d_
                            void *stream);
 /*
  * Device-side group barrier over peer memory (no host synchronisation; graph-capturable).
- * d_my_flags: this rank's uint32 [world + 1], zero-initialised, mapped by every peer;
+ * d_my_flags: this rank's uint32 [world + 2], zero-initialised, mapped by every peer
+ * (slot world + 1 becomes 1 if a wait gave up after ~10 s: a peer never arrived);
  * d_peer_flags[i] = rank i's flags array.  Each call arrives (release, system scope) in
  * slot `rank` of every peer and waits (acquire) until every peer arrived with the same
  * epoch.  hep_p2p_allgather first stores this rank's `bytes` (multiple of 16) of d_src

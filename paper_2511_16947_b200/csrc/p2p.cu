@@ -132,8 +132,20 @@ __global__ void __launch_bounds__(256) p2p_barrier_kernel(const uint64_t *__rest
     __threadfence_system();
     if (threadIdx.x < world)
         st_release_sys(reinterpret_cast<uint32_t *>(peer_flags[threadIdx.x]) + rank, epoch);
-    if (threadIdx.x < world)
-        while ((int32_t)(ld_acquire_sys(my_flags + threadIdx.x) - epoch) < 0) __nanosleep(64);
+    if (threadIdx.x < world) {
+        // a peer that never arrives (dead rank, broken mapping) must not hang the GPU: give up
+        // after ~10 s and raise the sticky flag in slot world + 1 (checked by the host)
+        uint64_t t0, t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        while ((int32_t)(ld_acquire_sys(my_flags + threadIdx.x) - epoch) < 0) {
+            __nanosleep(64);
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            if (t - t0 > 10000000000ull) {
+                atomicExch(my_flags + world + 1, 1u);
+                break;
+            }
+        }
+    }
     __syncthreads();
 }
 

@@ -312,12 +312,13 @@ class EPMoELayer:
         return tab
 
     def _sync_table(self) -> list:
-        """Device-side synchronisation state per driven rank (built once): flags [G + 1]
-        uint32 and the gathered histogram hist_all [G][E2] int64, both mapped by every
-        peer, with device tables of the peers' addresses."""
+        """Device-side synchronisation state per driven rank (built once): flags [G + 2]
+        uint32 (arrival epochs, own epoch counter, timeout flag) and the gathered histogram
+        hist_all [G][E2] int64, both mapped by every peer, with device tables of the
+        peers' addresses."""
         if getattr(self, "_sync", None) is None:
             G, E2 = self.G, self.E + (self.E & 1)
-            flags = [torch.zeros(G + 1, dtype=torch.int32, device=self.device) for _ in self.ranks]
+            flags = [torch.zeros(G + 2, dtype=torch.int32, device=self.device) for _ in self.ranks]
             hall = [torch.zeros(G, E2, dtype=torch.int64, device=self.device) for _ in self.ranks]
             pf = self.comm.exchange_ptrs([f.data_ptr() for f in flags])
             ph = self.comm.exchange_ptrs([h.data_ptr() for h in hall])
@@ -325,6 +326,12 @@ class EPMoELayer:
                            torch.tensor(b, dtype=torch.int64, device=self.device))
                           for f, h, a, b in zip(flags, hall, pf, ph)]
         return self._sync
+
+    def check_sync(self) -> None:
+        """Raise if a device-side barrier of this layer gave up waiting for a peer."""
+        for flags, _, _, _ in getattr(self, "_sync", None) or []:
+            if int(flags[self.G + 1].item()):
+                raise RuntimeError("EP device barrier timed out: a peer rank never arrived")
 
     def _device_barrier(self, s) -> None:
         L = _lib.lib()

@@ -197,6 +197,7 @@ def _p2p_worker(rank, world, port, q):
         dist.barrier()
         g.replay()
         torch.cuda.synchronize()
+        layer.check_sync()
         q.put((rank, outs[0].float().cpu().numpy(), out_g.float().cpu().numpy()))  # pickled by value
     except Exception as exc:  # report instead of hanging the parent
         q.put((rank, repr(exc), None))
