@@ -250,6 +250,22 @@ def run_ep(args, world, rank, local, dev):
     comm = DistComm()
     layer = EPMoELayer(pl, d, F, K, comm, [rank], seed=0, gate_bias=bias, device=dev, exchange=args.exchange)
     x = torch.randn(T, d, generator=torch.Generator(device=dev).manual_seed(1000 + rank), device=dev).to(torch.bfloat16)
+    ok = 1
+    try:  # the NVLink path maps the peers' buffers with CUDA IPC; fall back to NCCL if that is refused
+        layer.forward([x])
+        torch.cuda.synchronize()
+    except Exception as exc:  # noqa: BLE001 - any mapping/launch failure of the peer path
+        if args.exchange != "p2p":
+            raise
+        print(f"[bench] rank {rank}: NVLink peer exchange unavailable ({exc}); using NCCL all-to-all-v",
+              file=sys.stderr)
+        ok = 0
+    if args.exchange == "p2p":
+        flag = torch.tensor([ok], device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0:  # every rank switches together
+            args.exchange = "nccl"
+            layer = EPMoELayer(pl, d, F, K, comm, [rank], seed=0, gate_bias=bias, device=dev, exchange="nccl")
     for _ in range(args.warmup):
         layer.forward([x])
     torch.cuda.synchronize()
