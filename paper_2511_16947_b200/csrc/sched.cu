@@ -196,7 +196,7 @@ __device__ void lexmin_block(const SchedArgs &a, SchedSmem &s, int64_t *vtmp) {
     int par = 0;
     int4 nxt = s.emeta[0];
     for (int e = 0; e < E; ++e) {
-        const int b = nxt.x, n = nxt.y;
+        const int b = nxt.x, n = nxt.y & 0xff, ga2 = (nxt.y >> 8) & 0xff, gc2 = (nxt.y >> 16) & 0xff;
         uint32_t R = (uint32_t)nxt.z;
         U r = sizeof(U) == 4 ? (U)(uint32_t)nxt.w : (U)(s.totals[e] * Q);
         if (e + 1 < E) nxt = s.emeta[e + 1];  // prefetch the next expert
@@ -210,7 +210,7 @@ __device__ void lexmin_block(const SchedArgs &a, SchedSmem &s, int64_t *vtmp) {
             // arc a's family {S : c ∈ S, a ∉ S} never contains R, so it sees the slack
             // before the "+r on S ⊇ R" step; the net update afterwards is -v_a on
             // S ∋ a, S ∌ c and -v_c on S ∋ c, S ∌ a (S ⊇ R: +r - v_a - v_c = 0).
-            const int ga = s.arc_gpu[b], gc = s.arc_gpu[b + 1];
+            const int ga = ga2, gc = gc2;
             U mn = UMAX;
 #pragma unroll
             for (int j = 0; j < SPB; ++j) {
@@ -551,9 +551,12 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
                 s.C[S] = c;
             }
         }
-        for (int e = tid; e < E; e += nt)
-            s.emeta[e] = make_int4(s.grp_off[e], s.grp_off[e + 1] - s.grp_off[e], (int)s.mask[e],
-                                   (int)(uint32_t)(s.totals[e] * a.Q));
+        for (int e = tid; e < E; e += nt) {
+            // .y = #arcs | first two arc GPUs << 8 / << 16 (the d = 2 step reads no arc table)
+            const int b = s.grp_off[e], n = s.grp_off[e + 1] - b;
+            const int y = n | (n >= 2 ? (s.arc_gpu[b] << 8) | (s.arc_gpu[b + 1] << 16) : 0);
+            s.emeta[e] = make_int4(b, y, (int)s.mask[e], (int)(uint32_t)(s.totals[e] * a.Q));
+        }
         __syncthreads();
         prof_mark(a.flags, 2);
         // ---- step 4: lex-min canonical plan ------------------------------------
