@@ -170,16 +170,22 @@ __device__ __forceinline__ U block_min(U v, U (*red)[kSchedThreads / 32], int &p
     if (lane == 0) red[par][w] = v;
     if constexpr (NW == kSchedThreads / 32) __syncthreads();
     else asm volatile("bar.sync 1, %0;" ::"n"(NW * 32) : "memory");
-    U m = red[par][0];
+    U m;
+    if constexpr (sizeof(U) == 4 && NW == 4) {  // the four partials in one 16-byte load
+        const uint4 q = *reinterpret_cast<const uint4 *>(red[par]);
+        m = (U)min(min(q.x, q.y), min(q.z, q.w));
+    } else {
+        m = red[par][0];
 #pragma unroll
-    for (int i = 1; i < NW; ++i) m = red[par][i] < m ? red[par][i] : m;
+        for (int i = 1; i < NW; ++i) m = red[par][i] < m ? red[par][i] : m;
+    }
     par ^= 1;
     return m;
 }
 
 template <int SPB, typename U, int NT = kSchedThreads>
 __device__ void lexmin_block(const SchedArgs &a, SchedSmem &s, int64_t *vtmp) {
-    __shared__ U red[2][kSchedThreads / 32];
+    __shared__ __align__(16) U red[2][kSchedThreads / 32];
     const int tid = threadIdx.x;
     const int E = a.E;
     const uint32_t NS = 1u << a.G;
