@@ -83,9 +83,15 @@ struct SchedSmem {
 
 __host__ __device__ inline size_t align8(size_t x) { return (x + 7) & ~size_t(7); }
 
+// Row stride (int64 elements) of the staged load matrix: odd, so the per-expert rows that
+// one warp reads together (thread = expert in the routing passes) fall into different
+// shared-memory banks instead of the 16-way conflict of a G = 8 stride.
+__host__ __device__ inline int loads_stride(int G) { return G | 1; }
+
 __host__ __device__ inline size_t sched_smem_bytes(int G, int E, int nnz) {
     const size_t ns = size_t(1) << G;
-    return align8(8 * (size_t)E) + 2 * align8(8 * ns) + align8(8 * (size_t)E * G) + 2 * align8(8 * (size_t)nnz) +
+    return align8(8 * (size_t)E) + 2 * align8(8 * ns) + align8(8 * (size_t)E * loads_stride(G)) +
+           2 * align8(8 * (size_t)nnz) +
            align8(8 * (size_t)G) + align8(8 * (size_t)G * G) + align8(8 * (kSchedThreads / 32 + 2)) + 64 +
            align8(4 * (size_t)(E + 1)) + 3 * align8(4 * (size_t)nnz) + align8(4 * (size_t)E) + 16 * (size_t)E +
            align8((size_t)E * G) + 4 * (size_t)E * G;
@@ -98,7 +104,7 @@ __device__ inline SchedSmem carve(char *p, int G, int E, int nnz) {
     s.totals = (int64_t *)p; p += align8(8 * (size_t)E);
     s.W = (int64_t *)p; p += align8(8 * ns);
     s.C = (int64_t *)p; p += align8(8 * ns);
-    s.loads = (int64_t *)p; p += align8(8 * (size_t)E * G);
+    s.loads = (int64_t *)p; p += align8(8 * (size_t)E * loads_stride(G));
     s.xq = (int64_t *)p; p += align8(8 * (size_t)nnz);
     s.xi = (int64_t *)p; p += align8(8 * (size_t)nnz);
     s.gpu_load = (int64_t *)p; p += align8(8 * (size_t)G);
@@ -290,7 +296,7 @@ __device__ void route_pair(const SchedArgs &a, SchedSmem &s, int e, int src, int
                            int64_t pos2) {
     const int G = a.G;
     const int b = s.grp_off[e], n = s.grp_off[e + 1] - b;
-    const int64_t *L = s.loads + (size_t)e * G;
+    const int64_t *L = s.loads + (size_t)e * loads_stride(G);
     const int8_t *kx = s.kidx + (size_t)e * G;
     auto rem_of = [&](int g) -> int64_t {
         const int kk = kx[g];
@@ -341,7 +347,7 @@ template <bool EMIT>
 __device__ int route_expert_merge(const SchedArgs &a, SchedSmem &s, int e, int64_t pos) {
     const int G = a.G;
     const int b = s.grp_off[e], n = s.grp_off[e + 1] - b;
-    const int64_t *L = s.loads + (size_t)e * G;
+    const int64_t *L = s.loads + (size_t)e * loads_stride(G);
     const int8_t *kx = s.kidx + (size_t)e * G;
     int cnt = 0;
     auto emit = [&](int src, int dst, int64_t y) {
@@ -393,7 +399,7 @@ __device__ int route_expert_topo(const SchedArgs &a, SchedSmem &s, int e, int64_
     const int b = s.grp_off[e], n = s.grp_off[e + 1] - b;
     int64_t rin[HEP_MAX_GPUS], rx[HEP_MAX_GPUS];
     int64_t tot = 0, xs = 0;
-    for (int g = 0; g < G; ++g) { rin[g] = s.loads[e * G + g]; rx[g] = 0; tot += rin[g]; }
+    for (int g = 0; g < G; ++g) { rin[g] = s.loads[e * loads_stride(G) + g]; rx[g] = 0; tot += rin[g]; }
     if (n == 0 && tot == 0) return 0;
     bool neg = false;
     for (int k = 0; k < n; ++k) {
@@ -468,7 +474,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
             const int e = i / G, g = i - e * G;
             const int64_t v = a.loads[(int64_t)e * a.se + (int64_t)g * a.sg];
             bad |= v < 0;
-            s.loads[i] = v;
+            s.loads[e * loads_stride(G) + g] = v;
         }
     }
     for (int i = tid; i < G * G; i += nt) s.pair[i] = 0;
@@ -480,7 +486,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
     if (need_loads) {
         for (int e = tid; e < E; e += nt) {
             int64_t t = 0;
-            for (int g = 0; g < G; ++g) t += s.loads[e * G + g];
+            for (int g = 0; g < G; ++g) t += s.loads[e * loads_stride(G) + g];
             s.totals[e] = t;
             my_total += t;
             // scheduler.py:344-347: a loaded expert with an empty EDP group
@@ -672,7 +678,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
                 const int b = s.grp_off[e], n = s.grp_off[e + 1] - b;
                 int64_t tot = 0, xs = 0;
                 bool neg = false;
-                for (int g = 0; g < G; ++g) tot += s.loads[e * G + g];
+                for (int g = 0; g < G; ++g) tot += s.loads[e * loads_stride(G) + g];
                 for (int k = 0; k < n; ++k) { xs += s.xi[b + k]; neg |= s.xi[b + k] < 0; }
                 if (neg || xs != tot) set_status(status, HEP_E_CONTRACT);
             }
