@@ -94,6 +94,7 @@ struct Params {
     int tile_m;    // modes 0 / 2: rows per m-tile (0 = BM; 256 on the CTA pair)
     int light_first;  // grouped: weights of single-m-tile experts loaded evict-first
     int k_split;      // mode 0: contraction split into k_split ranges, partial s -> out + s*out_exp_stride
+    int wait_cluster;  // pair kernel: 1 = mbarrier waits with .acquire.cluster (L1 invalidate per wait)
     int clk_slot;  // > 0: CTA 0 stamps (clock64, globaltimer) at entry and exit into g_gemm_clk[clk_slot - 1]
 };
 
@@ -473,7 +474,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params p) {
     using S = Smem<BN, STAGES>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // align within the array (not through uintptr_t) so s_off etc. stay LDS, not generic loads
+    uint8_t *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t *sA = base;
     uint8_t *sB = base + STAGES * S::A_BYTES;
     uint64_t *full = reinterpret_cast<uint64_t *>(base + STAGES * S::STAGE_BYTES);
@@ -684,6 +686,17 @@ __global__ void __launch_bounds__(kThreads, 1)
 // ---------------------------------------------------------------------------
 constexpr int kPairRows = 256;
 
+// Pair-kernel mbarrier wait.  Every consumer of these barriers reads its data through
+// the async proxy (TMA -> MMA smem operands, MMA -> tcgen05.ld of TMEM, ordered by the
+// tcgen05 fences), so a CTA-scope wait suffices; an .acquire.cluster wait compiles to
+// an L1 invalidate (CCTL.IVALL) after every completed wait.
+__device__ __forceinline__ void pair_wait(const Params &p, uint64_t *bar, uint32_t parity) {
+    if (p.wait_cluster)
+        mbar_wait_cluster(bar, parity);
+    else
+        mbar_wait(bar, parity);
+}
+
 template <int STAGES>
 struct Smem2 {
     static constexpr int A_BYTES = 128 * BK * 2;
@@ -701,7 +714,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     constexpr uint32_t TMEM_COLS = 512;
     using S = Smem2<STAGES>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // align within the array (not through uintptr_t) so s_off etc. stay LDS, not generic loads
+    uint8_t *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t *sA = base;
     uint8_t *sB = base + STAGES * S::A_BYTES;
     uint64_t *full = reinterpret_cast<uint64_t *>(base + STAGES * S::STAGE_BYTES);
@@ -762,7 +776,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const int4 rows = make_int4(r[0], r[1], r[2], r[3]);
             for (int k = 0; k < kb; ++k) {
                 if (lane == 0) {
-                    mbar_wait_cluster(&empty[stage], phase ^ 1);
+                    pair_wait(p, &empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * S::STAGE_BYTES);
                 }
                 __syncwarp();
@@ -793,7 +807,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 // an expert with a single m-tile streams its weights once: keep them out of L2's way
                 const bool light = p.light_first && p.grouped == 1 && s_off[tl.expert + 1] - s_off[tl.expert] == 1;
                 for (int k = 0; k < tl.kb; ++k) {
-                    mbar_wait_cluster(&empty[stage], phase ^ 1);
+                    pair_wait(p, &empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], 2 * S::STAGE_BYTES);
                     if constexpr (A_MN) {
 #pragma unroll
@@ -827,11 +841,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             uint32_t acc_phase = 0;
             for (int64_t t = cid; t < n_total; t += ncl) {
                 const int tkb = (p.grouped == 2 || p.k_split > 1) ? decode(p, t, s_off).kb : kb;
-                mbar_wait_cluster(&tempty[acc], acc_phase ^ 1);
+                pair_wait(p, &tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
                 for (int k = 0; k < tkb; ++k) {
-                    mbar_wait_cluster(&full[stage], phase);
+                    pair_wait(p, &full[stage], phase);
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(sA + stage * S::A_BYTES);
                     const uint32_t b_addr = smem_u32(sB + stage * S::B_BYTES);
@@ -859,7 +873,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t acc_phase = 0;
         for (int64_t t = cid; t < n_total; t += ncl) {
             const Tile tl = decode(p, t, s_off);
-            mbar_wait_cluster(&tfull[acc], acc_phase);
+            pair_wait(p, &tfull[acc], acc_phase);
             tc_fence_after();
             const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
             const int local_row = (int)rank * 128 + row_in_cta;
@@ -1098,32 +1112,29 @@ static int launch(const void *A, int64_t a_rows, int64_t K, const void *B, int64
     return HEP_OK;
 }
 
-template <int STAGES, int EPI>
-static int launch2sm(const void *A, int64_t a_rows, int64_t K, const void *B, int64_t b_rows, const Params &p,
-                     cudaStream_t stream) {
-    using S = Smem2<STAGES>;
-    CUtensorMap ta, tb;
-    int rc = make_tmap(&ta, A, (uint64_t)a_rows, (uint64_t)K, p.gather_idx ? 1 : 128);  // gather: {64, 1} rows
-    if (rc) return rc;
-    rc = make_tmap(&tb, B, (uint64_t)b_rows, (uint64_t)K, 128);
-    if (rc) return rc;
-    auto kern = gemm2sm_kernel<STAGES, EPI>;
-    HEP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES));
-    const int grid = sm_count() & ~1;  // whole CTA pairs
-    kern<<<grid, kThreads, S::BYTES, stream>>>(ta, tb, p);
-    HEP_CHECK_LAUNCH();
-    return HEP_OK;
-}
-
 template <int STAGES, int EPI, bool A_MN, bool B_MN>
-static int launch2sm_maps(const CUtensorMap &ta, const CUtensorMap &tb, const Params &p, cudaStream_t stream) {
+static int launch2sm_maps(const CUtensorMap &ta, const CUtensorMap &tb, const Params &p0, cudaStream_t stream) {
     using S = Smem2<STAGES>;
+    Params p = p0;
+    const char *wc_env = getenv("HEP_PAIR_WAIT_CLUSTER");
+    p.wait_cluster = wc_env && wc_env[0] == '1';
     auto kern = gemm2sm_kernel<STAGES, EPI, A_MN, B_MN>;
     HEP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES));
     const int grid = sm_count() & ~1;
     kern<<<grid, kThreads, S::BYTES, stream>>>(ta, tb, p);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
+}
+
+template <int STAGES, int EPI>
+static int launch2sm(const void *A, int64_t a_rows, int64_t K, const void *B, int64_t b_rows, const Params &p,
+                     cudaStream_t stream) {
+    CUtensorMap ta, tb;
+    int rc = make_tmap(&ta, A, (uint64_t)a_rows, (uint64_t)K, p.gather_idx ? 1 : 128);  // gather: {64, 1} rows
+    if (rc) return rc;
+    rc = make_tmap(&tb, B, (uint64_t)b_rows, (uint64_t)K, 128);
+    if (rc) return rc;
+    return launch2sm_maps<STAGES, EPI, false, false>(ta, tb, p, stream);
 }
 
 // CTA pairs unless experts carry so few rows that 256-row tiles waste more than
