@@ -23,6 +23,6 @@ timeout 600 ncu --set full --clock-control none --import-source on --kernel-name
   -k regex:"gemm2sm_kernel|gemm_kernel|sched_kernel|permute|combine|chunk_map|plan_prep" -c 9 \
   -o gpurun_out/prof_mixtral_$R python bench.py --config mixtral --profile --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_mixtral_$R.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k regex:"gemm_kernel<.int.256|sched_kernel|permute|combine" -c 5 \
+  -k regex:"gemm2sm_kernel|gemm_kernel<.int.256|sched_kernel|permute|combine" -c 7 \
   -o gpurun_out/prof_dsv3_$R python bench.py --config dsv3 --profile --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_dsv3_$R.log 2>&1
 echo done
