@@ -94,7 +94,8 @@ struct Params {
     int tile_m;    // modes 0 / 2: rows per m-tile (0 = BM; 256 on the CTA pair)
     int light_first;  // grouped: weights of single-m-tile experts loaded evict-first
     int k_split;      // mode 0: contraction split into k_split ranges, partial s -> out + s*out_exp_stride
-    int wait_cluster;  // pair kernel: 1 = mbarrier waits with .acquire.cluster (L1 invalidate per wait)
+    int wait_cluster;
+    int st256;  // epilogue rows 32-B aligned: one 256-bit store per 16 bf16 / 8 fp32 columns (full L2 sectors)  // pair kernel: 1 = mbarrier waits with .acquire.cluster (L1 invalidate per wait)
     int clk_slot;  // > 0: CTA 0 stamps (clock64, globaltimer) at entry and exit into g_gemm_clk[clk_slot - 1]
 };
 
@@ -265,10 +266,15 @@ __device__ __forceinline__ void store_tile(const Params &p, uint32_t t_row, int6
                 dg[i] = pack_bf16(d0 * b0 * ds0, d1 * b1 * ds1);
                 du[i] = pack_bf16(d0 * a0 * s0, d1 * a1 * s1);
             }
-            st_global_v4_hint(out + gcol, make_uint4(dg[0], dg[1], dg[2], dg[3]), pol_out);
-            st_global_v4_hint(out + gcol + 8, make_uint4(dg[4], dg[5], dg[6], dg[7]), pol_out);
-            st_global_v4_hint(out + gcol + 128, make_uint4(du[0], du[1], du[2], du[3]), pol_out);
-            st_global_v4_hint(out + gcol + 136, make_uint4(du[4], du[5], du[6], du[7]), pol_out);
+            if (p.st256) {
+                st_global_v8_hint(out + gcol, dg, pol_out);
+                st_global_v8_hint(out + gcol + 128, du, pol_out);
+            } else {
+                st_global_v4_hint(out + gcol, make_uint4(dg[0], dg[1], dg[2], dg[3]), pol_out);
+                st_global_v4_hint(out + gcol + 8, make_uint4(dg[4], dg[5], dg[6], dg[7]), pol_out);
+                st_global_v4_hint(out + gcol + 128, make_uint4(du[0], du[1], du[2], du[3]), pol_out);
+                st_global_v4_hint(out + gcol + 136, make_uint4(du[4], du[5], du[6], du[7]), pol_out);
+            }
         }
     } else if constexpr (EPI == EPI_SWIGLU) {
         // columns [0, BN/2) = gate (W1 block), [BN/2, BN) = up (W3 block)
@@ -295,14 +301,23 @@ __device__ __forceinline__ void store_tile(const Params &p, uint32_t t_row, int6
                     pg[i] = pack_bf16(__uint_as_float(g[2 * i]), __uint_as_float(g[2 * i + 1]));
                     pu[i] = pack_bf16(__uint_as_float(u[2 * i]), __uint_as_float(u[2 * i + 1]));
                 }
-                st_global_v4_hint(pre, make_uint4(pg[0], pg[1], pg[2], pg[3]), pol_out);
-                st_global_v4_hint(pre + 8, make_uint4(pg[4], pg[5], pg[6], pg[7]), pol_out);
-                st_global_v4_hint(pre + BN / 2, make_uint4(pu[0], pu[1], pu[2], pu[3]), pol_out);
-                st_global_v4_hint(pre + BN / 2 + 8, make_uint4(pu[4], pu[5], pu[6], pu[7]), pol_out);
+                if (p.st256) {
+                    st_global_v8_hint(pre, pg, pol_out);
+                    st_global_v8_hint(pre + BN / 2, pu, pol_out);
+                } else {
+                    st_global_v4_hint(pre, make_uint4(pg[0], pg[1], pg[2], pg[3]), pol_out);
+                    st_global_v4_hint(pre + 8, make_uint4(pg[4], pg[5], pg[6], pg[7]), pol_out);
+                    st_global_v4_hint(pre + BN / 2, make_uint4(pu[0], pu[1], pu[2], pu[3]), pol_out);
+                    st_global_v4_hint(pre + BN / 2 + 8, make_uint4(pu[4], pu[5], pu[6], pu[7]), pol_out);
+                }
             }
             if (valid) {
-                st_global_v4_hint(out + c, make_uint4(packed[0], packed[1], packed[2], packed[3]), pol_out);
-                st_global_v4_hint(out + c + 8, make_uint4(packed[4], packed[5], packed[6], packed[7]), pol_out);
+                if (p.st256) {
+                    st_global_v8_hint(out + c, packed, pol_out);
+                } else {
+                    st_global_v4_hint(out + c, make_uint4(packed[0], packed[1], packed[2], packed[3]), pol_out);
+                    st_global_v4_hint(out + c + 8, make_uint4(packed[4], packed[5], packed[6], packed[7]), pol_out);
+                }
             }
         }
     } else if constexpr (EPI == EPI_BF16) {
@@ -323,7 +338,10 @@ __device__ __forceinline__ void store_tile(const Params &p, uint32_t t_row, int6
                 packed[i] = pack_bf16(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
                 packed[8 + i] = pack_bf16(__uint_as_float(w[2 * i]), __uint_as_float(w[2 * i + 1]));
             }
-            if (valid) {
+            if (valid && p.st256) {
+                st_global_v8_hint(out + c, packed, pol_out);
+                st_global_v8_hint(out + c + 16, packed + 8, pol_out);
+            } else if (valid) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const uint4 val = make_uint4(packed[4 * q], packed[4 * q + 1], packed[4 * q + 2], packed[4 * q + 3]);
@@ -347,7 +365,10 @@ __device__ __forceinline__ void store_tile(const Params &p, uint32_t t_row, int6
 #pragma unroll
                 for (int i = 0; i < 16; ++i) v[i] = 0u;
             if (valid) {
-                if (col0 + c + 16 <= p.out_cols) {
+                if (p.st256 && col0 + c + 16 <= p.out_cols) {
+                    st_global_v8_hint(out + c, v, pol_out);
+                    st_global_v8_hint(out + c + 8, v + 8, pol_out);
+                } else if (col0 + c + 16 <= p.out_cols) {
                     float4 *dst = reinterpret_cast<float4 *>(out + c);
 #pragma unroll
                     for (int i = 0; i < 4; ++i)
@@ -1079,10 +1100,28 @@ static int make_tmap_mn(CUtensorMap *m, const void *ptr, uint64_t k_rows, uint64
     return HEP_OK;
 }
 
+// 256-bit epilogue stores when every output row (and the training pre-activation
+// rows) starts 32-B aligned; peer-row (NVLink) destinations keep 16-B stores.
+// HEP_ST256=0 disables.
+template <int EPI>
+static Params with_store_width(const Params &p0) {
+    Params p = p0;
+    const char *env = getenv("HEP_ST256");
+    const int64_t esz = (EPI == EPI_F32) ? 4 : 2;
+    auto al = [](const void *q, int64_t stride_bytes) {
+        return q == nullptr || (reinterpret_cast<uintptr_t>(q) % 32 == 0 && stride_bytes % 32 == 0);
+    };
+    p.st256 = !(env && env[0] == '0') && EPI != EPI_GATE && p.row_addr == nullptr && p.out != nullptr &&
+              al(p.out, p.ld_out * esz) && (EPI != EPI_F32 || (p.out_exp_stride * esz) % 32 == 0) &&
+              al(p.aux, p.ld_aux * 2);
+    return p;
+}
+
 template <int BN, int STAGES, int EPI, bool A_MN, bool B_MN>
-static int launch_maps(const CUtensorMap &ta, const CUtensorMap &tb, const Params &p, int64_t max_tiles,
+static int launch_maps(const CUtensorMap &ta, const CUtensorMap &tb, const Params &p0, int64_t max_tiles,
                        cudaStream_t stream) {
     using S = Smem<BN, STAGES>;
+    const Params p = with_store_width<EPI>(p0);
     auto kern = gemm_kernel<BN, STAGES, EPI, A_MN, B_MN>;
     HEP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES));
     int grid = sm_count();
@@ -1096,26 +1135,18 @@ static int launch_maps(const CUtensorMap &ta, const CUtensorMap &tb, const Param
 template <int BN, int STAGES, int EPI>
 static int launch(const void *A, int64_t a_rows, int64_t K, const void *B, int64_t b_rows, const Params &p,
                   int64_t max_tiles, cudaStream_t stream) {
-    using S = Smem<BN, STAGES>;
     CUtensorMap ta, tb;
     int rc = make_tmap(&ta, A, (uint64_t)a_rows, (uint64_t)K, p.gather_idx ? 1 : BM);  // gather: {64, 1} rows
     if (rc) return rc;
     rc = make_tmap(&tb, B, (uint64_t)b_rows, (uint64_t)K, BN);
     if (rc) return rc;
-    auto kern = gemm_kernel<BN, STAGES, EPI>;
-    HEP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES));
-    int grid = sm_count();
-    if (max_tiles > 0 && max_tiles < grid) grid = (int)max_tiles;
-    if (grid < 1) grid = 1;
-    kern<<<grid, kThreads, S::BYTES, stream>>>(ta, tb, p);
-    HEP_CHECK_LAUNCH();
-    return HEP_OK;
+    return launch_maps<BN, STAGES, EPI, false, false>(ta, tb, p, max_tiles, stream);
 }
 
 template <int STAGES, int EPI, bool A_MN, bool B_MN>
 static int launch2sm_maps(const CUtensorMap &ta, const CUtensorMap &tb, const Params &p0, cudaStream_t stream) {
     using S = Smem2<STAGES>;
-    Params p = p0;
+    Params p = with_store_width<EPI>(p0);
     const char *wc_env = getenv("HEP_PAIR_WAIT_CLUSTER");
     p.wait_cluster = wc_env && wc_env[0] == '1';
     auto kern = gemm2sm_kernel<STAGES, EPI, A_MN, B_MN>;

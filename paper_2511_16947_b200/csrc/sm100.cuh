@@ -108,6 +108,13 @@ __device__ __forceinline__ void st_global_v4_hint(void *ptr, uint4 v, uint64_t p
                  : "memory");
 }
 
+// 32-byte store (sm_100: STG.E.*.256): one full L2 sector per lane; ptr 32-B aligned
+__device__ __forceinline__ void st_global_v8_hint(void *ptr, const uint32_t *v, uint64_t policy) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8}, %9;" ::"l"(ptr),
+                 "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "l"(policy)
+                 : "memory");
+}
+
 // ---------------- TMEM ----------------
 __device__ __forceinline__ void tmem_alloc(uint32_t *slot, uint32_t ncols) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(slot)),

@@ -1,15 +1,15 @@
 """Top stall-sampled SASS instructions of one kernel in an .ncu-rep
 (needs -lineinfo + --import-source at capture).  Usage:
-    python tools/ncu_hot.py rep.ncu-rep <kernel-regex> [N]"""
+    python tools/ncu_hot.py rep.ncu-rep <kernel-regex> [N] [skip]   (skip: matching launches to skip)"""
 import csv
 import io
 import subprocess
 import sys
 
 
-def main(rep, kern, n=30):
+def main(rep, kern, n=30, skip=0):
     raw = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name", f"regex:{kern}",
-                          "--launch-count", "1", "--print-source", "sass"], capture_output=True, text=True).stdout
+                          "--launch-skip", str(skip), "--launch-count", "1", "--print-source", "sass"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     h = rows[1]
     si = h.index("Warp Stall Sampling (All Samples)")
@@ -27,4 +27,4 @@ def main(rep, kern, n=30):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 30)
+    main(sys.argv[1], sys.argv[2], int(sys.argv[3]) if len(sys.argv) > 3 else 30, int(sys.argv[4]) if len(sys.argv) > 4 else 0)
