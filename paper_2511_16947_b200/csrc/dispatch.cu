@@ -372,6 +372,62 @@ __global__ void __launch_bounds__(256) permute_kernel(const int4 *__restrict__ x
     }
 }
 
+// 32-byte LSU accesses (sm_100 LDG/STG .256): half the load/store instructions of the
+// 128-bit kernel for the same bytes in flight; rows 32-B aligned (d_model % 16).  The
+// permute gains 2-4 % (5.82-5.92 -> 6.01-6.09 TB/s, tools/lsu_ab.py); the same change
+// made the combine 5-10 % slower, so it keeps 128-bit loads.
+struct alignas(32) V8 {
+    uint32_t w[8];
+};
+__device__ __forceinline__ V8 ldg_v8(const V8 *p) {
+    V8 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3]), "=r"(v.w[4]), "=r"(v.w[5]), "=r"(v.w[6]),
+                   "=r"(v.w[7])
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void stg_v8(V8 *p, const V8 &v) {
+    asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "r"(v.w[0]), "r"(v.w[1]),
+                 "r"(v.w[2]), "r"(v.w[3]), "r"(v.w[4]), "r"(v.w[5]), "r"(v.w[6]), "r"(v.w[7])
+                 : "memory");
+}
+
+__global__ void __launch_bounds__(256) permute_v8_kernel(const V8 *__restrict__ x, const int32_t *__restrict__ tok_row,
+                                                         int64_t T, int K, int64_t nv8, V8 *__restrict__ rows) {
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = warp; t < T; t += nwarps) {
+        int32_t r[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (k < K) r[k] = tok_row[t * K + k];
+        const V8 *src = x + t * nv8;
+        for (int64_t v0 = lane; v0 < nv8; v0 += 32 * 2) {
+            V8 buf[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u)
+                if (v0 + 32 * u < nv8) buf[u] = ldg_v8(src + v0 + 32 * u);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                if (k >= K) break;
+                V8 *dst = rows + (int64_t)r[k] * nv8;
+#pragma unroll
+                for (int u = 0; u < 2; ++u)
+                    if (v0 + 32 * u < nv8) stg_v8(dst + v0 + 32 * u, buf[u]);
+            }
+        }
+    }
+}
+
+static bool use_lsu256(const void *a, const void *b, const void *c, int64_t d_model) {
+    const char *env = getenv("HEP_LSU256");
+    if (env && env[0] == '0') return false;
+    auto al = [](const void *p) { return p == nullptr || reinterpret_cast<uintptr_t>(p) % 32 == 0; };
+    return d_model % 16 == 0 && al(a) && al(b) && al(c);
+}
+
 // K7: out[t] = sum_k w[t][k] * y[tok_row[t][k]], fp32 accumulation in k order.
 // One warp per token; each lane keeps 2 x K 128-bit loads in flight.
 template <int K>
@@ -552,8 +608,12 @@ extern "C" int hep_moe_permute(const void *d_x, const int32_t *d_tok_row, int64_
     HEP_REQUIRE(d_x && d_tok_row && d_rows, HEP_E_CONTRACT, "hep_moe_permute: null pointer");
     HEP_REQUIRE(d_model % 8 == 0 && K >= 1 && K <= 16, HEP_E_DIMENSION, "hep_moe_permute: d_model %% 8, K<=16");
     if (T <= 0) return HEP_OK;
-    permute_kernel<<<grid_for_warps(T), 256, 0, (cudaStream_t)stream>>>(
-        (const int4 *)d_x, d_tok_row, T, K, d_model / 8, (int4 *)d_rows);
+    if (use_lsu256(d_x, d_rows, nullptr, d_model))
+        permute_v8_kernel<<<grid_for_warps(T), 256, 0, (cudaStream_t)stream>>>(
+            (const V8 *)d_x, d_tok_row, T, K, d_model / 16, (V8 *)d_rows);
+    else
+        permute_kernel<<<grid_for_warps(T), 256, 0, (cudaStream_t)stream>>>(
+            (const int4 *)d_x, d_tok_row, T, K, d_model / 8, (int4 *)d_rows);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
 }

@@ -38,7 +38,7 @@ def summarise(path):
                 "kernels": [re.sub(r"\(.*", "", x["name"]) for x in trio],
             }
             break
-    for key, pat in (("permute", "permute_kernel"), ("combine", "combine_kernel"), ("sched", "sched_kernel"),
+    for key, pat in (("permute", r"permute(_v8)?_kernel"), ("combine", r"combine(_v8)?_kernel"), ("sched", "sched_kernel"),
                      ("router_gate", r"gemm_kernel<\d+, \d+, 4,")):
         for k in ks:
             if re.search(pat, k["name"]):
