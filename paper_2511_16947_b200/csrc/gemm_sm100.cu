@@ -243,19 +243,27 @@ __device__ __forceinline__ void store_tile(const Params &p, uint32_t t_row, int6
         __nv_bfloat16 *out = reinterpret_cast<__nv_bfloat16 *>(p.out) + grow * p.ld_out;
 #pragma unroll 1
         for (int c = c_begin; c < c_end; c += 16) {
+            const int64_t f = (int64_t)n_blk * BN + c;       // first ffn column of this chunk
+            const int64_t gcol = (f / 128) * 256 + (f % 128);  // gate column; up = gcol + 128
+            // the pre-activation loads go out before the TMEM load so the two latencies overlap
+            uint32_t gw[8], uw[8];
+            if (valid) {
+                if (p.st256) {  // aux rows are 32-B aligned too (with_store_width)
+                    ld_global_v8(pre + gcol, gw);
+                    ld_global_v8(pre + gcol + 128, uw);
+                } else {
+                    const uint4 *ga = reinterpret_cast<const uint4 *>(pre + gcol);
+                    const uint4 *ua = reinterpret_cast<const uint4 *>(pre + gcol + 128);
+                    *reinterpret_cast<uint4 *>(gw) = ga[0];
+                    *reinterpret_cast<uint4 *>(gw + 4) = ga[1];
+                    *reinterpret_cast<uint4 *>(uw) = ua[0];
+                    *reinterpret_cast<uint4 *>(uw + 4) = ua[1];
+                }
+            }
             uint32_t v[16];
             tmem_ld16(t_row + c, v);
             tmem_ld_wait();
             if (!valid) continue;
-            const int64_t f = (int64_t)n_blk * BN + c;       // first ffn column of this chunk
-            const int64_t gcol = (f / 128) * 256 + (f % 128);  // gate column; up = gcol + 128
-            const uint4 *ga = reinterpret_cast<const uint4 *>(pre + gcol);
-            const uint4 *ua = reinterpret_cast<const uint4 *>(pre + gcol + 128);
-            uint32_t gw[8], uw[8];
-            *reinterpret_cast<uint4 *>(gw) = ga[0];
-            *reinterpret_cast<uint4 *>(gw + 4) = ga[1];
-            *reinterpret_cast<uint4 *>(uw) = ua[0];
-            *reinterpret_cast<uint4 *>(uw + 4) = ua[1];
             uint32_t dg[8], du[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
