@@ -210,7 +210,9 @@ __device__ __forceinline__ Tile decode(const Params &p, int64_t t, const int32_t
     return tl;
 }
 
-__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+// fast reciprocal (MUFU.RCP + FMUL, ~2 ulp fp32) instead of IEEE division (FCHK + Newton
+// + slow-path call): far below the bf16 rounding of every output it feeds
+__device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
     __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
@@ -220,7 +222,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 // Epilogue of one accumulator tile row (this thread's TMEM lane): TMEM ->
 // registers -> fused op -> global.  t_row = TMEM address of the row's first
 // column, grow = global output row.
-__device__ __forceinline__ float sigmoid(float x) { return 1.0f / (1.0f + __expf(-x)); }
+__device__ __forceinline__ float sigmoid(float x) { return __fdividef(1.0f, 1.0f + __expf(-x)); }
 
 __device__ __forceinline__ float bf16lo(uint32_t v) { return __uint_as_float(v << 16); }
 __device__ __forceinline__ float bf16hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
