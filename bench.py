@@ -695,7 +695,7 @@ def main():
     perm_bytes = T * d * 2 * (1 + K) + T * K * 4
     comb_bytes = T * K * d * 2 + T * K * 4 * 2 + T * d * 2
     rg_bytes = T * d * 2 + layer.e_pad * d * 2 + T * layer.e_pad * 4 + T * K * 8  # x, Wg, logits, top-K
-    launches_per_step = layer.LAUNCHES_PER_FORWARD
+    launches_per_step = layer.launches_per_forward(T)
 
     if rank == 0:
         cores, model = cpu_info()

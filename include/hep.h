@@ -339,6 +339,10 @@ int hep_moe_expert_ffn_gather(const void *d_x, int64_t T, const int32_t *d_row_t
                               size_t workspace_bytes, int32_t *d_status, void *stream);
 /* workspace for hep_moe_expert_ffn's device-built m-tile list */
 size_t hep_moe_ffn_workspace(int n_seg, int64_t R, int n_experts);
+/* Kernel launches one expert-FFN forward issues for R rows over n_experts (4: two
+ * tile-list kernels + two GEMMs; 8 when the light experts run as a second 1-CTA
+ * GEMM pair).  gather != 0: the fused-permute variant. */
+int hep_moe_ffn_launches(int64_t R, int n_experts, int gather);
 
 /* K7 combine/un-permute: out[t] = sum_k w[t][k] * y[tok_row[t][k]] (fp32 accumulate in k order). */
 int hep_moe_combine(const void *d_y, const int32_t *d_tok_row, const float *d_topk_w, int64_t T, int K,

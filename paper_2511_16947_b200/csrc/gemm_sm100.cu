@@ -980,6 +980,16 @@ __device__ int64_t expert_tiles_warp(const int32_t *seg, int n_seg, int e, int32
     return cnt;
 }
 
+// total rows of expert e over its segments (warp-uniform result)
+__device__ int64_t expert_rows_warp(const int32_t *seg, int n_seg, int e, int lane) {
+    int64_t n = 0;
+    for (int s = lane; s < n_seg; s += 32)
+        if (seg[4 * s + 2] == e) n += seg[4 * s + 1];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) n += __shfl_xor_sync(0xffffffffu, n, o);
+    return n;
+}
+
 constexpr int kTileSegSmem = 2048;  // segments staged in shared memory (16 B each)
 constexpr int kTileWarps = 8;       // experts per block (one warp each)
 
@@ -992,12 +1002,15 @@ __device__ __forceinline__ const int32_t *stage_segments(const int32_t *seg_g, i
 
 // pass 1: m-tiles per expert (one warp per expert, experts spread over blocks/SMs)
 __global__ void __launch_bounds__(32 * kTileWarps) tile_count_kernel(const int32_t *seg_g, int n_seg, int n_exp,
-                                                                     int32_t *exp_cnt, int tile_rows) {
+                                                                     int32_t *exp_cnt, int tile_rows, int light_max,
+                                                                     int light_sel) {
     extern __shared__ int4 st[];
     const int32_t *seg = stage_segments(seg_g, n_seg, st);
     const int lane = threadIdx.x & 31, e = blockIdx.x * kTileWarps + (threadIdx.x >> 5);
     if (e >= n_exp) return;
-    const int64_t c = expert_tiles_warp<false>(seg, n_seg, e, nullptr, nullptr, 0, tile_rows, lane);
+    // light_max > 0: this list holds only the experts with (rows <= light_max) == light_sel
+    const bool keep = light_max <= 0 || ((expert_rows_warp(seg, n_seg, e, lane) <= light_max) == (light_sel != 0));
+    const int64_t c = keep ? expert_tiles_warp<false>(seg, n_seg, e, nullptr, nullptr, 0, tile_rows, lane) : 0;
     if (lane == 0) exp_cnt[e] = (int32_t)c;
 }
 
@@ -1033,16 +1046,17 @@ __global__ void __launch_bounds__(32 * kTileWarps) tile_write_kernel(const int32
     __syncthreads();  // off_sm (stage_segments only synchronises when it stages)
     const int32_t *seg = stage_segments(seg_g, n_seg, st);
     const int e = e_first + w;
-    if (e < n_exp) expert_tiles_warp<true>(seg, n_seg, e, mt_row0, mt_rows, off_sm[w], tile_rows, lane);
+    if (e < n_exp && exp_cnt[e] > 0) expert_tiles_warp<true>(seg, n_seg, e, mt_row0, mt_rows, off_sm[w], tile_rows, lane);
 }
 
 // build the device m-tile list of a grouped GEMM from its segments (2 launches)
 static int build_tiles(const int32_t *d_seg, int n_seg, int n_exp, int32_t *mt_row0, int32_t *mt_rows,
                        int32_t *exp_off, int32_t *exp_cnt, int64_t cap, int32_t *d_status, int tile_rows,
-                       cudaStream_t s) {
+                       cudaStream_t s, int light_max = 0, int light_sel = 0) {
     const size_t sm = n_seg <= kTileSegSmem ? 16 * (size_t)n_seg : 0;
     const int blocks = n_exp > 0 ? (n_exp + kTileWarps - 1) / kTileWarps : 1;
-    tile_count_kernel<<<blocks, 32 * kTileWarps, sm, s>>>(d_seg, n_seg, n_exp, exp_cnt, tile_rows);
+    tile_count_kernel<<<blocks, 32 * kTileWarps, sm, s>>>(d_seg, n_seg, n_exp, exp_cnt, tile_rows, light_max,
+                                                          light_sel);
     HEP_CHECK_LAUNCH();
     tile_write_kernel<<<blocks, 32 * kTileWarps, sm, s>>>(d_seg, n_seg, n_exp, exp_cnt, mt_row0, mt_rows, exp_off, cap,
                                                           d_status, tile_rows);
@@ -1302,8 +1316,9 @@ extern "C" int hep_router_topk(const void *d_x, const void *d_wg, int64_t T, int
 
 extern "C" size_t hep_moe_ffn_workspace(int n_seg, int64_t R, int n_experts) {
     const int64_t cap = R / BM + n_seg + 1;
-    // m-tile rows / sizes [cap] x2, expert tile offsets [E+1], per-expert tile counts [E]
-    return (size_t)(2 * cap + 2 * (int64_t)n_experts + 2) * sizeof(int32_t) + 64;
+    // two tile lists (CTA-pair tiles of the heavy experts, 1-CTA tiles of the light ones),
+    // each: m-tile rows / sizes [cap] x2, expert tile offsets [E+1], per-expert tile counts [E+1]
+    return 2 * (size_t)(2 * cap + 2 * (int64_t)n_experts + 2) * sizeof(int32_t) + 64;
 }
 
 static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg, int n_seg,
@@ -1311,6 +1326,18 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
                           void *d_workspace, size_t workspace_bytes, int32_t *d_status, void *stream,
                           const uint64_t *d_y_addr = nullptr, int64_t rows_hint = -1, const int32_t *d_row_tok = nullptr,
                           int64_t T = 0);
+
+// heavy/light split of the forward FFN (see expert_ffn_fwd): light_max rows or 0
+static int ffn_light_max(int64_t R, int n_experts, bool gather) {
+    const char *lr_env = getenv("HEP_FFN_LIGHT_ROWS");
+    // experts up to one pair tile (256 rows) run as 128-row tiles: DeepSeek-V3 shape FFN
+    // 14.18 -> 12.95 ms (threshold 128: 13.08), Qwen3 unchanged (profiles/r01/ab_light_r01k.txt)
+    return (use_pairs(R, n_experts) && n_experts >= 32 && !gather) ? (lr_env ? atoi(lr_env) : kPairRows) : 0;
+}
+
+extern "C" int hep_moe_ffn_launches(int64_t R, int n_experts, int gather) {
+    return ffn_light_max(R, n_experts, gather != 0) > 0 ? 8 : 4;
+}
 
 extern "C" int hep_moe_expert_ffn_gather(const void *d_x, int64_t T, const int32_t *d_row_tok, const void *d_w13,
                                          const void *d_w2, const int32_t *d_seg, int n_seg, int64_t R, int64_t d_model,
@@ -1368,9 +1395,29 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
     const bool pairs = use_pairs(rows_hint >= 0 ? rows_hint : R, n_experts);
     const char *pol_env = getenv("HEP_L2POL");
     const int pol_mode = pol_env ? atoi(pol_env) : 0;
+    // Light experts (<= light_max rows: one 128-row tile) leave the CTA-pair kernel, whose
+    // 256-row tiles would issue twice their useful MMA work, for a second launch of the
+    // 1-CTA kernel on their own tile list.  Only with many experts (HEP_FFN_LIGHT_ROWS,
+    // 0 disables; the gather variant keeps one list).
+    const int light_max = ffn_light_max(rows_hint >= 0 ? rows_hint : R, n_experts, d_row_tok != nullptr);
+    int32_t *mt_row0_l = exp_off + 2 * (n_experts + 1);
+    int32_t *mt_rows_l = mt_row0_l + cap;
+    int32_t *exp_off_l = mt_rows_l + cap;
     int rc0 = build_tiles(d_seg, n_seg, n_experts, mt_row0, mt_rows, exp_off, exp_off + n_experts + 1, cap, d_status,
-                          pairs ? kPairRows : BM, s);
+                          pairs ? kPairRows : BM, s, light_max, 0);
     if (rc0) return rc0;
+    if (light_max > 0) {
+        rc0 = build_tiles(d_seg, n_seg, n_experts, mt_row0_l, mt_rows_l, exp_off_l, exp_off_l + n_experts + 1, cap,
+                          d_status, BM, s, light_max, 1);
+        if (rc0) return rc0;
+    }
+    auto light_list = [&](Params q) {
+        q.mt_row0 = mt_row0_l;
+        q.mt_rows = mt_rows_l;
+        q.exp_mt_off = exp_off_l;
+        q.clk_slot = 0;
+        return q;
+    };
     Params p{};
     p.grouped = 1;
     p.pol_mode = pol_mode;
@@ -1409,6 +1456,10 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
     int rc = pairs ? launch2sm<6, EPI_SWIGLU>(d_rows, a_rows, d_model, d_w13, (int64_t)n_experts * 2 * ffn, p, s)
                    : launch<256, 4, EPI_SWIGLU>(d_rows, a_rows, d_model, d_w13, (int64_t)n_experts * 2 * ffn, p, 0, s);
     if (rc) return rc;
+    if (light_max > 0 &&
+        (rc = launch<256, 4, EPI_SWIGLU>(d_rows, a_rows, d_model, d_w13, (int64_t)n_experts * 2 * ffn, light_list(p), 0,
+                                         s)))
+        return rc;
     // GEMM 2: Y = H W2^T, B = W2 [E][d][F]
     p.aux = nullptr;
     p.gather_idx = nullptr;
@@ -1421,8 +1472,10 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
     p.out = d_y;
     p.ld_out = d_model;
     p.out_cols = d_model;
-    return pairs ? launch2sm<6, EPI_BF16>(d_h, R, ffn, d_w2, (int64_t)n_experts * d_model, p, s)
-                 : launch<256, 4, EPI_BF16>(d_h, R, ffn, d_w2, (int64_t)n_experts * d_model, p, 0, s);
+    rc = pairs ? launch2sm<6, EPI_BF16>(d_h, R, ffn, d_w2, (int64_t)n_experts * d_model, p, s)
+               : launch<256, 4, EPI_BF16>(d_h, R, ffn, d_w2, (int64_t)n_experts * d_model, p, 0, s);
+    if (rc || light_max <= 0) return rc;
+    return launch<256, 4, EPI_BF16>(d_h, R, ffn, d_w2, (int64_t)n_experts * d_model, light_list(p), 0, s);
 }
 
 // ===========================================================================

@@ -292,6 +292,12 @@ class MoELayer(torch.nn.Module):
     # kernel, second scheduler launch, per-phase assignment x4 each)
     LAUNCHES_PER_FORWARD = 11
 
+    def launches_per_forward(self, T: int) -> int:
+        """Kernels one forward on T tokens launches (LAUNCHES_PER_FORWARD counts the FFN as
+        4; with many light experts it runs them as a second 1-CTA GEMM pair: 8)."""
+        L = _lib.lib()
+        return self.LAUNCHES_PER_FORWARD - 4 + int(L.hep_moe_ffn_launches(T * self.K, self.E, int(self.fuse_permute)))
+
     def check_status(self):
         self.sched.check_status("MoELayer")
 

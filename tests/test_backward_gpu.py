@@ -121,3 +121,29 @@ def test_backward_pair_and_single_cta_agree(P, monkeypatch):
         assert _rel(dx, rdx) <= TOL and _rel(dw2, rw2) <= TOL and _rel(dw13, interleave_w13(rw1, rw3)) <= TOL
     for a, b in zip(res["0"], res["1"]):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("pair", ["0", "1"])
+def test_store_and_copy_widths_agree(P, monkeypatch, pair):
+    """256-bit epilogue stores / pre-activation loads (HEP_ST256) and the 256-bit
+    permute (HEP_LSU256) against their 128-bit fallbacks (taken for unaligned rows and
+    peer-row destinations): forward output and all gradients identical bit for bit."""
+    G, E, K, d, F, T, s = 4, 8, 2, 512, 1024, 4096, 1.0
+    pl = P.cayley_symmetric(P.ClusterShape(G, E, 2))
+    bias = torch.tensor(P.zipf_gate_bias(E, s, 0))
+    g = torch.Generator(device="cuda").manual_seed(23)
+    x = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
+    dout = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
+    monkeypatch.setenv("HEP_FFN_PAIR", pair)
+    res = {}
+    for wide in ("0", "1"):
+        monkeypatch.setenv("HEP_ST256", wide)
+        monkeypatch.setenv("HEP_LSU256", wide)
+        layer = P.MoELayer(pl, d, F, K, seed=2, gate_bias=bias, train=True)
+        y = layer(x).clone()
+        b = layer.buffers(T)
+        res[wide] = [y, b.rows.clone()] + [t.clone() for t in layer.backward_step(x, dout)]
+        torch.cuda.synchronize()
+        layer.check_status()
+    for a, b in zip(res["0"], res["1"]):
+        assert torch.equal(a, b)

@@ -151,6 +151,37 @@ def test_grouped_ffn_skewed_sizes_pair_and_single(L, E, d, F, monkeypatch):
     assert torch.equal(outs["0"][1], outs["1"][1])
 
 
+def test_grouped_ffn_light_expert_split(L, monkeypatch):
+    """CTA pairs with the light experts (<= HEP_FFN_LIGHT_ROWS rows) split off to the
+    1-CTA kernel on their own tile list: every threshold (none, 128, 256, all experts
+    light) gives the same bytes, and hep_moe_ffn_launches reports the extra launches."""
+    from paper_2511_16947_b200.layer import init_expert_weights, interleave_w13
+
+    E, d, F = 48, 256, 512
+    w1, w2, w3 = init_expert_weights(E, d, F, seed=7, device="cuda")
+    w13 = interleave_w13(w1, w3)
+    base = [0, 3, 64, 127, 128, 129, 200, 256, 257, 700, 1500, 2100]
+    sizes = [base[(5 * e) % len(base)] for e in range(E)]
+    segs, row = [], 0
+    for e in range(E):  # two segments per expert (two source GPUs), contiguous rows
+        a = sizes[e] // 3
+        segs += [(row, a, e, 0), (row + a, sizes[e] - a, e, 1)]
+        row += sizes[e]
+    R = row
+    x = torch.randn(R, d, device="cuda").to(torch.bfloat16)
+    monkeypatch.setenv("HEP_FFN_PAIR", "1")
+    outs = {}
+    for lr in ("0", "128", "256", "100000"):
+        monkeypatch.setenv("HEP_FFN_LIGHT_ROWS", lr)
+        outs[lr] = _run_ffn(L, x, w13, w2, segs, R, d, F, E)
+        assert int(L.lib().hep_moe_ffn_launches(R, E, 0)) == (4 if lr == "0" else 8)
+    for lr in ("128", "256", "100000"):
+        assert torch.equal(outs[lr][0], outs["0"][0]) and torch.equal(outs[lr][1], outs["0"][1]), lr
+    r0, n = segs[2 * 9][0], sizes[9]  # spot-check one heavy expert against fp32 torch
+    ref = _ffn_ref(x[r0:r0 + n].float(), w1[9].float(), w3[9].float(), w2[9].float())
+    assert (outs["128"][1][r0:r0 + n].float() - ref).abs().max().item() <= 1e-2 * ref.abs().max().item()
+
+
 @pytest.mark.parametrize("T,d,E,K,G,bias", [
     (4096, 512, 8, 2, 4, True), (2000, 256, 8, 1, 2, False), (4096, 1024, 40, 6, 8, True),
     (8192, 512, 128, 8, 8, True), (3000, 512, 128, 8, 3, False), (4096, 768, 200, 8, 8, True),

@@ -25,4 +25,17 @@ timeout 600 ncu --set full --clock-control none --import-source on --kernel-name
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
   -k regex:"gemm2sm_kernel|gemm_kernel<.int.256|sched_kernel|permute|combine" -c 7 \
   -o gpurun_out/prof_dsv3_$R python bench.py --config dsv3 --profile --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_dsv3_$R.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+  -k regex:"gemm2sm_kernel" -c 2 \
+  -o gpurun_out/prof_qwen3_$R python bench.py --config qwen3 --profile --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_qwen3_$R.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+  -k regex:"gemm2sm_kernel" --launch-skip 6 -c 6 \
+  -o gpurun_out/prof_train_qwen3_$R python tools/train_step.py --config qwen3 --iters 2 > gpurun_out/ncu_train_qwen3_$R.log 2>&1
+# summarise the full captures on the box (copy-back is capped at 64 MiB) and drop the reports
+for r in gpurun_out/prof_*_$R.ncu-rep; do
+  python tools/ncu_summary.py $r > ${r%.ncu-rep}.md 2>&1
+done
+python tools/ncu_hot.py gpurun_out/prof_qwen3_$R.ncu-rep gemm2sm 30 1 > gpurun_out/hot_qwen3_gemm2_$R.txt 2>&1
+python tools/ncu_hot.py gpurun_out/prof_train_qwen3_$R.ncu-rep gemm2sm 30 2 > gpurun_out/hot_train_qwen3_dgrad_$R.txt 2>&1
+rm -f gpurun_out/prof_*_$R.ncu-rep
 echo done
