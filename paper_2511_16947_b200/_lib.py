@@ -66,6 +66,7 @@ SIGNATURES = {
     "hep_ffn_debug_clock": (ctypes.c_int, [c_i64p]),
     "hep_moe_ffn_workspace": (ctypes.c_size_t, [ctypes.c_int, ctypes.c_int64, ctypes.c_int]),
     "hep_moe_ffn_launches": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int, ctypes.c_int]),
+    "hep_moe_ffn_bwd_launches": (ctypes.c_int, [ctypes.c_int64, ctypes.c_int]),
     "hep_moe_combine": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, vp, vp]),
     "hep_moe_gather_sum": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, vp, vp]),
     "hep_moe_combine_bwd": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, vp, vp, vp]),

@@ -1339,6 +1339,11 @@ extern "C" int hep_moe_ffn_launches(int64_t R, int n_experts, int gather) {
     return ffn_light_max(R, n_experts, gather != 0) > 0 ? 8 : 4;
 }
 
+extern "C" int hep_moe_ffn_bwd_launches(int64_t Rcap, int n_experts) {
+    // zero padding x2, tile list x2, 4 GEMMs; + tile list x2 and 2 dgrad GEMMs when split
+    return ffn_light_max(Rcap, n_experts, false) > 0 ? 12 : 8;
+}
+
 extern "C" int hep_moe_expert_ffn_gather(const void *d_x, int64_t T, const int32_t *d_row_tok, const void *d_w13,
                                          const void *d_w2, const int32_t *d_seg, int n_seg, int64_t R, int64_t d_model,
                                          int64_t ffn, int n_experts, void *d_h, void *d_y, void *d_workspace,
@@ -1510,10 +1515,25 @@ extern "C" int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, con
     // CTA pairs (256-row tiles, half the operand traffic per SM) on the same rule as the
     // forward; MN-major operands are two 64-wide boxes per CTA half
     const bool pairs = use_pairs(Rcap, n_experts) && d_model % 256 == 0 && (2 * ffn) % 256 == 0;
+    // light experts on a 1-CTA tile list, as in the forward (the weight-gradient GEMMs
+    // contract over the rows, so only the two dgrad GEMMs have row tiles to split)
+    const int light_max = pairs ? ffn_light_max(Rcap, n_experts, false) : 0;
     if ((rc = build_tiles(d_seg, n_seg, n_experts, mt_row0, mt_rows, exp_off, exp_off + n_experts + 1, cap, d_status,
-                          pairs ? kPairRows : BM, s)))
+                          pairs ? kPairRows : BM, s, light_max, 0)))
         return rc;
-    CUtensorMap ta, tb;
+    int32_t *mt_row0_l = exp_off + 2 * (n_experts + 1);
+    int32_t *mt_rows_l = mt_row0_l + cap;
+    int32_t *exp_off_l = mt_rows_l + cap;
+    if (light_max > 0 && (rc = build_tiles(d_seg, n_seg, n_experts, mt_row0_l, mt_rows_l, exp_off_l,
+                                           exp_off_l + n_experts + 1, cap, d_status, BM, s, light_max, 1)))
+        return rc;
+    auto light_list = [&](Params q) {
+        q.mt_row0 = mt_row0_l;
+        q.mt_rows = mt_rows_l;
+        q.exp_mt_off = exp_off_l;
+        return q;
+    };
+    CUtensorMap ta, tb;  // A boxes are 128 rows for both kernels (a CTA's half of a pair tile)
     Params p{};
     // --- dA13 = swiglu'(A13) * (dY W2)
     p.grouped = 1;
@@ -1534,6 +1554,8 @@ extern "C" int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, con
     if ((rc = pairs ? launch2sm_maps<6, EPI_SWIGLU_BWD, false, true>(ta, tb, p, s)
                     : launch_maps<256, 4, EPI_SWIGLU_BWD, false, true>(ta, tb, p, 0, s)))
         return rc;
+    if (light_max > 0 && (rc = launch_maps<256, 4, EPI_SWIGLU_BWD, false, true>(ta, tb, light_list(p), 0, s)))
+        return rc;
     if ((rc = hep_moe_zero_padding(d_expert_rows, d_seg, n_seg, n_experts, d_da13, 2 * ffn, stream))) return rc;
     // --- dX_rows = dA13 W13
     p.kblocks = (int)(2 * ffn / BK);
@@ -1548,6 +1570,7 @@ extern "C" int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, con
     if ((rc = pairs ? launch2sm_maps<6, EPI_BF16, false, true>(ta, tb, p, s)
                     : launch_maps<256, 4, EPI_BF16, false, true>(ta, tb, p, 0, s)))
         return rc;
+    if (light_max > 0 && (rc = launch_maps<256, 4, EPI_BF16, false, true>(ta, tb, light_list(p), 0, s))) return rc;
     // --- dW2_e = dY_e^T H_e   (fp32, [E][d][F])
     Params q{};
     q.grouped = 2;

@@ -350,7 +350,9 @@ class MoELayer(torch.nn.Module):
                                 dx.data_ptr(), s), "hep_moe_gather_sum")
         return dx, dwg[:E], dw13, dw2
 
-    LAUNCHES_PER_BACKWARD = 14  # combine_bwd, zero_pad x2, tiles x2, 4 GEMMs, gate_bwd, 2 router GEMMs (+ split-K sum), gather
+    # combine_bwd, zero_pad x2, tiles x2, 4 GEMMs, gate_bwd, 2 router GEMMs (+ split-K sum), gather;
+    # + 4 (light-expert tile list x2, two 1-CTA dgrad GEMMs) when hep_moe_ffn_bwd_launches says 12
+    LAUNCHES_PER_BACKWARD = 14
 
 
 class MoEFunction(torch.autograd.Function):

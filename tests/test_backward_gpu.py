@@ -147,3 +147,30 @@ def test_store_and_copy_widths_agree(P, monkeypatch, pair):
         layer.check_status()
     for a, b in zip(res["0"], res["1"]):
         assert torch.equal(a, b)
+
+
+def test_backward_light_expert_split(P, monkeypatch):
+    """CTA-pair backward with the light experts' dgrad tiles on the 1-CTA kernel
+    (HEP_FFN_LIGHT_ROWS): gradients identical bit for bit to the unsplit backward."""
+    G, E, K, d, F, T, s = 4, 64, 4, 256, 256, 8192, 1.5  # Cayley (p=2, q=5); R / E = 512 -> pairs
+    pl = P.cayley_symmetric(P.ClusterShape(G, E, 2))
+    bias = torch.tensor(P.zipf_gate_bias(E, s, 0))
+    g = torch.Generator(device="cuda").manual_seed(29)
+    x = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
+    dout = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
+    monkeypatch.setenv("HEP_FFN_PAIR", "1")
+    from paper_2511_16947_b200 import _lib
+
+    res = {}
+    for lr in ("0", "256"):
+        monkeypatch.setenv("HEP_FFN_LIGHT_ROWS", lr)
+        assert int(_lib.lib().hep_moe_ffn_bwd_launches(T * K, E)) == (8 if lr == "0" else 12)
+        layer = P.MoELayer(pl, d, F, K, seed=3, gate_bias=bias, train=True)
+        y = layer(x).clone()
+        res[lr] = [y] + [t.clone() for t in layer.backward_step(x, dout)]
+        torch.cuda.synchronize()
+        layer.check_status()
+    loads = layer.expert_loads(T)
+    assert min(loads) <= 256 < max(loads)  # both lists are populated
+    for a, b in zip(res["0"], res["256"]):
+        assert torch.equal(a, b)
