@@ -9,7 +9,7 @@ tail -2 gpurun_out/t_all_$R.log
 timeout 120 python tools/sched_timing.py > gpurun_out/sched_timing_$R.json 2>&1
 for c in mixtral qwen3 dsv3; do
   timeout 300 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    --kernel-name-base demangled -k regex:"hep::|gemm::|sched_kernel|permute|combine|chunk|plan_prep|gate_topk" -c 13 --csv \
+    --kernel-name-base demangled -k regex:"hep::|gemm::|sched_kernel|permute|combine|chunk|plan_prep|gate_topk" -c 17 --csv \
     --log-file gpurun_out/launches_${c}_$R.csv python bench.py --config $c --profile --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
 done
 python tools/traffic.py gpurun_out/launches_mixtral_$R.csv gpurun_out/launches_qwen3_$R.csv gpurun_out/launches_dsv3_$R.csv > gpurun_out/traffic_$R.json

@@ -4,8 +4,8 @@
 
 Each CSV is one `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,
 dram__bytes_write.sum --csv` run of `bench.py --config <cfg> --profile`.  The
-expert FFN (`hep_moe_expert_ffn` = two tile-list kernels + two grouped GEMMs) is
-summed over its four launches; permute and combine are single launches.
+expert FFN (`hep_moe_expert_ffn` = its tile-list kernels + grouped GEMMs: 4 launches, 8
+with the light-expert split) is summed from the first tile-list kernel up to the combine; permute and combine are single launches.
 bench.py reads the resulting JSON to fill `roofline.traffic`."""
 import csv
 import json
@@ -28,14 +28,23 @@ def summarise(path):
     ks = launches(path)
     out = {"source": os.path.relpath(path)}
     for i, k in enumerate(ks):
-        if "tile_count_kernel" in k["name"] and i + 3 < len(ks):
-            trio = ks[i:i + 4]  # tile count, tile list, SwiGLU GEMM, down-projection GEMM
+        if "tile_count_kernel" in k["name"]:
+            # hep_moe_expert_ffn: its tile-list kernels and grouped GEMMs (two, or four with the
+            # light-expert 1-CTA pair), up to the combine that follows
+            grp = []
+            for x in ks[i:]:
+                if re.search(r"combine", x["name"]):
+                    break
+                grp.append(x)
+            if not any(re.search(r"gemm(2sm)?_kernel", x["name"]) for x in grp) or not re.search(
+                    r"combine", " ".join(x["name"] for x in ks[i + len(grp):i + len(grp) + 1])):
+                break  # launch list cut before the FFN ended: no FFN entry
             out["ffn"] = {
-                "bytes": sum(x.get("dram__bytes_read.sum", 0) + x.get("dram__bytes_write.sum", 0) for x in trio),
-                "read": sum(x.get("dram__bytes_read.sum", 0) for x in trio),
-                "write": sum(x.get("dram__bytes_write.sum", 0) for x in trio),
-                "ns": sum(x.get("gpu__time_duration.sum", 0) for x in trio),
-                "kernels": [re.sub(r"\(.*", "", x["name"]) for x in trio],
+                "bytes": sum(x.get("dram__bytes_read.sum", 0) + x.get("dram__bytes_write.sum", 0) for x in grp),
+                "read": sum(x.get("dram__bytes_read.sum", 0) for x in grp),
+                "write": sum(x.get("dram__bytes_write.sum", 0) for x in grp),
+                "ns": sum(x.get("gpu__time_duration.sum", 0) for x in grp),
+                "kernels": [re.sub(r"\(.*", "", x["name"]) for x in grp],
             }
             break
     for key, pat in (("permute", r"permute(_v8)?_kernel"), ("combine", r"combine(_v8)?_kernel"), ("sched", "sched_kernel"),
