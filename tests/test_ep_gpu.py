@@ -166,6 +166,29 @@ def test_local_ep_p2p_exchange_matches_collectives(P, G, E, K, d, F, T, kind, s)
     assert torch.equal(sim(x), ref)
 
 
+def test_local_ep_p2p_light_split_on_pairs(P, monkeypatch):
+    """CTA pairs forced, so every rank's FFN splits its light slots onto the 1-CTA
+    kernel: the peer-row (NVLink store) epilogue of both kernels, the collectives
+    path and the single-device layer agree bit for bit."""
+    from paper_2511_16947_b200.ep import EPMoELayer, LocalComm
+
+    monkeypatch.setenv("HEP_FFN_PAIR", "1")
+    G, E, K, d, F, T, s = 8, 128, 8, 256, 256, 8192, 1.5
+    pl = _placement(P, G, E, "cayley", s)
+    bias = torch.tensor(P.zipf_gate_bias(E, s, 0))
+    x = torch.randn(T, d, generator=torch.Generator(device="cuda").manual_seed(12), device="cuda").to(torch.bfloat16)
+    xs = [x[r * (T // G):(r + 1) * (T // G)].contiguous() for r in range(G)]
+    a = EPMoELayer(pl, d, F, K, LocalComm(G), range(G), seed=6, gate_bias=bias)
+    b = EPMoELayer(pl, d, F, K, LocalComm(G), range(G), seed=6, gate_bias=bias, exchange="p2p")
+    ref = torch.cat([o.clone() for o in a.forward(xs)])
+    got = torch.cat([o.clone() for o in b.forward(xs)])
+    torch.cuda.synchronize()
+    assert torch.equal(got, ref)
+    sim = P.MoELayer(pl, d, F, K, seed=6, gate_bias=bias)
+    assert torch.equal(sim(x), ref)
+    assert int(P._lib.lib().hep_moe_ffn_launches(T * K, E, 0)) == 8
+
+
 def _p2p_worker(rank, world, port, q):
     import os
 
