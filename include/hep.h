@@ -343,7 +343,8 @@ size_t hep_moe_ffn_workspace(int n_seg, int64_t R, int n_experts);
  * tile-list kernels + two GEMMs; 8 when the light experts run as a second 1-CTA
  * GEMM pair).  gather != 0: the fused-permute variant. */
 int hep_moe_ffn_launches(int64_t R, int n_experts, int gather);
-/* Kernel launches one hep_moe_expert_ffn_bwd issues (8, or 12 with the light split). */
+/* Kernel launches one hep_moe_expert_ffn_bwd issues (9, or 13 with the light split;
+ * one fewer each with HEP_WGRAD_ORDER=0). */
 int hep_moe_ffn_bwd_launches(int64_t Rcap, int n_experts);
 
 /* K7 combine/un-permute: out[t] = sum_k w[t][k] * y[tok_row[t][k]] (fp32 accumulate in k order). */

@@ -74,6 +74,7 @@ struct Params {
     // mode 2 (weight gradients): expert e contracts over rows [exp_rows[e], exp_rows[e+1])
     // (64-row padded blocks), output tile grid m_tiles x n_tiles per expert
     const int64_t *exp_rows;
+    const int32_t *exp_perm;  // grouped == 2: expert visit order (staged in s_off), or null
     int m_tiles;
     int64_t out_exp_stride;  // elements between consecutive experts' outputs
     // EPI_SWIGLU: optional pre-activation store; EPI_SWIGLU_BWD: pre-activation input
@@ -151,8 +152,9 @@ __device__ __forceinline__ Tile decode(const Params &p, int64_t t, const int32_t
     const int tm = p.tile_m ? p.tile_m : BM;
     if (p.grouped == 2) {
         const int64_t per = (int64_t)p.m_tiles * p.n_tiles;
-        const int e = (int)(t / per);
-        const int64_t rem = t - (int64_t)e * per;
+        const int slot = (int)(t / per);
+        const int64_t rem = t - (int64_t)slot * per;
+        const int e = p.exp_perm ? off[slot] : slot;
         tl.expert = e;
         tl.n_blk = (int)(rem / p.m_tiles);
         tl.row0 = (int32_t)((rem % p.m_tiles) * tm);
@@ -517,6 +519,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     int32_t *s_off = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(tmem_slot) + 16);
     if (p.grouped == 1)
         for (int i = threadIdx.x; i <= p.n_exp; i += blockDim.x) s_off[i] = p.exp_mt_off[i];
+    else if (p.grouped == 2 && p.exp_perm)
+        for (int i = threadIdx.x; i < p.n_exp; i += blockDim.x) s_off[i] = p.exp_perm[i];
     int32_t *s_hist = s_off + kMaxExpSmem + 4;             // EPI_GATE: [n_src][E] counts
     int32_t *s_chunk = s_hist + kGateMaxSrc * kGateMaxE;  // EPI_GATE: [2][E] tile chunk counts
     float *s_bias = reinterpret_cast<float *>(s_chunk + 2 * kGateMaxE);  // EPI_GATE: [E_pad] bias
@@ -757,6 +761,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     int32_t *s_off = reinterpret_cast<int32_t *>(reinterpret_cast<uint8_t *>(tmem_slot) + 16);
     if (p.grouped == 1)
         for (int i = threadIdx.x; i <= p.n_exp; i += blockDim.x) s_off[i] = p.exp_mt_off[i];
+    else if (p.grouped == 2 && p.exp_perm)
+        for (int i = threadIdx.x; i < p.n_exp; i += blockDim.x) s_off[i] = p.exp_perm[i];
 
     const uint32_t rank = cluster_ctarank();
     const bool leader = rank == 0;
@@ -1318,7 +1324,8 @@ extern "C" size_t hep_moe_ffn_workspace(int n_seg, int64_t R, int n_experts) {
     const int64_t cap = R / BM + n_seg + 1;
     // two tile lists (CTA-pair tiles of the heavy experts, 1-CTA tiles of the light ones),
     // each: m-tile rows / sizes [cap] x2, expert tile offsets [E+1], per-expert tile counts [E+1]
-    return 2 * (size_t)(2 * cap + 2 * (int64_t)n_experts + 2) * sizeof(int32_t) + 64;
+    // + the weight-gradient expert order [E]
+    return (2 * (size_t)(2 * cap + 2 * (int64_t)n_experts + 2) + (size_t)n_experts) * sizeof(int32_t) + 64;
 }
 
 static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg, int n_seg,
@@ -1340,8 +1347,11 @@ extern "C" int hep_moe_ffn_launches(int64_t R, int n_experts, int gather) {
 }
 
 extern "C" int hep_moe_ffn_bwd_launches(int64_t Rcap, int n_experts) {
-    // zero padding x2, tile list x2, 4 GEMMs; + tile list x2 and 2 dgrad GEMMs when split
-    return ffn_light_max(Rcap, n_experts, false) > 0 ? 12 : 8;
+    // zero padding x2, tile list x2, 4 GEMMs, weight-gradient expert order; + tile list x2
+    // and 2 dgrad GEMMs when split
+    const char *ord_env = getenv("HEP_WGRAD_ORDER");
+    const int order = (ord_env && ord_env[0] == '0') ? 0 : 1;
+    return (ffn_light_max(Rcap, n_experts, false) > 0 ? 12 : 8) + order;
 }
 
 extern "C" int hep_moe_expert_ffn_gather(const void *d_x, int64_t T, const int32_t *d_row_tok, const void *d_w13,
@@ -1492,6 +1502,21 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
 //   dW2_e   = dY_e^T H_e                  wgrad GEMM, both operands MN-major, K = the
 //   dW13_e  = dA13_e^T X_e                expert's rows (K-ragged per expert)
 // ===========================================================================
+// Weight-gradient visit order: experts by descending row count (ties: lower id first),
+// so the long-K tiles of the heavy experts all start with the launch and stream their
+// operand panels together instead of drifting apart behind a mix of short tiles.
+__global__ void expert_order_kernel(const int64_t *exp_rows, int E, int32_t *perm) {
+    for (int e = threadIdx.x; e < E; e += blockDim.x) {
+        const int64_t n = exp_rows[e + 1] - exp_rows[e];
+        int rank = 0;
+        for (int j = 0; j < E; ++j) {
+            const int64_t m = exp_rows[j + 1] - exp_rows[j];
+            rank += (m > n) || (m == n && j < e);
+        }
+        perm[rank] = e;
+    }
+}
+
 extern "C" int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, const void *d_h, void *d_dy,
                                       const void *d_w13, const void *d_w2, const int32_t *d_seg, int n_seg,
                                       const int64_t *d_expert_rows, int64_t Rcap, int64_t d_model, int64_t ffn,
@@ -1575,6 +1600,13 @@ extern "C" int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, con
     Params q{};
     q.grouped = 2;
     q.exp_rows = d_expert_rows;
+    const char *ord_env = getenv("HEP_WGRAD_ORDER");
+    if (!(ord_env && ord_env[0] == '0')) {
+        int32_t *perm = exp_off_l + 2 * (n_experts + 1);  // after the two tile lists
+        expert_order_kernel<<<1, 1024, 0, s>>>(d_expert_rows, n_experts, perm);
+        HEP_CHECK_LAUNCH();
+        q.exp_perm = perm;
+    }
     q.n_exp = n_experts;
     const int tm = pairs ? kPairRows : BM;
     q.tile_m = pairs ? kPairRows : 0;

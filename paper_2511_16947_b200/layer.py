@@ -351,8 +351,9 @@ class MoELayer(torch.nn.Module):
         return dx, dwg[:E], dw13, dw2
 
     # combine_bwd, zero_pad x2, tiles x2, 4 GEMMs, gate_bwd, 2 router GEMMs (+ split-K sum), gather;
-    # + 4 (light-expert tile list x2, two 1-CTA dgrad GEMMs) when hep_moe_ffn_bwd_launches says 12
-    LAUNCHES_PER_BACKWARD = 14
+    # + the weight-gradient expert order, + 4 (light-expert tile list x2, two 1-CTA dgrad GEMMs)
+    # when split (hep_moe_ffn_bwd_launches: 9 / 13 for the FFN part)
+    LAUNCHES_PER_BACKWARD = 15
 
 
 class MoEFunction(torch.autograd.Function):

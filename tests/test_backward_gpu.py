@@ -164,7 +164,7 @@ def test_backward_light_expert_split(P, monkeypatch):
     res = {}
     for lr in ("0", "256"):
         monkeypatch.setenv("HEP_FFN_LIGHT_ROWS", lr)
-        assert int(_lib.lib().hep_moe_ffn_bwd_launches(T * K, E)) == (8 if lr == "0" else 12)
+        assert int(_lib.lib().hep_moe_ffn_bwd_launches(T * K, E)) == (9 if lr == "0" else 13)
         layer = P.MoELayer(pl, d, F, K, seed=3, gate_bias=bias, train=True)
         y = layer(x).clone()
         res[lr] = [y] + [t.clone() for t in layer.backward_step(x, dout)]
@@ -174,3 +174,27 @@ def test_backward_light_expert_split(P, monkeypatch):
     assert min(loads) <= 256 < max(loads)  # both lists are populated
     for a, b in zip(res["0"], res["256"]):
         assert torch.equal(a, b)
+
+
+def test_backward_wgrad_expert_order(P, monkeypatch):
+    """Weight-gradient tiles visited heaviest expert first (HEP_WGRAD_ORDER) or in
+    expert order: every output tile is one CTA's K-ordered sum, so the bits match."""
+    G, E, K, d, F, T, s = 4, 64, 4, 256, 256, 8192, 1.5
+    pl = P.cayley_symmetric(P.ClusterShape(G, E, 2))
+    bias = torch.tensor(P.zipf_gate_bias(E, s, 0))
+    g = torch.Generator(device="cuda").manual_seed(31)
+    x = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
+    dout = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
+    res = {}
+    for pair in ("0", "1"):
+        monkeypatch.setenv("HEP_FFN_PAIR", pair)
+        for order in ("0", "1"):
+            monkeypatch.setenv("HEP_WGRAD_ORDER", order)
+            layer = P.MoELayer(pl, d, F, K, seed=4, gate_bias=bias, train=True)
+            layer(x)
+            res[pair + order] = [t.clone() for t in layer.backward_step(x, dout)]
+            torch.cuda.synchronize()
+            layer.check_status()
+    for key in ("01", "10", "11"):
+        for a, b in zip(res["00"], res[key]):
+            assert torch.equal(a, b), key
