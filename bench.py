@@ -555,13 +555,12 @@ def main():
     ffn_ms, perm_ms, comb_ms = stage_ms["ffn"], stage_ms["permute"], stage_ms["combine"]
 
     # --- the SM clock the expert GEMMs actually ran at: CTA 0 stamps clock64 and the
-    # global timer at entry/exit of each GEMM (HEP_FFN_CLOCK=1), eager steps back to back
+    # global timer at entry/exit of each GEMM (hep_tuning.ffn_clock = 1), eager steps back to back
     ffn_clock = None
     if not args.profile:
         import ctypes as _ct
 
-        os.environ["HEP_FFN_CLOCK"] = "1"
-        try:
+        with _lib.tuning(ffn_clock=1):
             for i in range(min(args.steps, 10)):
                 staged_step(i)
             torch.cuda.synchronize()
@@ -572,8 +571,6 @@ def main():
             ffn_clock = {"gemm1_mhz": round(mhz[0], 1), "gemm2_mhz": round(mhz[1], 1),
                          "mhz": round((mhz[0] * ns[0] + mhz[1] * ns[1]) / max(1, ns[0] + ns[1]), 1),
                          "source": "clock64 / globaltimer of CTA 0 across each expert GEMM (eager steps)"}
-        finally:
-            del os.environ["HEP_FFN_CLOCK"]
 
     # --- scheduler latency: the K3 kernel alone, on this micro-batch's histogram
     n_sched = 200

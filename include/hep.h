@@ -42,6 +42,32 @@ int hep_abi_version(void);
 /* Number of SMs of the current device (grid sizing helper for callers). */
 int hep_device_sm_count(void);
 
+/*
+ * Launch-shape tuning, process-wide and explicit (the library never reads the
+ * environment).  The defaults are the measured winners; the A/B tools
+ * in tools/ change them through hep_tuning_set.  Values are read when an entry point
+ * launches, so a CUDA graph keeps the tuning that was active at capture time.
+ * A field set to -1 keeps / restores its default.
+ */
+typedef struct {
+    int st256;              /* 1: 256-bit epilogue stores / pre-activation loads when rows are 32-B aligned */
+    int pair_wait_cluster;  /* 1: CTA-pair mbarrier waits with .acquire.cluster (0, measured slower) */
+    int ffn_pair;           /* CTA-pair grouped GEMM: -2 auto (>= 512 rows per expert), 0 never, 1 always */
+    int ffn_light_rows;     /* light-expert split threshold in rows (default 256; 0 disables) */
+    int wgrad_order;        /* 1: weight-gradient tiles visit experts heaviest first */
+    int l2_policy;          /* 0: default TMA L2 hints; else (A | B << 2), 1 normal, 2 last, 3 first */
+    int light_first;        /* 1: single-m-tile experts load their weights evict-first */
+    int raster_gm1;         /* raster band (m-tiles) of the SwiGLU GEMM (16) */
+    int raster_gm2;         /* raster band of the down projection (8) */
+    int sched_lexmin_warps; /* warps on the scheduler's lex-min arc chain (4) */
+    int lsu256;             /* 1: 256-bit LDG/STG permute / combine when 32-B aligned */
+    int ffn_clock;          /* 1: diagnostics, CTA 0 of each expert GEMM stamps clock64/globaltimer */
+    int router_tile_rows;   /* router GEMM rows per CTA tile: 0 = auto (all SMs busy), else 128 */
+    int reserved[7];
+} hep_tuning;
+int hep_tuning_get(hep_tuning *out);
+int hep_tuning_set(const hep_tuning *in);
+
 /* ======================================================================
  * Scheduler: exact min-max replica loads + canonical lex-min plan,
  * integerization, locality-first routing, transfer volumes.
@@ -239,10 +265,16 @@ int hep_moe_assign_phase(hep_sched_t h, const hep_sched_out *sched, const int64_
  *                           asc]): (row_start, rows, local weight slot, src)
  *   d_counts  [2G] int64    rows sent to each dst, rows received from each src
  *                           (the all-to-all-v split sizes)
+ * recv_capacity > 0: rows a rank's fixed receive buffer holds (the NVLink path).  If the
+ * schedule sends more rows than that to ANY rank (every rank checks every destination on
+ * the identical plan, so all agree), sched->d_status = HEP_E_CAPACITY and the exchange is
+ * empty (zero counts and segments).  0 = unbounded (NCCL path, buffers sized per call).
+ * On a scheduler error (d_status set) the send positions are the identity t*K + k and
+ * the exchange is empty; the layer raises the status.
  */
 int hep_moe_assign_ep(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_topk_idx, int64_t T, int K, int rank,
-                      int32_t *d_tok_row, int32_t *d_seg, int64_t *d_counts, void *workspace, size_t workspace_bytes,
-                      void *stream);
+                      int64_t recv_capacity, int32_t *d_tok_row, int32_t *d_seg, int64_t *d_counts, void *workspace,
+                      size_t workspace_bytes, void *stream);
 size_t hep_moe_assign_ep_workspace(hep_sched_t h, int64_t T, int K);
 /*
  * EP training layout: map the receive buffer ([src][hosted expert], d_seg from
@@ -276,9 +308,12 @@ int hep_sched_hosted(hep_sched_t h, int rank, int *n_hosted, int *n_slots);
  *   hep_moe_expert_ffn).
  * The caller orders the exchanges across ranks (stream sync + a barrier): a rank's
  * receive buffer is complete once every source's dispatch kernel has finished.
+ * hep_moe_dispatch_p2p stores nothing when d_status (the scheduler's, may be NULL) is
+ * set or when any rank's receive total exceeds recv_capacity rows (0 = unchecked).
  */
 int hep_moe_dispatch_p2p(const void *d_x, const int32_t *d_tok_row, int64_t T, int K, int64_t d_model, int rank,
-                         int num_gpus, const int64_t *d_pair, const uint64_t *d_peer_recv, void *stream);
+                         int num_gpus, const int64_t *d_pair, const uint64_t *d_peer_recv, int64_t recv_capacity,
+                         const int32_t *d_status, void *stream);
 int hep_moe_return_addr(const int64_t *d_pair, int rank, int num_gpus, const uint64_t *d_peer_back, int64_t row_bytes,
                         int64_t capacity, uint64_t *d_addr, void *stream);
 int hep_moe_expert_ffn_p2p(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg, int n_seg,

@@ -34,9 +34,22 @@ class HepSchedOut(ctypes.Structure):
     ]
 
 
+TUNING_FIELDS = ("st256", "pair_wait_cluster", "ffn_pair", "ffn_light_rows", "wgrad_order", "l2_policy",
+                 "light_first", "raster_gm1", "raster_gm2", "sched_lexmin_warps", "lsu256", "ffn_clock",
+                 "router_tile_rows")
+
+
+class HepTuning(ctypes.Structure):
+    """``hep_tuning`` (include/hep.h): process-wide launch tuning, -1 = default."""
+
+    _fields_ = [(f, ctypes.c_int) for f in TUNING_FIELDS] + [("reserved", ctypes.c_int * 7)]
+
+
 # (name, restype, argtypes) for every symbol declared in include/hep.h
 SIGNATURES = {
     "hep_last_error": (ctypes.c_char_p, []),
+    "hep_tuning_get": (ctypes.c_int, [ctypes.POINTER(HepTuning)]),
+    "hep_tuning_set": (ctypes.c_int, [ctypes.POINTER(HepTuning)]),
     "hep_abi_version": (ctypes.c_int, []),
     "hep_device_sm_count": (ctypes.c_int, []),
     "hep_sched_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, c_i32p, c_i32p, c_i32p, ctypes.c_int, ctypes.POINTER(vp)]),
@@ -57,7 +70,7 @@ SIGNATURES = {
     "hep_moe_assign": (ctypes.c_int, [vp, ctypes.POINTER(HepSchedOut), vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, ctypes.c_int, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]),
     "hep_moe_assign_phase": (ctypes.c_int, [vp, ctypes.POINTER(HepSchedOut), vp, vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]),
     "hep_moe_assign_workspace": (ctypes.c_size_t, [vp, ctypes.c_int64, ctypes.c_int]),
-    "hep_moe_assign_ep": (ctypes.c_int, [vp, ctypes.POINTER(HepSchedOut), vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, ctypes.c_size_t, vp]),
+    "hep_moe_assign_ep": (ctypes.c_int, [vp, ctypes.POINTER(HepSchedOut), vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_size_t, vp]),
     "hep_moe_assign_ep_workspace": (ctypes.c_size_t, [vp, ctypes.c_int64, ctypes.c_int]),
     "hep_sched_hosted": (ctypes.c_int, [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     "hep_moe_permute": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, vp, vp]),
@@ -71,7 +84,7 @@ SIGNATURES = {
     "hep_moe_gather_sum": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, vp, vp]),
     "hep_moe_combine_bwd": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, vp, vp, vp]),
     "hep_moe_ep_train_layout": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp]),
-    "hep_moe_dispatch_p2p": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_int, vp, vp, vp]),
+    "hep_moe_dispatch_p2p": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_int64, vp, vp]),
     "hep_moe_return_addr": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int64, ctypes.c_int64, vp, vp]),
     "hep_moe_expert_ffn_p2p": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp, vp, vp, ctypes.c_size_t, vp, vp]),
     "hep_p2p_barrier": (ctypes.c_int, [vp, vp, ctypes.c_int, ctypes.c_int, vp]),
@@ -133,6 +146,40 @@ def require_cuda():
         raise RuntimeError("a CUDA (sm_100a) device is required: this package has no CPU path")
     lib()
     return torch
+
+
+def get_tuning() -> dict:
+    """The library's current launch tuning (``hep_tuning_get``)."""
+    t = HepTuning()
+    check(lib().hep_tuning_get(ctypes.byref(t)), "hep_tuning_get")
+    return {f: getattr(t, f) for f in TUNING_FIELDS}
+
+
+def set_tuning(**fields) -> dict:
+    """Change launch-tuning fields (``hep_tuning_set``); returns the previous values of
+    every field so the caller can restore them.  Unknown names raise."""
+    old = get_tuning()
+    bad = set(fields) - set(TUNING_FIELDS)
+    if bad:
+        raise ValueError(f"unknown tuning fields {sorted(bad)}")
+    t = HepTuning(**{**old, **{k: int(v) for k, v in fields.items()}})
+    check(lib().hep_tuning_set(ctypes.byref(t)), "hep_tuning_set")
+    return old
+
+
+class tuning:
+    """``with tuning(ffn_pair=1): ...`` — set tuning fields for a block, then restore."""
+
+    def __init__(self, **fields):
+        self.fields = fields
+        self.old = None
+
+    def __enter__(self):
+        self.old = set_tuning(**self.fields)
+        return self
+
+    def __exit__(self, *exc):
+        set_tuning(**self.old)
 
 
 def ptr(t) -> int | None:

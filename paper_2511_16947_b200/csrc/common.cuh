@@ -6,12 +6,16 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/hep.h"
 
 namespace hep {
 
 // thread-local message behind hep_last_error()
 void set_error(const char *fmt, ...);
+// process-wide launch tuning (hep_tuning_set); never read from the environment
+extern hep_tuning g_tuning;
 
 #define HEP_CHECK_CUDA(expr)                                                          \
     do {                                                                              \
@@ -21,6 +25,14 @@ void set_error(const char *fmt, ...);
             return HEP_E_CUDA;                                                        \
         }                                                                             \
     } while (0)
+
+// NVTX range around every hot C-ABI entry point (header-only NVTX3: a no-op unless a
+// tool such as ncu --nvtx is attached), so profiles attribute launches to their stage
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
+#define HEP_NVTX(name) ::hep::NvtxRange hep_nvtx_range_(name)
 
 #define HEP_CHECK_LAUNCH() HEP_CHECK_CUDA(cudaGetLastError())
 

@@ -81,8 +81,19 @@ __global__ void plan_prep_kernel(int G, int E, int nnz, const int32_t *grp_off, 
                                  const int64_t *rank_base, const int64_t *row_base_p, int64_t stage_cap) {
     __shared__ int64_t scan[64];
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int64_t n_ranges = *n_ranges_p;
     const int64_t row_off = row_base_p ? *row_base_p : 0;  // phase block start (pipelined split)
+    if (*status) {  // the scheduler failed (and left an empty plan): no segments, no rows
+        for (int p = tid; p < nnz; p += nt) {
+            seg[4 * p + 0] = (int32_t)row_off;
+            seg[4 * p + 1] = 0;
+            seg[4 * p + 2] = -1;
+            seg[4 * p + 3] = -1;
+        }
+        for (int e = tid; e <= E; e += nt) expert_rows[e] = row_off;
+        for (int i = tid; i < E * G; i += nt) w.es_cnt[i] = 0;
+        return;
+    }
+    const int64_t n_ranges = *n_ranges_p;
     // dynamic smem: [E*G] per-(expert, src) range counters, then the staged routing table
     extern __shared__ int4 s_dyn[];
     int32_t *s_cnt = reinterpret_cast<int32_t *>(s_dyn);
@@ -213,7 +224,7 @@ __global__ void chunk_scan_kernel(int n_src, int ncs, int E, const int32_t *chun
 // one warp per chunk; lanes k < K own pick k of each token (distinct experts)
 __global__ void chunk_map_kernel(const int32_t *topk_idx, int K, int E, int G, int64_t tps, int64_t T, int ncs,
                                  const int32_t *chunk_pre, AssignWs w, int32_t *tok_row, int32_t *row_tok,
-                                 int src_base, bool windowed) {
+                                 int src_base, bool windowed, const int32_t *status) {
     extern __shared__ int32_t sm[];
     int32_t *ctr = sm;                // [E]
     int32_t *l_cnt = ctr + E;         // [E]
@@ -223,6 +234,20 @@ __global__ void chunk_map_kernel(const int32_t *topk_idx, int K, int E, int G, i
     int32_t *l_idx = l_lo + E;        // [kChunk * K] this chunk's top-K picks
     const int src = blockIdx.x / ncs, c = blockIdx.x % ncs;
     const int lane = threadIdx.x;
+    if (*status) {
+        // no valid schedule for this micro-batch: identity map, (t, k) -> row t*K + k, so the
+        // permute / dispatch / combine queued behind stay inside their [T*K] buffers (the
+        // layer raises the status; the outputs of this micro-batch are not defined)
+        const int64_t ta = (int64_t)src * tps + (int64_t)c * kChunk;
+        int64_t tb = (int64_t)src * tps + tps;
+        if (ta + kChunk < tb) tb = ta + kChunk;
+        if (T < tb) tb = T;
+        for (int64_t i = ta * K + threadIdx.x; i < tb * K; i += blockDim.x) {
+            tok_row[i] = (int32_t)i;
+            if (row_tok) row_tok[i] = (int32_t)(i / K);
+        }
+        return;
+    }
     // stage this source's range lists with the whole block, independent loads (all G
     // slots of every expert; slots past es_cnt are never read)
     for (int e = threadIdx.x; e < E; e += blockDim.x) {
@@ -284,8 +309,36 @@ __global__ void chunk_map_kernel(const int32_t *topk_idx, int K, int E, int G, i
 // ---------------------------------------------------------------------------
 __global__ void ep_prep_kernel(int G, int E, int rank, const int64_t *ranges, const int64_t *n_ranges_p,
                                const int64_t *transfer, const int32_t *hosted, int n_hosted, const int32_t *nnz_exp,
-                               const int32_t *slots, int64_t *counts, int32_t *seg, AssignWs w, int32_t *status) {
+                               const int32_t *slots, int64_t *counts, int32_t *seg, AssignWs w, int32_t *status,
+                               int64_t recv_capacity) {
     const int tid = threadIdx.x, nt = blockDim.x;
+    __shared__ int fail;
+    if (tid == 0) {
+        // receive capacity (NVLink path: fixed buffers peers store into): every rank checks
+        // EVERY destination's total from the identical transfer plan, so all ranks agree
+        int f = *status != 0;
+        if (!f && recv_capacity > 0)
+            for (int d = 0; d < G; ++d) {
+                int64_t r = 0;
+                for (int s2 = 0; s2 < G; ++s2) r += transfer[s2 * G + d];
+                if (r > recv_capacity) f = 1;
+            }
+        if (f) atomicCAS(status, 0, HEP_E_CAPACITY);
+        fail = f;
+    }
+    __syncthreads();
+    if (fail) {  // empty exchange: nothing sent, nothing received, no FFN tiles
+        for (int i = tid; i < 2 * G; i += nt) counts[i] = 0;
+        for (int i = tid; i < G * n_hosted; i += nt) {
+            int32_t *sg = seg + 4 * (int64_t)i;
+            sg[0] = 0;
+            sg[1] = 0;
+            sg[2] = 0;
+            sg[3] = i / (n_hosted > 0 ? n_hosted : 1);
+        }
+        for (int i = tid; i < E * G; i += nt) w.es_cnt[i] = 0;
+        return;
+    }
     const int64_t n_ranges = *n_ranges_p;
     for (int i = tid; i < E * G * G; i += nt) w.cnt3[i] = 0;
     for (int i = tid; i < E * G; i += nt) w.es_cnt[i] = 0;
@@ -422,8 +475,7 @@ __global__ void __launch_bounds__(256) permute_v8_kernel(const V8 *__restrict__ 
 }
 
 static bool use_lsu256(const void *a, const void *b, const void *c, int64_t d_model) {
-    const char *env = getenv("HEP_LSU256");
-    if (env && env[0] == '0') return false;
+    if (g_tuning.lsu256 == 0) return false;
     auto al = [](const void *p) { return p == nullptr || reinterpret_cast<uintptr_t>(p) % 32 == 0; };
     return d_model % 16 == 0 && al(a) && al(b) && al(c);
 }
@@ -552,7 +604,7 @@ static int assign_impl(hep_sched_t h, const hep_sched_out *sched, bool windowed,
     HEP_REQUIRE(sm <= 200 * 1024, HEP_E_CAPACITY, "chunk_map smem %zu", sm);
     if (sm > 48 * 1024) HEP_CHECK_CUDA(cudaFuncSetAttribute(chunk_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     chunk_map_kernel<<<nblk, 256, sm, s>>>(d_topk_idx, K, E, G, tokens_per_src, T, ncs, w.chunk_pre, w, d_tok_row,
-                                           d_row_tok, 0, windowed);
+                                           d_row_tok, 0, windowed, sched->d_status);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
 }
@@ -561,6 +613,7 @@ extern "C" int hep_moe_assign(hep_sched_t h, const hep_sched_out *sched, const i
                               int64_t tokens_per_src, int row_align, int32_t *d_tok_row, int32_t *d_row_tok,
                               int32_t *d_seg, int64_t *d_expert_rows, void *workspace, size_t workspace_bytes,
                               void *stream) {
+    HEP_NVTX("hep_moe_assign");
     return assign_impl(h, sched, false, false, nullptr, nullptr, d_topk_idx, T, K, tokens_per_src, row_align, d_tok_row,
                        d_row_tok, d_seg, d_expert_rows, workspace, workspace_bytes, stream);
 }
@@ -578,6 +631,7 @@ extern "C" int hep_moe_assign_precounted(hep_sched_t h, const hep_sched_out *sch
                                          int64_t T, int K, int64_t tokens_per_src, int row_align, int32_t *d_tok_row,
                                          int32_t *d_row_tok, int32_t *d_seg, int64_t *d_expert_rows, void *workspace,
                                          size_t workspace_bytes, void *stream) {
+    HEP_NVTX("hep_moe_assign_precounted");
     return assign_impl(h, sched, false, true, nullptr, nullptr, d_topk_idx, T, K, tokens_per_src, row_align, d_tok_row,
                        d_row_tok, d_seg, d_expert_rows, workspace, workspace_bytes, stream);
 }
@@ -599,12 +653,14 @@ extern "C" int hep_moe_assign_phase(hep_sched_t h, const hep_sched_out *sched, c
                                     const int64_t *d_row_base, const int32_t *d_topk_idx, int64_t T, int K,
                                     int64_t tokens_per_src, int32_t *d_tok_row, int32_t *d_row_tok, int32_t *d_seg,
                                     int64_t *d_expert_rows, void *workspace, size_t workspace_bytes, void *stream) {
+    HEP_NVTX("hep_moe_assign_phase");
     return assign_impl(h, sched, true, false, d_rank_base, d_row_base, d_topk_idx, T, K, tokens_per_src, 1, d_tok_row,
                        d_row_tok, d_seg, d_expert_rows, workspace, workspace_bytes, stream);
 }
 
 extern "C" int hep_moe_permute(const void *d_x, const int32_t *d_tok_row, int64_t T, int K, int64_t d_model,
                                void *d_rows, void *stream) {
+    HEP_NVTX("hep_moe_permute");
     HEP_REQUIRE(d_x && d_tok_row && d_rows, HEP_E_CONTRACT, "hep_moe_permute: null pointer");
     HEP_REQUIRE(d_model % 8 == 0 && K >= 1 && K <= 16, HEP_E_DIMENSION, "hep_moe_permute: d_model %% 8, K<=16");
     if (T <= 0) return HEP_OK;
@@ -620,11 +676,13 @@ extern "C" int hep_moe_permute(const void *d_x, const int32_t *d_tok_row, int64_
 
 extern "C" int hep_moe_combine(const void *d_y, const int32_t *d_tok_row, const float *d_topk_w, int64_t T, int K,
                                int64_t d_model, void *d_out, void *stream) {
+    HEP_NVTX("hep_moe_combine");
     return hep_moe_gather_sum(d_y, d_tok_row, d_topk_w, nullptr, T, K, d_model, d_out, stream);
 }
 
 extern "C" int hep_moe_gather_sum(const void *d_y, const int32_t *d_tok_row, const float *d_topk_w, const void *d_add,
                                   int64_t T, int K, int64_t d_model, void *d_out, void *stream) {
+    HEP_NVTX("hep_moe_gather_sum");
     HEP_REQUIRE(d_y && d_tok_row && d_out, HEP_E_CONTRACT, "hep_moe_gather_sum: null pointer");
     HEP_REQUIRE(d_model % 8 == 0 && K >= 1 && K <= 16, HEP_E_DIMENSION, "hep_moe_combine: d_model %% 8, K<=16");
     if (T <= 0) return HEP_OK;
@@ -667,8 +725,9 @@ extern "C" int hep_sched_hosted(hep_sched_t h, int rank, int *n_hosted, int *n_s
 }
 
 extern "C" int hep_moe_assign_ep(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_topk_idx, int64_t T, int K,
-                                 int rank, int32_t *d_tok_row, int32_t *d_seg, int64_t *d_counts, void *workspace,
-                                 size_t workspace_bytes, void *stream) {
+                                 int rank, int64_t recv_capacity, int32_t *d_tok_row, int32_t *d_seg, int64_t *d_counts,
+                                 void *workspace, size_t workspace_bytes, void *stream) {
+    HEP_NVTX("hep_moe_assign_ep");
     HEP_REQUIRE(h && sched && d_topk_idx && d_tok_row && d_seg && d_counts && workspace, HEP_E_CONTRACT,
                 "hep_moe_assign_ep: null argument");
     HEP_REQUIRE(rank >= 0 && rank < h->G && K >= 1 && K <= 16, HEP_E_DIMENSION, "hep_moe_assign_ep: rank/K");
@@ -680,7 +739,7 @@ extern "C" int hep_moe_assign_ep(hep_sched_t h, const hep_sched_out *sched, cons
     const int n_hosted = h->h_hosted_off[rank + 1] - h->h_hosted_off[rank];
     ep_prep_kernel<<<1, 512, 0, s>>>(G, E, rank, sched->d_ranges, sched->d_n_ranges, sched->d_transfer,
                                      h->d_seg_nnz + h->h_hosted_off[rank], n_hosted, h->d_nnz_exp, h->d_slots,
-                                     d_counts, d_seg, w, sched->d_status);
+                                     d_counts, d_seg, w, sched->d_status, recv_capacity);
     HEP_CHECK_LAUNCH();
     if (T <= 0) return HEP_OK;
     const int ncs = (int)((tps + kChunk - 1) / kChunk);
@@ -693,7 +752,7 @@ extern "C" int hep_moe_assign_ep(hep_sched_t h, const hep_sched_out *sched, cons
     if (sm > 48 * 1024)
         HEP_CHECK_CUDA(cudaFuncSetAttribute(chunk_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     chunk_map_kernel<<<ncs, 256, sm, s>>>(d_topk_idx, K, E, G, tps, T, ncs, w.chunk_pre, w, d_tok_row, nullptr, rank,
-                                          false);
+                                          false, sched->d_status);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
 }
@@ -791,6 +850,7 @@ __global__ void gate_bwd_kernel(const int32_t *topk_idx, const float *topk_w, co
 
 extern "C" int hep_moe_combine_bwd(const void *d_dout, const void *d_y, const int32_t *d_tok_row, const float *d_topk_w,
                                    int64_t T, int K, int64_t d_model, void *d_dy, float *d_dw, void *stream) {
+    HEP_NVTX("hep_moe_combine_bwd");
     HEP_REQUIRE(d_dout && d_y && d_tok_row && d_topk_w && d_dy && d_dw, HEP_E_CONTRACT, "hep_moe_combine_bwd: null");
     HEP_REQUIRE(d_model % 8 == 0 && K >= 1 && K <= 16, HEP_E_DIMENSION, "hep_moe_combine_bwd: d_model %% 8, K<=16");
     if (T <= 0) return HEP_OK;
@@ -860,6 +920,7 @@ __global__ void __launch_bounds__(256) ep_layout_kernel(const int32_t *seg, int 
 
 extern "C" int hep_moe_ep_train_layout(const int32_t *d_seg, int n_hosted, int G, int n_slots, int row_align,
                                        int32_t *d_row_map, int32_t *d_seg_out, int64_t *d_slot_rows, void *stream) {
+    HEP_NVTX("hep_moe_ep_train_layout");
     HEP_REQUIRE(d_seg && d_row_map && d_seg_out && d_slot_rows, HEP_E_CONTRACT, "hep_moe_ep_train_layout: null");
     HEP_REQUIRE(G >= 1 && G <= HEP_MAX_GPUS && n_hosted >= 0 && n_slots >= n_hosted && n_slots <= 1024 &&
                     row_align >= 1,
@@ -884,6 +945,7 @@ extern "C" int hep_moe_zero_padding(const int64_t *d_expert_rows, const int32_t 
 
 extern "C" int hep_gate_bwd(const int32_t *d_topk_idx, const float *d_topk_w, const float *d_dw, int64_t T, int K,
                             int64_t ld, void *d_dlogits, void *stream) {
+    HEP_NVTX("hep_gate_bwd");
     HEP_REQUIRE(d_topk_idx && d_topk_w && d_dw && d_dlogits && K >= 1 && K <= ld, HEP_E_CONTRACT, "hep_gate_bwd");
     if (T <= 0) return HEP_OK;
     gate_bwd_kernel<<<(unsigned)((T + 255) / 256), 256, 0, (cudaStream_t)stream>>>(d_topk_idx, d_topk_w, d_dw, T, K, ld,

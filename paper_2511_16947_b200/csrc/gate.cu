@@ -161,6 +161,7 @@ using namespace hep;
 extern "C" int hep_gate_topk(const float *d_logits, int64_t ld_logits, const float *d_bias, int64_t T, int E, int K,
                              int64_t tokens_per_src, int n_src, int32_t *d_topk_idx, float *d_topk_w, int64_t *d_hist,
                              void *stream) {
+    HEP_NVTX("hep_gate_topk");
     HEP_REQUIRE(d_logits && d_topk_idx && d_topk_w && d_hist, HEP_E_CONTRACT, "hep_gate_topk: null pointer");
     HEP_REQUIRE(E >= 1 && E <= kMaxGateExperts && K >= 1 && K <= kMaxTopK && K <= E, HEP_E_DIMENSION,
                 "hep_gate_topk: E=%d K=%d", E, K);

@@ -17,7 +17,6 @@
 // M-tile, so one expert's weight block is streamed from HBM once per wave and
 // the expert's rows stay L2-resident across its N sweep.
 #include <cudaTypedefs.h>
-#include <stdlib.h>
 
 #include "common.cuh"
 #include "sm100.cuh"
@@ -100,7 +99,7 @@ struct Params {
     int clk_slot;  // > 0: CTA 0 stamps (clock64, globaltimer) at entry and exit into g_gemm_clk[clk_slot - 1]
 };
 
-// Diagnostics (HEP_FFN_CLOCK=1): SM clock cycles and wall nanoseconds of CTA 0 across
+// Diagnostics (hep_tuning.ffn_clock = 1): SM clock cycles and wall nanoseconds of CTA 0 across
 // the two expert GEMMs, i.e. the SM clock the tensor cores actually ran at (the
 // power-capped clock of a long GEMM is not what nvidia-smi samples between kernels).
 __device__ long long g_gemm_clk[2][4];
@@ -1132,16 +1131,15 @@ static int make_tmap_mn(CUtensorMap *m, const void *ptr, uint64_t k_rows, uint64
 
 // 256-bit epilogue stores when every output row (and the training pre-activation
 // rows) starts 32-B aligned; peer-row (NVLink) destinations keep 16-B stores.
-// HEP_ST256=0 disables.
+// hep_tuning.st256 = 0 disables.
 template <int EPI>
 static Params with_store_width(const Params &p0) {
     Params p = p0;
-    const char *env = getenv("HEP_ST256");
     const int64_t esz = (EPI == EPI_F32) ? 4 : 2;
     auto al = [](const void *q, int64_t stride_bytes) {
         return q == nullptr || (reinterpret_cast<uintptr_t>(q) % 32 == 0 && stride_bytes % 32 == 0);
     };
-    p.st256 = !(env && env[0] == '0') && EPI != EPI_GATE && p.row_addr == nullptr && p.out != nullptr &&
+    p.st256 = g_tuning.st256 != 0 && EPI != EPI_GATE && p.row_addr == nullptr && p.out != nullptr &&
               al(p.out, p.ld_out * esz) && (EPI != EPI_F32 || (p.out_exp_stride * esz) % 32 == 0) &&
               al(p.aux, p.ld_aux * 2);
     return p;
@@ -1177,8 +1175,7 @@ template <int STAGES, int EPI, bool A_MN, bool B_MN>
 static int launch2sm_maps(const CUtensorMap &ta, const CUtensorMap &tb, const Params &p0, cudaStream_t stream) {
     using S = Smem2<STAGES>;
     Params p = with_store_width<EPI>(p0);
-    const char *wc_env = getenv("HEP_PAIR_WAIT_CLUSTER");
-    p.wait_cluster = wc_env && wc_env[0] == '1';
+    p.wait_cluster = g_tuning.pair_wait_cluster == 1;
     auto kern = gemm2sm_kernel<STAGES, EPI, A_MN, B_MN>;
     HEP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES));
     const int grid = sm_count() & ~1;
@@ -1201,10 +1198,9 @@ static int launch2sm(const void *A, int64_t a_rows, int64_t K, const void *B, in
 // CTA pairs unless experts carry so few rows that 256-row tiles waste more than
 // the pair's halved operand traffic saves: measured in-process (tools/ffn_ab.py,
 // profiles/r01/ffn_ab_r01d.txt) the pair wins at 512 rows per expert (DeepSeek-V3
-// shape) and above.  HEP_FFN_PAIR=0/1 forces it.
+// shape) and above.  hep_tuning.ffn_pair = 0 / 1 forces it.
 static bool use_pairs(int64_t R, int n_experts) {
-    const char *env = getenv("HEP_FFN_PAIR");
-    if (env && *env) return env[0] == '1';
+    if (g_tuning.ffn_pair == 0 || g_tuning.ffn_pair == 1) return g_tuning.ffn_pair == 1;
     return n_experts > 0 && R / n_experts >= 512;
 }
 
@@ -1216,6 +1212,7 @@ using namespace hep::gemm;
 
 extern "C" int hep_gemm_bf16(const void *d_A, const void *d_B, void *d_D, int64_t M, int64_t N, int64_t K, int out_kind,
                              void *stream) {
+    HEP_NVTX("hep_gemm_bf16");
     HEP_REQUIRE(d_A && d_B && d_D, HEP_E_CONTRACT, "hep_gemm_bf16: null pointer");
     HEP_REQUIRE(M > 0 && N > 0 && K > 0 && K % BK == 0, HEP_E_DIMENSION, "hep_gemm_bf16: need K %% 64 == 0 (K=%lld)",
                 (long long)K);
@@ -1273,6 +1270,7 @@ extern "C" int hep_router_topk(const void *d_x, const void *d_wg, int64_t T, int
                                const float *d_bias, int K, int64_t tokens_per_src, int n_src, float *d_logits,
                                int32_t *d_topk_idx, float *d_topk_w, int64_t *d_hist, int32_t *d_chunk_cnt,
                                void *stream) {
+    HEP_NVTX("hep_router_topk");
     HEP_REQUIRE(d_x && d_wg && d_topk_idx && d_topk_w && d_hist, HEP_E_CONTRACT, "hep_router_topk: null pointer");
     HEP_REQUIRE(E >= 1 && K >= 1 && K <= E && e_pad >= E && e_pad % 16 == 0 && d_model % BK == 0, HEP_E_DIMENSION,
                 "hep_router_topk: E=%d e_pad=%d K=%d d=%lld", E, e_pad, K, (long long)d_model);
@@ -1336,10 +1334,9 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
 
 // heavy/light split of the forward FFN (see expert_ffn_fwd): light_max rows or 0
 static int ffn_light_max(int64_t R, int n_experts, bool gather) {
-    const char *lr_env = getenv("HEP_FFN_LIGHT_ROWS");
     // experts up to one pair tile (256 rows) run as 128-row tiles: DeepSeek-V3 shape FFN
     // 14.18 -> 12.95 ms (threshold 128: 13.08), Qwen3 unchanged (profiles/r01/ab_light_r01k.txt)
-    return (use_pairs(R, n_experts) && n_experts >= 32 && !gather) ? (lr_env ? atoi(lr_env) : kPairRows) : 0;
+    return (use_pairs(R, n_experts) && n_experts >= 32 && !gather) ? g_tuning.ffn_light_rows : 0;
 }
 
 extern "C" int hep_moe_ffn_launches(int64_t R, int n_experts, int gather) {
@@ -1349,8 +1346,7 @@ extern "C" int hep_moe_ffn_launches(int64_t R, int n_experts, int gather) {
 extern "C" int hep_moe_ffn_bwd_launches(int64_t Rcap, int n_experts) {
     // zero padding x2, tile list x2, 4 GEMMs, weight-gradient expert order; + tile list x2
     // and 2 dgrad GEMMs when split
-    const char *ord_env = getenv("HEP_WGRAD_ORDER");
-    const int order = (ord_env && ord_env[0] == '0') ? 0 : 1;
+    const int order = g_tuning.wgrad_order != 0 ? 1 : 0;
     return (ffn_light_max(Rcap, n_experts, false) > 0 ? 12 : 8) + order;
 }
 
@@ -1358,6 +1354,7 @@ extern "C" int hep_moe_expert_ffn_gather(const void *d_x, int64_t T, const int32
                                          const void *d_w2, const int32_t *d_seg, int n_seg, int64_t R, int64_t d_model,
                                          int64_t ffn, int n_experts, void *d_h, void *d_y, void *d_workspace,
                                          size_t workspace_bytes, int32_t *d_status, void *stream) {
+    HEP_NVTX("hep_moe_expert_ffn_gather");
     HEP_REQUIRE(d_x && d_row_tok, HEP_E_CONTRACT, "hep_moe_expert_ffn_gather: null pointer");
     HEP_REQUIRE(T > 0 && T < ((int64_t)1 << 31), HEP_E_DIMENSION, "hep_moe_expert_ffn_gather: T=%lld", (long long)T);
     return expert_ffn_fwd(d_x, d_w13, d_w2, d_seg, n_seg, R, d_model, ffn, n_experts, d_h, d_y, nullptr, d_workspace,
@@ -1368,6 +1365,7 @@ extern "C" int hep_moe_expert_ffn_p2p(const void *d_rows, const void *d_w13, con
                                       int n_seg, int64_t R, int64_t rows_hint, int64_t d_model, int64_t ffn,
                                       int n_experts, void *d_h, const uint64_t *d_y_addr, void *d_workspace,
                                       size_t workspace_bytes, int32_t *d_status, void *stream) {
+    HEP_NVTX("hep_moe_expert_ffn_p2p");
     HEP_REQUIRE(d_y_addr, HEP_E_CONTRACT, "hep_moe_expert_ffn_p2p: d_y_addr required");
     return expert_ffn_fwd(d_rows, d_w13, d_w2, d_seg, n_seg, R, d_model, ffn, n_experts, d_h, (void *)d_y_addr,
                           nullptr, d_workspace, workspace_bytes, d_status, stream, d_y_addr, rows_hint);
@@ -1377,6 +1375,7 @@ extern "C" int hep_moe_expert_ffn(const void *d_rows, const void *d_w13, const v
                                   int n_seg, int64_t R, int64_t d_model, int64_t ffn, int n_experts, void *d_h,
                                   void *d_y, void *d_workspace, size_t workspace_bytes, int32_t *d_status,
                                   void *stream) {
+    HEP_NVTX("hep_moe_expert_ffn");
     return expert_ffn_fwd(d_rows, d_w13, d_w2, d_seg, n_seg, R, d_model, ffn, n_experts, d_h, d_y, nullptr,
                           d_workspace, workspace_bytes, d_status, stream);
 }
@@ -1385,6 +1384,7 @@ extern "C" int hep_moe_expert_ffn_train(const void *d_rows, const void *d_w13, c
                                         int n_seg, int64_t R, int64_t d_model, int64_t ffn, int n_experts, void *d_h,
                                         void *d_y, void *d_pre, void *d_workspace, size_t workspace_bytes,
                                         int32_t *d_status, void *stream) {
+    HEP_NVTX("hep_moe_expert_ffn_train");
     HEP_REQUIRE(d_pre, HEP_E_CONTRACT, "hep_moe_expert_ffn_train: d_pre required");
     return expert_ffn_fwd(d_rows, d_w13, d_w2, d_seg, n_seg, R, d_model, ffn, n_experts, d_h, d_y, d_pre, d_workspace,
                           workspace_bytes, d_status, stream);
@@ -1408,12 +1408,11 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
     int32_t *mt_rows = mt_row0 + cap;
     int32_t *exp_off = mt_rows + cap;
     const bool pairs = use_pairs(rows_hint >= 0 ? rows_hint : R, n_experts);
-    const char *pol_env = getenv("HEP_L2POL");
-    const int pol_mode = pol_env ? atoi(pol_env) : 0;
+    const int pol_mode = g_tuning.l2_policy;
     // Light experts (<= light_max rows: one 128-row tile) leave the CTA-pair kernel, whose
     // 256-row tiles would issue twice their useful MMA work, for a second launch of the
     // 1-CTA kernel on their own tile list.  Only with many experts (HEP_FFN_LIGHT_ROWS,
-    // 0 disables; the gather variant keeps one list).
+    // hep_tuning.ffn_light_rows, 0 disables; the gather variant keeps one list).
     const int light_max = ffn_light_max(rows_hint >= 0 ? rows_hint : R, n_experts, d_row_tok != nullptr);
     int32_t *mt_row0_l = exp_off + 2 * (n_experts + 1);
     int32_t *mt_rows_l = mt_row0_l + cap;
@@ -1438,19 +1437,13 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
     p.pol_mode = pol_mode;
     // experts whose rows fit one m-tile stream their weights exactly once: load them
     // evict-first so they do not push the reused panels of the other experts out of L2
-    // (DeepSeek-V3 shape 13.36 -> 12.87 ms, Qwen3 2.06 -> 2.00 ms; HEP_LIGHT_FIRST=0 disables)
-    const char *lf_env = getenv("HEP_LIGHT_FIRST");
-    p.light_first = lf_env ? atoi(lf_env) : 1;
-    const char *clk_env = getenv("HEP_FFN_CLOCK");
-    const bool clk = clk_env && clk_env[0] == '1';
+    // (DeepSeek-V3 shape 13.36 -> 12.87 ms, Qwen3 2.06 -> 2.00 ms; hep_tuning.light_first = 0 disables)
+    p.light_first = g_tuning.light_first;
+    const bool clk = g_tuning.ffn_clock == 1;
     p.clk_slot = clk ? 1 : 0;
     // raster bands (m-tiles swept across all N-blocks before the next band): 16 for the
     // SwiGLU GEMM, 8 for the down projection (profiles/r01/raster*.txt)
-    const char *gm_env = getenv("HEP_RASTER_GM");
-    const char *gm1_env = getenv("HEP_RASTER_GM1");
-    const char *gm2_env = getenv("HEP_RASTER_GM2");
-    const int gm_default = gm_env ? atoi(gm_env) : -1;
-    p.raster_gm = gm1_env ? atoi(gm1_env) : (gm_default >= 0 ? gm_default : 16);
+    p.raster_gm = g_tuning.raster_gm1;
     p.mt_row0 = mt_row0;
     p.mt_rows = mt_rows;
     p.exp_mt_off = exp_off;
@@ -1480,7 +1473,7 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
     p.gather_idx = nullptr;
     p.clk_slot = clk ? 2 : 0;
     p.row_addr = d_y_addr;
-    p.raster_gm = gm2_env ? atoi(gm2_env) : (gm_default >= 0 ? gm_default : 8);
+    p.raster_gm = g_tuning.raster_gm2;
     p.kblocks = (int)(ffn / BK);
     p.n_tiles = (int)(d_model / 256);
     p.b_rows_per_exp = d_model;
@@ -1522,6 +1515,7 @@ extern "C" int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, con
                                       const int64_t *d_expert_rows, int64_t Rcap, int64_t d_model, int64_t ffn,
                                       int n_experts, void *d_da13, void *d_dx_rows, float *d_dw13, float *d_dw2,
                                       void *d_workspace, size_t workspace_bytes, int32_t *d_status, void *stream) {
+    HEP_NVTX("hep_moe_expert_ffn_bwd");
     HEP_REQUIRE(d_rows && d_pre && d_h && d_dy && d_w13 && d_w2 && d_seg && d_expert_rows && d_da13 && d_dx_rows &&
                     d_dw13 && d_dw2 && d_workspace,
                 HEP_E_CONTRACT, "hep_moe_expert_ffn_bwd: null pointer");
@@ -1600,8 +1594,7 @@ extern "C" int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, con
     Params q{};
     q.grouped = 2;
     q.exp_rows = d_expert_rows;
-    const char *ord_env = getenv("HEP_WGRAD_ORDER");
-    if (!(ord_env && ord_env[0] == '0')) {
+    if (g_tuning.wgrad_order != 0) {
         int32_t *perm = exp_off_l + 2 * (n_experts + 1);  // after the two tile lists
         expert_order_kernel<<<1, 1024, 0, s>>>(d_expert_rows, n_experts, perm);
         HEP_CHECK_LAUNCH();
@@ -1655,6 +1648,7 @@ __global__ void splitk_reduce_kernel(const float4 *__restrict__ part, int S, int
 // dlogits is bf16 [T][E64], Wg is [E64][d] (E64 = experts padded to 64), T % 64 == 0.
 extern "C" int hep_router_bwd(const void *d_x, const void *d_wg, const void *d_dlogits, int64_t T, int64_t d_model,
                               int E64, float *d_dwg, void *d_dxg, void *stream) {
+    HEP_NVTX("hep_router_bwd");
     HEP_REQUIRE(d_x && d_wg && d_dlogits && d_dwg && d_dxg, HEP_E_CONTRACT, "hep_router_bwd: null pointer");
     HEP_REQUIRE(T % 64 == 0 && E64 % 64 == 0 && d_model % 256 == 0, HEP_E_DIMENSION,
                 "hep_router_bwd: T %% 64, E64 %% 64, d %% 256");
@@ -1706,7 +1700,7 @@ extern "C" int hep_router_bwd(const void *d_x, const void *d_wg, const void *d_d
 }
 
 // [gemm][start cycles, start ns, end cycles, end ns] of CTA 0 in the last FFN launched
-// with HEP_FFN_CLOCK=1 (diagnostic: the effective SM clock of the expert GEMMs)
+// with hep_tuning.ffn_clock = 1 (diagnostic: the effective SM clock of the expert GEMMs)
 extern "C" int hep_ffn_debug_clock(int64_t *host_out8) {
     HEP_REQUIRE(host_out8, HEP_E_CONTRACT, "null output");
     long long tmp[8];

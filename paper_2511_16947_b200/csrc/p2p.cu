@@ -35,12 +35,26 @@ __device__ __forceinline__ void chunk_bases(const int64_t *pair, int G, int me, 
 __global__ void __launch_bounds__(256) dispatch_p2p_kernel(const int4 *__restrict__ x, const int32_t *__restrict__ tok_row,
                                                            int64_t T, int K, int64_t nvec, int me, int G,
                                                            const int64_t *__restrict__ pair,
-                                                           const uint64_t *__restrict__ peer_recv) {
+                                                           const uint64_t *__restrict__ peer_recv,
+                                                           int64_t recv_capacity, const int32_t *status) {
     __shared__ int64_t sbase[HEP_MAX_GPUS + 1], rbase[HEP_MAX_GPUS];
     __shared__ uint64_t peer[HEP_MAX_GPUS];
-    if (threadIdx.x == 0) chunk_bases(pair, G, me, sbase, rbase);
+    __shared__ int skip;
+    if (threadIdx.x == 0) {
+        chunk_bases(pair, G, me, sbase, rbase);
+        // no valid schedule, or some destination would receive more rows than its buffer
+        // holds (every rank evaluates all destinations on the identical plan: they agree)
+        int f = status != nullptr && *status != 0;
+        for (int d = 0; d < G && !f; ++d) {
+            int64_t r = 0;
+            for (int s2 = 0; s2 < G; ++s2) r += pair[s2 * G + d];
+            f = recv_capacity > 0 && r > recv_capacity;
+        }
+        skip = f;
+    }
     if (threadIdx.x < G) peer[threadIdx.x] = peer_recv[threadIdx.x];
     __syncthreads();
+    if (skip) return;
     const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -154,6 +168,7 @@ __global__ void __launch_bounds__(256) p2p_barrier_kernel(const uint64_t *__rest
 using namespace hep;
 
 extern "C" int hep_p2p_barrier(const uint64_t *d_peer_flags, uint32_t *d_my_flags, int rank, int world, void *stream) {
+    HEP_NVTX("hep_p2p_barrier");
     HEP_REQUIRE(d_peer_flags && d_my_flags, HEP_E_CONTRACT, "hep_p2p_barrier: null pointer");
     HEP_REQUIRE(world >= 1 && world <= HEP_MAX_GPUS && rank >= 0 && rank < world, HEP_E_DIMENSION,
                 "hep_p2p_barrier: rank %d of %d", rank, world);
@@ -165,6 +180,7 @@ extern "C" int hep_p2p_barrier(const uint64_t *d_peer_flags, uint32_t *d_my_flag
 extern "C" int hep_p2p_allgather(const void *d_src, int64_t bytes, const uint64_t *d_peer_dst,
                                  const uint64_t *d_peer_flags, uint32_t *d_my_flags, int rank, int world,
                                  void *stream) {
+    HEP_NVTX("hep_p2p_allgather");
     HEP_REQUIRE(d_src && d_peer_dst && d_peer_flags && d_my_flags, HEP_E_CONTRACT, "hep_p2p_allgather: null pointer");
     HEP_REQUIRE(world >= 1 && world <= HEP_MAX_GPUS && rank >= 0 && rank < world && bytes >= 0 && bytes % 16 == 0,
                 HEP_E_DIMENSION, "hep_p2p_allgather: rank %d of %d, %lld bytes (multiple of 16)", rank, world,
@@ -177,7 +193,8 @@ extern "C" int hep_p2p_allgather(const void *d_src, int64_t bytes, const uint64_
 
 extern "C" int hep_moe_dispatch_p2p(const void *d_x, const int32_t *d_tok_row, int64_t T, int K, int64_t d_model,
                                     int rank, int num_gpus, const int64_t *d_pair, const uint64_t *d_peer_recv,
-                                    void *stream) {
+                                    int64_t recv_capacity, const int32_t *d_status, void *stream) {
+    HEP_NVTX("hep_moe_dispatch_p2p");
     HEP_REQUIRE(d_x && d_tok_row && d_pair && d_peer_recv, HEP_E_CONTRACT, "hep_moe_dispatch_p2p: null pointer");
     HEP_REQUIRE(d_model % 8 == 0 && K >= 1 && K <= 16 && num_gpus >= 1 && num_gpus <= HEP_MAX_GPUS && rank >= 0 &&
                     rank < num_gpus,
@@ -185,13 +202,14 @@ extern "C" int hep_moe_dispatch_p2p(const void *d_x, const int32_t *d_tok_row, i
     if (T <= 0) return HEP_OK;
     const int64_t warps = T < 148 * 64 ? T : 148 * 64;
     dispatch_p2p_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-        (const int4 *)d_x, d_tok_row, T, K, d_model / 8, rank, num_gpus, d_pair, d_peer_recv);
+        (const int4 *)d_x, d_tok_row, T, K, d_model / 8, rank, num_gpus, d_pair, d_peer_recv, recv_capacity, d_status);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
 }
 
 extern "C" int hep_moe_return_addr(const int64_t *d_pair, int rank, int num_gpus, const uint64_t *d_peer_back,
                                    int64_t row_bytes, int64_t capacity, uint64_t *d_addr, void *stream) {
+    HEP_NVTX("hep_moe_return_addr");
     HEP_REQUIRE(d_pair && d_peer_back && d_addr, HEP_E_CONTRACT, "hep_moe_return_addr: null pointer");
     HEP_REQUIRE(num_gpus >= 1 && num_gpus <= HEP_MAX_GPUS && rank >= 0 && rank < num_gpus && row_bytes % 16 == 0,
                 HEP_E_DIMENSION, "hep_moe_return_addr: G, rank, row_bytes %% 16");

@@ -443,6 +443,21 @@ __device__ int route_expert_topo(const SchedArgs &a, SchedSmem &s, int e, int64_
     return cnt;
 }
 
+// On a device-detected error the kernel leaves an EMPTY plan instead of the previous
+// micro-batch's: no integerized rows, no ranges, zero GPU loads and transfer counts, so
+// the kernels queued behind it on the stream (assignment, dispatch, FFN) see no work
+// rather than a stale schedule that no longer matches this micro-batch's top-K.
+__device__ void clear_outputs(const SchedArgs &a, int tid, int nt) {
+    const bool integ = a.flags & (HEP_SCHED_SOLVE | HEP_SCHED_INTEGERIZE);
+    if (integ && a.out.d_xi && a.out.d_xi != a.xi_in)
+        for (int i = tid; i < a.nnz; i += nt) a.out.d_xi[i] = 0;
+    if (integ && a.out.d_gpu_load)
+        for (int g = tid; g < a.G; g += nt) a.out.d_gpu_load[g] = 0;
+    if ((a.flags & HEP_SCHED_ROUTE) && a.out.d_n_ranges && tid == 0) *a.out.d_n_ranges = 0;
+    if ((a.flags & HEP_SCHED_ROUTE) && (a.flags & HEP_SCHED_TRANSFER) && a.out.d_transfer)
+        for (int i = tid; i < a.G * a.G + 8 * a.G + 2; i += nt) a.out.d_transfer[i] = 0;
+}
+
 template <int SPL>
 __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
     extern __shared__ __align__(16) char smem_raw[];
@@ -499,7 +514,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
     const int64_t total_all = block_sum_i64(my_total + base_sum, s.scan);
     if (solve && (__int128)total_all * a.Q >= ((__int128)1 << 56)) set_status(status, HEP_E_CAPACITY);
     __syncthreads();
-    if (*status) return;
+    if (*status) { clear_outputs(a, tid, nt); return; }
     prof_mark(a.flags, 1);
 
     if (solve) {
@@ -654,7 +669,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
         __syncthreads();
         prof_mark(a.flags, 4);
     }
-    if (*status) return;
+    if (*status) { clear_outputs(a, tid, nt); return; }
 
     // ---- step 6: Algorithm 1 routing (router.py:114-158) --------------------------
     if (route) {
@@ -731,7 +746,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
         __syncthreads();
         prof_mark(a.flags, 5);
     }
-    if (*status) return;
+    if (*status) { clear_outputs(a, tid, nt); return; }
 
     // ---- step 7: transfer plan (router.py:178-226) from the pair matrix ----------
     if (route && (a.flags & HEP_SCHED_TRANSFER)) {
@@ -826,9 +841,8 @@ static int launch_spl(hep_sched *h, const SchedArgs &a, size_t smem, cudaStream_
 
 static int launch_sched(hep_sched *h, SchedArgs &a, cudaStream_t stream) {
     // lex-min arc chain on 4 warps (2 subsets per thread, named barrier): 93.4K vs 97.6K
-    // cycles at E=256 (8 warps), 97.7K on 2 warps; HEP_SCHED_LEXMIN_WARPS=8 for the whole block
-    const char *lw = getenv("HEP_SCHED_LEXMIN_WARPS");
-    a.lexmin_warps = lw ? atoi(lw) : 4;
+    // cycles at E=256 (8 warps), 97.7K on 2 warps; hep_tuning.sched_lexmin_warps = 8 for the whole block
+    a.lexmin_warps = g_tuning.sched_lexmin_warps;
     a.G = h->G;
     a.E = h->E;
     a.nnz = h->nnz;
@@ -972,6 +986,7 @@ extern "C" int hep_sched_sizes(hep_sched_t h, int64_t *nnz, int64_t *max_ranges,
 
 extern "C" int hep_sched_solve(hep_sched_t h, const int64_t *d_loads, int64_t stride_e, int64_t stride_g,
                                const int64_t *d_base, int flags, const hep_sched_out *out, void *stream) {
+    HEP_NVTX("hep_sched_solve");
     HEP_REQUIRE(h && out && d_loads, HEP_E_CONTRACT, "hep_sched_solve: null argument");
     HEP_REQUIRE(out->d_status, HEP_E_CONTRACT, "hep_sched_solve: d_status required");
     SchedArgs a{};
@@ -988,6 +1003,7 @@ extern "C" int hep_sched_solve(hep_sched_t h, const int64_t *d_loads, int64_t st
 
 extern "C" int hep_sched_integerize(hep_sched_t h, const int64_t *d_xnum, int64_t den, const hep_sched_out *out,
                                     void *stream) {
+    HEP_NVTX("hep_sched_integerize");
     HEP_REQUIRE(h && out && d_xnum && out->d_xq == d_xnum, HEP_E_CONTRACT,
                 "hep_sched_integerize: pass the numerators in out->d_xq");
     HEP_REQUIRE(den > 0, HEP_E_CONTRACT, "denominator must be positive");
@@ -1001,6 +1017,7 @@ extern "C" int hep_sched_integerize(hep_sched_t h, const int64_t *d_xnum, int64_
 
 extern "C" int hep_sched_route(hep_sched_t h, const int64_t *d_loads, int64_t stride_e, int64_t stride_g,
                                const int64_t *d_xi, int flags, const hep_sched_out *out, void *stream) {
+    HEP_NVTX("hep_sched_route");
     HEP_REQUIRE(h && out && d_loads && d_xi, HEP_E_CONTRACT, "hep_sched_route: null argument");
     SchedArgs a{};
     a.flags = HEP_SCHED_ROUTE | (flags & (HEP_SCHED_TRANSFER | HEP_SCHED_TOPO | HEP_SCHED_PROFILE));
@@ -1044,6 +1061,7 @@ __global__ void split_kernel(const int64_t *loads, int64_t se, int64_t sg, int E
 extern "C" int hep_sched_pipelined(hep_sched_t h, const int64_t *d_loads, int64_t stride_e, int64_t stride_g,
                                    int64_t share_num, int64_t share_den, int flags, int64_t *d_split,
                                    const hep_sched_out *former, const hep_sched_out *latter, void *stream) {
+    HEP_NVTX("hep_sched_pipelined");
     HEP_REQUIRE(h && d_loads && d_split && former && latter, HEP_E_CONTRACT, "hep_sched_pipelined: null argument");
     HEP_REQUIRE(former->d_status && latter->d_status && former->d_status != latter->d_status, HEP_E_CONTRACT,
                 "hep_sched_pipelined: the two phases need distinct d_status words");
@@ -1084,6 +1102,7 @@ extern "C" int hep_sched_pipelined(hep_sched_t h, const int64_t *d_loads, int64_
 
 extern "C" int hep_transfer_plan(int num_gpus, int gpus_per_node, const int64_t *d_ranges, int64_t n_ranges,
                                  int64_t *d_transfer, int32_t *d_status, void *stream) {
+    HEP_NVTX("hep_transfer_plan");
     HEP_REQUIRE(num_gpus >= 1 && num_gpus <= HEP_MAX_GPUS, HEP_E_CAPACITY, "num_gpus=%d", num_gpus);
     HEP_REQUIRE(d_transfer && d_status, HEP_E_CONTRACT, "null output");
     transfer_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(num_gpus, gpus_per_node, d_ranges, n_ranges, d_transfer,

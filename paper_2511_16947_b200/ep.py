@@ -38,6 +38,7 @@ and the combine sums k in a fixed order).
 from __future__ import annotations
 
 import ctypes
+import math
 
 import torch
 
@@ -68,6 +69,10 @@ class LocalComm:
     def all_gather(self, parts: list[torch.Tensor]) -> list[torch.Tensor]:
         full = torch.cat(parts, dim=0)
         return [full for _ in parts]
+
+    def all_gather_int(self, v: int) -> list[int]:
+        """All ranks are driven from here with the caller's (checked) shapes."""
+        return [v]
 
     def exchange_ptrs(self, ptrs: list[int]) -> list[list[int]]:
         """Every rank's device address of a buffer, for every driven rank."""
@@ -123,6 +128,11 @@ class DistComm:
         chunks = [torch.empty_like(q) for _ in range(self.world)]
         self.dist.all_gather(chunks, q, group=self.group)
         return [torch.cat(chunks, dim=0).to(p.device)]
+
+    def all_gather_int(self, v: int) -> list[int]:
+        out = [None] * self.world
+        self.dist.all_gather_object(out, int(v), group=self.group)
+        return out
 
     def exchange_ptrs(self, ptrs: list[int]) -> list[list[int]]:
         """CUDA IPC: all-gather (handle, offset) of this rank's buffer, map the peers'."""
@@ -191,12 +201,17 @@ class EPRank:
 
     def p2p_buffers(self, layer: "EPMoELayer", T: int) -> dict:
         """Exchange buffers of the NVLink path, fixed addresses (peers write into them):
-        recv [G*T*K][d] (worst case: every assignment of every source lands here),
-        back [T*K][d] (send layout; peers' FFN epilogues return rows into it)."""
+        recv / h [cap][d] / [cap][F] with cap = ceil(recv_capacity_factor * T*K) rows
+        (at most G*T*K, every assignment of every source), back [T*K][d] (send layout;
+        peers' FFN epilogues return rows into it).  A balanced schedule delivers
+        gpu_load[r] ~ T*K rows to every rank (max/mean <= 1.05 with adaptive placement);
+        a micro-batch whose schedule would deliver more than cap rows to ANY rank is
+        detected on the device (hep_moe_assign_ep / hep_moe_dispatch_p2p, identical
+        verdict on every rank), exchanges nothing and raises CapacityError."""
         b = self.buffers(layer, T)
         if "recv" not in b:
             dev, K, G, d = layer.device, layer.K, layer.G, layer.d
-            cap = max(G * T * K, 1)
+            cap = max(min(G * T * K, math.ceil(layer.recv_capacity_factor * T * K)), 1)
             b["cap"] = cap
             b["recv"] = torch.empty(cap, d, dtype=torch.bfloat16, device=dev)
             b["back"] = torch.empty(max(T * K, 1), d, dtype=torch.bfloat16, device=dev)
@@ -243,8 +258,14 @@ class EPMoELayer:
     """
 
     def __init__(self, placement: Placement, d_model: int, ffn: int, top_k: int, comm, ranks, *, seed: int = 0,
-                 gate_bias: torch.Tensor | None = None, device=None, train: bool = False, exchange: str = "nccl"):
+                 gate_bias: torch.Tensor | None = None, device=None, train: bool = False, exchange: str = "nccl",
+                 recv_capacity_factor: float = 3.0):
+        """recv_capacity_factor: NVLink path receive buffers hold this many times T*K rows
+        per rank (see EPRank.p2p_buffers); the NCCL path sizes its buffers per call."""
         _lib.require_cuda()
+        if recv_capacity_factor <= 0:
+            raise ValueError("recv_capacity_factor must be positive")
+        self.recv_capacity_factor = float(recv_capacity_factor)
         if exchange not in ("nccl", "p2p"):
             raise ValueError("exchange must be 'nccl' (all-to-all-v collectives) or 'p2p' (NVLink peer stores)")
         if exchange == "p2p" and train:
@@ -300,9 +321,14 @@ class EPMoELayer:
             return self._forward(xs, st, events or {})
 
     def _peer_table(self, T: int) -> list:
-        """Per driven rank: device tables of every rank's receive / return buffer address."""
+        """Per driven rank: device tables of every rank's receive / return buffer address.
+        Building it is collective; it also checks that every rank has the same T (the
+        peer buffers' capacities and the peers' store addresses assume it)."""
         tab = self._peer_tables.get(T)
         if tab is None:
+            all_t = self.comm.all_gather_int(T) if hasattr(self.comm, "all_gather_int") else [T]
+            if any(t != T for t in all_t):
+                raise ValueError(f"the NVLink exchange needs the same token count on every rank, got {all_t}")
             bs = [rk.p2p_buffers(self, T) for rk in self.ranks]
             recv = self.comm.exchange_ptrs([b["recv"].data_ptr() for b in bs])
             back = self.comm.exchange_ptrs([b["back"].data_ptr() for b in bs])
@@ -327,6 +353,12 @@ class EPMoELayer:
                           for f, h, a, b in zip(flags, hall, pf, ph)]
         return self._sync
 
+    def check_status(self) -> None:
+        """Raise the reference exception class for a device-detected error of the last
+        micro-batch on any driven rank (scheduler, assignment, receive capacity)."""
+        for rk in self.ranks:
+            rk.sched.check_status(f"EPMoELayer rank {rk.rank}")
+
     def check_sync(self) -> None:
         """Raise if a device-side barrier of this layer gave up waiting for a peer."""
         for flags, _, _, _ in getattr(self, "_sync", None) or []:
@@ -349,6 +381,9 @@ class EPMoELayer:
         ck = _lib.check
         K, E, G, d, F = self.K, self.E, self.G, self.d, self.F
         T0 = xs[0].shape[0]
+        if any(x.shape[0] != T0 for x in xs):
+            raise ValueError("the NVLink exchange needs the same token count on every rank "
+                             f"(got {[x.shape[0] for x in xs]})")
         tabs = self._peer_table(T0)
         bs = []
         for rk, x in zip(self.ranks, xs):
@@ -376,12 +411,14 @@ class EPMoELayer:
             ck(L.hep_sched_solve(rk.sched.handle, h.data_ptr(), 1, hist_stride, None, HEP_SCHED_ALL,
                                  ctypes.byref(rk.sched.out), s), "hep_sched_solve")
             ck(L.hep_moe_assign_ep(rk.sched.handle, ctypes.byref(rk.sched.out), b["topk_idx"].data_ptr(), T, K,
-                                   rk.rank, b["tok_row"].data_ptr(), b["seg"].data_ptr(), b["counts"].data_ptr(),
-                                   b["assign_ws"].data_ptr(), b["assign_ws"].numel(), s), "hep_moe_assign_ep")
+                                   rk.rank, b["cap"], b["tok_row"].data_ptr(), b["seg"].data_ptr(),
+                                   b["counts"].data_ptr(), b["assign_ws"].data_ptr(), b["assign_ws"].numel(), s),
+               "hep_moe_assign_ep")
             if "a2a" in ev:
                 ev["a2a"][0].record(st)
             ck(L.hep_moe_dispatch_p2p(x.data_ptr(), b["tok_row"].data_ptr(), T, K, d, rk.rank, G,
-                                      rk.sched.transfer.data_ptr(), p_recv.data_ptr(), s), "hep_moe_dispatch_p2p")
+                                      rk.sched.transfer.data_ptr(), p_recv.data_ptr(), b["cap"],
+                                      rk.sched.status.data_ptr(), s), "hep_moe_dispatch_p2p")
             if "a2a" in ev:
                 ev["a2a"][1].record(st)
             ck(L.hep_moe_return_addr(rk.sched.transfer.data_ptr(), rk.rank, G, p_back.data_ptr(), d * 2, b["cap"],
@@ -435,7 +472,7 @@ class EPMoELayer:
             ck(L.hep_sched_solve(rk.sched.handle, h.data_ptr(), 1, E, None, HEP_SCHED_ALL,
                                  ctypes.byref(rk.sched.out), s), "hep_sched_solve")
             ck(L.hep_moe_assign_ep(rk.sched.handle, ctypes.byref(rk.sched.out), b["topk_idx"].data_ptr(), T, K,
-                                   rk.rank, b["tok_row"].data_ptr(), b["seg"].data_ptr(), b["counts"].data_ptr(),
+                                   rk.rank, 0, b["tok_row"].data_ptr(), b["seg"].data_ptr(), b["counts"].data_ptr(),
                                    b["assign_ws"].data_ptr(), b["assign_ws"].numel(), s), "hep_moe_assign_ep")
             ck(L.hep_moe_permute(x.data_ptr(), b["tok_row"].data_ptr(), T, K, d, b["send"].data_ptr(), s),
                "hep_moe_permute")

@@ -350,10 +350,18 @@ class MoELayer(torch.nn.Module):
                                 dx.data_ptr(), s), "hep_moe_gather_sum")
         return dx, dwg[:E], dw13, dw2
 
-    # combine_bwd, zero_pad x2, tiles x2, 4 GEMMs, gate_bwd, 2 router GEMMs (+ split-K sum), gather;
-    # + the weight-gradient expert order, + 4 (light-expert tile list x2, two 1-CTA dgrad GEMMs)
-    # when split (hep_moe_ffn_bwd_launches: 9 / 13 for the FFN part)
-    LAUNCHES_PER_BACKWARD = 15
+    def launches_per_backward(self, T: int) -> int:
+        """Kernels one backward_step on T tokens launches: combine^T, the expert-FFN backward
+        (hep_moe_ffn_bwd_launches: zero padding x2, tile lists, 4 GEMMs, weight-gradient
+        expert order, + the light-expert split), gate^T, the router backward (2 GEMMs, + the
+        split-K sum when its contraction is split) and the gather-sum."""
+        L = _lib.lib()
+        R = self.buffers(T).R
+        e64, d = self.e64, self.d
+        tiles = (e64 + 127) // 128 * (d // 256)
+        S = min(L.hep_device_sm_count() // max(tiles, 1), T // (2 * e64), T // 64)
+        router = 2 + (1 if S > 1 else 0)
+        return 1 + int(L.hep_moe_ffn_bwd_launches(R, self.E)) + 1 + router + 1
 
 
 class MoEFunction(torch.autograd.Function):
@@ -423,10 +431,19 @@ class HostPipeline:
         self.n += 1
         return self.n - 1
 
-    def result(self, ticket: int) -> torch.Tensor:
+    def result(self, ticket: int, copy: bool = False) -> torch.Tensor:
+        """Batch ``ticket``'s output in host memory.  Without ``copy`` this is the pinned
+        slot buffer itself: valid until ``depth`` more batches are submitted (the slot's
+        next D2H copy overwrites it); ``copy=True`` returns a private clone.  Raises for a
+        ticket whose slot was already reused."""
+        if ticket < 0 or ticket >= self.n:
+            raise ValueError(f"ticket {ticket} was never submitted")
+        if ticket < self.n - self.depth:
+            raise RuntimeError(f"ticket {ticket}: its slot was reused by ticket {ticket + self.depth} "
+                               f"(results live for {self.depth} submits; use result(..., copy=True) earlier)")
         i = ticket % self.depth
         self.ev_out[i].synchronize()
-        return self.out_host[i]
+        return self.out_host[i].clone() if copy else self.out_host[i]
 
     def drain(self):
         for e in self.ev_out:

@@ -345,14 +345,27 @@ def integerize_plan(plan: ReplicaLoadPlan) -> ReplicaLoadPlan:
     import torch
 
     exact = [[Fraction(v) for v in row] for row in plan.entries]
+    width = max(1, max((len(r) for r in exact), default=1))
     den = 1
     for row in exact:
         for v in row:
             den = math.lcm(den, v.denominator)
     nums = [[int(v * den) for v in row] for row in exact]
     biggest = max((abs(x) for row in nums for x in row), default=0)
-    if biggest * max(1, max((len(r) for r in nums), default=1)) >= (1 << 62):
-        raise CapacityError("plan entries too large for exact int64 integerization")
+    if biggest * width >= (1 << 62):
+        # The common denominator of arbitrary (e.g. float) entries overflows int64.  The
+        # rounding depends only on each entry's floor, the order of the fractional parts
+        # within an expert and the expert total (integral within 1e-6, reference :707-713,
+        # the same tolerance the device applies), so use the finest binary fixed point
+        # that fits: den = 2^k, entries rounded to nearest.  Exact for the scheduler's own
+        # plans (denominator Q); a float plan differs from the reference only if two
+        # fractional parts of one expert agree to within 2^-k.
+        top = max((abs(v) for row in exact for v in row), default=Fraction(0))
+        k = 61 - (int(top) + 1).bit_length() - width.bit_length()
+        if k < 20:
+            raise CapacityError("plan entries too large for int64 integerization")
+        den = 1 << k
+        nums = [[round(v * den) for v in row] for row in exact]
     placement = Placement(plan.num_gpus, plan.groups, tuple(range(len(plan.groups))))
     dev = device_scheduler(placement)
     flat = [x for row in nums for x in row]

@@ -67,3 +67,14 @@ def oracle_lib():
 
     oracle.build()
     return oracle
+
+
+@pytest.fixture
+def tune():
+    """tune(ffn_pair=1, ...) sets library launch-tuning fields (hep_tuning_set) for
+    the test; the previous values are restored afterwards."""
+    from paper_2511_16947_b200 import _lib
+
+    saved = _lib.get_tuning()
+    yield lambda **kw: _lib.set_tuning(**kw)
+    _lib.set_tuning(**saved)

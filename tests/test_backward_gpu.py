@@ -95,7 +95,7 @@ def test_autograd_function(P):
     assert w13.grad.float().abs().sum() > 0 and wg.grad[:8].float().abs().sum() > 0
 
 
-def test_backward_pair_and_single_cta_agree(P, monkeypatch):
+def test_backward_pair_and_single_cta_agree(P, tune):
     """The backward GEMMs (SwiGLU dgrad, dX dgrad, K-ragged weight gradients) on the
     CTA-pair kernel (256-row tiles, MN-major operand halves) and on the 1-CTA kernel:
     both within tolerance of fp32 autograd and identical bit for bit (same K order)."""
@@ -109,7 +109,7 @@ def test_backward_pair_and_single_cta_agree(P, monkeypatch):
     dout = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
     res = {}
     for pair in ("0", "1"):
-        monkeypatch.setenv("HEP_FFN_PAIR", pair)
+        tune(ffn_pair=int(pair))
         layer = P.MoELayer(pl, d, F, K, seed=2, gate_bias=bias, train=True)
         layer(x)
         res[pair] = [t.clone() for t in layer.backward_step(x, dout)]
@@ -124,9 +124,9 @@ def test_backward_pair_and_single_cta_agree(P, monkeypatch):
 
 
 @pytest.mark.parametrize("pair", ["0", "1"])
-def test_store_and_copy_widths_agree(P, monkeypatch, pair):
-    """256-bit epilogue stores / pre-activation loads (HEP_ST256) and the 256-bit
-    permute (HEP_LSU256) against their 128-bit fallbacks (taken for unaligned rows and
+def test_store_and_copy_widths_agree(P, tune, pair):
+    """256-bit epilogue stores / pre-activation loads (hep_tuning.st256) and the 256-bit
+    permute (hep_tuning.lsu256) against their 128-bit fallbacks (taken for unaligned rows and
     peer-row destinations): forward output and all gradients identical bit for bit."""
     G, E, K, d, F, T, s = 4, 8, 2, 512, 1024, 4096, 1.0
     pl = P.cayley_symmetric(P.ClusterShape(G, E, 2))
@@ -134,11 +134,11 @@ def test_store_and_copy_widths_agree(P, monkeypatch, pair):
     g = torch.Generator(device="cuda").manual_seed(23)
     x = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
     dout = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
-    monkeypatch.setenv("HEP_FFN_PAIR", pair)
+    tune(ffn_pair=int(pair))
     res = {}
     for wide in ("0", "1"):
-        monkeypatch.setenv("HEP_ST256", wide)
-        monkeypatch.setenv("HEP_LSU256", wide)
+        tune(st256=int(wide))
+        tune(lsu256=int(wide))
         layer = P.MoELayer(pl, d, F, K, seed=2, gate_bias=bias, train=True)
         y = layer(x).clone()
         b = layer.buffers(T)
@@ -149,21 +149,21 @@ def test_store_and_copy_widths_agree(P, monkeypatch, pair):
         assert torch.equal(a, b)
 
 
-def test_backward_light_expert_split(P, monkeypatch):
+def test_backward_light_expert_split(P, tune):
     """CTA-pair backward with the light experts' dgrad tiles on the 1-CTA kernel
-    (HEP_FFN_LIGHT_ROWS): gradients identical bit for bit to the unsplit backward."""
+    (hep_tuning.ffn_light_rows): gradients identical bit for bit to the unsplit backward."""
     G, E, K, d, F, T, s = 4, 64, 4, 256, 256, 8192, 1.5  # Cayley (p=2, q=5); R / E = 512 -> pairs
     pl = P.cayley_symmetric(P.ClusterShape(G, E, 2))
     bias = torch.tensor(P.zipf_gate_bias(E, s, 0))
     g = torch.Generator(device="cuda").manual_seed(29)
     x = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
     dout = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
-    monkeypatch.setenv("HEP_FFN_PAIR", "1")
+    tune(ffn_pair=1)
     from paper_2511_16947_b200 import _lib
 
     res = {}
     for lr in ("0", "256"):
-        monkeypatch.setenv("HEP_FFN_LIGHT_ROWS", lr)
+        tune(ffn_light_rows=int(lr))
         assert int(_lib.lib().hep_moe_ffn_bwd_launches(T * K, E)) == (9 if lr == "0" else 13)
         layer = P.MoELayer(pl, d, F, K, seed=3, gate_bias=bias, train=True)
         y = layer(x).clone()
@@ -176,8 +176,8 @@ def test_backward_light_expert_split(P, monkeypatch):
         assert torch.equal(a, b)
 
 
-def test_backward_wgrad_expert_order(P, monkeypatch):
-    """Weight-gradient tiles visited heaviest expert first (HEP_WGRAD_ORDER) or in
+def test_backward_wgrad_expert_order(P, tune):
+    """Weight-gradient tiles visited heaviest expert first (hep_tuning.wgrad_order) or in
     expert order: every output tile is one CTA's K-ordered sum, so the bits match."""
     G, E, K, d, F, T, s = 4, 64, 4, 256, 256, 8192, 1.5
     pl = P.cayley_symmetric(P.ClusterShape(G, E, 2))
@@ -187,9 +187,9 @@ def test_backward_wgrad_expert_order(P, monkeypatch):
     dout = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
     res = {}
     for pair in ("0", "1"):
-        monkeypatch.setenv("HEP_FFN_PAIR", pair)
+        tune(ffn_pair=int(pair))
         for order in ("0", "1"):
-            monkeypatch.setenv("HEP_WGRAD_ORDER", order)
+            tune(wgrad_order=int(order))
             layer = P.MoELayer(pl, d, F, K, seed=4, gate_bias=bias, train=True)
             layer(x)
             res[pair + order] = [t.clone() for t in layer.backward_step(x, dout)]

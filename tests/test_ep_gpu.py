@@ -166,13 +166,13 @@ def test_local_ep_p2p_exchange_matches_collectives(P, G, E, K, d, F, T, kind, s)
     assert torch.equal(sim(x), ref)
 
 
-def test_local_ep_p2p_light_split_on_pairs(P, monkeypatch):
+def test_local_ep_p2p_light_split_on_pairs(P, tune):
     """CTA pairs forced, so every rank's FFN splits its light slots onto the 1-CTA
     kernel: the peer-row (NVLink store) epilogue of both kernels, the collectives
     path and the single-device layer agree bit for bit."""
     from paper_2511_16947_b200.ep import EPMoELayer, LocalComm
 
-    monkeypatch.setenv("HEP_FFN_PAIR", "1")
+    tune(ffn_pair=1)
     G, E, K, d, F, T, s = 8, 128, 8, 256, 256, 8192, 1.5
     pl = _placement(P, G, E, "cayley", s)
     bias = torch.tensor(P.zipf_gate_bias(E, s, 0))

@@ -114,7 +114,7 @@ def _run_ffn(L, x, w13, w2, segs, R, d, F, E):
 
 
 @pytest.mark.parametrize("E,d,F", [(24, 512, 768), (40, 256, 256), (12, 512, 1024)])
-def test_grouped_ffn_skewed_sizes_pair_and_single(L, E, d, F, monkeypatch):
+def test_grouped_ffn_skewed_sizes_pair_and_single(L, E, d, F, tune):
     """Skewed expert sizes as a Zipf gate produces them: most experts carry a handful
     of rows (one partial m-tile), a few carry many tiles with a partial tail.  Both the
     1-CTA kernel (128-row tiles) and the CTA-pair kernel (256-row tiles) are checked
@@ -135,7 +135,7 @@ def test_grouped_ffn_skewed_sizes_pair_and_single(L, E, d, F, monkeypatch):
     x = torch.randn(R, d, device=dev).to(torch.bfloat16)
     outs = {}
     for pair in ("0", "1"):
-        monkeypatch.setenv("HEP_FFN_PAIR", pair)
+        tune(ffn_pair=int(pair))
         outs[pair] = _run_ffn(L, x, w13, w2, segs, R, d, F, E)
     for pair in ("0", "1"):
         h, y = outs[pair]
@@ -151,8 +151,8 @@ def test_grouped_ffn_skewed_sizes_pair_and_single(L, E, d, F, monkeypatch):
     assert torch.equal(outs["0"][1], outs["1"][1])
 
 
-def test_grouped_ffn_light_expert_split(L, monkeypatch):
-    """CTA pairs with the light experts (<= HEP_FFN_LIGHT_ROWS rows) split off to the
+def test_grouped_ffn_light_expert_split(L, tune):
+    """CTA pairs with the light experts (<= hep_tuning.ffn_light_rows rows) split off to the
     1-CTA kernel on their own tile list: every threshold (none, 128, 256, all experts
     light) gives the same bytes, and hep_moe_ffn_launches reports the extra launches."""
     from paper_2511_16947_b200.layer import init_expert_weights, interleave_w13
@@ -169,10 +169,10 @@ def test_grouped_ffn_light_expert_split(L, monkeypatch):
         row += sizes[e]
     R = row
     x = torch.randn(R, d, device="cuda").to(torch.bfloat16)
-    monkeypatch.setenv("HEP_FFN_PAIR", "1")
+    tune(ffn_pair=1)
     outs = {}
     for lr in ("0", "128", "256", "100000"):
-        monkeypatch.setenv("HEP_FFN_LIGHT_ROWS", lr)
+        tune(ffn_light_rows=int(lr))
         outs[lr] = _run_ffn(L, x, w13, w2, segs, R, d, F, E)
         assert int(L.lib().hep_moe_ffn_launches(R, E, 0)) == (4 if lr == "0" else 8)
     for lr in ("128", "256", "100000"):

@@ -29,16 +29,15 @@ x = torch.randn(T, d, device="cuda").to(torch.bfloat16)
 dout = torch.randn(T, d, device="cuda").to(torch.bfloat16)
 layer(x)
 variants = [v.strip() for v in args.variants.split(";")]
-base = dict(os.environ)
+from _tuning import apply as apply_tuning  # noqa: E402
+from paper_2511_16947_b200 import _lib  # noqa: E402
+
+base = _lib.get_tuning()
 res = {v: [] for v in variants}
 grads = {}
 for r in range(args.rounds):
     for v in variants:
-        os.environ.clear()
-        os.environ.update(base)
-        for kv in v.split():
-            k_, _, val = kv.partition("=")
-            os.environ[k_] = val
+        apply_tuning(v, base)
         g = layer.backward_step(x, dout)
         torch.cuda.synchronize()
         if v not in grads:
@@ -52,8 +51,7 @@ for r in range(args.rounds):
         en.record()
         torch.cuda.synchronize()
         res[v].append(st.elapsed_time(en) / args.iters)
-os.environ.clear()
-os.environ.update(base)
+_lib.set_tuning(**base)
 g0 = grads[variants[0]]
 for v in variants:
     same = grads[v] == g0

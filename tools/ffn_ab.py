@@ -7,8 +7,8 @@ decide the achieved clock).
 The layer is built and placed as in bench.py (Zipf s=1 gate bias; adaptive
 replacement when it beats Cayley), one forward fills the receive rows, then
 each variant launches `hep_moe_expert_ffn` `iters` times back to back; the
-variants cycle `rounds` times.  Env knobs are read by the library at every
-call, so variants switch in-process.  Prints one JSON line per variant.
+variants cycle `rounds` times.  Variants are applied with hep_tuning_set (tools/_tuning.py),
+read by the library at every call, so they switch in-process.  Prints one JSON line per variant.
 """
 
 from __future__ import annotations
@@ -80,18 +80,16 @@ def main():
     hnd = pynvml.nvmlDeviceGetHandleByIndex(0)
     variants = [v.strip() for v in args.variants.split(";")]
     res = {v: {"ms": [], "J": [], "mhz": []} for v in variants}
-    base_env = dict(os.environ)
+    from _tuning import apply as apply_tuning
+
+    base_tuning = _lib.get_tuning()
     ref_y = {}
     for _ in range(3):
         ffn()
     torch.cuda.synchronize()
     for r in range(args.rounds):
         for v in variants:
-            os.environ.clear()
-            os.environ.update(base_env)
-            for kv in v.split():
-                k, _, val = kv.partition("=")
-                os.environ[k] = val
+            apply_tuning(v, base_tuning)
             for _ in range(3):
                 ffn()
             torch.cuda.synchronize()
@@ -111,8 +109,7 @@ def main():
             res[v]["ms"].append(ms)
             res[v]["J"].append((e1 - e0) / 1000.0 / args.iters)
             res[v]["mhz"].append(mhz)
-    os.environ.clear()
-    os.environ.update(base_env)
+    _lib.set_tuning(**base_tuning)
     y0 = ref_y[variants[0]]
     for v in variants:
         ms = statistics.median(res[v]["ms"])

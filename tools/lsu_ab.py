@@ -1,4 +1,4 @@
-"""A/B the 128-bit vs 256-bit LSU permute (K5) kernel (HEP_LSU256=0/1, read per
+"""A/B the 128-bit vs 256-bit LSU permute (K5) kernel (hep_tuning.lsu256 = 0/1, read per
 call) at the bench shapes on a random row map, interleaved rounds; checks both
 variants write identical bytes.  (A 256-bit combine measured 5-10 % slower and was
 dropped, profiles/r01/ab_lsu_r01i.txt; the combine rows here time the kept kernel.)"""
@@ -31,7 +31,7 @@ for name, (T, d, K) in SHAPES.items():
         res, ref = {"0": [], "1": []}, {}
         for r in range(10):
             for v in ("0", "1"):
-                os.environ["HEP_LSU256"] = v
+                L.set_tuning(lsu256=int(v))
                 for _ in range(3):
                     fn()
                 torch.cuda.synchronize()
