@@ -17,6 +17,7 @@ path).  Rank 0 prints ONE JSON line.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -184,19 +185,29 @@ def run_reference(args):
     E, K, d, F, T, G = CONFIGS[cfg]
     cores, model = cpu_info()
     sample = args.cpu_sample or {"tiny": 1024, "mixtral": 128, "qwen3": 512, "dsv3": 128}[cfg]
-    for _ in range(args.warmup):
+    steps = args.steps  # each step is a bounded sample: K steps stay within a few minutes of host time
+    for _ in range(min(args.warmup, 2)):
         cpu_reference_step(cfg, args.skew, max(8, sample // 8))
-    per = []
-    for i in range(args.steps):
+    per, walls = [], []
+    for i in range(steps):
+        t0 = time.perf_counter()
         pt, info = cpu_reference_step(cfg, args.skew, sample, seed=i)
+        walls.append(time.perf_counter() - t0)
         per.append(pt)
     value = 1.0 / statistics.mean(per)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(per) * T,
+        "steps": steps, "warmup": args.warmup,
+        # the MEASURED wall time of one sampled step (sample tokens + one full scheduler solve)
+        "ms_per_step": 1e3 * statistics.mean(walls),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": CONFIG_TEXT[cfg], "tokens_per_microbatch": T, "sim_ep": G, "top_k": K,
                    "zipf_s": args.skew},
+        "sample_tokens": sample,
+        "extrapolated": True,
+        "extrapolation": (f"value = 1 / per-token time, per-token time = (router+FFN time of the {sample}-token "
+                          f"sample) / {sample} + (scheduler time of the full {G}x{E} micro-batch) / {T}; one "
+                          f"full {T}-token micro-batch would take {1e3 * T * statistics.mean(per):.0f} ms"),
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port",
                          "sample": f"{sample} tokens/step through router+top-K+SwiGLU FFN (numpy fp32, BLAS threads) + "
                                    f"the Dinic scheduler oracle on one full {G}x{E} micro-batch load matrix; "
@@ -402,8 +413,469 @@ def run_ep(args, world, rank, local, dev):
 
 
 # ---------------------------------------------------------------------------
-# our arm
+# our arm, N = 1: the EP group of G virtual GPUs simulated on the one device
 # ---------------------------------------------------------------------------
+def _events(n, keys):
+    import torch
+
+    return [{k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in keys}
+            for _ in range(n)]
+
+
+def _pool(T, d, dev, seeds):
+    """Distinct synthetic micro-batches, X ~ N(0, 1) bf16, one seed each."""
+    import torch
+
+    return [torch.randn(T, d, generator=torch.Generator(device=dev).manual_seed(s), device=dev).to(torch.bfloat16)
+            for s in seeds]
+
+
+def _policy(n_seen: int):
+    """The reference's ReplacementPolicy (adaptive.py:50-66) with the check after the
+    warm-up window: threshold 1.1, Monte-Carlo 200 samples, window = check interval =
+    the number of warm-up (seen) micro-batches."""
+    from paper_2511_16947_b200.adaptive import ReplacementPolicy
+
+    return ReplacementPolicy(check_interval=n_seen, threshold=1.1, window=n_seen, mc_samples=200)
+
+
+def _mm(gl):
+    mean = sum(gl) / len(gl)
+    return max(gl) / mean if mean else 1.0
+
+
+def _stat(vals):
+    return {"mean": statistics.mean(vals), "max": max(vals), "per_batch": [round(v, 6) for v in vals]}
+
+
+def heldout_balance(layer, static_ds, xs, stream):
+    """max/mean GPU load of each micro-batch in ``xs`` under the layer's current
+    placement and under the static placement ``static_ds`` (same device histogram,
+    two device solves)."""
+    import torch
+
+    E = layer.E
+    cur, sta = [], []
+    for x in xs:
+        gl = layer.schedule(x, stream)
+        b = layer.buffers(x.shape[0])
+        static_ds.launch_solve(b.hist, 1, E, None, 15, stream)
+        torch.cuda.synchronize()
+        layer.check_status()
+        static_ds.check_status("static placement")
+        cur.append(_mm(gl.cpu().tolist()))
+        sta.append(_mm(static_ds.gpu_load.cpu().tolist()))
+    return cur, sta
+
+
+def balance_sweep(layer, pl_static, shape, seen, unseen, skews, stream):
+    """Mixtral-shaped balance vs skew: for each Zipf s the
+    reference's adaptive policy is decided on the warm-up (seen) micro-batches only and
+    scored, with the static Cayley placement, on held-out micro-batches."""
+    import torch
+
+    import paper_2511_16947_b200 as P
+    from paper_2511_16947_b200.adaptive import LoadHistory, evaluate_and_maybe_replace
+    from paper_2511_16947_b200.scheduler import DeviceScheduler
+
+    E = layer.E
+    bias0 = layer.gate_bias.clone()
+    static_ds = DeviceScheduler(pl_static, device=layer.device)
+    out = {}
+    for s in skews:
+        layer.gate_bias.copy_(torch.tensor(P.zipf_gate_bias(E, s, 0)))
+        hist = LoadHistory(len(seen))
+        for x in seen:
+            layer.schedule(x, stream)
+            hist.push(layer.buffers(x.shape[0]).hist.sum(dim=0).cpu().tolist())
+        dec = evaluate_and_maybe_replace(pl_static, hist, _policy(len(seen)), shape, 0)
+        ada_ds = DeviceScheduler(dec.placement, device=layer.device)
+        ada, sta = [], []
+        for x in unseen:
+            layer.schedule(x, stream)
+            b = layer.buffers(x.shape[0])
+            for ds, acc in ((static_ds, sta), (ada_ds, ada)):
+                ds.launch_solve(b.hist, 1, E, None, 15, stream)
+                torch.cuda.synchronize()
+                ds.check_status("balance sweep")
+                acc.append(_mm(ds.gpu_load.cpu().tolist()))
+        out[f"{s:g}"] = {"static_cayley": _stat(sta), "adaptive": _stat(ada), "replaced": dec.replaced,
+                         "predicted_ratio_static": round(dec.predicted_ratio, 6)}
+    layer.gate_bias.copy_(bias0)
+    return out
+
+
+def sched_cpu_baseline(configs, n_mb=50, skip=5, seed=0, skew=1.0):
+    """the reference's per-micro-batch scheduling path (solve cold /
+    warm -> integerize -> route -> transfer plan) on the counts-mode load matrices
+    gen_zipf_workload(shape, s, T*K, 50, seed), 1 host core, median / p99 over the
+    micro-batches after the first 5 — timed on the oracle (C restatement of the
+    reference's Dinic algorithm, oracle/hep_oracle.c; the Python reference cannot run
+    on the GPU box) — beside the device scheduler (hep_sched_solve, all stages) on the
+    same matrices."""
+    import numpy as np
+    import torch
+
+    from oracle import oracle as O
+    import paper_2511_16947_b200 as P
+    from paper_2511_16947_b200.scheduler import DeviceScheduler
+
+    def q(v):
+        v = sorted(v)
+        return {"median_us": round(statistics.median(v), 2), "p99_us": round(v[min(len(v) - 1, int(0.99 * len(v)))], 2)}
+
+    out = {}
+    for cfg in configs:
+        E, K, d, F, T, G = CONFIGS[cfg]
+        shape = P.ClusterShape(G, E, 2)
+        pl = P.cayley_symmetric(shape)
+        groups = [tuple(g) for g in pl.edp_groups]
+        wl = P.gen_zipf_workload(shape, skew, (T // G) * K, n_mb, seed)
+        mats = [np.asarray(mb.as_array(), dtype=np.int64) for mb in wl.micro_batches]
+        cold, warm = [], []
+        state = O.OracleState(G, groups)
+        for m in mats:
+            t0 = time.perf_counter()
+            O.full_path(G, groups, m)  # fresh state: cold
+            cold.append(1e6 * (time.perf_counter() - t0))
+            t0 = time.perf_counter()
+            O.full_path(G, groups, m, state=state)  # reused state: warm
+            warm.append(1e6 * (time.perf_counter() - t0))
+        ds = DeviceScheduler(pl)
+        dl = torch.as_tensor(np.stack(mats)).cuda()
+        st = torch.cuda.current_stream()
+        dev = []
+        for i in range(len(mats)):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            ds.launch_solve(dl[i], G, 1, None, 15, st)
+            e1.record(st)
+            torch.cuda.synchronize()
+            dev.append(1e3 * e0.elapsed_time(e1))
+        ds.check_status("sched baseline")
+        out[cfg] = {"cpu_cold": q(cold[skip:]), "cpu_warm": q(warm[skip:]), "device": q(dev[skip:]),
+                    "matrices": f"gen_zipf_workload(ClusterShape({G},{E},2), s={skew}, tokens_per_gpu={(T // G) * K}, "
+                                f"{n_mb}, seed={seed}), Cayley placement; first {skip} excluded"}
+    cores, model = cpu_info()
+    return {"configs": out, "cores": 1, "host_cpu_count": cores, "host_cpu": model, "kind": "port",
+            "what": "oracle/hep_oracle.c (the reference's Dinic + lex-min + integerize + Algorithm 1 + transfer "
+                    "plan restated in C) per micro-batch through its ctypes wrapper, time.perf_counter; device = "
+                    "one hep_sched_solve launch (same stages), CUDA events"}
+
+
+def measure_config(cfg, args, dev, *, steps, primary):
+    """One workload: held-out protocol, CUDA-graph timed region, stage / kernel
+    breakdown, balance, e2e.  Returns the line's fields (primary) or a summary."""
+    import torch
+
+    import paper_2511_16947_b200 as P
+    from paper_2511_16947_b200 import _lib
+    from paper_2511_16947_b200.layer import HostPipeline
+    from paper_2511_16947_b200.runner import LayerRunner
+    from paper_2511_16947_b200.scheduler import DeviceScheduler
+
+    L = _lib.lib()
+    E, K, d, F, T, G = CONFIGS[cfg]
+    shape = P.ClusterShape(G, E, 2)
+    pl_static = P.cayley_symmetric(shape)
+    bias = torch.tensor(P.zipf_gate_bias(E, args.skew, 0)) if args.skew > 0 else None
+    layer = P.MoELayer(pl_static, d, F, K, seed=0, gate_bias=bias, device=dev,
+                       pipeline_ratio=args.pipeline_ratio if primary else None)
+    n_seen = max(1, args.batches // 2)
+    n_unseen = max(1, args.batches - n_seen)
+    seen = _pool(T, d, dev, range(1000, 1000 + n_seen))
+    unseen = _pool(T, d, dev, range(1000 + n_seen, 1000 + n_seen + n_unseen))
+    stream = torch.cuda.current_stream()
+
+    # --- warm-up micro-batches through the reference's run_strategy loop (LayerRunner):
+    # expert loads into the LoadHistory, the adaptive check after them (seen batches only)
+    adaptive = args.placement == "adaptive" and layer.static_share is None
+    runner = LayerRunner(layer, _policy(n_seen) if adaptive else None, shape=shape)
+    for i in range(max(n_seen, args.warmup)):
+        runner.step(seen[i % n_seen])
+    torch.cuda.synchronize()
+    layer.check_status()
+    warm_rows = runner.metrics()
+    if adaptive:
+        runner.check()  # runner.i == n_seen (or a multiple): the policy runs here
+    dec = runner.last_decision
+    replacement = runner.events[-1] if runner.events else (dec.to_event(runner.i) if dec is not None else None)
+    if replacement is not None and dec is not None:
+        replacement = dict(replacement, replaced=dec.replaced, predicted_ratio=round(dec.predicted_ratio, 6))
+    placement_desc = f"cayley_symmetric(G={G}, E={E}, d=2)"
+    if runner.events:
+        placement_desc = ("adaptive (reference policy on the warm-up micro-batches): greedy replica counts + "
+                          f"Monte-Carlo layout (200 samples) from cayley_symmetric(G={G}, E={E}, d=2)")
+    for x in seen[: min(3, n_seen)]:  # warm the adopted placement's launch paths
+        layer.run(x, layer.buffers(T), stream)
+    torch.cuda.synchronize()
+    layer.check_status()
+    bufs = layer.buffers(T)
+
+    # --- timed region: K CUDA-graph replays cycling over the held-out micro-batches
+    graphs = None
+    if not args.profile and not args.eager:
+        try:
+            graphs = [layer.capture(x) for x in unseen]
+            for g in graphs:
+                g.replay()
+            torch.cuda.synchronize()
+        except Exception as exc:  # capture is an optimisation; eager launches are the same kernels
+            print(f"[bench] CUDA graph capture failed ({exc}); timing eager launches", file=sys.stderr)
+            graphs = None
+    stages = ("router", "gate", "sched", "assign", "permute", "ffn", "combine")
+    sampler = ClockSampler(int(os.environ.get("LOCAL_RANK", "0"))) if (primary and not args.profile) else None
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.__enter__()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(stream)
+    for i in range(steps):
+        if graphs is not None:
+            graphs[i % n_unseen].replay()
+        else:
+            layer.run(unseen[i % n_unseen], bufs, stream)
+    end.record(stream)
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.__exit__()
+    layer.check_status()
+    t_ms = start.elapsed_time(end)
+    ms_per_step = t_ms / steps
+    value = T * steps / (t_ms / 1e3)
+    del graphs
+
+    # --- stage breakdown: eager steps with events around every stage
+    n_st = min(steps, 20)
+    evs = _events(n_st, stages)
+    for i in range(n_st):
+        layer.run(unseen[i % n_unseen], bufs, stream, events=evs[i])
+    torch.cuda.synchronize()
+    stage_ms = {k: statistics.mean(e[k][0].elapsed_time(e[k][1]) for e in evs) for k in stages}
+    ffn_ms = stage_ms["ffn"]
+
+    # --- the SM clock the expert GEMMs ran at (CTA-0 clock64 / globaltimer stamps)
+    ffn_clock = None
+    if primary and not args.profile:
+        import ctypes as _ct
+
+        with _lib.tuning(ffn_clock=1):
+            for i in range(min(steps, 10)):
+                layer.run(unseen[i % n_unseen], bufs, stream)
+            torch.cuda.synchronize()
+            stc = (_ct.c_int64 * 8)()
+            _lib.check(L.hep_ffn_debug_clock(stc), "hep_ffn_debug_clock")
+        mhz = [1e3 * (stc[4 * g + 2] - stc[4 * g]) / max(1, stc[4 * g + 3] - stc[4 * g + 1]) for g in range(2)]
+        ns = [stc[4 * g + 3] - stc[4 * g + 1] for g in range(2)]
+        ffn_clock = {"gemm1_mhz": round(mhz[0], 1), "gemm2_mhz": round(mhz[1], 1),
+                     "mhz": round((mhz[0] * ns[0] + mhz[1] * ns[1]) / max(1, ns[0] + ns[1]), 1),
+                     "source": "clock64 / globaltimer of CTA 0 across each expert GEMM (eager steps)"}
+
+    # --- scheduler latency: the K3 kernel alone on the last micro-batch's histogram
+    xl = unseen[(steps - 1) % n_unseen]
+    layer.run(xl, bufs, stream)
+    n_sched = 200
+    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s0.record(stream)
+    for _ in range(n_sched):
+        layer.sched.launch_solve(bufs.hist, 1, E, None, 15, stream)
+    s1.record(stream)
+    torch.cuda.synchronize()
+    sched_us = 1e3 * s0.elapsed_time(s1) / n_sched
+
+    # --- HBM-bound kernels re-launched back to back on that micro-batch (idempotent)
+    def _b2b_ms(fn, n=20):
+        fn()
+        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        q0.record(stream)
+        for _ in range(n):
+            fn()
+        q1.record(stream)
+        torch.cuda.synchronize()
+        return q0.elapsed_time(q1) / n
+
+    tps = T // G
+    cs = stream.cuda_stream
+    perm_ms = _b2b_ms(lambda: _lib.check(L.hep_moe_permute(xl.data_ptr(), bufs.tok_row.data_ptr(), T, K, d,
+                                                           bufs.rows.data_ptr(), cs), "permute"))
+    comb_ms = _b2b_ms(lambda: _lib.check(L.hep_moe_combine(bufs.y.data_ptr(), bufs.tok_row.data_ptr(),
+                                                           bufs.topk_w.data_ptr(), T, K, d, bufs.out.data_ptr(), cs),
+                                         "combine"))
+    chunk = None if layer.static_share is not None else bufs.assign_ws.data_ptr() + bufs.chunk_off
+    rg_ms = _b2b_ms(lambda: _lib.check(L.hep_router_topk(
+        xl.data_ptr(), layer.wg.data_ptr(), T, d, E, layer.e_pad, _lib.ptr(layer.gate_bias), K, tps, G,
+        bufs.logits.data_ptr(), bufs.topk_idx.data_ptr(), bufs.topk_w.data_ptr(), bufs.hist.data_ptr(), chunk, cs),
+        "router"))
+    layer.run(xl, bufs, stream)  # restore the micro-batch's own state after the re-launches
+    torch.cuda.synchronize()
+    layer.check_status()
+
+    # --- balance on the held-out micro-batches: the timed placement vs static Cayley
+    static_ds = DeviceScheduler(pl_static, device=dev)
+    if layer.static_share is None:
+        cur, sta = heldout_balance(layer, static_ds, unseen, stream)
+    else:  # pipelined: the device loads of the two phases (former + scheduled)
+        cur, sta = [], []
+        for x in unseen:
+            layer.run(x, bufs, stream)
+            torch.cuda.synchronize()
+            gl = (layer.sched.gpu_load + layer.sched.former.gpu_load).cpu().tolist()
+            cur.append(_mm(gl))
+        sta = cur
+    gpu_load = layer.sched.gpu_load.cpu().tolist()
+    m_num, m_den = layer.sched.m[:2].cpu().tolist()
+
+    # --- e2e through the public API with host buffers (pinned), HostPipeline
+    n_host = min(n_unseen, 4)
+    pipe = HostPipeline(layer, T)
+    xh = [unseen[i].cpu().pin_memory() for i in range(n_host)]
+    for i in range(3):
+        pipe.submit(xh[i % n_host])
+    pipe.drain()
+    torch.cuda.synchronize()
+    n_e2e = steps if primary else min(steps, 20)
+    t0 = time.perf_counter()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e0.record(pipe.s_in)
+    last = None
+    for i in range(n_e2e):
+        last = pipe.submit(xh[i % n_host])
+    out_last = pipe.result(last)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e1.record(pipe.s_out)
+    torch.cuda.synchronize()
+    e_ms = max(e0.elapsed_time(e1), (time.perf_counter() - t0) * 1e3)
+    e2e_value = T * n_e2e / (e_ms / 1e3)
+    assert torch.isfinite(out_last.float()).all()
+    del pipe, xh
+
+    hbm, tf_burst, tf_sus, peak_src = load_peaks()
+    R = T * K
+    ffn_flops = 6.0 * d * F * R
+    ffn_tflops = ffn_flops / (ffn_ms / 1e3) / 1e12
+    perm_bytes = T * d * 2 * (1 + K) + T * K * 4
+    comb_bytes = T * K * d * 2 + T * K * 4 * 2 + T * d * 2
+    rg_bytes = T * d * 2 + layer.e_pad * d * 2 + T * layer.e_pad * 4 + T * K * 8  # x, Wg, logits, top-K
+    traffic = load_traffic(cfg)
+    res = {
+        "value": value, "ms_per_step": ms_per_step, "steps": steps,
+        "config": {"workload": CONFIG_TEXT[cfg], "tokens_per_microbatch_per_gpu": T, "sim_ep": G,
+                   "tokens_per_virtual_gpu": T // G, "top_k": K, "d_model": d, "ffn": F, "experts": E,
+                   "placement": placement_desc,
+                   "schedule": ("harmony" if layer.static_share is None
+                                else f"harmony_pipelined (pipeline_ratio={args.pipeline_ratio})"),
+                   "zipf_s": args.skew, "pass": "forward",
+                   "launch": "cuda-graph replay" if not args.eager and not args.profile else "eager",
+                   "microbatches": f"{n_seen} warm-up (seen: placement decided on them) + {n_unseen} held-out "
+                                   f"(timed, cycled), seeds 1000..{1000 + n_seen + n_unseen - 1}",
+                   "l2": "inputs larger than L2 (x %.0f MB per micro-batch, expert weights %.2f GB per step)"
+                         % (T * d * 2 / 1e6, 3 * E * d * F * 2 / 1e9)},
+        "max_mean_gpu_load": statistics.mean(cur),
+        "max_mean_gpu_load_max": max(cur),
+        "max_mean_gpu_load_static_cayley": statistics.mean(sta),
+        "balance_heldout": {"timed_placement": _stat(cur), "static_cayley": _stat(sta),
+                            "protocol": "placement decided by the reference policy (adaptive.py:119-166) on the "
+                                        "warm-up micro-batches' expert loads only; max/mean of the integerized "
+                                        "per-GPU loads of each held-out micro-batch (device scheduler)"},
+        "replacement": replacement,
+        "m_exact_last": [m_num, m_den],
+        "gpu_loads_last": gpu_load,
+        "scheduler_us": sched_us,
+        "stage_ms": stage_ms,
+        "roofline": {
+            "bound": "tensor", "kernel": "hep_moe_expert_ffn (tcgen05 SwiGLU grouped GEMM x2)",
+            "achieved": ffn_tflops, "peak": tf_sus, "unit": "TFLOP/s", "frac": ffn_tflops / tf_sus,
+            "frac_of_burst_peak": ffn_tflops / tf_burst, "ffn_sm_clock": ffn_clock,
+            # dense bf16 tcgen05 rate at the clock the GEMMs ran at: 8192 flop/clk/SM x SMs
+            "frac_of_peak_at_ffn_clock": (ffn_tflops / (8192 * L.hep_device_sm_count() * ffn_clock["mhz"] * 1e6 / 1e12)
+                                          if ffn_clock else None),
+            "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside back-to-back steps)",
+            "algorithmic_flops_per_launch": ffn_flops,
+            # minimal DRAM bytes of one launch: every weight once, X read, H written + read, Y written
+            "algorithmic_bytes_per_launch": E * 3 * d * F * 2 + R * d * 2 * 2 + R * F * 2 * 2,
+            "traffic": traffic.get("ffn", {}).get("bytes"), "traffic_source": traffic.get("source"),
+        },
+        "hbm_kernels": {
+            "permute": {"GB/s": perm_bytes / (perm_ms / 1e3) / 1e9, "frac": perm_bytes / (perm_ms / 1e3) / 1e9 / hbm,
+                        "algorithmic_bytes": perm_bytes, "traffic": traffic.get("permute", {}).get("bytes")},
+            "combine": {"GB/s": comb_bytes / (comb_ms / 1e3) / 1e9, "frac": comb_bytes / (comb_ms / 1e3) / 1e9 / hbm,
+                        "algorithmic_bytes": comb_bytes, "traffic": traffic.get("combine", {}).get("bytes")},
+            # K1 fused router GEMM + gate: reads x and Wg, writes logits, top-K, weights
+            "router_gate": {"GB/s": rg_bytes / (rg_ms / 1e3) / 1e9, "frac": rg_bytes / (rg_ms / 1e3) / 1e9 / hbm,
+                            "algorithmic_bytes": rg_bytes, "us": 1e3 * rg_ms,
+                            "traffic": traffic.get("router_gate", {}).get("bytes")},
+            "timing": "each kernel re-launched 20x back to back on a held-out micro-batch, CUDA events",
+            "peak_GB/s": hbm,
+        },
+        "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": T * d * 2,
+                "d2h_bytes_per_step": T * d * 2},
+        "gpu_launches_per_step": layer.launches_per_forward(T),
+        "clocks": sampler.summary() if sampler else None,
+        "warmup_microbatch_metrics": [
+            {"index": m.index, "max_load": m.max_gpu_load, "balance_ratio": round(m.balance_ratio, 6),
+             "a2a_intra": m.a2a_intra, "local": m.local_volume, "layer_us": round(m.layer_time, 1)}
+            for m in warm_rows],
+    }
+    if primary and cfg == "mixtral" and layer.static_share is None and not args.profile and args.balance_sweep:
+        res["balance_sweep"] = balance_sweep(layer, pl_static, shape, seen, unseen, (1.0, 1.5, 2.0), stream)
+    if primary and not args.profile and not args.no_train:
+        res["train_step"] = measure_train(layer.placement, bias, cfg, unseen, dev, steps)
+    del layer, seen, unseen, bufs, static_ds
+    gc.collect()
+    torch.cuda.empty_cache()
+    return res
+
+
+def measure_train(placement, bias, cfg, xs, dev, steps):
+    """Forward + backward of the training layer (same kernels, 64-row aligned expert
+    blocks, pre-activations kept), reported beside the forward line."""
+    import torch
+
+    import paper_2511_16947_b200 as P
+
+    E, K, d, F, T, G = CONFIGS[cfg]
+    tl = P.MoELayer(placement, d, F, K, seed=0, gate_bias=bias, device=dev, train=True)
+    dout = torch.randn(T, d, generator=torch.Generator(device=dev).manual_seed(77), device=dev).to(torch.bfloat16)
+    stream = torch.cuda.current_stream()
+    for i in range(2):
+        tl(xs[i % len(xs)])
+        tl.backward_step(xs[i % len(xs)], dout)
+    torch.cuda.synchronize()
+    n_tr = max(3, steps // 5)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_tr)]
+    fev = _events(n_tr, ("ffn",))
+    t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0e.record(stream)
+    for i in range(n_tr):
+        x = xs[i % len(xs)]
+        tl.run(x, tl.buffers(T), stream, events=fev[i])
+        ev[i][0].record(stream)
+        tl.backward_step(x, dout)
+        ev[i][1].record(stream)
+    t1e.record(stream)
+    torch.cuda.synchronize()
+    tl.check_status()
+    tr_ms = t0e.elapsed_time(t1e) / n_tr
+    info = {
+        "tokens_per_s": T / (tr_ms / 1e3), "ms_per_step": tr_ms,
+        "backward_ms": statistics.mean(a.elapsed_time(b) for a, b in ev),
+        "expert_ffn_fwd_ms": statistics.mean(f["ffn"][0].elapsed_time(f["ffn"][1]) for f in fev),
+        "launches_per_step": tl.launches_per_forward(T) + tl.launches_per_backward(T),
+        "note": "forward + backward (dx, dWg, dW13, dW2) of the same layer, no optimizer; held-out micro-batches; "
+                "backward = combine^T, SwiGLU dgrad x2 + wgrad x2 (tcgen05), router^T, permute^T",
+        "steps": n_tr,
+    }
+    del tl
+    gc.collect()
+    torch.cuda.empty_cache()
+    return info
+
+
+OTHER_KEYS = ("value", "ms_per_step", "steps", "max_mean_gpu_load", "max_mean_gpu_load_max",
+              "max_mean_gpu_load_static_cayley", "replacement", "scheduler_us", "stage_ms", "e2e",
+              "gpu_launches_per_step")
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -413,6 +885,13 @@ def main():
     ap.add_argument("--config", default="mixtral", choices=sorted(CONFIGS))
     ap.add_argument("--skew", type=float, default=1.0)
     ap.add_argument("--placement", default="adaptive", choices=["adaptive", "cayley"])
+    ap.add_argument("--batches", type=int, default=16,
+                    help="distinct micro-batches: the first half warm up / feed the adaptive policy, the second "
+                         "half (held out) is timed")
+    ap.add_argument("--other-configs", default="qwen3,dsv3",
+                    help="also measure these configs (shorter) and fold them into the line ('' = none)")
+    ap.add_argument("--other-steps", type=int, default=40)
+    ap.add_argument("--no-balance-sweep", dest="balance_sweep", action="store_false")
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-train", action="store_true", help="skip the forward+backward training-step measurement")
@@ -424,6 +903,8 @@ def main():
                     help="N>1 token exchange: NVLink peer stores fused into the dispatch / GEMM kernels, or NCCL all-to-all-v")
     ap.add_argument("--eager", action="store_true", help="time eager launches instead of a CUDA-graph replay")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks/cpu legs)")
+    ap.add_argument("--tune", default="",
+                    help="library launch tuning for A/B runs, e.g. 'ffn_pair=0 raster_gm1=8' (hep_tuning_set)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if not args.profile else args.warmup
     if args.impl == "reference":
@@ -433,9 +914,13 @@ def main():
     import torch
     import torch.distributed as dist
 
-    import paper_2511_16947_b200 as P
     from paper_2511_16947_b200 import _lib
 
+    if args.tune:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from _tuning import apply as apply_tuning
+
+        apply_tuning(args.tune)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -448,340 +933,55 @@ def main():
         else:
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-
-    E, K, d, F, T, G = CONFIGS[args.config]
     if world > 1:
         run_ep(args, world, rank, local, dev)
         return
-    shape = P.ClusterShape(G, E, 2)
-    pl = P.cayley_symmetric(shape)
-    bias = torch.tensor(P.zipf_gate_bias(E, args.skew, 0)) if args.skew > 0 else None
-    layer = P.MoELayer(pl, d, F, K, seed=0, gate_bias=bias, device=dev, pipeline_ratio=args.pipeline_ratio)
-    gx = torch.Generator(device=dev).manual_seed(1000 + rank)
-    x = torch.randn(T, d, generator=gx, device=dev).to(torch.bfloat16)
-    bufs = layer.buffers(T)
-    stream = torch.cuda.current_stream()
-    L = _lib.lib()
+    _lib.require_cuda()
 
-    def step():
-        layer.run(x, layer.buffers(T), stream)
-
-    def gpu_balance():
-        gl = layer.sched.gpu_load.cpu().tolist()
-        mean = sum(gl) / len(gl)
-        return (max(gl) / mean if mean else 1.0), gl
-
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    layer.check_status()
-    static_max_mean, static_loads = gpu_balance()
-    placement_desc = f"cayley_symmetric(G={G}, E={E}, d=2)"
-    replacement = None
-    if args.placement == "adaptive":
-        # the paper's adaptive replacement (adaptive.py:119-166): score the static
-        # placement on the observed expert loads and adopt the greedy + Monte-Carlo
-        # candidate when it is better; a one-off, off the per-micro-batch path
-        from paper_2511_16947_b200.adaptive import LoadHistory, ReplacementPolicy, evaluate_and_maybe_replace
-
-        hist = LoadHistory(8)
-        hist.push(layer.expert_loads(T))
-        dec = evaluate_and_maybe_replace(pl, hist, ReplacementPolicy(threshold=1.0, mc_samples=200), shape, 0)
-        replacement = dec.to_event(args.warmup)
-        if dec.replaced:
-            layer.set_placement(dec.placement)
-            placement_desc = (f"adaptive: greedy replica counts {list(P.placement.greedy_replica_counts(hist.entries[0], E * 2, max_count=G))}"
-                              f" + Monte-Carlo layout (200 samples), from cayley_symmetric(G={G}, E={E}, d=2)")
-            for _ in range(args.warmup):
-                step()
-            torch.cuda.synchronize()
-            layer.check_status()
-    bufs = layer.buffers(T)
-
-    # --- timed region: K steps back to back; per-stage events on the launching stream
-    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-
-    stages = ("router", "gate", "sched", "assign", "permute", "ffn", "combine")
-    evs = [{k: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for k in stages}
-           for _ in range(args.steps)]
-
-    def staged_step(i):
-        layer.run(x, bufs, stream, events=evs[i])
-
-    # the timed step is one CUDA-graph replay of the whole forward (11 kernels, no host
-    # sync); per-stage times come from an eager pass with events around each stage
-    graph = None
-    if not args.profile and not args.eager:
-        try:
-            graph = layer.capture(x)
-            for _ in range(2):
-                graph.replay()
-            torch.cuda.synchronize()
-        except Exception as exc:  # capture is an optimisation; eager launches are the same kernels
-            print(f"[bench] CUDA graph capture failed ({exc}); timing eager launches", file=sys.stderr)
-            graph = None
-    sampler = ClockSampler(local) if not args.profile else None
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    if sampler:
-        sampler.__enter__()
-    start.record(stream)
-    for i in range(args.steps):
-        if graph is not None:
-            graph.replay()
-        else:
-            staged_step(i)
-    end.record(stream)
-    torch.cuda.synchronize()
-    if sampler:
-        sampler.__exit__()
-    if world > 1:
-        dist.barrier()
-    layer.check_status()
-    t_ms = start.elapsed_time(end)
-    if world > 1:
-        tt = torch.tensor([t_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = float(tt.item())
-    ms_per_step = t_ms / args.steps
-    value = world * T * args.steps / (t_ms / 1e3)
-    if graph is not None:  # stage breakdown from eager steps
-        for i in range(args.steps):
-            staged_step(i)
-        torch.cuda.synchronize()
-
-    stage_ms = {k: statistics.mean(e[k][0].elapsed_time(e[k][1]) for e in evs) for k in stages}
-    ffn_ms, perm_ms, comb_ms = stage_ms["ffn"], stage_ms["permute"], stage_ms["combine"]
-
-    # --- the SM clock the expert GEMMs actually ran at: CTA 0 stamps clock64 and the
-    # global timer at entry/exit of each GEMM (hep_tuning.ffn_clock = 1), eager steps back to back
-    ffn_clock = None
+    res = measure_config(args.config, args, dev, steps=args.steps, primary=True)
+    others = {}
     if not args.profile:
-        import ctypes as _ct
-
-        with _lib.tuning(ffn_clock=1):
-            for i in range(min(args.steps, 10)):
-                staged_step(i)
-            torch.cuda.synchronize()
-            st = (_ct.c_int64 * 8)()
-            _lib.check(L.hep_ffn_debug_clock(st), "hep_ffn_debug_clock")
-            mhz = [1e3 * (st[4 * g + 2] - st[4 * g]) / max(1, st[4 * g + 3] - st[4 * g + 1]) for g in range(2)]
-            ns = [st[4 * g + 3] - st[4 * g + 1] for g in range(2)]
-            ffn_clock = {"gemm1_mhz": round(mhz[0], 1), "gemm2_mhz": round(mhz[1], 1),
-                         "mhz": round((mhz[0] * ns[0] + mhz[1] * ns[1]) / max(1, ns[0] + ns[1]), 1),
-                         "source": "clock64 / globaltimer of CTA 0 across each expert GEMM (eager steps)"}
-
-    # --- scheduler latency: the K3 kernel alone, on this micro-batch's histogram
-    n_sched = 200
-    s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s0.record(stream)
-    for _ in range(n_sched):
-        layer.sched.launch_solve(bufs.hist, 1, E, None, 15, stream)
-    s1.record(stream)
-    torch.cuda.synchronize()
-    sched_us = 1e3 * s0.elapsed_time(s1) / n_sched
-
-    # --- the HBM-bound kernels re-launched back to back on this micro-batch (they are
-    # idempotent), so the host's eager launch latency does not enter their bandwidth
-    def _b2b_ms(fn, n=20):
-        fn()
-        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        q0.record(stream)
-        for _ in range(n):
-            fn()
-        q1.record(stream)
-        torch.cuda.synchronize()
-        return q0.elapsed_time(q1) / n
-
-    tps = T // G
-    perm_ms = _b2b_ms(lambda: _lib.check(L.hep_moe_permute(x.data_ptr(), bufs.tok_row.data_ptr(), T, K, d,
-                                                           bufs.rows.data_ptr(), stream.cuda_stream), "permute"))
-    comb_ms = _b2b_ms(lambda: _lib.check(L.hep_moe_combine(bufs.y.data_ptr(), bufs.tok_row.data_ptr(),
-                                                           bufs.topk_w.data_ptr(), T, K, d, bufs.out.data_ptr(),
-                                                           stream.cuda_stream), "combine"))
-    chunk = None if layer.static_share is not None else bufs.assign_ws.data_ptr() + bufs.chunk_off
-    rg_ms = _b2b_ms(lambda: _lib.check(L.hep_router_topk(
-        x.data_ptr(), layer.wg.data_ptr(), T, d, E, layer.e_pad, _lib.ptr(layer.gate_bias), K, tps, G,
-        bufs.logits.data_ptr(), bufs.topk_idx.data_ptr(), bufs.topk_w.data_ptr(), bufs.hist.data_ptr(), chunk,
-        stream.cuda_stream), "router"))
-    torch.cuda.synchronize()
-    layer.check_status()
-
-    gpu_load = layer.sched.gpu_load.cpu().tolist()
-    m_num, m_den = layer.sched.m[:2].cpu().tolist()
-    mean_load = sum(gpu_load) / len(gpu_load)
-    max_mean = max(gpu_load) / mean_load if mean_load else 1.0
-
-    # --- e2e through the public API with host buffers (pinned): every step copies
-    # its input batch host->device and its output device->host inside the timed
-    # region (HostPipeline overlaps batch i+1's H2D and batch i-1's D2H with batch i)
-    from paper_2511_16947_b200.layer import HostPipeline
-
-    pipe = HostPipeline(layer, T)
-    xh = [x.cpu().pin_memory() for _ in range(2)]
-    for i in range(3):
-        pipe.submit(xh[i % 2])
-    pipe.drain()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e0.record(pipe.s_in)
-    last = None
-    for i in range(args.steps):
-        last = pipe.submit(xh[i % 2])
-    out_last = pipe.result(last)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e1.record(pipe.s_out)
-    torch.cuda.synchronize()
-    e_ms = e0.elapsed_time(e1)
-    e_wall = (time.perf_counter() - t0) * 1e3
-    e_ms = max(e_ms, e_wall)  # device span from first H2D to last D2H, never below the host clock
-    if world > 1:
-        tt = torch.tensor([e_ms], device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e_ms = float(tt.item())
-    e2e_value = world * T * args.steps / (e_ms / 1e3)
-    assert torch.isfinite(out_last.float()).all()
-
-    # --- training step (forward + backward through the same kernels), reported beside
-    train_info = None
-    if not args.profile and not args.no_train:
-        del pipe
-        tl = P.MoELayer(layer.placement, d, F, K, seed=0, gate_bias=bias, device=dev, train=True)
-        dout = torch.randn(T, d, generator=torch.Generator(device=dev).manual_seed(77), device=dev).to(torch.bfloat16)
-        for _ in range(2):
-            tl(x)
-            tl.backward_step(x, dout)
-        torch.cuda.synchronize()
-        n_tr = max(3, args.steps // 5)
-        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(n_tr)]
-        fev = [{"ffn": (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))} for _ in range(n_tr)]
-        t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        t0e.record(stream)
-        for i in range(n_tr):
-            tl.run(x, tl.buffers(T), stream, events=fev[i])
-            ev[i][0].record(stream)
-            tl.backward_step(x, dout)
-            ev[i][1].record(stream)
-        t1e.record(stream)
-        torch.cuda.synchronize()
-        tl.check_status()
-        tr_ms = t0e.elapsed_time(t1e) / n_tr
-        bwd_ms = statistics.mean(a.elapsed_time(b) for a, b in ev)
-        ffn_f = statistics.mean(f["ffn"][0].elapsed_time(f["ffn"][1]) for f in fev)
-        train_info = {
-            "tokens_per_s": T / (tr_ms / 1e3),
-            "ms_per_step": tr_ms,
-            "backward_ms": bwd_ms,
-            "expert_ffn_fwd_ms": ffn_f,
-            "note": "forward + backward (dx, dWg, dW13, dW2) of the same layer, no optimizer; "
-                    "backward = combine^T, SwiGLU dgrad x2 + wgrad x2 (tcgen05), router^T, permute^T",
-            "steps": n_tr,
-        }
-        del tl
-        torch.cuda.empty_cache()
-
-    hbm, tf_burst, tf_sus, peak_src = load_peaks()
-    traffic = load_traffic(args.config)
-    R = T * K
-    ffn_flops = 6.0 * d * F * R
-    ffn_tflops = ffn_flops / (ffn_ms / 1e3) / 1e12
-    perm_bytes = T * d * 2 * (1 + K) + T * K * 4
-    comb_bytes = T * K * d * 2 + T * K * 4 * 2 + T * d * 2
-    rg_bytes = T * d * 2 + layer.e_pad * d * 2 + T * layer.e_pad * 4 + T * K * 8  # x, Wg, logits, top-K
-    launches_per_step = layer.launches_per_forward(T)
-
-    if rank == 0:
-        cores, model = cpu_info()
-        cpu_line = None
-        if not args.no_cpu_baseline and not args.profile:
-            sample = args.cpu_sample or {"tiny": 1024, "mixtral": 128, "qwen3": 512, "dsv3": 128}[args.config]
-            per = []
-            for i in range(3):
-                pt, info = cpu_reference_step(args.config, args.skew, sample, seed=i)
-                per.append(pt)
-            cpu_line = {"value": 1.0 / statistics.mean(per), "unit": "tokens/s", "cores": cores, "kind": "port",
-                        "sample": f"{sample} tokens x 3 steps through the CPU restatement (router+top-K+SwiGLU FFN "
-                                  f"numpy fp32 on all host threads) + Dinic scheduler oracle on a full {G}x{E} "
-                                  f"micro-batch; host: {model}"}
-        line = {
-            "metric": METRIC,
-            "value": value,
-            "unit": "tokens/s",
-            "n_gpus": world,
-            "steps": args.steps,
-            "warmup": args.warmup,
-            "ms_per_step": ms_per_step,
-            "higher_is_better": True,
-            "scaling": "weak",
-            "vs_baseline": None,
-            "dtype": "bf16",
-            "data": "synthetic",
-            "config": {
-                "workload": CONFIG_TEXT[args.config],
-                "tokens_per_microbatch_per_gpu": T,
-                "sim_ep": G,
-                "tokens_per_virtual_gpu": T // G,
-                "top_k": K, "d_model": d, "ffn": F, "experts": E,
-                "placement": placement_desc,
-                "schedule": ("harmony" if args.pipeline_ratio is None
-                             else f"harmony_pipelined (pipeline_ratio={args.pipeline_ratio})"),
-                "zipf_s": args.skew,
-                "pass": "forward",
-                "launch": "cuda-graph replay" if graph is not None else "eager",
-                "l2": "inputs larger than L2 (x %.0f MB, expert weights %.2f GB per step)" % (T * d * 2 / 1e6,
-                                                                                               3 * E * d * F * 2 / 1e9),
-            },
-            "max_mean_gpu_load": max_mean,
-            "max_mean_gpu_load_static_cayley": static_max_mean,
-            "replacement": replacement,
-            "m_exact": [m_num, m_den],
-            "gpu_loads": gpu_load,
-            "scheduler_us": sched_us,
-            "stage_ms": stage_ms,
-            "roofline": {
-                "bound": "tensor",
-                "kernel": "hep_moe_expert_ffn (tcgen05 SwiGLU grouped GEMM x2)",
-                "achieved": ffn_tflops,
-                "peak": tf_sus,
-                "unit": "TFLOP/s",
-                "frac": ffn_tflops / tf_sus,
-                "frac_of_burst_peak": ffn_tflops / tf_burst,
-                # dense bf16 tcgen05 rate at the clock the GEMMs ran at: 8192 flop/clk/SM x 148 SMs
-                "ffn_sm_clock": ffn_clock,
-                "frac_of_peak_at_ffn_clock": (ffn_tflops / (8192 * L.hep_device_sm_count() * ffn_clock["mhz"] * 1e6 / 1e12)
-                                              if ffn_clock else None),
-                "peak_source": f"{peak_src} bf16_tflops_sustained (kernel timed inside back-to-back steps)",
-                "algorithmic_flops_per_launch": ffn_flops,
-                # minimal DRAM bytes of one launch: every weight once, X read, H written + read, Y written
-                "algorithmic_bytes_per_launch": E * 3 * d * F * 2 + R * d * 2 * 2 + R * F * 2 * 2,
-                "traffic": traffic.get("ffn", {}).get("bytes"),
-                "traffic_source": traffic.get("source"),
-            },
-            "hbm_kernels": {
-                "permute": {"GB/s": perm_bytes / (perm_ms / 1e3) / 1e9, "frac": perm_bytes / (perm_ms / 1e3) / 1e9 / hbm,
-                            "algorithmic_bytes": perm_bytes, "traffic": traffic.get("permute", {}).get("bytes")},
-                "combine": {"GB/s": comb_bytes / (comb_ms / 1e3) / 1e9, "frac": comb_bytes / (comb_ms / 1e3) / 1e9 / hbm,
-                            "algorithmic_bytes": comb_bytes, "traffic": traffic.get("combine", {}).get("bytes")},
-                # K1 fused router GEMM + gate: reads x and Wg, writes logits, top-K, weights
-                "router_gate": {"GB/s": rg_bytes / (rg_ms / 1e3) / 1e9, "frac": rg_bytes / (rg_ms / 1e3) / 1e9 / hbm,
-                                "algorithmic_bytes": rg_bytes, "traffic": traffic.get("router_gate", {}).get("bytes")},
-                "timing": "each kernel re-launched 20x back to back on the step's data, CUDA events",
-                "peak_GB/s": hbm,
-            },
-            "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": T * d * 2,
-                    "d2h_bytes_per_step": T * d * 2},
-            "gpu_launches": launches_per_step * args.steps,
-            "clocks": sampler.summary() if sampler else None,
-            "cpu_baseline": cpu_line,
-            "train_step": train_info,
-        }
-        print(json.dumps(line))
-    if world > 1:
-        dist.destroy_process_group()
+        for c in [c.strip() for c in args.other_configs.split(",") if c.strip()]:
+            if c == args.config or c not in CONFIGS:
+                continue
+            o = measure_config(c, args, dev, steps=args.other_steps, primary=False)
+            others[c] = {k: o[k] for k in OTHER_KEYS}
+            others[c]["roofline"] = {k: o["roofline"][k] for k in ("achieved", "peak", "unit", "frac",
+                                                                   "frac_of_burst_peak", "traffic")}
+            others[c]["hbm_kernels"] = {k: {"GB/s": v["GB/s"], "frac": v["frac"]}
+                                        for k, v in o["hbm_kernels"].items() if isinstance(v, dict)}
+            others[c]["workload"] = o["config"]["workload"]
+    E, K, d, F, T, G = CONFIGS[args.config]
+    cores, model = cpu_info()
+    cpu_line = sched_base = None
+    if not args.no_cpu_baseline and not args.profile:
+        sample = args.cpu_sample or {"tiny": 1024, "mixtral": 128, "qwen3": 512, "dsv3": 128}[args.config]
+        per, walls = [], []
+        for i in range(3):
+            t0 = time.perf_counter()
+            pt, info = cpu_reference_step(args.config, args.skew, sample, seed=i)
+            walls.append(time.perf_counter() - t0)
+            per.append(pt)
+        cpu_line = {"value": 1.0 / statistics.mean(per), "unit": "tokens/s", "cores": cores, "kind": "port",
+                    "sample": f"{sample} tokens x 3 steps through the CPU restatement (router+top-K+SwiGLU FFN "
+                              f"numpy fp32 on all host threads) + Dinic scheduler oracle on a full {G}x{E} "
+                              f"micro-batch; tokens/s extrapolated from the sample; host: {model}",
+                    "sample_step_wall_ms": [round(1e3 * w, 1) for w in walls], "extrapolated": True}
+        sched_base = sched_cpu_baseline(["mixtral", "qwen3", "dsv3"])
+    line = {
+        "metric": METRIC, "value": res["value"], "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": res["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": res["config"],
+    }
+    for k, v in res.items():
+        if k not in ("value", "ms_per_step", "steps", "config", "gpu_launches_per_step"):
+            line[k] = v
+    line["gpu_launches"] = res["gpu_launches_per_step"] * args.steps
+    line["cpu_baseline"] = cpu_line
+    line["scheduler_cpu_baseline"] = sched_base
+    line["other_configs"] = others or None
+    line["tuning"] = _lib.get_tuning()
+    print(json.dumps(line))
 
 
 if __name__ == "__main__":

@@ -42,9 +42,12 @@ enum Epi { EPI_SWIGLU = 0, EPI_BF16 = 1, EPI_F32 = 2, EPI_SWIGLU_BWD = 3, EPI_GA
 // logit row and the epilogue thread selects its top-K, the softmax weights and
 // counts the load-matrix histogram without the logits ever leaving the SM.
 constexpr int kGateMaxK = 8;
-constexpr int kGateMaxSrc = 16;
+constexpr int kGateMaxSrc = HEP_MAX_GPUS;
 constexpr int kGateMaxE = 256;
-constexpr int kGateSmemBytes = 4 * (kGateMaxSrc * kGateMaxE + 3 * kGateMaxE);
+// [n_src][E] histogram, [3][E] chunk counters of a tile (a tile of <= 128 rows touches at
+// most 3 aligned 64-token chunks), [E] bias, and the column-half merge buffers
+// (128 rows x KG x (key, expert, logit))
+constexpr int kGateSmemBytes = 4 * (kGateMaxSrc * kGateMaxE + 4 * kGateMaxE) + 128 * kGateMaxK * 12;
 struct GateParams {
     const float *bias;   // [E] selection bias or null
     int K, E;            // top-K, experts (columns >= E are padding)
@@ -95,8 +98,9 @@ struct Params {
     int light_first;  // grouped: weights of single-m-tile experts loaded evict-first
     int k_split;      // mode 0: contraction split into k_split ranges, partial s -> out + s*out_exp_stride
     int wait_cluster;
-    int st256;  // epilogue rows 32-B aligned: one 256-bit store per 16 bf16 / 8 fp32 columns (full L2 sectors)  // pair kernel: 1 = mbarrier waits with .acquire.cluster (L1 invalidate per wait)
-    int clk_slot;  // > 0: CTA 0 stamps (clock64, globaltimer) at entry and exit into g_gemm_clk[clk_slot - 1]
+    int st256;  // epilogue rows 32-B aligned: one 256-bit store per 16 bf16 / 8 fp32 columns (full L2 sectors)
+    int clk_slot;
+    int a_box_rows;  // mode 0, K-major A: rows per A TMA box (= tile_m when < 128; 0 = BM)  // > 0: CTA 0 stamps (clock64, globaltimer) at entry and exit into g_gemm_clk[clk_slot - 1]
 };
 
 // Diagnostics (hep_tuning.ffn_clock = 1): SM clock cycles and wall nanoseconds of CTA 0 across
@@ -400,25 +404,51 @@ __device__ __forceinline__ uint32_t order_key(float f) {
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-// EPI_GATE epilogue of one 128-token tile, run by the 4 warps of column slice 0
-// (one TMEM lane quarter each; named barrier 1 is shared by those 128 threads).
+// EPI_GATE epilogue of one accumulator tile (<= 128 tokens), run by all 8 epilogue
+// warps: warp pair (q, q+4) shares TMEM lane quarter q; with E_pad % 32 == 0 the two
+// warps scan one column half each and half 1 hands its top-KG list to half 0 through
+// shared memory (nhalf = 2), else half 0 scans every column (nhalf = 1).  Named
+// barrier 1 spans the 128 * nhalf participating threads.
 // Selection and weights are exactly hep_gate_topk's (gate.cu): top-K of the order key
 // of (logit + bias) with ties to the lower expert id (strict '>' while scanning experts
-// in ascending order keeps the earlier one), softmax over the K selected logits in pick
-// order.  The running top-KG list is a branch-free insertion network: every slot's new
-// value depends only on the previous column's list, so the KG compare/selects of one
-// column issue back to back.  Histogram counts go to shared memory (flushed once per
-// CTA); the per-64-token chunk counts of the tile's two chunks are written directly.
+// in ascending order keeps the earlier one; half 1's entries, all of higher expert id,
+// are inserted after half 0's scan in their own order, so the merged list is the
+// sequential scan's), softmax over the K selected logits in pick order.  The running
+// top-KG list is a branch-free insertion network: every slot's new value depends only
+// on the previous column's list, so the KG compare/selects of one column issue back to
+// back.  Histogram counts go to shared memory (flushed once per CTA); the per-64-token
+// chunk counts (chunks aligned to 64 tokens) are stored directly when the tile is made
+// of whole chunks, else added with integer atomics into the zeroed global counts.
+template <int KG>
+__device__ __forceinline__ void gate_insert(uint32_t key, int e, float l, uint32_t (&tk)[KG], int (&te)[KG],
+                                            float (&tv)[KG]) {
+#pragma unroll
+    for (int j = KG - 1; j >= 0; --j) {
+        const bool up = j > 0 && key > tk[j > 0 ? j - 1 : 0];  // slot j takes slot j-1's entry
+        const bool here = key > tk[j];                          // ... or the new one
+        tk[j] = up ? tk[j > 0 ? j - 1 : 0] : (here ? key : tk[j]);
+        te[j] = up ? te[j > 0 ? j - 1 : 0] : (here ? e : te[j]);
+        tv[j] = up ? tv[j > 0 ? j - 1 : 0] : (here ? l : tv[j]);
+    }
+}
+
+__device__ __forceinline__ void gate_bar(int nthr) { asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory"); }
+
 template <int KG>
 __device__ __forceinline__ void gate_tile(const Params &p, uint32_t t_row, int64_t row0, int rows, int row_in_tile,
-                                          int32_t *s_hist, int32_t *s_chunk, const float *s_bias, int E_pad) {
+                                          int half, int nhalf, int32_t *s_hist, int32_t *s_chunk,
+                                          const float *s_bias, uint8_t *s_merge, int E_pad) {
     const GateParams &g = p.gate;
     const int E = g.E;
-    const int tid = row_in_tile;  // 0..127 over the 4 participating warps
+    const int nthr = 128 * nhalf;
+    const int tid = half * 128 + row_in_tile;
+    // chunk counters: aligned 64-token chunks [c0, c0 + 3) relative to this tile
+    const int64_t c0 = row0 >> 6;
+    const bool whole = (row0 & 63) == 0 && ((rows & 63) == 0 || row0 + rows == p.M);
     if (g.chunk_cnt) {
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's chunk counts are out
-        for (int i = tid; i < 2 * E; i += 128) s_chunk[i] = 0;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        gate_bar(nthr);  // previous tile's chunk counts are out
+        for (int i = tid; i < 3 * E; i += nthr) s_chunk[i] = 0;
+        gate_bar(nthr);
     }
     const bool valid = row_in_tile < rows;
     const int64_t t = row0 + row_in_tile;
@@ -431,9 +461,11 @@ __device__ __forceinline__ void gate_tile(const Params &p, uint32_t t_row, int64
         te[i] = 0;
         tv[i] = 0.f;
     }
+    const int c_lo = nhalf == 2 ? half * (E_pad / 2) : 0;
+    const int c_hi = nhalf == 2 ? c_lo + E_pad / 2 : E_pad;
     float *lrow = (valid && p.out) ? reinterpret_cast<float *>(p.out) + t * p.ld_out : nullptr;
 #pragma unroll 1
-    for (int c = 0; c < E_pad; c += 16) {
+    for (int c = c_lo; c < c_hi; c += 16) {
         uint32_t v[16];
         tmem_ld16(t_row + c, v);
         tmem_ld_wait();
@@ -450,17 +482,27 @@ __device__ __forceinline__ void gate_tile(const Params &p, uint32_t t_row, int64
             const float l = __uint_as_float(v[i]);
             // padding columns get key 0, which never enters (strict '>' against >= 0)
             const uint32_t key = e < E ? order_key(l + s_bias[e]) : 0u;
-#pragma unroll
-            for (int j = KG - 1; j >= 0; --j) {
-                const bool up = j > 0 && key > tk[j > 0 ? j - 1 : 0];  // slot j takes slot j-1's entry
-                const bool here = key > tk[j];                          // ... or the new one
-                tk[j] = up ? tk[j > 0 ? j - 1 : 0] : (here ? key : tk[j]);
-                te[j] = up ? te[j > 0 ? j - 1 : 0] : (here ? e : te[j]);
-                tv[j] = up ? tv[j > 0 ? j - 1 : 0] : (here ? l : tv[j]);
-            }
+            gate_insert<KG>(key, e, l, tk, te, tv);
         }
     }
-    if (valid) {
+    if (nhalf == 2) {  // half 1 -> half 0 through shared memory, then half 0 inserts
+        uint32_t *mk = reinterpret_cast<uint32_t *>(s_merge) + row_in_tile * KG;
+        int32_t *me = reinterpret_cast<int32_t *>(s_merge + 128 * KG * 4) + row_in_tile * KG;
+        float *mv = reinterpret_cast<float *>(s_merge + 128 * KG * 8) + row_in_tile * KG;
+        if (half == 1)
+#pragma unroll
+            for (int k = 0; k < KG; ++k) {
+                mk[k] = tk[k];
+                me[k] = te[k];
+                mv[k] = tv[k];
+            }
+        gate_bar(nthr);
+        if (half == 0)
+#pragma unroll
+            for (int k = 0; k < KG; ++k) gate_insert<KG>(mk[k], me[k], mv[k], tk, te, tv);
+        gate_bar(nthr);  // the merge buffer is free for the next tile
+    }
+    if (half == 0 && valid) {
         float mx = tv[0];
 #pragma unroll
         for (int k = 1; k < KG; ++k) mx = fmaxf(mx, tv[k]);
@@ -472,25 +514,27 @@ __device__ __forceinline__ void gate_tile(const Params &p, uint32_t t_row, int64
         }
         const int64_t s64 = t / g.tps;
         const int src = (int)(s64 < g.n_src - 1 ? s64 : g.n_src - 1);
+        const int ch = (int)((t >> 6) - c0);
 #pragma unroll
         for (int k = 0; k < KG; ++k) {
             g.topk_idx[t * KG + k] = te[k];
             g.topk_w[t * KG + k] = ex[k] / den;
             atomicAdd(&s_hist[src * E + te[k]], 1);
-            if (g.chunk_cnt) atomicAdd(&s_chunk[(row_in_tile >> 6) * E + te[k]], 1);
+            if (g.chunk_cnt) atomicAdd(&s_chunk[ch * E + te[k]], 1);
         }
     }
     if (g.chunk_cnt) {
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        // tile = chunks of 64 tokens (the launch guarantees tps % 64 == 0 and 128-row tiles)
-        for (int i = tid; i < 2 * E; i += 128) {
-            const int half = i / E, e = i - half * E;
-            const int64_t t0 = row0 + 64 * half;
-            if (64 * half < rows) {
-                const int64_t src = t0 / g.tps;
-                const int64_t c = (t0 - src * g.tps) >> 6;
-                g.chunk_cnt[((int64_t)src * g.ncs + c) * E + e] = s_chunk[i];
-            }
+        gate_bar(nthr);
+        // chunk j of the tile is global chunk c0 + j = (src * ncs + c) in the [n_src][ncs][E]
+        // layout (the launch guarantees tps % 64 == 0, so chunks never straddle sources)
+        const int64_t n_chunks = ((row0 + rows - 1) >> 6) - c0 + 1;
+        for (int i = tid; i < n_chunks * E; i += nthr) {
+            const int j = i / E, e = i - j * E;
+            int32_t *dst = g.chunk_cnt + (c0 + j) * E + e;
+            if (whole)
+                *dst = s_chunk[i];
+            else if (s_chunk[i])
+                atomicAdd(dst, s_chunk[i]);
         }
     }
 }
@@ -521,8 +565,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     else if (p.grouped == 2 && p.exp_perm)
         for (int i = threadIdx.x; i < p.n_exp; i += blockDim.x) s_off[i] = p.exp_perm[i];
     int32_t *s_hist = s_off + kMaxExpSmem + 4;             // EPI_GATE: [n_src][E] counts
-    int32_t *s_chunk = s_hist + kGateMaxSrc * kGateMaxE;  // EPI_GATE: [2][E] tile chunk counts
-    float *s_bias = reinterpret_cast<float *>(s_chunk + 2 * kGateMaxE);  // EPI_GATE: [E_pad] bias
+    int32_t *s_chunk = s_hist + kGateMaxSrc * kGateMaxE;  // EPI_GATE: [3][E] tile chunk counts
+    float *s_bias = reinterpret_cast<float *>(s_chunk + 3 * kGateMaxE);  // EPI_GATE: [E_pad] bias
+    uint8_t *s_merge = reinterpret_cast<uint8_t *>(s_bias + kGateMaxE);   // EPI_GATE: column-half merge
     if constexpr (EPI == EPI_GATE) {
         for (int i = threadIdx.x; i < p.gate.n_src * p.gate.E; i += blockDim.x) s_hist[i] = 0;
         for (int i = threadIdx.x; i < BN; i += blockDim.x)
@@ -605,9 +650,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                                        : (B_MN ? b_row - tl.n_blk * BN : 0);
                 // an expert with a single m-tile streams its weights once: keep them out of L2's way
                 const bool light = p.light_first && p.grouped == 1 && s_off[tl.expert + 1] - s_off[tl.expert] == 1;
+                // A boxes of a_box_rows rows (router tiles of < 128 tokens): the MMA still reads
+                // 128 rows, the rows past the box are stale and land only in ignored accumulator rows
+                const uint32_t tx = (!A_MN && p.a_box_rows > 0) ? (uint32_t)(p.a_box_rows * BK * 2) + S::B_BYTES
+                                                                : (uint32_t)S::STAGE_BYTES;
                 for (int k = 0; k < tl.kb; ++k) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], S::STAGE_BYTES);
+                    mbar_arrive_expect_tx(&full[stage], tx);
                     if constexpr (A_MN) {
 #pragma unroll
                         for (int i = 0; i < BM / 64; ++i)
@@ -674,12 +723,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
             if constexpr (EPI == EPI_GATE) {
-                if (half == 0) {
+                // both column halves when E_pad splits into 16-column steps, else half 0 alone
+                constexpr int NH = (BN % 32 == 0 && kEpiSplit == 2) ? 2 : 1;
+                if (half < NH) {
 #define HEP_GATE_K(KK) \
-    case KK: gate_tile<KK>(p, t_row, tl.row0, tl.rows, row_in_tile, s_hist, s_chunk, s_bias, BN); break;
+    case KK: gate_tile<KK>(p, t_row, tl.row0, tl.rows, row_in_tile, half, NH, s_hist, s_chunk, s_bias, s_merge, BN); break;
                     switch (p.gate.K) {  // the insertion network is unrolled per K
                         HEP_GATE_K(1) HEP_GATE_K(2) HEP_GATE_K(3) HEP_GATE_K(4)
-                        HEP_GATE_K(5) HEP_GATE_K(6) HEP_GATE_K(7) default: gate_tile<8>(p, t_row, tl.row0, tl.rows, row_in_tile, s_hist, s_chunk, s_bias, BN); break;
+                        HEP_GATE_K(5) HEP_GATE_K(6) HEP_GATE_K(7)
+                        default: gate_tile<8>(p, t_row, tl.row0, tl.rows, row_in_tile, half, NH, s_hist, s_chunk, s_bias, s_merge, BN); break;
                     }
 #undef HEP_GATE_K
                 }
@@ -1244,19 +1296,34 @@ extern "C" int hep_gemm_bf16(const void *d_A, const void *d_B, void *d_D, int64_
     return launch<256, 4, EPI_BF16>(d_A, M, K, d_B, N, p, mt * p.n_tiles, s);
 }
 
+// Router tile height: the T tokens split into equal tiles of <= 128 rows (multiple of 16)
+// so that the tiles fill whole waves of all SMs (16384 tokens: 147 tiles of 112 rows on
+// 148 SMs instead of 128 tiles of 128 rows leaving 20 SMs idle).  hep_tuning.router_tile_rows
+// overrides (128 = the plain 128-row tiling).
+static int router_tile_rows(int64_t T) {
+    if (g_tuning.router_tile_rows > 0) return g_tuning.router_tile_rows < BM ? (g_tuning.router_tile_rows + 15) / 16 * 16 : BM;
+    const int64_t sms = sm_count();
+    const int64_t waves = (T + BM * sms - 1) / (BM * sms);
+    int64_t tm = (T + waves * sms - 1) / (waves * sms);
+    tm = (tm + 15) / 16 * 16;
+    return (int)(tm < 16 ? 16 : (tm > BM ? BM : tm));
+}
+
 template <int BN, int STAGES>
 static int launch_gate(const void *x, const void *wg, int64_t T, int64_t d_model, int e_pad, const Params &p,
                        cudaStream_t s) {
     using S = Smem<BN, STAGES>;
+    static_assert(S::BYTES + kGateSmemBytes <= 232448, "router+gate kernel shared memory");
     CUtensorMap ta, tb;
-    int rc = make_tmap(&ta, x, (uint64_t)T, (uint64_t)d_model, BM);
+    const int tm = p.tile_m > 0 ? p.tile_m : BM;
+    int rc = make_tmap(&ta, x, (uint64_t)T, (uint64_t)d_model, (uint32_t)tm);
     if (rc) return rc;
     rc = make_tmap(&tb, wg, (uint64_t)e_pad, (uint64_t)d_model, BN);  // rows past e_pad: TMA zero fill
     if (rc) return rc;
     auto kern = gemm_kernel<BN, STAGES, EPI_GATE>;
     const int bytes = (int)S::BYTES + kGateSmemBytes;
     HEP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    const int64_t tiles = (T + BM - 1) / BM;
+    const int64_t tiles = (T + tm - 1) / tm;
     const int grid = (int)(tiles < sm_count() ? tiles : sm_count());
     kern<<<grid, kThreads, bytes, s>>>(ta, tb, p);
     HEP_CHECK_LAUNCH();
@@ -1308,6 +1375,15 @@ extern "C" int hep_router_topk(const void *d_x, const void *d_wg, int64_t T, int
     p.gate.topk_w = d_topk_w;
     p.gate.hist = d_hist;
     p.gate.chunk_cnt = chunks_fused ? d_chunk_cnt : nullptr;
+    const int tm = router_tile_rows(T);
+    if (tm < BM) {
+        p.tile_m = tm;
+        p.a_box_rows = tm;
+        // tiles no longer hold whole 64-token chunks: the epilogue adds its chunk counts
+        // with integer atomics (order-free) into zeroed counters
+        if (chunks_fused && tm % 64 != 0)
+            HEP_CHECK_CUDA(cudaMemsetAsync(d_chunk_cnt, 0, sizeof(int32_t) * (size_t)n_src * p.gate.ncs * E, s));
+    }
     int rc;
     if (e_pad <= 16) rc = launch_gate<16, 8>(d_x, d_wg, T, d_model, e_pad, p, s);
     else if (e_pad <= 32) rc = launch_gate<32, 8>(d_x, d_wg, T, d_model, e_pad, p, s);

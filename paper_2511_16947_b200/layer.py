@@ -164,6 +164,26 @@ class MoELayer(torch.nn.Module):
         self.sched = DeviceScheduler(placement, device=self.device)
         self._bufs.clear()
 
+    @torch.no_grad()
+    def schedule(self, x: torch.Tensor, stream=None) -> torch.Tensor:
+        """K1 + K3 only (router GEMM with the fused gate, then the scheduler) on ``x``:
+        the micro-batch's histogram, exact schedule, routing and transfer plan on the
+        device without moving tokens (balance studies; the schedule is the one a full
+        forward computes).  Returns the device tensor of integerized per-GPU loads [G]."""
+        if self.static_share is not None:
+            raise ValueError("schedule() covers the single-phase harmony schedule")
+        L = _lib.lib()
+        st = stream if stream is not None else torch.cuda.current_stream()
+        T, K, E, G = x.shape[0], self.K, self.E, self.G
+        b = self.buffers(T)
+        _lib.check(L.hep_router_topk(x.data_ptr(), self.wg.data_ptr(), T, self.d, E, self.e_pad,
+                                     _lib.ptr(self.gate_bias), K, T // G, G, b.logits.data_ptr(),
+                                     b.topk_idx.data_ptr(), b.topk_w.data_ptr(), b.hist.data_ptr(), None,
+                                     st.cuda_stream), "hep_router_topk")
+        _lib.check(L.hep_sched_solve(self.sched.handle, b.hist.data_ptr(), 1, E, None, HEP_SCHED_ALL,
+                                     ctypes.byref(self.sched.out), st.cuda_stream), "hep_sched_solve")
+        return self.sched.gpu_load
+
     def expert_loads(self, T: int) -> list[int]:
         """Per-expert token counts of the last micro-batch (host copy of the
         device histogram's column sums; for the adaptive policy)."""
