@@ -62,7 +62,7 @@ typedef struct {
     int sched_lexmin_warps; /* warps on the scheduler's lex-min arc chain (4) */
     int lsu256;             /* 1: 256-bit LDG/STG permute / combine when 32-B aligned */
     int ffn_clock;          /* 1: diagnostics, CTA 0 of each expert GEMM stamps clock64/globaltimer */
-    int router_tile_rows;   /* router GEMM rows per CTA tile: 0 = auto (all SMs busy), else 128 */
+    int router_tile_rows;   /* router GEMM rows per CTA tile, multiple of 16 (0 = 128; shorter tiles measured slower) */
     int reserved[7];
 } hep_tuning;
 int hep_tuning_get(hep_tuning *out);

@@ -1296,17 +1296,16 @@ extern "C" int hep_gemm_bf16(const void *d_A, const void *d_B, void *d_D, int64_
     return launch<256, 4, EPI_BF16>(d_A, M, K, d_B, N, p, mt * p.n_tiles, s);
 }
 
-// Router tile height: the T tokens split into equal tiles of <= 128 rows (multiple of 16)
-// so that the tiles fill whole waves of all SMs (16384 tokens: 147 tiles of 112 rows on
-// 148 SMs instead of 128 tiles of 128 rows leaving 20 SMs idle).  hep_tuning.router_tile_rows
-// overrides (128 = the plain 128-row tiling).
+// Router tile height (hep_tuning.router_tile_rows, multiple of 16, <= 128; 0 = 128).  Shorter
+// tiles that fill every SM (16384 tokens: 147 tiles of 112 rows instead of 128 of 128) were
+// measured SLOWER (Mixtral 31.1 vs 28.7 us, Qwen3 48.7 vs 47.4, DSv3 75.5 vs 72.0,
+// profiles/r02/router_ab_r02c.txt): the kernel's time is one tile's DRAM-bound mainloop plus
+// its exposed gate epilogue, both per CTA, and the epilogue costs the same for a short tile
+// (every TMEM lane runs the scan), so the 128-row tiling stays the default.
 static int router_tile_rows(int64_t T) {
+    (void)T;
     if (g_tuning.router_tile_rows > 0) return g_tuning.router_tile_rows < BM ? (g_tuning.router_tile_rows + 15) / 16 * 16 : BM;
-    const int64_t sms = sm_count();
-    const int64_t waves = (T + BM * sms - 1) / (BM * sms);
-    int64_t tm = (T + waves * sms - 1) / (waves * sms);
-    tm = (tm + 15) / 16 * 16;
-    return (int)(tm < 16 ? 16 : (tm > BM ? BM : tm));
+    return BM;
 }
 
 template <int BN, int STAGES>

@@ -1,17 +1,40 @@
-"""Time the fused router+gate kernel (hep_router_topk) against the unfused chain
-(hep_gemm_bf16 + hep_gate_topk + hep_gate_chunk_counts) at the bench shapes."""
+"""A/B the fused router+gate kernel (hep_router_topk) at the bench shapes:
+router tile heights (hep_tuning.router_tile_rows: 0 / 128 = 128-row tiles, 112 = the
+all-SM split of 16384 tokens, ...) interleaved over rounds in one process, plus the unfused chain
+(hep_gemm_bf16 + hep_gate_topk + hep_gate_chunk_counts) for reference.  Prints the
+median µs per launch and algorithmic GB/s (x, Wg, logits, top-K) / HBM peak; checks
+that every variant produces the same top-K, histogram and chunk counts.
+
+    python tools/router_ab.py [--variants 0,128] [--rounds 5] [--hot]
+--hot: before each timed batch, run 20 ms of bf16 GEMMs (the FFN's power state)."""
+import argparse
+import json
 import os
+import statistics
 import sys
 
 import torch
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
 from paper_2511_16947_b200 import _lib as L  # noqa: E402
 
 SHAPES = {"mixtral": (16384, 4096, 8, 2), "qwen3": (32768, 2048, 128, 8), "dsv3": (16384, 7168, 256, 8)}
+ap = argparse.ArgumentParser()
+ap.add_argument("--variants", default="0,128")
+ap.add_argument("--rounds", type=int, default=5)
+ap.add_argument("--iters", type=int, default=30)
+ap.add_argument("--hot", action="store_true")
+ap.add_argument("--shapes", default="mixtral,qwen3,dsv3")
+args = ap.parse_args()
+peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
+    os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6553.6}
 lib = L.lib()
 s = L.stream_handle()
-for name, (T, d, E, K) in SHAPES.items():
+base = L.get_tuning()
+ha = torch.randn(8192, 8192, device="cuda").to(torch.bfloat16) if args.hot else None
+for name in args.shapes.split(","):
+    T, d, E, K = SHAPES[name]
     G = 8
     e_pad = max(16, (E + 15) // 16 * 16)
     x = torch.randn(T, d, device="cuda").to(torch.bfloat16)
@@ -23,11 +46,11 @@ for name, (T, d, E, K) in SHAPES.items():
     w = torch.empty(T, K, device="cuda")
     h = torch.empty(G, E, dtype=torch.int64, device="cuda")
     c = torch.empty(G * (tps // 64) * E, dtype=torch.int32, device="cuda")
+    nbytes = T * d * 2 + e_pad * d * 2 + T * e_pad * 4 + T * K * 8
 
-    def fused(logits=True):
-        lib.hep_router_topk(x.data_ptr(), wg.data_ptr(), T, d, E, e_pad, b.data_ptr(), K, tps, G,
-                            lg.data_ptr() if logits else None, idx.data_ptr(), w.data_ptr(), h.data_ptr(),
-                            c.data_ptr(), s)
+    def fused():
+        L.check(lib.hep_router_topk(x.data_ptr(), wg.data_ptr(), T, d, E, e_pad, b.data_ptr(), K, tps, G, lg.data_ptr(),
+                                    idx.data_ptr(), w.data_ptr(), h.data_ptr(), c.data_ptr(), s), "router")
 
     def unfused():
         lib.hep_gemm_bf16(x.data_ptr(), wg.data_ptr(), lg.data_ptr(), T, e_pad, d, 0, s)
@@ -35,18 +58,34 @@ for name, (T, d, E, K) in SHAPES.items():
                           h.data_ptr(), s)
         lib.hep_gate_chunk_counts(idx.data_ptr(), T, K, E, tps, G, c.data_ptr(), s)
 
-    def gemm_only():
-        lib.hep_gemm_bf16(x.data_ptr(), wg.data_ptr(), lg.data_ptr(), T, e_pad, d, 0, s)
-
-    for label, fn in (("fused", fused), ("fused_nologits", lambda: fused(False)), ("unfused", unfused),
-                      ("gemm_only", gemm_only)):
-        for _ in range(3):
-            fn()
-        torch.cuda.synchronize()
-        st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        st.record()
-        for _ in range(50):
-            fn()
-        en.record()
-        torch.cuda.synchronize()
-        print(f"{name:8s} {label:15s} {st.elapsed_time(en) / 50 * 1000:8.1f} us")
+    variants = [("tile=" + v, int(v)) for v in args.variants.split(",")] + [("unfused", None)]
+    res = {lab: [] for lab, _ in variants}
+    outs = {}
+    for r in range(args.rounds):
+        for lab, tile in variants:
+            if tile is not None:
+                L.set_tuning(**{**base, "router_tile_rows": tile})
+            fn = fused if tile is not None else unfused
+            for _ in range(3):
+                fn()
+            torch.cuda.synchronize()
+            if lab not in outs:
+                outs[lab] = (idx.clone(), h.clone(), c.clone(), lg.clone())
+            if ha is not None:
+                for _ in range(10):
+                    ha @ ha
+            st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            st.record()
+            for _ in range(args.iters):
+                fn()
+            en.record()
+            torch.cuda.synchronize()
+            res[lab].append(st.elapsed_time(en) / args.iters * 1000)
+    L.set_tuning(**base)
+    ref = outs["unfused"]
+    for lab, _ in variants:
+        us = statistics.median(res[lab])
+        same = all(torch.equal(a, b_) for a, b_ in zip(outs[lab], ref))
+        print(json.dumps({"shape": name, "variant": lab, "us": round(us, 2), "GB/s": round(nbytes / us / 1e3, 1),
+                          "frac": round(nbytes / us / 1e3 / peaks["hbm_gbs"], 3), "same_as_unfused": same,
+                          "hot": args.hot, "all_us": [round(v, 1) for v in res[lab]]}))
