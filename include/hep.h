@@ -150,15 +150,18 @@ int hep_sched_route(hep_sched_t h, const int64_t *d_loads, int64_t stride_e, int
  *                    (_even_split_plan :301-322), integerized, routed, transfer plan -> *former
  *   scheduled phase: exact solve of latter with gpu_base = the static phase's integerized
  *                    GPU loads, integerize, route, transfer                          -> *latter
- * share = 1 - pipeline_ratio (:375).  d_split: caller buffer int64 [2][E][G] (former,
- * latter; expert-major) that the route stages read.  The static phase's outputs are
- * final before the scheduled phase's solve starts (same stream), so its dispatch can be
- * issued on another stream right after the first two launches.  The phases need
- * distinct d_status words.  flags: TRANSFER / TOPO as for hep_sched_solve.
+ * share = 1 - pipeline_ratio (:375).  d_split: caller buffer int64 [2*E*G + G]: former and
+ * latter loads ([E][G] each, expert-major; the route stages read them) and the static phase's
+ * integerized GPU loads [G] (= the scheduled phase's gpu_base, computed by the split kernel).
+ * stream_static (a cudaStream_t, or NULL = `stream`): the static phase's integerize / route /
+ * transfer run there, forked after the split, concurrently with the scheduled phase's solve
+ * on `stream`; its assignment and dispatch can follow on stream_static (simulator.py:451-453)
+ * and the caller joins it back before the expert GEMMs.  The phases need distinct d_status
+ * words.  flags: TRANSFER / TOPO as for hep_sched_solve.
  */
 int hep_sched_pipelined(hep_sched_t h, const int64_t *d_loads, int64_t stride_e, int64_t stride_g, int64_t share_num,
                         int64_t share_den, int flags, int64_t *d_split, const hep_sched_out *former,
-                        const hep_sched_out *latter, void *stream);
+                        const hep_sched_out *latter, void *stream, void *stream_static);
 /* Diagnostics: per-phase SM clock stamps of the last HEP_SCHED_PROFILE launch (n <= 16). */
 int hep_sched_debug_timing(int64_t *host_out, int n);
 /* Aggregate an arbitrary routing table. Replaces build_transfer_plan (router.py:178-226). */
@@ -240,18 +243,21 @@ int hep_moe_assign_precounted(hep_sched_t h, const hep_sched_out *sched, const i
                               void *stream);
 size_t hep_moe_assign_chunk_offset(hep_sched_t h, int64_t T, int K);
 /*
- * K4 for one phase of the pipelined split (hep_sched_pipelined): the assignments of
- * (expert e, source src) whose rank q (sequence order) lies in this phase's window
- * [rank_base[e][src], rank_base[e][src] + this phase's count) get rows; the others are
- * left untouched.  Static phase: d_rank_base = d_row_base = NULL (window starts at 0);
- * scheduled phase: d_rank_base = the static share [E][G] (d_split), d_row_base = the
- * static phase's d_expert_rows + E (its row count), so the receive buffer is
- * [phase][expert][dst][src][rank] and the static phase's rows are final before the
- * scheduled phase is solved.  Same workspace as hep_moe_assign; row_align = 1.
+ * K4 for one phase (0 static, 1 scheduled) of the pipelined split (hep_sched_pipelined,
+ * d_split = its [2][E][G] split): the assignments of (expert e, source src) whose rank q
+ * (sequence order) lies in this phase's window -- [0, former[e][src]) for phase 0,
+ * [former[e][src], former + latter) for phase 1 -- get rows; the others are left untouched in
+ * d_tok_row and set to -1 in d_tok_row_phase (optional [T][K]: this phase's own row map, the
+ * input of its hep_moe_permute, which skips negative rows).  Receive layout
+ * [expert][phase][dst][src][rank]: expert e's block starts at the prefix of the experts' total
+ * loads (known from d_split before the scheduled phase is solved) and holds the static rows
+ * first, so each expert stays one contiguous grouped-GEMM run and the two phases write
+ * disjoint rows: they may run concurrently on two streams, each with ITS OWN workspace.
+ * d_seg gets this phase's nnz segments; row_align = 1.
  */
-int hep_moe_assign_phase(hep_sched_t h, const hep_sched_out *sched, const int64_t *d_rank_base,
-                         const int64_t *d_row_base, const int32_t *d_topk_idx, int64_t T, int K, int64_t tokens_per_src,
-                         int32_t *d_tok_row, int32_t *d_row_tok, int32_t *d_seg, int64_t *d_expert_rows,
+int hep_moe_assign_phase(hep_sched_t h, const hep_sched_out *sched, const int64_t *d_split, int phase,
+                         const int32_t *d_topk_idx, int64_t T, int K, int64_t tokens_per_src, int32_t *d_tok_row,
+                         int32_t *d_tok_row_phase, int32_t *d_row_tok, int32_t *d_seg, int64_t *d_expert_rows,
                          void *workspace, size_t workspace_bytes, void *stream);
 
 /*
@@ -339,7 +345,8 @@ int hep_ipc_handle(const void *d_ptr, void *handle_out, int64_t *offset_out);
 int hep_ipc_open(const void *handle, void **d_ptr);
 int hep_ipc_close(void *d_ptr);
 
-/* K5 permute/dispatch: rows[tok_row[t][k]] = x[t]  (bf16, 128-bit vectorised scatter). */
+/* K5 permute/dispatch: rows[tok_row[t][k]] = x[t]  (bf16, 128/256-bit vectorised scatter);
+ * negative rows are skipped, and a token with no non-negative row is not read. */
 int hep_moe_permute(const void *d_x, const int32_t *d_tok_row, int64_t T, int K, int64_t d_model, void *d_rows,
                     void *stream);
 

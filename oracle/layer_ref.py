@@ -83,18 +83,20 @@ def receive_rows(groups, G: int, xi, ranges, topk_idx: np.ndarray, tps: int):
 
 
 def receive_rows_pipelined(groups, G: int, former, latter, former_loads, topk_idx: np.ndarray, tps: int):
-    """Pipelined split (simulator.py:420-435) receive layout [phase][expert][dst][src][rank]:
-    within (expert, src) the first former_loads[e][src] assignments in token order
-    belong to the static phase (its ranges), the rest to the scheduled phase (its
-    ranges, ranks continuing).  ``former`` / ``latter`` = dict(xi=..., ranges=...)."""
+    """Pipelined split (simulator.py:420-435) receive layout [expert][phase][dst][src][rank]:
+    expert e's block starts at the prefix of the experts' total loads and holds the static
+    phase's rows first; within (expert, src) the first former_loads[e][src] assignments in
+    token order belong to the static phase (its ranges), the rest to the scheduled phase
+    (its ranges, ranks continuing).  ``former`` / ``latter`` = dict(xi=..., ranges=...)."""
     T, K = topk_idx.shape
     E = len(groups)
+    tot = [sum(former["xi"][e]) + sum(latter["xi"][e]) for e in range(E)]
+    start = np.concatenate([[0], np.cumsum(tot)]).astype(np.int64)
     lists = {}
-    row0 = 0
     for ph, plan in enumerate((former, latter)):
         base = {}
-        row = row0
         for e in range(E):
+            row = int(start[e]) + (sum(former["xi"][e]) if ph else 0)
             for dst in sorted(groups[e]):
                 base[(e, dst)] = row
                 row += plan["xi"][e][list(groups[e]).index(dst)]
@@ -106,7 +108,6 @@ def receive_rows_pipelined(groups, G: int, former, latter, former_loads, topk_id
                 r = base[(e, d)] + sum(c2 for (s2, d2, c2) in rs if d2 == d and s2 < s)
                 rank = (former_loads[e][s] if ph else 0) + sum(c2 for (s2, d2, c2) in rs[:j] if s2 == s)
                 lists.setdefault((e, s), []).append((rank, rank + c, r - rank))
-        row0 = row
     tok_row = np.zeros((T, K), dtype=np.int64)
     ctr = {}
     for t in range(T):
@@ -117,7 +118,7 @@ def receive_rows_pipelined(groups, G: int, former, latter, former_loads, topk_id
             ctr[(e, s)] = q + 1
             (hit,) = [lst for lst in lists[(e, s)] if lst[0] <= q < lst[1]]
             tok_row[t, k] = q + hit[2]
-    return tok_row, row0
+    return tok_row, int(start[-1])
 
 
 def bf16_round(a: np.ndarray) -> np.ndarray:

@@ -57,7 +57,7 @@ SIGNATURES = {
     "hep_sched_sizes": (ctypes.c_int, [vp, c_i64p, c_i64p, c_i64p, c_i64p]),
     "hep_sched_solve": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int64, vp, ctypes.c_int, ctypes.POINTER(HepSchedOut), vp]),
     "hep_sched_integerize": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.POINTER(HepSchedOut), vp]),
-    "hep_sched_pipelined": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp, ctypes.POINTER(HepSchedOut), ctypes.POINTER(HepSchedOut), vp]),
+    "hep_sched_pipelined": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp, ctypes.POINTER(HepSchedOut), ctypes.POINTER(HepSchedOut), vp, vp]),
     "hep_sched_route": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int64, vp, ctypes.c_int, ctypes.POINTER(HepSchedOut), vp]),
     "hep_sched_debug_timing": (ctypes.c_int, [c_i64p, ctypes.c_int]),
     "hep_transfer_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, vp, ctypes.c_int64, vp, vp, vp]),
@@ -68,7 +68,7 @@ SIGNATURES = {
     "hep_moe_assign_precounted": (ctypes.c_int, [vp, ctypes.POINTER(HepSchedOut), vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, ctypes.c_int, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]),
     "hep_moe_assign_chunk_offset": (ctypes.c_size_t, [vp, ctypes.c_int64, ctypes.c_int]),
     "hep_moe_assign": (ctypes.c_int, [vp, ctypes.POINTER(HepSchedOut), vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, ctypes.c_int, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]),
-    "hep_moe_assign_phase": (ctypes.c_int, [vp, ctypes.POINTER(HepSchedOut), vp, vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]),
+    "hep_moe_assign_phase": (ctypes.c_int, [vp, ctypes.POINTER(HepSchedOut), vp, ctypes.c_int, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]),
     "hep_moe_assign_workspace": (ctypes.c_size_t, [vp, ctypes.c_int64, ctypes.c_int]),
     "hep_moe_assign_ep": (ctypes.c_int, [vp, ctypes.POINTER(HepSchedOut), vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_size_t, vp]),
     "hep_moe_assign_ep_workspace": (ctypes.c_size_t, [vp, ctypes.c_int64, ctypes.c_int]),

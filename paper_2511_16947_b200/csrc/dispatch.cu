@@ -78,10 +78,13 @@ __global__ void plan_prep_kernel(int G, int E, int nnz, const int32_t *grp_off, 
                                  const int32_t *sorted, const int32_t *nnz_exp, const int64_t *xi,
                                  const int64_t *ranges, const int64_t *n_ranges_p, int64_t *expert_rows,
                                  int32_t *seg, AssignWs w, int32_t *status, int row_align,
-                                 const int64_t *rank_base, const int64_t *row_base_p, int64_t stage_cap) {
+                                 const int64_t *split, int phase, int64_t stage_cap) {
     __shared__ int64_t scan[64];
     const int tid = threadIdx.x, nt = blockDim.x;
-    const int64_t row_off = row_base_p ? *row_base_p : 0;  // phase block start (pipelined split)
+    // pipelined split: split = [2][E][G] (static share, scheduled share); this phase's ranks of
+    // (e, src) start after the static share's in the scheduled phase
+    const int64_t *rank_base = (split && phase == 1) ? split : nullptr;
+    const int64_t row_off = 0;
     if (*status) {  // the scheduler failed (and left an empty plan): no segments, no rows
         for (int p = tid; p < nnz; p += nt) {
             seg[4 * p + 0] = (int32_t)row_off;
@@ -104,19 +107,31 @@ __global__ void plan_prep_kernel(int G, int E, int nnz, const int32_t *grp_off, 
     }
     for (int i = tid; i <= E; i += nt) w.first[i] = -1;
     // expert blocks ([expert][dst asc][src][rank]), each starting on a row_align boundary
-    // (64 in training so weight-gradient GEMMs contract over whole 64-row blocks)
+    // (64 in training so weight-gradient GEMMs contract over whole 64-row blocks).  Pipelined
+    // split: [expert][phase][dst][src][rank] -- expert e's block holds both phases (its size
+    // is the expert's total load, known from the split before the scheduled phase is solved),
+    // the static rows first, so the grouped GEMM sees ONE contiguous run per expert and the
+    // two phases' assignments can run on different streams
     const int chunk = (E + nt - 1) / nt;
     const int e0 = min(E, tid * chunk), e1 = min(E, e0 + chunk);
     int64_t mine = 0;
     for (int e = e0; e < e1; ++e) {
         int64_t n = 0;
-        for (int p = grp_off[e]; p < grp_off[e + 1]; ++p) n += xi[sorted[p]];
+        if (split)
+            for (int g = 0; g < G; ++g) n += split[(int64_t)e * G + g] + split[((int64_t)E + e) * G + g];
+        else
+            for (int p = grp_off[e]; p < grp_off[e + 1]; ++p) n += xi[sorted[p]];
         mine += (n + row_align - 1) / row_align * row_align;
     }
     int64_t total;
     int64_t row = block_excl_scan_i64(mine, scan, &total) + row_off;
     total += row_off;
     for (int e = e0; e < e1; ++e) {
+        int64_t skip = 0;  // the static phase's rows of e precede the scheduled phase's
+        if (split && phase == 1)
+            for (int g = 0; g < G; ++g) skip += split[(int64_t)e * G + g];
+        const int64_t blk = row;
+        row += skip;
         expert_rows[e] = row;
         int64_t r = row;
         for (int p = grp_off[e]; p < grp_off[e + 1]; ++p) {  // segments in the scheduler's sorted arc order
@@ -128,7 +143,13 @@ __global__ void plan_prep_kernel(int G, int E, int nnz, const int32_t *grp_off, 
             w.row_base[i] = (int32_t)r;
             r += xi[i];
         }
-        row += (r - row + row_align - 1) / row_align * row_align;
+        if (split) {  // next expert block: after both phases' rows of e
+            int64_t n = 0;
+            for (int g = 0; g < G; ++g) n += split[(int64_t)e * G + g] + split[((int64_t)E + e) * G + g];
+            row = blk + n;
+        } else {
+            row += (r - row + row_align - 1) / row_align * row_align;
+        }
     }
     if (tid == 0) {
         expert_rows[E] = total;
@@ -224,7 +245,7 @@ __global__ void chunk_scan_kernel(int n_src, int ncs, int E, const int32_t *chun
 // one warp per chunk; lanes k < K own pick k of each token (distinct experts)
 __global__ void chunk_map_kernel(const int32_t *topk_idx, int K, int E, int G, int64_t tps, int64_t T, int ncs,
                                  const int32_t *chunk_pre, AssignWs w, int32_t *tok_row, int32_t *row_tok,
-                                 int src_base, bool windowed, const int32_t *status) {
+                                 int src_base, bool windowed, const int32_t *status, int32_t *tok_row_phase) {
     extern __shared__ int32_t sm[];
     int32_t *ctr = sm;                // [E]
     int32_t *l_cnt = ctr + E;         // [E]
@@ -244,6 +265,7 @@ __global__ void chunk_map_kernel(const int32_t *topk_idx, int K, int E, int G, i
         if (T < tb) tb = T;
         for (int64_t i = ta * K + threadIdx.x; i < tb * K; i += blockDim.x) {
             tok_row[i] = (int32_t)i;
+            if (tok_row_phase) tok_row_phase[i] = -1;
             if (row_tok) row_tok[i] = (int32_t)(i / K);
         }
         return;
@@ -285,12 +307,16 @@ __global__ void chunk_map_kernel(const int32_t *topk_idx, int K, int E, int G, i
             const int n = l_cnt[e];
             // pipelined split: this phase owns ranks [lo, end of its last range) of (e, src)
             const bool mine = !windowed || (n > 0 && q >= l_lo[e] && q < l_end[e * G + n - 1]);
+            const int64_t t = t0 + a / K;
+            const int64_t tk = t * K + (a - (a / K) * K);
             if (mine) {
                 while (j + 1 < n && q >= l_end[e * G + j]) ++j;
                 const int row = q + l_delta[e * G + j];
-                const int64_t t = t0 + a / K;
-                tok_row[t * K + (a - (a / K) * K)] = row;
+                tok_row[tk] = row;
+                if (tok_row_phase) tok_row_phase[tk] = row;
                 if (row_tok) row_tok[row] = (int32_t)t;
+            } else if (tok_row_phase) {
+                tok_row_phase[tk] = -1;  // the other phase's assignment: this phase's permute skips it
             }
         }
         __syncwarp();
@@ -407,6 +433,11 @@ __global__ void __launch_bounds__(256) permute_kernel(const int4 *__restrict__ x
 #pragma unroll
         for (int k = 0; k < 16; ++k)
             if (k < K) r[k] = tok_row[t * K + k];
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (k < K) any |= r[k] >= 0;
+        if (!any) continue;  // no assignment of this token in this phase: x[t] is not read
         const int4 *src = x + t * nvec;
         for (int64_t v0 = lane; v0 < nvec; v0 += 32 * 4) {
             int4 buf[4];
@@ -416,6 +447,7 @@ __global__ void __launch_bounds__(256) permute_kernel(const int4 *__restrict__ x
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
                 if (k >= K) break;
+                if (r[k] < 0) continue;  // not this phase's assignment (pipelined split)
                 int4 *dst = rows + (int64_t)r[k] * nvec;
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
@@ -456,6 +488,11 @@ __global__ void __launch_bounds__(256) permute_v8_kernel(const V8 *__restrict__ 
 #pragma unroll
         for (int k = 0; k < 16; ++k)
             if (k < K) r[k] = tok_row[t * K + k];
+        bool any = false;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (k < K) any |= r[k] >= 0;
+        if (!any) continue;  // no assignment of this token in this phase: x[t] is not read
         const V8 *src = x + t * nv8;
         for (int64_t v0 = lane; v0 < nv8; v0 += 32 * 2) {
             V8 buf[2];
@@ -465,6 +502,7 @@ __global__ void __launch_bounds__(256) permute_v8_kernel(const V8 *__restrict__ 
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
                 if (k >= K) break;
+                if (r[k] < 0) continue;  // not this phase's assignment (pipelined split)
                 V8 *dst = rows + (int64_t)r[k] * nv8;
 #pragma unroll
                 for (int u = 0; u < 2; ++u)
@@ -563,10 +601,10 @@ extern "C" size_t hep_moe_assign_workspace(hep_sched_t h, int64_t T, int K) {
 }
 
 static int assign_impl(hep_sched_t h, const hep_sched_out *sched, bool windowed, bool precounted,
-                       const int64_t *d_rank_base,
-                       const int64_t *d_row_base, const int32_t *d_topk_idx, int64_t T, int K, int64_t tokens_per_src,
-                       int row_align, int32_t *d_tok_row, int32_t *d_row_tok, int32_t *d_seg, int64_t *d_expert_rows,
-                       void *workspace, size_t workspace_bytes, void *stream) {
+                       const int64_t *d_split, int phase, const int32_t *d_topk_idx, int64_t T, int K,
+                       int64_t tokens_per_src, int row_align, int32_t *d_tok_row, int32_t *d_row_tok, int32_t *d_seg,
+                       int64_t *d_expert_rows, void *workspace, size_t workspace_bytes, void *stream,
+                       int32_t *d_tok_row_phase = nullptr) {
     HEP_REQUIRE(row_align >= 1 && row_align <= 1024, HEP_E_DIMENSION, "row_align=%d", row_align);
     HEP_REQUIRE(h && sched && d_topk_idx && d_tok_row && d_row_tok && d_seg && d_expert_rows && workspace,
                 HEP_E_CONTRACT, "hep_moe_assign: null argument");
@@ -588,7 +626,7 @@ static int assign_impl(hep_sched_t h, const hep_sched_out *sched, bool windowed,
         HEP_CHECK_CUDA(cudaFuncSetAttribute(plan_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPrepSmemMax));
     plan_prep_kernel<<<1, 512, prep_sm, s>>>(G, E, h->nnz, h->d_grp_off, h->d_grp_gpu, h->d_sorted, h->d_nnz_exp,
                                              sched->d_xi, sched->d_ranges, sched->d_n_ranges, d_expert_rows, d_seg, w,
-                                             sched->d_status, row_align, d_rank_base, d_row_base, stage_cap);
+                                             sched->d_status, row_align, d_split, phase, stage_cap);
     HEP_CHECK_LAUNCH();
     if (T <= 0) return HEP_OK;
     const int ncs = (int)((tokens_per_src + kChunk - 1) / kChunk);
@@ -604,7 +642,7 @@ static int assign_impl(hep_sched_t h, const hep_sched_out *sched, bool windowed,
     HEP_REQUIRE(sm <= 200 * 1024, HEP_E_CAPACITY, "chunk_map smem %zu", sm);
     if (sm > 48 * 1024) HEP_CHECK_CUDA(cudaFuncSetAttribute(chunk_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     chunk_map_kernel<<<nblk, 256, sm, s>>>(d_topk_idx, K, E, G, tokens_per_src, T, ncs, w.chunk_pre, w, d_tok_row,
-                                           d_row_tok, 0, windowed, sched->d_status);
+                                           d_row_tok, 0, windowed, sched->d_status, d_tok_row_phase);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
 }
@@ -614,7 +652,7 @@ extern "C" int hep_moe_assign(hep_sched_t h, const hep_sched_out *sched, const i
                               int32_t *d_seg, int64_t *d_expert_rows, void *workspace, size_t workspace_bytes,
                               void *stream) {
     HEP_NVTX("hep_moe_assign");
-    return assign_impl(h, sched, false, false, nullptr, nullptr, d_topk_idx, T, K, tokens_per_src, row_align, d_tok_row,
+    return assign_impl(h, sched, false, false, nullptr, 0, d_topk_idx, T, K, tokens_per_src, row_align, d_tok_row,
                        d_row_tok, d_seg, d_expert_rows, workspace, workspace_bytes, stream);
 }
 
@@ -632,7 +670,7 @@ extern "C" int hep_moe_assign_precounted(hep_sched_t h, const hep_sched_out *sch
                                          int32_t *d_row_tok, int32_t *d_seg, int64_t *d_expert_rows, void *workspace,
                                          size_t workspace_bytes, void *stream) {
     HEP_NVTX("hep_moe_assign_precounted");
-    return assign_impl(h, sched, false, true, nullptr, nullptr, d_topk_idx, T, K, tokens_per_src, row_align, d_tok_row,
+    return assign_impl(h, sched, false, true, nullptr, 0, d_topk_idx, T, K, tokens_per_src, row_align, d_tok_row,
                        d_row_tok, d_seg, d_expert_rows, workspace, workspace_bytes, stream);
 }
 
@@ -649,13 +687,14 @@ extern "C" int hep_gate_chunk_counts(const int32_t *d_topk_idx, int64_t T, int K
     return HEP_OK;
 }
 
-extern "C" int hep_moe_assign_phase(hep_sched_t h, const hep_sched_out *sched, const int64_t *d_rank_base,
-                                    const int64_t *d_row_base, const int32_t *d_topk_idx, int64_t T, int K,
-                                    int64_t tokens_per_src, int32_t *d_tok_row, int32_t *d_row_tok, int32_t *d_seg,
+extern "C" int hep_moe_assign_phase(hep_sched_t h, const hep_sched_out *sched, const int64_t *d_split, int phase,
+                                    const int32_t *d_topk_idx, int64_t T, int K, int64_t tokens_per_src,
+                                    int32_t *d_tok_row, int32_t *d_tok_row_phase, int32_t *d_row_tok, int32_t *d_seg,
                                     int64_t *d_expert_rows, void *workspace, size_t workspace_bytes, void *stream) {
     HEP_NVTX("hep_moe_assign_phase");
-    return assign_impl(h, sched, true, false, d_rank_base, d_row_base, d_topk_idx, T, K, tokens_per_src, 1, d_tok_row,
-                       d_row_tok, d_seg, d_expert_rows, workspace, workspace_bytes, stream);
+    HEP_REQUIRE(d_split && (phase == 0 || phase == 1), HEP_E_CONTRACT, "hep_moe_assign_phase: split and phase 0/1");
+    return assign_impl(h, sched, true, false, d_split, phase, d_topk_idx, T, K, tokens_per_src, 1, d_tok_row,
+                       d_row_tok, d_seg, d_expert_rows, workspace, workspace_bytes, stream, d_tok_row_phase);
 }
 
 extern "C" int hep_moe_permute(const void *d_x, const int32_t *d_tok_row, int64_t T, int K, int64_t d_model,
@@ -752,7 +791,7 @@ extern "C" int hep_moe_assign_ep(hep_sched_t h, const hep_sched_out *sched, cons
     if (sm > 48 * 1024)
         HEP_CHECK_CUDA(cudaFuncSetAttribute(chunk_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     chunk_map_kernel<<<ncs, 256, sm, s>>>(d_topk_idx, K, E, G, tps, T, ncs, w.chunk_pre, w, d_tok_row, nullptr, rank,
-                                          false, sched->d_status);
+                                          false, sched->d_status, nullptr);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
 }

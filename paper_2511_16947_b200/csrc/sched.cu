@@ -951,6 +951,7 @@ extern "C" int hep_sched_create(int num_gpus, int num_experts, const int32_t *gr
     for (int e = 0; e < E; ++e)
         for (int i = off[e]; i < off[e + 1]; ++i) kidx[(size_t)e * G + gpu[i]] = (int8_t)(i - off[e]);
     if (ce == cudaSuccess) ce = up((void **)&h->d_kidx, kidx.data(), (size_t)E * G);
+    if (ce == cudaSuccess) ce = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
     if (ce != cudaSuccess) {
         set_error("hep_sched_create: %s", cudaGetErrorString(ce));
         hep_sched_destroy(h);
@@ -971,6 +972,7 @@ extern "C" int hep_sched_destroy(hep_sched_t h) {
     cudaFree(h->d_seg_nnz);
     cudaFree(h->d_nnz_exp);
     cudaFree(h->d_kidx);
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     delete h;
     return HEP_OK;
 }
@@ -1034,9 +1036,14 @@ namespace hep {
 // Pipelined split (simulator.py:291-322): former = floor(v * num / den), latter = v - former
 // ([E][G] each, expert-major), and the static phase's even plan over each expert's replicas
 // as numerators over Q (Q/n is integral: n <= G).  One thread per expert.
+// Also the static phase's integerized per-GPU loads (integerize_plan of the even plan,
+// scheduler.py:697-735: every replica gets floor(tot / n), the tot mod n remainder units go to
+// the replicas with the lowest GPU ids -- all remainders tie), i.e. the scheduled phase's
+// gpu_base, so its solve need not wait for the static phase's routing.  base[G] is zeroed
+// by the launcher; integer atomics, order-free.
 __global__ void split_kernel(const int64_t *loads, int64_t se, int64_t sg, int E, int G, int64_t num, int64_t den,
-                             const int32_t *grp_off, int64_t Q, int64_t *former, int64_t *latter, int64_t *xq_former,
-                             int32_t *status) {
+                             const int32_t *grp_off, const int32_t *grp_gpu, int64_t Q, int64_t *former,
+                             int64_t *latter, int64_t *xq_former, int64_t *base, int32_t *status) {
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= E) return;
     int64_t tot = 0;
@@ -1054,13 +1061,22 @@ __global__ void split_kernel(const int64_t *loads, int64_t se, int64_t sg, int E
         return;
     }
     const int64_t x = tot * (Q / n);
-    for (int k = 0; k < n; ++k) xq_former[b + k] = x;
+    const int64_t q = tot / n, r = tot - q * n;
+    for (int k = 0; k < n; ++k) {
+        xq_former[b + k] = x;
+        const int g = grp_gpu[b + k];
+        int rank = 0;  // position of g among the group's GPU ids
+        for (int j = 0; j < n; ++j) rank += grp_gpu[b + j] < g;
+        const int64_t v = q + (rank < r ? 1 : 0);
+        if (v) atomicAdd(reinterpret_cast<unsigned long long *>(base + g), (unsigned long long)v);
+    }
 }
 }  // namespace hep
 
 extern "C" int hep_sched_pipelined(hep_sched_t h, const int64_t *d_loads, int64_t stride_e, int64_t stride_g,
                                    int64_t share_num, int64_t share_den, int flags, int64_t *d_split,
-                                   const hep_sched_out *former, const hep_sched_out *latter, void *stream) {
+                                   const hep_sched_out *former, const hep_sched_out *latter, void *stream,
+                                   void *stream_static) {
     HEP_NVTX("hep_sched_pipelined");
     HEP_REQUIRE(h && d_loads && d_split && former && latter, HEP_E_CONTRACT, "hep_sched_pipelined: null argument");
     HEP_REQUIRE(former->d_status && latter->d_status && former->d_status != latter->d_status, HEP_E_CONTRACT,
@@ -1069,15 +1085,23 @@ extern "C" int hep_sched_pipelined(hep_sched_t h, const int64_t *d_loads, int64_
                 "static share %lld/%lld outside [0, 1]", (long long)share_num, (long long)share_den);
     cudaStream_t s = (cudaStream_t)stream;
     const int E = h->E, G = h->G;
-    int64_t *f_loads = d_split, *l_loads = d_split + (int64_t)E * G;
+    int64_t *f_loads = d_split, *l_loads = d_split + (int64_t)E * G, *base = d_split + 2 * (int64_t)E * G;
     HEP_CHECK_CUDA(cudaMemsetAsync(former->d_status, 0, sizeof(int32_t), s));
+    HEP_CHECK_CUDA(cudaMemsetAsync(base, 0, sizeof(int64_t) * (size_t)G, s));
     if (E > 0) {
         split_kernel<<<(E + 127) / 128, 128, 0, s>>>(d_loads, stride_e, stride_g, E, G, share_num, share_den,
-                                                     h->d_grp_off, h->Q, f_loads, l_loads, former->d_xq,
-                                                     former->d_status);
+                                                     h->d_grp_off, h->d_grp_gpu, h->Q, f_loads, l_loads, former->d_xq,
+                                                     base, former->d_status);
         HEP_CHECK_LAUNCH();
     }
-    // static phase: integerize the even plan, route, transfer (no solve)
+    // static phase: integerize the even plan, route, transfer (no solve) -- on stream_static when
+    // given, forked after the split, so it runs concurrently with the scheduled phase's solve
+    cudaStream_t ss = s;
+    if (stream_static) {
+        ss = (cudaStream_t)stream_static;
+        HEP_CHECK_CUDA(cudaEventRecord(h->ev_fork, s));
+        HEP_CHECK_CUDA(cudaStreamWaitEvent(ss, h->ev_fork, 0));
+    }
     SchedArgs a{};
     a.flags = HEP_SCHED_INTEGERIZE | HEP_SCHED_ROUTE | (flags & (HEP_SCHED_TRANSFER | HEP_SCHED_TOPO));
     a.loads = f_loads;
@@ -1086,15 +1110,15 @@ extern "C" int hep_sched_pipelined(hep_sched_t h, const int64_t *d_loads, int64_
     a.den = h->Q;
     a.status_in = 1;
     a.out = *former;
-    int rc = launch_sched(h, a, s);
+    int rc = launch_sched(h, a, ss);
     if (rc) return rc;
-    // scheduled phase: exact solve with the static phase's GPU loads as gpu_base
+    // scheduled phase: exact solve with the static phase's GPU loads as gpu_base (from the split)
     SchedArgs b{};
     b.flags = (flags & HEP_SCHED_ALL) | HEP_SCHED_SOLVE;
     b.loads = l_loads;
     b.se = G;
     b.sg = 1;
-    b.base = former->d_gpu_load;
+    b.base = base;
     b.den = h->Q;
     b.out = *latter;
     return launch_sched(h, b, s);

@@ -18,5 +18,6 @@ struct hep_sched {
     int32_t *d_nnz_exp = nullptr;    // [nnz]  expert of each nnz entry
     int8_t *d_kidx = nullptr;        // [E*G]  list position of GPU g in expert e's group (-1: absent)
     size_t smem_set = 0;             // dynamic smem opt-in already granted
+    cudaEvent_t ev_fork = nullptr;   // pipelined split: forks the static phase onto its stream
     std::vector<int32_t> h_grp_off, h_grp_gpu, h_slots, h_hosted_off;
 };

@@ -87,13 +87,16 @@ class MoEBuffers:
         self.hist = torch.zeros(G, E, dtype=torch.int64, device=device)
         self.tok_row = torch.empty(T, K, **i32)
         self.row_tok = torch.empty(max(R, 1), **i32)
-        # pipelined split: [phase][expert][dst][src][rank], one segment list per phase
+        # pipelined split: [expert][phase][dst][src][rank], one segment list per phase; the two
+        # phases' assignments run on two streams, each with its own workspace and row map
         self.n_seg = sched.nnz * (2 if pipelined else 1)
         self.seg = torch.empty(max(self.n_seg, 1), 4, **i32)
         self.expert_rows = torch.empty(E + 1, dtype=torch.int64, device=device)
         self.expert_rows2 = torch.empty(E + 1, dtype=torch.int64, device=device) if pipelined else None
         ws = L.hep_moe_assign_workspace(sched.handle, T, K)
         self.assign_ws = torch.empty(max(int(ws), 256), dtype=torch.uint8, device=device)
+        self.assign_ws2 = torch.empty(max(int(ws), 256), dtype=torch.uint8, device=device) if pipelined else None
+        self.tok_row_ph = [torch.empty(T, K, **i32) for _ in range(2)] if pipelined else None
         self.chunk_off = int(L.hep_moe_assign_chunk_offset(sched.handle, T, K))  # router-written chunk counts
         self.rows = alloc(max(R, 1), d_model, **bf)
         self.h = alloc(max(R, 1), ffn, **bf)
@@ -129,7 +132,9 @@ class MoELayer(torch.nn.Module):
         # profiles/r01/ffn_ab_r01d.txt), so the permute kernel is the default.  Never in
         # training (the weight gradients contract over the permuted rows).
         self.fuse_permute = fuse_permute and not train
-        self.LAUNCHES_PER_FORWARD = (11 if self.static_share is None else 18) - (1 if self.fuse_permute else 0)
+        # pipelined: split + 2 scheduler launches, 2 x 4 assignment kernels, 2 permutes
+        self.LAUNCHES_PER_FORWARD = (11 if self.static_share is None else 19) - (
+            (1 if self.static_share is None else 2) if self.fuse_permute else 0)
         torch_ = _lib.require_cuda()
         self.device = torch_.device("cuda", torch_.cuda.current_device()) if device is None else torch_.device(device)
         self.placement = placement
@@ -153,6 +158,11 @@ class MoELayer(torch.nn.Module):
         self.w2 = w2
         self.gate_bias = None if gate_bias is None else gate_bias.to(self.device, torch.float32).contiguous()
         self._bufs: dict[int, MoEBuffers] = {}
+        if self.static_share is not None:
+            # the static phase's assignment + dispatch run on a side stream while the scheduled
+            # phase is solved (simulator.py:451-453); events fork and join it
+            self._side = torch.cuda.Stream(device=self.device)
+            self._ev_join = torch.cuda.Event()
 
     def set_placement(self, placement: Placement) -> None:
         """Adopt a new placement (adaptive replacement, ``adaptive.py``).  The
@@ -243,7 +253,9 @@ class MoELayer(torch.nn.Module):
             ck(L.hep_sched_solve(self.sched.handle, b.hist.data_ptr(), 1, E, None, HEP_SCHED_ALL,
                                  ctypes.byref(self.sched.out), s), "hep_sched_solve")
         else:
-            self.sched.launch_pipelined(b.hist, 1, E, self.static_share, HEP_SCHED_ALL, st)
+            # the static phase's routing runs on the side stream, forked after the split, while
+            # the scheduled phase is solved here
+            self.sched.launch_pipelined(b.hist, 1, E, self.static_share, HEP_SCHED_ALL, st, stream_static=self._side)
         mark("sched", 1)
         mark("assign", 0)
         if self.static_share is None:
@@ -251,23 +263,42 @@ class MoELayer(torch.nn.Module):
                                            K, tps, b.row_align, b.tok_row.data_ptr(), b.row_tok.data_ptr(),
                                            b.seg.data_ptr(), b.expert_rows.data_ptr(), b.assign_ws.data_ptr(),
                                            b.assign_ws.numel(), s), "hep_moe_assign_precounted")
+            mark("assign", 1)
+            mark("permute", 0)
+            if not self.fuse_permute:
+                ck(L.hep_moe_permute(x.data_ptr(), b.tok_row.data_ptr(), T, K, self.d, b.rows.data_ptr(), s),
+                   "hep_moe_permute")
+            mark("permute", 1)
         else:
+            # harmony_pipelined: the static phase's routing, assignment and dispatch (permute)
+            # run on the side stream, overlapping the scheduled phase's solve, assignment and
+            # permute on this stream (simulator.py:420-435, :451-453).  The two phases write
+            # disjoint entries of tok_row / row_tok / seg and disjoint rows.
             nnz = self.sched.nnz
-            ck(L.hep_moe_assign_phase(self.sched.handle, ctypes.byref(self.sched.former.out), None, None,
-                                      b.topk_idx.data_ptr(), T, K, tps, b.tok_row.data_ptr(), b.row_tok.data_ptr(),
-                                      b.seg.data_ptr(), b.expert_rows.data_ptr(), b.assign_ws.data_ptr(),
-                                      b.assign_ws.numel(), s), "hep_moe_assign_phase(static)")
-            ck(L.hep_moe_assign_phase(self.sched.handle, ctypes.byref(self.sched.out), self.sched.split.data_ptr(),
-                                      b.expert_rows.data_ptr() + 8 * E, b.topk_idx.data_ptr(), T, K, tps,
-                                      b.tok_row.data_ptr(), b.row_tok.data_ptr(), b.seg.data_ptr() + 16 * nnz,
-                                      b.expert_rows2.data_ptr(), b.assign_ws.data_ptr(), b.assign_ws.numel(), s),
+            split = self.sched.split.data_ptr()
+            side = self._side
+            ss = side.cuda_stream
+            tr0 = None if self.fuse_permute else b.tok_row_ph[0].data_ptr()
+            ck(L.hep_moe_assign_phase(self.sched.handle, ctypes.byref(self.sched.former.out), split, 0,
+                                      b.topk_idx.data_ptr(), T, K, tps, b.tok_row.data_ptr(), tr0,
+                                      b.row_tok.data_ptr(), b.seg.data_ptr(), b.expert_rows.data_ptr(),
+                                      b.assign_ws2.data_ptr(), b.assign_ws2.numel(), ss),
+               "hep_moe_assign_phase(static)")
+            if not self.fuse_permute:
+                ck(L.hep_moe_permute(x.data_ptr(), tr0, T, K, self.d, b.rows.data_ptr(), ss), "hep_moe_permute(static)")
+            self._ev_join.record(side)
+            tr1 = None if self.fuse_permute else b.tok_row_ph[1].data_ptr()
+            ck(L.hep_moe_assign_phase(self.sched.handle, ctypes.byref(self.sched.out), split, 1,
+                                      b.topk_idx.data_ptr(), T, K, tps, b.tok_row.data_ptr(), tr1,
+                                      b.row_tok.data_ptr(), b.seg.data_ptr() + 16 * nnz, b.expert_rows2.data_ptr(),
+                                      b.assign_ws.data_ptr(), b.assign_ws.numel(), s),
                "hep_moe_assign_phase(scheduled)")
-        mark("assign", 1)
-        mark("permute", 0)
-        if not self.fuse_permute:
-            ck(L.hep_moe_permute(x.data_ptr(), b.tok_row.data_ptr(), T, K, self.d, b.rows.data_ptr(), s),
-               "hep_moe_permute")
-        mark("permute", 1)
+            mark("assign", 1)
+            mark("permute", 0)
+            if not self.fuse_permute:
+                ck(L.hep_moe_permute(x.data_ptr(), tr1, T, K, self.d, b.rows.data_ptr(), s), "hep_moe_permute(scheduled)")
+            st.wait_event(self._ev_join)  # both phases' rows and segments are in place
+            mark("permute", 1)
         mark("ffn", 0)
         if self.fuse_permute:  # K5 fused into GEMM 1: x rows gathered by TMA through row_tok
             ck(L.hep_moe_expert_ffn_gather(x.data_ptr(), T, b.row_tok.data_ptr(), self.w13.data_ptr(),

@@ -178,20 +178,24 @@ class DeviceScheduler:
             "hep_sched_route",
         )
 
-    def launch_pipelined(self, d_loads, stride_e: int, stride_g: int, share, flags: int = HEP_SCHED_ALL, stream=None):
+    def launch_pipelined(self, d_loads, stride_e: int, stride_g: int, share, flags: int = HEP_SCHED_ALL, stream=None,
+                         stream_static=None):
         """Pipelined split (``simulator.py:420-435``): the static share's phase goes to
         ``self.former`` (a ``SchedBuffers``), the scheduled share's to this object.
-        ``share`` = static share as a Fraction (1 - pipeline_ratio)."""
+        ``share`` = static share as a Fraction (1 - pipeline_ratio).  ``stream_static``: the
+        static phase runs there, concurrently with the scheduled phase's solve (the caller
+        joins it back)."""
         share = Fraction(share)
         if self.former is None:
             self.former = SchedBuffers(self)
-            self.split = _lib.require_cuda().zeros(2 * max(self.E * self.G, 1), dtype=_lib.require_cuda().int64,
-                                                   device=self.device)
+            # [former E*G | latter E*G | static phase's integerized GPU loads G]
+            self.split = _lib.require_cuda().zeros(2 * max(self.E * self.G, 1) + self.G,
+                                                   dtype=_lib.require_cuda().int64, device=self.device)
         _lib.check(
             _lib.lib().hep_sched_pipelined(
                 self._h, d_loads.data_ptr(), stride_e, stride_g, share.numerator, share.denominator, flags,
                 self.split.data_ptr(), ctypes.byref(self.former.out), ctypes.byref(self.out),
-                _lib.stream_handle(stream),
+                _lib.stream_handle(stream), None if stream_static is None else stream_static.cuda_stream,
             ),
             "hep_sched_pipelined",
         )

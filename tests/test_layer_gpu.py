@@ -184,10 +184,11 @@ def test_baseline_shapes_full_size(P, cfg):
 @pytest.mark.parametrize("ratio,kind", [(0.5, "cayley"), (0.3, "cayley"), (0.8, "identical"), (1.0, "cayley")])
 def test_pipelined_split_layer(P, ratio, kind):
     """harmony_pipelined on the device: static share split evenly over replicas and
-    assigned first, scheduled share solved with gpu_base.  Both phases' schedules
-    and the [phase][expert][dst][src][rank] token->row map bit-exact against the
-    oracle; the layer output bit-identical to the single-phase layer (rows are
-    independent in the GEMMs, combine sums k in a fixed order)."""
+    assigned first (on a side stream, overlapping the scheduled phase's solve),
+    scheduled share solved with gpu_base.  Both phases' schedules and the
+    [expert][phase][dst][src][rank] token->row map bit-exact against the oracle; the
+    layer output bit-identical to the single-phase layer (rows are independent in the
+    GEMMs, combine sums k in a fixed order), eager and CUDA-graph replayed."""
     from fractions import Fraction
 
     from oracle import layer_ref
@@ -219,6 +220,22 @@ def test_pipelined_split_layer(P, ratio, kind):
                                                        b.topk_idx.cpu().numpy(), T // G)
     assert n_rows == T * K
     assert np.array_equal(b.tok_row.cpu().numpy(), tok_row)
+    # each phase's own row map: its rows, -1 for the other phase's assignments
+    for ph in range(2):
+        m = b.tok_row_ph[ph].cpu().numpy()
+        own = m >= 0
+        assert np.array_equal(m[own], tok_row[own])
+    assert np.array_equal(b.tok_row_ph[0].cpu().numpy() >= 0, ~(b.tok_row_ph[1].cpu().numpy() >= 0))
+    # the two-stream step captured as one CUDA graph, replayed on another micro-batch
+    x2 = torch.randn(T, d, generator=torch.Generator(device="cuda").manual_seed(9), device="cuda").to(torch.bfloat16)
+    ref2 = plain(x2).clone()
+    xin = x.clone()
+    g = pip.capture(xin)
+    xin.copy_(x2)
+    g.replay()
+    torch.cuda.synchronize()
+    pip.check_status()
+    assert torch.equal(pip.buffers(T).out, ref2)
 
 
 @pytest.mark.parametrize("G,E,K,d,F,T,case", [
