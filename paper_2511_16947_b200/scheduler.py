@@ -81,15 +81,25 @@ class SolveOptions:
 
 @dataclass
 class SolveStats:
-    """Counters (reference :138-148).  The device solver has no probe loop:
-    one launch computes m and the plan, so ``probes`` counts solves and
-    ``iterations_last`` counts kernel launches of the last solve (1)."""
+    """Counters (reference :138-148), restated for the device solver.  It has no probe
+    loop and no augmenting paths: one exact density evaluation over the 2^G GPU subsets
+    gives m (counted as one probe) and the lex-min sweep fixes one (expert, GPU) arc per
+    step (each step is the reference's reroute max-flow of ``lex_min_plan``, counted in
+    ``bfs_phases``).  A cold solve (fresh ``SolverState``) also builds the flow network --
+    the placement tables the reference keeps in ``SolverState._flow`` -- counted in
+    ``network_builds``; a warm solve reuses them, which is all a warm start saves here
+    (the plan is the same canonical lex-min plan either way, reference test C7).
+    ``iterations_last`` = the last solve's network build + probe + arc steps;
+    ``device_us_last`` = its scheduler kernel time (CUDA events)."""
 
     solves: int = 0
     probes: int = 0
     bfs_phases: int = 0
     pivots: int = 0
     iterations_last: int = 0
+    network_builds: int = 0
+    device_us_last: float = 0.0
+    device_us_total: float = 0.0
 
     @property
     def iterations_total(self) -> int:
@@ -304,15 +314,26 @@ def _device_solve(state: SolverState, loads: LoadMatrix, gpu_base) -> ReplicaLoa
         if len(gpu_base) != G:
             raise DimensionError(f"gpu_base has {len(gpu_base)} entries for {G} GPUs")
         d_base = torch.as_tensor(np.asarray(gpu_base, dtype=np.int64)).to(dev.device)
-    dev.launch_solve(d_loads, G, 1, d_base, flags=HEP_SCHED_SOLVE)
+    st = torch.cuda.current_stream(dev.device)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    dev.launch_solve(d_loads, G, 1, d_base, flags=HEP_SCHED_SOLVE, stream=st)
+    e1.record(st)
     dev.check_status("solve_replica_loads")
     m_num, m_den, Q, _ = dev.m.cpu().tolist()
     xq = dev.rows(dev.xq)
     entries = tuple(tuple(Fraction(v, Q) for v in row) for row in xq)
     objective = Fraction(m_num, m_den)
+    cold = state.stats.solves == 0  # a fresh state builds (or fetches) the placement tables
+    steps = dev.nnz  # lex-min arc steps
     state.stats.solves += 1
     state.stats.probes += 1
-    state.stats.iterations_last = 1
+    state.stats.bfs_phases += steps
+    state.stats.network_builds += int(cold)
+    state.stats.iterations_last = int(cold) + 1 + steps
+    us = 1e3 * e0.elapsed_time(e1)
+    state.stats.device_us_last = us
+    state.stats.device_us_total += us
     state.last_objective = objective
     return ReplicaLoadPlan(num_gpus=G, groups=placement.edp_groups, entries=entries, objective=objective)
 

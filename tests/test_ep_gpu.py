@@ -189,7 +189,7 @@ def test_local_ep_p2p_light_split_on_pairs(P, tune):
     assert int(P._lib.lib().hep_moe_ffn_launches(T * K, E, 0)) == 8
 
 
-def _p2p_worker(rank, world, port, q):
+def _p2p_worker(rank, world, port, q, kind="cayley"):
     import os
 
     import torch.distributed as dist
@@ -202,7 +202,7 @@ def _p2p_worker(rank, world, port, q):
         from paper_2511_16947_b200.ep import DistComm, EPMoELayer
 
         G, E, K, d, F, T = world, 8, 2, 256, 256, 2048
-        pl = P.cayley_symmetric(P.ClusterShape(G, E, 2))
+        pl = _placement(P, G, E, kind, 1.5)
         bias = torch.tensor(P.zipf_gate_bias(E, 1.0, 0))
         x = torch.randn(G * T, d, generator=torch.Generator(device="cuda").manual_seed(12), device="cuda")
         x = x.to(torch.bfloat16)[rank * T:(rank + 1) * T].contiguous()
@@ -228,22 +228,23 @@ def _p2p_worker(rank, world, port, q):
         dist.destroy_process_group()
 
 
-def test_ep_p2p_over_cuda_ipc_two_processes(P):
-    """One process per rank (both on this GPU), peer buffers mapped with CUDA IPC and the
+@pytest.mark.parametrize("world,kind", [(2, "cayley"), (4, "asym")])
+def test_ep_p2p_over_cuda_ipc_processes(P, world, kind):
+    """One process per rank (all on this GPU), peer buffers mapped with CUDA IPC and the
     ranks synchronised by device-side barriers: the NVLink-path forward — eager, and
-    replayed from a CUDA graph — equals the in-process reference bit for bit."""
+    replayed from a CUDA graph — equals the in-process reference bit for bit; 2 ranks on
+    the Cayley placement and 4 ranks on an asymmetric (adaptive) placement."""
     import socket
 
     import torch.multiprocessing as mp
     from paper_2511_16947_b200.ep import EPMoELayer, LocalComm
 
-    world = 2
     with socket.socket() as so:
         so.bind(("127.0.0.1", 0))
         port = so.getsockname()[1]
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_p2p_worker, args=(r, world, port, q, kind)) for r in range(world)]
     for p in procs:
         p.start()
     res = {}
@@ -253,7 +254,7 @@ def test_ep_p2p_over_cuda_ipc_two_processes(P):
     for p in procs:
         p.join(timeout=60)
     G, E, K, d, F, T = world, 8, 2, 256, 256, 2048
-    pl = P.cayley_symmetric(P.ClusterShape(G, E, 2))
+    pl = _placement(P, G, E, kind, 1.5)
     bias = torch.tensor(P.zipf_gate_bias(E, 1.0, 0))
     x = torch.randn(G * T, d, generator=torch.Generator(device="cuda").manual_seed(12), device="cuda").to(torch.bfloat16)
     ref = EPMoELayer(pl, d, F, K, LocalComm(G), range(G), seed=7, gate_bias=bias).forward(
