@@ -290,9 +290,11 @@ size_t hep_moe_assign_ep_workspace(hep_sched_t h, int64_t T, int K);
  * d_seg_out [n_slots][4] (row_start, rows, slot, 0) and d_slot_rows [n_slots+1] (block
  * starts; the last entry = rows of the aligned buffer), the d_seg / d_expert_rows
  * arguments of hep_moe_expert_ffn_train / hep_moe_expert_ffn_bwd with n_experts = n_slots.
+ * row_map_len > 0: entries [R_recv, row_map_len) are set to -1 (the NVLink path's fixed-size
+ * receive buffer, R_recv known only on the device; hep_moe_permute skips them).
  */
 int hep_moe_ep_train_layout(const int32_t *d_seg, int n_hosted, int G, int n_slots, int row_align, int32_t *d_row_map,
-                            int32_t *d_seg_out, int64_t *d_slot_rows, void *stream);
+                            int64_t row_map_len, int32_t *d_seg_out, int64_t *d_slot_rows, void *stream);
 /* experts hosted by `rank` and the number of local weight slots it needs */
 int hep_sched_hosted(hep_sched_t h, int rank, int *n_hosted, int *n_slots);
 
@@ -322,6 +324,13 @@ int hep_moe_dispatch_p2p(const void *d_x, const int32_t *d_tok_row, int64_t T, i
                          const int32_t *d_status, void *stream);
 int hep_moe_return_addr(const int64_t *d_pair, int rank, int num_gpus, const uint64_t *d_peer_back, int64_t row_bytes,
                         int64_t capacity, uint64_t *d_addr, void *stream);
+/* Received rows back to their sources (the NVLink return of the training path): row
+ * d_src[d_row_map ? d_row_map[i] : i] -> d_addr[i] (hep_moe_return_addr's table), for i below
+ * this rank's received count (sum_s pair[s][rank], at most capacity); nothing when d_status is
+ * set. */
+int hep_moe_rows_to_addr(const void *d_src, const int32_t *d_row_map, const int64_t *d_pair, int rank, int num_gpus,
+                         int64_t capacity, int64_t d_model, const uint64_t *d_addr, const int32_t *d_status,
+                         void *stream);
 int hep_moe_expert_ffn_p2p(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg, int n_seg,
                            int64_t R, int64_t rows_hint, int64_t d_model, int64_t ffn, int n_experts, void *d_h,
                            const uint64_t *d_y_addr, void *d_workspace, size_t workspace_bytes, int32_t *d_status,

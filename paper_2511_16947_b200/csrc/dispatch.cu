@@ -918,8 +918,8 @@ namespace hep {
 // a few hundred adds) and writes row_map for the segment's rows; block 0 also writes
 // the per-slot segments and the slot row offsets.
 __global__ void __launch_bounds__(256) ep_layout_kernel(const int32_t *seg, int n_hosted, int G, int n_slots,
-                                                        int align, int32_t *row_map, int32_t *seg_out,
-                                                        int64_t *slot_rows) {
+                                                        int align, int32_t *row_map, int64_t row_map_len,
+                                                        int32_t *seg_out, int64_t *slot_rows) {
     extern __shared__ int64_t sm_tot[];  // [n_slots] totals, then aligned starts
     const int tid = threadIdx.x, nt = blockDim.x;
     for (int i = tid; i < n_slots; i += nt) sm_tot[i] = 0;
@@ -947,6 +947,12 @@ __global__ void __launch_bounds__(256) ep_layout_kernel(const int32_t *seg, int 
         if (blockIdx.x == 0) slot_rows[n_slots] = run;
     }
     __syncthreads();
+    if (row_map_len > 0) {  // received rows past this micro-batch's count map to -1 (skipped)
+        int64_t R = 0;
+        for (int i = 0; i < G * n_hosted; ++i) R += seg[4 * i + 1];
+        for (int64_t i = R + (int64_t)blockIdx.x * nt + tid; i < row_map_len; i += (int64_t)gridDim.x * nt)
+            row_map[i] = -1;
+    }
     if (n_hosted == 0) return;
     const int b = blockIdx.x, src = b / n_hosted, h = b % n_hosted;
     const int32_t *sg = seg + 4 * b;
@@ -958,7 +964,8 @@ __global__ void __launch_bounds__(256) ep_layout_kernel(const int32_t *seg, int 
 }  // namespace hep
 
 extern "C" int hep_moe_ep_train_layout(const int32_t *d_seg, int n_hosted, int G, int n_slots, int row_align,
-                                       int32_t *d_row_map, int32_t *d_seg_out, int64_t *d_slot_rows, void *stream) {
+                                       int32_t *d_row_map, int64_t row_map_len, int32_t *d_seg_out,
+                                       int64_t *d_slot_rows, void *stream) {
     HEP_NVTX("hep_moe_ep_train_layout");
     HEP_REQUIRE(d_seg && d_row_map && d_seg_out && d_slot_rows, HEP_E_CONTRACT, "hep_moe_ep_train_layout: null");
     HEP_REQUIRE(G >= 1 && G <= HEP_MAX_GPUS && n_hosted >= 0 && n_slots >= n_hosted && n_slots <= 1024 &&
@@ -968,7 +975,7 @@ extern "C" int hep_moe_ep_train_layout(const int32_t *d_seg, int n_hosted, int G
     if (n_slots == 0) return HEP_OK;
     const int blocks = n_hosted > 0 ? G * n_hosted : 1;
     ep_layout_kernel<<<blocks, 256, sizeof(int64_t) * n_slots, (cudaStream_t)stream>>>(
-        d_seg, n_hosted, G, n_slots, row_align, d_row_map, d_seg_out, d_slot_rows);
+        d_seg, n_hosted, G, n_slots, row_align, d_row_map, row_map_len, d_seg_out, d_slot_rows);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
 }

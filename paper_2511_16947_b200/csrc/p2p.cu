@@ -207,6 +207,45 @@ extern "C" int hep_moe_dispatch_p2p(const void *d_x, const int32_t *d_tok_row, i
     return HEP_OK;
 }
 
+namespace hep {
+// received rows -> their source ranks: rows[i] (or rows[row_map[i]]) -> the address addr[i]
+// (a peer's buffer over NVLink, or local), i < this rank's received count from the transfer
+// plan (at most capacity); one warp per row, 16-byte vector copies
+__global__ void __launch_bounds__(256) rows_to_addr_kernel(const int4 *__restrict__ src, const int32_t *__restrict__ row_map,
+                                                           const int64_t *__restrict__ pair, int me, int G,
+                                                           int64_t cap, int64_t nvec, const uint64_t *__restrict__ addr,
+                                                           const int32_t *status) {
+    if (status && *status) return;
+    int64_t n = 0;
+    for (int s = 0; s < G; ++s) n += pair[s * G + me];
+    if (n > cap) n = cap;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = warp; i < n; i += nwarps) {
+        const int64_t r = row_map ? row_map[i] : i;
+        const int4 *s = src + r * nvec;
+        int4 *d = reinterpret_cast<int4 *>(addr[i]);
+        for (int64_t v = lane; v < nvec; v += 32) d[v] = __ldg(s + v);
+    }
+}
+}  // namespace hep
+
+extern "C" int hep_moe_rows_to_addr(const void *d_src, const int32_t *d_row_map, const int64_t *d_pair, int rank,
+                                    int num_gpus, int64_t capacity, int64_t d_model, const uint64_t *d_addr,
+                                    const int32_t *d_status, void *stream) {
+    HEP_NVTX("hep_moe_rows_to_addr");
+    HEP_REQUIRE(d_src && d_pair && d_addr, HEP_E_CONTRACT, "hep_moe_rows_to_addr: null pointer");
+    HEP_REQUIRE(d_model % 8 == 0 && num_gpus >= 1 && num_gpus <= HEP_MAX_GPUS && rank >= 0 && rank < num_gpus,
+                HEP_E_DIMENSION, "hep_moe_rows_to_addr: d_model %% 8, rank / G");
+    if (capacity <= 0) return HEP_OK;
+    const int64_t warps = capacity < 148 * 64 ? capacity : 148 * 64;
+    rows_to_addr_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        (const int4 *)d_src, d_row_map, d_pair, rank, num_gpus, capacity, d_model / 8, d_addr, d_status);
+    HEP_CHECK_LAUNCH();
+    return HEP_OK;
+}
+
 extern "C" int hep_moe_return_addr(const int64_t *d_pair, int rank, int num_gpus, const uint64_t *d_peer_back,
                                    int64_t row_bytes, int64_t capacity, uint64_t *d_addr, void *stream) {
     HEP_NVTX("hep_moe_return_addr");

@@ -221,6 +221,22 @@ class EPRank:
             n_seg = max(G * self.n_hosted, 1)
             b["ffn_ws"] = torch.empty(max(int(L.hep_moe_ffn_workspace(n_seg, cap, self.n_slots)), 256),
                                       dtype=torch.uint8, device=dev)
+            if layer.train_mode:  # NVLink training: the backward's two exchanges and the aligned layout
+                F, ns = layer.F, self.n_slots
+                Ral = cap + 63 * ns
+                bf = dict(dtype=torch.bfloat16, device=dev)
+                i32 = dict(dtype=torch.int32, device=dev)
+                b.update(
+                    dy_recv=torch.empty(cap, d, **bf),       # peers' dY rows land here (receive layout)
+                    dx_back=torch.empty(max(T * K, 1), d, **bf),  # peers' dX rows return here (send layout)
+                    dx_addr=torch.empty(cap, dtype=torch.int64, device=dev),
+                    ident=torch.arange(max(T * K, 1), dtype=torch.int32, device=dev),
+                    row_map=torch.empty(cap, **i32), seg_al=torch.empty(ns, 4, **i32),
+                    slot_rows=torch.empty(ns + 1, dtype=torch.int64, device=dev), Ral=Ral,
+                    rows_al=torch.zeros(Ral, d, **bf), h_al=torch.zeros(Ral, F, **bf),
+                    y_al=torch.zeros(Ral, d, **bf), pre_al=torch.zeros(Ral, 2 * F, **bf),
+                    ffn_ws_al=torch.empty(max(int(L.hep_moe_ffn_workspace(ns, Ral, ns)), 256), dtype=torch.uint8,
+                                          device=dev))
         return b
 
     def buffers(self, layer: "EPMoELayer", T: int) -> dict:
@@ -268,10 +284,9 @@ class EPMoELayer:
         self.recv_capacity_factor = float(recv_capacity_factor)
         if exchange not in ("nccl", "p2p"):
             raise ValueError("exchange must be 'nccl' (all-to-all-v collectives) or 'p2p' (NVLink peer stores)")
-        if exchange == "p2p" and train:
-            raise ValueError("the peer-memory exchange is built for the forward pass; train with exchange='nccl'")
         self.exchange = exchange
         self._peer_tables: dict[int, list] = {}
+        self._peer_tables_bwd: dict[int, list] = {}
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
         self.placement, self.comm = placement, comm
         self.G, self.E, self.K, self.d, self.F = placement.num_gpus, placement.num_experts, top_k, d_model, ffn
@@ -306,6 +321,7 @@ class EPMoELayer:
         self.placement = placement
         self.ranks = new_ranks
         self._peer_tables.clear()  # new exchange buffers: peers re-map them on the next forward
+        self._peer_tables_bwd.clear()
         return stats
 
     @torch.no_grad()
@@ -334,6 +350,12 @@ class EPMoELayer:
             back = self.comm.exchange_ptrs([b["back"].data_ptr() for b in bs])
             tab = [(torch.tensor(rv, dtype=torch.int64, device=self.device),
                     torch.tensor(bk, dtype=torch.int64, device=self.device)) for rv, bk in zip(recv, back)]
+            if self.train_mode:
+                dyr = self.comm.exchange_ptrs([b["dy_recv"].data_ptr() for b in bs])
+                dxb = self.comm.exchange_ptrs([b["dx_back"].data_ptr() for b in bs])
+                self._peer_tables_bwd[T] = [(torch.tensor(a, dtype=torch.int64, device=self.device),
+                                             torch.tensor(c, dtype=torch.int64, device=self.device))
+                                            for a, c in zip(dyr, dxb)]
             self._peer_tables[T] = tab
         return tab
 
@@ -432,6 +454,10 @@ class EPMoELayer:
         for rk, b, x in zip(self.ranks, bs, xs):
             n_seg = G * rk.n_hosted
             x_rows = x.shape[0]  # balanced schedule: about T*K rows land on every rank
+            if self.train_mode:
+                self._train_ffn_p2p(rk, b, s)
+                b["x"] = x
+                continue
             if n_seg:
                 ck(L.hep_moe_expert_ffn_p2p(b["recv"].data_ptr(), rk.w13.data_ptr(), rk.w2.data_ptr(),
                                             b["seg"].data_ptr(), n_seg, b["cap"], x_rows * K, d, F, rk.n_slots,
@@ -451,6 +477,113 @@ class EPMoELayer:
                                  b["out"].data_ptr(), s), "hep_moe_combine")
             outs.append(b["out"])
         return outs
+
+    def _train_ffn_p2p(self, rk: EPRank, b: dict, s) -> None:
+        """NVLink training forward, FFN part: the received rows (count known only on the
+        device) are laid out per local weight slot, 64-row aligned (row_map entries past the
+        count are -1 and skipped), the training FFN keeps the pre-activations, and the output
+        rows go straight back into the sources' return buffers."""
+        L = _lib.lib()
+        ck = _lib.check
+        G, d, F = self.G, self.d, self.F
+        ns, cap, Ral = rk.n_slots, b["cap"], b["Ral"]
+        st = rk.sched.status.data_ptr()
+        ck(L.hep_moe_ep_train_layout(b["seg"].data_ptr(), rk.n_hosted, G, ns, 64, b["row_map"].data_ptr(), cap,
+                                     b["seg_al"].data_ptr(), b["slot_rows"].data_ptr(), s), "hep_moe_ep_train_layout")
+        ck(L.hep_moe_permute(b["recv"].data_ptr(), b["row_map"].data_ptr(), cap, 1, d, b["rows_al"].data_ptr(), s),
+           "hep_moe_permute(align)")
+        # padding rows are never written by the GEMMs, the weight-gradient GEMMs contract over
+        # them: X and H padding must be zero
+        ck(L.hep_moe_zero_padding(b["slot_rows"].data_ptr(), b["seg_al"].data_ptr(), ns, ns, b["rows_al"].data_ptr(), d,
+                                  s), "hep_moe_zero_padding(rows)")
+        ck(L.hep_moe_zero_padding(b["slot_rows"].data_ptr(), b["seg_al"].data_ptr(), ns, ns, b["h_al"].data_ptr(), F,
+                                  s), "hep_moe_zero_padding(h)")
+        ck(L.hep_moe_expert_ffn_train(b["rows_al"].data_ptr(), rk.w13.data_ptr(), rk.w2.data_ptr(),
+                                      b["seg_al"].data_ptr(), ns, Ral, d, F, ns, b["h_al"].data_ptr(),
+                                      b["y_al"].data_ptr(), b["pre_al"].data_ptr(), b["ffn_ws_al"].data_ptr(),
+                                      b["ffn_ws_al"].numel(), st, s), "hep_moe_expert_ffn_train")
+        ck(L.hep_moe_rows_to_addr(b["y_al"].data_ptr(), b["row_map"].data_ptr(), rk.sched.transfer.data_ptr(), rk.rank,
+                                  G, cap, d, b["y_addr"].data_ptr(), st, s), "hep_moe_rows_to_addr(y)")
+
+    def _backward_p2p(self, douts, st):
+        """NVLink training backward: dY rows stored into the destinations' receive buffers
+        (the dispatch kernel on the send layout), the expert FFN backward on the aligned
+        layout, dX rows stored back into the sources' buffers, device barriers between."""
+        L = _lib.lib()
+        s = st.cuda_stream
+        ck = _lib.check
+        K, E, G, d, F = self.K, self.E, self.G, self.d, self.F
+        dev = self.device
+        T = douts[0].shape[0]
+        bs = [rk.p2p_buffers(self, T) for rk in self.ranks]
+        tabs = self._peer_table(T)
+        btabs = self._peer_tables_bwd[T]
+        dws = []
+        for rk, b, dout, (p_recv, p_back), (p_dyrecv, p_dxback) in zip(self.ranks, bs, douts, tabs, btabs):
+            dy = torch.empty(max(T * K, 1), d, dtype=torch.bfloat16, device=dev)
+            dw = torch.empty(T, K, dtype=torch.float32, device=dev)
+            ck(L.hep_moe_combine_bwd(dout.contiguous().data_ptr(), b["back"].data_ptr(), b["tok_row"].data_ptr(),
+                                     b["topk_w"].data_ptr(), T, K, d, dy.data_ptr(), dw.data_ptr(), s),
+               "hep_moe_combine_bwd")
+            # every send position p (= its row of dy) to its destination's receive slot
+            ck(L.hep_moe_dispatch_p2p(dy.data_ptr(), b["ident"].data_ptr(), T * K, 1, d, rk.rank, G,
+                                      rk.sched.transfer.data_ptr(), p_dyrecv.data_ptr(), b["cap"],
+                                      rk.sched.status.data_ptr(), s), "hep_moe_dispatch_p2p(dY)")
+            ck(L.hep_moe_return_addr(rk.sched.transfer.data_ptr(), rk.rank, G, p_dxback.data_ptr(), d * 2, b["cap"],
+                                     b["dx_addr"].data_ptr(), s), "hep_moe_return_addr(dX)")
+            b["dy_keep"] = dy
+            dws.append(dw)
+        self._sync_ranks(s)  # every dY row arrived
+        dw13s, dw2s = [], []
+        for rk, b in zip(self.ranks, bs):
+            ns, Ral, cap = rk.n_slots, b["Ral"], b["cap"]
+            bf = dict(dtype=torch.bfloat16, device=dev)
+            dy_al = torch.zeros(Ral, d, **bf)
+            ck(L.hep_moe_permute(b["dy_recv"].data_ptr(), b["row_map"].data_ptr(), cap, 1, d, dy_al.data_ptr(), s),
+               "hep_moe_permute(dY align)")
+            da13 = torch.empty(Ral, 2 * F, **bf)
+            dx_al = torch.empty(Ral, d, **bf)
+            dw13 = torch.empty(ns, 2 * F, d, dtype=torch.float32, device=dev)
+            dw2 = torch.empty(ns, d, F, dtype=torch.float32, device=dev)
+            ck(L.hep_moe_expert_ffn_bwd(b["rows_al"].data_ptr(), b["pre_al"].data_ptr(), b["h_al"].data_ptr(),
+                                        dy_al.data_ptr(), rk.w13.data_ptr(), rk.w2.data_ptr(), b["seg_al"].data_ptr(),
+                                        ns, b["slot_rows"].data_ptr(), Ral, d, F, ns, da13.data_ptr(),
+                                        dx_al.data_ptr(), dw13.data_ptr(), dw2.data_ptr(), b["ffn_ws_al"].data_ptr(),
+                                        b["ffn_ws_al"].numel(), rk.sched.status.data_ptr(), s),
+               "hep_moe_expert_ffn_bwd")
+            ck(L.hep_moe_rows_to_addr(dx_al.data_ptr(), b["row_map"].data_ptr(), rk.sched.transfer.data_ptr(),
+                                      rk.rank, G, cap, d, b["dx_addr"].data_ptr(), rk.sched.status.data_ptr(), s),
+               "hep_moe_rows_to_addr(dX)")
+            b["dx_al_keep"] = dx_al
+            dw13s.append(dw13)
+            dw2s.append(dw2)
+        self._sync_ranks(s)  # every dX row is back at its source
+        dxs, dwgs = [], []
+        for b, dw in zip(bs, dws):
+            x = b["x"]
+            dlogits = torch.empty(T, self.e64, dtype=torch.bfloat16, device=dev)
+            dwg = torch.empty(self.e64, d, dtype=torch.float32, device=dev)
+            dxg = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+            dx = torch.empty(T, d, dtype=torch.bfloat16, device=dev)
+            ck(L.hep_gate_bwd(b["topk_idx"].data_ptr(), b["topk_w"].data_ptr(), dw.data_ptr(), T, K, self.e64,
+                              dlogits.data_ptr(), s), "hep_gate_bwd")
+            ck(L.hep_router_bwd(x.data_ptr(), self.wg.data_ptr(), dlogits.data_ptr(), T, d, self.e64,
+                                dwg.data_ptr(), dxg.data_ptr(), s), "hep_router_bwd")
+            ck(L.hep_moe_gather_sum(b["dx_back"].data_ptr(), b["tok_row"].data_ptr(), None, dxg.data_ptr(), T, K, d,
+                                    dx.data_ptr(), s), "hep_moe_gather_sum")
+            dxs.append(dx)
+            dwgs.append(dwg)
+        self.comm.all_reduce(dwgs)
+        edp_reduce(self.placement, self.comm, [rk.rank for rk in self.ranks], dw13s, dw2s)
+        return [(dx, dwg[:E], dw13, dw2) for dx, dwg, dw13, dw2 in zip(dxs, dwgs, dw13s, dw2s)]
+
+    def _sync_ranks(self, s) -> None:
+        """Order the exchanges across ranks: device barrier (DistComm device_sync) or a
+        stream drain + host barrier."""
+        if getattr(self.comm, "device_sync", False):
+            self._device_barrier(s)
+        else:
+            self.comm.barrier()
 
     def _forward(self, xs, st, ev):
         L = _lib.lib()
@@ -531,7 +664,7 @@ class EPMoELayer:
         row_map = torch.empty(max(R, 1), **i32)
         seg_al = torch.empty(ns, 4, **i32)
         slot_rows = torch.empty(ns + 1, dtype=torch.int64, device=self.device)
-        ck(L.hep_moe_ep_train_layout(b["seg"].data_ptr(), rk.n_hosted, G, ns, 64, row_map.data_ptr(),
+        ck(L.hep_moe_ep_train_layout(b["seg"].data_ptr(), rk.n_hosted, G, ns, 64, row_map.data_ptr(), 0,
                                      seg_al.data_ptr(), slot_rows.data_ptr(), s), "hep_moe_ep_train_layout")
         Ral = R + 63 * ns
         bf = dict(dtype=torch.bfloat16, device=self.device)
@@ -570,6 +703,8 @@ class EPMoELayer:
             raise RuntimeError("construct EPMoELayer(train=True) to run the backward pass")
         st = stream if stream is not None else torch.cuda.current_stream()
         with torch.cuda.stream(st):
+            if self.exchange == "p2p":
+                return self._backward_p2p(douts, st)
             return self._backward(douts, st)
 
     def _backward(self, douts, st):

@@ -264,3 +264,37 @@ def test_ep_p2p_over_cuda_ipc_processes(P, world, kind):
         assert not isinstance(o1, str), o1
         want = ref[r].float().cpu().numpy()
         assert np.array_equal(o1, want) and np.array_equal(o2, want), r
+
+
+@pytest.mark.parametrize("G,E,K,d,F,T,kind,s", [
+    (4, 8, 2, 512, 512, 4096, "cayley", 1.0),
+    (8, 32, 4, 256, 256, 4096, "asym", 1.5),
+])
+def test_local_ep_training_over_peer_stores(P, G, E, K, d, F, T, kind, s):
+    """EP training with both directions of both exchanges as peer stores (dispatch kernel,
+    FFN output rows and dX rows stored into the sources' buffers, dY rows into the
+    destinations'): forward, dx and every gradient bit-identical to the NCCL-style
+    all-to-all-v training path (the exchanges only move rows; the GEMM tiles are the same)."""
+    from paper_2511_16947_b200.ep import EPMoELayer, LocalComm
+
+    pl = _placement(P, G, E, kind, s)
+    bias = torch.tensor(P.zipf_gate_bias(E, s, 0))
+    g = torch.Generator(device="cuda").manual_seed(31)
+    x = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
+    dout = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
+    tps = T // G
+    xs = [x[r * tps:(r + 1) * tps].contiguous() for r in range(G)]
+    ds = [dout[r * tps:(r + 1) * tps].contiguous() for r in range(G)]
+    res = {}
+    for exchange in ("nccl", "p2p"):
+        ep = EPMoELayer(pl, d, F, K, LocalComm(G), range(G), seed=8, gate_bias=bias, train=True, exchange=exchange)
+        outs = [o.clone() for o in ep.forward(xs)]
+        grads = ep.backward(ds)
+        torch.cuda.synchronize()
+        ep.check_status()
+        res[exchange] = (outs, grads)
+    (o1, g1), (o2, g2) = res["nccl"], res["p2p"]
+    for r in range(G):
+        assert torch.equal(o1[r], o2[r]), r
+        for a, b in zip(g1[r], g2[r]):
+            assert torch.equal(a, b), r

@@ -3,7 +3,7 @@
 # traffic), bench (3 configs + pipelined variant + reference arm), full ncu captures
 # of the top kernels.  Output under gpurun_out/ (copy what is judged to profiles/).
 set -x
-R=${ROUND:-r01}
+R=${ROUND:-r02}
 timeout 1200 python -m pytest tests -m gpu -q --timeout 900 > gpurun_out/t_all_$R.log 2>&1
 tail -2 gpurun_out/t_all_$R.log
 timeout 120 python tools/sched_timing.py > gpurun_out/sched_timing_$R.json 2>&1
@@ -12,13 +12,18 @@ for c in mixtral qwen3 dsv3; do
     --kernel-name-base demangled -k regex:"hep::|gemm::|sched_kernel|permute|combine|chunk|plan_prep|gate_topk" -c 17 --csv \
     --log-file gpurun_out/launches_${c}_$R.csv python bench.py --config $c --profile --steps 1 --warmup 1 --no-cpu-baseline > /dev/null 2>&1
 done
-python tools/traffic.py gpurun_out/launches_mixtral_$R.csv gpurun_out/launches_qwen3_$R.csv gpurun_out/launches_dsv3_$R.csv > gpurun_out/traffic_$R.json
+# the launch lists are committed under profiles/<round>/ afterwards: record that path
+python tools/traffic.py --tracked=profiles/${R%?} gpurun_out/launches_mixtral_$R.csv gpurun_out/launches_qwen3_$R.csv gpurun_out/launches_dsv3_$R.csv > gpurun_out/traffic_$R.json
 cp gpurun_out/traffic_$R.json profiles/traffic.json
-for c in mixtral qwen3 dsv3; do
-  timeout 900 python bench.py --config $c > gpurun_out/bench_${c}_$R.json 2> gpurun_out/bench_${c}_$R.err
+# the default line (Mixtral + Qwen3 / DSv3 folded in), then each config as the primary
+timeout 900 python bench.py > gpurun_out/bench_default_$R.json 2> gpurun_out/bench_default_$R.err
+for c in qwen3 dsv3; do
+  timeout 900 python bench.py --config $c --other-configs "" > gpurun_out/bench_${c}_$R.json 2> gpurun_out/bench_${c}_$R.err
 done
-timeout 600 python bench.py --config mixtral --pipeline-ratio 0.5 --no-cpu-baseline --no-train > gpurun_out/bench_mixtral_pipelined_$R.json 2>&1
-timeout 300 python bench.py --impl reference --config mixtral --steps 3 --warmup 1 > gpurun_out/bench_ref_mixtral_$R.json 2>&1
+for c in qwen3 dsv3; do
+  timeout 600 python bench.py --config $c --pipeline-ratio 0.5 --other-configs "" --no-cpu-baseline --no-train --no-balance-sweep > gpurun_out/bench_${c}_pipelined_$R.json 2>&1
+done
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref_mixtral_$R.json 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
   -k regex:"gemm2sm_kernel|gemm_kernel|sched_kernel|permute|combine|chunk_map|plan_prep" -c 9 \
   -o gpurun_out/prof_mixtral_$R python bench.py --config mixtral --profile --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_mixtral_$R.log 2>&1

@@ -1,6 +1,6 @@
 """Per-launch DRAM traffic of the hot kernels from ncu launch lists.
 
-    python tools/traffic.py profiles/r01/launches_<cfg>_<round>.csv ... > profiles/traffic.json
+    python tools/traffic.py [--tracked=profiles/<round>] launches_<cfg>_<round>.csv ... > profiles/traffic.json
 
 Each CSV is one `ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,
 dram__bytes_write.sum --csv` run of `bench.py --config <cfg> --profile`.  The
@@ -24,9 +24,10 @@ def launches(path):
     return [rows[k] for k in sorted(rows)]
 
 
-def summarise(path):
+def summarise(path, tracked_dir=None):
     ks = launches(path)
-    out = {"source": os.path.relpath(path)}
+    # the launch lists are copied into profiles/<round>/ (tracked); record that path
+    out = {"source": os.path.join(tracked_dir, os.path.basename(path)) if tracked_dir else os.path.relpath(path)}
     for i, k in enumerate(ks):
         if "tile_count_kernel" in k["name"]:
             # hep_moe_expert_ffn: its tile-list kernels and grouped GEMMs (two, or four with the
@@ -59,7 +60,11 @@ def summarise(path):
 
 if __name__ == "__main__":
     res = {}
-    for p in sys.argv[1:]:
+    args = sys.argv[1:]
+    tracked = None
+    if args and args[0].startswith("--tracked="):
+        tracked = args.pop(0).split("=", 1)[1]
+    for p in args:
         m = re.search(r"launches_([a-z0-9]+)_", os.path.basename(p))
-        res[m.group(1) if m else p] = summarise(p)
+        res[m.group(1) if m else p] = summarise(p, tracked)
     print(json.dumps(res, indent=1))
