@@ -298,3 +298,75 @@ def test_local_ep_training_over_peer_stores(P, G, E, K, d, F, T, kind, s):
         assert torch.equal(o1[r], o2[r]), r
         for a, b in zip(g1[r], g2[r]):
             assert torch.equal(a, b), r
+
+
+def _p2p_train_worker(rank, world, port, q):
+    import os
+
+    import torch.distributed as dist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2511_16947_b200 as P
+        from paper_2511_16947_b200.ep import DistComm, EPMoELayer
+
+        G, E, K, d, F, T = world, 8, 2, 256, 256, 2048
+        pl = _placement(P, G, E, "cayley", 1.0)
+        bias = torch.tensor(P.zipf_gate_bias(E, 1.0, 0))
+        g = torch.Generator(device="cuda").manual_seed(13)
+        x = torch.randn(G * T, d, generator=g, device="cuda").to(torch.bfloat16)[rank * T:(rank + 1) * T].contiguous()
+        dout = torch.randn(G * T, d, generator=g, device="cuda").to(torch.bfloat16)[rank * T:(rank + 1) * T].contiguous()
+        layer = EPMoELayer(pl, d, F, K, DistComm(), [rank], seed=9, gate_bias=bias, train=True, exchange="p2p")
+        out = layer.forward([x])[0].clone()
+        dx, dwg, dw13, dw2 = layer.backward([dout])[0]
+        torch.cuda.synchronize()
+        layer.check_sync()
+        layer.check_status()
+        q.put((rank, [t.float().cpu().numpy() for t in (out, dx, dwg, dw13, dw2)]))
+    except Exception as exc:  # report instead of hanging the parent
+        q.put((rank, repr(exc)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ep_training_over_cuda_ipc_two_processes(P):
+    """EP training with the NVLink exchanges between two real processes (CUDA IPC peer
+    buffers, device-side barriers; the EDP gradient reduction and the router all-reduce
+    over the process group): forward, dx and all gradients equal to the in-process
+    LocalComm training step bit for bit."""
+    import socket
+
+    import torch.multiprocessing as mp
+    from paper_2511_16947_b200.ep import EPMoELayer, LocalComm
+
+    world = 2
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_p2p_train_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {}
+    for _ in range(world):
+        r, v = q.get(timeout=300)
+        res[r] = v
+    for p in procs:
+        p.join(timeout=60)
+    G, E, K, d, F, T = world, 8, 2, 256, 256, 2048
+    pl = _placement(P, G, E, "cayley", 1.0)
+    bias = torch.tensor(P.zipf_gate_bias(E, 1.0, 0))
+    g = torch.Generator(device="cuda").manual_seed(13)
+    x = torch.randn(G * T, d, generator=g, device="cuda").to(torch.bfloat16)
+    dout = torch.randn(G * T, d, generator=g, device="cuda").to(torch.bfloat16)
+    ep = EPMoELayer(pl, d, F, K, LocalComm(G), range(G), seed=9, gate_bias=bias, train=True, exchange="p2p")
+    outs = ep.forward([x[r * T:(r + 1) * T].contiguous() for r in range(G)])
+    grads = ep.backward([dout[r * T:(r + 1) * T].contiguous() for r in range(G)])
+    for r in range(world):
+        assert not isinstance(res[r], str), res[r]
+        want = [outs[r]] + list(grads[r])
+        for got, ref in zip(res[r], want):
+            assert np.array_equal(got, ref.float().cpu().numpy()), r
