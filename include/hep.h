@@ -164,6 +164,23 @@ int hep_sched_pipelined(hep_sched_t h, const int64_t *d_loads, int64_t stride_e,
                         const hep_sched_out *latter, void *stream, void *stream_static);
 /* Diagnostics: per-phase SM clock stamps of the last HEP_SCHED_PROFILE launch (n <= 16). */
 int hep_sched_debug_timing(int64_t *host_out, int n);
+/* Dense two-phase primal simplex with Bland's rule on one thread-block cluster (csrc/lp.cu).
+ * Replaces simplex_solve (simplex.py:99-192), the solver of solve_comm_aware
+ * (scheduler.py:622-689) on the _comm_aware_lp (:480-547) / _topology_aware_lp (:550-619)
+ * programs:  min c.x  s.t.  a_eq x = b_eq,  a_ub x <= b_ub,  x >= 0.  All matrices dense
+ * row-major fp64 in device memory (a_eq [m_eq][n], a_ub [m_ub][n]).  d_basis_in: the
+ * previous optimal basis [m_eq+m_ub] (warm start, simplex.py:127-144) or NULL.  Outputs:
+ * d_x_full [n+m_ub] (structural values first; the caller clips [:n] at 0), d_basis_out
+ * [m_eq+m_ub], d_info [8] = {pivots, status (0 ok, 1 infeasible, 2 unbounded, 3 pivot
+ * limit), warm start used, artificials, phase-1 pivots, phase-2 pivots}.  A cold solve
+ * is bit-identical to the reference (same pivots, same fp64 roundings).  d_work: caller-
+ * owned, hep_lp_workspace() bytes.  Asynchronous on `stream`. */
+size_t hep_lp_workspace(int64_t n, int64_t m_eq, int64_t m_ub);
+int hep_lp_solve(const double *d_c, const double *d_a_eq, const double *d_b_eq, const double *d_a_ub,
+                 const double *d_b_ub, int64_t n, int64_t m_eq, int64_t m_ub, const int64_t *d_basis_in,
+                 double tol, int64_t max_iter, void *d_work, size_t work_bytes, double *d_x_full,
+                 int64_t *d_basis_out, int64_t *d_info, void *stream);
+
 /* Aggregate an arbitrary routing table. Replaces build_transfer_plan (router.py:178-226). */
 int hep_transfer_plan(int num_gpus, int gpus_per_node, const int64_t *d_ranges, int64_t n_ranges,
                       int64_t *d_transfer, int32_t *d_status, void *stream);

@@ -58,6 +58,7 @@ from .scheduler import (
     BALANCE_ONLY,
     COMM_AWARE,
     TOPOLOGY_AWARE,
+    CommPlanStats,
     SolveOptions,
     SolverState,
     SolveStats,
@@ -66,6 +67,7 @@ from .scheduler import (
     solve_replica_loads,
     warm_solve,
 )
+from .simplex import LinearProgram, SimplexError, SimplexResult, simplex_solve
 from .workload import Workload, gen_zipf_workload, load_trace, save_trace, zipf_gate_bias
 from .sweep import STRATEGIES, CostModel, MicrobatchMetrics, RunResult, SweepResult, run_skew_sweep, run_strategy
 from .layer import MoELayer

@@ -60,6 +60,8 @@ SIGNATURES = {
     "hep_sched_pipelined": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp, ctypes.POINTER(HepSchedOut), ctypes.POINTER(HepSchedOut), vp, vp]),
     "hep_sched_route": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int64, vp, ctypes.c_int, ctypes.POINTER(HepSchedOut), vp]),
     "hep_sched_debug_timing": (ctypes.c_int, [c_i64p, ctypes.c_int]),
+    "hep_lp_workspace": (ctypes.c_size_t, [ctypes.c_int64, ctypes.c_int64, ctypes.c_int64]),
+    "hep_lp_solve": (ctypes.c_int, [vp, vp, vp, vp, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, vp, ctypes.c_double, ctypes.c_int64, vp, ctypes.c_size_t, vp, vp, vp, vp]),
     "hep_transfer_plan": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, vp, ctypes.c_int64, vp, vp, vp]),
     "hep_gate_topk": (ctypes.c_int, [vp, ctypes.c_int64, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int, vp, vp, vp, vp]),
     "hep_gemm_bf16": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp]),

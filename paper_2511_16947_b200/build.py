@@ -19,7 +19,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libhep.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["capi.cu", "sched.cu", "gate.cu", "gemm_sm100.cu", "dispatch.cu", "p2p.cu"]
+SOURCES = ["capi.cu", "sched.cu", "gate.cu", "gemm_sm100.cu", "dispatch.cu", "p2p.cu", "lp.cu"]
 HEADERS = ["common.cuh", "sm100.cuh", os.path.join("..", "..", "include", "hep.h")]
 
 NVCC_FLAGS = [

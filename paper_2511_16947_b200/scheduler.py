@@ -3,7 +3,9 @@
 Same public surface as the reference ``harmonyep.scheduler``
 (``/root/reference/pkg/src/harmonyep/scheduler.py``):
 
-  SolveOptions          :67-94    (balance mode; comm-aware modes are out of scope)
+  SolveOptions          :67-94
+  CommPlanStats         :97-135
+  solve_comm_aware      :622-689  (LP on the device: simplex.py / csrc/lp.cu)
   SolveStats            :138-148
   SolverState           :151-170  (here: owns the device placement tables + output buffers)
   solve_replica_loads   :405-433
@@ -38,6 +40,7 @@ from .core import (
     DimensionError,
     LoadMatrix,
     Placement,
+    PlacementError,
     ReplicaLoadPlan,
     StaleStateError,
     Topology,
@@ -284,6 +287,7 @@ class SolverState:
         self.stats = SolveStats()
         self.last_objective = None
         self._dev: DeviceScheduler | None = None
+        self._basis = None  # device simplex basis of the comm-aware modes (warm start)
 
     def _check_loads(self, loads: LoadMatrix) -> None:
         if (loads.num_experts, loads.num_gpus) != (self.placement.num_experts, self.placement.num_gpus):
@@ -359,7 +363,11 @@ def warm_solve(prev_state: SolverState, new_loads: LoadMatrix, *,
         raise StaleStateError("warm state is not a SolverState")
     prev_state._check_loads(new_loads)
     if prev_state.options.mode != BALANCE_ONLY:
-        raise ContractViolation("communication-aware warm solves are out of scope (DESIGN.md §scope)")
+        if prev_state.topology is None:
+            raise StaleStateError("comm-mode state lost its topology")
+        plan, _stats, state = solve_comm_aware(prev_state.placement, new_loads, prev_state.topology,
+                                               prev_state.options, _state=prev_state)
+        return plan, state
     plan = _device_solve(prev_state, new_loads, gpu_base)
     return plan, prev_state
 
@@ -404,7 +412,191 @@ def integerize_plan(plan: ReplicaLoadPlan) -> ReplicaLoadPlan:
                            objective=objective)
 
 
-def solve_comm_aware(*_args, **_kwargs):
-    """Communication-aware LP modes (reference scheduler.py:480-689) are outside
-    the scoped hot path; see DESIGN.md."""
-    raise NotImplementedError("comm-aware / topology-aware LP modes are not part of the B200 hot path")
+@dataclass(frozen=True)
+class CommPlanStats:
+    """Per-GPU all-to-all volumes implied by a plan (reference scheduler.py:97-135):
+    ``local[g]`` = tokens kept on their source GPU, ``send[g]`` = tokens leaving g
+    (including tokens of experts g does not host), ``recv[g]`` = tokens arriving,
+    ``comp`` = max GPU load, ``comm`` = max over GPUs of max(send, recv)."""
+
+    send: tuple
+    recv: tuple
+    local: tuple
+    comp: object
+    comm: object
+
+    @classmethod
+    def from_plan(cls, placement: Placement, loads: LoadMatrix, plan: ReplicaLoadPlan) -> "CommPlanStats":
+        G = placement.num_gpus
+        inp = loads.entries
+        local = [0] * G
+        recv = [0] * G
+        gpu = [0] * G
+        for e, grp in enumerate(placement.edp_groups):
+            for g, x in zip(grp, plan.entries[e]):
+                kept = min(x, inp[e][g])
+                local[g] += kept
+                recv[g] += x - kept
+                gpu[g] += x
+        send = [sum(inp[e][g] for e in range(loads.num_experts)) - local[g] for g in range(G)]
+        comp = max(gpu) if gpu else 0
+        comm = max((max(a, b) for a, b in zip(send, recv)), default=0)
+        return cls(tuple(send), tuple(recv), tuple(local), comp, comm)
+
+
+def _comm_aware_lp(placement: Placement, loads: LoadMatrix, alpha: float):
+    """min comp + alpha*comm over replica loads x and kept-local volumes l
+    (reference scheduler.py:480-547; same variable and row order, so the device
+    simplex walks the same pivots).  Columns: x[arcs] | l[arcs] | comp | comm, arcs =
+    (expert, GPU) in EDP-list order.  Rows: per-expert conservation (eq); then
+    comp >= load(g); l <= x and l <= input per arc; send(g) <= comm, recv(g) <= comm."""
+    from .simplex import LinearProgram
+
+    E, G = placement.num_experts, placement.num_gpus
+    ae = np.array([e for e, grp in enumerate(placement.edp_groups) for _ in grp], dtype=np.int64)
+    ag = np.array([g for grp in placement.edp_groups for g in grp], dtype=np.int64)
+    na = ae.size
+    n = 2 * na + 2
+    i_comp, i_comm = 2 * na, 2 * na + 1
+    inp = loads.as_array().astype(np.float64)  # [E][G]
+    arange = np.arange(na)
+    c = np.zeros(n)
+    c[i_comp], c[i_comm] = 1.0, alpha
+    a_eq = np.zeros((E, n))
+    a_eq[ae, arange] = 1.0
+    b_eq = np.asarray(loads.expert_totals(), dtype=np.float64)
+    # inequality rows: [G comp] [2 per arc] [2 per GPU: send, recv]
+    m_ub = G + 2 * na + 2 * G
+    a_ub = np.zeros((m_ub, n))
+    b_ub = np.zeros(m_ub)
+    a_ub[ag, arange] = 1.0
+    a_ub[:G, i_comp] = -1.0
+    r_lx = G + 2 * arange  # l - x <= 0
+    a_ub[r_lx, na + arange] = 1.0
+    a_ub[r_lx, arange] = -1.0
+    r_li = r_lx + 1  # l <= input
+    a_ub[r_li, na + arange] = 1.0
+    b_ub[r_li] = inp[ae, ag]
+    r_send = G + 2 * na + 2 * np.arange(G)
+    r_recv = r_send + 1
+    a_ub[r_send[ag], na + arange] = -1.0
+    a_ub[r_recv[ag], arange] = 1.0
+    a_ub[r_recv[ag], na + arange] = -1.0
+    a_ub[r_send, i_comm] = -1.0
+    a_ub[r_recv, i_comm] = -1.0
+    b_ub[r_send] = -inp.sum(axis=0)
+    arcs = list(zip(ae.tolist(), ag.tolist()))
+    return LinearProgram(c=c, a_eq=a_eq, b_eq=b_eq, a_ub=a_ub, b_ub=b_ub), arcs
+
+
+def _topology_aware_lp(placement: Placement, loads: LoadMatrix, topology: Topology, alpha_intra: float,
+                       alpha_inter: float):
+    """min comp + a1*comm_intra + a2*comm_inter over explicit token flows
+    f[(e, src, dst)] (reference scheduler.py:550-619; same column and row order).
+    Columns: flows (expert, source GPU, replica GPU in EDP-list order) | comp | ci | cx.
+    Rows: per-(expert, source) conservation for experts with replicas (eq); then
+    comp >= load(dst); then per GPU the non-empty rows of intra send / intra recv /
+    inter send / inter recv <= ci / ci / cx / cx."""
+    from .simplex import LinearProgram
+
+    G = placement.num_gpus
+    fe, fs, fd = [], [], []
+    for e, grp in enumerate(placement.edp_groups):
+        for src in range(G):
+            for dst in grp:
+                fe.append(e)
+                fs.append(src)
+                fd.append(dst)
+    fe, fs, fd = (np.array(v, dtype=np.int64) for v in (fe, fs, fd))
+    nf = fe.size
+    n = nf + 3
+    i_comp, i_ci, i_cx = nf, nf + 1, nf + 2
+    c = np.zeros(n)
+    c[i_comp], c[i_ci], c[i_cx] = 1.0, alpha_intra, alpha_inter
+    hosted = [e for e, grp in enumerate(placement.edp_groups) if grp]
+    eq_row = {e: i for i, e in enumerate(hosted)}  # row of (e, src) = eq_row[e] * G + src
+    inp = loads.as_array().astype(np.float64)
+    a_eq = np.zeros((len(hosted) * G, n))
+    fidx = np.arange(nf)
+    if nf:
+        rows = np.array([eq_row[e] for e in fe.tolist()], dtype=np.int64) * G + fs
+        a_eq[rows, fidx] = 1.0
+    b_eq = inp[np.repeat(np.array(hosted, dtype=np.int64), G), np.tile(np.arange(G), len(hosted))] \
+        if hosted else np.zeros(0)
+    node = np.array([topology.node_of(g) for g in range(G)], dtype=np.int64)
+    comp = np.zeros((G, n))
+    comp[fd, fidx] = 1.0
+    comp[:, i_comp] = -1.0
+    cross = fs != fd
+    same = node[fs] == node[fd]
+    si, ri, sx, rx = (np.zeros((G, n)) for _ in range(4))
+    m_i = cross & same
+    m_x = cross & ~same
+    si[fs[m_i], fidx[m_i]] = 1.0
+    ri[fd[m_i], fidx[m_i]] = 1.0
+    sx[fs[m_x], fidx[m_x]] = 1.0
+    rx[fd[m_x], fidx[m_x]] = 1.0
+    ub = [comp[g] for g in range(G)]
+    for g in range(G):
+        for mat, iv in ((si, i_ci), (ri, i_ci), (sx, i_cx), (rx, i_cx)):
+            row = mat[g]
+            if row.any():
+                row[iv] = -1.0
+                ub.append(row)
+    a_ub = np.array(ub)
+    b_ub = np.zeros(len(ub))
+    flows = list(zip(fe.tolist(), fs.tolist(), fd.tolist()))
+    return LinearProgram(c=c, a_eq=a_eq, b_eq=b_eq, a_ub=a_ub, b_ub=b_ub), flows
+
+
+def solve_comm_aware(placement: Placement, loads: LoadMatrix, topology: Topology, options: SolveOptions, *,
+                     _state: SolverState | None = None):
+    """Minimise comp + alpha*comm (``comm_aware``) or comp + alpha_intra*intra +
+    alpha_inter*inter (``topology_aware``) -- reference scheduler.py:622-689.  The LP is
+    built on the host and solved by the device simplex (``simplex.simplex_solve`` ->
+    ``hep_lp_solve``), warm-started from the state's previous basis.  Returns
+    (float plan, CommPlanStats recomputed from the plan, state)."""
+    from .simplex import simplex_solve
+
+    if options.mode not in (COMM_AWARE, TOPOLOGY_AWARE):
+        raise ContractViolation(
+            f"solve_comm_aware requires mode in {{{COMM_AWARE}, {TOPOLOGY_AWARE}}}, got {options.mode!r}")
+    if _state is None and options.warm_state is not None:
+        _state = options.warm_state
+    _check_dims(placement, loads)
+    if topology.num_gpus != placement.num_gpus:
+        raise DimensionError("topology does not match placement")
+    for e, (load, grp) in enumerate(zip(loads.expert_totals(), placement.edp_groups)):
+        if load > 0 and not grp:
+            raise PlacementError(f"expert {e} has load {load} but an empty EDP group")
+    state = _state or SolverState(placement, options, topology)
+    state._check_loads(loads)
+    if options.mode == COMM_AWARE:
+        lp, keys = _comm_aware_lp(placement, loads, options.alpha)
+    else:
+        lp, keys = _topology_aware_lp(placement, loads, topology, options.alpha_intra, options.alpha_inter)
+    res = simplex_solve(lp, basis=state._basis)
+    state._basis = res.basis
+    state.stats.pivots += res.iterations
+    state.stats.iterations_last = res.iterations
+    state.stats.solves += 1
+    state.stats.device_us_last = res.device_us
+    state.stats.device_us_total += res.device_us
+    E, G = placement.num_experts, placement.num_gpus
+    x = [[0.0] * G for _ in range(E)]
+    if options.mode == COMM_AWARE:
+        for k, (e, g) in enumerate(keys):
+            x[e][g] = float(res.x[k])
+    else:
+        for k, (e, _src, dst) in enumerate(keys):
+            x[e][dst] += float(res.x[k])  # flow order, as the reference accumulates
+    entries = tuple(tuple(x[e][g] for g in grp) for e, grp in enumerate(placement.edp_groups))
+    loads_g = [0.0] * G
+    for e, grp in enumerate(placement.edp_groups):
+        for g, v in zip(grp, entries[e]):
+            loads_g[g] += v
+    plan = ReplicaLoadPlan(num_gpus=G, groups=placement.edp_groups, entries=entries,
+                           objective=max(loads_g) if loads_g else 0.0)
+    stats = CommPlanStats.from_plan(placement, loads, plan)
+    state.last_objective = res.objective
+    return plan, stats, state

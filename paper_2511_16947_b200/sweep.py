@@ -29,12 +29,25 @@ from .core import (
     ConfigError,
     ContractViolation,
     Placement,
+    Topology,
     aggregate_expert_loads,
     gpu_load_balance_ratio,
 )
 from .placement import identical_placement
 from .router import RoutingTable, TransferPlan
-from .scheduler import HEP_SCHED_ALL, HEP_SCHED_ROUTE, HEP_SCHED_TRANSFER, DeviceScheduler
+from .scheduler import (
+    COMM_AWARE,
+    HEP_SCHED_ALL,
+    HEP_SCHED_ROUTE,
+    HEP_SCHED_TOPO,
+    HEP_SCHED_TRANSFER,
+    TOPOLOGY_AWARE,
+    DeviceScheduler,
+    SolveOptions,
+    integerize_plan,
+    solve_comm_aware,
+    warm_solve,
+)
 from .workload import Workload, gen_zipf_workload
 
 STRATEGIES = ("vanilla_ep", "merged_ep", "harmony", "harmony_comm_aware", "harmony_pipelined")
@@ -140,6 +153,40 @@ class _Runner:
         gl = tuple(bufs.gpu_load.cpu().tolist()) if gpu_loads is None else tuple(gpu_loads)
         return _Phase(bufs.host_ranges(), tp, gl)
 
+    def run_comm_aware(self, placement: Placement, loads, cost: "CostModel", state):
+        """``harmony_comm_aware`` (simulator.py:406-419): the device simplex solves
+        comp + alpha*comm (topology-aware when the shape has several nodes), cold on the
+        first micro-batch of a placement and warm from the previous basis after; the
+        integerized plan is routed topology-aware on the device.  Returns (phases,
+        device µs = LP solve + routing, state)."""
+        t = self.torch
+        G = self.shape.num_gpus
+        topology = Topology.from_shape(self.shape)
+        if state is None:
+            mode = TOPOLOGY_AWARE if topology.num_nodes > 1 else COMM_AWARE
+            opts = SolveOptions(mode=mode, alpha=cost.alpha_inter, alpha_intra=cost.alpha_intra,
+                                alpha_inter=cost.alpha_inter)
+            plan, _stats, state = solve_comm_aware(placement, loads, topology, opts)
+        else:
+            plan, state = warm_solve(state, loads)
+        lp_us = state.stats.device_us_last
+        ip = integerize_plan(plan)
+        self.loads.copy_(t.as_tensor(np.asarray(loads.as_array(), dtype=np.int64)))
+        ds = self.ds(placement)
+        flat = [v for row in ip.entries for v in row]
+        d_xi = t.tensor(flat or [0], dtype=t.int64, device=self.device)
+        s0, s1 = self.ev
+        s0.record()
+        ds.launch_route(self.loads, G, 1, d_xi, HEP_SCHED_ROUTE | HEP_SCHED_TRANSFER | HEP_SCHED_TOPO)
+        s1.record()
+        t.cuda.synchronize(self.device)
+        ds.check_status("harmony_comm_aware")
+        gl = [0] * G
+        for group, row in zip(placement.edp_groups, ip.entries):
+            for g, v in zip(group, row):
+                gl[g] += v
+        return [self.phase_of(ds, ds, gl)], lp_us + 1e3 * s0.elapsed_time(s1), state
+
     def run_mb(self, strategy: str, placement: Placement, loads, static_share: Fraction):
         t = self.torch
         G = self.shape.num_gpus
@@ -185,8 +232,6 @@ def run_strategy(workload: Workload, strategy: str, placement: Placement | None,
     """Reference ``run_strategy`` (simulator.py:346-483) on the device scheduler."""
     if strategy not in STRATEGIES:
         raise ConfigError([f"unknown strategy {strategy!r}; expected one of {STRATEGIES}"])
-    if strategy == "harmony_comm_aware":
-        raise NotImplementedError("harmony_comm_aware (float simplex LP) is outside the device hot path")
     shape = workload.shape
     if strategy in ("vanilla_ep", "merged_ep"):
         placement = placement if placement is not None else identical_placement(shape)
@@ -206,6 +251,7 @@ def run_strategy(workload: Workload, strategy: str, placement: Placement | None,
     current = placement
     schedules = strategy != "vanilla_ep"
     static_share = Fraction(1) - Fraction(cost.pipeline_ratio)
+    comm_state = None  # warm-start state of harmony_comm_aware, reset on replacement
     for i, loads in enumerate(workload.micro_batches):
         migration = 0.0
         if (policy is not None and schedules and strategy != "merged_ep" and i > 0
@@ -213,9 +259,13 @@ def run_strategy(workload: Workload, strategy: str, placement: Placement | None,
             decision = evaluate_and_maybe_replace(current, history, policy, shape, seed)
             if decision.replaced:
                 current = decision.placement
+                comm_state = None
                 migration = decision.migration_cost_total
                 events.append(decision.to_event(i))
-        phases, us = runner.run_mb(strategy, current, loads, static_share)
+        if strategy == "harmony_comm_aware":
+            phases, us, comm_state = runner.run_comm_aware(current, loads, cost, comm_state)
+        else:
+            phases, us = runner.run_mb(strategy, current, loads, static_share)
         sched_us.append(us)
         if schedules:
             lp_solves += 1
