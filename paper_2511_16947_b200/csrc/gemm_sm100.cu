@@ -47,7 +47,7 @@ constexpr int kGateMaxE = 256;
 // [n_src][E] histogram, [3][E] chunk counters of a tile (a tile of <= 128 rows touches at
 // most 3 aligned 64-token chunks), [E] bias, and the column-half merge buffers
 // (128 rows x KG x (key, expert, logit))
-constexpr int kGateSmemBytes = 4 * (kGateMaxSrc * kGateMaxE + 4 * kGateMaxE) + 128 * kGateMaxK * 12;
+constexpr int kGateSmemBytes = 4 * (kGateMaxSrc * kGateMaxE + 4 * kGateMaxE) + 128 * (kGateMaxK * 12 + 16);
 struct GateParams {
     const float *bias;   // [E] selection bias or null
     int K, E;            // top-K, experts (columns >= E are padding)
@@ -406,17 +406,22 @@ __device__ __forceinline__ uint32_t order_key(float f) {
 
 // EPI_GATE epilogue of one accumulator tile (<= 128 tokens), run by all 8 epilogue
 // warps: warp pair (q, q+4) shares TMEM lane quarter q; with E_pad % 32 == 0 the two
-// warps scan one column half each and half 1 hands its top-KG list to half 0 through
-// shared memory (nhalf = 2), else half 0 scans every column (nhalf = 1).  Named
-// barrier 1 spans the 128 * nhalf participating threads.
+// warps scan one column half each (nhalf = 2), else half 0 scans every column (nhalf =
+// 1).  Named barrier 1 spans the 128 * nhalf participating threads.
 // Selection and weights are exactly hep_gate_topk's (gate.cu): top-K of the order key
-// of (logit + bias) with ties to the lower expert id (strict '>' while scanning experts
-// in ascending order keeps the earlier one; half 1's entries, all of higher expert id,
-// are inserted after half 0's scan in their own order, so the merged list is the
-// sequential scan's), softmax over the K selected logits in pick order.  The running
-// top-KG list is a branch-free insertion network: every slot's new value depends only
-// on the previous column's list, so the KG compare/selects of one column issue back to
-// back.  Histogram counts go to shared memory (flushed once per CTA); the per-64-token
+// of (logit + bias) with ties to the lower expert id, softmax over the K selected
+// logits in pick order (key descending, ties by expert id).  Two passes over the
+// thread's row, so the per-column work is a handful of instructions:
+//   1. the K largest KEYS (a multiset: ties kept) by a min/max network -- slot j takes
+//      min(slot j-1, max(key, slot j)), 2 IMNMX per slot, no expert/logit tracking;
+//      half 1 hands its K keys to half 0, which merges them and fixes the threshold
+//      vK = the K-th key and how many vK-keyed experts each half contributes (the lower
+//      expert ids -- half 0's -- first);
+//   2. a rescan selects exactly those experts (key > vK, or key == vK within the
+//      half's quota) in ascending expert order into a shared K-entry list; half 0 then
+//      orders the K entries with the strict insertion network (the same list a full
+//      sequential scan keeps) and computes the weights.
+// Histogram counts go to shared memory (flushed once per CTA); the per-64-token
 // chunk counts (chunks aligned to 64 tokens) are stored directly when the tile is made
 // of whole chunks, else added with integer atomics into the zeroed global counts.
 template <int KG>
@@ -432,12 +437,25 @@ __device__ __forceinline__ void gate_insert(uint32_t key, int e, float l, uint32
     }
 }
 
+// top-KG key multiset, sorted descending: tk[j] <- min(tk[j-1], max(key, tk[j]))
+template <int KG>
+__device__ __forceinline__ void key_insert(uint32_t key, uint32_t (&tk)[KG]) {
+#pragma unroll
+    for (int j = KG - 1; j > 0; --j) tk[j] = min(tk[j - 1], max(key, tk[j]));
+    tk[0] = max(key, tk[0]);
+}
+
 __device__ __forceinline__ void gate_bar(int nthr) { asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory"); }
 
-template <int KG>
+template <int KG, int SPAN>
 __device__ __forceinline__ void gate_tile(const Params &p, uint32_t t_row, int64_t row0, int rows, int row_in_tile,
                                           int half, int nhalf, int32_t *s_hist, int32_t *s_chunk,
-                                          const float *s_bias, uint8_t *s_merge, int E_pad) {
+                                          const float *s_bias, uint8_t *s_merge) {
+    // SPAN = columns per thread (E_pad / nhalf); TMEM is read CW columns per wait (64
+    // columns per wait -- four loads in flight -- measured slower: Qwen3 45.3 -> 53.7 µs)
+    constexpr int CW = 16;
+    constexpr int NJ = CW / 16;
+    static_assert(SPAN % CW == 0 && CW % 16 == 0, "gate column span");
     const GateParams &g = p.gate;
     const int E = g.E;
     const int nthr = 128 * nhalf;
@@ -452,57 +470,128 @@ __device__ __forceinline__ void gate_tile(const Params &p, uint32_t t_row, int64
     }
     const bool valid = row_in_tile < rows;
     const int64_t t = row0 + row_in_tile;
+    // shared buffers: half 1's keys [128][KG] | (vK, quota, offset) [128][4] | list e / logit [128][KG]
+    uint32_t *mk = reinterpret_cast<uint32_t *>(s_merge) + row_in_tile * KG;
+    int32_t *bc = reinterpret_cast<int32_t *>(s_merge + 128 * KG * 4) + row_in_tile * 4;
+    int32_t *le = reinterpret_cast<int32_t *>(s_merge + 128 * KG * 4 + 128 * 16) + row_in_tile * KG;
+    float *lv = reinterpret_cast<float *>(s_merge + 128 * KG * 8 + 128 * 16) + row_in_tile * KG;
+    const int c_lo = half * SPAN;
+    const int c_hi = c_lo + SPAN;
+    // ---- pass 1: logits out, top-KG keys -------------------------------------------
     uint32_t tk[KG];
-    int te[KG];
-    float tv[KG];
 #pragma unroll
-    for (int i = 0; i < KG; ++i) {
-        tk[i] = 0u;
-        te[i] = 0;
-        tv[i] = 0.f;
-    }
-    const int c_lo = nhalf == 2 ? half * (E_pad / 2) : 0;
-    const int c_hi = nhalf == 2 ? c_lo + E_pad / 2 : E_pad;
+    for (int i = 0; i < KG; ++i) tk[i] = 0u;
     float *lrow = (valid && p.out) ? reinterpret_cast<float *>(p.out) + t * p.ld_out : nullptr;
 #pragma unroll 1
-    for (int c = c_lo; c < c_hi; c += 16) {
-        uint32_t v[16];
-        tmem_ld16(t_row + c, v);
+    for (int c = c_lo; c < c_hi; c += CW) {
+        uint32_t v[NJ][16];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) tmem_ld16(t_row + c + 16 * j, v[j]);
         tmem_ld_wait();
-        if (lrow && c < p.out_cols) {  // logits buffer is [T][e_pad]; BN may be wider
-            float4 *dst = reinterpret_cast<float4 *>(lrow + c);
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-                dst[i] = make_float4(__uint_as_float(v[4 * i]), __uint_as_float(v[4 * i + 1]),
-                                     __uint_as_float(v[4 * i + 2]), __uint_as_float(v[4 * i + 3]));
-        }
+        for (int j = 0; j < NJ; ++j) {
+            const int cj = c + 16 * j;
+            if (lrow && cj < p.out_cols) {  // logits buffer is [T][e_pad]; BN may be wider
+                float4 *dst = reinterpret_cast<float4 *>(lrow + cj);
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const int e = c + i;
-            const float l = __uint_as_float(v[i]);
-            // padding columns get key 0, which never enters (strict '>' against >= 0)
-            const uint32_t key = e < E ? order_key(l + s_bias[e]) : 0u;
-            gate_insert<KG>(key, e, l, tk, te, tv);
+                for (int i = 0; i < 4; ++i)
+                    dst[i] = make_float4(__uint_as_float(v[j][4 * i]), __uint_as_float(v[j][4 * i + 1]),
+                                         __uint_as_float(v[j][4 * i + 2]), __uint_as_float(v[j][4 * i + 3]));
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const int e = cj + i;
+                // padding columns get key 0, below every real score
+                const uint32_t key = e < E ? order_key(__uint_as_float(v[j][i]) + s_bias[e]) : 0u;
+                key_insert<KG>(key, tk);
+            }
         }
     }
-    if (nhalf == 2) {  // half 1 -> half 0 through shared memory, then half 0 inserts
-        uint32_t *mk = reinterpret_cast<uint32_t *>(s_merge) + row_in_tile * KG;
-        int32_t *me = reinterpret_cast<int32_t *>(s_merge + 128 * KG * 4) + row_in_tile * KG;
-        float *mv = reinterpret_cast<float *>(s_merge + 128 * KG * 8) + row_in_tile * KG;
+    // ---- threshold and per-half quotas ------------------------------------------------
+    uint32_t vK;
+    int quota, offset;
+    if (nhalf == 2) {
         if (half == 1)
 #pragma unroll
-            for (int k = 0; k < KG; ++k) {
-                mk[k] = tk[k];
-                me[k] = te[k];
-                mv[k] = tv[k];
-            }
+            for (int k = 0; k < KG; ++k) mk[k] = tk[k];
         gate_bar(nthr);
-        if (half == 0)
+        if (half == 0) {
+            uint32_t tm[KG];
 #pragma unroll
-            for (int k = 0; k < KG; ++k) gate_insert<KG>(mk[k], me[k], mv[k], tk, te, tv);
-        gate_bar(nthr);  // the merge buffer is free for the next tile
+            for (int k = 0; k < KG; ++k) tm[k] = tk[k];
+#pragma unroll
+            for (int k = 0; k < KG; ++k) key_insert<KG>(mk[k], tm);
+            vK = tm[KG - 1];
+            int need = 0, gt0 = 0, c0h = 0;
+#pragma unroll
+            for (int k = 0; k < KG; ++k) {
+                need += tm[k] == vK;
+                gt0 += tk[k] > vK;
+                c0h += tk[k] == vK;
+            }
+            quota = c0h < need ? c0h : need;  // the lower expert ids take the ties first
+            offset = 0;
+            bc[0] = (int32_t)vK;
+            bc[1] = need - quota;
+            bc[2] = gt0 + quota;
+        }
+        gate_bar(nthr);
+        if (half == 1) {
+            vK = (uint32_t)bc[0];
+            quota = bc[1];
+            offset = bc[2];
+        }
+    } else {
+        vK = tk[KG - 1];
+        quota = 0;
+#pragma unroll
+        for (int k = 0; k < KG; ++k) quota += tk[k] == vK;
+        offset = 0;
     }
+    // ---- pass 2: the selected experts, ascending, into the shared list -----------------
+    int cnt = offset;
+#pragma unroll 1
+    for (int c = c_lo; c < c_hi; c += CW) {
+        uint32_t v[NJ][16];
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) tmem_ld16(t_row + c + 16 * j, v[j]);
+        tmem_ld_wait();
+        if (valid) {
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    const int e = c + 16 * j + i;
+                    const float l = __uint_as_float(v[j][i]);
+                    const uint32_t key = e < E ? order_key(l + s_bias[e]) : 0u;
+                    const bool tie = key == vK && quota > 0;
+                    if (e < E && (key > vK || tie)) {
+                        le[cnt] = e;
+                        lv[cnt] = l;
+                        ++cnt;
+                        quota -= tie;
+                    }
+                }
+            }
+        }
+    }
+    if (nhalf == 2) gate_bar(nthr);  // half 1's entries are in the list
     if (half == 0 && valid) {
+        uint32_t tkf[KG];
+        int te[KG];
+        float tv[KG];
+#pragma unroll
+        for (int k = 0; k < KG; ++k) {
+            tkf[k] = 0u;
+            te[k] = 0;
+            tv[k] = 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < KG; ++k) {
+            const int e = le[k];
+            const float l = lv[k];
+            gate_insert<KG>(order_key(l + s_bias[e]), e, l, tkf, te, tv);
+        }
         float mx = tv[0];
 #pragma unroll
         for (int k = 1; k < KG; ++k) mx = fmaxf(mx, tv[k]);
@@ -523,6 +612,7 @@ __device__ __forceinline__ void gate_tile(const Params &p, uint32_t t_row, int64
             if (g.chunk_cnt) atomicAdd(&s_chunk[ch * E + te[k]], 1);
         }
     }
+    if (nhalf == 2) gate_bar(nthr);  // the merge buffers are free for the next tile
     if (g.chunk_cnt) {
         gate_bar(nthr);
         // chunk j of the tile is global chunk c0 + j = (src * ncs + c) in the [n_src][ncs][E]
@@ -727,11 +817,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 constexpr int NH = (BN % 32 == 0 && kEpiSplit == 2) ? 2 : 1;
                 if (half < NH) {
 #define HEP_GATE_K(KK) \
-    case KK: gate_tile<KK>(p, t_row, tl.row0, tl.rows, row_in_tile, half, NH, s_hist, s_chunk, s_bias, s_merge, BN); break;
+    case KK: gate_tile<KK, BN / NH>(p, t_row, tl.row0, tl.rows, row_in_tile, half, NH, s_hist, s_chunk, s_bias, s_merge); break;
                     switch (p.gate.K) {  // the insertion network is unrolled per K
                         HEP_GATE_K(1) HEP_GATE_K(2) HEP_GATE_K(3) HEP_GATE_K(4)
                         HEP_GATE_K(5) HEP_GATE_K(6) HEP_GATE_K(7)
-                        default: gate_tile<8>(p, t_row, tl.row0, tl.rows, row_in_tile, half, NH, s_hist, s_chunk, s_bias, s_merge, BN); break;
+                        default: gate_tile<8, BN / NH>(p, t_row, tl.row0, tl.rows, row_in_tile, half, NH, s_hist, s_chunk, s_bias, s_merge); break;
                     }
 #undef HEP_GATE_K
                 }
