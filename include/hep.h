@@ -63,7 +63,9 @@ typedef struct {
     int lsu256;             /* 1: 256-bit LDG/STG permute / combine when 32-B aligned */
     int ffn_clock;          /* 1: diagnostics, CTA 0 of each expert GEMM stamps clock64/globaltimer */
     int router_tile_rows;   /* router GEMM rows per CTA tile, multiple of 16 (0 = 128; shorter tiles measured slower) */
-    int reserved[7];
+    int pair_wave_sync;     /* > 0: grouped CTA-pair GEMMs with >= this many 64-deep k-blocks per tile start
+                               each wave of tiles together (TMA producers meet at a grid-wide counter) */
+    int reserved[6];
 } hep_tuning;
 int hep_tuning_get(hep_tuning *out);
 int hep_tuning_set(const hep_tuning *in);

@@ -100,6 +100,7 @@ struct Params {
     int wait_cluster;
     int st256;  // epilogue rows 32-B aligned: one 256-bit store per 16 bf16 / 8 fp32 columns (full L2 sectors)
     int clk_slot;
+    unsigned int *wave_ctr;  // pair kernel: producers' wave counter (zeroed before the launch) or null
     int a_box_rows;  // mode 0, K-major A: rows per A TMA box (= tile_m when < 128; 0 = BM)  // > 0: CTA 0 stamps (clock64, globaltimer) at entry and exit into g_gemm_clk[clk_slot - 1]
 };
 
@@ -973,7 +974,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             const uint32_t full_l = mapa_shared(smem_u32(&full[0]), 0);  // leader's full[0]
             int stage = 0;
             uint32_t phase = 0;
+            int64_t wave_target = 0;
             for (int64_t t = cid; t < n_total; t += ncl) {
+                if (p.wave_ctr && t >= ncl) {
+                    // every producer of the grid starts wave w = t / ncl together: arrive once
+                    // per wave, wait for the arrivals of every CTA that has a tile in it
+                    const int64_t w = t / ncl;
+                    const int64_t in_wave = n_total - w * ncl < ncl ? n_total - w * ncl : ncl;
+                    wave_target += 2 * in_wave;
+                    atomicAdd(p.wave_ctr, 1u);
+                    while ((int64_t)ld_acquire_gpu_u32(p.wave_ctr) < wave_target) __nanosleep(64);
+                }
                 const Tile tl = decode(p, t, s_off);
                 const int32_t a_row = tl.row0 + (int32_t)rank * 128;
                 const int32_t b_row = (int32_t)(tl.expert * p.b_rows_per_exp + (int64_t)tl.n_blk * BN) + (int32_t)rank * 128;
@@ -1313,11 +1324,21 @@ static int launch(const void *A, int64_t a_rows, int64_t K, const void *B, int64
     return launch_maps<BN, STAGES, EPI, false, false>(ta, tb, p, max_tiles, stream);
 }
 
+__device__ unsigned int g_wave_ctr;
+
 template <int STAGES, int EPI, bool A_MN, bool B_MN>
 static int launch2sm_maps(const CUtensorMap &ta, const CUtensorMap &tb, const Params &p0, cudaStream_t stream) {
     using S = Smem2<STAGES>;
     Params p = with_store_width<EPI>(p0);
     p.wait_cluster = g_tuning.pair_wait_cluster == 1;
+    p.wave_ctr = nullptr;
+    if (g_tuning.pair_wave_sync > 0 && p.kblocks >= g_tuning.pair_wave_sync && p.grouped == 1 &&
+        p.gather_idx == nullptr) {
+        void *ctr = nullptr;
+        HEP_CHECK_CUDA(cudaGetSymbolAddress(&ctr, g_wave_ctr));
+        HEP_CHECK_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), stream));
+        p.wave_ctr = static_cast<unsigned int *>(ctr);
+    }
     auto kern = gemm2sm_kernel<STAGES, EPI, A_MN, B_MN>;
     HEP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES));
     const int grid = sm_count() & ~1;

@@ -270,5 +270,12 @@ __device__ __forceinline__ uint32_t elect_one() {
     return pred;
 }
 
+// acquire load at GPU scope (a counter other CTAs update with atomics)
+__device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const unsigned int *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
 }  // namespace sm100
 }  // namespace hep
