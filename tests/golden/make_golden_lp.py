@@ -162,6 +162,24 @@ def main():
         r["balance_inter"] = int(bal_tp.inter_volume)
         r["topo_inter"] = int(topo_tp.inter_volume)
         cases.append(r)
+    # broad random family: the reference's property-test generator, G 4..10, E 4..20,
+    # d 2..3, both modes, several alphas / node sizes
+    rng = np.random.default_rng(20251017)
+    for i in range(300):
+        _shape, placement, loads = random_instance(rng)
+        G = placement.num_gpus
+        if i % 2 == 0:
+            alpha = float(rng.choice([0.05, 0.1, 0.5, 1.0, 2.0]))
+            opts = h.SolveOptions(mode=COMM_AWARE, alpha=alpha)
+            topo = h.Topology(G, G)
+        else:
+            gpn = int(rng.choice([g for g in (1, 2, 3, 4, 5) if G % g == 0 and g < G] or [G]))
+            ai = float(rng.choice([0.0, 0.1, 0.3]))
+            opts = h.SolveOptions(mode=TOPOLOGY_AWARE, alpha_intra=ai, alpha_inter=max(ai, float(rng.choice([0.5, 1.0]))))
+            topo = h.Topology(G, gpn)
+        r = record(h, placement, loads, topo, opts)[0]
+        r["family"] = "random300"
+        cases.append(r)
     # larger comm-aware LPs (Cayley placements at BASELINE-like expert counts, one node)
     for E in (32, 64):
         shape = h.ClusterShape(8, E, 2)
@@ -174,11 +192,11 @@ def main():
 
     # warm sequences (warm_solve on one state)
     warm = []
-    for E, gpn, mode in ((16, 8, COMM_AWARE), (16, 4, TOPOLOGY_AWARE)):
+    for E, gpn, mode, n_mb in ((16, 8, COMM_AWARE, 8), (16, 4, TOPOLOGY_AWARE, 8), (8, 8, COMM_AWARE, 30)):
         shape = h.ClusterShape(8, E, 2, gpus_per_node=gpn)
         placement = h.cayley_symmetric(shape)
         topo = h.Topology(8, gpn)
-        wl = h.gen_zipf_workload(shape, 1.0, 1024, 8, 5)
+        wl = h.gen_zipf_workload(shape, 1.0, 1024, n_mb, 5)
         opts = h.SolveOptions(mode=mode, alpha=1.0, alpha_intra=0.1, alpha_inter=1.0)
         state = None
         seq = []
