@@ -983,7 +983,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                     const int64_t in_wave = n_total - w * ncl < ncl ? n_total - w * ncl : ncl;
                     wave_target += 2 * in_wave;
                     atomicAdd(p.wave_ctr, 1u);
-                    while ((int64_t)ld_acquire_gpu_u32(p.wave_ctr) < wave_target) __nanosleep(64);
+                    // bounded: the counter only paces the producers, so a CTA that is not
+                    // resident (another kernel holds its SM) delays the wave by 200 µs at most
+                    const uint64_t t_start = globaltimer_ns();
+                    while ((int64_t)ld_acquire_gpu_u32(p.wave_ctr) < wave_target && globaltimer_ns() - t_start < 200000)
+                        __nanosleep(64);
                 }
                 const Tile tl = decode(p, t, s_off);
                 const int32_t a_row = tl.row0 + (int32_t)rank * 128;
@@ -1177,8 +1181,10 @@ __global__ void __launch_bounds__(32 * kTileWarps) tile_count_kernel(const int32
 __global__ void __launch_bounds__(32 * kTileWarps) tile_write_kernel(const int32_t *seg_g, int n_seg, int n_exp,
                                                                      const int32_t *exp_cnt, int32_t *mt_row0,
                                                                      int32_t *mt_rows, int32_t *exp_mt_off,
-                                                                     int64_t cap, int32_t *status, int tile_rows) {
+                                                                     int64_t cap, int32_t *status, int tile_rows,
+                                                                     unsigned int *zero2) {
     extern __shared__ int4 st[];
+    if (zero2 && blockIdx.x == 0 && threadIdx.x < 2) zero2[threadIdx.x] = 0u;  // the pair GEMMs' wave counters
     __shared__ int64_t scan[64];
     __shared__ int64_t off_sm[kTileWarps];
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5;
@@ -1210,14 +1216,14 @@ __global__ void __launch_bounds__(32 * kTileWarps) tile_write_kernel(const int32
 // build the device m-tile list of a grouped GEMM from its segments (2 launches)
 static int build_tiles(const int32_t *d_seg, int n_seg, int n_exp, int32_t *mt_row0, int32_t *mt_rows,
                        int32_t *exp_off, int32_t *exp_cnt, int64_t cap, int32_t *d_status, int tile_rows,
-                       cudaStream_t s, int light_max = 0, int light_sel = 0) {
+                       cudaStream_t s, int light_max = 0, int light_sel = 0, unsigned int *wave_ctr = nullptr) {
     const size_t sm = n_seg <= kTileSegSmem ? 16 * (size_t)n_seg : 0;
     const int blocks = n_exp > 0 ? (n_exp + kTileWarps - 1) / kTileWarps : 1;
     tile_count_kernel<<<blocks, 32 * kTileWarps, sm, s>>>(d_seg, n_seg, n_exp, exp_cnt, tile_rows, light_max,
                                                           light_sel);
     HEP_CHECK_LAUNCH();
     tile_write_kernel<<<blocks, 32 * kTileWarps, sm, s>>>(d_seg, n_seg, n_exp, exp_cnt, mt_row0, mt_rows, exp_off, cap,
-                                                          d_status, tile_rows);
+                                                          d_status, tile_rows, wave_ctr);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
 }
@@ -1324,21 +1330,14 @@ static int launch(const void *A, int64_t a_rows, int64_t K, const void *B, int64
     return launch_maps<BN, STAGES, EPI, false, false>(ta, tb, p, max_tiles, stream);
 }
 
-__device__ unsigned int g_wave_ctr;
-
 template <int STAGES, int EPI, bool A_MN, bool B_MN>
 static int launch2sm_maps(const CUtensorMap &ta, const CUtensorMap &tb, const Params &p0, cudaStream_t stream) {
     using S = Smem2<STAGES>;
     Params p = with_store_width<EPI>(p0);
     p.wait_cluster = g_tuning.pair_wait_cluster == 1;
-    p.wave_ctr = nullptr;
-    if (g_tuning.pair_wave_sync > 0 && p.kblocks >= g_tuning.pair_wave_sync && p.grouped == 1 &&
-        p.gather_idx == nullptr) {
-        void *ctr = nullptr;
-        HEP_CHECK_CUDA(cudaGetSymbolAddress(&ctr, g_wave_ctr));
-        HEP_CHECK_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned int), stream));
-        p.wave_ctr = static_cast<unsigned int *>(ctr);
-    }
+    // wave-synchronised producers only for long tiles (hep_tuning.pair_wave_sync k-blocks)
+    if (g_tuning.pair_wave_sync <= 0 || p.kblocks < g_tuning.pair_wave_sync || p.grouped != 1 || p.gather_idx)
+        p.wave_ctr = nullptr;
     auto kern = gemm2sm_kernel<STAGES, EPI, A_MN, B_MN>;
     HEP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES));
     const int grid = sm_count() & ~1;
@@ -1508,8 +1507,13 @@ extern "C" size_t hep_moe_ffn_workspace(int n_seg, int64_t R, int n_experts) {
     const int64_t cap = R / BM + n_seg + 1;
     // two tile lists (CTA-pair tiles of the heavy experts, 1-CTA tiles of the light ones),
     // each: m-tile rows / sizes [cap] x2, expert tile offsets [E+1], per-expert tile counts [E+1]
-    // + the weight-gradient expert order [E]
+    // + the weight-gradient expert order [E]; the 64-byte tail holds the forward pair GEMMs'
+    // two wave counters (ffn_wave_ctr)
     return (2 * (size_t)(2 * cap + 2 * (int64_t)n_experts + 2) + (size_t)n_experts) * sizeof(int32_t) + 64;
+}
+
+static unsigned int *ffn_wave_ctr(void *ws, int64_t cap, int n_experts) {
+    return reinterpret_cast<unsigned int *>(ws) + 2 * (2 * cap + 2 * (int64_t)n_experts + 2) + n_experts;
 }
 
 static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w2, const int32_t *d_seg, int n_seg,
@@ -1603,8 +1607,9 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
     int32_t *mt_row0_l = exp_off + 2 * (n_experts + 1);
     int32_t *mt_rows_l = mt_row0_l + cap;
     int32_t *exp_off_l = mt_rows_l + cap;
+    unsigned int *wave_ctr = ffn_wave_ctr(d_workspace, cap, n_experts);
     int rc0 = build_tiles(d_seg, n_seg, n_experts, mt_row0, mt_rows, exp_off, exp_off + n_experts + 1, cap, d_status,
-                          pairs ? kPairRows : BM, s, light_max, 0);
+                          pairs ? kPairRows : BM, s, light_max, 0, wave_ctr);
     if (rc0) return rc0;
     if (light_max > 0) {
         rc0 = build_tiles(d_seg, n_seg, n_experts, mt_row0_l, mt_rows_l, exp_off_l, exp_off_l + n_experts + 1, cap,
@@ -1647,6 +1652,7 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
     p.gather_idx = d_row_tok;
     p.gather_oob = (int32_t)T;
     const int64_t a_rows = d_row_tok ? T : R;
+    p.wave_ctr = wave_ctr;
     int rc = pairs ? launch2sm<6, EPI_SWIGLU>(d_rows, a_rows, d_model, d_w13, (int64_t)n_experts * 2 * ffn, p, s)
                    : launch<256, 4, EPI_SWIGLU>(d_rows, a_rows, d_model, d_w13, (int64_t)n_experts * 2 * ffn, p, 0, s);
     if (rc) return rc;
@@ -1660,6 +1666,7 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
     p.clk_slot = clk ? 2 : 0;
     p.row_addr = d_y_addr;
     p.raster_gm = g_tuning.raster_gm2;
+    p.wave_ctr = wave_ctr + 1;
     p.kblocks = (int)(ffn / BK);
     p.n_tiles = (int)(d_model / 256);
     p.b_rows_per_exp = d_model;

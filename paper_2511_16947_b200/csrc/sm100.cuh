@@ -270,6 +270,12 @@ __device__ __forceinline__ uint32_t elect_one() {
     return pred;
 }
 
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 // acquire load at GPU scope (a counter other CTAs update with atomics)
 __device__ __forceinline__ uint32_t ld_acquire_gpu_u32(const unsigned int *p) {
     uint32_t v;
