@@ -65,7 +65,8 @@ typedef struct {
     int router_tile_rows;   /* router GEMM rows per CTA tile, multiple of 16 (0 = 128; shorter tiles measured slower) */
     int pair_wave_sync;     /* > 0: grouped CTA-pair GEMMs with >= this many 64-deep k-blocks per tile start
                                each wave of tiles together (TMA producers meet at a grid-wide counter) */
-    int reserved[6];
+    int lp_dsm;             /* 1: comm-aware LP tableau in the cluster's distributed shared memory when it fits */
+    int reserved[5];
 } hep_tuning;
 int hep_tuning_get(hep_tuning *out);
 int hep_tuning_set(const hep_tuning *in);
@@ -174,7 +175,8 @@ int hep_sched_debug_timing(int64_t *host_out, int n);
  * previous optimal basis [m_eq+m_ub] (warm start, simplex.py:127-144) or NULL.  Outputs:
  * d_x_full [n+m_ub] (structural values first; the caller clips [:n] at 0), d_basis_out
  * [m_eq+m_ub], d_info [8] = {pivots, status (0 ok, 1 infeasible, 2 unbounded, 3 pivot
- * limit), warm start used, artificials, phase-1 pivots, phase-2 pivots}.  A cold solve
+ * limit), warm start used, artificials, phase-1 pivots, phase-2 pivots, cluster size when the
+ * tableau sat in distributed shared memory (0: global memory)}.  A cold solve
  * is bit-identical to the reference (same pivots, same fp64 roundings).  d_work: caller-
  * owned, hep_lp_workspace() bytes.  Asynchronous on `stream`. */
 size_t hep_lp_workspace(int64_t n, int64_t m_eq, int64_t m_ub);

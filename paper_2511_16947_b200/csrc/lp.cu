@@ -41,6 +41,11 @@ namespace lp {
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
+// shared int scratch: reductions [kWarps + 8], then the warm start's assigned/want [2m]
+// or the ratio test's warp counts [kWarps + 1] (never live together)
+__host__ __device__ constexpr int64_t sint_count(int64_t m) {
+    return kWarps + 8 + (2 * m + 2 > kWarps + 2 ? 2 * m + 2 : kWarps + 2);
+}
 
 enum : int { ST_OK = 0, ST_INFEASIBLE = 1, ST_UNBOUNDED = 2, ST_MAXITER = 3 };
 
@@ -50,14 +55,14 @@ struct Args {
     int64_t n, m_eq, m_ub;
     double tol;
     int64_t max_iter;
-    double *T0, *T1;          // workspace tableaux [(m+1) * ld]
+    double *T0, *T1;          // workspace tableaux [(m+1) * ld] (T1: warm-start staging)
     int64_t ld;
+    int dsm;                  // 1: rows live in the cluster's shared memory (row i on CTA i % ncta)
     double *x_full;           // out [width] (reference x_full before the [:n] clip)
     int64_t *basis_out;       // out [m]
     int64_t *info;            // out [8]: pivots, status, warm_used, n_art, phase1_pivots, phase2_pivots
 };
 
-__device__ __forceinline__ double ldcg(const double *p) { return __ldcg(p); }
 
 // one thread-block cluster; all CTAs run the same control flow on the same data
 struct Ctx {
@@ -65,19 +70,34 @@ struct Ctx {
     int rank, ncta;
     int m, width, total;  // rows (excl. objective), vars+slacks, columns excl. rhs
     int64_t ld;
-    double *T;
+    double *T;      // global tableau (dsm = 0)
+    bool dsm;
+    double *rows_local;  // dsm: this CTA's row block; CTA r's block = mapa(rows_local, r)
+    int lg;              // log2(ncta)
     int *basis;     // smem copy, identical in every CTA
     double *prow;   // smem [total+1] normalised pivot row
     int *nz;        // smem [total+1] nonzero columns of the pivot row
     int *s_int;     // smem scratch ints
     double *scol;   // smem [m+1] pivot column T[i][col] of every row (incl. objective)
     double *sratio; // smem [m] rhs/col for eligible rows, +inf otherwise
-    int *rows;      // smem [m+1] owned rows with a nonzero pivot-column entry
+    int *rows;      // smem [m+1] owned rows with a nonzero pivot-column entry / ratio candidates
+    double *sdbl;   // smem [kWarps + 1] double scratch
     double tol;
 };
 
+// row i of the tableau: global row-major, or (dsm) row i / ncta of CTA i % ncta's
+// shared-memory block, reached through its generic DSMEM address
+__device__ __forceinline__ double *rp(const Ctx &c, int i) {
+    if (!c.dsm) return c.T + (int64_t)i * c.ld;
+    double *blk = static_cast<double *>(__cluster_map_shared_rank(c.rows_local, (unsigned)(i & (c.ncta - 1))));
+    return blk + (int64_t)(i >> c.lg) * c.ld;
+}
+// a tableau element another CTA may have written before the last cluster barrier:
+// global through L2 (ld.global.cg, never a stale L1 line), DSMEM directly
+__device__ __forceinline__ double lda(const Ctx &c, const double *p) { return c.dsm ? *p : __ldcg(p); }
+
 // barrier.cluster.arrive (.release) + barrier.cluster.wait (.acquire): orders every
-// CTA's global tableau writes before the other CTAs' (L2, ld.global.cg) reads
+// CTA's tableau writes (global or DSMEM) before the other CTAs' reads
 __device__ __forceinline__ void cluster_sync(Ctx &c) { c.cl.sync(); }
 
 // block-wide min of an int (INT_MAX = none); all threads get the result
@@ -100,13 +120,13 @@ __device__ int block_min_int(int v, int *scratch) {
 
 // _run_phase's entering rule: lowest column j < allowed with obj[j] < -tol
 __device__ int choose_entering(Ctx &c, int allowed) {
-    const double *obj = c.T + (int64_t)c.m * c.ld;
+    const double *obj = rp(c, c.m);
     const double ntol = -c.tol;
     int best = INT_MAX;
     for (int j0 = threadIdx.x; j0 < allowed && best == INT_MAX; j0 += 4 * kThreads) {
         double v[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = j0 + u * kThreads < allowed ? ldcg(obj + j0 + u * kThreads) : 0.0;
+        for (int u = 0; u < 4; ++u) v[u] = j0 + u * kThreads < allowed ? lda(c, obj + j0 + u * kThreads) : 0.0;
 #pragma unroll
         for (int u = 0; u < 4; ++u)
             if (best == INT_MAX && v[u] < ntol) best = j0 + u * kThreads;
@@ -123,8 +143,8 @@ __device__ void load_column(Ctx &c, int col) {
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
             const int i = i0 + u * kThreads;
-            a[u] = i <= c.m ? ldcg(c.T + (int64_t)i * c.ld + col) : 0.0;
-            rhs[u] = i < c.m ? ldcg(c.T + (int64_t)i * c.ld + c.total) : 0.0;
+            a[u] = i <= c.m ? lda(c, rp(c, i) + col) : 0.0;
+            rhs[u] = i < c.m ? lda(c, rp(c, i) + c.total) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
@@ -136,52 +156,114 @@ __device__ void load_column(Ctx &c, int col) {
     __syncthreads();
 }
 
-// _run_phase's leaving rule, the reference's sequential scan over rows 0..m-1
-// (simplex.py:75-86) on the ratios in shared memory: warp 0 walks the rows 32 at a
-// time and skips a chunk in one step when none of its ratios can displace the current
-// best (a replacement needs ratio <= best + tol).  Returns -1 if unbounded.
-__device__ int choose_leaving(Ctx &c) {
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-        const double tol = c.tol;
-        bool have = false;
-        double best = 0.0;
-        int leave = -1;
-        for (int base = 0; base < c.m; base += 32) {
-            const int i = base + lane;
-            const bool el = i < c.m && c.scol[i] > tol;
-            const double ratio = el ? c.sratio[i] : __longlong_as_double(0x7ff0000000000000LL);
-            unsigned any = __ballot_sync(0xffffffffu, el);
-            if (!any) continue;
-            if (have) {
-                double mn = ratio;
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
-                // nobody here can be accepted (a replacement needs ratio <= best + tol;
-                // the margin absorbs the rounding of best + tol and |ratio - best|)
-                if (mn > best + 2.0 * tol + fabs(best) * 1e-12) continue;
-            }
-            const int bi = i < c.m ? c.basis[i] : 0;
-            while (any) {
-                const int l = __ffs(any) - 1;
-                any &= any - 1;
-                const double r = __shfl_sync(0xffffffffu, ratio, l);
-                const int b = __shfl_sync(0xffffffffu, bi, l);
-                bool take;
-                if (!have) take = true;
-                else if (r < best - tol) take = true;
-                else take = fabs(r - best) <= tol && b < c.basis[leave];
-                if (take) {
-                    have = true;
-                    best = r;
-                    leave = base + l;
-                }
-            }
+// _run_phase's leaving rule: the reference's sequential scan over rows 0..m-1
+// (simplex.py:75-86) -- best ratio, a replacement when ratio < best - tol or, within
+// tol, on a lower basis id.  Exact but cheap: a block-wide prefix minimum of the
+// eligible ratios in row order marks the candidates (ratio <= min of the earlier rows
+// + 64 tol); one thread then runs the sequential rule over the candidates alone.  A
+// skipped row can only have been accepted if the running best had drifted more than
+// ~63 tol above the running minimum through chains of tolerance ties; the scan checks
+// that drift and falls back to the full sequential scan if it ever exceeds 32 tol.
+// Returns -1 if unbounded.  Uses c.rows as the candidate list.
+__device__ int seq_leaving(Ctx &c, const int *list, int n, bool all_rows, double *drift) {
+    const double tol = c.tol;
+    bool have = false;
+    double best = 0.0, runmin = 0.0, dmax = 0.0;
+    int leave = -1;
+    for (int k = 0; k < n; ++k) {
+        const int i = all_rows ? k : list[k];
+        if (all_rows && !(c.scol[i] > tol)) continue;
+        const double r = c.sratio[i];
+        bool take;
+        if (!have) take = true;
+        else if (r < best - tol) take = true;
+        else take = fabs(r - best) <= tol && c.basis[i] < c.basis[leave];
+        runmin = have ? fmin(runmin, r) : r;
+        if (take) {
+            have = true;
+            best = r;
+            leave = i;
         }
-        if (lane == 0) c.s_int[kWarps + 1] = leave;
+        dmax = fmax(dmax, best - runmin - fabs(runmin) * 1e-12);
+    }
+    *drift = dmax;
+    return leave;
+}
+
+__device__ int choose_leaving(Ctx &c) {
+    const double INF = __longlong_as_double(0x7ff0000000000000LL);
+    const double tol = c.tol, W = 64.0 * tol;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double *s_wmin = c.sdbl;            // [kWarps] warp minima -> exclusive prefix
+    int *s_wcnt = c.s_int + kWarps + 8;  // [kWarps] warp candidate counts -> exclusive prefix
+    __shared__ double s_carry;
+    __shared__ int s_ncand, s_leave;
+    if (threadIdx.x == 0) {
+        s_carry = INF;
+        s_ncand = 0;
     }
     __syncthreads();
-    int r = c.s_int[kWarps + 1];
+    for (int base = 0; base < c.m; base += kThreads) {
+        const int i = base + threadIdx.x;
+        const bool el = i < c.m && c.scol[i] > tol;
+        const double r = el ? c.sratio[i] : INF;
+        double v = r;  // inclusive warp prefix minimum
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v = fmin(v, t);
+        }
+        double ex = __shfl_up_sync(0xffffffffu, v, 1);
+        if (lane == 0) ex = INF;
+        if (lane == 31) s_wmin[w] = v;
+        __syncthreads();
+        if (w == 0) {
+            const double x = lane < kWarps ? s_wmin[lane] : INF;
+            double y = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const double t = __shfl_up_sync(0xffffffffu, y, o);
+                if (lane >= o) y = fmin(y, t);
+            }
+            double yx = __shfl_up_sync(0xffffffffu, y, 1);
+            if (lane == 0) yx = INF;
+            if (lane < kWarps) s_wmin[lane] = fmin(yx, s_carry);  // min of everything before warp `lane`
+            if (lane == 31) s_wmin[kWarps] = fmin(y, s_carry);     // carry for the next tile
+        }
+        __syncthreads();
+        const double before = fmin(s_wmin[w], ex);
+        const bool cand = el && (before == INF || r <= before + W + fabs(before) * 4e-12);
+        const unsigned bal = __ballot_sync(0xffffffffu, cand);
+        if (lane == 0) s_wcnt[w] = __popc(bal);
+        __syncthreads();
+        if (w == 0) {
+            const int x = lane < kWarps ? s_wcnt[lane] : 0;
+            int y = x;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, y, o);
+                if (lane >= o) y += t;
+            }
+            if (lane < kWarps) s_wcnt[lane] = y - x;
+            if (lane == 31) s_wcnt[kWarps] = y;
+        }
+        __syncthreads();
+        if (cand) c.rows[s_ncand + s_wcnt[w] + __popc(bal & ((1u << lane) - 1))] = i;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            s_ncand += s_wcnt[kWarps];
+            s_carry = s_wmin[kWarps];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        double drift;
+        int l = seq_leaving(c, c.rows, s_ncand, false, &drift);
+        if (drift > 32.0 * tol) l = seq_leaving(c, nullptr, c.m, true, &drift);  // tie chains: scan every row
+        s_leave = l;
+    }
+    __syncthreads();
+    const int r = s_leave;
     __syncthreads();
     return r;
 }
@@ -189,49 +271,55 @@ __device__ int choose_leaving(Ctx &c) {
 // _pivot (simplex.py:53-58) on row r, column col, over columns [0, ncols); the
 // pivot column must be in c.scol (load_column)
 __device__ void pivot(Ctx &c, int r, int col, int ncols) {
-    const double *Tr = c.T + (int64_t)r * c.ld;
+    const double *Tr = rp(c, r);
     const double p = c.scol[r];
     // normalised pivot row (the reference divides the stored row by the scalar
     // pivot value first) and its nonzero pattern, in every CTA
     for (int j0 = threadIdx.x; j0 < ncols; j0 += 4 * kThreads) {
         double v[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = j0 + u * kThreads < ncols ? ldcg(Tr + j0 + u * kThreads) : 0.0;
+        for (int u = 0; u < 4; ++u) v[u] = j0 + u * kThreads < ncols ? lda(c, Tr + j0 + u * kThreads) : 0.0;
 #pragma unroll
         for (int u = 0; u < 4; ++u)
             if (j0 + u * kThreads < ncols) c.prow[j0 + u * kThreads] = __ddiv_rn(v[u], p);
     }
     __syncthreads();
-    // compact nonzero columns (warp 0) and owned rows i != r with a nonzero pivot-
-    // column entry (warp 1); order is irrelevant to the result
-    if (threadIdx.x < 32) {
-        int cnt = 0;
-        for (int base = 0; base < ncols; base += 32) {
-            const int j = base + threadIdx.x;
+    // compact the nonzero columns and the owned rows i != r with a nonzero pivot-column
+    // entry (order is irrelevant to the result): every warp ballots 32 at a time and
+    // reserves its slots with one shared-memory atomic
+    if (threadIdx.x == 0) {
+        c.s_int[kWarps + 2] = 0;
+        c.s_int[kWarps + 4] = 0;
+    }
+    __syncthreads();
+    {
+        const int lane = threadIdx.x & 31;
+        for (int j0 = threadIdx.x - lane; j0 < ncols; j0 += kThreads) {
+            const int j = j0 + lane;
             const bool nzj = j < ncols && c.prow[j] != 0.0;
             const unsigned bal = __ballot_sync(0xffffffffu, nzj);
-            if (nzj) c.nz[cnt + __popc(bal & ((1u << threadIdx.x) - 1))] = j;
-            cnt += __popc(bal);
+            int at = 0;
+            if (lane == 0 && bal) at = atomicAdd(&c.s_int[kWarps + 2], __popc(bal));
+            at = __shfl_sync(0xffffffffu, at, 0);
+            if (nzj) c.nz[at + __popc(bal & ((1u << lane) - 1))] = j;
         }
-        if (threadIdx.x == 0) c.s_int[kWarps + 2] = cnt;
-    } else if (threadIdx.x < 64) {
-        const int lane = threadIdx.x - 32;
-        int cnt = 0;
-        for (int base = c.rank; base <= c.m; base += 32 * c.ncta) {
-            const int i = base + lane * c.ncta;
-            const bool act = i <= c.m && i != r && c.scol[i] != 0.0;
+        const int n_own = (c.m - c.rank) / c.ncta + 1;  // rows rank, rank + ncta, ... <= m
+        for (int k0 = threadIdx.x - lane; k0 < n_own; k0 += kThreads) {
+            const int i = c.rank + (k0 + lane) * c.ncta;
+            const bool act = k0 + lane < n_own && i <= c.m && i != r && c.scol[i] != 0.0;
             const unsigned bal = __ballot_sync(0xffffffffu, act);
-            if (act) c.rows[cnt + __popc(bal & ((1u << lane) - 1))] = i;
-            cnt += __popc(bal);
+            int at = 0;
+            if (lane == 0 && bal) at = atomicAdd(&c.s_int[kWarps + 4], __popc(bal));
+            at = __shfl_sync(0xffffffffu, at, 0);
+            if (act) c.rows[at + __popc(bal & ((1u << lane) - 1))] = i;
         }
-        if (lane == 0) c.s_int[kWarps + 4] = cnt;
     }
     __syncthreads();
     const int nnz = c.s_int[kWarps + 2], nrows = c.s_int[kWarps + 4];
     cluster_sync(c);  // (A) every CTA holds row r; nobody has written yet
     // the pivot row itself (its owner)
     if (r % c.ncta == c.rank) {
-        double *Tr_w = c.T + (int64_t)r * c.ld;
+        double *Tr_w = rp(c, r);
         for (int j = threadIdx.x; j < ncols; j += kThreads) Tr_w[j] = c.prow[j];
     }
     // T[i][j] -= f_i * prow[j] over (active rows) x (nonzero columns), flattened so
@@ -249,10 +337,10 @@ __device__ void pivot(Ctx &c, int r, int col, int ncols) {
             if (idx < work) {
                 const int ri = (int)(idx / nnz), k = (int)(idx - (int64_t)ri * nnz);
                 const int i = c.rows[ri], j = c.nz[k];
-                ptr[u] = c.T + (int64_t)i * c.ld + j;
+                ptr[u] = rp(c, i) + j;
                 f[u] = c.scol[i];
                 pr[u] = c.prow[j];
-                v[u] = ldcg(ptr[u]);
+                v[u] = lda(c, ptr[u]);
             }
         }
 #pragma unroll
@@ -284,25 +372,26 @@ __device__ int64_t run_phase(Ctx &c, int allowed, int ncols, int64_t max_iter, i
     }
 }
 
-// assemble [a | slacks | (artificials) | b] with the b < 0 rows negated
-__device__ void assemble(Ctx &c, const Args &a, double *T, int ncols_rhs_at, bool with_slack_art, int n_art_max) {
+// assemble [a | slacks | (artificials) | b] with the b < 0 rows negated, rhs at
+// column ncols_rhs_at; the cluster's threads split the elements (any CTA may write any
+// row: DSMEM stores in dsm mode)
+__device__ void assemble(Ctx &c, const Args &a, int ncols_rhs_at) {
     const int n = (int)a.n, m_eq = (int)a.m_eq;
     const int tid = threadIdx.x + c.rank * kThreads, nth = kThreads * c.ncta;
-    for (int64_t idx = tid; idx < (int64_t)(c.m + 1) * c.ld; idx += nth) T[idx] = 0.0;
+    for (int64_t idx = tid; idx < (int64_t)(c.m + 1) * c.ld; idx += nth)
+        rp(c, (int)(idx / c.ld))[idx % c.ld] = 0.0;
     cluster_sync(c);
     for (int64_t idx = tid; idx < (int64_t)c.m * n; idx += nth) {
         const int i = (int)(idx / n), j = (int)(idx % n);
         const double b = i < m_eq ? a.b_eq[i] : a.b_ub[i - m_eq];
         double v = i < m_eq ? a.a_eq[(int64_t)i * n + j] : a.a_ub[(int64_t)(i - m_eq) * n + j];
-        T[(int64_t)i * c.ld + j] = b < 0 ? -v : v;
+        rp(c, i)[j] = b < 0 ? -v : v;
     }
     for (int i = tid; i < c.m; i += nth) {
         const double b = i < m_eq ? a.b_eq[i] : a.b_ub[i - m_eq];
-        if (i >= m_eq) T[(int64_t)i * c.ld + n + (i - m_eq)] = b < 0 ? -1.0 : 1.0;
-        T[(int64_t)i * c.ld + ncols_rhs_at] = b < 0 ? -b : b;
+        if (i >= m_eq) rp(c, i)[n + (i - m_eq)] = b < 0 ? -1.0 : 1.0;
+        rp(c, i)[ncols_rhs_at] = b < 0 ? -b : b;
     }
-    (void)with_slack_art;
-    (void)n_art_max;
     cluster_sync(c);
 }
 
@@ -318,6 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) lp_kernel(Args a) {
     // smem: sv[kThreads] doubles | prow[ld] doubles | si[kThreads] | nz[ld] | basis[m] | ints
     const int m1 = c.m > 0 ? c.m : 1;
     double *sv = reinterpret_cast<double *>(smem_raw);
+    c.sdbl = sv;  // the argmax scratch of the warm start is not live at the same time
     c.prow = sv + kThreads;
     c.scol = c.prow + a.ld;
     c.sratio = c.scol + (c.m + 1);
@@ -326,6 +416,16 @@ __global__ void __launch_bounds__(kThreads, 1) lp_kernel(Args a) {
     c.basis = c.nz + a.ld;
     c.rows = c.basis + m1;
     c.s_int = c.rows + (c.m + 1);
+    c.T = a.T0;
+    c.dsm = a.dsm != 0;
+    c.rows_local = nullptr;
+    c.lg = 0;
+    while ((1 << c.lg) < c.ncta) ++c.lg;
+    if (c.dsm) {
+        // this CTA's rows follow the scratch arrays (16-byte aligned); peer[r] = CTA r's block
+        uintptr_t off = reinterpret_cast<uintptr_t>(c.s_int + sint_count(c.m));
+        c.rows_local = reinterpret_cast<double *>((off + 15) & ~(uintptr_t)15);
+    }
     const int m = c.m, width = c.width, n = (int)a.n, m_eq = (int)a.m_eq;
     int status = ST_OK;
     int64_t iters = 0, p1 = 0, p2 = 0;
@@ -342,9 +442,8 @@ __global__ void __launch_bounds__(kThreads, 1) lp_kernel(Args a) {
     if (warm_ok) {
         // [a | b] with rhs at column `width`; Gauss-Jordan on the basis columns with
         // partial pivoting (first maximum |entry| among the unassigned rows, as idamax)
-        c.T = a.T0;
         c.total = width;
-        assemble(c, a, c.T, width, true, 0);
+        assemble(c, a, width);
         int *assigned = c.s_int + kWarps + 8;  // [m] row -> basis position or -1
         for (int i = threadIdx.x; i < m; i += kThreads) assigned[i] = -1;
         __syncthreads();
@@ -395,27 +494,31 @@ __global__ void __launch_bounds__(kThreads, 1) lp_kernel(Args a) {
             const int tid = threadIdx.x + c.rank * kThreads, nth = kThreads * c.ncta;
             for (int64_t idx = tid; idx < (int64_t)m * (width + 1); idx += nth) {
                 const int i = (int)(idx / (width + 1)), j = (int)(idx % (width + 1));
-                a.T1[(int64_t)assigned[i] * c.ld + j] = ldcg(c.T + (int64_t)i * c.ld + j);
+                a.T1[(int64_t)assigned[i] * c.ld + j] = lda(c, rp(c, i) + j);
             }
             cluster_sync(c);
-            c.T = a.T1;
+            for (int64_t idx = tid; idx < (int64_t)m * (width + 1); idx += nth) {
+                const int k = (int)(idx / (width + 1)), j = (int)(idx % (width + 1));
+                rp(c, k)[j] = __ldcg(a.T1 + (int64_t)k * c.ld + j);
+            }
+            cluster_sync(c);
             for (int i = threadIdx.x; i < m; i += kThreads) c.basis[i] = want[i];
             __syncthreads();
             int infeas = INT_MAX;
             for (int i = threadIdx.x; i < m; i += kThreads)
-                if (ldcg(c.T + (int64_t)i * c.ld + width) < -c.tol) infeas = i;
+                if (lda(c, rp(c, i) + width) < -c.tol) infeas = i;
             infeas = block_min_int(infeas, c.s_int);
             if (infeas == INT_MAX) {
                 warm = 1;
                 // objective row: c, then eliminate the basic columns in basis-row order
                 // (basic columns are exact unit vectors here, so each column is independent)
-                double *obj = c.T + (int64_t)m * c.ld;
+                double *obj = rp(c, m);
                 for (int j = threadIdx.x + c.rank * kThreads; j <= width; j += nth) {
                     double o = j < n ? a.c[j] : 0.0;
                     for (int i = 0; i < m; ++i) {
                         const int bvi = c.basis[i];
                         const double coeff = bvi < n ? a.c[bvi] : 0.0;
-                        if (coeff != 0.0) o = __dsub_rn(o, __dmul_rn(coeff, ldcg(c.T + (int64_t)i * c.ld + j)));
+                        if (coeff != 0.0) o = __dsub_rn(o, __dmul_rn(coeff, lda(c, rp(c, i) + j)));
                     }
                     obj[j] = o;
                 }
@@ -429,7 +532,6 @@ __global__ void __launch_bounds__(kThreads, 1) lp_kernel(Args a) {
 
     if (!warm) {
         // ---- cold start: phase 1 with artificials (simplex.py:146-177) ----
-        c.T = a.T0;
         iters = 0;
         p2 = 0;
         status = ST_OK;
@@ -446,33 +548,33 @@ __global__ void __launch_bounds__(kThreads, 1) lp_kernel(Args a) {
         __syncthreads();
         n_art = c.s_int[kWarps + 3];
         c.total = width + n_art;
-        assemble(c, a, c.T, c.total, true, n_art);
+        assemble(c, a, c.total);
         const int tid = threadIdx.x + c.rank * kThreads, nth = kThreads * c.ncta;
         for (int i = tid; i < m; i += nth)
-            if (c.basis[i] >= width) c.T[(int64_t)i * c.ld + c.basis[i]] = 1.0;
+            if (c.basis[i] >= width) rp(c, i)[c.basis[i]] = 1.0;
         cluster_sync(c);
         if (n_art) {
             // objective: 1 on the artificial columns, minus every artificial row in
             // row order (column-independent sequential subtraction)
-            double *obj = c.T + (int64_t)m * c.ld;
+            double *obj = rp(c, m);
             for (int j = tid; j <= c.total; j += nth) {
                 double o = (j >= width && j < c.total) ? 1.0 : 0.0;
                 for (int i = 0; i < m; ++i)
-                    if (c.basis[i] >= width) o = __dsub_rn(o, ldcg(c.T + (int64_t)i * c.ld + j));
+                    if (c.basis[i] >= width) o = __dsub_rn(o, lda(c, rp(c, i) + j));
                 obj[j] = o;
             }
             cluster_sync(c);
             p1 = run_phase(c, c.total, c.total + 1, a.max_iter, &status);
             iters += p1;
-            if (status == ST_OK && ldcg(obj + c.total) < -1e-7) status = ST_INFEASIBLE;
+            if (status == ST_OK && lda(c, obj + c.total) < -1e-7) status = ST_INFEASIBLE;
             if (status == ST_OK) {
                 // drive surviving artificials out of the basis where possible
                 for (int i = 0; i < m; ++i) {
                     if (c.basis[i] < width) continue;
                     int j0 = INT_MAX;
-                    const double *Ti = c.T + (int64_t)i * c.ld;
+                    const double *Ti = rp(c, i);
                     for (int j = threadIdx.x; j < width; j += kThreads)
-                        if (fabs(ldcg(Ti + j)) > c.tol) { j0 = j; break; }
+                        if (fabs(lda(c, Ti + j)) > c.tol) { j0 = j; break; }
                     j0 = block_min_int(j0, c.s_int);
                     if (j0 != INT_MAX) {
                         load_column(c, j0);
@@ -487,13 +589,13 @@ __global__ void __launch_bounds__(kThreads, 1) lp_kernel(Args a) {
             // order, row -= obj[bv] * T[i].  Basic columns are exact unit vectors after
             // pivoting, so obj[bv_i] is still its initial value when row i is reached
             // and every column can be computed independently in the same order.
-            double *obj = c.T + (int64_t)m * c.ld;
+            double *obj = rp(c, m);
             for (int j = tid; j <= c.total; j += nth) {
                 double o = j < n ? a.c[j] : 0.0;
                 for (int i = 0; i < m; ++i) {
                     const int bvi = c.basis[i];
                     const double coeff = bvi < n ? a.c[bvi] : 0.0;
-                    if (coeff != 0.0) o = __dsub_rn(o, __dmul_rn(coeff, ldcg(c.T + (int64_t)i * c.ld + j)));
+                    if (coeff != 0.0) o = __dsub_rn(o, __dmul_rn(coeff, lda(c, rp(c, i) + j)));
                 }
                 obj[j] = o;
             }
@@ -509,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, 1) lp_kernel(Args a) {
         __syncthreads();
         for (int i = threadIdx.x; i < m; i += kThreads) {
             const int bv = c.basis[i];
-            if (bv < width) a.x_full[bv] = ldcg(c.T + (int64_t)i * c.ld + c.total);
+            if (bv < width) a.x_full[bv] = lda(c, rp(c, i) + c.total);
             a.basis_out[i] = bv;
         }
         if (threadIdx.x == 0) {
@@ -519,8 +621,10 @@ __global__ void __launch_bounds__(kThreads, 1) lp_kernel(Args a) {
             a.info[3] = n_art;
             a.info[4] = p1;
             a.info[5] = p2;
+            a.info[6] = c.dsm ? c.ncta : 0;
         }
     }
+    cluster_sync(c);  // dsm: rank 0 read the other CTAs' rows; they stay resident until here
 }
 
 static size_t smem_bytes(int64_t ld, int64_t m) {
@@ -528,7 +632,7 @@ static size_t smem_bytes(int64_t ld, int64_t m) {
     // assigned[m] + want[m] + 1) + argmax scratch (kThreads doubles + ints)
     const size_t m1 = m > 0 ? (size_t)m : 1;
     size_t b = (size_t)(kThreads + ld + (m + 1) + m1) * sizeof(double) + (size_t)(kThreads + ld) * sizeof(int);
-    b += (m1 + (size_t)(m + 1)) * sizeof(int) + (size_t)(kWarps + 8 + 2 * m + 2) * sizeof(int);
+    b += (m1 + (size_t)(m + 1)) * sizeof(int) + (size_t)sint_count(m) * sizeof(int);
     return b;
 }
 
@@ -561,8 +665,42 @@ extern "C" int hep_lp_solve(const double *d_c, const double *d_a_eq, const doubl
     // cluster size: ~16+ rows per CTA, up to 8 CTAs (portable cluster size)
     int ncta = 1;
     while (ncta < 8 && (m + 1) > 16 * ncta) ncta *= 2;
-    HEP_CHECK_CUDA(cudaFuncSetAttribute(lp::lp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    // distributed shared memory: the tableau's rows spread over the cluster's shared
+    // memory when they fit (8 or, non-portable, 16 CTAs), else global memory (L2)
+    int dsm = 0;
+    size_t smem_launch = smem;
+    if (g_tuning.lp_dsm != 0) {
+        for (int nc = ncta < 8 ? 8 : ncta; nc <= 8 && !dsm; nc *= 2) {
+            const int64_t rpc = (m + 1 + nc - 1) / nc;
+            const size_t need = ((smem + 15) & ~(size_t)15) + 16 + (size_t)rpc * (size_t)ld * sizeof(double);
+            if (need > 227 * 1024) continue;
+            HEP_CHECK_CUDA(cudaFuncSetAttribute(lp::lp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)need));
+            if (nc > 8)
+                HEP_CHECK_CUDA(cudaFuncSetAttribute(lp::lp_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            cudaLaunchConfig_t q = {};
+            q.gridDim = dim3(nc);
+            q.blockDim = dim3(lp::kThreads);
+            q.dynamicSmemBytes = need;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = nc;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            q.attrs = at;
+            q.numAttrs = 1;
+            int n_cl = 0;
+            if (cudaOccupancyMaxActiveClusters(&n_cl, lp::lp_kernel, &q) == cudaSuccess && n_cl >= 1) {
+                dsm = 1;
+                ncta = nc;
+                smem_launch = need;
+            } else {
+                (void)cudaGetLastError();
+            }
+        }
+    }
+    HEP_CHECK_CUDA(cudaFuncSetAttribute(lp::lp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_launch));
     lp::Args a;
+    a.dsm = dsm;
     a.c = d_c;
     a.a_eq = d_a_eq;
     a.b_eq = d_b_eq;
@@ -583,7 +721,7 @@ extern "C" int hep_lp_solve(const double *d_c, const double *d_a_eq, const doubl
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(ncta);
     cfg.blockDim = dim3(lp::kThreads);
-    cfg.dynamicSmemBytes = smem;
+    cfg.dynamicSmemBytes = smem_launch;
     cfg.stream = static_cast<cudaStream_t>(stream);
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;

@@ -19,6 +19,12 @@ from conftest import load_golden  # noqa: E402
 
 
 def main():
+    from paper_2511_16947_b200 import _lib
+
+    if len(sys.argv) > 1:  # e.g. "lp_dsm=0"
+        k, v = sys.argv[1].split("=")
+        _lib.set_tuning(**{k: int(v)})
+        print(json.dumps({"tuning": {k: int(v)}}))
     G = load_golden("lp_cases.json.gz")
     ref_ms = {c["family"]: c["ref_ms"] for c in G["cases"] if c["family"].startswith("cayley")}
     c9 = [c for c in G["cases"] if c["family"] == "c9"]
