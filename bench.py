@@ -929,6 +929,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-train", action="store_true", help="skip the forward+backward training-step measurement")
+    ap.add_argument("--no-stress-sweep", dest="stress_sweep", action="store_false",
+                    help="skip BASELINE configs[4] (Zipf 0/1/2 x 4K/64K/1M tokens x G 2/4/8, Qwen3-shaped layer)")
     ap.add_argument("--pipeline-ratio", type=float, default=None,
                     help="harmony_pipelined: share of tokens through the exact scheduler (rest split statically)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -1014,6 +1016,27 @@ def main():
     line["cpu_baseline"] = cpu_line
     line["scheduler_cpu_baseline"] = sched_base
     line["other_configs"] = others or None
+    if args.stress_sweep and not args.profile:
+        # BASELINE configs[4], after the timed region: router / scheduler / assignment / dispatch
+        # per micro-batch (CUDA events over 20 back-to-back launches of each stage), exact max/mean
+        # load, and the CPU reference scheduler (Dinic port, 1 core) on the same load matrix
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from stress_sweep import sweep_points
+
+        t0 = time.perf_counter()
+        pts = list(sweep_points([2, 4, 8], [0.0, 1.0, 2.0], [4096, 65536, 1048576], reps=20))
+        line["stress_sweep"] = {
+            "config": "BASELINE configs[4]: Qwen3-30B-A3B-shaped layer (E=128, K=8, d=2048), Zipf s x tokens per "
+                      "micro-batch x G scheduling GPUs, simulated EP on one B200, Cayley placement",
+            "columns": ["G", "zipf_s", "tokens", "router_gate_us", "sched_us", "assign_us", "dispatch_us",
+                        "dispatch_GB/s", "max_mean_gpu_load", "cpu_reference_sched_us"],
+            "rows": [[p[k] for k in ("G", "zipf_s", "tokens", "router_gate_us", "sched_us", "assign_us",
+                                     "dispatch_us", "dispatch_GB/s", "max_mean_gpu_load", "cpu_reference_sched_us")]
+                     for p in pts],
+            "cpu_reference": "oracle/hep_oracle.c (the reference's Dinic scheduler + integerize + routing restated "
+                             "in C), 1 core, same load matrix",
+            "wall_s": round(time.perf_counter() - t0, 1),
+        }
     line["tuning"] = _lib.get_tuning()
     print(json.dumps(line))
 

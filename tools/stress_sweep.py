@@ -24,33 +24,26 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--tokens", default="4096,16384,65536,262144,1048576")
-    ap.add_argument("--skews", default="0,0.5,1,1.5,2")
-    ap.add_argument("--gpus", default="2,4,8")
-    ap.add_argument("--reps", type=int, default=20)
-    args = ap.parse_args()
+def sweep_points(gpus, skews, tokens, reps=20, cpu_reps=3):
+    """Yield one dict per (G, s, T) point (see the module docstring)."""
+    import ctypes
 
     import torch
 
-    import ctypes
-
     import paper_2511_16947_b200 as P
     from paper_2511_16947_b200 import _lib
-    from oracle import oracle as O
+    from oracle import oracle as O  # the CPU reference scheduler (checker / baseline only)
 
     L = _lib.lib()
-
     E, K, d, F = 128, 8, 2048, 768
     stages = ("router", "sched", "assign", "permute")
-    for G in [int(v) for v in args.gpus.split(",")]:
+    for G in gpus:
         shape = P.ClusterShape(G, E, 2)
         pl = P.cayley_symmetric(shape)
-        for s in [float(v) for v in args.skews.split(",")]:
+        for s in skews:
             bias = torch.tensor(P.zipf_gate_bias(E, s, 0)) if s > 0 else None
             layer = P.MoELayer(pl, d, F, K, seed=0, gate_bias=bias)
-            for T in [int(v) for v in args.tokens.split(",")]:
+            for T in tokens:
                 T -= T % G
                 x = torch.randn(T, d, generator=torch.Generator(device="cuda").manual_seed(T), device="cuda")
                 x = x.to(torch.bfloat16)
@@ -78,22 +71,21 @@ def main():
                     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     launches[k]()
                     e0.record()
-                    for _ in range(args.reps):
+                    for _ in range(reps):
                         launches[k]()
                     e1.record()
                     torch.cuda.synchronize()
-                    ms[k] = e0.elapsed_time(e1) / args.reps
+                    ms[k] = e0.elapsed_time(e1) / reps
                 layer.check_status()
                 gl = layer.sched.gpu_load.cpu().tolist()
                 mean = sum(gl) / len(gl)
                 loads = b.hist.cpu().numpy().T.copy()  # [E][G] load matrix of this micro-batch
                 t0 = time.perf_counter()
-                n_cpu = 3
-                for _ in range(n_cpu):
+                for _ in range(cpu_reps):
                     O.full_path(G, pl.edp_groups, loads)
-                cpu_us = (time.perf_counter() - t0) / n_cpu * 1e6
+                cpu_us = (time.perf_counter() - t0) / cpu_reps * 1e6
                 perm_bytes = T * d * 2 * (1 + K) + T * K * 4
-                print(json.dumps({
+                yield {
                     "G": G, "zipf_s": s, "tokens": T, "E": E, "K": K, "d_model": d,
                     "sched_us": round(1e3 * ms["sched"], 1), "assign_us": round(1e3 * ms["assign"], 1),
                     "router_gate_us": round(1e3 * ms["router"], 1),
@@ -101,11 +93,24 @@ def main():
                     "dispatch_GB/s": round(perm_bytes / (ms["permute"] / 1e3) / 1e9, 1),
                     "max_mean_gpu_load": round(max(gl) / mean, 4) if mean else 1.0,
                     "cpu_reference_sched_us": round(cpu_us, 1),
-                    "cpu_reference": "Dinic oracle port (C, 1 core) on the same load matrix",
-                }), flush=True)
-                del x
+                }
+                del x, b
+                layer._bufs.clear()
             del layer
             torch.cuda.empty_cache()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--tokens", default="4096,16384,65536,262144,1048576")
+    ap.add_argument("--skews", default="0,0.5,1,1.5,2")
+    ap.add_argument("--gpus", default="2,4,8")
+    ap.add_argument("--reps", type=int, default=20)
+    args = ap.parse_args()
+    for rec in sweep_points([int(v) for v in args.gpus.split(",")], [float(v) for v in args.skews.split(",")],
+                            [int(v) for v in args.tokens.split(",")], args.reps):
+        rec["cpu_reference"] = "Dinic oracle port (C, 1 core) on the same load matrix"
+        print(json.dumps(rec), flush=True)
 
 
 if __name__ == "__main__":
