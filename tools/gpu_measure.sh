@@ -24,6 +24,7 @@ for c in qwen3 dsv3; do
   timeout 600 python bench.py --config $c --pipeline-ratio 0.5 --other-configs "" --no-cpu-baseline --no-train --no-balance-sweep > gpurun_out/bench_${c}_pipelined_$R.json 2>&1
 done
 timeout 600 python bench.py --impl reference > gpurun_out/bench_ref_mixtral_$R.json 2>&1
+timeout 300 python tools/lp_timing.py > gpurun_out/lp_timing_$R.jsonl 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
   -k regex:"gemm2sm_kernel|gemm_kernel|sched_kernel|permute|combine|chunk_map|plan_prep" -c 9 \
   -o gpurun_out/prof_mixtral_$R python bench.py --config mixtral --profile --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_mixtral_$R.log 2>&1
