@@ -66,7 +66,10 @@ typedef struct {
     int pair_wave_sync;     /* > 0: grouped CTA-pair GEMMs with >= this many 64-deep k-blocks per tile start
                                each wave of tiles together (TMA producers meet at a grid-wide counter) */
     int lp_dsm;             /* 1: comm-aware LP tableau in the cluster's distributed shared memory when it fits */
-    int reserved[5];
+    int light_wave_sync;    /* 1: the 1-CTA grouped GEMMs (light experts) also start waves together (same threshold;
+                               0 by default: DSv3 light GEMMs already read only their algorithmic bytes,
+                               profiles/r02/wave_ab_r02h.txt) */
+    int reserved[4];
 } hep_tuning;
 int hep_tuning_get(hep_tuning *out);
 int hep_tuning_set(const hep_tuning *in);

@@ -731,7 +731,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t pol_b = p.pol_mode ? pick_policy((p.pol_mode >> 2) & 3) : policy_evict_last();
             const uint64_t pol_first = policy_evict_first();
             uint32_t phase = 0;
+            int64_t wave_target = 0;
             for (int64_t t = blockIdx.x; t < n_total; t += gridDim.x) {
+                if (p.wave_ctr && t >= gridDim.x) {  // as in gemm2sm_kernel: waves start together
+                    const int64_t w = t / gridDim.x;
+                    const int64_t in_wave = n_total - w * gridDim.x < gridDim.x ? n_total - w * gridDim.x : gridDim.x;
+                    wave_target += in_wave;
+                    atomicAdd(p.wave_ctr, 1u);
+                    const uint64_t t_start = globaltimer_ns();
+                    while ((int64_t)ld_acquire_gpu_u32(p.wave_ctr) < wave_target && globaltimer_ns() - t_start < 200000)
+                        __nanosleep(64);
+                }
                 const Tile tl = decode(p, t, s_off);
                 const int32_t b_row = (int32_t)(tl.expert * p.b_rows_per_exp + (int64_t)tl.n_blk * BN);
                 // contraction offsets: mode 2 contracts over the expert's rows; an MN-major
@@ -1184,7 +1194,7 @@ __global__ void __launch_bounds__(32 * kTileWarps) tile_write_kernel(const int32
                                                                      int64_t cap, int32_t *status, int tile_rows,
                                                                      unsigned int *zero2) {
     extern __shared__ int4 st[];
-    if (zero2 && blockIdx.x == 0 && threadIdx.x < 2) zero2[threadIdx.x] = 0u;  // the pair GEMMs' wave counters
+    if (zero2 && blockIdx.x == 0 && threadIdx.x < 4) zero2[threadIdx.x] = 0u;  // the expert GEMMs' wave counters
     __shared__ int64_t scan[64];
     __shared__ int64_t off_sm[kTileWarps];
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5;
@@ -1308,7 +1318,10 @@ template <int BN, int STAGES, int EPI, bool A_MN, bool B_MN>
 static int launch_maps(const CUtensorMap &ta, const CUtensorMap &tb, const Params &p0, int64_t max_tiles,
                        cudaStream_t stream) {
     using S = Smem<BN, STAGES>;
-    const Params p = with_store_width<EPI>(p0);
+    Params p = with_store_width<EPI>(p0);
+    if (g_tuning.pair_wave_sync <= 0 || p.kblocks < g_tuning.pair_wave_sync || p.grouped != 1 || p.gather_idx ||
+        g_tuning.light_wave_sync == 0)
+        p.wave_ctr = nullptr;
     auto kern = gemm_kernel<BN, STAGES, EPI, A_MN, B_MN>;
     HEP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES));
     int grid = sm_count();
@@ -1621,6 +1634,7 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
         q.mt_rows = mt_rows_l;
         q.exp_mt_off = exp_off_l;
         q.clk_slot = 0;
+        q.wave_ctr = q.wave_ctr ? q.wave_ctr + 2 : nullptr;  // counters 2 / 3: the light GEMMs
         return q;
     };
     Params p{};
