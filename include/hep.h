@@ -69,7 +69,11 @@ typedef struct {
     int light_wave_sync;    /* 1: the 1-CTA grouped GEMMs (light experts) also start waves together (same threshold;
                                0 by default: DSv3 light GEMMs already read only their algorithmic bytes,
                                profiles/r02/wave_ab_r02h.txt) */
-    int reserved[4];
+    int router_mc;          /* router GEMM: thread-block cluster size sharing each Wg tile by TMA multicast
+                               (0 auto, 1 off, 2 or 4) */
+    int router_pair;        /* router GEMM on CTA pairs (cta_group::2, half the Wg tile per CTA): 0 auto (E_pad > 128),
+                               1 off, 2 on (E_pad > 64) */
+    int reserved[2];
 } hep_tuning;
 int hep_tuning_get(hep_tuning *out);
 int hep_tuning_set(const hep_tuning *in);

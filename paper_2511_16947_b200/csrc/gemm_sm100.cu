@@ -102,6 +102,11 @@ struct Params {
     int clk_slot;
     unsigned int *wave_ctr;  // pair kernel: producers' wave counter (zeroed before the launch) or null
     int a_box_rows;  // mode 0, K-major A: rows per A TMA box (= tile_m when < 128; 0 = BM)  // > 0: CTA 0 stamps (clock64, globaltimer) at entry and exit into g_gemm_clk[clk_slot - 1]
+    // mode 0 (the router GEMM): > 1 = the launch's thread-block cluster size; every CTA of a
+    // cluster TMA-loads 1/b_mc of each B (Wg) tile and multicasts it to all of them, so B
+    // crosses L2 -> SM once per cluster.  The cluster's CTAs walk their tiles in lockstep
+    // (tiles past the last one are empty: B only, no MMAs, no epilogue work)
+    int b_mc;
 };
 
 // Diagnostics (hep_tuning.ffn_clock = 1): SM clock cycles and wall nanoseconds of CTA 0 across
@@ -116,6 +121,27 @@ __device__ __forceinline__ void clk_stamp(const Params &p, int at) {
         g_gemm_clk[p.clk_slot - 1][2 * at + 1] = ns;
     }
 }
+
+// Diagnostics build only (-DHEP_ROUTER_STAMPS, tools/router_stamps.py): %globaltimer of every
+// router CTA at entry, last MMA issued, epilogue start / end, exit
+#ifdef HEP_ROUTER_STAMPS
+__device__ unsigned long long g_router_stamps[256][8];
+#define ROUTER_STAMP(i)                                                                   \
+    do {                                                                                 \
+        if (EPI == EPI_GATE && blockIdx.x < 256) g_router_stamps[blockIdx.x][i] = globaltimer_ns(); \
+    } while (0)
+#define GATE_STAMP(i)                                                                              \
+    do {                                                                                           \
+        if (row_in_tile == 0 && half == 0 && blockIdx.x < 256) g_router_stamps[blockIdx.x][i] = globaltimer_ns(); \
+    } while (0)
+#else
+#define GATE_STAMP(i) \
+    do {              \
+    } while (0)
+#define ROUTER_STAMP(i) \
+    do {                \
+    } while (0)
+#endif
 
 __device__ __forceinline__ uint64_t pick_policy(int k) {
     return k == 2 ? sm100::policy_evict_last() : (k == 3 ? sm100::policy_evict_first() : sm100::policy_evict_normal());
@@ -404,6 +430,11 @@ __device__ __forceinline__ uint32_t order_key(float f) {
     const uint32_t u = __float_as_uint(f + 0.0f);  // -0 -> +0: equal scores must tie
     return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
+// order_key of a value known not to be -0 (SHF + LOP3)
+__device__ __forceinline__ uint32_t order_key_nz(float f) {
+    const uint32_t u = __float_as_uint(f);
+    return u ^ ((uint32_t)((int32_t)u >> 31) | 0x80000000u);
+}
 
 // EPI_GATE epilogue of one accumulator tile (<= 128 tokens), run by all 8 epilogue
 // warps: warp pair (q, q+4) shares TMEM lane quarter q; with E_pad % 32 == 0 the two
@@ -447,6 +478,30 @@ __device__ __forceinline__ void key_insert(uint32_t key, uint32_t (&tk)[KG]) {
 }
 
 __device__ __forceinline__ void gate_bar(int nthr) { asm volatile("bar.sync 1, %0;" ::"r"(nthr) : "memory"); }
+// v[i] for a runtime i < 16 without local memory: a 4-level select tree
+__device__ __forceinline__ uint32_t pick16(const uint32_t (&v)[16], int i) {
+    uint32_t a[8], b[4], c[2];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) a[j] = (i & 8) ? v[j + 8] : v[j];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) b[j] = (i & 4) ? a[j + 4] : a[j];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) c[j] = (i & 2) ? b[j + 2] : b[j];
+    return (i & 1) ? c[1] : c[0];
+}
+// named barrier 1 that also ORs a predicate over its nthr threads
+__device__ __forceinline__ bool gate_bar_or(int nthr, bool v) {
+    uint32_t r;
+    asm volatile(
+        "{\n\t.reg .pred p, q;\n\t"
+        "setp.ne.u32 p, %1, 0;\n\t"
+        "bar.red.or.pred q, 1, %2, p;\n\t"
+        "selp.u32 %0, 1, 0, q;\n}"
+        : "=r"(r)
+        : "r"((uint32_t)v), "r"(nthr)
+        : "memory");
+    return r != 0;
+}
 
 template <int KG, int SPAN>
 __device__ __forceinline__ void gate_tile(const Params &p, uint32_t t_row, int64_t row0, int rows, int row_in_tile,
@@ -479,9 +534,14 @@ __device__ __forceinline__ void gate_tile(const Params &p, uint32_t t_row, int64
     const int c_lo = half * SPAN;
     const int c_hi = c_lo + SPAN;
     // ---- pass 1: logits out, top-KG keys -------------------------------------------
-    uint32_t tk[KG];
+    // two independent networks (even / odd columns), merged after the scan: the per-column
+    // min/max chain is latency-bound at two warps per scheduler, so this doubles its ILP.
+    // s_bias holds bias + 0.0f (never -0) and -inf on padding columns, so logit + bias is
+    // never -0 and order_key needs no normalising add; padding keys (of -inf) stay below
+    // every finite score
+    uint32_t tk[KG], tk2[KG];
 #pragma unroll
-    for (int i = 0; i < KG; ++i) tk[i] = 0u;
+    for (int i = 0; i < KG; ++i) tk[i] = tk2[i] = 0u;
     float *lrow = (valid && p.out) ? reinterpret_cast<float *>(p.out) + t * p.ld_out : nullptr;
 #pragma unroll 1
     for (int c = c_lo; c < c_hi; c += CW) {
@@ -500,17 +560,18 @@ __device__ __forceinline__ void gate_tile(const Params &p, uint32_t t_row, int64
                                          __uint_as_float(v[j][4 * i + 2]), __uint_as_float(v[j][4 * i + 3]));
             }
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-                const int e = cj + i;
-                // padding columns get key 0, below every real score
-                const uint32_t key = e < E ? order_key(__uint_as_float(v[j][i]) + s_bias[e]) : 0u;
-                key_insert<KG>(key, tk);
+            for (int i = 0; i < 16; i += 2) {
+                key_insert<KG>(order_key_nz(__uint_as_float(v[j][i]) + s_bias[cj + i]), tk);
+                key_insert<KG>(order_key_nz(__uint_as_float(v[j][i + 1]) + s_bias[cj + i + 1]), tk2);
             }
         }
     }
+#pragma unroll
+    for (int k = 0; k < KG; ++k) key_insert<KG>(tk2[k], tk);
+    GATE_STAMP(5);
     // ---- threshold and per-half quotas ------------------------------------------------
     uint32_t vK;
-    int quota, offset;
+    int quota, offset, lim;  // lim: one past this half's last slot in the K-entry list
     if (nhalf == 2) {
         if (half == 1)
 #pragma unroll
@@ -532,6 +593,7 @@ __device__ __forceinline__ void gate_tile(const Params &p, uint32_t t_row, int64
             }
             quota = c0h < need ? c0h : need;  // the lower expert ids take the ties first
             offset = 0;
+            lim = gt0 + quota;
             bc[0] = (int32_t)vK;
             bc[1] = need - quota;
             bc[2] = gt0 + quota;
@@ -541,6 +603,7 @@ __device__ __forceinline__ void gate_tile(const Params &p, uint32_t t_row, int64
             vK = (uint32_t)bc[0];
             quota = bc[1];
             offset = bc[2];
+            lim = KG;
         }
     } else {
         vK = tk[KG - 1];
@@ -548,35 +611,69 @@ __device__ __forceinline__ void gate_tile(const Params &p, uint32_t t_row, int64
 #pragma unroll
         for (int k = 0; k < KG; ++k) quota += tk[k] == vK;
         offset = 0;
+        lim = KG;
     }
+    GATE_STAMP(6);
     // ---- pass 2: the selected experts, ascending, into the shared list -----------------
+    // Fast path: one compare per column into a 16-bit mask of the columns with key >= vK;
+    // their expert ids and logits (pick16) go to the list.  That set is exactly the
+    // selection unless a half
+    // holds more vK-keyed columns than its quota (exact score ties at the K-th place): then
+    // its count overshoots `lim`, and the whole tile reruns the exact scan below.
     int cnt = offset;
+    bool exact = false;
+    {
 #pragma unroll 1
-    for (int c = c_lo; c < c_hi; c += CW) {
-        uint32_t v[NJ][16];
+        for (int c = c_lo; c < c_hi; c += 16) {
+            uint32_t v[16];
+            tmem_ld16(t_row + c, v);
+            tmem_ld_wait();
+            uint32_t m = 0;
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) tmem_ld16(t_row + c + 16 * j, v[j]);
-        tmem_ld_wait();
-        if (valid) {
+            for (int i = 0; i < 16; ++i)
+                if (order_key_nz(__uint_as_float(v[i]) + s_bias[c + i]) >= vK) m |= 1u << i;
+            while (m) {
+                const int i = __ffs(m) - 1;
+                m &= m - 1;
+                if (cnt < KG) {
+                    le[cnt] = c + i;
+                    lv[cnt] = __uint_as_float(pick16(v, i));
+                }
+                ++cnt;
+            }
+        }
+        exact = gate_bar_or(nthr, valid && cnt != lim);  // also: both halves' entries are in
+        cnt = offset;
+    }
+    if (exact) {
+#pragma unroll 1
+        for (int c = c_lo; c < c_hi; c += CW) {
+            uint32_t v[NJ][16];
 #pragma unroll
-            for (int j = 0; j < NJ; ++j) {
+            for (int j = 0; j < NJ; ++j) tmem_ld16(t_row + c + 16 * j, v[j]);
+            tmem_ld_wait();
+            if (valid) {
 #pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    const int e = c + 16 * j + i;
-                    const float l = __uint_as_float(v[j][i]);
-                    const uint32_t key = e < E ? order_key(l + s_bias[e]) : 0u;
-                    const bool tie = key == vK && quota > 0;
-                    if (e < E && (key > vK || tie)) {
-                        le[cnt] = e;
-                        lv[cnt] = l;
-                        ++cnt;
-                        quota -= tie;
+                for (int j = 0; j < NJ; ++j) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int e = c + 16 * j + i;
+                        const float l = __uint_as_float(v[j][i]);
+                        const uint32_t key = e < E ? order_key(l + s_bias[e]) : 0u;
+                        const bool tie = key == vK && quota > 0;
+                        if (e < E && (key > vK || tie)) {
+                            le[cnt] = e;
+                            lv[cnt] = l;
+                            ++cnt;
+                            quota -= tie;
+                        }
                     }
                 }
             }
         }
+        if (nhalf == 2) gate_bar(nthr);  // half 1's entries are in the list
     }
-    if (nhalf == 2) gate_bar(nthr);  // half 1's entries are in the list
+    GATE_STAMP(7);
     if (half == 0 && valid) {
         uint32_t tkf[KG];
         int te[KG];
@@ -661,17 +758,20 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t *s_merge = reinterpret_cast<uint8_t *>(s_bias + kGateMaxE);   // EPI_GATE: column-half merge
     if constexpr (EPI == EPI_GATE) {
         for (int i = threadIdx.x; i < p.gate.n_src * p.gate.E; i += blockDim.x) s_hist[i] = 0;
-        for (int i = threadIdx.x; i < BN; i += blockDim.x)
-            s_bias[i] = (p.gate.bias && i < p.gate.E) ? p.gate.bias[i] : 0.f;
+        for (int i = threadIdx.x; i < BN; i += blockDim.x)  // + 0.0f: -0 -> +0 (see gate_tile)
+            s_bias[i] = i >= p.gate.E ? -__int_as_float(0x7f800000) : (p.gate.bias ? p.gate.bias[i] + 0.0f : 0.f);
     }
 
+    if (threadIdx.x == 0) ROUTER_STAMP(0);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int mc = (EPI == EPI_GATE && !A_MN && !B_MN && p.grouped == 0) ? p.b_mc : 0;  // router only
+    const uint32_t mc_rank = mc > 1 ? cluster_ctarank() : 0u;
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], mc > 1 ? mc : 1);  // multicast B: every cluster CTA's MMAs release the slot
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
@@ -683,12 +783,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 1) tmem_alloc(tmem_slot, S::TMEM_COLS);
     tc_fence_before();
     __syncthreads();
+    if (mc > 1) cluster_sync();  // peers multicast into this CTA's smem / barriers only after init
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     clk_stamp(p, 0);
 
     const int64_t n_total = total_tiles(p);
     const int kb = p.kblocks;
+    // multicast B: a cluster's CTAs walk tiles in lockstep, so a CTA runs while its cluster's
+    // first tile exists (t - rank < n_total); tiles >= n_total are empty (rows = 0)
+    const int64_t t_end = n_total + (mc > 1 ? (int64_t)mc_rank : 0);
 
     if (warp == 0 && p.gather_idx) {
         // ============ TMA producer, A rows gathered by token (the fused permute) ============
@@ -732,7 +836,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t pol_first = policy_evict_first();
             uint32_t phase = 0;
             int64_t wave_target = 0;
-            for (int64_t t = blockIdx.x; t < n_total; t += gridDim.x) {
+            const uint16_t mc_mask = (uint16_t)((1u << (mc > 1 ? mc : 1)) - 1u);
+            for (int64_t t = blockIdx.x; t < t_end; t += gridDim.x) {
                 if (p.wave_ctr && t >= gridDim.x) {  // as in gemm2sm_kernel: waves start together
                     const int64_t w = t / gridDim.x;
                     const int64_t in_wave = n_total - w * gridDim.x < gridDim.x ? n_total - w * gridDim.x : gridDim.x;
@@ -742,7 +847,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     while ((int64_t)ld_acquire_gpu_u32(p.wave_ctr) < wave_target && globaltimer_ns() - t_start < 200000)
                         __nanosleep(64);
                 }
-                const Tile tl = decode(p, t, s_off);
+                const bool empty_tile = t >= n_total;  // multicast B only
+                const Tile tl = decode(p, empty_tile ? 0 : t, s_off);
                 const int32_t b_row = (int32_t)(tl.expert * p.b_rows_per_exp + (int64_t)tl.n_blk * BN);
                 // contraction offsets: mode 2 contracts over the expert's rows; an MN-major
                 // weight (mode 1) is [K][N] per expert, stacked along K
@@ -753,11 +859,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool light = p.light_first && p.grouped == 1 && s_off[tl.expert + 1] - s_off[tl.expert] == 1;
                 // A boxes of a_box_rows rows (router tiles of < 128 tokens): the MMA still reads
                 // 128 rows, the rows past the box are stale and land only in ignored accumulator rows
-                const uint32_t tx = (!A_MN && p.a_box_rows > 0) ? (uint32_t)(p.a_box_rows * BK * 2) + S::B_BYTES
-                                                                : (uint32_t)S::STAGE_BYTES;
+                const uint32_t tx = empty_tile ? (uint32_t)S::B_BYTES
+                                    : (!A_MN && p.a_box_rows > 0) ? (uint32_t)(p.a_box_rows * BK * 2) + S::B_BYTES
+                                                                  : (uint32_t)S::STAGE_BYTES;
                 for (int k = 0; k < tl.kb; ++k) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], tx);
+                    if (!A_MN && !B_MN && mc > 1) {
+                        // B slice mc_rank (BN / mc rows, a multiple of the 8-row swizzle atom) to
+                        // every CTA of the cluster; A (this CTA's tokens) locally
+                        if (!empty_tile)
+                            tma_load_2d_hint(sA + stage * S::A_BYTES, &tmA, &full[stage], a_k0 + k * BK, tl.row0, pol_a);
+                        const int slice = BN / mc;
+                        tma_load_2d_mc(sB + stage * S::B_BYTES + mc_rank * slice * (BK * 2), &tmB, &full[stage], k * BK,
+                                       b_row + (int32_t)mc_rank * slice, mc_mask, pol_b);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
                     if constexpr (A_MN) {
 #pragma unroll
                         for (int i = 0; i < BM / 64; ++i)
@@ -778,6 +896,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
+            if (mc > 1)  // producer tail: every cluster CTA's release of every slot has landed here
+                for (int i = 0; i < STAGES; ++i) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
         }
     } else if (warp == 1) {
         if (lane == 0) {
@@ -787,7 +910,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int64_t t = blockIdx.x; t < n_total; t += gridDim.x) {
+            const uint16_t mc_mask = (uint16_t)((1u << (mc > 1 ? mc : 1)) - 1u);
+            for (int64_t t = blockIdx.x; t < t_end; t += gridDim.x) {
                 const int tkb = (p.grouped == 2 || p.k_split > 1) ? decode(p, t, s_off).kb : kb;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
@@ -795,6 +919,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int k = 0; k < tkb; ++k) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
+                    if (mc > 1) {  // the slot's B slices came from every CTA: release it in all of them
+                        if (t < n_total) {
+                            const uint32_t a_addr = smem_u32(sA + stage * S::A_BYTES);
+                            const uint32_t b_addr = smem_u32(sB + stage * S::B_BYTES);
+#pragma unroll
+                            for (int kk = 0; kk < BK / 16; ++kk)
+                                mma_bf16(d_tmem, desc_kmajor_sw128(a_addr + kk * 32), desc_kmajor_sw128(b_addr + kk * 32),
+                                         idesc_bf16_f32(BM, BN), (k | kk) ? 1u : 0u);
+                        }
+                        mma_commit_mc(&empty[stage], mc_mask);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
                     const uint32_t a_addr = smem_u32(sA + stage * S::A_BYTES);
                     const uint32_t b_addr = smem_u32(sB + stage * S::B_BYTES);
 #pragma unroll
@@ -809,6 +946,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mma_commit(&tfull[acc]);  // accumulator ready for the epilogue
                 if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
+            ROUTER_STAMP(1);
         }
     } else {
         // ===================== epilogue (warps 2..9) =====================
@@ -818,15 +956,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int row_in_tile = quarter * 32 + lane;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int64_t t = blockIdx.x; t < n_total; t += gridDim.x) {
-            const Tile tl = decode(p, t, s_off);
+        for (int64_t t = blockIdx.x; t < t_end; t += gridDim.x) {
+            const Tile tl = decode(p, t < n_total ? t : 0, s_off);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
+            if (warp == 2 && lane == 0) ROUTER_STAMP(2);
             const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
             if constexpr (EPI == EPI_GATE) {
                 // both column halves when E_pad splits into 16-column steps, else half 0 alone
                 constexpr int NH = (BN % 32 == 0 && kEpiSplit == 2) ? 2 : 1;
-                if (half < NH) {
+                if (half < NH && t < n_total) {
 #define HEP_GATE_K(KK) \
     case KK: gate_tile<KK, BN / NH>(p, t_row, tl.row0, tl.rows, row_in_tile, half, NH, s_hist, s_chunk, s_bias, s_merge); break;
                     switch (p.gate.K) {  // the insertion network is unrolled per K
@@ -844,11 +983,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_relaxed(&tempty[acc]);
+            if (warp == 2 && lane == 0) ROUTER_STAMP(3);
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
     }
     tc_fence_before();
     __syncthreads();
+    // multicast B: peers' last commits arrive on this CTA's barriers; nobody exits before them
+    if (mc > 1) cluster_sync();
     clk_stamp(p, 1);
     if (warp == 1) {
         tc_fence_after();
@@ -857,6 +999,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     if constexpr (EPI == EPI_GATE) {  // integer sums: order-free, deterministic
         for (int i = threadIdx.x; i < p.gate.n_src * p.gate.E; i += blockDim.x)
             if (s_hist[i]) atomicAdd(reinterpret_cast<unsigned long long *>(p.gate.hist) + i, (unsigned long long)s_hist[i]);
+#ifdef HEP_ROUTER_STAMPS
+        __syncthreads();
+        if (threadIdx.x == 0) ROUTER_STAMP(4);
+#endif
     }
 }
 
@@ -884,22 +1030,26 @@ __device__ __forceinline__ void pair_wait(const Params &p, uint64_t *bar, uint32
         mbar_wait(bar, parity);
 }
 
-template <int STAGES>
+template <int STAGES, int BN = 256>
 struct Smem2 {
     static constexpr int A_BYTES = 128 * BK * 2;
-    static constexpr int B_BYTES = 128 * BK * 2;
+    static constexpr int B_BYTES = (BN / 2) * BK * 2;  // this CTA's half of the B tile
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr size_t BYTES = 1024 + (size_t)STAGES * STAGE_BYTES + 8 * (2 * STAGES + 4) + 16 + kOffBytes;
 };
 
 // A_MN / B_MN as in gemm_kernel (the backward GEMMs): an MN-major operand half of 128
 // rows is two 64 x 64 boxes per stage, 8 KB apart (the descriptor's LBO).
-template <int STAGES, int EPI, bool A_MN = false, bool B_MN = false>
+// BN_ = N of the pair MMA (256; 128 for the router+gate of <= 128 experts): each CTA stages
+// BN_ / 2 rows of the B tile.
+template <int STAGES, int EPI, bool A_MN = false, bool B_MN = false, int BN_ = 256>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm2sm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, const Params p) {
-    constexpr int BN = 256;
-    constexpr uint32_t TMEM_COLS = 512;
-    using S = Smem2<STAGES>;
+    constexpr int BN = BN_;
+    constexpr int BH = BN / 2;  // B rows per CTA
+    static_assert(BN == 256 || (!A_MN && !B_MN), "MN-major operands: BN = 256 only");
+    constexpr uint32_t TMEM_COLS = 2 * BN;
+    using S = Smem2<STAGES, BN>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // align within the array (not through uintptr_t) so s_off etc. stay LDS, not generic loads
     uint8_t *base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -915,6 +1065,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int i = threadIdx.x; i <= p.n_exp; i += blockDim.x) s_off[i] = p.exp_mt_off[i];
     else if (p.grouped == 2 && p.exp_perm)
         for (int i = threadIdx.x; i < p.n_exp; i += blockDim.x) s_off[i] = p.exp_perm[i];
+
+    int32_t *s_hist = s_off + kMaxExpSmem + 4;             // EPI_GATE: as in gemm_kernel
+    int32_t *s_chunk = s_hist + kGateMaxSrc * kGateMaxE;
+    float *s_bias = reinterpret_cast<float *>(s_chunk + 3 * kGateMaxE);
+    uint8_t *s_merge = reinterpret_cast<uint8_t *>(s_bias + kGateMaxE);
+    if constexpr (EPI == EPI_GATE) {
+        for (int i = threadIdx.x; i < p.gate.n_src * p.gate.E; i += blockDim.x) s_hist[i] = 0;
+        for (int i = threadIdx.x; i < BN; i += blockDim.x)  // + 0.0f: -0 -> +0 (see gate_tile)
+            s_bias[i] = i >= p.gate.E ? -__int_as_float(0x7f800000) : (p.gate.bias ? p.gate.bias[i] + 0.0f : 0.f);
+    }
 
     const uint32_t rank = cluster_ctarank();
     const bool leader = rank == 0;
@@ -955,7 +1115,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t phase = 0;
         for (int64_t t = cid; t < n_total; t += ncl) {
             const Tile tl = decode(p, t, s_off);
-            const int32_t b_row = (int32_t)(tl.expert * p.b_rows_per_exp + (int64_t)tl.n_blk * BN) + (int32_t)rank * 128;
+            const int32_t b_row = (int32_t)(tl.expert * p.b_rows_per_exp + (int64_t)tl.n_blk * BN) + (int32_t)rank * BH;
             int r[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -1001,7 +1161,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 }
                 const Tile tl = decode(p, t, s_off);
                 const int32_t a_row = tl.row0 + (int32_t)rank * 128;
-                const int32_t b_row = (int32_t)(tl.expert * p.b_rows_per_exp + (int64_t)tl.n_blk * BN) + (int32_t)rank * 128;
+                const int32_t b_row = (int32_t)(tl.expert * p.b_rows_per_exp + (int64_t)tl.n_blk * BN) + (int32_t)rank * BH;
                 // contraction offsets (gemm_kernel's): mode 2 contracts over the expert's rows;
                 // an MN-major weight is [K][N] per expert, stacked along K
                 const int32_t a_k0 = (int32_t)tl.k0;
@@ -1080,8 +1240,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
             tc_fence_after();
             const uint32_t t_row = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
             const int local_row = (int)rank * 128 + row_in_cta;
-            store_tile<BN, EPI>(p, t_row, (int64_t)tl.row0 + local_row, local_row < tl.rows, tl.n_blk, pol_out, tl.expert,
-                                tl.kb == 0, half);
+            if constexpr (EPI == EPI_GATE) {
+                // this CTA's 128 accumulator rows are tokens [row0 + 128 rank, ...): the 1-CTA
+                // kernel's gate epilogue on them
+                const int sub_rows = tl.rows - (int)rank * 128;
+                if (sub_rows > 0) {
+                    const int32_t sub0 = tl.row0 + (int32_t)rank * 128;
+                    const int nr = sub_rows < 128 ? sub_rows : 128;
+                    switch (p.gate.K) {
+#define HEP_GATE2_K(KK) \
+    case KK: gate_tile<KK, BN / 2>(p, t_row, sub0, nr, row_in_cta, half, 2, s_hist, s_chunk, s_bias, s_merge); break;
+                        HEP_GATE2_K(1) HEP_GATE2_K(2) HEP_GATE2_K(3) HEP_GATE2_K(4)
+                        HEP_GATE2_K(5) HEP_GATE2_K(6) HEP_GATE2_K(7)
+#undef HEP_GATE2_K
+                        default: gate_tile<8, BN / 2>(p, t_row, sub0, nr, row_in_cta, half, 2, s_hist, s_chunk, s_bias, s_merge); break;
+                    }
+                }
+            } else {
+                store_tile<BN, EPI>(p, t_row, (int64_t)tl.row0 + local_row, local_row < tl.rows, tl.n_blk, pol_out, tl.expert,
+                                    tl.kb == 0, half);
+            }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster_relaxed(tempty_l + 8 * acc);
@@ -1095,6 +1273,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc_2sm(tmem_base, TMEM_COLS);
+    }
+    if constexpr (EPI == EPI_GATE) {  // integer sums: order-free, deterministic
+        for (int i = threadIdx.x; i < p.gate.n_src * p.gate.E; i += blockDim.x)
+            if (s_hist[i]) atomicAdd(reinterpret_cast<unsigned long long *>(p.gate.hist) + i, (unsigned long long)s_hist[i]);
     }
 }
 
@@ -1379,6 +1561,11 @@ static bool use_pairs(int64_t R, int n_experts) {
     return n_experts > 0 && R / n_experts >= 512;
 }
 
+__global__ void zero_i64_kernel(int64_t *p, int n) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) p[i] = 0;
+}
+
 }  // namespace gemm
 }  // namespace hep
 
@@ -1438,15 +1625,75 @@ static int launch_gate(const void *x, const void *wg, int64_t T, int64_t d_model
     static_assert(S::BYTES + kGateSmemBytes <= 232448, "router+gate kernel shared memory");
     CUtensorMap ta, tb;
     const int tm = p.tile_m > 0 ? p.tile_m : BM;
+    // Wg multicast cluster size (hep_tuning.router_mc; 0 = auto): the B tile is split into
+    // mc slices of BN / mc rows, each a whole number of 8-row swizzle atoms
+    int mc = g_tuning.router_mc > 0 ? g_tuning.router_mc : 1;  // auto: off (measured slower, router_ab_r02i)
+    if (mc != 2 && mc != 4) mc = 1;
+    while (mc > 1 && BN / mc < 8) mc >>= 1;
     int rc = make_tmap(&ta, x, (uint64_t)T, (uint64_t)d_model, (uint32_t)tm);
     if (rc) return rc;
-    rc = make_tmap(&tb, wg, (uint64_t)e_pad, (uint64_t)d_model, BN);  // rows past e_pad: TMA zero fill
+    rc = make_tmap(&tb, wg, (uint64_t)e_pad, (uint64_t)d_model, (uint32_t)(BN / mc));  // rows past e_pad: zero fill
     if (rc) return rc;
     auto kern = gemm_kernel<BN, STAGES, EPI_GATE>;
     const int bytes = (int)S::BYTES + kGateSmemBytes;
     HEP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     const int64_t tiles = (T + tm - 1) / tm;
-    const int grid = (int)(tiles < sm_count() ? tiles : sm_count());
+    int grid = (int)(tiles < sm_count() ? tiles : sm_count());
+    Params q = p;
+    q.b_mc = mc;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = bytes;
+    cfg.stream = s;
+    if (mc > 1) {
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = mc;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        // whole clusters, no more than can be co-resident (a cluster lives on one GPC)
+        static int max_clusters[5] = {};  // per <BN, STAGES> instance
+        int &mcl = max_clusters[mc];
+        if (mcl == 0) {
+            cfg.gridDim = dim3((unsigned)(sm_count() / mc * mc));
+            HEP_CHECK_CUDA(cudaOccupancyMaxActiveClusters(&mcl, (void *)kern, &cfg));
+            if (mcl < 1) mcl = 1;
+        }
+        const int64_t want = (tiles + mc - 1) / mc;
+        grid = (int)(want < mcl ? want : mcl) * mc;
+    }
+    cfg.gridDim = dim3((unsigned)grid);
+    HEP_CHECK_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, q));
+    HEP_CHECK_LAUNCH();
+    return HEP_OK;
+}
+
+// Router+gate on CTA pairs (cta_group::2, M = 256 tokens per pair): each CTA stages its 128
+// token rows and HALF of the Wg tile, so a stage is 16 KB + BN * 64 B instead of 16 KB +
+// BN * 128 B and the ring keeps 1.5x (BN = 256) / 1.6x (BN = 128) more token bytes in
+// flight per SM; each CTA's TMEM holds its 128 tokens x BN logits and runs the same gate
+// epilogue.  hep_tuning.router_pair: 0 auto (E_pad > 64), 1 off, 2 on.
+template <int BN, int STAGES>
+static int launch_gate2(const void *x, const void *wg, int64_t T, int64_t d_model, int e_pad, const Params &p0,
+                        cudaStream_t s) {
+    using S = Smem2<STAGES, BN>;
+    static_assert(S::BYTES + kGateSmemBytes <= 232448, "pair router+gate kernel shared memory");
+    CUtensorMap ta, tb;
+    int rc = make_tmap(&ta, x, (uint64_t)T, (uint64_t)d_model, 128);
+    if (rc) return rc;
+    rc = make_tmap(&tb, wg, (uint64_t)e_pad, (uint64_t)d_model, BN / 2);  // rows past e_pad: TMA zero fill
+    if (rc) return rc;
+    Params p = p0;
+    p.tile_m = kPairRows;
+    p.wait_cluster = g_tuning.pair_wait_cluster == 1;
+    auto kern = gemm2sm_kernel<STAGES, EPI_GATE, false, false, BN>;
+    const int bytes = (int)S::BYTES + kGateSmemBytes;
+    HEP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    const int64_t tiles = (T + kPairRows - 1) / kPairRows;
+    const int64_t pairs = sm_count() / 2;
+    const int grid = 2 * (int)(tiles < pairs ? tiles : pairs);
     kern<<<grid, kThreads, bytes, s>>>(ta, tb, p);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
@@ -1454,6 +1701,12 @@ static int launch_gate(const void *x, const void *wg, int64_t T, int64_t d_model
 
 extern "C" int hep_gate_chunk_counts(const int32_t *d_topk_idx, int64_t T, int K, int E, int64_t tokens_per_src,
                                      int n_src, int32_t *d_chunk_cnt, void *stream);
+
+#ifdef HEP_ROUTER_STAMPS
+extern "C" int hep_diag_router_stamps(unsigned long long *out) {
+    return cudaMemcpyFromSymbol(out, hep::gemm::g_router_stamps, sizeof(hep::gemm::g_router_stamps)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 extern "C" int hep_router_topk(const void *d_x, const void *d_wg, int64_t T, int64_t d_model, int E, int e_pad,
                                const float *d_bias, int K, int64_t tokens_per_src, int n_src, float *d_logits,
@@ -1475,7 +1728,23 @@ extern "C" int hep_router_topk(const void *d_x, const void *d_wg, int64_t T, int
         if (rc || !d_chunk_cnt) return rc;
         return hep_gate_chunk_counts(d_topk_idx, T, K, E, tokens_per_src, n_src, d_chunk_cnt, stream);
     }
-    HEP_CHECK_CUDA(cudaMemsetAsync(d_hist, 0, sizeof(int64_t) * (size_t)n_src * E, s));
+#ifdef HEP_ROUTER_STAMPS
+    const int zero_mode = g_tuning.reserved[0];  // diagnostics: 0 memset, 1 zero kernel (max-smem carveout), 2 none
+#else
+    const int zero_mode = 0;
+#endif
+    if (zero_mode == 0) {
+        HEP_CHECK_CUDA(cudaMemsetAsync(d_hist, 0, sizeof(int64_t) * (size_t)n_src * E, s));
+    } else if (zero_mode == 1) {
+        static bool attr = false;
+        if (!attr) {
+            HEP_CHECK_CUDA(cudaFuncSetAttribute(hep::gemm::zero_i64_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+            attr = true;
+        }
+        const int n = n_src * E;
+        hep::gemm::zero_i64_kernel<<<(n + 255) / 256, 256, 0, s>>>(d_hist, n);
+        HEP_CHECK_LAUNCH();
+    }
     if (T <= 0) return HEP_OK;
     // chunk counts come out of the epilogue when every 64-token chunk lies inside one tile
     const bool chunks_fused = d_chunk_cnt && tokens_per_src % 64 == 0 && tokens_per_src * n_src == T;
@@ -1507,7 +1776,10 @@ extern "C" int hep_router_topk(const void *d_x, const void *d_wg, int64_t T, int
             HEP_CHECK_CUDA(cudaMemsetAsync(d_chunk_cnt, 0, sizeof(int32_t) * (size_t)n_src * p.gate.ncs * E, s));
     }
     int rc;
-    if (e_pad <= 16) rc = launch_gate<16, 8>(d_x, d_wg, T, d_model, e_pad, p, s);
+    const bool pair = tm == BM && e_pad > 64 && (g_tuning.router_pair == 2 || (g_tuning.router_pair == 0 && e_pad > 128));
+    if (pair && e_pad <= 128) rc = launch_gate2<128, 8>(d_x, d_wg, T, d_model, e_pad, p, s);
+    else if (pair) rc = launch_gate2<256, 6>(d_x, d_wg, T, d_model, e_pad, p, s);
+    else if (e_pad <= 16) rc = launch_gate<16, 8>(d_x, d_wg, T, d_model, e_pad, p, s);
     else if (e_pad <= 32) rc = launch_gate<32, 8>(d_x, d_wg, T, d_model, e_pad, p, s);
     else if (e_pad <= 64) rc = launch_gate<64, 6>(d_x, d_wg, T, d_model, e_pad, p, s);
     else if (e_pad <= 128) rc = launch_gate<128, 5>(d_x, d_wg, T, d_model, e_pad, p, s);

@@ -251,6 +251,24 @@ __device__ __forceinline__ void mma_bf16_2sm(uint32_t tmem_d, uint64_t adesc, ui
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// TMA tile load multicast to the same smem offset of every CTA in `mask` (each CTA's
+// same-offset mbarrier receives the bytes it was sent)
+__device__ __forceinline__ void tma_load_2d_mc(void *smem_dst, const void *tmap, uint64_t *bar, int32_t c0,
+                                               int32_t c1, uint16_t mask, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        ".L2::cache_hint [%0], [%1, {%3, %4}], [%2], %5, %6;" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask), "l"(policy)
+        : "memory");
+}
+// 1-CTA MMAs: arrive on the same-offset mbarrier of every CTA in `mask` once they complete
+__device__ __forceinline__ void mma_commit_mc(uint64_t *bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
 // arrive on the same-offset mbarrier of every CTA in `mask` once the pair's MMAs complete
 __device__ __forceinline__ void mma_commit_2sm_mc(uint64_t *bar, uint16_t mask) {
     asm volatile(

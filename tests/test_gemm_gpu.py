@@ -189,16 +189,21 @@ def test_grouped_ffn_light_expert_split(L, tune):
     (2048, 256, 20, 3, 10, True), (1024, 512, 48, 5, 2, False), (1024, 256, 32, 7, 4, True),
     (16384, 512, 8, 2, 8, True), (32768, 256, 128, 8, 8, True), (16384, 256, 256, 8, 8, True),
 ])
-@pytest.mark.parametrize("tile", [0, 128, 80, 48])
-def test_router_topk_fused_equals_unfused(L, T, d, E, K, G, bias, tile, tune):
+@pytest.mark.parametrize("tile,mc,pair", [(0, 0, 0), (0, 1, 1), (0, 2, 1), (0, 4, 1), (128, 1, 1), (80, 4, 0),
+                                          (48, 2, 0), (0, 0, 2)])
+def test_router_topk_fused_equals_unfused(L, T, d, E, K, G, bias, tile, mc, pair, tune):
     """hep_router_topk (gate in the router GEMM's epilogue) against the unfused chain
     hep_gemm_bf16 -> hep_gate_topk -> hep_gate_chunk_counts: logits, top-K indices,
     weights, histogram and per-64-token chunk counts bit for bit (E > 256 and K > 8 take
     the unfused path inside the same entry point).  tile = router rows per CTA tile
     (0 = the automatic all-SM split, e.g. 112 rows at 16384 tokens; 80 / 48: tiles that
     cut through 64-token chunks, whose counts then go through global atomics); the gate
-    epilogue runs on both column halves (merged through shared memory) when E_pad % 32 == 0."""
-    tune(router_tile_rows=tile)
+    epilogue runs on both column halves (merged through shared memory) when E_pad % 32 == 0.
+    mc = hep_tuning.router_mc: clusters of mc CTAs sharing each Wg tile by TMA multicast
+    (0 = auto; tile counts that are not a multiple of mc leave empty tiles in the last
+    cluster).  pair = hep_tuning.router_pair: 0 auto / 2 on = CTA pairs (256 tokens per
+    pair, half the Wg tile per CTA) for E_pad > 64, 1 = the 1-CTA kernel."""
+    tune(router_tile_rows=tile, router_mc=mc, router_pair=pair)
     dev = "cuda"
     g = torch.Generator(device=dev).manual_seed(T + E + K)
     e_pad = max(16, (E + 15) // 16 * 16)

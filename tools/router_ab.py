@@ -6,8 +6,11 @@ median µs per launch and algorithmic GB/s (x, Wg, logits, top-K) / HBM peak; ch
 that every variant produces the same top-K, histogram and chunk counts.
 
     python tools/router_ab.py [--variants 0,128] [--rounds 5] [--hot]
+    python tools/router_ab.py --variants "router_mc=1,router_mc=2,router_mc=4"
+(a variant is a tile height or "field=value[;field=value]" of hep_tuning)
 --hot: before each timed batch, run 20 ms of bf16 GEMMs (the FFN's power state)."""
 import argparse
+import ctypes
 import json
 import os
 import statistics
@@ -25,10 +28,14 @@ ap.add_argument("--variants", default="0,128")
 ap.add_argument("--rounds", type=int, default=5)
 ap.add_argument("--iters", type=int, default=30)
 ap.add_argument("--hot", action="store_true")
+ap.add_argument("--diag", action="store_true", help="load libhep_diag.so (tools/build_diag.sh)")
+ap.add_argument("--graph", action="store_true", help="time a CUDA graph of the iters launches (no host launch cost)")
 ap.add_argument("--shapes", default="mixtral,qwen3,dsv3")
 args = ap.parse_args()
 peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
     os.path.join(ROOT, "MEASURED_PEAKS.json")) else {"hbm_gbs": 6553.6}
+if args.diag:
+    L.LIB_PATH = os.path.join(ROOT, "paper_2511_16947_b200", "libhep_diag.so")
 lib = L.lib()
 s = L.stream_handle()
 base = L.get_tuning()
@@ -48,23 +55,33 @@ for name in args.shapes.split(","):
     c = torch.empty(G * (tps // 64) * E, dtype=torch.int32, device="cuda")
     nbytes = T * d * 2 + e_pad * d * 2 + T * e_pad * 4 + T * K * 8
 
-    def fused():
+    def fused(s=s):
         L.check(lib.hep_router_topk(x.data_ptr(), wg.data_ptr(), T, d, E, e_pad, b.data_ptr(), K, tps, G, lg.data_ptr(),
                                     idx.data_ptr(), w.data_ptr(), h.data_ptr(), c.data_ptr(), s), "router")
 
-    def unfused():
+    def unfused(s=s):
         lib.hep_gemm_bf16(x.data_ptr(), wg.data_ptr(), lg.data_ptr(), T, e_pad, d, 0, s)
         lib.hep_gate_topk(lg.data_ptr(), e_pad, b.data_ptr(), T, E, K, tps, G, idx.data_ptr(), w.data_ptr(),
                           h.data_ptr(), s)
         lib.hep_gate_chunk_counts(idx.data_ptr(), T, K, E, tps, G, c.data_ptr(), s)
 
-    variants = [("tile=" + v, int(v)) for v in args.variants.split(",")] + [("unfused", None)]
+    def parse_variant(v):
+        if "=" not in v:
+            return ("tile=" + v, {"router_tile_rows": int(v)})
+        return (v, {kv.split("=")[0]: int(kv.split("=")[1]) for kv in v.split(";") if not kv.startswith("zero")})
+
+    variants = [parse_variant(v) for v in args.variants.split(",")] + [("unfused", None)]
     res = {lab: [] for lab, _ in variants}
     outs = {}
     for r in range(args.rounds):
         for lab, tile in variants:
             if tile is not None:
-                L.set_tuning(**{**base, "router_tile_rows": tile})
+                L.set_tuning(**{**base, **tile})
+                zm = [int(kv.split("=")[1]) for kv in lab.split(";") if kv.startswith("zero=")]
+                t = L.HepTuning()
+                lib.hep_tuning_get(ctypes.byref(t))
+                t.reserved[0] = zm[0] if zm else 0  # diagnostics build: hist zeroing mode
+                lib.hep_tuning_set(ctypes.byref(t))
             fn = fused if tile is not None else unfused
             for _ in range(3):
                 fn()
@@ -75,11 +92,27 @@ for name in args.shapes.split(","):
                 for _ in range(10):
                     ha @ ha
             st, en = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            st.record()
-            for _ in range(args.iters):
-                fn()
-            en.record()
-            torch.cuda.synchronize()
+            if args.graph:
+                gr = torch.cuda.CUDAGraph()
+                cs = torch.cuda.Stream()
+                with torch.cuda.stream(cs):
+                    sc = L.stream_handle()
+                    gr.capture_begin()
+                    for _ in range(args.iters):
+                        fn(sc)
+                    gr.capture_end()
+                gr.replay()
+                torch.cuda.synchronize()
+                st.record()
+                gr.replay()
+                en.record()
+                torch.cuda.synchronize()
+            else:
+                st.record()
+                for _ in range(args.iters):
+                    fn()
+                en.record()
+                torch.cuda.synchronize()
             res[lab].append(st.elapsed_time(en) / args.iters * 1000)
     L.set_tuning(**base)
     ref = outs["unfused"]
