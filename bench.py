@@ -571,7 +571,8 @@ def sched_cpu_baseline(configs, n_mb=50, skip=5, seed=0, skew=1.0):
 
 def hbm_b2b_ms(layer, bufs, x, stream, n=20):
     """permute, combine and the fused router+gate, each re-launched n times back to back on
-    the micro-batch ``x`` the buffers hold (idempotent kernels), CUDA events: ms per launch."""
+    the micro-batch ``x`` the buffers hold (idempotent kernels), captured in a CUDA graph,
+    CUDA events around one replay: ms per launch."""
     import torch
 
     from paper_2511_16947_b200 import _lib
@@ -581,11 +582,20 @@ def hbm_b2b_ms(layer, bufs, x, stream, n=20):
     K, E, G = layer.K, layer.E, layer.G
 
     def b2b(fn):
+        # n launches captured in one CUDA graph (as the layer step runs), one warm replay,
+        # then a timed replay: device time per launch without host launch overhead
         fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            g.capture_begin()
+            for _ in range(n):
+                fn()
+            g.capture_end()
+        g.replay()
         q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         q0.record(stream)
-        for _ in range(n):
-            fn()
+        g.replay()
         q1.record(stream)
         torch.cuda.synchronize()
         return q0.elapsed_time(q1) / n
@@ -597,10 +607,10 @@ def hbm_b2b_ms(layer, bufs, x, stream, n=20):
     comb = b2b(lambda: _lib.check(L.hep_moe_combine(bufs.y.data_ptr(), tr.data_ptr(), bufs.topk_w.data_ptr(), T, K, d,
                                                     bufs.out.data_ptr(), cs), "combine"))
     chunk = None if layer.static_share is not None else bufs.assign_ws.data_ptr() + bufs.chunk_off
-    rg = b2b(lambda: _lib.check(L.hep_router_topk(
+    rg = b2b(lambda: _lib.check(L.hep_router_topk_ws(
         x.data_ptr(), layer.wg.data_ptr(), T, d, E, layer.e_pad, _lib.ptr(layer.gate_bias), K, T // G, G,
-        bufs.logits.data_ptr(), bufs.topk_idx.data_ptr(), bufs.topk_w.data_ptr(), bufs.hist.data_ptr(), chunk, cs),
-        "router"))
+        bufs.logits.data_ptr(), bufs.topk_idx.data_ptr(), bufs.topk_w.data_ptr(), bufs.hist.data_ptr(), chunk,
+        bufs.router_sync.data_ptr(), cs), "router"))
     return perm, comb, rg
 
 
@@ -824,7 +834,7 @@ def measure_config(cfg, args, dev, *, steps, primary):
             "traffic": traffic.get("ffn", {}).get("bytes"), "traffic_source": traffic.get("source"),
         },
         "hbm_kernels": hbm_block(hbm_b2b_before, (perm_ms, comb_ms, rg_ms), (perm_bytes, comb_bytes, rg_bytes), hbm,
-                                 traffic),
+                                 traffic, router_flops=2 * T * d * layer.e_pad, tf_burst=tf_burst),
         "e2e": {"value": e2e_value, "unit": "tokens/s", "h2d_bytes_per_step": T * d * 2,
                 "d2h_bytes_per_step": T * d * 2},
         "gpu_launches_per_step": layer.launches_per_forward(T),
@@ -844,9 +854,11 @@ def measure_config(cfg, args, dev, *, steps, primary):
     return res
 
 
-def hbm_block(before, after, nbytes, hbm, traffic):
+def hbm_block(before, after, nbytes, hbm, traffic, router_flops=None, tf_burst=None):
     """hbm_kernels: algorithmic bytes / back-to-back launch time / HBM copy peak, measured
-    before the timed region (the kernel's own rate) with the after-region figure beside."""
+    before the timed region (the kernel's own rate) with the after-region figure beside.
+    router_gate also carries its tensor-core side: the router GEMM's 2*T*d*E_pad flops (the
+    DeepSeek-V3 shape sits at the ridge point: HBM time ~ tensor time)."""
     out = {}
     for i, (name, tkey) in enumerate((("permute", "permute"), ("combine", "combine"), ("router_gate", "router_gate"))):
         gbs = nbytes[i] / (before[i] / 1e3) / 1e9
@@ -854,8 +866,16 @@ def hbm_block(before, after, nbytes, hbm, traffic):
         out[name] = {"GB/s": gbs, "frac": gbs / hbm, "us": 1e3 * before[i], "algorithmic_bytes": nbytes[i],
                      "after_timed_region": {"GB/s": gbs_after, "frac": gbs_after / hbm, "us": 1e3 * after[i]},
                      "traffic": traffic.get(tkey, {}).get("bytes")}
-    out["timing"] = ("each kernel re-launched 20x back to back on a held-out micro-batch, CUDA events; before the "
-                     "timed region (the kernel's rate) and after it (after 100 power-capped FFN steps)")
+    if router_flops and tf_burst:
+        us = out["router_gate"]["us"]
+        t_hbm, t_tc = nbytes[2] / hbm / 1e3, router_flops / tf_burst / 1e6  # µs at each peak
+        out["router_gate"]["tensor"] = {"flops": router_flops, "TFLOP/s": router_flops / us / 1e6,
+                                        "frac_of_burst": router_flops / us / 1e6 / tf_burst}
+        out["router_gate"]["roofline_us"] = {"hbm": t_hbm, "tensor": t_tc, "bound": "hbm" if t_hbm >= t_tc else "tensor",
+                                             "frac_of_bound": max(t_hbm, t_tc) / us}
+    out["timing"] = ("each kernel re-launched 20x back to back on a held-out micro-batch inside one CUDA graph, "
+                     "CUDA events around a replay; before the timed region (the kernel's rate) and after it (after "
+                     "100 power-capped FFN steps)")
     out["peak_GB/s"] = hbm
     return out
 

@@ -230,6 +230,18 @@ int hep_gate_topk(const float *d_logits, int64_t ld_logits, const float *d_bias,
 int hep_router_topk(const void *d_x, const void *d_wg, int64_t T, int64_t d_model, int E, int e_pad,
                     const float *d_bias, int K, int64_t tokens_per_src, int n_src, float *d_logits,
                     int32_t *d_topk_idx, float *d_topk_w, int64_t *d_hist, int32_t *d_chunk_cnt, void *stream);
+/*
+ * hep_router_topk without the separate zeroing launch of d_hist: the fused kernel's CTA 0
+ * zeroes it and the other CTAs add their counts once it is done, synchronised through
+ * d_sync (hep_router_sync_bytes() bytes, zeroed once by the caller; the kernel leaves them
+ * zero again, so the call can be captured in a CUDA graph and replayed).  One d_sync per
+ * concurrently running call (per layer / stream).  The unfused path ignores d_sync.
+ */
+int hep_router_topk_ws(const void *d_x, const void *d_wg, int64_t T, int64_t d_model, int E, int e_pad,
+                       const float *d_bias, int K, int64_t tokens_per_src, int n_src, float *d_logits,
+                       int32_t *d_topk_idx, float *d_topk_w, int64_t *d_hist, int32_t *d_chunk_cnt,
+                       unsigned int *d_sync, void *stream);
+size_t hep_router_sync_bytes(void);
 /* Per-64-token-chunk expert counts of a top-K assignment (the unfused producer of d_chunk_cnt). */
 int hep_gate_chunk_counts(const int32_t *d_topk_idx, int64_t T, int K, int E, int64_t tokens_per_src, int n_src,
                           int32_t *d_chunk_cnt, void *stream);

@@ -66,6 +66,8 @@ SIGNATURES = {
     "hep_gate_topk": (ctypes.c_int, [vp, ctypes.c_int64, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int, vp, vp, vp, vp]),
     "hep_gemm_bf16": (ctypes.c_int, [vp, vp, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp]),
     "hep_router_topk": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int, vp, vp, vp, vp, vp, vp]),
+    "hep_router_topk_ws": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int, vp, vp, vp, vp, vp, vp, vp]),
+    "hep_router_sync_bytes": (ctypes.c_size_t, []),
     "hep_gate_chunk_counts": (ctypes.c_int, [vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int, vp, vp]),
     "hep_moe_assign_precounted": (ctypes.c_int, [vp, ctypes.POINTER(HepSchedOut), vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, ctypes.c_int, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]),
     "hep_moe_assign_chunk_offset": (ctypes.c_size_t, [vp, ctypes.c_int64, ctypes.c_int]),

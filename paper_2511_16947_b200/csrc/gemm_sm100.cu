@@ -58,6 +58,11 @@ struct GateParams {
     float *topk_w;       // [T][K]
     int64_t *hist;       // [n_src][E], zeroed by the caller's launch sequence
     int32_t *chunk_cnt;  // [n_src][ncs][E] or null
+    // in-kernel histogram zeroing (hep_router_topk_ws): {flag, ticket}, zero between launches.
+    // CTA 0 zeroes hist, then raises flag; every CTA flushes its counts once flag is up and
+    // takes a ticket; the last ticket lowers flag and ticket again (self-resetting, so a
+    // captured graph can replay it).  null: the caller's launch sequence zeroes hist.
+    unsigned int *sync;
 };
 
 struct Params {
@@ -727,6 +732,39 @@ __device__ __forceinline__ void gate_tile(const Params &p, uint32_t t_row, int64
     }
 }
 
+// hist zeroing by CTA 0 (GateParams::sync), at kernel entry
+__device__ __forceinline__ void gate_hist_zero(const GateParams &g) {
+    if (!g.sync || blockIdx.x != 0) return;
+    for (int i = threadIdx.x; i < g.n_src * g.E; i += blockDim.x) g.hist[i] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        atomicExch(&g.sync[0], 1u);
+    }
+}
+
+// the CTA's histogram counts into hist (integer sums: order-free, deterministic); with
+// GateParams::sync, after CTA 0's zeroing and followed by the self-reset of the sync words
+__device__ __forceinline__ void gate_hist_flush(const GateParams &g, const int32_t *s_hist) {
+    if (g.sync) {
+        if (threadIdx.x == 0)
+            while (ld_acquire_gpu_u32(&g.sync[0]) == 0u) __nanosleep(32);
+        __syncthreads();
+    }
+    for (int i = threadIdx.x; i < g.n_src * g.E; i += blockDim.x)
+        if (s_hist[i]) atomicAdd(reinterpret_cast<unsigned long long *>(g.hist) + i, (unsigned long long)s_hist[i]);
+    if (g.sync) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(&g.sync[1], 1u) == gridDim.x - 1) {  // every CTA has flushed
+                atomicExch(&g.sync[0], 0u);
+                atomicExch(&g.sync[1], 0u);
+            }
+        }
+    }
+}
+
 // A_MN / B_MN: operand stored MN-major in global memory (the contraction index
 // is the row index, e.g. activations [rows][d] contracted over rows for weight
 // gradients, or weights [K][N] used untransposed).  Such an operand is staged as
@@ -760,6 +798,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = threadIdx.x; i < p.gate.n_src * p.gate.E; i += blockDim.x) s_hist[i] = 0;
         for (int i = threadIdx.x; i < BN; i += blockDim.x)  // + 0.0f: -0 -> +0 (see gate_tile)
             s_bias[i] = i >= p.gate.E ? -__int_as_float(0x7f800000) : (p.gate.bias ? p.gate.bias[i] + 0.0f : 0.f);
+        gate_hist_zero(p.gate);
     }
 
     if (threadIdx.x == 0) ROUTER_STAMP(0);
@@ -996,9 +1035,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         tmem_dealloc(tmem_base, S::TMEM_COLS);
     }
-    if constexpr (EPI == EPI_GATE) {  // integer sums: order-free, deterministic
-        for (int i = threadIdx.x; i < p.gate.n_src * p.gate.E; i += blockDim.x)
-            if (s_hist[i]) atomicAdd(reinterpret_cast<unsigned long long *>(p.gate.hist) + i, (unsigned long long)s_hist[i]);
+    if constexpr (EPI == EPI_GATE) {
+        gate_hist_flush(p.gate, s_hist);
 #ifdef HEP_ROUTER_STAMPS
         __syncthreads();
         if (threadIdx.x == 0) ROUTER_STAMP(4);
@@ -1074,6 +1112,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int i = threadIdx.x; i < p.gate.n_src * p.gate.E; i += blockDim.x) s_hist[i] = 0;
         for (int i = threadIdx.x; i < BN; i += blockDim.x)  // + 0.0f: -0 -> +0 (see gate_tile)
             s_bias[i] = i >= p.gate.E ? -__int_as_float(0x7f800000) : (p.gate.bias ? p.gate.bias[i] + 0.0f : 0.f);
+        gate_hist_zero(p.gate);
     }
 
     const uint32_t rank = cluster_ctarank();
@@ -1274,10 +1313,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         tc_fence_after();
         tmem_dealloc_2sm(tmem_base, TMEM_COLS);
     }
-    if constexpr (EPI == EPI_GATE) {  // integer sums: order-free, deterministic
-        for (int i = threadIdx.x; i < p.gate.n_src * p.gate.E; i += blockDim.x)
-            if (s_hist[i]) atomicAdd(reinterpret_cast<unsigned long long *>(p.gate.hist) + i, (unsigned long long)s_hist[i]);
-    }
+    if constexpr (EPI == EPI_GATE) gate_hist_flush(p.gate, s_hist);
 }
 
 // ---------------------------------------------------------------------------
@@ -1561,11 +1597,6 @@ static bool use_pairs(int64_t R, int n_experts) {
     return n_experts > 0 && R / n_experts >= 512;
 }
 
-__global__ void zero_i64_kernel(int64_t *p, int n) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < n) p[i] = 0;
-}
-
 }  // namespace gemm
 }  // namespace hep
 
@@ -1708,10 +1739,25 @@ extern "C" int hep_diag_router_stamps(unsigned long long *out) {
 }
 #endif
 
+extern "C" int hep_router_topk_ws(const void *d_x, const void *d_wg, int64_t T, int64_t d_model, int E, int e_pad,
+                                  const float *d_bias, int K, int64_t tokens_per_src, int n_src, float *d_logits,
+                                  int32_t *d_topk_idx, float *d_topk_w, int64_t *d_hist, int32_t *d_chunk_cnt,
+                                  unsigned int *d_sync, void *stream);
+
 extern "C" int hep_router_topk(const void *d_x, const void *d_wg, int64_t T, int64_t d_model, int E, int e_pad,
                                const float *d_bias, int K, int64_t tokens_per_src, int n_src, float *d_logits,
                                int32_t *d_topk_idx, float *d_topk_w, int64_t *d_hist, int32_t *d_chunk_cnt,
                                void *stream) {
+    return hep_router_topk_ws(d_x, d_wg, T, d_model, E, e_pad, d_bias, K, tokens_per_src, n_src, d_logits, d_topk_idx,
+                              d_topk_w, d_hist, d_chunk_cnt, nullptr, stream);
+}
+
+extern "C" size_t hep_router_sync_bytes(void) { return 16; }
+
+extern "C" int hep_router_topk_ws(const void *d_x, const void *d_wg, int64_t T, int64_t d_model, int E, int e_pad,
+                                  const float *d_bias, int K, int64_t tokens_per_src, int n_src, float *d_logits,
+                                  int32_t *d_topk_idx, float *d_topk_w, int64_t *d_hist, int32_t *d_chunk_cnt,
+                                  unsigned int *d_sync, void *stream) {
     HEP_NVTX("hep_router_topk");
     HEP_REQUIRE(d_x && d_wg && d_topk_idx && d_topk_w && d_hist, HEP_E_CONTRACT, "hep_router_topk: null pointer");
     HEP_REQUIRE(E >= 1 && K >= 1 && K <= E && e_pad >= E && e_pad % 16 == 0 && d_model % BK == 0, HEP_E_DIMENSION,
@@ -1728,23 +1774,9 @@ extern "C" int hep_router_topk(const void *d_x, const void *d_wg, int64_t T, int
         if (rc || !d_chunk_cnt) return rc;
         return hep_gate_chunk_counts(d_topk_idx, T, K, E, tokens_per_src, n_src, d_chunk_cnt, stream);
     }
-#ifdef HEP_ROUTER_STAMPS
-    const int zero_mode = g_tuning.reserved[0];  // diagnostics: 0 memset, 1 zero kernel (max-smem carveout), 2 none
-#else
-    const int zero_mode = 0;
-#endif
-    if (zero_mode == 0) {
-        HEP_CHECK_CUDA(cudaMemsetAsync(d_hist, 0, sizeof(int64_t) * (size_t)n_src * E, s));
-    } else if (zero_mode == 1) {
-        static bool attr = false;
-        if (!attr) {
-            HEP_CHECK_CUDA(cudaFuncSetAttribute(hep::gemm::zero_i64_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-            attr = true;
-        }
-        const int n = n_src * E;
-        hep::gemm::zero_i64_kernel<<<(n + 255) / 256, 256, 0, s>>>(d_hist, n);
-        HEP_CHECK_LAUNCH();
-    }
+    // the fused kernel zeroes hist itself when given the sync words (and tokens to launch for)
+    const bool zero_in_kernel = d_sync != nullptr && T > 0;
+    if (!zero_in_kernel) HEP_CHECK_CUDA(cudaMemsetAsync(d_hist, 0, sizeof(int64_t) * (size_t)n_src * E, s));
     if (T <= 0) return HEP_OK;
     // chunk counts come out of the epilogue when every 64-token chunk lies inside one tile
     const bool chunks_fused = d_chunk_cnt && tokens_per_src % 64 == 0 && tokens_per_src * n_src == T;
@@ -1766,6 +1798,7 @@ extern "C" int hep_router_topk(const void *d_x, const void *d_wg, int64_t T, int
     p.gate.topk_w = d_topk_w;
     p.gate.hist = d_hist;
     p.gate.chunk_cnt = chunks_fused ? d_chunk_cnt : nullptr;
+    p.gate.sync = zero_in_kernel ? d_sync : nullptr;
     const int tm = router_tile_rows(T);
     if (tm < BM) {
         p.tile_m = tm;

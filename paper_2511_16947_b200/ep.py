@@ -252,6 +252,7 @@ class EPRank:
                 topk_idx=torch.empty(T, K, **i32),
                 topk_w=torch.empty(T, K, dtype=torch.float32, device=dev),
                 hist_buf=torch.zeros(E + (E & 1), dtype=torch.int64, device=dev),  # 16-byte rows
+                router_sync=torch.zeros(4, dtype=torch.int32, device=dev),  # hep_router_topk_ws
                 tok_row=torch.empty(T, K, **i32),
                 seg=torch.empty(n_seg, 4, **i32),
                 counts=torch.empty(2 * G, dtype=torch.int64, device=dev),
@@ -412,9 +413,9 @@ class EPMoELayer:
             T = x.shape[0]
             b = rk.p2p_buffers(self, T)
             bs.append(b)
-            ck(L.hep_router_topk(x.data_ptr(), self.wg.data_ptr(), T, d, E, self.e_pad, _lib.ptr(self.gate_bias), K,
-                                 T, 1, b["logits"].data_ptr(), b["topk_idx"].data_ptr(), b["topk_w"].data_ptr(),
-                                 b["hist"].data_ptr(), None, s), "hep_router_topk")
+            ck(L.hep_router_topk_ws(x.data_ptr(), self.wg.data_ptr(), T, d, E, self.e_pad, _lib.ptr(self.gate_bias), K,
+                                    T, 1, b["logits"].data_ptr(), b["topk_idx"].data_ptr(), b["topk_w"].data_ptr(),
+                                    b["hist"].data_ptr(), None, b["router_sync"].data_ptr(), s), "hep_router_topk")
         sync = getattr(self.comm, "device_sync", False)
         if sync:  # histogram rows straight into every peer's hist_all, then a device barrier
             E2 = E + (E & 1)
@@ -595,9 +596,9 @@ class EPMoELayer:
             T = x.shape[0]
             b = rk.buffers(self, T)
             bs.append(b)
-            ck(L.hep_router_topk(x.data_ptr(), self.wg.data_ptr(), T, d, E, self.e_pad, _lib.ptr(self.gate_bias), K,
-                                 T, 1, b["logits"].data_ptr(), b["topk_idx"].data_ptr(), b["topk_w"].data_ptr(),
-                                 b["hist"].data_ptr(), None, s), "hep_router_topk")
+            ck(L.hep_router_topk_ws(x.data_ptr(), self.wg.data_ptr(), T, d, E, self.e_pad, _lib.ptr(self.gate_bias), K,
+                                    T, 1, b["logits"].data_ptr(), b["topk_idx"].data_ptr(), b["topk_w"].data_ptr(),
+                                    b["hist"].data_ptr(), None, b["router_sync"].data_ptr(), s), "hep_router_topk")
         hists = self.comm.all_gather([b["hist"] for b in bs])  # [G][E] on every rank
         for rk, x, b, h in zip(self.ranks, xs, bs, hists):
             T = x.shape[0]

@@ -85,6 +85,8 @@ class MoEBuffers:
         self.topk_idx = torch.empty(T, K, **i32)
         self.topk_w = torch.empty(T, K, dtype=torch.float32, device=device)
         self.hist = torch.zeros(G, E, dtype=torch.int64, device=device)
+        # hep_router_topk_ws: the router kernel zeroes hist itself through these (self-resetting)
+        self.router_sync = torch.zeros(4, dtype=torch.int32, device=device)
         self.tok_row = torch.empty(T, K, **i32)
         self.row_tok = torch.empty(max(R, 1), **i32)
         # pipelined split: [expert][phase][dst][src][rank], one segment list per phase; the two
@@ -186,10 +188,10 @@ class MoELayer(torch.nn.Module):
         st = stream if stream is not None else torch.cuda.current_stream()
         T, K, E, G = x.shape[0], self.K, self.E, self.G
         b = self.buffers(T)
-        _lib.check(L.hep_router_topk(x.data_ptr(), self.wg.data_ptr(), T, self.d, E, self.e_pad,
-                                     _lib.ptr(self.gate_bias), K, T // G, G, b.logits.data_ptr(),
-                                     b.topk_idx.data_ptr(), b.topk_w.data_ptr(), b.hist.data_ptr(), None,
-                                     st.cuda_stream), "hep_router_topk")
+        _lib.check(L.hep_router_topk_ws(x.data_ptr(), self.wg.data_ptr(), T, self.d, E, self.e_pad,
+                                        _lib.ptr(self.gate_bias), K, T // G, G, b.logits.data_ptr(),
+                                        b.topk_idx.data_ptr(), b.topk_w.data_ptr(), b.hist.data_ptr(), None,
+                                        b.router_sync.data_ptr(), st.cuda_stream), "hep_router_topk")
         _lib.check(L.hep_sched_solve(self.sched.handle, b.hist.data_ptr(), 1, E, None, HEP_SCHED_ALL,
                                      ctypes.byref(self.sched.out), st.cuda_stream), "hep_sched_solve")
         return self.sched.gpu_load
@@ -241,9 +243,9 @@ class MoELayer(torch.nn.Module):
         # into its epilogue; the logits are also written (parity tests, inspection)
         mark("router", 0)
         chunk = None if self.static_share is not None else b.assign_ws.data_ptr() + b.chunk_off
-        ck(L.hep_router_topk(x.data_ptr(), self.wg.data_ptr(), T, self.d, E, self.e_pad, _lib.ptr(self.gate_bias), K,
-                             tps, G, b.logits.data_ptr(), b.topk_idx.data_ptr(), b.topk_w.data_ptr(),
-                             b.hist.data_ptr(), chunk, s), "hep_router_topk")
+        ck(L.hep_router_topk_ws(x.data_ptr(), self.wg.data_ptr(), T, self.d, E, self.e_pad, _lib.ptr(self.gate_bias),
+                                K, tps, G, b.logits.data_ptr(), b.topk_idx.data_ptr(), b.topk_w.data_ptr(),
+                                b.hist.data_ptr(), chunk, b.router_sync.data_ptr(), s), "hep_router_topk")
         mark("router", 1)
         mark("gate", 0)  # fused into the router kernel
         mark("gate", 1)

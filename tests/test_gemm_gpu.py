@@ -248,3 +248,56 @@ def test_router_topk_fused_equals_unfused(L, T, d, E, K, G, bias, tile, mc, pair
                                     i2.data_ptr(), w2.data_ptr(), h2.data_ptr(), c2.data_ptr(), s), "router_topk")
         torch.cuda.synchronize()
         assert torch.equal(i0, i2) and torch.equal(w0, w2) and torch.equal(h0, h2) and torch.equal(c0, c2)
+
+
+@pytest.mark.parametrize("T,d,E,K,G,pair", [(4096, 512, 8, 2, 4, 0), (8192, 512, 128, 8, 8, 0),
+                                            (4096, 768, 256, 8, 8, 0), (4096, 768, 256, 8, 8, 1), (3000, 256, 40, 6, 3, 0)])
+def test_router_topk_ws_zeroes_in_kernel(L, T, d, E, K, G, pair, tune):
+    """hep_router_topk_ws (the kernel's CTA 0 zeroes the histogram, the others add after it,
+    self-resetting sync words) equals hep_router_topk (separate zeroing launch) on a histogram
+    buffer full of garbage, leaves the sync words zero, and replays inside a CUDA graph."""
+    tune(router_pair=pair)
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(T + E)
+    e_pad = max(16, (E + 15) // 16 * 16)
+    x = torch.randn(T, d, generator=g, device=dev).to(torch.bfloat16)
+    wg = torch.zeros(max(64, e_pad), d, dtype=torch.bfloat16, device=dev)
+    wg[:E] = (torch.randn(E, d, generator=g, device=dev) / d ** 0.5).to(torch.bfloat16)
+    tps = (T + G - 1) // G
+    lib, s = L.lib(), L.stream_handle()
+    assert int(lib.hep_router_sync_bytes()) <= 16
+
+    def run(ws, h, sync=None, stream=s):
+        lg = torch.empty(T, e_pad, device=dev)
+        i = torch.empty(T, K, dtype=torch.int32, device=dev)
+        w = torch.empty(T, K, device=dev)
+        if ws:
+            L.check(lib.hep_router_topk_ws(x.data_ptr(), wg.data_ptr(), T, d, E, e_pad, None, K, tps, G, lg.data_ptr(),
+                                           i.data_ptr(), w.data_ptr(), h.data_ptr(), None, sync.data_ptr(), stream), "ws")
+        else:
+            L.check(lib.hep_router_topk(x.data_ptr(), wg.data_ptr(), T, d, E, e_pad, None, K, tps, G, lg.data_ptr(),
+                                        i.data_ptr(), w.data_ptr(), h.data_ptr(), None, stream), "router")
+        return i, w
+
+    h0 = torch.full((G, E), 12345, dtype=torch.int64, device=dev)
+    i0, w0 = run(False, h0)
+    sync = torch.zeros(4, dtype=torch.int32, device=dev)
+    for _ in range(3):
+        h1 = torch.full((G, E), -777, dtype=torch.int64, device=dev)
+        i1, w1 = run(True, h1, sync)
+        torch.cuda.synchronize()
+        assert torch.equal(h0, h1) and torch.equal(i0, i1) and torch.equal(w0, w1)
+        assert int(sync.abs().sum()) == 0
+    h2 = torch.full((G, E), 99, dtype=torch.int64, device=dev)
+    gr = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    with torch.cuda.stream(cs):
+        gr.capture_begin()
+        run(True, h2, sync, stream=cs.cuda_stream)
+        gr.capture_end()
+    for _ in range(3):
+        h2.fill_(-5)
+        gr.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(h0, h2)
+        assert int(sync.abs().sum()) == 0

@@ -7,10 +7,10 @@ that every variant produces the same top-K, histogram and chunk counts.
 
     python tools/router_ab.py [--variants 0,128] [--rounds 5] [--hot]
     python tools/router_ab.py --variants "router_mc=1,router_mc=2,router_mc=4"
-(a variant is a tile height or "field=value[;field=value]" of hep_tuning)
+(a variant is a tile height or "field=value[;field=value]" of hep_tuning; "ws=1": through
+hep_router_topk_ws, the histogram zeroed inside the kernel)
 --hot: before each timed batch, run 20 ms of bf16 GEMMs (the FFN's power state)."""
 import argparse
-import ctypes
 import json
 import os
 import statistics
@@ -55,7 +55,15 @@ for name in args.shapes.split(","):
     c = torch.empty(G * (tps // 64) * E, dtype=torch.int32, device="cuda")
     nbytes = T * d * 2 + e_pad * d * 2 + T * e_pad * 4 + T * K * 8
 
+    sync = torch.zeros(4, dtype=torch.int32, device="cuda")
+    use_ws = [False]
+
     def fused(s=s):
+        if use_ws[0]:  # in-kernel histogram zeroing (self-resetting sync words)
+            L.check(lib.hep_router_topk_ws(x.data_ptr(), wg.data_ptr(), T, d, E, e_pad, b.data_ptr(), K, tps, G,
+                                           lg.data_ptr(), idx.data_ptr(), w.data_ptr(), h.data_ptr(), c.data_ptr(),
+                                           sync.data_ptr(), s), "router")
+            return
         L.check(lib.hep_router_topk(x.data_ptr(), wg.data_ptr(), T, d, E, e_pad, b.data_ptr(), K, tps, G, lg.data_ptr(),
                                     idx.data_ptr(), w.data_ptr(), h.data_ptr(), c.data_ptr(), s), "router")
 
@@ -68,7 +76,7 @@ for name in args.shapes.split(","):
     def parse_variant(v):
         if "=" not in v:
             return ("tile=" + v, {"router_tile_rows": int(v)})
-        return (v, {kv.split("=")[0]: int(kv.split("=")[1]) for kv in v.split(";") if not kv.startswith("zero")})
+        return (v, {kv.split("=")[0]: int(kv.split("=")[1]) for kv in v.split(";") if not kv.startswith("ws")})
 
     variants = [parse_variant(v) for v in args.variants.split(",")] + [("unfused", None)]
     res = {lab: [] for lab, _ in variants}
@@ -77,11 +85,8 @@ for name in args.shapes.split(","):
         for lab, tile in variants:
             if tile is not None:
                 L.set_tuning(**{**base, **tile})
-                zm = [int(kv.split("=")[1]) for kv in lab.split(";") if kv.startswith("zero=")]
-                t = L.HepTuning()
-                lib.hep_tuning_get(ctypes.byref(t))
-                t.reserved[0] = zm[0] if zm else 0  # diagnostics build: hist zeroing mode
-                lib.hep_tuning_set(ctypes.byref(t))
+                use_ws[0] = "ws=1" in lab
+
             fn = fused if tile is not None else unfused
             for _ in range(3):
                 fn()
