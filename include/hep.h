@@ -398,6 +398,11 @@ int hep_ipc_close(void *d_ptr);
  * negative rows are skipped, and a token with no non-negative row is not read. */
 int hep_moe_permute(const void *d_x, const int32_t *d_tok_row, int64_t T, int K, int64_t d_model, void *d_rows,
                     void *stream);
+/* hep_moe_permute with at most blocks_per_sm (1..8) resident 256-thread blocks per SM (8 fills
+ * every SM): the pipelined split's static-phase permute leaves room for the scheduled phase's
+ * solve / assignment kernels on the other stream. */
+int hep_moe_permute_ex(const void *d_x, const int32_t *d_tok_row, int64_t T, int K, int64_t d_model, void *d_rows,
+                       int blocks_per_sm, void *stream);
 
 /*
  * K6 expert FFN as grouped GEMM (tcgen05/TMEM/TMA, SwiGLU fused in the first

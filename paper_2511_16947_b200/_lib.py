@@ -78,6 +78,7 @@ SIGNATURES = {
     "hep_moe_assign_ep_workspace": (ctypes.c_size_t, [vp, ctypes.c_int64, ctypes.c_int]),
     "hep_sched_hosted": (ctypes.c_int, [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     "hep_moe_permute": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, vp, vp]),
+    "hep_moe_permute_ex": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, vp, ctypes.c_int, vp]),
     "hep_moe_expert_ffn": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp, vp, vp, ctypes.c_size_t, vp, vp]),
     "hep_moe_expert_ffn_gather": (ctypes.c_int, [vp, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp, vp, vp, ctypes.c_size_t, vp, vp]),
     "hep_ffn_debug_clock": (ctypes.c_int, [c_i64p]),

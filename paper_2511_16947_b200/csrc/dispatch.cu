@@ -578,12 +578,12 @@ __global__ void __launch_bounds__(256) combine_kernel(const int4 *__restrict__ y
     }
 }
 
-static int grid_for_warps(int64_t T) {
+static int grid_for_warps(int64_t T, int blocks_per_sm = 8) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t want = (T + 7) / 8;  // 8 warps per block
-    const int64_t cap = (int64_t)sms * 8;
+    const int64_t cap = (int64_t)sms * blocks_per_sm;
     const int64_t g = want < cap ? want : cap;
     return (int)(g > 1 ? g : 1);
 }
@@ -697,20 +697,27 @@ extern "C" int hep_moe_assign_phase(hep_sched_t h, const hep_sched_out *sched, c
                        d_row_tok, d_seg, d_expert_rows, workspace, workspace_bytes, stream, d_tok_row_phase);
 }
 
-extern "C" int hep_moe_permute(const void *d_x, const int32_t *d_tok_row, int64_t T, int K, int64_t d_model,
-                               void *d_rows, void *stream) {
+extern "C" int hep_moe_permute_ex(const void *d_x, const int32_t *d_tok_row, int64_t T, int K, int64_t d_model,
+                                  void *d_rows, int blocks_per_sm, void *stream) {
     HEP_NVTX("hep_moe_permute");
     HEP_REQUIRE(d_x && d_tok_row && d_rows, HEP_E_CONTRACT, "hep_moe_permute: null pointer");
     HEP_REQUIRE(d_model % 8 == 0 && K >= 1 && K <= 16, HEP_E_DIMENSION, "hep_moe_permute: d_model %% 8, K<=16");
+    HEP_REQUIRE(blocks_per_sm >= 1 && blocks_per_sm <= 8, HEP_E_CONTRACT, "hep_moe_permute: blocks_per_sm 1..8");
     if (T <= 0) return HEP_OK;
+    const int grid = grid_for_warps(T, blocks_per_sm);
     if (use_lsu256(d_x, d_rows, nullptr, d_model))
-        permute_v8_kernel<<<grid_for_warps(T), 256, 0, (cudaStream_t)stream>>>(
-            (const V8 *)d_x, d_tok_row, T, K, d_model / 16, (V8 *)d_rows);
+        permute_v8_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const V8 *)d_x, d_tok_row, T, K, d_model / 16,
+                                                                   (V8 *)d_rows);
     else
-        permute_kernel<<<grid_for_warps(T), 256, 0, (cudaStream_t)stream>>>(
-            (const int4 *)d_x, d_tok_row, T, K, d_model / 8, (int4 *)d_rows);
+        permute_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((const int4 *)d_x, d_tok_row, T, K, d_model / 8,
+                                                                (int4 *)d_rows);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
+}
+
+extern "C" int hep_moe_permute(const void *d_x, const int32_t *d_tok_row, int64_t T, int K, int64_t d_model,
+                               void *d_rows, void *stream) {
+    return hep_moe_permute_ex(d_x, d_tok_row, T, K, d_model, d_rows, 8, stream);
 }
 
 extern "C" int hep_moe_combine(const void *d_y, const int32_t *d_tok_row, const float *d_topk_w, int64_t T, int K,

@@ -165,6 +165,10 @@ class MoELayer(torch.nn.Module):
             # phase is solved (simulator.py:451-453); events fork and join it
             self._side = torch.cuda.Stream(device=self.device)
             self._ev_join = torch.cuda.Event()
+        # pipelined split: resident 256-thread blocks per SM of the static phase's permute (8 =
+        # all; fewer leave room for the scheduled phase's solve and assignment, which run
+        # concurrently on the main stream)
+        self.static_permute_blocks_per_sm = 8  # measured: fewer does not shorten the chain (profiles/r02/pipelined_timeline_r02i.txt)
 
     def set_placement(self, placement: Placement) -> None:
         """Adopt a new placement (adaptive replacement, ``adaptive.py``).  The
@@ -222,10 +226,12 @@ class MoELayer(torch.nn.Module):
         self.run(x, b, stream)
         return b.out
 
-    def run(self, x: torch.Tensor, b: MoEBuffers, stream=None, events: dict | None = None) -> None:
+    def run(self, x: torch.Tensor, b: MoEBuffers, stream=None, events: dict | None = None,
+            dispatch_only: bool = False) -> None:
         """Launch the whole forward chain on `stream`.  ``events`` optionally maps
         a stage name ("router", "gate", "sched", "assign", "permute", "ffn",
-        "combine") to a (start, end) pair of torch.cuda.Event recorded around it."""
+        "combine") to a (start, end) pair of torch.cuda.Event recorded around it.
+        ``dispatch_only``: stop after the permute (timing of the scheduling chain)."""
         L = _lib.lib()
         st = stream if stream is not None else torch.cuda.current_stream()
         s = st.cuda_stream
@@ -287,7 +293,9 @@ class MoELayer(torch.nn.Module):
                                       b.assign_ws2.data_ptr(), b.assign_ws2.numel(), ss),
                "hep_moe_assign_phase(static)")
             if not self.fuse_permute:
-                ck(L.hep_moe_permute(x.data_ptr(), tr0, T, K, self.d, b.rows.data_ptr(), ss), "hep_moe_permute(static)")
+                # capped occupancy: SM room for the solve / assignment running on the main stream
+                ck(L.hep_moe_permute_ex(x.data_ptr(), tr0, T, K, self.d, b.rows.data_ptr(),
+                                        self.static_permute_blocks_per_sm, ss), "hep_moe_permute(static)")
             self._ev_join.record(side)
             tr1 = None if self.fuse_permute else b.tok_row_ph[1].data_ptr()
             ck(L.hep_moe_assign_phase(self.sched.handle, ctypes.byref(self.sched.out), split, 1,
@@ -301,6 +309,8 @@ class MoELayer(torch.nn.Module):
                 ck(L.hep_moe_permute(x.data_ptr(), tr1, T, K, self.d, b.rows.data_ptr(), s), "hep_moe_permute(scheduled)")
             st.wait_event(self._ev_join)  # both phases' rows and segments are in place
             mark("permute", 1)
+        if dispatch_only:
+            return
         mark("ffn", 0)
         if self.fuse_permute:  # K5 fused into GEMM 1: x rows gathered by TMA through row_tok
             ck(L.hep_moe_expert_ffn_gather(x.data_ptr(), T, b.row_tok.data_ptr(), self.w13.data_ptr(),
@@ -323,10 +333,11 @@ class MoELayer(torch.nn.Module):
                              b.out.data_ptr(), s), "hep_moe_combine")
         mark("combine", 1)
 
-    def capture(self, x: torch.Tensor) -> "torch.cuda.CUDAGraph":
+    def capture(self, x: torch.Tensor, dispatch_only: bool = False) -> "torch.cuda.CUDAGraph":
         """Record one forward on ``x`` (fixed buffers, no host sync anywhere in the
         chain) as a CUDA graph; ``graph.replay()`` re-runs all 11 kernels with one
-        launch.  ``x`` must stay the input tensor (refill it in place)."""
+        launch.  ``x`` must stay the input tensor (refill it in place).
+        ``dispatch_only``: the chain up to the permute only (see ``run``)."""
         b = self.buffers(x.shape[0])
         side = torch.cuda.Stream(device=self.device)
         side.wait_stream(torch.cuda.current_stream())
@@ -336,7 +347,7 @@ class MoELayer(torch.nn.Module):
         torch.cuda.synchronize(self.device)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=side):
-            self.run(x, b, side)
+            self.run(x, b, side, dispatch_only=dispatch_only)
         return g
 
     # kernels launched per forward: router GEMM + gate epilogue, scheduler, assign x3
