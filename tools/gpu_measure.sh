@@ -29,7 +29,7 @@ timeout 600 ncu --set full --clock-control none --import-source on --kernel-name
   -k regex:"gemm2sm_kernel|gemm_kernel|sched_kernel|permute|combine|chunk_map|plan_prep" -c 9 \
   -o gpurun_out/prof_mixtral_$R python bench.py --config mixtral --profile --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_mixtral_$R.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k regex:"gemm2sm_kernel|gemm_kernel<.int.256|sched_kernel|permute|combine" -c 7 \
+  -k regex:"gemm2sm_kernel|gemm_kernel<.int.256|sched_kernel|permute|combine" -c 8 \
   -o gpurun_out/prof_dsv3_$R python bench.py --config dsv3 --profile --steps 1 --warmup 0 --no-cpu-baseline > gpurun_out/ncu_dsv3_$R.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
   -k regex:"gemm2sm_kernel" -c 2 \
@@ -37,11 +37,21 @@ timeout 600 ncu --set full --clock-control none --import-source on --kernel-name
 timeout 600 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
   -k regex:"gemm2sm_kernel" --launch-skip 6 -c 6 \
   -o gpurun_out/prof_train_qwen3_$R python tools/train_step.py --config qwen3 --iters 2 > gpurun_out/ncu_train_qwen3_$R.log 2>&1
+# K1 router+gate: back-to-back A/B inside CUDA graphs (memset vs in-kernel histogram zeroing,
+# 1-CTA vs CTA pairs), per-CTA timeline (diagnostics build, tools/build_diag.sh), and one full
+# ncu capture per shape
+timeout 300 python tools/router_ab.py --variants "router_pair=1,router_pair=2,ws=1" --graph --rounds 5 > gpurun_out/router_ab_$R.txt 2>&1
+timeout 200 python tools/router_stamps.py > gpurun_out/router_stamps_$R.txt 2>&1
+for c in mixtral qwen3 dsv3; do
+  timeout 300 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"gemm" \
+    --launch-skip 3 -c 1 -o gpurun_out/prof_router_${c}_$R python tools/router_one.py $c 5 > /dev/null 2>&1
+done
 # summarise the full captures on the box (copy-back is capped at 64 MiB) and drop the reports
 for r in gpurun_out/prof_*_$R.ncu-rep; do
   python tools/ncu_summary.py $r > ${r%.ncu-rep}.md 2>&1
 done
 python tools/ncu_hot.py gpurun_out/prof_qwen3_$R.ncu-rep gemm2sm 30 1 > gpurun_out/hot_qwen3_gemm2_$R.txt 2>&1
 python tools/ncu_hot.py gpurun_out/prof_train_qwen3_$R.ncu-rep gemm2sm 30 2 > gpurun_out/hot_train_qwen3_dgrad_$R.txt 2>&1
+python tools/ncu_hot.py gpurun_out/prof_router_dsv3_$R.ncu-rep gemm 30 > gpurun_out/hot_router_dsv3_$R.txt 2>&1
 rm -f gpurun_out/prof_*_$R.ncu-rep
 echo done

@@ -49,7 +49,7 @@ def summarise(path, tracked_dir=None):
             }
             break
     for key, pat in (("permute", r"permute(_v8)?_kernel"), ("combine", r"combine(_v8)?_kernel"), ("sched", "sched_kernel"),
-                     ("router_gate", r"gemm_kernel<\d+, \d+, 4,")):
+                     ("router_gate", r"gemm_kernel<\d+, \d+, 4,|gemm2sm_kernel<\d+, 4,")):
         for k in ks:
             if re.search(pat, k["name"]):
                 out[key] = {"bytes": k.get("dram__bytes_read.sum", 0) + k.get("dram__bytes_write.sum", 0),
