@@ -584,30 +584,32 @@ def hbm_b2b_ms(layer, bufs, x, stream, n=20):
     def b2b(fn):
         # n launches captured in one CUDA graph (as the layer step runs), one warm replay,
         # then a timed replay: device time per launch without host launch overhead
-        fn()
+        fn(stream.cuda_stream)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
-        with torch.cuda.stream(stream):
+        cap = torch.cuda.Stream()  # capture needs a non-default stream
+        with torch.cuda.stream(cap):
             g.capture_begin()
             for _ in range(n):
-                fn()
+                fn(cap.cuda_stream)
             g.capture_end()
-        g.replay()
-        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        q0.record(stream)
-        g.replay()
-        q1.record(stream)
+        torch.cuda.synchronize()
+        with torch.cuda.stream(cap):
+            g.replay()
+            q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            q0.record(cap)
+            g.replay()
+            q1.record(cap)
         torch.cuda.synchronize()
         return q0.elapsed_time(q1) / n
 
-    cs = stream.cuda_stream
     tr = bufs.tok_row if layer.static_share is None else bufs.tok_row
-    perm = b2b(lambda: _lib.check(L.hep_moe_permute(x.data_ptr(), tr.data_ptr(), T, K, d, bufs.rows.data_ptr(), cs),
-                                  "permute"))
-    comb = b2b(lambda: _lib.check(L.hep_moe_combine(bufs.y.data_ptr(), tr.data_ptr(), bufs.topk_w.data_ptr(), T, K, d,
-                                                    bufs.out.data_ptr(), cs), "combine"))
+    perm = b2b(lambda cs: _lib.check(L.hep_moe_permute(x.data_ptr(), tr.data_ptr(), T, K, d, bufs.rows.data_ptr(), cs),
+                                     "permute"))
+    comb = b2b(lambda cs: _lib.check(L.hep_moe_combine(bufs.y.data_ptr(), tr.data_ptr(), bufs.topk_w.data_ptr(), T, K,
+                                                       d, bufs.out.data_ptr(), cs), "combine"))
     chunk = None if layer.static_share is not None else bufs.assign_ws.data_ptr() + bufs.chunk_off
-    rg = b2b(lambda: _lib.check(L.hep_router_topk_ws(
+    rg = b2b(lambda cs: _lib.check(L.hep_router_topk_ws(
         x.data_ptr(), layer.wg.data_ptr(), T, d, E, layer.e_pad, _lib.ptr(layer.gate_bias), K, T // G, G,
         bufs.logits.data_ptr(), bufs.topk_idx.data_ptr(), bufs.topk_w.data_ptr(), bufs.hist.data_ptr(), chunk,
         bufs.router_sync.data_ptr(), cs), "router"))
@@ -664,8 +666,12 @@ def measure_config(cfg, args, dev, *, steps, primary):
     bufs = layer.buffers(T)
 
     # --- the HBM-bound kernels' own rate, measured before the long power-capped timed region
-    # (the kernel's capability; the same measurement after it is reported beside)
+    # (the kernel's capability; the same measurement after it is reported beside).  The
+    # warm-up's FFN work leaves the GPU power-capped for a while: rest 0.5 s first so this
+    # figure is taken at the nominal clock
     layer.run(unseen[0], bufs, stream)
+    torch.cuda.synchronize()
+    time.sleep(0.5)
     hbm_b2b_before = hbm_b2b_ms(layer, bufs, unseen[0], stream)
     layer.run(unseen[0], bufs, stream)
     torch.cuda.synchronize()
@@ -874,8 +880,8 @@ def hbm_block(before, after, nbytes, hbm, traffic, router_flops=None, tf_burst=N
         out["router_gate"]["roofline_us"] = {"hbm": t_hbm, "tensor": t_tc, "bound": "hbm" if t_hbm >= t_tc else "tensor",
                                              "frac_of_bound": max(t_hbm, t_tc) / us}
     out["timing"] = ("each kernel re-launched 20x back to back on a held-out micro-batch inside one CUDA graph, "
-                     "CUDA events around a replay; before the timed region (the kernel's rate) and after it (after "
-                     "100 power-capped FFN steps)")
+                     "CUDA events around a replay; before the timed region after a 0.5 s rest (the kernel's rate at "
+                     "the nominal clock) and right after it (after the power-capped FFN steps: the in-step rate)")
     out["peak_GB/s"] = hbm
     return out
 

@@ -17,7 +17,8 @@ from paper_2511_16947_b200 import _lib as L  # noqa: E402
 L.LIB_PATH = os.path.join(ROOT, "paper_2511_16947_b200", "libhep_diag.so")
 SHAPES = {"mixtral": (16384, 4096, 8, 2), "qwen3": (32768, 2048, 128, 8), "dsv3": (16384, 7168, 256, 8)}
 names = [a for a in sys.argv[1:] if "=" not in a] or list(SHAPES)
-L.set_tuning(**{kv.split("=")[0]: int(kv.split("=")[1]) for kv in sys.argv[1:] if "=" in kv})
+# the stamps are compiled into the 1-CTA kernel only (router_pair=1; DSv3 would take the pair kernel)
+L.set_tuning(**{"router_pair": 1, **{kv.split("=")[0]: int(kv.split("=")[1]) for kv in sys.argv[1:] if "=" in kv}})
 lib, s = L.lib(), L.stream_handle()
 fn = lib.hep_diag_router_stamps
 fn.argtypes = [ctypes.c_void_p]
