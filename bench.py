@@ -571,8 +571,8 @@ def sched_cpu_baseline(configs, n_mb=50, skip=5, seed=0, skew=1.0):
 
 def hbm_b2b_ms(layer, bufs, x, stream, n=20):
     """permute, combine and the fused router+gate, each re-launched n times back to back on
-    the micro-batch ``x`` the buffers hold (idempotent kernels), captured in a CUDA graph,
-    CUDA events around one replay: ms per launch."""
+    the micro-batch ``x`` the buffers hold (idempotent kernels), captured in a CUDA graph;
+    5 warm replays, then the median of 5 timed replays (CUDA events): ms per launch."""
     import torch
 
     from paper_2511_16947_b200 import _lib
@@ -594,14 +594,18 @@ def hbm_b2b_ms(layer, bufs, x, stream, n=20):
                 fn(cap.cuda_stream)
             g.capture_end()
         torch.cuda.synchronize()
+        times = []
         with torch.cuda.stream(cap):
-            g.replay()
-            q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            q0.record(cap)
-            g.replay()
-            q1.record(cap)
+            for _ in range(5):  # clocks up (the GPU idles down during the rest before this)
+                g.replay()
+            for _ in range(5):
+                q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                q0.record(cap)
+                g.replay()
+                q1.record(cap)
+                times.append((q0, q1))
         torch.cuda.synchronize()
-        return q0.elapsed_time(q1) / n
+        return statistics.median(a.elapsed_time(b) for a, b in times) / n
 
     tr = bufs.tok_row if layer.static_share is None else bufs.tok_row
     perm = b2b(lambda cs: _lib.check(L.hep_moe_permute(x.data_ptr(), tr.data_ptr(), T, K, d, bufs.rows.data_ptr(), cs),
@@ -880,7 +884,7 @@ def hbm_block(before, after, nbytes, hbm, traffic, router_flops=None, tf_burst=N
         out["router_gate"]["roofline_us"] = {"hbm": t_hbm, "tensor": t_tc, "bound": "hbm" if t_hbm >= t_tc else "tensor",
                                              "frac_of_bound": max(t_hbm, t_tc) / us}
     out["timing"] = ("each kernel re-launched 20x back to back on a held-out micro-batch inside one CUDA graph, "
-                     "CUDA events around a replay; before the timed region after a 0.5 s rest (the kernel's rate at "
+                     "median of 5 timed replays after 5 warm ones; before the timed region after a 0.5 s rest (the kernel's rate at "
                      "the nominal clock) and right after it (after the power-capped FFN steps: the in-step rate)")
     out["peak_GB/s"] = hbm
     return out
