@@ -664,9 +664,9 @@ __device__ __forceinline__ void gate_tile(const Params &p, uint32_t t_row, int64
     // ---- pass 2: the selected experts, ascending, into the shared list -----------------
     // Fast path: one compare per column into a 16-bit mask of the columns with key >= vK;
     // their expert ids and logits (pick16) go to the list.  That set is exactly the
-    // selection unless a half
-    // holds more vK-keyed columns than its quota (exact score ties at the K-th place): then
-    // its count overshoots `lim`, and the whole tile reruns the exact scan below.
+    // selection unless a half holds more vK-keyed columns than its quota (exact score ties
+    // at the K-th place): then its count overshoots `lim`, and the whole tile reruns the
+    // exact scan below.
     int cnt = offset;
     bool exact = false;
     {
@@ -789,8 +789,15 @@ __device__ __forceinline__ void gate_hist_zero(const GateParams &g) {
 // GateParams::sync, after CTA 0's zeroing and followed by the self-reset of the sync words
 __device__ __forceinline__ void gate_hist_flush(const GateParams &g, const int32_t *s_hist) {
     if (g.sync) {
-        if (threadIdx.x == 0)
-            while (ld_acquire_gpu_u32(&g.sync[0]) == 0u) __nanosleep(32);
+        // CTA 0 is dispatched first and zeroes at entry, long before any CTA gets here; the
+        // wait is bounded anyway (a grid that cannot run its CTA 0 fails loudly, not silently)
+        if (threadIdx.x == 0) {
+            const uint64_t t0 = globaltimer_ns();
+            while (ld_acquire_gpu_u32(&g.sync[0]) == 0u) {
+                __nanosleep(32);
+                if (globaltimer_ns() - t0 > 200000000ull) __trap();
+            }
+        }
         __syncthreads();
     }
     for (int i = threadIdx.x; i < g.n_src * g.E; i += blockDim.x)
