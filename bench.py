@@ -805,6 +805,19 @@ def measure_config(cfg, args, dev, *, steps, primary):
     comb_bytes = T * K * d * 2 + T * K * 4 * 2 + T * d * 2
     rg_bytes = T * d * 2 + layer.e_pad * d * 2 + T * layer.e_pad * 4 + T * K * 8  # x, Wg, logits, top-K
     traffic = load_traffic(cfg)
+    # per-expert roofline: every expert's two GEMMs at its own bound -- tensor (6dF flop per
+    # row at the sustained peak) or HBM (its weights once + its rows' X / H / Y at the copy
+    # peak).  Experts with few rows (DeepSeek-V3's long tail) are weight-streaming bound, so
+    # this is the FFN's time floor when experts are processed one after another
+    er = bufs.expert_rows.cpu().tolist()
+    rows_e = [er[e + 1] - er[e] for e in range(E)]
+    t_e = [max(6.0 * d * F * r / (tf_sus * 1e12), (3.0 * d * F * 2 + r * (4.0 * d + 4.0 * F)) / (hbm * 1e9))
+           for r in rows_e if r > 0]
+    per_expert = {"ms": 1e3 * sum(t_e), "frac": 1e3 * sum(t_e) / ffn_ms,
+                  "hbm_bound_experts": sum(1 for r in rows_e if r > 0 and
+                                           6.0 * d * F * r / (tf_sus * 1e12) < (3.0 * d * F * 2 + r * (4.0 * d + 4.0 * F)) / (hbm * 1e9)),
+                  "experts_with_rows": sum(1 for r in rows_e if r > 0),
+                  "rows_min_max": [min(rows_e), max(rows_e)]}
     res = {
         "value": value, "ms_per_step": ms_per_step, "steps": steps,
         "config": {"workload": CONFIG_TEXT[cfg], "tokens_per_microbatch_per_gpu": T, "sim_ep": G,
@@ -842,6 +855,7 @@ def measure_config(cfg, args, dev, *, steps, primary):
             # minimal DRAM bytes of one launch: every weight once, X read, H written + read, Y written
             "algorithmic_bytes_per_launch": E * 3 * d * F * 2 + R * d * 2 * 2 + R * F * 2 * 2,
             "traffic": traffic.get("ffn", {}).get("bytes"), "traffic_source": traffic.get("source"),
+            "per_expert_roofline": per_expert,
         },
         "hbm_kernels": hbm_block(hbm_b2b_before, (perm_ms, comb_ms, rg_ms), (perm_bytes, comb_bytes, rg_bytes), hbm,
                                  traffic, router_flops=2 * T * d * layer.e_pad, tf_burst=tf_burst),
@@ -1013,7 +1027,8 @@ def main():
             o = measure_config(c, args, dev, steps=args.other_steps, primary=False)
             others[c] = {k: o[k] for k in OTHER_KEYS}
             others[c]["roofline"] = {k: o["roofline"][k] for k in ("achieved", "peak", "unit", "frac",
-                                                                   "frac_of_burst_peak", "traffic")}
+                                                                   "frac_of_burst_peak", "traffic",
+                                                                   "per_expert_roofline")}
             others[c]["hbm_kernels"] = {k: {"GB/s": v["GB/s"], "frac": v["frac"]}
                                         for k, v in o["hbm_kernels"].items() if isinstance(v, dict)}
             others[c]["workload"] = o["config"]["workload"]
