@@ -301,3 +301,44 @@ def test_router_topk_ws_zeroes_in_kernel(L, T, d, E, K, G, pair, tune):
         torch.cuda.synchronize()
         assert torch.equal(h0, h2)
         assert int(sync.abs().sum()) == 0
+
+
+@pytest.mark.parametrize("T,d,E,K,G", [(16384, 4096, 8, 2, 8), (32768, 2048, 128, 8, 8), (16384, 7168, 256, 8, 8)])
+def test_router_topk_ws_fullsize_equals_unfused(L, T, d, E, K, G):
+    """The BASELINE shapes (Mixtral / Qwen3 / DeepSeek-V3) with the default launch tuning
+    (DeepSeek-V3 on the CTA-pair router kernel) through hep_router_topk_ws, the entry point
+    the layer uses, against the unfused chain: logits, top-K, weights, histogram and chunk
+    counts bit for bit, with a Zipf-skewed selection bias as in the bench."""
+    import paper_2511_16947_b200 as P
+
+    dev = "cuda"
+    g = torch.Generator(device=dev).manual_seed(T + E)
+    e_pad = max(16, (E + 15) // 16 * 16)
+    x = torch.randn(T, d, generator=g, device=dev).to(torch.bfloat16)
+    wg = torch.zeros(max(64, e_pad), d, dtype=torch.bfloat16, device=dev)
+    wg[:E] = (torch.randn(E, d, generator=g, device=dev) / d ** 0.5).to(torch.bfloat16)
+    b = torch.tensor(P.zipf_gate_bias(E, 1.0, 0), dtype=torch.float32, device=dev)
+    tps = T // G
+    ncs = tps // 64
+    lib, s = L.lib(), L.stream_handle()
+
+    def bufs():
+        return (torch.full((T, e_pad), float("nan"), device=dev), torch.full((T, K), -1, dtype=torch.int32, device=dev),
+                torch.full((T, K), float("nan"), device=dev), torch.full((G, E), 77, dtype=torch.int64, device=dev),
+                torch.full((G * ncs * E,), -7, dtype=torch.int32, device=dev))
+
+    lg0, i0, w0, h0, c0 = bufs()
+    h0.zero_()
+    L.check(lib.hep_gemm_bf16(x.data_ptr(), wg.data_ptr(), lg0.data_ptr(), T, e_pad, d, 0, s), "gemm")
+    L.check(lib.hep_gate_topk(lg0.data_ptr(), e_pad, b.data_ptr(), T, E, K, tps, G, i0.data_ptr(), w0.data_ptr(),
+                              h0.data_ptr(), s), "gate")
+    L.check(lib.hep_gate_chunk_counts(i0.data_ptr(), T, K, E, tps, G, c0.data_ptr(), s), "chunks")
+    lg1, i1, w1, h1, c1 = bufs()
+    sync = torch.zeros(4, dtype=torch.int32, device=dev)
+    L.check(lib.hep_router_topk_ws(x.data_ptr(), wg.data_ptr(), T, d, E, e_pad, b.data_ptr(), K, tps, G, lg1.data_ptr(),
+                                   i1.data_ptr(), w1.data_ptr(), h1.data_ptr(), c1.data_ptr(), sync.data_ptr(), s), "ws")
+    torch.cuda.synchronize()
+    assert torch.equal(lg0, lg1) and torch.equal(i0, i1) and torch.equal(w0, w1)
+    assert torch.equal(h0, h1) and int(h1.sum()) == T * K
+    assert torch.equal(c0, c1)
+    assert int(sync.abs().sum()) == 0
