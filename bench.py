@@ -671,11 +671,12 @@ def measure_config(cfg, args, dev, *, steps, primary):
 
     # --- the HBM-bound kernels' own rate, measured before the long power-capped timed region
     # (the kernel's capability; the same measurement after it is reported beside).  The
-    # warm-up's FFN work leaves the GPU power-capped for a while: rest 0.5 s first so this
+    # warm-up's FFN work leaves the GPU power-capped for a while (the router right after FFN
+    # bursts runs ~20 % slower, profiles/r02/router_ab_r02d.txt --hot): rest 2 s first so this
     # figure is taken at the nominal clock
     layer.run(unseen[0], bufs, stream)
     torch.cuda.synchronize()
-    time.sleep(0.5)
+    time.sleep(2.0)
     hbm_b2b_before = hbm_b2b_ms(layer, bufs, unseen[0], stream)
     layer.run(unseen[0], bufs, stream)
     torch.cuda.synchronize()
@@ -898,7 +899,7 @@ def hbm_block(before, after, nbytes, hbm, traffic, router_flops=None, tf_burst=N
         out["router_gate"]["roofline_us"] = {"hbm": t_hbm, "tensor": t_tc, "bound": "hbm" if t_hbm >= t_tc else "tensor",
                                              "frac_of_bound": max(t_hbm, t_tc) / us}
     out["timing"] = ("each kernel re-launched 20x back to back on a held-out micro-batch inside one CUDA graph, "
-                     "median of 5 timed replays after 5 warm ones; before the timed region after a 0.5 s rest (the kernel's rate at "
+                     "median of 5 timed replays after 5 warm ones; before the timed region after a 2 s rest (the kernel's rate at "
                      "the nominal clock) and right after it (after the power-capped FFN steps: the in-step rate)")
     out["peak_GB/s"] = hbm
     return out
