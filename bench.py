@@ -264,7 +264,10 @@ def run_ep(args, world, rank, local, dev):
                  "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if dist.get_backend() == "nccl" else None}
     if rank == 0:
         print(f"[bench] communicator: {comm_info}", file=sys.stderr)
-    layer = EPMoELayer(pl, d, F, K, comm, [rank], seed=0, gate_bias=bias, device=dev, exchange=args.exchange)
+    if args.pipeline_ratio is not None:  # harmony_pipelined: the static share's all-to-all-v overlaps the solve
+        args.exchange = "nccl"
+    layer = EPMoELayer(pl, d, F, K, comm, [rank], seed=0, gate_bias=bias, device=dev, exchange=args.exchange,
+                       pipeline_ratio=args.pipeline_ratio)
     x = torch.randn(T, d, generator=torch.Generator(device=dev).manual_seed(1000 + rank), device=dev).to(torch.bfloat16)
     ok = 1
     try:  # the NVLink path maps the peers' buffers with CUDA IPC; fall back to NCCL if that is refused
@@ -360,7 +363,10 @@ def run_ep(args, world, rank, local, dev):
     sent_rows = int(pair[rank].sum().item() - pair[rank, rank].item())
     a2a_bytes = sent_rows * d * 2
     a2a_gbs = -_max_over_ranks(-(a2a_bytes / (a2a_ms / 1e3) / 1e9), dev)  # slowest rank
-    R = int(layer.ranks[0].bufs[T]["counts"][G:].sum().item())  # rows this rank received (outside the timing)
+    if layer.static_share is not None:  # pipelined: both phases' received rows; the a2a events bracket phase 1's
+        R = int(layer.ranks[0].bufs[T]["R_recv"])
+    else:
+        R = int(layer.ranks[0].bufs[T]["counts"][G:].sum().item())  # rows this rank received (outside the timing)
     ffn_tf = 6.0 * d * F * R / (ffn_ms / 1e3) / 1e12
     min_tf = -_max_over_ranks(-ffn_tf, dev)
     hbm, tf_burst, tf_sus, peak_src = load_peaks()
@@ -389,6 +395,9 @@ def run_ep(args, world, rank, local, dev):
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": CONFIG_TEXT[args.config], "tokens_per_microbatch_per_gpu": T, "ep": world,
                        "top_k": K, "d_model": d, "ffn": F, "experts": E, "zipf_s": args.skew, "pass": "forward",
+                       "schedule": ("harmony" if layer.static_share is None else
+                                    f"harmony_pipelined (pipeline_ratio={args.pipeline_ratio}: the static share's "
+                                    "all-to-all-v on a side stream while the scheduled share is solved)"),
                        "launch": ("cuda-graph replay (device-side barriers, no host sync)" if graph is not None
                                   else "eager"),
                        "exchange": (("NVLink peer stores: dispatch kernel -> peers' receive buffers, down-projection "
@@ -400,7 +409,10 @@ def run_ep(args, world, rank, local, dev):
             "comm": comm_info,
             "e2e": {"value": world * T * args.steps / (e_ms / 1e3), "unit": "tokens/s",
                     "h2d_bytes_per_step": T * d * 2, "d2h_bytes_per_step": T * d * 2},
-            "gpu_launches": args.steps * (13 if args.exchange == "p2p" else 12),
+            # router, scheduler, assignment (4), permute, FFN (4), combine = 12; the NVLink path adds
+            # the dispatch kernel; the pipelined split adds the split kernel, the static phase's
+            # scheduler launch, a second assignment (4) and permute = 19
+            "gpu_launches": args.steps * (13 if args.exchange == "p2p" else (19 if layer.static_share is not None else 12)),
             "roofline": {"bound": "tensor", "kernel": "hep_moe_expert_ffn on the received rows (rank 0)",
                          "achieved": ffn_tf, "peak": tf_sus, "unit": "TFLOP/s", "frac": ffn_tf / tf_sus,
                          "min_over_ranks": min_tf, "rows_rank0": R,

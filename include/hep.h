@@ -323,6 +323,21 @@ int hep_moe_assign_ep(hep_sched_t h, const hep_sched_out *sched, const int32_t *
                       size_t workspace_bytes, void *stream);
 size_t hep_moe_assign_ep_workspace(hep_sched_t h, int64_t T, int K);
 /*
+ * hep_moe_assign_ep for one phase of the pipelined split (simulator.py:420-435) in the EP
+ * layer: sched = that phase's plan (hep_sched_pipelined: former = phase 0, the static share;
+ * latter = phase 1), d_split its [2][E][G] split.  Phase p owns the ranks [lo, lo + share)
+ * of every (expert, this source) token sequence (lo = 0, or the static share for phase 1);
+ * its assignments get send positions from send_row_offset on (the phases share one send
+ * buffer), the others are left untouched in d_tok_row and -1 in d_tok_row_phase (the input
+ * of this phase's hep_moe_permute).  d_seg / d_counts: this phase's receive segments and
+ * split sizes.  The two phases may run concurrently on two streams, each with its own
+ * workspace: the static share's exchange then overlaps the scheduled share's solve.
+ */
+int hep_moe_assign_ep_phase(hep_sched_t h, const hep_sched_out *sched, const int64_t *d_split, int phase,
+                            const int32_t *d_topk_idx, int64_t T, int K, int rank, int64_t send_row_offset,
+                            int32_t *d_tok_row, int32_t *d_tok_row_phase, int32_t *d_seg, int64_t *d_counts,
+                            void *workspace, size_t workspace_bytes, void *stream);
+/*
  * EP training layout: map the receive buffer ([src][hosted expert], d_seg from
  * hep_moe_assign_ep) onto a [local slot][src] layout where every slot's rows form one
  * block starting on a multiple of row_align (the weight-gradient GEMMs contract over

@@ -75,6 +75,7 @@ SIGNATURES = {
     "hep_moe_assign_phase": (ctypes.c_int, [vp, ctypes.POINTER(HepSchedOut), vp, ctypes.c_int, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]),
     "hep_moe_assign_workspace": (ctypes.c_size_t, [vp, ctypes.c_int64, ctypes.c_int]),
     "hep_moe_assign_ep": (ctypes.c_int, [vp, ctypes.POINTER(HepSchedOut), vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int64, vp, vp, vp, vp, ctypes.c_size_t, vp]),
+    "hep_moe_assign_ep_phase": (ctypes.c_int, [vp, ctypes.POINTER(HepSchedOut), vp, ctypes.c_int, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int64, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]),
     "hep_moe_assign_ep_workspace": (ctypes.c_size_t, [vp, ctypes.c_int64, ctypes.c_int]),
     "hep_sched_hosted": (ctypes.c_int, [vp, ctypes.c_int, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
     "hep_moe_permute": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, vp, vp]),

@@ -333,10 +333,15 @@ __global__ void chunk_map_kernel(const int32_t *topk_idx, int K, int E, int G, i
 // local weight slot.  Every rank derives all offsets from the same routing
 // table, so both sides agree without exchanging anything but the rows.
 // ---------------------------------------------------------------------------
+// Pipelined split (split != null): this phase's plan covers ranks [lo, lo + share) of every
+// (expert, source) token sequence, lo = 0 (phase 0, the static share) or the static share
+// split[e][src] (phase 1); send rows start at row_off (the two phases' send layouts share one
+// buffer, phase 1 after phase 0's worst case).
 __global__ void ep_prep_kernel(int G, int E, int rank, const int64_t *ranges, const int64_t *n_ranges_p,
                                const int64_t *transfer, const int32_t *hosted, int n_hosted, const int32_t *nnz_exp,
                                const int32_t *slots, int64_t *counts, int32_t *seg, AssignWs w, int32_t *status,
-                               int64_t recv_capacity) {
+                               int64_t recv_capacity, const int64_t *split = nullptr, int phase = 0,
+                               int64_t row_off = 0) {
     const int tid = threadIdx.x, nt = blockDim.x;
     __shared__ int fail;
     if (tid == 0) {
@@ -367,7 +372,10 @@ __global__ void ep_prep_kernel(int G, int E, int rank, const int64_t *ranges, co
     }
     const int64_t n_ranges = *n_ranges_p;
     for (int i = tid; i < E * G * G; i += nt) w.cnt3[i] = 0;
-    for (int i = tid; i < E * G; i += nt) w.es_cnt[i] = 0;
+    for (int i = tid; i < E * G; i += nt) {
+        w.es_cnt[i] = 0;
+        w.es_lo[i] = (split && phase == 1) ? (int32_t)split[i] : 0;  // the phase's first rank of (e, src)
+    }
     for (int i = tid; i <= E; i += nt) w.first[i] = -1;
     __syncthreads();
     for (int64_t r = tid; r < n_ranges; r += nt) {
@@ -384,7 +392,7 @@ __global__ void ep_prep_kernel(int G, int E, int rank, const int64_t *ranges, co
         int64_t run = 0;
         for (int dd = 0; dd < d; ++dd) run += transfer[rank * G + dd];
         for (int e = 0; e < E; ++e) {
-            w.sbase[e * G + d] = (int32_t)run;
+            w.sbase[e * G + d] = (int32_t)(run + row_off);
             run += w.cnt3[((int64_t)e * G + rank) * G + d];
         }
         // receive segments of source d: [src][hosted expert asc]
@@ -407,8 +415,8 @@ __global__ void ep_prep_kernel(int G, int E, int rank, const int64_t *ranges, co
     for (int e = tid; e < E; e += nt) {
         const int r0 = w.first[e];
         if (r0 < 0) continue;
-        int64_t rank_start = 0;
         const int es = e * G + rank;
+        int64_t rank_start = w.es_lo[es];
         for (int64_t j = r0; j < n_ranges && ranges[4 * j] == e; ++j) {
             if (ranges[4 * j + 1] != rank) continue;
             const int dst = (int)ranges[4 * j + 2];
@@ -770,10 +778,10 @@ extern "C" int hep_sched_hosted(hep_sched_t h, int rank, int *n_hosted, int *n_s
     return HEP_OK;
 }
 
-extern "C" int hep_moe_assign_ep(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_topk_idx, int64_t T, int K,
-                                 int rank, int64_t recv_capacity, int32_t *d_tok_row, int32_t *d_seg, int64_t *d_counts,
-                                 void *workspace, size_t workspace_bytes, void *stream) {
-    HEP_NVTX("hep_moe_assign_ep");
+static int assign_ep_impl(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_topk_idx, int64_t T, int K,
+                          int rank, int64_t recv_capacity, int32_t *d_tok_row, int32_t *d_seg, int64_t *d_counts,
+                          void *workspace, size_t workspace_bytes, void *stream, const int64_t *d_split, int phase,
+                          int64_t row_off, int32_t *d_tok_row_phase) {
     HEP_REQUIRE(h && sched && d_topk_idx && d_tok_row && d_seg && d_counts && workspace, HEP_E_CONTRACT,
                 "hep_moe_assign_ep: null argument");
     HEP_REQUIRE(rank >= 0 && rank < h->G && K >= 1 && K <= 16, HEP_E_DIMENSION, "hep_moe_assign_ep: rank/K");
@@ -785,7 +793,7 @@ extern "C" int hep_moe_assign_ep(hep_sched_t h, const hep_sched_out *sched, cons
     const int n_hosted = h->h_hosted_off[rank + 1] - h->h_hosted_off[rank];
     ep_prep_kernel<<<1, 512, 0, s>>>(G, E, rank, sched->d_ranges, sched->d_n_ranges, sched->d_transfer,
                                      h->d_seg_nnz + h->h_hosted_off[rank], n_hosted, h->d_nnz_exp, h->d_slots,
-                                     d_counts, d_seg, w, sched->d_status, recv_capacity);
+                                     d_counts, d_seg, w, sched->d_status, recv_capacity, d_split, phase, row_off);
     HEP_CHECK_LAUNCH();
     if (T <= 0) return HEP_OK;
     const int ncs = (int)((tps + kChunk - 1) / kChunk);
@@ -798,9 +806,28 @@ extern "C" int hep_moe_assign_ep(hep_sched_t h, const hep_sched_out *sched, cons
     if (sm > 48 * 1024)
         HEP_CHECK_CUDA(cudaFuncSetAttribute(chunk_map_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     chunk_map_kernel<<<ncs, 256, sm, s>>>(d_topk_idx, K, E, G, tps, T, ncs, w.chunk_pre, w, d_tok_row, nullptr, rank,
-                                          false, sched->d_status, nullptr);
+                                          d_split != nullptr, sched->d_status, d_tok_row_phase);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
+}
+
+extern "C" int hep_moe_assign_ep(hep_sched_t h, const hep_sched_out *sched, const int32_t *d_topk_idx, int64_t T, int K,
+                                 int rank, int64_t recv_capacity, int32_t *d_tok_row, int32_t *d_seg, int64_t *d_counts,
+                                 void *workspace, size_t workspace_bytes, void *stream) {
+    HEP_NVTX("hep_moe_assign_ep");
+    return assign_ep_impl(h, sched, d_topk_idx, T, K, rank, recv_capacity, d_tok_row, d_seg, d_counts, workspace,
+                          workspace_bytes, stream, nullptr, 0, 0, nullptr);
+}
+
+extern "C" int hep_moe_assign_ep_phase(hep_sched_t h, const hep_sched_out *sched, const int64_t *d_split, int phase,
+                                       const int32_t *d_topk_idx, int64_t T, int K, int rank, int64_t send_row_offset,
+                                       int32_t *d_tok_row, int32_t *d_tok_row_phase, int32_t *d_seg, int64_t *d_counts,
+                                       void *workspace, size_t workspace_bytes, void *stream) {
+    HEP_NVTX("hep_moe_assign_ep_phase");
+    HEP_REQUIRE(d_split && (phase == 0 || phase == 1) && send_row_offset >= 0, HEP_E_CONTRACT,
+                "hep_moe_assign_ep_phase: split, phase 0/1, row offset >= 0");
+    return assign_ep_impl(h, sched, d_topk_idx, T, K, rank, 0, d_tok_row, d_seg, d_counts, workspace, workspace_bytes,
+                          stream, d_split, phase, send_row_offset, d_tok_row_phase);
 }
 
 // ===========================================================================

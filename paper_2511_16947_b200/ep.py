@@ -39,6 +39,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+from fractions import Fraction
 
 import torch
 
@@ -276,10 +277,22 @@ class EPMoELayer:
 
     def __init__(self, placement: Placement, d_model: int, ffn: int, top_k: int, comm, ranks, *, seed: int = 0,
                  gate_bias: torch.Tensor | None = None, device=None, train: bool = False, exchange: str = "nccl",
-                 recv_capacity_factor: float = 3.0):
+                 recv_capacity_factor: float = 3.0, pipeline_ratio: float | Fraction | None = None):
         """recv_capacity_factor: NVLink path receive buffers hold this many times T*K rows
-        per rank (see EPRank.p2p_buffers); the NCCL path sizes its buffers per call."""
+        per rank (see EPRank.p2p_buffers); the NCCL path sizes its buffers per call.
+        pipeline_ratio: harmony_pipelined (simulator.py:420-435, :451-453) -- the 1 - ratio
+        static share of every (expert, source) is split evenly over the expert's replicas and
+        dispatched (its all-to-all-v on a side stream) while the scheduled share is solved
+        with the static share's GPU loads as gpu_base; NCCL exchange, forward only."""
         _lib.require_cuda()
+        self.static_share = None
+        if pipeline_ratio is not None:
+            if not (0.0 < float(pipeline_ratio) <= 1.0):
+                raise ValueError("pipeline_ratio must be in (0, 1]")  # SimulationConfig (simulator.py:117-118)
+            if train or exchange != "nccl":
+                raise ValueError("the pipelined split runs on the NCCL exchange, forward only")
+            self.static_share = Fraction(1) - Fraction(pipeline_ratio)
+            self._side = torch.cuda.Stream()
         if recv_capacity_factor <= 0:
             raise ValueError("recv_capacity_factor must be positive")
         self.recv_capacity_factor = float(recv_capacity_factor)
@@ -335,6 +348,8 @@ class EPMoELayer:
         with torch.cuda.stream(st):
             if self.exchange == "p2p":
                 return self._forward_p2p(xs, st, events or {})
+            if self.static_share is not None:
+                return self._forward_pipelined(xs, st, events or {})
             return self._forward(xs, st, events or {})
 
     def _peer_table(self, T: int) -> list:
@@ -636,6 +651,125 @@ class EPMoELayer:
             T = x.shape[0]
             if self.train_mode:
                 b["x"], b["back"] = x, back
+            ck(L.hep_moe_combine(back.data_ptr(), b["tok_row"].data_ptr(), b["topk_w"].data_ptr(), T, K, d,
+                                 b["out"].data_ptr(), s), "hep_moe_combine")
+            outs.append(b["out"])
+        return outs
+
+    def _phase_buffers(self, rk: EPRank, T: int) -> dict:
+        """Per-rank buffers of the pipelined split: the phases' row maps, segments, split
+        sizes and workspaces (they run on two streams), one send buffer holding phase 0's
+        rows at [0, T*K) and phase 1's at [T*K, 2*T*K)."""
+        b = rk.buffers(self, T)
+        if "send2" not in b:
+            L = _lib.lib()
+            dev, K, G = self.device, self.K, self.G
+            i32 = dict(dtype=torch.int32, device=dev)
+            ws = max(int(L.hep_moe_assign_ep_workspace(rk.sched.handle, T, K)), 256)
+            n_seg = max(G * rk.n_hosted, 1)
+            b.update(
+                tok_row_ph=[torch.empty(T, K, **i32) for _ in range(2)],
+                seg_ph=[torch.empty(n_seg, 4, **i32) for _ in range(2)],
+                counts_ph=[torch.empty(2 * G, dtype=torch.int64, device=dev) for _ in range(2)],
+                assign_ws_ph=[torch.empty(ws, dtype=torch.uint8, device=dev) for _ in range(2)],
+                send2=torch.empty(max(2 * T * K, 1), self.d, dtype=torch.bfloat16, device=dev),
+                back2=torch.zeros(max(2 * T * K, 1), self.d, dtype=torch.bfloat16, device=dev),
+            )
+        return b
+
+    def _forward_pipelined(self, xs, st, ev):
+        """harmony_pipelined over the EP group (simulator.py:420-435, :451-453).  Per rank:
+        router -> histogram all-gather -> hep_sched_pipelined (split; the static phase's
+        even plan, routing and transfer plan on the side stream; the scheduled share's
+        solve with gpu_base on this stream).  The static phase's assignment, permute and
+        all-to-all-v run on the side stream (the host reads only its split sizes) while
+        the scheduled phase is solved, assigned and exchanged here; the expert FFN then
+        runs once over both phases' received rows (one weight stream), the outputs go
+        back per phase, and the combine reads both phases' returned rows."""
+        L = _lib.lib()
+        s = st.cuda_stream
+        side = self._side
+        ss = side.cuda_stream
+        ck = _lib.check
+        K, E, G, d, F = self.K, self.E, self.G, self.d, self.F
+        bs = []
+        for rk, x in zip(self.ranks, xs):
+            T = x.shape[0]
+            b = self._phase_buffers(rk, T)
+            bs.append(b)
+            ck(L.hep_router_topk_ws(x.data_ptr(), self.wg.data_ptr(), T, d, E, self.e_pad, _lib.ptr(self.gate_bias), K,
+                                    T, 1, b["logits"].data_ptr(), b["topk_idx"].data_ptr(), b["topk_w"].data_ptr(),
+                                    b["hist"].data_ptr(), None, b["router_sync"].data_ptr(), s), "hep_router_topk")
+        hists = self.comm.all_gather([b["hist"] for b in bs])  # [G][E] on every rank
+        for rk, x, b, h in zip(self.ranks, xs, bs, hists):
+            T = x.shape[0]
+            b["hist_all"] = h
+            rk.sched.launch_pipelined(h, 1, E, self.static_share, HEP_SCHED_ALL, st, stream_static=side)
+            split = rk.sched.split.data_ptr()
+            # phase 0 (static share) on the side stream, behind its plan
+            ck(L.hep_moe_assign_ep_phase(rk.sched.handle, ctypes.byref(rk.sched.former.out), split, 0,
+                                         b["topk_idx"].data_ptr(), T, K, rk.rank, 0, b["tok_row"].data_ptr(),
+                                         b["tok_row_ph"][0].data_ptr(), b["seg_ph"][0].data_ptr(),
+                                         b["counts_ph"][0].data_ptr(), b["assign_ws_ph"][0].data_ptr(),
+                                         b["assign_ws_ph"][0].numel(), ss), "hep_moe_assign_ep_phase(static)")
+            ck(L.hep_moe_permute(x.data_ptr(), b["tok_row_ph"][0].data_ptr(), T, K, d, b["send2"].data_ptr(), ss),
+               "hep_moe_permute(static)")
+        with torch.cuda.stream(side):
+            # the static share's split sizes (a side-stream sync: the solve keeps running)
+            c0 = [b["counts_ph"][0].cpu().tolist() for b in bs]
+            recv0 = self.comm.all_to_all([b["send2"][: sum(c[:G])] for b, c in zip(bs, c0)], [c[:G] for c in c0],
+                                         [c[G:] for c in c0])
+        for rk, x, b in zip(self.ranks, xs, bs):
+            T = x.shape[0]
+            ck(L.hep_moe_assign_ep_phase(rk.sched.handle, ctypes.byref(rk.sched.out), rk.sched.split.data_ptr(), 1,
+                                         b["topk_idx"].data_ptr(), T, K, rk.rank, T * K, b["tok_row"].data_ptr(),
+                                         b["tok_row_ph"][1].data_ptr(), b["seg_ph"][1].data_ptr(),
+                                         b["counts_ph"][1].data_ptr(), b["assign_ws_ph"][1].data_ptr(),
+                                         b["assign_ws_ph"][1].numel(), s), "hep_moe_assign_ep_phase(scheduled)")
+            ck(L.hep_moe_permute(x.data_ptr(), b["tok_row_ph"][1].data_ptr(), T, K, d, b["send2"].data_ptr(), s),
+               "hep_moe_permute(scheduled)")
+        c1 = [b["counts_ph"][1].cpu().tolist() for b in bs]
+        if "a2a" in ev:
+            ev["a2a"][0].record(st)
+        recv1 = self.comm.all_to_all([b["send2"][x.shape[0] * K: x.shape[0] * K + sum(c[:G])]
+                                      for b, c, x in zip(bs, c1, xs)], [c[:G] for c in c1], [c[G:] for c in c1])
+        if "a2a" in ev:
+            ev["a2a"][1].record(st)
+        st.wait_stream(side)
+        for r in recv0:
+            r.record_stream(st)
+        ys0, ys1 = [], []
+        if "ffn" in ev:
+            ev["ffn"][0].record(st)
+        for rk, b, r0, r1 in zip(self.ranks, bs, recv0, recv1):
+            R0, R1 = r0.shape[0], r1.shape[0]
+            recv = torch.cat([r0, r1], dim=0)
+            seg1 = b["seg_ph"][1].clone()
+            seg1[:, 0] += R0  # phase 1's rows follow phase 0's in the FFN input
+            seg = torch.cat([b["seg_ph"][0], seg1], dim=0)
+            y = torch.empty(max(R0 + R1, 1), d, dtype=torch.bfloat16, device=self.device)
+            if R0 + R1 > 0:
+                h = torch.empty(R0 + R1, F, dtype=torch.bfloat16, device=self.device)
+                n_seg = seg.shape[0]
+                ws = torch.empty(int(L.hep_moe_ffn_workspace(n_seg, R0 + R1, rk.n_slots)), dtype=torch.uint8,
+                                 device=self.device)
+                ck(L.hep_moe_expert_ffn(recv.data_ptr(), rk.w13.data_ptr(), rk.w2.data_ptr(), seg.data_ptr(), n_seg,
+                                        R0 + R1, d, F, rk.n_slots, h.data_ptr(), y.data_ptr(), ws.data_ptr(),
+                                        ws.numel(), rk.sched.status.data_ptr(), s), "hep_moe_expert_ffn")
+            ys0.append(y[:R0])
+            ys1.append(y[R0:R0 + R1])
+        if "ffn" in ev:
+            ev["ffn"][1].record(st)
+        backs0 = self.comm.all_to_all(ys0, [c[G:] for c in c0], [c[:G] for c in c0])
+        backs1 = self.comm.all_to_all(ys1, [c[G:] for c in c1], [c[:G] for c in c1])
+        outs = []
+        for x, b, k0, k1, a, c in zip(xs, bs, backs0, backs1, c0, c1):
+            T = x.shape[0]
+            back = b["back2"]
+            back[: k0.shape[0]].copy_(k0)  # returned rows at their send positions (phase 1 from T*K)
+            back[T * K: T * K + k1.shape[0]].copy_(k1)
+            b["send_counts_ph"], b["recv_counts_ph"] = [a[:G], c[:G]], [a[G:], c[G:]]
+            b["R_recv"] = sum(a[G:]) + sum(c[G:])
             ck(L.hep_moe_combine(back.data_ptr(), b["tok_row"].data_ptr(), b["topk_w"].data_ptr(), T, K, d,
                                  b["out"].data_ptr(), s), "hep_moe_combine")
             outs.append(b["out"])

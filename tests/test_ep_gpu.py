@@ -370,3 +370,41 @@ def test_ep_training_over_cuda_ipc_two_processes(P):
         want = [outs[r]] + list(grads[r])
         for got, ref in zip(res[r], want):
             assert np.array_equal(got, ref.float().cpu().numpy()), r
+
+
+@pytest.mark.parametrize("G,E,K,d,F,T,kind,s,ratio", [
+    (4, 8, 2, 512, 512, 4096, "cayley", 1.0, 0.5),
+    (8, 32, 4, 256, 256, 4096, "asym", 1.5, 0.5),
+    (8, 128, 8, 256, 256, 8192, "cayley", 1.0, 0.25),
+    (2, 8, 2, 256, 128, 2048, "cayley", 0.0, 1.0),
+])
+def test_local_ep_pipelined_split(P, G, E, K, d, F, T, kind, s, ratio):
+    """harmony_pipelined over the EP group: the static share's assignment, permute and
+    all-to-all-v on a side stream while the scheduled share is solved; one FFN over both
+    phases' received rows.  The outputs equal the plain EP layer and the single-device
+    pipelined layer bit for bit, and every rank holds the same two-phase schedule as the
+    single-device layer's (static plan, scheduled plan, GPU loads)."""
+    from paper_2511_16947_b200.ep import EPMoELayer, LocalComm
+
+    pl = _placement(P, G, E, kind, s)
+    bias = torch.tensor(P.zipf_gate_bias(E, s, 0)) if s > 0 else None
+    x = torch.randn(T, d, generator=torch.Generator(device="cuda").manual_seed(13), device="cuda").to(torch.bfloat16)
+    xs = [x[r * (T // G):(r + 1) * (T // G)].contiguous() for r in range(G)]
+    plain = EPMoELayer(pl, d, F, K, LocalComm(G), range(G), seed=5, gate_bias=bias)
+    pipe = EPMoELayer(pl, d, F, K, LocalComm(G), range(G), seed=5, gate_bias=bias, pipeline_ratio=ratio)
+    ref = torch.cat([o.clone() for o in plain.forward(xs)])
+    got = torch.cat([o.clone() for o in pipe.forward(xs)])
+    got2 = torch.cat([o.clone() for o in pipe.forward(xs)])  # buffers reused across micro-batches
+    torch.cuda.synchronize()
+    for rk in pipe.ranks:
+        rk.sched.check_status("pipelined")
+    assert torch.equal(got, ref), (got.float() - ref.float()).abs().max().item()
+    assert torch.equal(got2, ref)
+    sim = P.MoELayer(pl, d, F, K, seed=5, gate_bias=bias, pipeline_ratio=ratio)
+    assert torch.equal(sim(x), ref)
+    torch.cuda.synchronize()
+    s0 = pipe.ranks[0].sched
+    for rk in pipe.ranks:
+        assert torch.equal(rk.sched.xi, sim.sched.xi) and torch.equal(rk.sched.ranges, sim.sched.ranges)
+        assert torch.equal(rk.sched.split, sim.sched.split)
+        assert torch.equal(rk.sched.former.xi, s0.former.xi)
