@@ -347,6 +347,9 @@ int hep_moe_assign_ep_phase(hep_sched_t h, const hep_sched_out *sched, const int
  * arguments of hep_moe_expert_ffn_train / hep_moe_expert_ffn_bwd with n_experts = n_slots.
  * row_map_len > 0: entries [R_recv, row_map_len) are set to -1 (the NVLink path's fixed-size
  * receive buffer, R_recv known only on the device; hep_moe_permute skips them).
+ * G = the number of [src] blocks in d_seg (up to 2 * HEP_MAX_GPUS: the pipelined split's
+ * two phases).  With row_align = 1 it is also the inference regrouping of the NCCL path
+ * (one contiguous run per local slot instead of one per (source, slot)).
  */
 int hep_moe_ep_train_layout(const int32_t *d_seg, int n_hosted, int G, int n_slots, int row_align, int32_t *d_row_map,
                             int64_t row_map_len, int32_t *d_seg_out, int64_t *d_slot_rows, void *stream);

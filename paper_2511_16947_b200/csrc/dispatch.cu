@@ -1002,7 +1002,8 @@ extern "C" int hep_moe_ep_train_layout(const int32_t *d_seg, int n_hosted, int G
                                        int64_t *d_slot_rows, void *stream) {
     HEP_NVTX("hep_moe_ep_train_layout");
     HEP_REQUIRE(d_seg && d_row_map && d_seg_out && d_slot_rows, HEP_E_CONTRACT, "hep_moe_ep_train_layout: null");
-    HEP_REQUIRE(G >= 1 && G <= HEP_MAX_GPUS && n_hosted >= 0 && n_slots >= n_hosted && n_slots <= 1024 &&
+    // G = the [src] blocks of d_seg: the group size, or twice it (the pipelined split's two phases)
+    HEP_REQUIRE(G >= 1 && G <= 2 * HEP_MAX_GPUS && n_hosted >= 0 && n_slots >= n_hosted && n_slots <= 1024 &&
                     row_align >= 1,
                 HEP_E_DIMENSION, "hep_moe_ep_train_layout: G %d n_hosted %d n_slots %d align %d", G, n_hosted,
                 n_slots, row_align);

@@ -317,6 +317,9 @@ class EPMoELayer:
         w1, w2, w3 = init_expert_weights(self.E, d_model, ffn, seed, self.device)
         self.ranks = [EPRank(self, r, w1, w2, w3) for r in ranks]
         del w1, w2, w3
+        # NCCL path, inference: regroup the received rows per local weight slot before the FFN
+        # (see _ffn_rows); False runs the FFN on the [src][expert] runs directly
+        self.regroup_rows = True
 
     @torch.no_grad()
     def migrate(self, placement: Placement) -> dict:
@@ -748,14 +751,8 @@ class EPMoELayer:
             seg1[:, 0] += R0  # phase 1's rows follow phase 0's in the FFN input
             seg = torch.cat([b["seg_ph"][0], seg1], dim=0)
             y = torch.empty(max(R0 + R1, 1), d, dtype=torch.bfloat16, device=self.device)
-            if R0 + R1 > 0:
-                h = torch.empty(R0 + R1, F, dtype=torch.bfloat16, device=self.device)
-                n_seg = seg.shape[0]
-                ws = torch.empty(int(L.hep_moe_ffn_workspace(n_seg, R0 + R1, rk.n_slots)), dtype=torch.uint8,
-                                 device=self.device)
-                ck(L.hep_moe_expert_ffn(recv.data_ptr(), rk.w13.data_ptr(), rk.w2.data_ptr(), seg.data_ptr(), n_seg,
-                                        R0 + R1, d, F, rk.n_slots, h.data_ptr(), y.data_ptr(), ws.data_ptr(),
-                                        ws.numel(), rk.sched.status.data_ptr(), s), "hep_moe_expert_ffn")
+            if R0 + R1 > 0:  # 2G source blocks: [phase][src][hosted expert]
+                self._ffn_rows(rk, recv, seg, 2 * G, y)
             ys0.append(y[:R0])
             ys1.append(y[R0:R0 + R1])
         if "ffn" in ev:
@@ -775,6 +772,41 @@ class EPMoELayer:
             outs.append(b["out"])
         return outs
 
+    def _ffn_rows(self, rk: EPRank, recv: torch.Tensor, seg: torch.Tensor, n_blocks: int, y: torch.Tensor) -> None:
+        """K6 over received rows in the all-to-all-v layout ([src][hosted expert]: n_blocks
+        source blocks, seg [n_blocks * n_hosted][4]); Y into y in the same order.  With
+        regroup_rows the rows are first gathered into one contiguous run per local weight
+        slot (hep_moe_ep_train_layout with row_align 1, a permute), so an expert's rows
+        from all sources share m-tiles instead of each (source, expert) run filling its
+        own partial tiles, and the outputs are gathered back afterwards."""
+        L = _lib.lib()
+        ck = _lib.check
+        s = torch.cuda.current_stream().cuda_stream
+        d, F, ns = self.d, self.F, rk.n_slots
+        R = recv.shape[0]
+        dev = self.device
+        if self.regroup_rows:
+            i32 = dict(dtype=torch.int32, device=dev)
+            row_map = torch.empty(R, **i32)
+            seg_al = torch.empty(ns, 4, **i32)
+            slot_rows = torch.empty(ns + 1, dtype=torch.int64, device=dev)
+            ck(L.hep_moe_ep_train_layout(seg.data_ptr(), rk.n_hosted, n_blocks, ns, 1, row_map.data_ptr(), 0,
+                                         seg_al.data_ptr(), slot_rows.data_ptr(), s), "hep_moe_ep_train_layout")
+            rows = torch.empty(R, d, dtype=torch.bfloat16, device=dev)
+            ck(L.hep_moe_permute(recv.data_ptr(), row_map.data_ptr(), R, 1, d, rows.data_ptr(), s),
+               "hep_moe_permute(regroup)")
+            src_rows, src_seg, n_seg, y_out = rows, seg_al, ns, torch.empty(R, d, dtype=torch.bfloat16, device=dev)
+        else:
+            src_rows, src_seg, n_seg, y_out = recv, seg, n_blocks * rk.n_hosted, y
+        h = torch.empty(R, F, dtype=torch.bfloat16, device=dev)
+        ws = torch.empty(int(L.hep_moe_ffn_workspace(n_seg, R, ns)), dtype=torch.uint8, device=dev)
+        ck(L.hep_moe_expert_ffn(src_rows.data_ptr(), rk.w13.data_ptr(), rk.w2.data_ptr(), src_seg.data_ptr(), n_seg, R,
+                                d, F, ns, h.data_ptr(), y_out.data_ptr(), ws.data_ptr(), ws.numel(),
+                                rk.sched.status.data_ptr(), s), "hep_moe_expert_ffn")
+        if self.regroup_rows:  # back to the receive order
+            ck(L.hep_moe_gather_sum(y_out.data_ptr(), row_map.data_ptr(), None, None, R, 1, d, y.data_ptr(), s),
+               "hep_moe_gather_sum(ungroup)")
+
     def _expert_ffn(self, rk: EPRank, b: dict, recv: torch.Tensor) -> torch.Tensor:
         """K6 on the received rows of one rank; returns Y in receive order."""
         L = _lib.lib()
@@ -785,13 +817,7 @@ class EPMoELayer:
         y = torch.empty(max(R, 1), d, dtype=torch.bfloat16, device=self.device)
         if not self.train_mode:
             if R > 0:
-                h = torch.empty(R, F, dtype=torch.bfloat16, device=self.device)
-                n_seg = G * rk.n_hosted
-                ws = torch.empty(int(L.hep_moe_ffn_workspace(n_seg, R, rk.n_slots)), dtype=torch.uint8,
-                                 device=self.device)
-                ck(L.hep_moe_expert_ffn(recv.data_ptr(), rk.w13.data_ptr(), rk.w2.data_ptr(), b["seg"].data_ptr(),
-                                        n_seg, R, d, F, rk.n_slots, h.data_ptr(), y.data_ptr(), ws.data_ptr(),
-                                        ws.numel(), rk.sched.status.data_ptr(), s), "hep_moe_expert_ffn")
+                self._ffn_rows(rk, recv, b["seg"], G, y)
             return y[:R]
         # training: per-slot 64-row aligned blocks (weight-gradient GEMMs), pre-activations kept
         ns = rk.n_slots
