@@ -382,6 +382,12 @@ int hep_moe_dispatch_p2p(const void *d_x, const int32_t *d_tok_row, int64_t T, i
                          const int32_t *d_status, void *stream);
 int hep_moe_return_addr(const int64_t *d_pair, int rank, int num_gpus, const uint64_t *d_peer_back, int64_t row_bytes,
                         int64_t capacity, uint64_t *d_addr, void *stream);
+/* hep_moe_return_addr for received rows regrouped per weight slot: receive row i's return
+ * address goes to d_addr[d_row_map[i]] (d_row_map from hep_moe_ep_train_layout), so the
+ * FFN on the regrouped rows stores every output row straight to its source. */
+int hep_moe_return_addr_map(const int64_t *d_pair, int rank, int num_gpus, const uint64_t *d_peer_back,
+                            int64_t row_bytes, int64_t capacity, const int32_t *d_row_map, uint64_t *d_addr,
+                            void *stream);
 /* Received rows back to their sources (the NVLink return of the training path): row
  * d_src[d_row_map ? d_row_map[i] : i] -> d_addr[i] (hep_moe_return_addr's table), for i below
  * this rank's received count (sum_s pair[s][rank], at most capacity); nothing when d_status is

@@ -93,6 +93,7 @@ SIGNATURES = {
     "hep_moe_rows_to_addr": (ctypes.c_int, [vp, vp, vp, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, vp, vp, vp]),
     "hep_moe_dispatch_p2p": (ctypes.c_int, [vp, vp, ctypes.c_int64, ctypes.c_int, ctypes.c_int64, ctypes.c_int, ctypes.c_int, vp, vp, ctypes.c_int64, vp, vp]),
     "hep_moe_return_addr": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int64, ctypes.c_int64, vp, vp]),
+    "hep_moe_return_addr_map": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp, ctypes.c_int64, ctypes.c_int64, vp, vp, vp]),
     "hep_moe_expert_ffn_p2p": (ctypes.c_int, [vp, vp, vp, vp, ctypes.c_int, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int64, ctypes.c_int, vp, vp, vp, ctypes.c_size_t, vp, vp]),
     "hep_p2p_barrier": (ctypes.c_int, [vp, vp, ctypes.c_int, ctypes.c_int, vp]),
     "hep_p2p_allgather": (ctypes.c_int, [vp, ctypes.c_int64, vp, vp, vp, ctypes.c_int, ctypes.c_int, vp]),

@@ -86,7 +86,8 @@ __global__ void __launch_bounds__(256) dispatch_p2p_kernel(const int4 *__restric
 }
 
 __global__ void return_addr_kernel(const int64_t *__restrict__ pair, int me, int G, const uint64_t *__restrict__ peer_back,
-                                   int64_t row_bytes, int64_t cap, uint64_t *__restrict__ addr) {
+                                   int64_t row_bytes, int64_t cap, uint64_t *__restrict__ addr,
+                                   const int32_t *__restrict__ row_map = nullptr) {
     __shared__ int64_t rb[HEP_MAX_GPUS + 1], sb[HEP_MAX_GPUS];
     if (threadIdx.x == 0) {
         // this rank as destination: receive chunk s starts at rb[s]; source s sent it from
@@ -106,7 +107,11 @@ __global__ void return_addr_kernel(const int64_t *__restrict__ pair, int me, int
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         int s = 0;
         while (s + 1 < G && i >= rb[s + 1]) ++s;
-        addr[i] = peer_back[s] + (uint64_t)((sb[s] + i - rb[s]) * row_bytes);
+        const uint64_t a = peer_back[s] + (uint64_t)((sb[s] + i - rb[s]) * row_bytes);
+        if (row_map)  // receive row i now sits at row_map[i] (rows regrouped per weight slot)
+            addr[row_map[i]] = a;
+        else
+            addr[i] = a;
     }
 }
 
@@ -242,6 +247,21 @@ extern "C" int hep_moe_rows_to_addr(const void *d_src, const int32_t *d_row_map,
     const int64_t warps = capacity < 148 * 64 ? capacity : 148 * 64;
     rows_to_addr_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
         (const int4 *)d_src, d_row_map, d_pair, rank, num_gpus, capacity, d_model / 8, d_addr, d_status);
+    HEP_CHECK_LAUNCH();
+    return HEP_OK;
+}
+
+extern "C" int hep_moe_return_addr_map(const int64_t *d_pair, int rank, int num_gpus, const uint64_t *d_peer_back,
+                                       int64_t row_bytes, int64_t capacity, const int32_t *d_row_map, uint64_t *d_addr,
+                                       void *stream) {
+    HEP_NVTX("hep_moe_return_addr");
+    HEP_REQUIRE(d_pair && d_peer_back && d_addr, HEP_E_CONTRACT, "hep_moe_return_addr: null pointer");
+    HEP_REQUIRE(num_gpus >= 1 && num_gpus <= HEP_MAX_GPUS && rank >= 0 && rank < num_gpus && row_bytes % 16 == 0,
+                HEP_E_DIMENSION, "hep_moe_return_addr: G, rank, row_bytes %% 16");
+    if (capacity <= 0) return HEP_OK;
+    const int64_t blocks = (capacity + 255) / 256 < 148 * 4 ? (capacity + 255) / 256 : 148 * 4;
+    return_addr_kernel<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(d_pair, rank, num_gpus, d_peer_back,
+                                                                           row_bytes, capacity, d_addr, d_row_map);
     HEP_CHECK_LAUNCH();
     return HEP_OK;
 }

@@ -222,6 +222,14 @@ class EPRank:
             n_seg = max(G * self.n_hosted, 1)
             b["ffn_ws"] = torch.empty(max(int(L.hep_moe_ffn_workspace(n_seg, cap, self.n_slots)), 256),
                                       dtype=torch.uint8, device=dev)
+            if not layer.train_mode and layer.regroup_rows:  # received rows regrouped per weight slot
+                ns = self.n_slots
+                b.update(row_map_g=torch.empty(cap, dtype=torch.int32, device=dev),
+                         seg_g=torch.empty(ns, 4, dtype=torch.int32, device=dev),
+                         slot_rows_g=torch.empty(ns + 1, dtype=torch.int64, device=dev),
+                         rows_g=torch.empty(cap, d, dtype=torch.bfloat16, device=dev),
+                         ffn_ws_g=torch.empty(max(int(L.hep_moe_ffn_workspace(ns, cap, ns)), 256), dtype=torch.uint8,
+                                              device=dev))
             if layer.train_mode:  # NVLink training: the backward's two exchanges and the aligned layout
                 F, ns = layer.F, self.n_slots
                 Ral = cap + 63 * ns
@@ -317,8 +325,9 @@ class EPMoELayer:
         w1, w2, w3 = init_expert_weights(self.E, d_model, ffn, seed, self.device)
         self.ranks = [EPRank(self, r, w1, w2, w3) for r in ranks]
         del w1, w2, w3
-        # NCCL path, inference: regroup the received rows per local weight slot before the FFN
-        # (see _ffn_rows); False runs the FFN on the [src][expert] runs directly
+        # inference: regroup the received rows per local weight slot before the FFN (NCCL path:
+        # _ffn_rows; NVLink path: the return addresses move with the rows); False runs the FFN
+        # on the [src][expert] runs directly
         self.regroup_rows = True
 
     @torch.no_grad()
@@ -462,8 +471,16 @@ class EPMoELayer:
                                       rk.sched.status.data_ptr(), s), "hep_moe_dispatch_p2p")
             if "a2a" in ev:
                 ev["a2a"][1].record(st)
-            ck(L.hep_moe_return_addr(rk.sched.transfer.data_ptr(), rk.rank, G, p_back.data_ptr(), d * 2, b["cap"],
-                                     b["y_addr"].data_ptr(), s), "hep_moe_return_addr")
+            if "row_map_g" in b:  # regrouped: the receive rows per weight slot, their return addresses with them
+                ck(L.hep_moe_ep_train_layout(b["seg"].data_ptr(), rk.n_hosted, G, rk.n_slots, 1,
+                                             b["row_map_g"].data_ptr(), b["cap"], b["seg_g"].data_ptr(),
+                                             b["slot_rows_g"].data_ptr(), s), "hep_moe_ep_train_layout")
+                ck(L.hep_moe_return_addr_map(rk.sched.transfer.data_ptr(), rk.rank, G, p_back.data_ptr(), d * 2,
+                                             b["cap"], b["row_map_g"].data_ptr(), b["y_addr"].data_ptr(), s),
+                   "hep_moe_return_addr_map")
+            else:
+                ck(L.hep_moe_return_addr(rk.sched.transfer.data_ptr(), rk.rank, G, p_back.data_ptr(), d * 2, b["cap"],
+                                         b["y_addr"].data_ptr(), s), "hep_moe_return_addr")
         if sync:
             self._device_barrier(s)  # every receive buffer complete
         else:
@@ -477,7 +494,15 @@ class EPMoELayer:
                 self._train_ffn_p2p(rk, b, s)
                 b["x"] = x
                 continue
-            if n_seg:
+            if n_seg and "row_map_g" in b:  # one run per weight slot; outputs still go straight to the sources
+                ck(L.hep_moe_permute(b["recv"].data_ptr(), b["row_map_g"].data_ptr(), b["cap"], 1, d,
+                                     b["rows_g"].data_ptr(), s), "hep_moe_permute(regroup)")
+                ck(L.hep_moe_expert_ffn_p2p(b["rows_g"].data_ptr(), rk.w13.data_ptr(), rk.w2.data_ptr(),
+                                            b["seg_g"].data_ptr(), rk.n_slots, b["cap"], x_rows * K, d, F, rk.n_slots,
+                                            b["h"].data_ptr(), b["y_addr"].data_ptr(), b["ffn_ws_g"].data_ptr(),
+                                            b["ffn_ws_g"].numel(), rk.sched.status.data_ptr(), s),
+                   "hep_moe_expert_ffn_p2p")
+            elif n_seg:
                 ck(L.hep_moe_expert_ffn_p2p(b["recv"].data_ptr(), rk.w13.data_ptr(), rk.w2.data_ptr(),
                                             b["seg"].data_ptr(), n_seg, b["cap"], x_rows * K, d, F, rk.n_slots,
                                             b["h"].data_ptr(),

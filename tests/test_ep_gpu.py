@@ -157,11 +157,18 @@ def test_local_ep_p2p_exchange_matches_collectives(P, G, E, K, d, F, T, kind, s)
     ref = torch.cat([o.clone() for o in a.forward(xs)])
     got = torch.cat([o.clone() for o in b.forward(xs)])
     got2 = torch.cat([o.clone() for o in b.forward(xs)])  # buffers reused across micro-batches
+    # both exchanges without the per-slot regrouping of the received rows
+    c = EPMoELayer(pl, d, F, K, LocalComm(G), range(G), seed=6, gate_bias=bias, exchange="p2p")
+    c.regroup_rows = False
+    a.regroup_rows = False
+    got3 = torch.cat([o.clone() for o in c.forward(xs)])
+    ref3 = torch.cat([o.clone() for o in a.forward(xs)])
     torch.cuda.synchronize()
     for rk in b.ranks:
         rk.sched.check_status("p2p")
     assert torch.equal(got, ref)
     assert torch.equal(got2, ref)
+    assert torch.equal(got3, ref) and torch.equal(ref3, ref)
     sim = P.MoELayer(pl, d, F, K, seed=6, gate_bias=bias)
     assert torch.equal(sim(x), ref)
 

@@ -25,6 +25,7 @@ ap.add_argument("--configs", default="qwen3,dsv3")
 ap.add_argument("--ratio", type=float, default=0.5)
 ap.add_argument("--rounds", type=int, default=5)
 ap.add_argument("--iters", type=int, default=5)
+ap.add_argument("--p2p", action="store_true", help="the NVLink peer-store exchange with and without regrouping instead")
 args = ap.parse_args()
 dev = torch.device("cuda", 0)
 for cfg in args.configs.split(","):
@@ -33,11 +34,17 @@ for cfg in args.configs.split(","):
     bias = torch.tensor(P.zipf_gate_bias(E, 1.0, 0))
     x = torch.randn(T, d, generator=torch.Generator(device=dev).manual_seed(1000), device=dev).to(torch.bfloat16)
     xs = [x[r * (T // G):(r + 1) * (T // G)].contiguous() for r in range(G)]
-    layers = {"plain": EPMoELayer(pl, d, F, K, LocalComm(G), range(G), seed=0, gate_bias=bias),
-              "plain, no regroup": EPMoELayer(pl, d, F, K, LocalComm(G), range(G), seed=0, gate_bias=bias),
-              f"pipelined {args.ratio}": EPMoELayer(pl, d, F, K, LocalComm(G), range(G), seed=0, gate_bias=bias,
-                                                    pipeline_ratio=args.ratio)}
-    layers["plain, no regroup"].regroup_rows = False
+    layers = {"plain": EPMoELayer(pl, d, F, K, LocalComm(G), range(G), seed=0, gate_bias=bias)}
+    if not args.p2p:  # (DeepSeek-V3: each 8-rank layer holds 45 GB of expert weights)
+        layers["plain, no regroup"] = EPMoELayer(pl, d, F, K, LocalComm(G), range(G), seed=0, gate_bias=bias)
+        layers["plain, no regroup"].regroup_rows = False
+        layers[f"pipelined {args.ratio}"] = EPMoELayer(pl, d, F, K, LocalComm(G), range(G), seed=0, gate_bias=bias,
+                                                       pipeline_ratio=args.ratio)
+    else:
+        layers["p2p"] = EPMoELayer(pl, d, F, K, LocalComm(G), range(G), seed=0, gate_bias=bias, exchange="p2p")
+        layers["p2p, no regroup"] = EPMoELayer(pl, d, F, K, LocalComm(G), range(G), seed=0, gate_bias=bias,
+                                               exchange="p2p")
+        layers["p2p, no regroup"].regroup_rows = False
     outs, res = {}, {k: [] for k in layers}
     for k, lay in layers.items():
         for _ in range(2):
