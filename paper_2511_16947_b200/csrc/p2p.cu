@@ -108,10 +108,12 @@ __global__ void return_addr_kernel(const int64_t *__restrict__ pair, int me, int
         int s = 0;
         while (s + 1 < G && i >= rb[s + 1]) ++s;
         const uint64_t a = peer_back[s] + (uint64_t)((sb[s] + i - rb[s]) * row_bytes);
-        if (row_map)  // receive row i now sits at row_map[i] (rows regrouped per weight slot)
-            addr[row_map[i]] = a;
-        else
+        if (row_map) {  // receive row i now sits at row_map[i] (rows regrouped per weight slot); -1 =
+            const int32_t j = row_map[i];  // no such row (an empty exchange after a capacity overflow)
+            if (j >= 0) addr[j] = a;
+        } else {
             addr[i] = a;
+        }
     }
 }
 
