@@ -5,12 +5,13 @@
     compute-sanitizer --tool synccheck python tools/sanitize.py
 
 Covers: fused router+gate (one and two epilogue column halves, 64-aligned and
-chunk-straddling tiles), the scheduler (solve / integerize / route / transfer,
+chunk-straddling tiles, CTA pairs, in-kernel histogram zeroing), the scheduler (solve / integerize / route / transfer,
 pipelined split on two streams), the assignment kernels, permute (128/256-bit),
 the expert FFN (1-CTA and CTA-pair grouped GEMMs, light-expert split), combine,
 the backward (dgrad / K-ragged wgrad / router backward), and the EP exchange
 over peer stores with all ranks in one process (dispatch, return addresses,
-the down-projection epilogue storing into the sources' buffers)."""
+the down-projection epilogue storing into the sources' buffers, rows regrouped per slot)
+and the EP pipelined split."""
 import os
 import sys
 
@@ -46,6 +47,14 @@ def main():
         torch.cuda.synchronize()
         layer.check_status()
         print("router tile 80: ok", flush=True)
+    # router on CTA pairs (E_pad > 128), histogram zeroed in the kernel (the layer's default entry)
+    with _lib.tuning(router_pair=2):
+        pl = P.cayley_symmetric(P.ClusterShape(8, 256, 2))
+        layer = P.MoELayer(pl, 256, 256, 8, seed=5, gate_bias=torch.tensor(P.zipf_gate_bias(256, 1.0, 0)))
+        layer(torch.randn(4096, 256, generator=g, device="cuda").to(torch.bfloat16))
+        torch.cuda.synchronize()
+        layer.check_status()
+        print("router CTA pairs E=256: ok", flush=True)
     # pipelined split on two streams
     pl = P.cayley_symmetric(P.ClusterShape(8, 16, 2))
     pip = P.MoELayer(pl, 256, 256, 2, seed=3, gate_bias=torch.tensor(P.zipf_gate_bias(16, 1.2, 1)), pipeline_ratio=0.5)
@@ -64,6 +73,16 @@ def main():
         torch.cuda.synchronize()
         ep.check_status()
         print(f"EP LocalComm {exchange}: ok", flush=True)
+    # EP pipelined split (static share exchanged on a side stream), rows regrouped per slot
+    G, E, K, d, F, T = 4, 16, 2, 256, 256, 2048
+    pl = P.cayley_symmetric(P.ClusterShape(G, E, 2))
+    ep = EPMoELayer(pl, d, F, K, LocalComm(G), range(G), seed=6, gate_bias=torch.tensor(P.zipf_gate_bias(E, 1.0, 0)),
+                    pipeline_ratio=0.5)
+    x = torch.randn(T, d, generator=g, device="cuda").to(torch.bfloat16)
+    ep.forward([x[r * (T // G):(r + 1) * (T // G)].contiguous() for r in range(G)])
+    torch.cuda.synchronize()
+    ep.check_status()
+    print("EP pipelined split: ok", flush=True)
     print("sanitize run complete")
 
 
