@@ -73,7 +73,8 @@ typedef struct {
                                (0 auto, 1 off, 2 or 4) */
     int router_pair;        /* router GEMM on CTA pairs (cta_group::2, half the Wg tile per CTA): 0 auto (E_pad > 128),
                                1 off, 2 on (E_pad > 64) */
-    int reserved[2];
+    int wgrad_wave_sync;    /* 1: the weight-gradient CTA-pair GEMMs start each wave of tiles together */
+    int reserved[1];
 } hep_tuning;
 int hep_tuning_get(hep_tuning *out);
 int hep_tuning_set(const hep_tuning *in);

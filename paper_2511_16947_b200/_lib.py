@@ -36,13 +36,13 @@ class HepSchedOut(ctypes.Structure):
 
 TUNING_FIELDS = ("st256", "pair_wait_cluster", "ffn_pair", "ffn_light_rows", "wgrad_order", "l2_policy",
                  "light_first", "raster_gm1", "raster_gm2", "sched_lexmin_warps", "lsu256", "ffn_clock",
-                 "router_tile_rows", "pair_wave_sync", "lp_dsm", "light_wave_sync", "router_mc", "router_pair")
+                 "router_tile_rows", "pair_wave_sync", "lp_dsm", "light_wave_sync", "router_mc", "router_pair", "wgrad_wave_sync")
 
 
 class HepTuning(ctypes.Structure):
     """``hep_tuning`` (include/hep.h): process-wide launch tuning, -1 = default."""
 
-    _fields_ = [(f, ctypes.c_int) for f in TUNING_FIELDS] + [("reserved", ctypes.c_int * 2)]
+    _fields_ = [(f, ctypes.c_int) for f in TUNING_FIELDS] + [("reserved", ctypes.c_int * 1)]
 
 
 # (name, restype, argtypes) for every symbol declared in include/hep.h

@@ -1461,7 +1461,7 @@ __global__ void __launch_bounds__(32 * kTileWarps) tile_write_kernel(const int32
                                                                      int64_t cap, int32_t *status, int tile_rows,
                                                                      unsigned int *zero2) {
     extern __shared__ int4 st[];
-    if (zero2 && blockIdx.x == 0 && threadIdx.x < 4) zero2[threadIdx.x] = 0u;  // the expert GEMMs' wave counters
+    if (zero2 && blockIdx.x == 0 && threadIdx.x < 8) zero2[threadIdx.x] = 0u;  // the expert GEMMs' wave counters
     __shared__ int64_t scan[64];
     __shared__ int64_t off_sm[kTileWarps];
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5;
@@ -1616,7 +1616,10 @@ static int launch2sm_maps(const CUtensorMap &ta, const CUtensorMap &tb, const Pa
     Params p = with_store_width<EPI>(p0);
     p.wait_cluster = g_tuning.pair_wait_cluster == 1;
     // wave-synchronised producers only for long tiles (hep_tuning.pair_wave_sync k-blocks)
-    if (g_tuning.pair_wave_sync <= 0 || p.kblocks < g_tuning.pair_wave_sync || p.grouped != 1 || p.gather_idx)
+    // (grouped == 2, the K-ragged weight gradients: only when the caller set the counter,
+    // hep_tuning.wgrad_wave_sync)
+    if (p.grouped != 2 &&
+        (g_tuning.pair_wave_sync <= 0 || p.kblocks < g_tuning.pair_wave_sync || p.grouped != 1 || p.gather_idx))
         p.wave_ctr = nullptr;
     auto kern = gemm2sm_kernel<STAGES, EPI, A_MN, B_MN>;
     HEP_CHECK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::BYTES));
@@ -2098,8 +2101,10 @@ extern "C" int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, con
     // light experts on a 1-CTA tile list, as in the forward (the weight-gradient GEMMs
     // contract over the rows, so only the two dgrad GEMMs have row tiles to split)
     const int light_max = pairs ? ffn_light_max(Rcap, n_experts, false) : 0;
+    // wave counters 4 / 5 of the workspace tail: the weight-gradient pair GEMMs (hep_tuning.wgrad_wave_sync)
+    unsigned int *wave_ctr = ffn_wave_ctr(d_workspace, cap, n_experts);
     if ((rc = build_tiles(d_seg, n_seg, n_experts, mt_row0, mt_rows, exp_off, exp_off + n_experts + 1, cap, d_status,
-                          pairs ? kPairRows : BM, s, light_max, 0)))
+                          pairs ? kPairRows : BM, s, light_max, 0, wave_ctr)))
         return rc;
     int32_t *mt_row0_l = exp_off + 2 * (n_experts + 1);
     int32_t *mt_rows_l = mt_row0_l + cap;
@@ -2171,6 +2176,7 @@ extern "C" int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, con
     q.ld_out = ffn;
     q.out_cols = ffn;
     q.out_exp_stride = d_model * ffn;
+    if (g_tuning.wgrad_wave_sync) q.wave_ctr = wave_ctr + 4;
     if ((rc = make_tmap_mn(&ta, d_dy, (uint64_t)Rcap, (uint64_t)d_model))) return rc;
     if ((rc = make_tmap_mn(&tb, d_h, (uint64_t)Rcap, (uint64_t)ffn))) return rc;
     if ((rc = pairs ? launch2sm_maps<6, EPI_F32, true, true>(ta, tb, q, s)
@@ -2184,6 +2190,7 @@ extern "C" int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, con
     q.ld_out = d_model;
     q.out_cols = d_model;
     q.out_exp_stride = 2 * ffn * d_model;
+    if (g_tuning.wgrad_wave_sync) q.wave_ctr = wave_ctr + 5;
     if ((rc = make_tmap_mn(&ta, d_da13, (uint64_t)Rcap, (uint64_t)(2 * ffn)))) return rc;
     if ((rc = make_tmap_mn(&tb, d_rows, (uint64_t)Rcap, (uint64_t)d_model))) return rc;
     return pairs ? launch2sm_maps<6, EPI_F32, true, true>(ta, tb, q, s)
