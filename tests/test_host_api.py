@@ -193,3 +193,23 @@ def test_trace_roundtrip_and_errors(tmp_path):
     ok.write_text("microbatch,expert,gpu,tokens\n2,0,0,5\n2,0,0,6\n")
     w = P.load_trace(str(ok), shape)
     assert len(w.micro_batches) == 3 and w.micro_batches[2].entries[0][0] == 11 and w.micro_batches[0].total() == 0
+
+
+def test_tuning_struct_matches_header():
+    """hep_tuning (include/hep.h) and its ctypes mirror (_lib.HepTuning) list the same int
+    fields in the same order, reserved tail included: a mismatch would silently shift every
+    tuning knob after it.  The library's defaults round-trip through hep_tuning_get / set."""
+    import re
+
+    from paper_2511_16947_b200 import _lib
+
+    hdr = open(os.path.join(ROOT, "include", "hep.h")).read()
+    body = re.search(r"typedef struct \{(.*?)\} hep_tuning;", hdr, re.S).group(1)
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = re.findall(r"int\s+(\w+)\s*(?:\[(\d+)\])?\s*;", body)
+    names = [f for f, n in fields if not n]
+    reserved = [int(n) for f, n in fields if n]
+    assert tuple(names) == _lib.TUNING_FIELDS
+    assert reserved == [dict(_lib.HepTuning._fields_)["reserved"]._length_]
+    t = _lib.get_tuning()
+    assert set(t) == set(_lib.TUNING_FIELDS)
