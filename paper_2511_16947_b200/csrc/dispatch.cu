@@ -78,7 +78,7 @@ __global__ void plan_prep_kernel(int G, int E, int nnz, const int32_t *grp_off, 
                                  const int32_t *sorted, const int32_t *nnz_exp, const int64_t *xi,
                                  const int64_t *ranges, const int64_t *n_ranges_p, int64_t *expert_rows,
                                  int32_t *seg, AssignWs w, int32_t *status, int row_align,
-                                 const int64_t *split, int phase, int64_t stage_cap) {
+                                 const int64_t *split, int phase, int64_t stage_cap, int meta_staged) {
     __shared__ int64_t scan[64];
     const int tid = threadIdx.x, nt = blockDim.x;
     // pipelined split: split = [2][E][G] (static share, scheduled share); this phase's ranks of
@@ -101,11 +101,30 @@ __global__ void plan_prep_kernel(int G, int E, int nnz, const int32_t *grp_off, 
     extern __shared__ int4 s_dyn[];
     int32_t *s_cnt = reinterpret_cast<int32_t *>(s_dyn);
     int4 *s_rng = s_dyn + (E * G + 3) / 4;
+    if (meta_staged) {
+        // one CTA walks chains of dependent reads (sorted -> xi, grp_off -> grp_gpu) below:
+        // stage the small plan arrays in shared memory first, all loads in flight at once
+        int64_t *s_xi = reinterpret_cast<int64_t *>(s_rng + stage_cap);
+        int32_t *s_off = reinterpret_cast<int32_t *>(s_xi + nnz);
+        int32_t *s_sorted = s_off + E + 1;
+        int32_t *s_gpu = s_sorted + nnz;
+        for (int i = tid; i < nnz; i += nt) {
+            s_xi[i] = xi[i];
+            s_sorted[i] = sorted[i];
+            s_gpu[i] = grp_gpu[i];
+        }
+        for (int i = tid; i <= E; i += nt) s_off[i] = grp_off[i];
+        xi = s_xi;
+        grp_off = s_off;
+        sorted = s_sorted;
+        grp_gpu = s_gpu;
+    }
     for (int i = tid; i < E * G; i += nt) {
         s_cnt[i] = 0;
         w.es_lo[i] = rank_base ? (int32_t)rank_base[i] : 0;
     }
     for (int i = tid; i <= E; i += nt) w.first[i] = -1;
+    if (meta_staged) __syncthreads();
     // expert blocks ([expert][dst asc][src][rank]), each starting on a row_align boundary
     // (64 in training so weight-gradient GEMMs contract over whole 64-row blocks).  Pipelined
     // split: [expert][phase][dst][src][rank] -- expert e's block holds both phases (its size
@@ -629,12 +648,15 @@ static int assign_impl(hep_sched_t h, const hep_sched_out *sched, bool windowed,
     HEP_REQUIRE(cnt_sm <= kPrepSmemMax, HEP_E_CAPACITY, "plan_prep: E*G too large");
     int64_t stage_cap = h->max_ranges;
     if (cnt_sm + 16 * stage_cap > kPrepSmemMax) stage_cap = 0;  // too large to stage: read the table from global
-    const size_t prep_sm = cnt_sm + 16 * (size_t)stage_cap;
+    // + the plan arrays (xi, grp_off, sorted, grp_gpu) when they fit too
+    const size_t meta_sm = 16 * (((size_t)h->nnz * 16 + 4 * ((size_t)E + 1) + 15) / 16);
+    const int meta_staged = cnt_sm + 16 * (size_t)stage_cap + meta_sm <= kPrepSmemMax;
+    const size_t prep_sm = cnt_sm + 16 * (size_t)stage_cap + (meta_staged ? meta_sm : 0);
     if (prep_sm + 512 > 48 * 1024)  // + the kernel's static scan buffer
         HEP_CHECK_CUDA(cudaFuncSetAttribute(plan_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPrepSmemMax));
     plan_prep_kernel<<<1, 512, prep_sm, s>>>(G, E, h->nnz, h->d_grp_off, h->d_grp_gpu, h->d_sorted, h->d_nnz_exp,
                                              sched->d_xi, sched->d_ranges, sched->d_n_ranges, d_expert_rows, d_seg, w,
-                                             sched->d_status, row_align, d_split, phase, stage_cap);
+                                             sched->d_status, row_align, d_split, phase, stage_cap, meta_staged);
     HEP_CHECK_LAUNCH();
     if (T <= 0) return HEP_OK;
     const int ncs = (int)((tokens_per_src + kChunk - 1) / kChunk);
