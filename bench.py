@@ -409,10 +409,11 @@ def run_ep(args, world, rank, local, dev):
             "comm": comm_info,
             "e2e": {"value": world * T * args.steps / (e_ms / 1e3), "unit": "tokens/s",
                     "h2d_bytes_per_step": T * d * 2, "d2h_bytes_per_step": T * d * 2},
-            # router, scheduler, assignment (4), permute, FFN (4), combine = 12; the NVLink path adds
-            # the dispatch kernel; the pipelined split adds the split kernel, the static phase's
-            # scheduler launch, a second assignment (4) and permute = 19
-            "gpu_launches": args.steps * (13 if args.exchange == "p2p" else (19 if layer.static_share is not None else 12)),
+            # router, scheduler, assignment (4), permute, FFN (4), combine = 12, + the per-slot
+            # regrouping (layout, permute, gather back) = 15; the NVLink path: 13 + layout and
+            # regroup permute = 15; the pipelined split adds the split kernel, the static phase's
+            # scheduler launch, a second assignment (4) and permute = 22
+            "gpu_launches": args.steps * (15 if args.exchange == "p2p" else (22 if layer.static_share is not None else 15)),
             "roofline": {"bound": "tensor", "kernel": "hep_moe_expert_ffn on the received rows (rank 0)",
                          "achieved": ffn_tf, "peak": tf_sus, "unit": "TFLOP/s", "frac": ffn_tf / tf_sus,
                          "min_over_ranks": min_tf, "rows_rank0": R,
