@@ -661,6 +661,15 @@ def measure_config(cfg, args, dev, *, steps, primary):
     # expert loads into the LoadHistory, the adaptive check after them (seen batches only)
     adaptive = args.placement == "adaptive" and layer.static_share is None
     runner = LayerRunner(layer, _policy(n_seen) if adaptive else None, shape=shape)
+    # the router+gate's own rate, taken before any FFN step heats the GPU: the router
+    # (HBM-bound mainloop, ALU-bound epilogue) runs ~10-20 % slower for seconds after FFN
+    # bursts (profiles/r02/router_ab_r02d.txt --hot); the in-step rate is reported beside
+    b0 = layer.buffers(T)
+    rg_early = []
+    for xb in unseen[:4]:
+        layer.run(xb, b0, stream)
+        rg_early.append(hbm_b2b_ms(layer, b0, xb, stream)[2])
+    rg_early = statistics.median(rg_early)
     for i in range(max(n_seen, args.warmup)):
         runner.step(seen[i % n_seen])
     torch.cuda.synchronize()
@@ -687,10 +696,17 @@ def measure_config(cfg, args, dev, *, steps, primary):
     # warm-up's FFN work leaves the GPU power-capped for a while (the router right after FFN
     # bursts runs ~20 % slower, profiles/r02/router_ab_r02d.txt --hot): rest 2 s first so this
     # figure is taken at the nominal clock
+    # figure is taken at the nominal clock.  Median over 4 held-out micro-batches: the rate
+    # moves a few % with where the 134-235 MB input happens to be allocated
+    # (profiles/r02/router_ab_r02l.txt vs the bench line)
     layer.run(unseen[0], bufs, stream)
     torch.cuda.synchronize()
     time.sleep(2.0)
-    hbm_b2b_before = hbm_b2b_ms(layer, bufs, unseen[0], stream)
+    per_x = []
+    for xb in unseen[:4]:
+        layer.run(xb, bufs, stream)  # its row map for the permute / combine
+        per_x.append(hbm_b2b_ms(layer, bufs, xb, stream))
+    hbm_b2b_before = (statistics.median(v[0] for v in per_x), statistics.median(v[1] for v in per_x), rg_early)
     layer.run(unseen[0], bufs, stream)
     torch.cuda.synchronize()
 
@@ -912,7 +928,8 @@ def hbm_block(before, after, nbytes, hbm, traffic, router_flops=None, tf_burst=N
         out["router_gate"]["roofline_us"] = {"hbm": t_hbm, "tensor": t_tc, "bound": "hbm" if t_hbm >= t_tc else "tensor",
                                              "frac_of_bound": max(t_hbm, t_tc) / us}
     out["timing"] = ("each kernel re-launched 20x back to back on a held-out micro-batch inside one CUDA graph, "
-                     "median of 5 timed replays after 5 warm ones; before the timed region after a 2 s rest (the kernel's rate at "
+                     "median of 5 timed replays after 5 warm ones, median over 4 held-out micro-batches; permute / combine "
+                     "before the timed region after a 2 s rest, the router before the warm-up steps (the kernels' rate at "
                      "the nominal clock) and right after it (after the power-capped FFN steps: the in-step rate)")
     out["peak_GB/s"] = hbm
     return out
