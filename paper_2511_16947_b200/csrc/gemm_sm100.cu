@@ -1895,8 +1895,13 @@ static int expert_ffn_fwd(const void *d_rows, const void *d_w13, const void *d_w
 // heavy/light split of the forward FFN (see expert_ffn_fwd): light_max rows or 0
 static int ffn_light_max(int64_t R, int n_experts, bool gather) {
     // experts up to one pair tile (256 rows) run as 128-row tiles: DeepSeek-V3 shape FFN
-    // 14.18 -> 12.95 ms (threshold 128: 13.08), Qwen3 unchanged (profiles/r01/ab_light_r01k.txt)
-    return (use_pairs(R, n_experts) && n_experts >= 32 && !gather) ? g_tuning.ffn_light_rows : 0;
+    // 14.18 -> 12.95 ms (threshold 128: 13.08) (profiles/r01/ab_light_r01k.txt).  Only when
+    // experts average under 1024 rows (many light experts): at the Qwen3 shape (2048 rows
+    // per expert, a few dozen light ones) the two extra GEMM launches cost more than the
+    // half-empty pair tiles, 1.95 -> 1.88 ms without the split (profiles/r02/ab_light_r02l.txt)
+    return (use_pairs(R, n_experts) && n_experts >= 32 && !gather && R < 1024 * (int64_t)n_experts)
+               ? g_tuning.ffn_light_rows
+               : 0;
 }
 
 extern "C" int hep_moe_ffn_launches(int64_t R, int n_experts, int gather) {
