@@ -74,6 +74,7 @@ typedef struct {
     int router_pair;        /* router GEMM on CTA pairs (cta_group::2, half the Wg tile per CTA): 0 auto (E_pad > 128),
                                1 off, 2 on (E_pad > 64) */
     int wgrad_wave_sync;    /* 1: the weight-gradient CTA-pair GEMMs start each wave of tiles together */
+    int wgrad_raster;       /* 1: weight-gradient tiles walk the shorter tile dimension fastest */
     int reserved[1];
 } hep_tuning;
 int hep_tuning_get(hep_tuning *out);
