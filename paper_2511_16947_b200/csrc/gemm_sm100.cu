@@ -2148,6 +2148,9 @@ extern "C" int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, con
     p.out_cols = 2 * ffn;
     p.aux = const_cast<void *>(d_pre);
     p.ld_aux = 2 * ffn;
+    // the two dgrad pair GEMMs start their waves together like the forward's (counters 6 / 7;
+    // launch2sm_maps keeps the counter only for tiles of >= pair_wave_sync k-blocks)
+    p.wave_ctr = wave_ctr + 6;
     if ((rc = make_tmap(&ta, d_dy, (uint64_t)Rcap, (uint64_t)d_model, pairs ? 128 : BM))) return rc;
     if ((rc = make_tmap_mn(&tb, d_w2, (uint64_t)n_experts * d_model, (uint64_t)ffn))) return rc;
     if ((rc = pairs ? launch2sm_maps<6, EPI_SWIGLU_BWD, false, true>(ta, tb, p, s)
@@ -2155,6 +2158,7 @@ extern "C" int hep_moe_expert_ffn_bwd(const void *d_rows, const void *d_pre, con
         return rc;
     if (light_max > 0 && (rc = launch_maps<256, 4, EPI_SWIGLU_BWD, false, true>(ta, tb, light_list(p), 0, s)))
         return rc;
+    p.wave_ctr = wave_ctr + 7;
     if ((rc = hep_moe_zero_padding(d_expert_rows, d_seg, n_seg, n_experts, d_da13, 2 * ffn, stream))) return rc;
     // --- dX_rows = dA13 W13
     p.kblocks = (int)(2 * ffn / BK);
