@@ -8,14 +8,19 @@
 //               (M=128, N=BN, K=16 per instruction, fp32 accumulator in TMEM,
 //               two accumulator buffers so the epilogue of tile i overlaps
 //               the MMAs of tile i+1)
-//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> fused op -> global
+//   warps 2..9  epilogue, two warps per TMEM lane quarter (column halves):
+//               tcgen05.ld TMEM -> registers -> fused op -> global
 //               (EPI_SWIGLU: silu(gate) * up -> bf16 H, the first expert GEMM;
-//                EPI_BF16: plain bf16 store, the down projection;
-//                EPI_F32: fp32 logits, the router GEMM)
+//                EPI_BF16: plain bf16 store, the down projection / dgrad;
+//                EPI_F32: fp32 output, the weight gradients;
+//                EPI_SWIGLU_BWD: the SwiGLU backward fused into the dgrad;
+//                EPI_GATE: the router GEMM with top-K / softmax / histogram fused)
+// plus the CTA-pair variant (gemm2sm_kernel, cta_group::2, M = 256 per pair).
 // Grouped mode walks a device-resident m-tile list built from the scheduler's
-// segments (no host sync): tiles are ordered expert-major, then N-block, then
-// M-tile, so one expert's weight block is streamed from HBM once per wave and
-// the expert's rows stay L2-resident across its N sweep.
+// segments (no host sync): tiles are ordered expert-major, then in raster bands of
+// m-tiles swept across the N-blocks, so an expert's weight panels and rows are reused
+// from L2 within a wave; long-K tiles start each wave together (wave counters).
+// Weight gradients (mode 2) walk the shorter tile dimension fastest.
 #include <cudaTypedefs.h>
 
 #include "common.cuh"
