@@ -840,14 +840,7 @@ def measure_config(cfg, args, dev, *, steps, primary):
     # peak).  Experts with few rows (DeepSeek-V3's long tail) are weight-streaming bound, so
     # this is the FFN's time floor when experts are processed one after another
     er = bufs.expert_rows.cpu().tolist()
-    rows_e = [er[e + 1] - er[e] for e in range(E)]
-    t_e = [max(6.0 * d * F * r / (tf_sus * 1e12), (3.0 * d * F * 2 + r * (4.0 * d + 4.0 * F)) / (hbm * 1e9))
-           for r in rows_e if r > 0]
-    per_expert = {"ms": 1e3 * sum(t_e), "frac": 1e3 * sum(t_e) / ffn_ms,
-                  "hbm_bound_experts": sum(1 for r in rows_e if r > 0 and
-                                           6.0 * d * F * r / (tf_sus * 1e12) < (3.0 * d * F * 2 + r * (4.0 * d + 4.0 * F)) / (hbm * 1e9)),
-                  "experts_with_rows": sum(1 for r in rows_e if r > 0),
-                  "rows_min_max": [min(rows_e), max(rows_e)]}
+    per_expert = per_expert_roofline([er[e + 1] - er[e] for e in range(E)], d, F, tf_sus, hbm, ffn_ms)
     res = {
         "value": value, "ms_per_step": ms_per_step, "steps": steps,
         "config": {"workload": CONFIG_TEXT[cfg], "tokens_per_microbatch_per_gpu": T, "sim_ep": G,
@@ -906,6 +899,18 @@ def measure_config(cfg, args, dev, *, steps, primary):
     gc.collect()
     torch.cuda.empty_cache()
     return res
+
+
+def per_expert_roofline(rows_e, d, F, tf_sus, hbm, ffn_ms):
+    """The FFN's floor when experts run one after another, each at its own bound: tensor
+    (6*d*F flop per row at tf_sus TFLOP/s) or HBM (its three weight matrices once plus its
+    rows' X in, H out and in, Y out at hbm GB/s), whichever is longer; ms and frac of ffn_ms."""
+    t_tc = [6.0 * d * F * r / (tf_sus * 1e12) for r in rows_e]
+    t_hbm = [(3.0 * d * F * 2 + r * (4.0 * d + 4.0 * F)) / (hbm * 1e9) for r in rows_e]
+    live = [i for i, r in enumerate(rows_e) if r > 0]
+    ms = 1e3 * sum(max(t_tc[i], t_hbm[i]) for i in live)
+    return {"ms": ms, "frac": ms / ffn_ms, "hbm_bound_experts": sum(1 for i in live if t_tc[i] < t_hbm[i]),
+            "experts_with_rows": len(live), "rows_min_max": [min(rows_e), max(rows_e)]}
 
 
 def hbm_block(before, after, nbytes, hbm, traffic, router_flops=None, tf_burst=None):
