@@ -841,6 +841,10 @@ def measure_config(cfg, args, dev, *, steps, primary):
     # this is the FFN's time floor when experts are processed one after another
     er = bufs.expert_rows.cpu().tolist()
     per_expert = per_expert_roofline([er[e + 1] - er[e] for e in range(E)], d, F, tf_sus, hbm, ffn_ms)
+    # the same floor with the burst tensor peak (a kernel timed alone); the sustained one
+    # above is cuBLAS's long-run rate under the power cap, which a power-capped FFN can match
+    per_expert["frac_burst"] = per_expert_roofline([er[e + 1] - er[e] for e in range(E)], d, F, tf_burst, hbm,
+                                                   ffn_ms)["frac"]
     res = {
         "value": value, "ms_per_step": ms_per_step, "steps": steps,
         "config": {"workload": CONFIG_TEXT[cfg], "tokens_per_microbatch_per_gpu": T, "sim_ep": G,
