@@ -1703,6 +1703,10 @@ extern "C" int hep_gemm_bf16(const void *d_A, const void *d_B, void *d_D, int64_
     return launch<256, 4, EPI_BF16>(d_A, M, K, d_B, N, p, mt * p.n_tiles, s);
 }
 
+#ifndef HEP_ROUTER_STAGES_128
+#define HEP_ROUTER_STAGES_128 5  // TMA ring depth of the 128-expert router+gate (diagnostics builds vary it)
+#endif
+
 // Router tile height (hep_tuning.router_tile_rows, multiple of 16, <= 128; 0 = 128).  Shorter
 // tiles that fill every SM (16384 tokens: 147 tiles of 112 rows instead of 128 of 128) were
 // measured SLOWER (Mixtral 31.1 vs 28.7 us, Qwen3 48.7 vs 47.4, DSv3 75.5 vs 72.0,
@@ -1881,7 +1885,7 @@ extern "C" int hep_router_topk_ws(const void *d_x, const void *d_wg, int64_t T, 
     else if (e_pad <= 16) rc = launch_gate<16, 8>(d_x, d_wg, T, d_model, e_pad, p, s);
     else if (e_pad <= 32) rc = launch_gate<32, 8>(d_x, d_wg, T, d_model, e_pad, p, s);
     else if (e_pad <= 64) rc = launch_gate<64, 6>(d_x, d_wg, T, d_model, e_pad, p, s);
-    else if (e_pad <= 128) rc = launch_gate<128, 5>(d_x, d_wg, T, d_model, e_pad, p, s);
+    else if (e_pad <= 128) rc = launch_gate<128, HEP_ROUTER_STAGES_128>(d_x, d_wg, T, d_model, e_pad, p, s);
     else rc = launch_gate<256, 4>(d_x, d_wg, T, d_model, e_pad, p, s);
     if (rc || !d_chunk_cnt || chunks_fused) return rc;
     return hep_gate_chunk_counts(d_topk_idx, T, K, E, tokens_per_src, n_src, d_chunk_cnt, stream);
