@@ -31,6 +31,7 @@ def main():
     ap.add_argument("--rounds", type=int, default=4)
     ap.add_argument("--skew", type=float, default=1.0)
     ap.add_argument("--placement", default="adaptive", choices=["adaptive", "cayley"])
+    ap.add_argument("--diag", action="store_true", help="load libhep_diag.so (a diagnostics build)")
     args = ap.parse_args()
 
     import torch
@@ -39,6 +40,9 @@ def main():
     import bench
     import paper_2511_16947_b200 as P
     from paper_2511_16947_b200 import _lib
+
+    if args.diag:
+        _lib.LIB_PATH = os.path.join(ROOT, "paper_2511_16947_b200", "libhep_diag.so")
 
     E, K, d, F, T, G = bench.CONFIGS[args.config]
     dev = torch.device("cuda", 0)
