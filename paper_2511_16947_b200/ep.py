@@ -91,14 +91,21 @@ class LocalComm:
             p.copy_(acc)
 
     def all_to_all(self, sends: list[torch.Tensor], send_counts: list[list[int]],
-                   recv_counts: list[list[int]]) -> list[torch.Tensor]:
+                   recv_counts: list[list[int]], outs: list[torch.Tensor] | None = None) -> list[torch.Tensor]:
+        """outs (optional): per-rank destination tensors the received rows are written into
+        (their first sum(recv_counts) rows); returned in place of new tensors."""
         G = self.world
         offs = [_offsets(send_counts[s]) for s in range(G)]
         out = []
         for d in range(G):
             pieces = [sends[s][offs[s][d]: offs[s][d] + send_counts[s][d]] for s in range(G)]
             assert sum(p.shape[0] for p in pieces) == sum(recv_counts[d])
-            out.append(torch.cat(pieces, dim=0))
+            if outs is None:
+                out.append(torch.cat(pieces, dim=0))
+            else:
+                dst = outs[d][: sum(recv_counts[d])]
+                torch.cat(pieces, dim=0, out=dst)
+                out.append(dst)
         return out
 
 
@@ -169,12 +176,21 @@ class DistComm:
             p.copy_(q)
 
     def all_to_all(self, sends: list[torch.Tensor], send_counts: list[list[int]],
-                   recv_counts: list[list[int]]) -> list[torch.Tensor]:
+                   recv_counts: list[list[int]], outs: list[torch.Tensor] | None = None) -> list[torch.Tensor]:
+        """outs (optional): the destination tensor (its first sum(recv_counts) rows) NCCL
+        receives into, instead of a new one."""
         (s,) = sends
         q = self._h(s.contiguous())
-        recv = torch.empty((sum(recv_counts[0]),) + tuple(s.shape[1:]), dtype=s.dtype, device=q.device)
+        n = sum(recv_counts[0])
+        if outs is not None and not self.host_staged:
+            recv = outs[0][:n]
+        else:
+            recv = torch.empty((n,) + tuple(s.shape[1:]), dtype=s.dtype, device=q.device)
         self.dist.all_to_all_single(recv, q, output_split_sizes=list(recv_counts[0]),
                                     input_split_sizes=list(send_counts[0]), group=self.group)
+        if outs is not None and self.host_staged:
+            outs[0][:n].copy_(recv)
+            return [outs[0][:n]]
         return [recv.to(s.device)]
 
 
@@ -701,6 +717,8 @@ class EPMoELayer:
                 counts_ph=[torch.empty(2 * G, dtype=torch.int64, device=dev) for _ in range(2)],
                 assign_ws_ph=[torch.empty(ws, dtype=torch.uint8, device=dev) for _ in range(2)],
                 send2=torch.empty(max(2 * T * K, 1), self.d, dtype=torch.bfloat16, device=dev),
+                # both phases' received rows; at most every source's T*K assignments
+                recv2=torch.empty(max(G * T * K, 1), self.d, dtype=torch.bfloat16, device=dev),
                 back2=torch.zeros(max(2 * T * K, 1), self.d, dtype=torch.bfloat16, device=dev),
             )
         return b
@@ -746,7 +764,7 @@ class EPMoELayer:
             # the static share's split sizes (a side-stream sync: the solve keeps running)
             c0 = [b["counts_ph"][0].cpu().tolist() for b in bs]
             recv0 = self.comm.all_to_all([b["send2"][: sum(c[:G])] for b, c in zip(bs, c0)], [c[:G] for c in c0],
-                                         [c[G:] for c in c0])
+                                         [c[G:] for c in c0], outs=[b["recv2"] for b in bs])
         for rk, x, b in zip(self.ranks, xs, bs):
             T = x.shape[0]
             ck(L.hep_moe_assign_ep_phase(rk.sched.handle, ctypes.byref(rk.sched.out), rk.sched.split.data_ptr(), 1,
@@ -759,19 +777,19 @@ class EPMoELayer:
         c1 = [b["counts_ph"][1].cpu().tolist() for b in bs]
         if "a2a" in ev:
             ev["a2a"][0].record(st)
+        # phase 1's rows land right after phase 0's in the same receive buffer (no concatenation)
         recv1 = self.comm.all_to_all([b["send2"][x.shape[0] * K: x.shape[0] * K + sum(c[:G])]
-                                      for b, c, x in zip(bs, c1, xs)], [c[:G] for c in c1], [c[G:] for c in c1])
+                                      for b, c, x in zip(bs, c1, xs)], [c[:G] for c in c1], [c[G:] for c in c1],
+                                     outs=[b["recv2"][sum(a[G:]):] for b, a in zip(bs, c0)])
         if "a2a" in ev:
             ev["a2a"][1].record(st)
         st.wait_stream(side)
-        for r in recv0:
-            r.record_stream(st)
         ys0, ys1 = [], []
         if "ffn" in ev:
             ev["ffn"][0].record(st)
         for rk, b, r0, r1 in zip(self.ranks, bs, recv0, recv1):
             R0, R1 = r0.shape[0], r1.shape[0]
-            recv = torch.cat([r0, r1], dim=0)
+            recv = b["recv2"][: R0 + R1]  # [phase 0 rows | phase 1 rows]
             seg1 = b["seg_ph"][1].clone()
             seg1[:, 0] += R0  # phase 1's rows follow phase 0's in the FFN input
             seg = torch.cat([b["seg_ph"][0], seg1], dim=0)
@@ -782,14 +800,14 @@ class EPMoELayer:
             ys1.append(y[R0:R0 + R1])
         if "ffn" in ev:
             ev["ffn"][1].record(st)
-        backs0 = self.comm.all_to_all(ys0, [c[G:] for c in c0], [c[:G] for c in c0])
-        backs1 = self.comm.all_to_all(ys1, [c[G:] for c in c1], [c[:G] for c in c1])
+        # the outputs return straight to their send positions (phase 1's from T*K on)
+        self.comm.all_to_all(ys0, [c[G:] for c in c0], [c[:G] for c in c0], outs=[b["back2"] for b in bs])
+        self.comm.all_to_all(ys1, [c[G:] for c in c1], [c[:G] for c in c1],
+                             outs=[b["back2"][x.shape[0] * K:] for b, x in zip(bs, xs)])
         outs = []
-        for x, b, k0, k1, a, c in zip(xs, bs, backs0, backs1, c0, c1):
+        for x, b, a, c in zip(xs, bs, c0, c1):
             T = x.shape[0]
             back = b["back2"]
-            back[: k0.shape[0]].copy_(k0)  # returned rows at their send positions (phase 1 from T*K)
-            back[T * K: T * K + k1.shape[0]].copy_(k1)
             b["send_counts_ph"], b["recv_counts_ph"] = [a[:G], c[:G]], [a[G:], c[G:]]
             b["R_recv"] = sum(a[G:]) + sum(c[G:])
             ck(L.hep_moe_combine(back.data_ptr(), b["tok_row"].data_ptr(), b["topk_w"].data_ptr(), T, K, d,
