@@ -213,3 +213,33 @@ def test_tuning_struct_matches_header():
     assert reserved == [dict(_lib.HepTuning._fields_)["reserved"]._length_]
     t = _lib.get_tuning()
     assert set(t) == set(_lib.TUNING_FIELDS)
+
+
+def test_capi_argument_validation_without_a_device():
+    """Entry points validate their arguments before touching the device: bad shapes and
+    contract violations come back as the reference's error classes (status codes 1 / 3),
+    on a machine without a GPU too."""
+    import ctypes
+
+    from paper_2511_16947_b200 import _lib
+    from paper_2511_16947_b200.core import ContractViolation, DimensionError
+
+    L = _lib.lib()
+    fake = ctypes.c_void_p(256)  # never dereferenced: validation fails first
+    # hep_moe_permute_ex: blocks_per_sm outside 1..8
+    with pytest.raises(ContractViolation):
+        _lib.check(L.hep_moe_permute_ex(fake, fake, 16, 2, 64, fake, 9, None), "hep_moe_permute_ex")
+    with pytest.raises(DimensionError):  # d_model % 8
+        _lib.check(L.hep_moe_permute_ex(fake, fake, 16, 2, 60, fake, 8, None), "hep_moe_permute_ex")
+    # hep_router_topk_ws: K > E, e_pad not a multiple of 16
+    with pytest.raises(DimensionError):
+        _lib.check(L.hep_router_topk_ws(fake, fake, 128, 256, 4, 16, None, 8, 128, 1, None, fake, fake, fake, None,
+                                        None, None), "hep_router_topk_ws")
+    with pytest.raises(DimensionError):
+        _lib.check(L.hep_router_topk_ws(fake, fake, 128, 256, 8, 12, None, 2, 128, 1, None, fake, fake, fake, None,
+                                        None, None), "hep_router_topk_ws")
+    # hep_moe_assign_ep_phase: phase must be 0 or 1
+    out = _lib.HepSchedOut()
+    with pytest.raises(ContractViolation):
+        _lib.check(L.hep_moe_assign_ep_phase(fake, ctypes.byref(out), fake, 2, fake, 16, 2, 0, 0, fake, fake, fake,
+                                             fake, fake, 1 << 20, None), "hep_moe_assign_ep_phase")
