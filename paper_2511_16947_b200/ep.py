@@ -238,7 +238,7 @@ class EPRank:
             n_seg = max(G * self.n_hosted, 1)
             b["ffn_ws"] = torch.empty(max(int(L.hep_moe_ffn_workspace(n_seg, cap, self.n_slots)), 256),
                                       dtype=torch.uint8, device=dev)
-            if not layer.train_mode and layer.regroup_rows:  # received rows regrouped per weight slot
+            if not layer.train_mode:  # received rows regrouped per weight slot (regroup_rows)
                 ns = self.n_slots
                 b.update(row_map_g=torch.empty(cap, dtype=torch.int32, device=dev),
                          seg_g=torch.empty(ns, 4, dtype=torch.int32, device=dev),
@@ -487,7 +487,7 @@ class EPMoELayer:
                                       rk.sched.status.data_ptr(), s), "hep_moe_dispatch_p2p")
             if "a2a" in ev:
                 ev["a2a"][1].record(st)
-            if "row_map_g" in b:  # regrouped: the receive rows per weight slot, their return addresses with them
+            if self.regroup_rows and not self.train_mode:  # regrouped: rows per weight slot, return addresses with them
                 ck(L.hep_moe_ep_train_layout(b["seg"].data_ptr(), rk.n_hosted, G, rk.n_slots, 1,
                                              b["row_map_g"].data_ptr(), b["cap"], b["seg_g"].data_ptr(),
                                              b["slot_rows_g"].data_ptr(), s), "hep_moe_ep_train_layout")
@@ -510,7 +510,7 @@ class EPMoELayer:
                 self._train_ffn_p2p(rk, b, s)
                 b["x"] = x
                 continue
-            if n_seg and "row_map_g" in b:  # one run per weight slot; outputs still go straight to the sources
+            if n_seg and self.regroup_rows:  # one run per weight slot; outputs still go straight to the sources
                 ck(L.hep_moe_permute(b["recv"].data_ptr(), b["row_map_g"].data_ptr(), b["cap"], 1, d,
                                      b["rows_g"].data_ptr(), s), "hep_moe_permute(regroup)")
                 ck(L.hep_moe_expert_ffn_p2p(b["rows_g"].data_ptr(), rk.w13.data_ptr(), rk.w2.data_ptr(),

@@ -163,12 +163,14 @@ def test_local_ep_p2p_exchange_matches_collectives(P, G, E, K, d, F, T, kind, s)
     a.regroup_rows = False
     got3 = torch.cat([o.clone() for o in c.forward(xs)])
     ref3 = torch.cat([o.clone() for o in a.forward(xs)])
+    b.regroup_rows = False  # toggled after the buffers exist
+    got4 = torch.cat([o.clone() for o in b.forward(xs)])
     torch.cuda.synchronize()
     for rk in b.ranks:
         rk.sched.check_status("p2p")
     assert torch.equal(got, ref)
     assert torch.equal(got2, ref)
-    assert torch.equal(got3, ref) and torch.equal(ref3, ref)
+    assert torch.equal(got3, ref) and torch.equal(ref3, ref) and torch.equal(got4, ref)
     sim = P.MoELayer(pl, d, F, K, seed=6, gate_bias=bias)
     assert torch.equal(sim(x), ref)
 
