@@ -36,7 +36,8 @@ class HepSchedOut(ctypes.Structure):
 
 TUNING_FIELDS = ("st256", "pair_wait_cluster", "ffn_pair", "ffn_light_rows", "wgrad_order", "l2_policy",
                  "light_first", "raster_gm1", "raster_gm2", "sched_lexmin_warps", "lsu256", "ffn_clock",
-                 "router_tile_rows", "pair_wave_sync", "lp_dsm", "light_wave_sync", "router_mc", "router_pair", "wgrad_wave_sync", "wgrad_raster")
+                 "router_tile_rows", "pair_wave_sync", "lp_dsm", "light_wave_sync", "router_mc", "router_pair", "wgrad_wave_sync", "wgrad_raster",
+                 "sched_route_serial")
 
 
 class HepTuning(ctypes.Structure):

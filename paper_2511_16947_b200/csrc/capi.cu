@@ -16,7 +16,7 @@ void set_error(const char *fmt, ...) {
 static const hep_tuning kDefaultTuning = {
     /*st256*/ 1, /*pair_wait_cluster*/ 0, /*ffn_pair*/ -2, /*ffn_light_rows*/ 256, /*wgrad_order*/ 1,
     /*l2_policy*/ 0, /*light_first*/ 1, /*raster_gm1*/ 16, /*raster_gm2*/ 8, /*sched_lexmin_warps*/ 4,
-    /*lsu256*/ 1, /*ffn_clock*/ 0, /*router_tile_rows*/ 0, /*pair_wave_sync*/ 60, /*lp_dsm*/ 1, /*light_wave_sync*/ 0, /*router_mc*/ 0, /*router_pair*/ 0, /*wgrad_wave_sync*/ 0, /*wgrad_raster*/ 1, {0}};
+    /*lsu256*/ 1, /*ffn_clock*/ 0, /*router_tile_rows*/ 0, /*pair_wave_sync*/ 60, /*lp_dsm*/ 1, /*light_wave_sync*/ 0, /*router_mc*/ 0, /*router_pair*/ 0, /*wgrad_wave_sync*/ 0, /*wgrad_raster*/ 1, /*sched_route_serial*/ 0, {0}};
 hep_tuning g_tuning = kDefaultTuning;
 }  // namespace hep
 

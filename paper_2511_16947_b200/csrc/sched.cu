@@ -57,6 +57,7 @@ struct SchedArgs {
     const int64_t *xi_in;  // route-only: caller plan (global)
     int status_in;         // keep an error already in out.d_status (set by a preceding kernel)
     int lexmin_warps;      // warps on the lex-min arc chain (8 = whole block, 4)
+    int route_serial;      // Algorithm 1 as per-thread merges only (no route_lanes)
     hep_sched_out out;
 };
 
@@ -336,6 +337,100 @@ __device__ void route_pair(const SchedArgs &a, SchedSmem &s, int e, int src, int
         }
     }
     *c2 = cnt;
+}
+
+// Segmented scans over W-lane groups (W = 8 / 16, one group per expert).
+template <typename T>
+__device__ __forceinline__ T seg_incl_scan(T v, int idx, int W) {
+#pragma unroll
+    for (int d = 1; d < 16; d <<= 1) {
+        if (d >= W) break;
+        const T t = __shfl_up_sync(0xffffffffu, v, d, W);
+        if (idx >= d) v += t;
+    }
+    return v;
+}
+
+// Algorithm 1 with one lane per (expert, source): W lanes per expert (W = 8 for G <= 8,
+// else 16), 32 / W experts per warp per step.  The same table as route_pair (phase-1 range
+// of src, then src's pieces of the final sweep, whose offset A_src is the segmented prefix
+// of the remaining source amounts), but the per-expert prefixes -- A_src and the table
+// positions -- are warp shuffles instead of per-thread loops.  COUNT pass: ecount[e] =
+// the expert's number of ranges; EMIT pass: ranges from ecount[e] (scanned) on.
+template <bool EMIT>
+__device__ void route_lanes(const SchedArgs &a, SchedSmem &s, int64_t *ecount) {
+    const int G = a.G, E = a.E;
+    const int W = G <= 8 ? 8 : 16;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    const int epw = 32 / W, sub = lane / W, src = lane % W;
+    for (int e0 = warp * epw; e0 < E; e0 += nw * epw) {  // uniform per warp: shuffles see all lanes
+        const int e = e0 + sub;
+        const bool ok = e < E && src < G;
+        int b = 0, n = 0;
+        const int64_t *L = nullptr;
+        int64_t y1 = 0, rem = 0;
+        if (ok) {
+            b = s.grp_off[e];
+            n = s.grp_off[e + 1] - b;
+            L = s.loads + (size_t)e * loads_stride(G);
+            const int kk = s.kidx[(size_t)e * G + src];
+            const int64_t in = L[src];
+            if (kk >= 0) {
+                const int64_t xk = s.xi[b + kk];
+                y1 = in < xk ? in : xk;
+                rem = in > xk ? in - xk : 0;
+            } else {
+                rem = in;
+            }
+        }
+        const int64_t A = seg_incl_scan<int64_t>(rem, src, W) - rem;
+        int c2 = 0;
+        int64_t pos2 = 0;
+        int c1 = y1 > 0;
+        const int i1 = seg_incl_scan<int>(c1, src, W);
+        const int n1 = __shfl_sync(0xffffffffu, i1, W - 1, W);
+        int pass_c2 = 0;
+        if (ok && rem > 0) {  // count this source's pieces of the sweep
+            int64_t B = 0;
+            for (int k = 0; k < n && B < A + rem; ++k) {
+                const int64_t qd = s.xi[b + k] - L[s.grp_gpu[b + k]];
+                const int64_t q = qd > 0 ? qd : 0;
+                const int64_t lo = A > B ? A : B, hi = (A + rem) < (B + q) ? (A + rem) : (B + q);
+                pass_c2 += hi > lo;
+                B += q;
+            }
+        }
+        const int i2 = seg_incl_scan<int>(pass_c2, src, W);
+        const int n2 = __shfl_sync(0xffffffffu, i2, W - 1, W);
+        if (!EMIT) {
+            if (ok && src == 0) ecount[e] = (int64_t)n1 + n2;
+            continue;
+        }
+        if (!ok) continue;
+        const int64_t base = ecount[e];
+        if (y1 > 0) {
+            int64_t *r_ = a.out.d_ranges + 4 * (base + i1 - 1);
+            r_[0] = e; r_[1] = src; r_[2] = src; r_[3] = y1;
+            atomicAdd(&s.pair[src * G + src], (unsigned long long)y1);
+        }
+        if (rem > 0) {
+            pos2 = base + n1 + (i2 - pass_c2);
+            int64_t B = 0;
+            for (int k = 0; k < n && B < A + rem; ++k) {
+                const int dst = s.grp_gpu[b + k];
+                const int64_t qd = s.xi[b + k] - L[dst];
+                const int64_t q = qd > 0 ? qd : 0;
+                const int64_t lo = A > B ? A : B, hi = (A + rem) < (B + q) ? (A + rem) : (B + q);
+                if (hi > lo) {
+                    int64_t *r_ = a.out.d_ranges + 4 * (pos2 + c2);
+                    r_[0] = e; r_[1] = src; r_[2] = dst; r_[3] = hi - lo;
+                    atomicAdd(&s.pair[src * G + dst], (unsigned long long)(hi - lo));
+                    ++c2;
+                }
+                B += q;
+            }
+        }
+    }
 }
 
 // One thread per expert (used when E is large enough to fill the block):
@@ -677,8 +772,23 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
         // pass 0: range counts (one thread per (expert, source); per expert for topology routing)
         int64_t *ecount = s.totals;  // totals are no longer needed once the plan exists
         int16_t *rc1 = s.rc, *rc2 = s.rc + E * G;
-        const bool per_expert = !topo && E >= nt / 4;  // enough experts to fill the block
-        if (!topo) {
+        // one lane per (expert, source) (route_lanes) while that takes at most 4 steps per
+        // warp (E <= 128 at G <= 8): 6.2K vs 11K cycles at E = 8, 16.7K vs 21K at E = 128;
+        // above it the per-thread merges win (24K vs 30K at E = 256, profiles/r02/sched_ab_r02q.txt);
+        // hep_tuning.sched_route_serial = 1 forces the per-thread merges
+        const bool lanes = !topo && !a.route_serial && E * (G <= 8 ? 8 : 16) <= 4 * nt;
+        const bool per_expert = !topo && !lanes && E >= nt / 4;  // enough experts to fill the block
+        if (lanes) {
+            route_lanes<false>(a, s, ecount);
+            for (int e = tid; e < E; e += nt) {  // _check_plan (router.py:97-111)
+                const int b = s.grp_off[e], n = s.grp_off[e + 1] - b;
+                int64_t tot = 0, xs = 0;
+                bool neg = false;
+                for (int g = 0; g < G; ++g) tot += s.loads[e * loads_stride(G) + g];
+                for (int k = 0; k < n; ++k) { xs += s.xi[b + k]; neg |= s.xi[b + k] < 0; }
+                if (neg || xs != tot) set_status(status, HEP_E_CONTRACT);
+            }
+        } else if (!topo) {
             if (per_expert) {
                 for (int e = tid; e < E; e += nt) rc1[e * G] = (int16_t)route_expert_merge<false>(a, s, e, 0);
             } else {
@@ -725,7 +835,9 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
         if (total_ranges > a.max_ranges) set_status(status, HEP_E_CAPACITY);
         __syncthreads();
         if (*status == 0) {
-            if (per_expert) {
+            if (lanes) {
+                route_lanes<true>(a, s, ecount);
+            } else if (per_expert) {
                 for (int e = tid; e < E; e += nt) route_expert_merge<true>(a, s, e, ecount[e]);
             } else if (!topo) {
                 for (int i = tid; i < E * G; i += nt) {
@@ -843,6 +955,7 @@ static int launch_sched(hep_sched *h, SchedArgs &a, cudaStream_t stream) {
     // lex-min arc chain on 4 warps (2 subsets per thread, named barrier): 93.4K vs 97.6K
     // cycles at E=256 (8 warps), 97.7K on 2 warps; hep_tuning.sched_lexmin_warps = 8 for the whole block
     a.lexmin_warps = g_tuning.sched_lexmin_warps;
+    a.route_serial = g_tuning.sched_route_serial;
     a.G = h->G;
     a.E = h->E;
     a.nnz = h->nnz;

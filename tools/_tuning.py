@@ -11,6 +11,7 @@ NAMES = {
     "HEP_SCHED_LEXMIN_WARPS": "sched_lexmin_warps", "HEP_LSU256": "lsu256", "HEP_FFN_CLOCK": "ffn_clock",
     "HEP_ROUTER_TILE_ROWS": "router_tile_rows", "HEP_WAVE_SYNC": "pair_wave_sync", "HEP_LP_DSM": "lp_dsm", "HEP_LIGHT_WAVE_SYNC": "light_wave_sync",
     "HEP_ROUTER_MC": "router_mc", "HEP_ROUTER_PAIR": "router_pair", "HEP_WGRAD_WAVE_SYNC": "wgrad_wave_sync", "HEP_WGRAD_RASTER": "wgrad_raster",
+    "HEP_SCHED_ROUTE_SERIAL": "sched_route_serial",
 }
 
 
