@@ -76,7 +76,7 @@ typedef struct {
     int wgrad_wave_sync;    /* 1: the weight-gradient CTA-pair GEMMs start each wave of tiles together */
     int wgrad_raster;       /* 1: weight-gradient tiles walk the shorter tile dimension fastest */
     int sched_route_serial; /* 1: scheduler routing (Algorithm 1) always as per-thread merges; 0: one lane
-                               per (expert, source) with warp-shuffle prefixes while E <= 128 (G <= 8) */
+                               per (expert, source) with warp-shuffle prefixes while E <= 32 (G <= 8) */
     int reserved[1];
 } hep_tuning;
 int hep_tuning_get(hep_tuning *out);

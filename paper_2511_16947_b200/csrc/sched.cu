@@ -287,6 +287,33 @@ __device__ void lexmin_block(const SchedArgs &a, SchedSmem &s, int64_t *vtmp) {
     }
 }
 
+// 64-bit shared-memory accumulation (pair matrix, W[S], GPU loads) with native 32-bit
+// atomics (the 64-bit atomicAdd on shared memory is a CAS spin loop, slow under the
+// same-address contention of E experts adding into 2^G or G*G slots):
+// the low word's returned old value gives this add's carry, so the high word receives
+// exactly the carries of every add -- the little-endian u64 view holds the exact sum.
+__device__ __forceinline__ void pair_add(unsigned long long *p, int64_t y) {
+    uint32_t *w = reinterpret_cast<uint32_t *>(p);
+    const uint32_t lo = (uint32_t)y, hi = (uint32_t)((uint64_t)y >> 32);
+    const uint32_t old = atomicAdd(w, lo);
+    const uint32_t up = hi + (uint32_t)(old + lo < old);
+    if (up) atomicAdd(w + 1, up);
+}
+
+// One routing-table row (expert, src, dst, count) as a single 256-bit store when the table
+// is 32-byte aligned (every row then is): a quarter of the store instructions the table
+// costs otherwise -- they queue ahead of the kernel's later global accesses.
+__device__ __forceinline__ void put_range(int64_t *r_, int64_t e, int64_t src, int64_t dst, int64_t y) {
+    if (((uintptr_t)r_ & 31) == 0) {
+        asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(r_),
+                     "r"((uint32_t)e), "r"((uint32_t)(e >> 32)), "r"((uint32_t)src), "r"((uint32_t)(src >> 32)),
+                     "r"((uint32_t)dst), "r"((uint32_t)(dst >> 32)), "r"((uint32_t)y), "r"((uint32_t)(y >> 32))
+                     : "memory");
+    } else {
+        r_[0] = e; r_[1] = src; r_[2] = dst; r_[3] = y;
+    }
+}
+
 // Non-topology routing, one thread per (expert e, source src): the phase-1
 // range of src (if it hosts e) and src's ranges of the final merge, whose
 // offset A_src is the prefix of the remaining source amounts and whose
@@ -311,8 +338,8 @@ __device__ void route_pair(const SchedArgs &a, SchedSmem &s, int e, int src, int
     *c1 = y1 > 0;
     if (EMIT && y1 > 0) {
         int64_t *r_ = a.out.d_ranges + 4 * pos1;
-        r_[0] = e; r_[1] = src; r_[2] = src; r_[3] = y1;
-        atomicAdd(&s.pair[src * G + src], (unsigned long long)y1);
+        put_range(r_, e, src, src, y1);
+        pair_add(&s.pair[src * G + src], y1);
     }
     const int64_t rem = rem_of(src);
     int cnt = 0;
@@ -328,8 +355,8 @@ __device__ void route_pair(const SchedArgs &a, SchedSmem &s, int e, int src, int
             if (hi > lo) {
                 if (EMIT) {
                     int64_t *r_ = a.out.d_ranges + 4 * (pos2 + cnt);
-                    r_[0] = e; r_[1] = src; r_[2] = dst; r_[3] = hi - lo;
-                    atomicAdd(&s.pair[src * G + dst], (unsigned long long)(hi - lo));
+                    put_range(r_, e, src, dst, hi - lo);
+                    pair_add(&s.pair[src * G + dst], hi - lo);
                 }
                 ++cnt;
             }
@@ -410,8 +437,8 @@ __device__ void route_lanes(const SchedArgs &a, SchedSmem &s, int64_t *ecount) {
         const int64_t base = ecount[e];
         if (y1 > 0) {
             int64_t *r_ = a.out.d_ranges + 4 * (base + i1 - 1);
-            r_[0] = e; r_[1] = src; r_[2] = src; r_[3] = y1;
-            atomicAdd(&s.pair[src * G + src], (unsigned long long)y1);
+            put_range(r_, e, src, src, y1);
+            pair_add(&s.pair[src * G + src], y1);
         }
         if (rem > 0) {
             pos2 = base + n1 + (i2 - pass_c2);
@@ -423,8 +450,8 @@ __device__ void route_lanes(const SchedArgs &a, SchedSmem &s, int64_t *ecount) {
                 const int64_t lo = A > B ? A : B, hi = (A + rem) < (B + q) ? (A + rem) : (B + q);
                 if (hi > lo) {
                     int64_t *r_ = a.out.d_ranges + 4 * (pos2 + c2);
-                    r_[0] = e; r_[1] = src; r_[2] = dst; r_[3] = hi - lo;
-                    atomicAdd(&s.pair[src * G + dst], (unsigned long long)(hi - lo));
+                    put_range(r_, e, src, dst, hi - lo);
+                    pair_add(&s.pair[src * G + dst], hi - lo);
                     ++c2;
                 }
                 B += q;
@@ -448,8 +475,8 @@ __device__ int route_expert_merge(const SchedArgs &a, SchedSmem &s, int e, int64
     auto emit = [&](int src, int dst, int64_t y) {
         if (EMIT) {
             int64_t *r_ = a.out.d_ranges + 4 * (pos + cnt);
-            r_[0] = e; r_[1] = src; r_[2] = dst; r_[3] = y;
-            atomicAdd(&s.pair[src * G + dst], (unsigned long long)y);
+            put_range(r_, e, src, dst, y);
+            pair_add(&s.pair[src * G + dst], y);
         }
         ++cnt;
     };
@@ -508,8 +535,8 @@ __device__ int route_expert_topo(const SchedArgs &a, SchedSmem &s, int e, int64_
     auto emit = [&](int src, int dst, int64_t y) {
         if (EMIT) {
             int64_t *r_ = a.out.d_ranges + 4 * (pos + cnt);
-            r_[0] = e; r_[1] = src; r_[2] = dst; r_[3] = y;
-            atomicAdd(&s.pair[src * G + dst], (unsigned long long)y);
+            put_range(r_, e, src, dst, y);
+            pair_add(&s.pair[src * G + dst], y);
         }
         ++cnt;
     };
@@ -618,7 +645,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
         __syncthreads();
         for (int e = tid; e < E; e += nt)
             if (s.totals[e] > 0 && s.mask[e])
-                atomicAdd((unsigned long long *)&s.W[s.mask[e]], (unsigned long long)s.totals[e]);
+                pair_add((unsigned long long *)&s.W[s.mask[e]], s.totals[e]);
         __syncthreads();
         for (int bit = 0; bit < G; ++bit) {
             for (int S = tid; S < NS; S += nt)
@@ -749,7 +776,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
                 s.xi[b + best] += 1;
             }
             for (int k = 0; k < n; ++k)
-                atomicAdd((unsigned long long *)&s.gpu_load[s.grp_gpu[b + k]], (unsigned long long)s.xi[b + k]);
+                pair_add((unsigned long long *)&s.gpu_load[s.grp_gpu[b + k]], s.xi[b + k]);
         }
         __syncthreads();
         for (int i = tid; i < nnz; i += nt) a.out.d_xi[i] = s.xi[i];
@@ -772,11 +799,11 @@ __global__ void __launch_bounds__(kSchedThreads, 1) sched_kernel(SchedArgs a) {
         // pass 0: range counts (one thread per (expert, source); per expert for topology routing)
         int64_t *ecount = s.totals;  // totals are no longer needed once the plan exists
         int16_t *rc1 = s.rc, *rc2 = s.rc + E * G;
-        // one lane per (expert, source) (route_lanes) while that takes at most 4 steps per
-        // warp (E <= 128 at G <= 8): 6.2K vs 11K cycles at E = 8, 16.7K vs 21K at E = 128;
-        // above it the per-thread merges win (24K vs 30K at E = 256, profiles/r02/sched_ab_r02q.txt);
+        // one lane per (expert, source) (route_lanes) while that is one step per warp
+        // (E <= 32 at G <= 8): 6.1K vs 9.5K cycles at E = 8; from E = 128 on the per-thread
+        // merges win (14.1K vs 15.6K at E = 128, profiles/r02/sched_ab_notes.md);
         // hep_tuning.sched_route_serial = 1 forces the per-thread merges
-        const bool lanes = !topo && !a.route_serial && E * (G <= 8 ? 8 : 16) <= 4 * nt;
+        const bool lanes = !topo && !a.route_serial && E * (G <= 8 ? 8 : 16) <= nt;
         const bool per_expert = !topo && !lanes && E >= nt / 4;  // enough experts to fill the block
         if (lanes) {
             route_lanes<false>(a, s, ecount);
@@ -905,7 +932,7 @@ __global__ void transfer_kernel(int G, int gpn, const int64_t *ranges, int64_t n
         const int64_t *r = ranges + 4 * i;
         if (r[1] < 0 || r[1] >= G || r[2] < 0 || r[2] >= G) { set_status(status, HEP_E_DIMENSION); continue; }
         if (r[3] < 0) { set_status(status, HEP_E_CONTRACT); continue; }
-        atomicAdd(&pair[r[1] * G + r[2]], (unsigned long long)r[3]);
+        pair_add(&pair[r[1] * G + r[2]], r[3]);
     }
     __syncthreads();
     if (gpn <= 0) gpn = G;
