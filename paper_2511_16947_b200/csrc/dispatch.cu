@@ -192,31 +192,29 @@ __global__ void plan_prep_kernel(int G, int E, int nnz, const int32_t *grp_off, 
         if (r == 0 || rng(r - 1).x != e) w.first[e] = (int)r;
     }
     __syncthreads();
-    for (int e = tid; e < E; e += nt) {
-        const int r0 = w.first[e];
-        if (r0 < 0) continue;
-        int r1 = r0;
-        while (r1 < n_ranges && rng(r1).x == e) ++r1;
-        for (int j = r0; j < r1; ++j) {
-            const int4 rj = rng(j);
-            const int src = rj.y, dst = rj.z;
-            const int64_t cnt = rj.w;
-            int nz = -1;
-            for (int i = grp_off[e]; i < grp_off[e + 1]; ++i)
-                if (grp_gpu[i] == dst) nz = i;
-            if (nz < 0) { atomicCAS(status, 0, HEP_E_CONTRACT); continue; }
-            int64_t row = w.row_base[nz], rank = rank_base ? rank_base[e * G + src] : 0;
-            for (int k = r0; k < r1; ++k) {
-                const int4 rk = rng(k);
-                const int ks = rk.y, kd = rk.z;
-                if (kd == dst && ks < src) row += rk.w;
-                if (k < j && ks == src) rank += rk.w;
-            }
-            const int es = e * G + src;
-            const int slot = s_cnt[es]++;  // (e, *) belongs to this thread alone
-            w.es_end[es * G + slot] = (int32_t)(rank + cnt);
-            w.es_delta[es * G + slot] = (int32_t)(row - rank);
+    // one thread per range j (a thread per expert walked its ranges serially: E = 8 left
+    // 504 of the 512 threads idle): row and rank offsets from the expert's ranges before j,
+    // and j's slot among its (expert, src) ranges = how many of them precede it
+    for (int64_t j = tid; j < n_ranges; j += nt) {
+        const int4 rj = rng(j);
+        const int e = rj.x, src = rj.y, dst = rj.z;
+        const int64_t cnt = rj.w;
+        int nz = -1;
+        for (int i = grp_off[e]; i < grp_off[e + 1]; ++i)
+            if (grp_gpu[i] == dst) nz = i;
+        if (nz < 0) { atomicCAS(status, 0, HEP_E_CONTRACT); continue; }
+        int64_t row = w.row_base[nz], rank = rank_base ? rank_base[e * G + src] : 0;
+        int slot = 0;
+        for (int64_t k = w.first[e]; k < n_ranges; ++k) {
+            const int4 rk = rng(k);
+            if (rk.x != e) break;
+            if (rk.z == dst && rk.y < src) row += rk.w;
+            if (k < j && rk.y == src) { rank += rk.w; ++slot; }
         }
+        const int es = e * G + src;
+        atomicAdd(&s_cnt[es], 1);
+        w.es_end[es * G + slot] = (int32_t)(rank + cnt);
+        w.es_delta[es * G + slot] = (int32_t)(row - rank);
     }
     __syncthreads();
     for (int i = tid; i < E * G; i += nt) w.es_cnt[i] = s_cnt[i];
