@@ -428,21 +428,24 @@ __global__ void ep_prep_kernel(int G, int E, int rank, const int64_t *ranges, co
         if (row >= ((int64_t)1 << 31)) atomicCAS(status, 0, HEP_E_CAPACITY);
     }
     __syncthreads();
-    // per (expert, this source): ranges in table order -> send positions
-    for (int e = tid; e < E; e += nt) {
-        const int r0 = w.first[e];
-        if (r0 < 0) continue;
+    // per (expert, this source): ranges in table order -> send positions, one thread per
+    // range of this source (its slot and first rank from the expert's earlier ranges)
+    for (int64_t j = tid; j < n_ranges; j += nt) {
+        if (ranges[4 * j + 1] != rank) continue;
+        const int e = (int)ranges[4 * j];
+        const int dst = (int)ranges[4 * j + 2];
+        const int64_t c = ranges[4 * j + 3];
         const int es = e * G + rank;
         int64_t rank_start = w.es_lo[es];
-        for (int64_t j = r0; j < n_ranges && ranges[4 * j] == e; ++j) {
-            if (ranges[4 * j + 1] != rank) continue;
-            const int dst = (int)ranges[4 * j + 2];
-            const int64_t c = ranges[4 * j + 3];
-            const int slot = w.es_cnt[es]++;
-            w.es_end[es * G + slot] = (int32_t)(rank_start + c);
-            w.es_delta[es * G + slot] = (int32_t)(w.sbase[e * G + dst] - rank_start);
-            rank_start += c;
-        }
+        int slot = 0;
+        for (int64_t k = w.first[e]; k < j; ++k)
+            if (ranges[4 * k + 1] == rank) {
+                rank_start += ranges[4 * k + 3];
+                ++slot;
+            }
+        atomicAdd(&w.es_cnt[es], 1);
+        w.es_end[es * G + slot] = (int32_t)(rank_start + c);
+        w.es_delta[es * G + slot] = (int32_t)(w.sbase[e * G + dst] - rank_start);
     }
 }
 
